@@ -1,0 +1,286 @@
+"""CPU ORACLE -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` leg may import this package. The
+product path (``paper_2512_23917_b200``) never imports it and shares no code
+with it; the only module both sides use is ``synth`` (seeded inputs, no
+arithmetic of the method).
+
+Every function is the plain definition from the paper (PAPER.md line numbers)
+or, where the paper has no definition (the H_eff, TEBD and MPS chains), the
+textbook definition recorded in DESIGN.md section "Readings". The numeric core
+is ``tci_oracle.c`` (plain loops, double precision, -ffp-contract=off); this
+module only marshals numpy arrays and composes the chains from ``contract``
+calls in the order DESIGN.md states.
+
+Parity pins live in ``tests/test_oracle_pins.py``; functions without a pin
+would be marked "parity unpinned" here -- currently every function below is
+pinned (DESIGN.md section "Pins").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Sequence, Union
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "tci_oracle.c")
+_SO = os.path.join(_HERE, "libtci_oracle.so")
+
+Labels = Union[str, Sequence[int]]
+
+ERROR_NAMES = {
+    1: "SHAPE_MISMATCH", 2: "ORDER_MISMATCH", 3: "OUT_OF_RANGE",
+    4: "LABEL_CONFLICT", 5: "PARSE", 7: "UNSUPPORTED", 8: "INVALID_ARGUMENT",
+    12: "NOMEM",
+}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        self.code = code
+        super().__init__(f"oracle error {code} ({ERROR_NAMES.get(code, '?')}) {what}")
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain C, OpenMP, no FMA contraction)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call([
+            "gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+            "-fPIC", "-shared", "-std=c99", "-o", tmp, _SRC])
+        os.replace(tmp, _SO)
+    return _SO
+
+
+_lib_handle = None
+
+
+def _lib():
+    global _lib_handle
+    if _lib_handle is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        dp = ctypes.POINTER(ctypes.c_double)
+        ci = ctypes.c_int
+        lib.oracle_contract.argtypes = [ci, ci, i64p, i32p, dp, ci, i64p, i32p, dp, ci, i32p, dp, ci]
+        lib.oracle_contract_abs.argtypes = [ci, i64p, i32p, dp, ci, i64p, i32p, dp, ci, i32p, dp, ci]
+        lib.oracle_contract_shape.argtypes = [ci, i64p, i32p, ci, i64p, i32p, ci, i32p, i64p]
+        lib.oracle_permute.argtypes = [ci, ci, i64p, i32p, dp, dp, ci]
+        lib.oracle_max_threads.restype = ci
+        _lib_handle = lib
+    return _lib_handle
+
+
+def max_threads() -> int:
+    return int(_lib().oracle_max_threads())
+
+
+# ----------------------------------------------------------------------------
+# marshalling helpers
+# ----------------------------------------------------------------------------
+
+def _labels(l: Labels, order: int) -> np.ndarray:
+    """String API: one byte per label (reading R12)."""
+    if isinstance(l, str):
+        b = l.encode("latin-1")
+        if len(b) != order:
+            raise OracleError(2, f"label string {l!r} has {len(b)} labels for order {order}")
+        arr = np.frombuffer(b, dtype=np.uint8).astype(np.int32)
+    else:
+        arr = np.asarray(list(l), dtype=np.int32)
+        if arr.size != order:
+            raise OracleError(2, f"{arr.size} labels for order {order}")
+    return np.ascontiguousarray(arr)
+
+
+def _as_f64(x: np.ndarray):
+    """Widen exactly to float64 / complex128 (reading R14)."""
+    x = np.asarray(x)
+    # np.require keeps 0-d arrays 0-d (ascontiguousarray would make them 1-d)
+    if np.iscomplexobj(x):
+        return np.require(x, dtype=np.complex128, requirements="C"), True
+    return np.require(x, dtype=np.float64, requirements="C"), False
+
+
+def _p(a, t):
+    return a.ctypes.data_as(ctypes.POINTER(t))
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _shape(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a.shape, dtype=np.int64).reshape(-1))
+
+
+# ----------------------------------------------------------------------------
+# core functions
+# ----------------------------------------------------------------------------
+
+def contract_shape(sa, la: Labels, sb, lb: Labels, lc: Labels):
+    lib = _lib()
+    sa = np.ascontiguousarray(np.asarray(sa, dtype=np.int64).reshape(-1))
+    sb = np.ascontiguousarray(np.asarray(sb, dtype=np.int64).reshape(-1))
+    la_ = _labels(la, sa.size)
+    lb_ = _labels(lb, sb.size)
+    nc = len(lc.encode("latin-1")) if isinstance(lc, str) else len(list(lc))
+    lc_ = _labels(lc, nc)
+    sc = np.zeros(max(nc, 1), dtype=np.int64)
+    st = lib.oracle_contract_shape(sa.size, _p(sa, ctypes.c_int64), _p(la_, ctypes.c_int32),
+                                   sb.size, _p(sb, ctypes.c_int64), _p(lb_, ctypes.c_int32),
+                                   nc, _p(lc_, ctypes.c_int32), _p(sc, ctypes.c_int64))
+    if st:
+        raise OracleError(st)
+    return tuple(int(x) for x in sc[:nc])
+
+
+def contract(a: np.ndarray, la: Labels, b: np.ndarray, lb: Labels, lc: Labels,
+             threads: int | None = None) -> np.ndarray:
+    """tci::contract, Eq. (3)."""
+    lib = _lib()
+    a, ca = _as_f64(a)
+    b, cb = _as_f64(b)
+    cplx = ca or cb
+    if cplx:
+        a = a.astype(np.complex128)
+        b = b.astype(np.complex128)
+    sc = contract_shape(a.shape, la, b.shape, lb, lc)
+    la_ = _labels(la, a.ndim)
+    lb_ = _labels(lb, b.ndim)
+    lc_ = _labels(lc, len(sc))
+    c = np.empty(sc, dtype=np.complex128 if cplx else np.float64)
+    sa, sb = _shape(a), _shape(b)
+    st = lib.oracle_contract(int(cplx), a.ndim, _p(sa, ctypes.c_int64), _p(la_, ctypes.c_int32), _dptr(a),
+                             b.ndim, _p(sb, ctypes.c_int64), _p(lb_, ctypes.c_int32), _dptr(b),
+                             len(sc), _p(lc_, ctypes.c_int32), _dptr(c),
+                             int(threads or max_threads()))
+    if st:
+        raise OracleError(st)
+    return c
+
+
+def contract_abs(a: np.ndarray, la: Labels, b: np.ndarray, lb: Labels, lc: Labels,
+                 threads: int | None = None) -> np.ndarray:
+    """|A|.|B| under the same contraction (real only): the Higham bound term."""
+    lib = _lib()
+    a = np.require(a, dtype=np.float64, requirements="C")
+    b = np.require(b, dtype=np.float64, requirements="C")
+    sc = contract_shape(a.shape, la, b.shape, lb, lc)
+    la_, lb_, lc_ = _labels(la, a.ndim), _labels(lb, b.ndim), _labels(lc, len(sc))
+    c = np.empty(sc, dtype=np.float64)
+    sa, sb = _shape(a), _shape(b)
+    st = lib.oracle_contract_abs(a.ndim, _p(sa, ctypes.c_int64), _p(la_, ctypes.c_int32), _dptr(a),
+                                 b.ndim, _p(sb, ctypes.c_int64), _p(lb_, ctypes.c_int32), _dptr(b),
+                                 len(sc), _p(lc_, ctypes.c_int32), _dptr(c), int(threads or max_threads()))
+    if st:
+        raise OracleError(st)
+    return c
+
+
+def permute(a: np.ndarray, perm: Sequence[int], threads: int | None = None) -> np.ndarray:
+    """tci::transpose, Eq. (1)."""
+    lib = _lib()
+    a, cplx = _as_f64(a)
+    perm_ = np.ascontiguousarray(np.asarray(list(perm), dtype=np.int32))
+    if perm_.size != a.ndim:
+        raise OracleError(2)
+    for p in perm_:
+        if p < 0 or p >= a.ndim:
+            raise OracleError(8)
+    out = np.empty(tuple(a.shape[p] for p in perm_), dtype=a.dtype)
+    sa = _shape(a)
+    st = lib.oracle_permute(int(cplx), a.ndim, _p(sa, ctypes.c_int64), _p(perm_, ctypes.c_int32),
+                            _dptr(a), _dptr(out), int(threads or max_threads()))
+    if st:
+        raise OracleError(st)
+    return out
+
+
+def reshape(a: np.ndarray, new_shape: Sequence[int]) -> np.ndarray:
+    """tci::reshape: metadata only, element order kept."""
+    new_shape = tuple(int(s) for s in new_shape)
+    if any(s < 1 for s in new_shape):
+        raise OracleError(3)
+    if int(np.prod(new_shape, dtype=np.int64)) != a.size:
+        raise OracleError(1)
+    return np.ascontiguousarray(a).reshape(new_shape)
+
+
+# ----------------------------------------------------------------------------
+# chains (definitions: DESIGN.md "Readings" R15-R17; no paper text exists)
+# ----------------------------------------------------------------------------
+
+def heff(L, W1, W2, R, psi, threads=None):
+    """Two-site H_eff.psi (R15), FLOP-optimal order L.psi -> W1 -> W2 -> R.
+
+    L[a,w,b], psi[a,s,t,c], W1[w,v,s,p], W2[v,x,t,q], R[c,x,e] -> out[b,p,q,e].
+    """
+    T1 = contract(L, "awb", psi, "astc", "wbstc", threads)
+    T2 = contract(T1, "wbstc", W1, "wvsp", "btcvp", threads)
+    T3 = contract(T2, "btcvp", W2, "vxtq", "bpqcx", threads)
+    return contract(T3, "bpqcx", R, "cxe", "bpqe", threads)
+
+
+def heff_alt(L, W1, W2, R, psi, threads=None):
+    """Same operator, a different pairwise order (R first): order invariance."""
+    U1 = contract(psi, "astc", R, "cxe", "astxe", threads)
+    U2 = contract(U1, "astxe", W2, "vxtq", "asvqe", threads)
+    U3 = contract(U2, "asvqe", W1, "wvsp", "awpqe", threads)
+    return contract(U3, "awpqe", L, "awb", "bpqe", threads)
+
+
+def heff_rows(L, W1, W2, R, psi, rows, threads=None):
+    """Rows out[b0,:,:,:] for b0 in rows: the chain on the slice L[:,:,b0]."""
+    res = []
+    for b0 in rows:
+        Lr = np.ascontiguousarray(L[:, :, int(b0):int(b0) + 1])
+        res.append(heff(Lr, W1, W2, R, psi, threads)[0])
+    return np.stack(res)
+
+
+def heff_dense(L, W1, W2, R, shape_psi, threads=None):
+    """Dense matrix H[(b p q e), (a s t c)] by applying H_eff to basis vectors."""
+    n = int(np.prod(shape_psi))
+    cols = []
+    dt = np.result_type(L, W1, W2, R)
+    for k in range(n):
+        e = np.zeros(n, dtype=dt)
+        e[k] = 1
+        cols.append(heff(L, W1, W2, R, e.reshape(shape_psi), threads).reshape(-1))
+    return np.stack(cols, axis=1)
+
+
+def tebd_theta(A, B, U, la="asb", lb="btc", lu="pqst", lt="apqc", threads=None):
+    """theta = (A.B).U (R16): AB over b, then the gate over (s,t)."""
+    # intermediate keeps the non-b legs of A then of B, in label order
+    lab = "".join(ch for ch in la if ch not in lb) + "".join(ch for ch in lb if ch not in la)
+    AB = contract(A, la, B, lb, lab, threads)
+    return contract(AB, lab, U, lu, lt, threads)
+
+
+def mps_overlap(bra, ket, threads=None):
+    """<bra|ket> by the transfer chain of DESIGN.md R17 (real data, no conj)."""
+    E = np.ones((1, 1), dtype=np.result_type(bra[0], ket[0]))
+    for Ab, Ak in zip(bra, ket):
+        X = contract(E, "xz", Ab, "xsy", "zsy", threads)
+        E = contract(X, "zsy", Ak, "zsw", "yw", threads)
+    return E
+
+
+def mps_norm2(sites, threads=None):
+    return mps_overlap(sites, sites, threads)
+
+
+def mps_mpo_apply(A, W, threads=None):
+    """Site-local uncompressed MPO application (R18):
+    B[a,w,t,b,v] = sum_s A[a,s,b] W[w,v,s,t], then reshape to [(a w), t, (b v)]."""
+    Bt = contract(A, "asb", W, "wvst", "awtbv", threads)
+    a, w, t, b, v = Bt.shape
+    return reshape(Bt, (a * w, t, b * v))

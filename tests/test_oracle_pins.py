@@ -1,0 +1,485 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+Each test checks the oracle against something other than itself: values the
+paper prints (tests/golden/paper_examples.json), closed forms
+(tests/golden/closed_forms.json), library routines that reduce to the same
+definition (numpy.einsum / matmul / transpose), exact rational arithmetic,
+brute-force pure-Python sums, invariances and the Higham error bound. DESIGN.md
+section "Pins" maps every oracle function to the tests here.
+"""
+import itertools
+import math
+import string
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import synth
+from conftest import golden, max_abs, rel_frob
+
+
+# ---------------------------------------------------------------------------
+# helpers independent of the oracle
+# ---------------------------------------------------------------------------
+
+def brute_contract(A, la, B, lb, lc):
+    """Eq. (3) by a pure-Python sum over all label assignments (tiny only)."""
+    dims = {}
+    for l, d in zip(la, A.shape):
+        dims[l] = d
+    for l, d in zip(lb, B.shape):
+        dims[l] = d
+    summed = [l for l in la if l in lb and l not in lc]
+    out = np.zeros([dims[l] for l in lc], dtype=np.result_type(A, B))
+    for oc in itertools.product(*[range(dims[l]) for l in lc]):
+        asg = dict(zip(lc, oc))
+        acc = 0
+        for sc in itertools.product(*[range(dims[l]) for l in summed]):
+            asg.update(zip(summed, sc))
+            acc += A[tuple(asg[l] for l in la)] * B[tuple(asg[l] for l in lb)]
+        out[oc] = acc
+    return out
+
+
+def rnd(shape, seed, tid=1, cplx=False):
+    return synth.random_np(shape, "c128" if cplx else "r64", seed, tid)
+
+
+# ---------------------------------------------------------------------------
+# paper worked examples
+# ---------------------------------------------------------------------------
+
+def test_paper_contract_example(oracle_mod):
+    g = golden("paper_examples.json")["contract_shape"]
+    a = rnd(g["a_shape"], 11, 1)
+    b = rnd(g["b_shape"], 11, 2)
+    c_list = oracle_mod.contract(a, g["labels_list"]["a"], b, g["labels_list"]["b"], g["labels_list"]["c"])
+    c_str = oracle_mod.contract(a, g["labels_str"]["a"], b, g["labels_str"]["b"], g["labels_str"]["c"])
+    assert list(c_list.shape) == g["c_shape"]
+    assert np.array_equal(c_list, c_str)           # list and string APIs equivalent
+    assert rel_frob(c_str, np.einsum("ijk,kjl->li", a, b)) < 1e-15
+    assert rel_frob(c_str, brute_contract(a, "ijk", b, "kjl", "li")) < 1e-15
+
+
+def test_paper_transpose_example(oracle_mod):
+    g = golden("paper_examples.json")["transpose"]
+    a = rnd(g["a_shape"], 12)
+    a2 = oracle_mod.permute(a, g["inplace_order"])
+    assert a[tuple(g["elem_before"])] == a2[tuple(g["elem_after"])]
+    b = oracle_mod.permute(a2, g["out_order"])
+    assert list(b.shape) == g["out_shape_after_inplace"]
+
+
+def test_paper_reshape_example(oracle_mod):
+    g = golden("paper_examples.json")["reshape"]
+    a = rnd(g["a_shape"], 13)
+    r = oracle_mod.reshape(a, g["inplace_shape"])
+    assert list(r.shape) == g["inplace_shape"]
+    assert np.array_equal(r.reshape(-1), a.reshape(-1))      # element order preserved
+    r2 = oracle_mod.reshape(r, g["out_shape"])
+    assert list(r2.shape) == g["out_shape"]
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.reshape(a, [5, 5])
+    assert e.value.code == 1
+
+
+def test_paper_scenario_shapes(oracle_mod):
+    for i, case in enumerate(golden("paper_examples.json")["scenario_shapes"]["cases"]):
+        a = rnd(case["a"], 20 + i, 1)
+        b = rnd(case["b"], 20 + i, 2)
+        c = oracle_mod.contract(a, case["la"], b, case["lb"], case["lc"])
+        assert list(c.shape) == case["c"]
+        assert c.size == max(1, int(np.prod(case["c"])))
+
+
+def test_scenario_overlap_identity(oracle_mod):
+    """Section III: truncated SVD of a normalized 6-qubit state,
+    psi1 = u.s.vt by two contracts (the 2nd aliasing psi1), overlap by a full
+    contraction. Exact identity: <psi|psi1> = 1 - eps with eps of P:2088-2090
+    (reading R24 on the fidelity line P:351)."""
+    psi = rnd((2,) * 6, 31)
+    psi /= np.linalg.norm(psi)
+    m = psi.reshape(8, 8)
+    U, s, Vt = np.linalg.svd(m)
+    chi = 2
+    eps = float(np.sum(s[chi:] ** 2) / np.sum(s ** 2))
+    u = U[:, :chi].reshape(2, 2, 2, chi)
+    S = np.diag(s[:chi])
+    vt = Vt[:chi, :].reshape(chi, 2, 2, 2)
+    psi1 = oracle_mod.contract(u, "ijkl", S, "lm", "ijkm")
+    psi1 = oracle_mod.contract(psi1, "ijkl", vt, "lmno", "ijkmno")
+    ovlp = oracle_mod.contract(psi, "ijklmn", psi1, "ijklmn", "")
+    assert ovlp.shape == ()
+    assert abs(float(ovlp) - (1.0 - eps)) < 1e-14
+
+
+def test_frobenius_and_close_examples():
+    g = golden("paper_examples.json")
+    assert rel_frob(np.eye(3), np.zeros((3, 3))) == pytest.approx(g["frobenius_norm_eye3"]["value"], abs=0)
+    c = g["close"]
+    A = np.eye(3)
+    B = A.copy()
+    B[tuple(c["perturb_coor"])] = c["perturb_value"]
+    assert not (max_abs(A, B) <= c["eps_false"])
+    assert max_abs(A, B) <= c["eps_true"]
+
+
+# ---------------------------------------------------------------------------
+# reductions to library routines / brute force
+# ---------------------------------------------------------------------------
+
+def test_matmul_special_case(oracle_mod):
+    """|I|=|J|=|S|=1 is matrix multiplication."""
+    for cplx in (False, True):
+        a = rnd((37, 64), 40, 1, cplx)
+        b = rnd((64, 19), 40, 2, cplx)
+        assert rel_frob(oracle_mod.contract(a, "ik", b, "kj", "ij"), a @ b) < 1e-15
+        assert rel_frob(oracle_mod.contract(a, "ik", b, "kj", "ji"), (a @ b).T) < 1e-15
+
+
+def test_eq4_example(oracle_mod):
+    """C_ilm = sum_jk A_ijk B_jklm (Eq. (4))."""
+    A = rnd((3, 4, 5), 41, 1)
+    B = rnd((4, 5, 2, 3), 41, 2)
+    C = oracle_mod.contract(A, "ijk", B, "jklm", "ilm")
+    assert rel_frob(C, brute_contract(A, "ijk", B, "jklm", "ilm")) < 1e-15
+    assert rel_frob(C, np.einsum("ijk,jklm->ilm", A, B)) < 1e-15
+
+
+def _random_instance(rng, cplx):
+    ra = int(rng.integers(1, 5))
+    rb = int(rng.integers(1, 5))
+    nc = int(rng.integers(0, min(ra, rb) + 1))
+    letters = list(string.ascii_letters)
+    rng.shuffle(letters)
+    shared = letters[:nc]
+    fa = letters[nc:nc + ra - nc]
+    fb = letters[ra:ra + rb - nc]
+    la = shared + fa
+    lb = shared + fb
+    rng.shuffle(la)
+    rng.shuffle(lb)
+    lc = fa + fb
+    rng.shuffle(lc)
+    dims = {l: int(rng.integers(1, 6)) for l in la + lb}
+    seed = int(rng.integers(1, 1 << 30))
+    A = rnd([dims[l] for l in la], seed, 1, cplx)
+    B = rnd([dims[l] for l in lb], seed, 2, cplx)
+    return A, "".join(la), B, "".join(lb), "".join(lc)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_random_sweep_vs_einsum(oracle_mod, cplx):
+    """SPEC.md:381 / SURVEY 8(c).5: 200 random contracts, order <= 4, dims <= 5."""
+    rng = np.random.default_rng(1234 + cplx)
+    for _ in range(100):
+        A, la, B, lb, lc = _random_instance(rng, cplx)
+        C = oracle_mod.contract(A, la, B, lb, lc)
+        ref = np.einsum(f"{la},{lb}->{lc}", A, B)
+        assert rel_frob(C, ref) <= 1e-12, (la, lb, lc)
+
+
+def test_random_small_vs_bruteforce(oracle_mod):
+    rng = np.random.default_rng(99)
+    for k in range(30):
+        A, la, B, lb, lc = _random_instance(rng, k % 2 == 1)
+        if A.size * B.size > 4000:
+            continue
+        C = oracle_mod.contract(A, la, B, lb, lc)
+        assert rel_frob(C, brute_contract(A, la, B, lb, lc)) <= 1e-14
+
+
+def test_exact_rational_within_higham_bound(oracle_mod):
+    """Per element |C - C_exact| <= gamma_K (|A|.|B|), gamma_K = Ku/(1-Ku),
+    with C_exact summed in exact rationals (the inputs are dyadic rationals)."""
+    A = rnd((6, 50, 4), 51, 1)
+    B = rnd((4, 50, 7), 51, 2)
+    C = oracle_mod.contract(A, "iks", B, "skj", "ij")
+    Cabs = oracle_mod.contract_abs(A, "iks", B, "skj", "ij")
+    K = 50 * 4
+    u = 2.0 ** -53
+    gam = K * u / (1 - K * u)
+    for i in range(6):
+        for j in range(7):
+            exact = sum(Fraction(A[i, k, s]) * Fraction(B[s, k, j]) for k in range(50) for s in range(4))
+            err = abs(Fraction(C[i, j]) - exact)
+            assert err <= Fraction(gam) * Fraction(Cabs[i, j])
+            # |A|.|B| itself equals the exact sum of moduli within the same bound
+            exa = sum(abs(Fraction(A[i, k, s]) * Fraction(B[s, k, j])) for k in range(50) for s in range(4))
+            assert abs(Fraction(Cabs[i, j]) - exa) <= Fraction(gam) * exa
+
+
+# ---------------------------------------------------------------------------
+# exact identities and invariances
+# ---------------------------------------------------------------------------
+
+def test_identity_contraction_bitwise(oracle_mod):
+    for cplx in (False, True):
+        a = rnd((13, 9), 60, 1, cplx)
+        I = np.eye(9, dtype=a.dtype)
+        assert np.array_equal(oracle_mod.contract(a, "ij", I, "jk", "ik"), a)
+        I2 = np.eye(13, dtype=a.dtype)
+        assert np.array_equal(oracle_mod.contract(I2, "ki", a, "ij", "kj"), a)
+
+
+def test_trace(oracle_mod):
+    a = rnd((17, 17), 61)
+    t = oracle_mod.contract(a, "ij", np.eye(17), "ij", "")
+    assert abs(float(t) - np.trace(a)) <= 1e-15 * np.sum(np.abs(np.diag(a)))
+
+
+def test_outer_product_and_scalars(oracle_mod):
+    a = rnd((3, 4), 62, 1)
+    b = rnd((5,), 62, 2)
+    c = oracle_mod.contract(a, "ij", b, "k", "kji")
+    assert np.array_equal(c, np.einsum("ij,k->kji", a, b))   # one product per element: exact
+    s = np.array(2.5)
+    assert np.array_equal(oracle_mod.contract(s, "", a, "ij", "ji"), (2.5 * a).T)
+    d = oracle_mod.contract(s, "", np.array(-3.0), "", "")
+    assert d.shape == () and float(d) == -7.5
+
+
+def test_permute_vs_numpy_and_roundtrip(oracle_mod):
+    rng = np.random.default_rng(5)
+    for n in range(0, 7):
+        shape = tuple(int(x) for x in rng.integers(1, 5, size=n))
+        for cplx in (False, True):
+            a = rnd(shape, 70 + n, 1, cplx)
+            perm = list(rng.permutation(n))
+            b = oracle_mod.permute(a, perm)
+            assert np.array_equal(b, np.transpose(a, perm))     # Eq. (1) == NumPy axes semantics
+            inv = list(np.argsort(perm))
+            assert np.array_equal(oracle_mod.permute(b, inv), a)
+
+
+def test_relabel_invariance_bitwise(oracle_mod):
+    A = rnd((4, 6, 5), 80, 1, True)
+    B = rnd((5, 6, 3), 80, 2, True)
+    c1 = oracle_mod.contract(A, "ikl", B, "lkj", "ji")
+    c2 = oracle_mod.contract(A, [7, -3, 100], B, [100, -3, 42], [42, 7])
+    assert np.array_equal(c1, c2)
+
+
+def test_operand_swap_and_leg_permutation(oracle_mod):
+    A = rnd((4, 6, 5), 81, 1)
+    B = rnd((5, 6, 3), 81, 2)
+    c1 = oracle_mod.contract(A, "ikl", B, "lkj", "ij")
+    c2 = oracle_mod.contract(B, "lkj", A, "ikl", "ij")
+    c3 = oracle_mod.contract(np.transpose(A, (2, 0, 1)).copy(), "lik", B, "lkj", "ij")
+    assert rel_frob(c2, c1) <= 1e-15 and rel_frob(c3, c1) <= 1e-15
+
+
+def test_associativity(oracle_mod):
+    A = rnd((6, 7), 82, 1)
+    B = rnd((7, 8, 5), 82, 2)
+    C = rnd((5, 9), 82, 3)
+    l = oracle_mod.contract(oracle_mod.contract(A, "ij", B, "jkl", "ikl"), "ikl", C, "lm", "ikm")
+    r = oracle_mod.contract(A, "ij", oracle_mod.contract(B, "jkl", C, "lm", "jkm"), "jkm", "ikm")
+    assert rel_frob(l, r) <= 1e-11
+
+
+def test_thread_count_bitwise(oracle_mod):
+    A = rnd((40, 33, 20), 83, 1, True)
+    B = rnd((20, 33, 50), 83, 2, True)
+    c1 = oracle_mod.contract(A, "iks", B, "skj", "ji", threads=1)
+    c8 = oracle_mod.contract(A, "iks", B, "skj", "ji", threads=8)
+    assert np.array_equal(c1, c8)
+
+
+# ---------------------------------------------------------------------------
+# error kinds
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("la,lb,lc,code", [
+    ("iij", "jk", "ik", 4),      # repeated label in one operand
+    ("ij", "jk", "ijk", 4),      # label in all three lists (R3)
+    ("ijm", "jk", "ik", 4),      # label in one input, not in gamma (R4)
+    ("ij", "jk", "ikz", 4),      # gamma label absent (R5)
+    ("ij", "jk", "ii", 4),       # repeated output label
+])
+def test_label_errors(oracle_mod, la, lb, lc, code):
+    a = np.zeros([2] * len(la))
+    b = np.zeros([2] * len(lb))
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.contract(a, la, b, lb, lc)
+    assert e.value.code == code
+
+
+def test_shape_and_order_errors(oracle_mod):
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.contract(np.zeros((2, 3)), "ij", np.zeros((4, 5)), "jk", "ik")
+    assert e.value.code == 1
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.contract(np.zeros((2, 3)), "ijk", np.zeros((3, 5)), "jk", "ik")
+    assert e.value.code == 2
+    with pytest.raises(oracle_mod.OracleError) as e:
+        oracle_mod.contract(np.zeros([1] * 17), list(range(17)), np.zeros(1), [0], list(range(1, 17)))
+    assert e.value.code == 7
+
+
+# ---------------------------------------------------------------------------
+# chains: H_eff, TEBD, MPS (definitions DESIGN.md R15-R18)
+# ---------------------------------------------------------------------------
+
+def brute_heff(L, W1, W2, R, psi):
+    """Single 7-index sum, pure Python (SURVEY 8(c).5 brute force)."""
+    chi_l, D, chi_lo = L.shape
+    _, d, _, chi_r = psi.shape
+    D2 = W1.shape[1]
+    D3 = W2.shape[1]
+    chi_ro = R.shape[2]
+    out = np.zeros((chi_lo, d, d, chi_ro), dtype=np.result_type(L, psi))
+    for b, p, q, e in itertools.product(range(chi_lo), range(d), range(d), range(chi_ro)):
+        acc = 0
+        for a, s, t, c, w, v, x in itertools.product(range(chi_l), range(d), range(d), range(chi_r),
+                                                     range(D), range(D2), range(D3)):
+            acc += L[a, w, b] * psi[a, s, t, c] * W1[w, v, s, p] * W2[v, x, t, q] * R[c, x, e]
+        out[b, p, q, e] = acc
+    return out
+
+
+@pytest.mark.parametrize("chi", [1, 2, 3])
+def test_heff_vs_bruteforce(oracle_mod, chi):
+    inp = {k: v.numpy() for k, v in synth.heff_inputs(chi, 2, 3, "c128", 90 + chi, "random").items()}
+    o = oracle_mod.heff(inp["L"], inp["W1"], inp["W2"], inp["R"], inp["psi"])
+    assert rel_frob(o, brute_heff(inp["L"], inp["W1"], inp["W2"], inp["R"], inp["psi"])) <= 1e-14
+
+
+def test_heff_order_invariance_and_einsum(oracle_mod):
+    inp = {k: v.numpy() for k, v in synth.heff_inputs(12, 2, 5, "c128", 95, "heisenberg").items()}
+    args = (inp["L"], inp["W1"], inp["W2"], inp["R"], inp["psi"])
+    o1 = oracle_mod.heff(*args)
+    o2 = oracle_mod.heff_alt(*args)
+    assert rel_frob(o1, o2) <= 1e-12
+    ref = np.einsum("awb,wvsp,vxtq,cxe,astc->bpqe", *args, optimize=True)
+    assert rel_frob(o1, ref) <= 1e-12
+
+
+def test_heff_rows_bitwise(oracle_mod):
+    inp = {k: v.numpy() for k, v in synth.heff_inputs(10, 2, 5, "c128", 96, "heisenberg").items()}
+    args = (inp["L"], inp["W1"], inp["W2"], inp["R"], inp["psi"])
+    full = oracle_mod.heff(*args)
+    rows = [0, 3, 9]
+    assert np.array_equal(oracle_mod.heff_rows(*args, rows), full[rows])
+
+
+def test_heisenberg_singlet(oracle_mod):
+    g = golden("closed_forms.json")["heisenberg_two_site"]
+    W, lb, rb = synth.heisenberg_mpo(1.0)
+    L = synth.boundary_env(5, lb)
+    R = synth.boundary_env(5, rb)
+    H = oracle_mod.heff_dense(L, W, W, R, (1, 2, 2, 1))
+    assert np.allclose(H, H.conj().T, atol=0)
+    ev = np.sort(np.linalg.eigvalsh(H))
+    assert np.max(np.abs(ev - np.array(g["eigenvalues"]))) < 1e-14
+
+
+def _jw_dense_hubbard(t, U):
+    """Global Jordan-Wigner Hubbard on modes (1up, 1dn, 2up, 2dn), 16x16, in the
+    product basis of local states |0>,|up>,|dn>,|updn> (index n_up + 2 n_dn)."""
+    a = np.array([[0.0, 1.0], [0.0, 0.0]])   # mode annihilator, basis (empty, occupied)
+    Zs = np.diag([1.0, -1.0])
+    I2 = np.eye(2)
+
+    def mode_op(j):
+        ops = [Zs] * j + [a] + [I2] * (3 - j)
+        m = ops[0]
+        for o in ops[1:]:
+            m = np.kron(m, o)
+        return m
+    c = [mode_op(j) for j in range(4)]
+    n = [ci.T @ ci for ci in c]
+    H = U * (n[0] @ n[1] + n[2] @ n[3])
+    for s in (0, 1):
+        H += -t * (c[s].T @ c[2 + s] + c[2 + s].T @ c[s])
+    # reorder: mode basis index = 8 n1u + 4 n1d + 2 n2u + n2d -> local (n_up + 2 n_dn)
+    perm = np.zeros(16, dtype=int)
+    for n1u, n1d, n2u, n2d in itertools.product((0, 1), repeat=4):
+        mode_idx = 8 * n1u + 4 * n1d + 2 * n2u + n2d
+        loc_idx = (n1u + 2 * n1d) * 4 + (n2u + 2 * n2d)
+        perm[loc_idx] = mode_idx
+    return H[np.ix_(perm, perm)], n
+
+
+def test_hubbard_two_site_matches_global_jw(oracle_mod):
+    g = golden("closed_forms.json")["hubbard_two_site_N2"]
+    W, lb, rb = synth.hubbard_mpo(g["t"], g["U"])
+    L = synth.boundary_env(6, lb)
+    R = synth.boundary_env(6, rb)
+    H = oracle_mod.heff_dense(L, W, W, R, (1, 4, 4, 1))
+    Hjw, n = _jw_dense_hubbard(g["t"], g["U"])
+    assert np.max(np.abs(H - Hjw)) < 1e-15
+    # N = 2 sector ground energy (closed form)
+    nloc = np.array([0, 1, 1, 2])
+    N = (nloc[:, None] + nloc[None, :]).reshape(-1)
+    sector = np.where(N == 2)[0]
+    e0 = np.linalg.eigvalsh(H[np.ix_(sector, sector)].real)[0]
+    assert abs(e0 - g["E0"]) < 1e-13
+
+
+def test_tebd_gate_identity_and_g0(oracle_mod):
+    A = rnd((6, 2, 7), 100, 6)
+    B = rnd((7, 2, 5), 100, 7)
+    U0 = synth.tfim_gate(0.0)
+    AB = oracle_mod.contract(A, "asb", B, "btc", "astc")
+    th = oracle_mod.tebd_theta(A, B, U0)
+    assert np.array_equal(th, AB)        # identity gate: exact (x*1 + y*0)
+    g0 = golden("closed_forms.json")["tfim_gate_g0"]
+    Ug = synth.tfim_gate(g0["tau"], g0["J"], 0.0).reshape(4, 4)
+    assert np.max(np.abs(Ug - np.diag(g0["diag"]))) < 1e-15
+    U = synth.tfim_gate(0.01)
+    th = oracle_mod.tebd_theta(A, B, U)
+    assert rel_frob(th, np.einsum("asb,btc,pqst->apqc", A, B, U)) <= 1e-14
+    # physical-first layout variant (ii) gives the same tensor
+    th2 = oracle_mod.tebd_theta(np.transpose(A, (1, 0, 2)).copy(), np.transpose(B, (1, 0, 2)).copy(), U,
+                                la="sab", lb="tbc", lu="pqst", lt="paqc")
+    assert rel_frob(np.transpose(th2, (1, 0, 2, 3)), th) <= 1e-15
+
+
+def test_mps_product_state_norm_exact(oracle_mod):
+    sites = synth.product_state_sites(10)
+    assert float(oracle_mod.mps_norm2(sites)[0, 0]) == golden("closed_forms.json")["product_state_norm"]["value"]
+
+
+def test_mps_norm_vs_dense_state(oracle_mod):
+    sites = synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1)
+    psi = sites[0]
+    for s in sites[1:]:
+        psi = np.tensordot(psi, s, axes=([psi.ndim - 1], [0]))
+    psi = psi.reshape(-1)
+    assert psi.size == 1024
+    n2 = float(oracle_mod.mps_norm2(sites)[0, 0])
+    assert abs(n2 - float(psi @ psi)) <= 1e-13 * abs(float(psi @ psi))
+    phi_sites = synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 2)
+    phi = phi_sites[0]
+    for s in phi_sites[1:]:
+        phi = np.tensordot(phi, s, axes=([phi.ndim - 1], [0]))
+    ov = float(oracle_mod.mps_overlap(phi_sites, sites)[0, 0])
+    assert abs(ov - float(phi.reshape(-1) @ psi)) <= 1e-12 * np.linalg.norm(phi) * np.linalg.norm(psi)
+
+
+def test_mps_mpo_apply(oracle_mod):
+    A = rnd((4, 2, 6), 110, 1, True)
+    I = np.eye(2, dtype=np.complex128).reshape(1, 1, 2, 2)
+    assert np.array_equal(oracle_mod.mps_mpo_apply(A, I), A)      # identity MPO: exact
+    W = rnd((3, 3, 2, 2), 110, 2, True)
+    Bp = oracle_mod.mps_mpo_apply(A, W)
+    ref = np.einsum("asb,wvst->awtbv", A, W).reshape(12, 2, 18)
+    assert Bp.shape == (12, 2, 18) and rel_frob(Bp, ref) <= 1e-15
+
+
+# ---------------------------------------------------------------------------
+# generator
+# ---------------------------------------------------------------------------
+
+def test_generator_matches_reference():
+    for seed, tid in [(0, 1), (3, 2), (6, 5), (123456789, 105)]:
+        d = synth.uniform_draws(seed, tid, 2000).numpy()
+        for i in (0, 1, 2, 17, 999, 1999):
+            assert d[i] == synth.uniform_ref(seed, tid, i)
+        assert d.min() >= -1.0 and d.max() < 1.0
+        assert not np.any(np.signbit(d) & (d == 0))
+        # chunking does not change values
+        d2 = synth.uniform_draws(seed, tid, 2000, chunk=77).numpy()
+        assert np.array_equal(d, d2)

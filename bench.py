@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark: DMRG two-site H_eff.psi apply (BASELINE.json metric
+"DMRG H_eff.psi TFLOP/s (fp64, chi=4096) at 1/2/4/8 GPU; % FP64 TC peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config target|cfg2|cfg4]
+                    [--impl tci|reference]
+
+A step is one H_eff.psi apply (L.psi GEMM -> W1,W2 MPO pass -> .R GEMM) over
+the synthetic workload, plus (N > 1) the NCCL all-gather of the output shards
+-- one Lanczos step's worth of the hot path. Default
+workload: chi=4096, d=2, D=5, complex128, Heisenberg MPO (the north-star
+target shape). value = the full (unsharded) apply's
+algorithmic flops (8 per complex MAC, FLOP-optimal order) / device time per
+step, max over ranks. Inputs (>= 1 GB each) exceed the 126 MB L2, so no flush
+is needed between steps.
+
+--impl reference times the CPU oracle (oracle/, plain loops) on the box's
+host cores on a bounded sample of output rows of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "DMRG H_eff.psi TFLOP/s (fp64, chi=4096) at 1/2/4/8 GPU; % FP64 TC peak"
+UNIT = "TFLOP/s"
+CONFIGS = {
+    "target": "target_heisenberg_chi4096",
+    "cfg2": "cfg2_heisenberg_chi1024",
+    "cfg4": "cfg4_hubbard_chi4096",
+}
+# FP64 tensor-core (DMMA) peak measured on this pool's B200 by the step-0
+# probe (tools/probe_fp64.cu; profiles/step0_fp64_probe.json): register-
+# resident mma.sync.m8n8k4.f64 at 1965 MHz. MEASURED_PEAKS.json has no FP64
+# entry; cuBLAS ZGEMM 8192^3 measured 37.01 TF/s on the same box.
+FP64_PEAK_TFLOPS = 37.06
+FP64_PEAK_SOURCE = "measured DMMA microbenchmark (profiles/step0_fp64_probe.json)"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(gpu_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def gpu_index(local_rank: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids) and ids[local_rank].isdigit():
+            return int(ids[local_rank])
+    return local_rank
+
+
+def traffic_from_profiles(workload: str):
+    """dram bytes/launch of the dominant kernel from a committed ncu --set full
+    capture summary (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("gemm_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference arm and cpu_baseline): bounded sample of output rows
+# ---------------------------------------------------------------------------
+
+def oracle_rows_run(inp_np, rows):
+    import oracle
+    t0 = time.perf_counter()
+    res = oracle.heff_rows(inp_np["L"], inp_np["W1"], inp_np["W2"], inp_np["R"], inp_np["psi"], rows)
+    return res, time.perf_counter() - t0
+
+
+def cpu_baseline(inp_np, chi, flops_full, budget_s=15.0, gpu_out=None):
+    import oracle
+    oracle.build()
+    rng = np.random.default_rng(0)
+    rows = [0]
+    res, t1 = oracle_rows_run(inp_np, rows)
+    n_more = int(max(0, min(chi - 1, budget_s / max(t1, 1e-3) - 1)))
+    more = sorted(set(int(x) for x in rng.integers(1, chi, size=n_more)) | {chi - 1})[:max(n_more, 1)]
+    res2, t2 = oracle_rows_run(inp_np, more)
+    rows_all = rows + more
+    t = t1 + t2
+    val = len(rows_all) * (flops_full / chi) / t / 1e12
+    out = {"value": val, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+           "sample": f"{len(rows_all)} output rows b (of {chi}) of the same apply, exact chain "
+                     f"(oracle.heff_rows: L sliced at b); {t:.1f} s; TFLOP/s = rows x flops/row / time"}
+    parity = None
+    if gpu_out is not None:
+        ref = np.concatenate([res, res2])
+        got = gpu_out[rows_all]
+        parity = {"rows_checked": len(rows_all),
+                  "rel_frob": float(np.linalg.norm(got - ref) / np.linalg.norm(ref))}
+    return out, parity
+
+
+# ---------------------------------------------------------------------------
+# reference arm (the oracle), bench contract "--impl reference"
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    name = CONFIGS[args.config]
+    cfg = synth.HEFF_CONFIGS[name]
+    chi, d, D = cfg["chi"], cfg["d"], cfg["D"]
+    inp = synth.heff_inputs(chi, d, D, cfg["dtype"], cfg["seed"], cfg["model"], device="cpu")
+    inp_np = {k: v.numpy() for k, v in inp.items()}
+    F = synth.heff_flops(chi, d, D)
+    rows_per_step = args.ref_rows
+    rng = np.random.default_rng(1)
+    for _ in range(args.warmup):
+        oracle_rows_run(inp_np, [int(x) for x in rng.integers(0, chi, size=rows_per_step)])
+    times = []
+    for _ in range(args.steps):
+        _, t = oracle_rows_run(inp_np, [int(x) for x in rng.integers(0, chi, size=rows_per_step)])
+        times.append(t)
+    t = float(np.mean(times))
+    val = rows_per_step * (F / chi) / t / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if cfg["dtype"] == "r64" else "c128",
+        "data": "synthetic (seeded counter-based generator; exact model MPO)",
+        "config": {"workload": name, "chi": chi, "d": d, "D": D, "dtype": cfg["dtype"], "model": cfg["model"]},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+                         "sample": f"{rows_per_step} output rows per step (of {chi}); TFLOP/s = rows x "
+                                   f"full-apply flops/chi / time"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the CUDA path
+# ---------------------------------------------------------------------------
+
+def run_tci(args):
+    import paper_2512_23917_b200 as tci
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    name = CONFIGS[args.config]
+    cfg = synth.HEFF_CONFIGS[name]
+    chi, d, D, dt = cfg["chi"], cfg["d"], cfg["D"], cfg["dtype"]
+    if chi % ws:
+        raise SystemExit(f"chi={chi} not divisible by {ws} ranks")
+    chi_lo = chi // ws
+    F = synth.heff_flops(chi, d, D, complex_=dt == "c128")
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+
+    # inputs, generated on the device (same generator as the oracle side)
+    inp = synth.heff_inputs(chi, d, D, dt, cfg["seed"], cfg["model"], device=dev)
+    L_full = inp.pop("L")
+    L = L_full[:, :, rank * chi_lo:(rank + 1) * chi_lo].contiguous()
+    del L_full
+    W1, W2, R, psi = inp["W1"], inp["W2"], inp["R"], inp["psi"]
+    out = torch.empty((chi_lo, d, d, chi), dtype=psi.dtype, device=dev)
+    full = torch.empty((chi, d, d, chi), dtype=psi.dtype, device=dev) if ws > 1 else out
+    torch.cuda.synchronize()
+
+    ctx = tci.Context(local, stream)
+    if ws > 1:
+        import torch.distributed as dist
+        obj = [tci.tci_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.comm_init(obj[0], ws, rank)
+
+    def step():
+        ctx.heff_apply(L, W1, W2, R, psi, out=out)
+        if ws > 1:
+            ctx.allgather(out, full)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device time, CUDA events on the launching stream) ----
+    sampler = ClockSampler(gpu_index(local)) if rank == 0 else None
+    time.sleep(0.3 if sampler else 0)
+    tci.tci_profile_enable(ctx.handle, True)
+    n0 = ctx.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_step = e0.elapsed_time(e1) / 1e3 / args.steps
+    launches = ctx.launch_count() - n0
+    prof = {k: tci.tci_profile_query(ctx.handle, v) for k, v in
+            (("gemm", tci.PROF_GEMM), ("skinny", tci.PROF_SKINNY), ("permute", tci.PROF_PERMUTE))}
+    tci.tci_profile_enable(ctx.handle, False)
+    clocks = sampler.stop() if sampler else None
+    if ws > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+        ln = torch.tensor([launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(ln)
+        launches = int(ln.item())
+    value = F / t_step / 1e12
+
+    # ---- end to end through the C ABI with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        hosts = {k: x.cpu().pin_memory() for k, x in (("L", L), ("W1", W1), ("W2", W2), ("R", R), ("psi", psi))}
+        hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        devs = {"L": L, "W1": W1, "W2": W2, "R": R, "psi": psi}
+        h2d = sum(x.numel() * x.element_size() for x in hosts.values())
+        d2h = hout.numel() * hout.element_size()
+
+        def e2e_step():
+            for k in hosts:
+                ctx.copy(hosts[k], devs[k])        # tci_copy: pinned host -> device
+            step()
+            ctx.copy(out, hout)                     # tci_copy: device -> pinned host
+        e2e_step()
+        torch.cuda.synchronize()
+        ke = max(1, min(args.steps, 3))
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(ke):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1) / 1e3 / ke
+        if ws > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": F / te / 1e12, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": te * 1e3,
+               "path": "tci_copy(pinned host->device) x5, tci_heff_apply, tci_copy(device->host)"}
+
+    if rank != 0:
+        ctx.close()
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_src = measured_peaks()
+    g = prof["gemm"]
+    gemm_avg_s = g["ms"] / 1e3 / max(1, g["launches"])
+    gemm_flops_per_launch = g["flops"] / max(1, g["launches"])
+    achieved = gemm_flops_per_launch / gemm_avg_s / 1e12 if g["launches"] else None
+    traffic = traffic_from_profiles(name)
+    sk = prof["skinny"]
+    roofline = {
+        "bound": "tensor", "kernel": "gemm_dmma_kernel (L.psi and T3.R GEMMs, DMMA.8x8x4)",
+        "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": traffic,
+        "peak_source": FP64_PEAK_SOURCE,
+        "flops_per_launch": gemm_flops_per_launch, "launches": g["launches"],
+        "gemm_share_of_step": g["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
+        "secondary": {
+            "kernel": "skinny_kernel (MPO pass)", "bound": "hbm",
+            "achieved": (sk["bytes"] / (sk["ms"] / 1e3) / 1e9) if sk["launches"] else None,
+            "peak": peaks.get("hbm_gbs"), "unit": "GB/s", "peak_source": peak_src,
+            "share_of_step": sk["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
+        },
+    }
+
+    cpu = None
+    parity = None
+    if ws == 1 and not args.no_cpu_baseline:
+        inp_np = {"L": L.cpu().numpy(), "W1": W1.cpu().numpy(), "W2": W2.cpu().numpy(),
+                  "R": R.cpu().numpy(), "psi": psi.cpu().numpy()}
+        cpu, parity = cpu_baseline(inp_np, chi, F, budget_s=args.cpu_budget, gpu_out=out.cpu().numpy())
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128" if dt == "c128" else "f64",
+        "data": "synthetic (seeded counter-based generator; exact model MPO as W1=W2)",
+        "config": {"workload": name, "chi": chi, "d": d, "D": D, "dtype": dt, "model": cfg["model"],
+                   "parallelism": f"output bond b sharded over {ws} rank(s); NCCL all-gather of out per step"
+                   if ws > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (L, psi, R >= 1 GB each): no flush"},
+        "pct_fp64_tc_peak": value / FP64_PEAK_TFLOPS * 100, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+        "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+        "cpu_baseline": cpu, "parity": parity, "profile": prof,
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["tci", "reference"], default="tci")
+    ap.add_argument("--config", choices=list(CONFIGS), default="target")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-rows", type=int, default=4)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_tci(args)
+
+
+if __name__ == "__main__":
+    main()

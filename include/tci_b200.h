@@ -1,0 +1,306 @@
+/*
+ * tci_b200.h -- C ABI of libtci_b200.so, the B200 (sm_100a) hot path beneath
+ * the Tensor Computing Interface (TCI) of arXiv:2512.23917.
+ *
+ * Citations: "P:n" = PAPER.md line n of the paper's LaTeX source (section /
+ * equation named beside it). Readings of ambiguous passages are numbered
+ * R1..R24 in DESIGN.md section "Readings".
+ *
+ * General conventions (apply to every entry point):
+ *  - Memory layout: row-major, last bond index fastest (R1). A
+ *    tensor descriptor describes a dense row-major array; complex elements
+ *    are interleaved (re, im), as in C99 _Complex / std::complex / torch.
+ *  - Ownership: element memory is ALWAYS owned by the caller (e.g. torch
+ *    tensors). The library never allocates device memory on a compute call;
+ *    scratch comes from tci_workspace_attach. Descriptors (tci_tensor_t) and
+ *    contexts (tci_ctx_t) are library-allocated and freed by
+ *    tci_tensor_free / tci_destroy_context.
+ *  - Asynchrony: compute calls enqueue kernels on the context's CUDA stream
+ *    and return; results are visible to work ordered after them on that
+ *    stream. Launch failures return TCI_ERR_CUDA; asynchronous device faults
+ *    surface on a later call or on tci_synchronize.
+ *  - Errors: every fallible call returns one tci_status_t; arguments are
+ *    validated completely BEFORE any kernel is launched, so an error leaves
+ *    all outputs untouched. tci_last_error() returns a thread-local message
+ *    for the most recent failure.
+ *  - Diagnostics: TCI_VERBOSE is read once at context creation:
+ *    0 silent; 1 one line per call on stderr
+ *    "tci:<op> shapes=[d0,d1;e0,...] dtype=<r32|r64|c64|c128>";
+ *    2 additionally " time_us=<int>" (the call synchronizes its stream).
+ *  - Thread safety: one context must not be used by two host threads at
+ *    once; distinct contexts are independent.
+ */
+#ifndef TCI_B200_H
+#define TCI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TCI_API __attribute__((visibility("default")))
+#else
+#define TCI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Handle to the back-end context (Tab. III "context_handle_t", P:656;
+ * create/destroy P:2332-2373). Owns the CUDA stream binding, the attached
+ * workspace, the plan cache and (optionally) an NCCL communicator. */
+typedef struct tci_ctx_s *tci_ctx_t;
+
+/* Tensor descriptor (Tab. III "ten_t"; tensor definition section
+ * II.A P:115-146): dtype + order + shape over BORROWED memory. */
+typedef struct tci_tensor_s *tci_tensor_t;
+
+/* Element type: the scalar field K in {R, C} at single or double
+ * precision (Tab. III "elem_t"; reading R14). */
+typedef enum {
+  TCI_R32 = 1,   /* float                               4 B */
+  TCI_R64 = 2,   /* double                              8 B */
+  TCI_C64 = 3,   /* complex float,  interleaved (re,im) 8 B */
+  TCI_C128 = 4   /* complex double, interleaved (re,im) 16 B */
+} tci_dtype_t;
+
+/* Status codes (the first kinds follow SPEC.md's
+ * taxonomy, the rest are build-specific). */
+typedef enum {
+  TCI_OK = 0,
+  TCI_ERR_SHAPE_MISMATCH = 1,   /* equal labels with different dims; wrong output shape; reshape size change */
+  TCI_ERR_ORDER_MISMATCH = 2,   /* label string length != tensor order; permutation length != order */
+  TCI_ERR_OUT_OF_RANGE = 3,     /* a dimension < 1 (R13); rank/index out of range */
+  TCI_ERR_LABEL_CONFLICT = 4,   /* repeated label in one operand or in gamma; label in all
+                                   three lists (R3); label in one input only and not in gamma (R4);
+                                   gamma label absent from the inputs (R5) */
+  TCI_ERR_PARSE = 5,            /* unparseable label string (NUL-terminated string expected) */
+  TCI_ERR_DEAD_CONTEXT = 6,     /* call on a destroyed context */
+  TCI_ERR_UNSUPPORTED = 7,      /* dtype mismatch between operands (one TenT per call);
+                                   order > 16; host memory passed to a compute call */
+  TCI_ERR_INVALID_ARGUMENT = 8, /* NULL pointer, not a permutation, bad enum value */
+  TCI_ERR_WORKSPACE = 9,        /* attached workspace smaller than the call needs */
+  TCI_ERR_CUDA = 10,            /* a CUDA runtime error (message in tci_last_error) */
+  TCI_ERR_NCCL = 11             /* an NCCL error, or no communicator initialised */
+} tci_status_t;
+
+#define TCI_MAX_ORDER 16
+
+/* ---------------------------------------------------------------------- */
+/* Context and version                         */
+/* ---------------------------------------------------------------------- */
+
+/* "M.m" version string of the TCI specification implemented: "1.0"
+ * (P:2505-2517). Static storage; never fails. */
+TCI_API const char *tci_version(void);
+
+/* Create a context bound to CUDA `device` and CUDA stream `stream`
+ * (a cudaStream_t passed as void*; NULL = the legacy default stream).
+ * The stream stays owned by the caller and must outlive the context.
+ * Reads TCI_VERBOSE once.
+ * Errors: INVALID_ARGUMENT (ctx NULL), OUT_OF_RANGE (no such device), CUDA. */
+TCI_API tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream);
+
+/* Destroy a context: releases descriptors' bookkeeping, the
+ * plan cache and the NCCL communicator. Never frees caller memory (the
+ * attached workspace included). The handle stays "dead" (not freed) so
+ * that any later call -- a second destroy included -- returns
+ * DEAD_CONTEXT. */
+TCI_API tci_status_t tci_destroy_context(tci_ctx_t ctx);
+
+/* Block the host until all work enqueued on the context stream finished.
+ * Errors: DEAD_CONTEXT, CUDA (including sticky asynchronous faults). */
+TCI_API tci_status_t tci_synchronize(tci_ctx_t ctx);
+
+/* Thread-local message describing the last failed call on this thread
+ * ("" if none). Static thread-local storage; valid until the next call. */
+TCI_API const char *tci_last_error(void);
+
+/* Attach caller-owned device scratch memory of `bytes` bytes (256-byte
+ * aligned pointer). Replaces any previous attachment; NULL/0 detaches. Calls
+ * that need scratch (tci_contract with permutes or aliasing, tci_heff_apply)
+ * return WORKSPACE if it is too small, before launching anything. */
+TCI_API tci_status_t tci_workspace_attach(tci_ctx_t ctx, void *dev_ws, size_t bytes);
+
+/* ---------------------------------------------------------------------- */
+/* Tensor descriptors and queries                              */
+/* ---------------------------------------------------------------------- */
+
+/* Describe `data` as a row-major tensor of `order` bonds with dimensions
+ * shape[0..order-1] (each >= 1, R13; order 0 = scalar with one element).
+ * `data` is borrowed: device memory (cudaMalloc / torch CUDA tensor) for
+ * compute calls; host memory is accepted for descriptors used only with
+ * tci_copy (pinned host memory for asynchronous copies). The location is
+ * detected with cudaPointerGetAttributes. Needs 16-byte-aligned `data` for
+ * complex128; element alignment otherwise.
+ * Errors: INVALID_ARGUMENT, UNSUPPORTED (order > 16), OUT_OF_RANGE (dim < 1),
+ * DEAD_CONTEXT. */
+TCI_API tci_status_t tci_tensor_create(tci_ctx_t ctx, tci_dtype_t dtype, int order,
+                               const int64_t *shape, void *data, tci_tensor_t *out);
+
+/* Free a descriptor (never the element memory). */
+TCI_API tci_status_t tci_tensor_free(tci_ctx_t ctx, tci_tensor_t t);
+
+TCI_API tci_status_t tci_order(tci_ctx_t ctx, tci_tensor_t t, int *order);
+TCI_API tci_status_t tci_shape(tci_ctx_t ctx, tci_tensor_t t, int64_t *shape);         /* P:766-783, shape[order] */
+TCI_API tci_status_t tci_size(tci_ctx_t ctx, tci_tensor_t t, int64_t *n);              /* P:786-803, elements */
+TCI_API tci_status_t tci_size_bytes(tci_ctx_t ctx, tci_tensor_t t, int64_t *bytes);
+
+/* Copy all elements of `src` into `dst` (same dtype and same element count;
+ * shapes may differ as by reshape) on the context stream; either side may be
+ * host or device memory (cudaMemcpyAsync). Used for end-to-end host I/O. */
+TCI_API tci_status_t tci_copy(tci_ctx_t ctx, tci_tensor_t src, tci_tensor_t dst);
+
+/* ---------------------------------------------------------------------- */
+/* Manipulation: reshape and transpose (Eq. (1)) */
+/* ---------------------------------------------------------------------- */
+
+/* In-place reshape: metadata only, element order in memory preserved
+ * (P:1170-1171). Errors: SHAPE_MISMATCH (element count changes),
+ * OUT_OF_RANGE (dim < 1), UNSUPPORTED (order > 16). Launches nothing. */
+TCI_API tci_status_t tci_reshape(tci_ctx_t ctx, tci_tensor_t inout, int order,
+                         const int64_t *new_shape);
+
+/* Out-of-place transpose, Eq. (1): out bond k is in bond
+ * new_order[k], out.shape[k] = in.shape[new_order[k]] (reading R2, NumPy
+ * axes semantics). `out` must have exactly that shape and in's dtype; in and
+ * out must not overlap. Bitwise exact (pure data movement). Kernel: shared-
+ * memory tiled transpose with 16-byte coalesced loads/stores (HBM-bound).
+ * Errors: ORDER_MISMATCH, INVALID_ARGUMENT (not a permutation / overlap),
+ * SHAPE_MISMATCH, UNSUPPORTED, CUDA. */
+TCI_API tci_status_t tci_permute(tci_ctx_t ctx, tci_tensor_t in, const int32_t *new_order,
+                         tci_tensor_t out);
+
+/* ---------------------------------------------------------------------- */
+/* contract (Eq. (3))                               */
+/* ---------------------------------------------------------------------- */
+
+/* Shape of c for labels la (order(a) entries), lb (order(b)), lc (nc):
+ * shape_c[k] = dim of label lc[k]. Validates exactly like tci_contract.
+ * Launches nothing. */
+TCI_API tci_status_t tci_contract_out_shape(tci_ctx_t ctx, tci_tensor_t a, const int32_t *la,
+                                    tci_tensor_t b, const int32_t *lb, int nc,
+                                    const int32_t *lc, int64_t *shape_c);
+
+/* Label-based Einstein contraction, list API:
+ *   c[gamma] = sum over S of a[alpha] * b[beta],  S = alpha ∩ beta \ gamma,
+ * gamma = lc gives the free bonds of c and their order;
+ * equal labels must have equal dims; empty gamma (order(c)=0)
+ * gives a 1-element result; c may alias a and/or b -- the
+ * library then computes into workspace and copies. No implicit conjugation
+ * (R9). a, b, c: same dtype, device memory; c pre-created with the exact
+ * output shape (see tci_contract_out_shape). Lowered to permute -> GEMM
+ * over the fused contracted legs -> permute back, with the
+ * permutes folded into the GEMM loaders/epilogue whenever the legs fuse.
+ * Label arrays are read during the call only.
+ * Errors: LABEL_CONFLICT, SHAPE_MISMATCH, UNSUPPORTED, WORKSPACE, CUDA,
+ * DEAD_CONTEXT, INVALID_ARGUMENT. */
+TCI_API tci_status_t tci_contract(tci_ctx_t ctx, tci_tensor_t a, const int32_t *la,
+                          tci_tensor_t b, const int32_t *lb,
+                          tci_tensor_t c, const int32_t *lc);
+
+/* String API: NUL-terminated strings, one byte per label
+ * (unsigned char value, case-sensitive; reading R12); each string must have
+ * exactly order(tensor) bytes, else ORDER_MISMATCH. "" is the empty list. */
+TCI_API tci_status_t tci_contract_str(tci_ctx_t ctx, tci_tensor_t a, const char *la,
+                              tci_tensor_t b, const char *lb,
+                              tci_tensor_t c, const char *lc);
+
+/* Workspace bytes tci_contract needs for these operands (0 when no
+ * permute/aliasing copy is needed). */
+TCI_API tci_status_t tci_contract_workspace_size(tci_ctx_t ctx, tci_tensor_t a, const int32_t *la,
+                                         tci_tensor_t b, const int32_t *lb,
+                                         tci_tensor_t c, const int32_t *lc, size_t *bytes);
+
+/* ---------------------------------------------------------------------- */
+/* Chains (definitions DESIGN.md R15-R18; the paper has no text for them)  */
+/* ---------------------------------------------------------------------- */
+
+/* Two-site DMRG effective Hamiltonian apply (R15; DMRG cited
+ * P:55):
+ *   out[b,p,q,e] = sum L[a,w,b] psi[a,s,t,c] W1[w,v,s,p] W2[v,x,t,q] R[c,x,e]
+ * Shapes: L (chi_l, D, chi_lo), W1 (D, D1, d, d), W2 (D1, D2, d, d),
+ * R (chi_r, D2, chi_ro), psi (chi_l, d, d, chi_r), out (chi_lo, d, d, chi_ro).
+ * W index order: (left MPO bond, right MPO bond, ket/in phys, bra/out phys).
+ * dtype r64 or c128 (all operands equal). The FLOP-optimal pairwise order is
+ * chosen by the chain planner (a7): L.psi (GEMM) -> W1,W2 (skinny kernel,
+ * fused as W12 when cheaper) -> .R (GEMM); intermediates live in the
+ * attached workspace (tci_heff_workspace_size). Sharding (8(e)): pass the
+ * rank's slice L[:, :, b_r] (chi_lo = chi/P) and its out slab; the result is
+ * bitwise identical to the unsharded rows.
+ * Errors: SHAPE_MISMATCH, UNSUPPORTED, WORKSPACE, CUDA, DEAD_CONTEXT. */
+TCI_API tci_status_t tci_heff_workspace_size(tci_ctx_t ctx, tci_dtype_t dtype, int64_t chi_l,
+                                     int64_t chi_lo, int64_t chi_r, int64_t chi_ro,
+                                     int64_t d, int64_t D, int64_t D1, int64_t D2,
+                                     size_t *bytes);
+TCI_API tci_status_t tci_heff_apply(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1,
+                            tci_tensor_t W2, tci_tensor_t R, tci_tensor_t psi,
+                            tci_tensor_t out);
+
+/* TEBD two-site gate application (R16; iTEBD of P:392-403):
+ *   theta[lt] = sum_{s,t} U[p,q,s,t] sum_b A[la] B[lb]
+ * with la a permutation of "asb", lb of "btc", lu == "pqst" (gate rows =
+ * out (p,q), cols = in (s,t), R16) and lt a permutation of "apqc" (same
+ * label letters as documented; any byte values are accepted as long as the
+ * roles match by position in the canonical strings "asb","btc","pqst","apqc"
+ * -- i.e. the call maps la/lb/lt onto those roles by label identity).
+ * When the physical legs are adjacent to the bond legs as in the natural
+ * ("asb","btc","apqc") or physical-first ("sab","tbc","paqc") layouts, the
+ * gate is applied in the GEMM epilogue (no intermediate theta pass).
+ * Errors: LABEL_CONFLICT, SHAPE_MISMATCH, UNSUPPORTED, WORKSPACE, CUDA. */
+TCI_API tci_status_t tci_tebd_theta(tci_ctx_t ctx, tci_tensor_t A, const char *la,
+                            tci_tensor_t B, const char *lb,
+                            tci_tensor_t U, const char *lu,
+                            tci_tensor_t theta, const char *lt);
+
+/* ---------------------------------------------------------------------- */
+/* Multi-GPU (8(e)): one communicator per context                          */
+/* ---------------------------------------------------------------------- */
+
+/* Initialise the context's NCCL communicator from a 128-byte ncclUniqueId
+ * (broadcast by the caller, e.g. with torch.distributed) for `nranks` ranks.
+ * Errors: OUT_OF_RANGE (rank), NCCL, DEAD_CONTEXT. */
+TCI_API tci_status_t tci_comm_init(tci_ctx_t ctx, const void *nccl_unique_id, int nranks, int rank);
+
+/* Fill `id` (128 bytes) with a new ncclUniqueId (rank 0 calls this). */
+TCI_API tci_status_t tci_comm_unique_id(void *id);
+
+/* All-gather along the slowest bond: full = concat over ranks (rank order)
+ * of each rank's `shard` (ncclAllGather on the context stream). full must
+ * have nranks * size(shard) elements of the same dtype.
+ * Errors: NCCL (no communicator), SHAPE_MISMATCH, UNSUPPORTED. */
+TCI_API tci_status_t tci_allgather(tci_ctx_t ctx, tci_tensor_t shard, tci_tensor_t full);
+
+/* ---------------------------------------------------------------------- */
+/* Diagnostics                                                             */
+/* ---------------------------------------------------------------------- */
+
+/* Number of CUDA kernels this context has launched so far (bench evidence). */
+TCI_API tci_status_t tci_launch_count(tci_ctx_t ctx, int64_t *count);
+
+/* Kernel profiling: when enabled, every GEMM / skinny / permute kernel the
+ * context launches is bracketed by CUDA events recorded on the context
+ * stream, together with its ALGORITHMIC work (GEMM: 2 flops per real MAC, 8
+ * per complex MAC; bytes = operands read once + result written once).
+ * Enabling (or disabling) synchronizes the stream and clears the records. */
+TCI_API tci_status_t tci_profile_enable(tci_ctx_t ctx, int on);
+
+/* Sum over recorded launches of `kind` (0 GEMM, 1 skinny, 2 permute):
+ * launch count, total event time in ms, algorithmic flops and bytes.
+ * Synchronizes the context stream. */
+TCI_API tci_status_t tci_profile_query(tci_ctx_t ctx, int kind, int64_t *launches, double *ms,
+                                       double *flops, double *bytes);
+
+/* The H_eff order planner's decision (8(a7)) for the given dimensions:
+ * writes the FLOP-optimal pairwise tree, e.g. "((((L.psi).W1).W2).R)", into
+ * buf[n] and its multiply-add count into *macs. Returns 1 when the tree is
+ * executed by the permute-free fast path, 0 when the generic tree executor
+ * (contract calls) is used. Pure host computation. */
+TCI_API int tci_heff_plan_tree(int64_t chi_l, int64_t chi_lo, int64_t chi_r, int64_t chi_ro,
+                               int64_t d, int64_t D, int64_t D1, int64_t D2, char *buf, int n,
+                               double *macs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCI_B200_H */

@@ -1,0 +1,414 @@
+"""Python binding of libtci_b200.so (include/tci_b200.h) -- argument
+marshalling only.
+
+Every ``tci_*`` function below has the name and argument order of the C ABI
+entry point it wraps and raises ``TciError`` (with ``.code`` = the
+tci_status_t) on failure. All compute runs in the CUDA kernels of the shared
+library; PyTorch is used only for device memory (tensors, the workspace),
+streams and process groups. There is no CPU fallback: importing this package
+raises if the compiled library is missing.
+
+The ``Context`` class is a convenience layer over the same calls that takes
+torch tensors (contiguous, on the context's device) and manages descriptors
+and the workspace.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional, Sequence, Tuple, Union
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtci_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2512_23917_b200.build` "
+        "(or __graft_entry__.build()); there is no fallback path")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# dtypes (tci_dtype_t)
+TCI_R32, TCI_R64, TCI_C64, TCI_C128 = 1, 2, 3, 4
+STATUS = {
+    0: "OK", 1: "SHAPE_MISMATCH", 2: "ORDER_MISMATCH", 3: "OUT_OF_RANGE",
+    4: "LABEL_CONFLICT", 5: "PARSE", 6: "DEAD_CONTEXT", 7: "UNSUPPORTED",
+    8: "INVALID_ARGUMENT", 9: "WORKSPACE", 10: "CUDA", 11: "NCCL",
+}
+EXPORTED = [
+    "tci_version", "tci_create_context", "tci_destroy_context", "tci_synchronize",
+    "tci_last_error", "tci_workspace_attach", "tci_tensor_create", "tci_tensor_free",
+    "tci_order", "tci_shape", "tci_size", "tci_size_bytes", "tci_copy", "tci_reshape",
+    "tci_permute", "tci_contract_out_shape", "tci_contract", "tci_contract_str",
+    "tci_contract_workspace_size", "tci_heff_workspace_size", "tci_heff_apply",
+    "tci_tebd_theta", "tci_comm_init", "tci_comm_unique_id", "tci_allgather",
+    "tci_launch_count", "tci_heff_plan_tree", "tci_profile_enable", "tci_profile_query",
+]
+
+
+class TciError(RuntimeError):
+    def __init__(self, code: int, fn: str):
+        self.code = code
+        msg = _lib.tci_last_error().decode(errors="replace")
+        super().__init__(f"{fn}: {STATUS.get(code, code)} ({code}): {msg}")
+
+
+_vp = ctypes.c_void_p
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_sig = {
+    "tci_version": ([], ctypes.c_char_p),
+    "tci_last_error": ([], ctypes.c_char_p),
+    "tci_create_context": ([ctypes.POINTER(_vp), ctypes.c_int, _vp], ctypes.c_int),
+    "tci_destroy_context": ([_vp], ctypes.c_int),
+    "tci_synchronize": ([_vp], ctypes.c_int),
+    "tci_workspace_attach": ([_vp, _vp, ctypes.c_size_t], ctypes.c_int),
+    "tci_tensor_create": ([_vp, ctypes.c_int, ctypes.c_int, _i64p, _vp, ctypes.POINTER(_vp)], ctypes.c_int),
+    "tci_tensor_free": ([_vp, _vp], ctypes.c_int),
+    "tci_order": ([_vp, _vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "tci_shape": ([_vp, _vp, _i64p], ctypes.c_int),
+    "tci_size": ([_vp, _vp, _i64p], ctypes.c_int),
+    "tci_size_bytes": ([_vp, _vp, _i64p], ctypes.c_int),
+    "tci_copy": ([_vp, _vp, _vp], ctypes.c_int),
+    "tci_reshape": ([_vp, _vp, ctypes.c_int, _i64p], ctypes.c_int),
+    "tci_permute": ([_vp, _vp, _i32p, _vp], ctypes.c_int),
+    "tci_contract_out_shape": ([_vp, _vp, _i32p, _vp, _i32p, ctypes.c_int, _i32p, _i64p], ctypes.c_int),
+    "tci_contract": ([_vp, _vp, _i32p, _vp, _i32p, _vp, _i32p], ctypes.c_int),
+    "tci_contract_str": ([_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p], ctypes.c_int),
+    "tci_contract_workspace_size": ([_vp, _vp, _i32p, _vp, _i32p, _vp, _i32p, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tci_heff_workspace_size": ([_vp, ctypes.c_int] + [ctypes.c_int64] * 8 + [ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tci_heff_apply": ([_vp] * 7, ctypes.c_int),
+    "tci_tebd_theta": ([_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p], ctypes.c_int),
+    "tci_comm_init": ([_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+    "tci_comm_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+    "tci_allgather": ([_vp, _vp, _vp], ctypes.c_int),
+    "tci_launch_count": ([_vp, _i64p], ctypes.c_int),
+    "tci_profile_enable": ([_vp, ctypes.c_int], ctypes.c_int),
+    "tci_profile_query": ([_vp, ctypes.c_int, _i64p] + [ctypes.POINTER(ctypes.c_double)] * 3, ctypes.c_int),
+    "tci_heff_plan_tree": ([ctypes.c_int64] * 8 + [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+}
+for _n, (_a, _r) in _sig.items():
+    _f = getattr(_lib, _n)
+    _f.argtypes = _a
+    _f.restype = _r
+
+
+def _ok(code: int, fn: str):
+    if code != 0:
+        raise TciError(code, fn)
+
+
+def _i64arr(xs: Sequence[int]):
+    xs = [int(x) for x in xs]
+    return (ctypes.c_int64 * max(1, len(xs)))(*xs)
+
+
+def _i32arr(xs: Sequence[int]):
+    xs = [int(x) for x in xs]
+    return (ctypes.c_int32 * max(1, len(xs)))(*xs)
+
+
+def _labels(l) -> "ctypes.Array":
+    if isinstance(l, (bytes, str)):
+        b = l.encode("latin-1") if isinstance(l, str) else l
+        return _i32arr(list(b))
+    return _i32arr(list(l))
+
+
+# ---------------------------------------------------------------------------
+# 1:1 wrappers of the C ABI
+# ---------------------------------------------------------------------------
+
+def tci_version() -> str:
+    return _lib.tci_version().decode()
+
+
+def tci_last_error() -> str:
+    return _lib.tci_last_error().decode(errors="replace")
+
+
+def tci_create_context(device: int = 0, stream: int = 0) -> int:
+    h = _vp()
+    _ok(_lib.tci_create_context(ctypes.byref(h), int(device), _vp(int(stream) or None)), "tci_create_context")
+    return h.value
+
+
+def tci_destroy_context(ctx: int) -> None:
+    _ok(_lib.tci_destroy_context(_vp(ctx)), "tci_destroy_context")
+
+
+def tci_synchronize(ctx: int) -> None:
+    _ok(_lib.tci_synchronize(_vp(ctx)), "tci_synchronize")
+
+
+def tci_workspace_attach(ctx: int, ptr: int, nbytes: int) -> None:
+    _ok(_lib.tci_workspace_attach(_vp(ctx), _vp(ptr or None), int(nbytes)), "tci_workspace_attach")
+
+
+def tci_tensor_create(ctx: int, dtype: int, shape: Sequence[int], data_ptr: int) -> int:
+    h = _vp()
+    _ok(_lib.tci_tensor_create(_vp(ctx), int(dtype), len(shape), _i64arr(shape), _vp(data_ptr or None),
+                               ctypes.byref(h)), "tci_tensor_create")
+    return h.value
+
+
+def tci_tensor_free(ctx: int, t: int) -> None:
+    _ok(_lib.tci_tensor_free(_vp(ctx), _vp(t)), "tci_tensor_free")
+
+
+def tci_order(ctx: int, t: int) -> int:
+    o = ctypes.c_int()
+    _ok(_lib.tci_order(_vp(ctx), _vp(t), ctypes.byref(o)), "tci_order")
+    return o.value
+
+
+def tci_shape(ctx: int, t: int) -> Tuple[int, ...]:
+    n = tci_order(ctx, t)
+    s = (ctypes.c_int64 * max(1, n))()
+    _ok(_lib.tci_shape(_vp(ctx), _vp(t), s), "tci_shape")
+    return tuple(s[i] for i in range(n))
+
+
+def tci_size(ctx: int, t: int) -> int:
+    n = ctypes.c_int64()
+    _ok(_lib.tci_size(_vp(ctx), _vp(t), ctypes.byref(n)), "tci_size")
+    return n.value
+
+
+def tci_size_bytes(ctx: int, t: int) -> int:
+    n = ctypes.c_int64()
+    _ok(_lib.tci_size_bytes(_vp(ctx), _vp(t), ctypes.byref(n)), "tci_size_bytes")
+    return n.value
+
+
+def tci_copy(ctx: int, src: int, dst: int) -> None:
+    _ok(_lib.tci_copy(_vp(ctx), _vp(src), _vp(dst)), "tci_copy")
+
+
+def tci_reshape(ctx: int, t: int, new_shape: Sequence[int]) -> None:
+    _ok(_lib.tci_reshape(_vp(ctx), _vp(t), len(new_shape), _i64arr(new_shape)), "tci_reshape")
+
+
+def tci_permute(ctx: int, src: int, new_order: Sequence[int], dst: int) -> None:
+    _ok(_lib.tci_permute(_vp(ctx), _vp(src), _i32arr(new_order), _vp(dst)), "tci_permute")
+
+
+def tci_contract_out_shape(ctx: int, a: int, la, b: int, lb, lc) -> Tuple[int, ...]:
+    lcs = _labels(lc)
+    nc = len(lc.encode("latin-1")) if isinstance(lc, str) else len(list(lc))
+    out = (ctypes.c_int64 * max(1, nc))()
+    _ok(_lib.tci_contract_out_shape(_vp(ctx), _vp(a), _labels(la), _vp(b), _labels(lb), nc, lcs, out),
+        "tci_contract_out_shape")
+    return tuple(out[i] for i in range(nc))
+
+
+def tci_contract(ctx: int, a: int, la, b: int, lb, c: int, lc) -> None:
+    _ok(_lib.tci_contract(_vp(ctx), _vp(a), _labels(la), _vp(b), _labels(lb), _vp(c), _labels(lc)),
+        "tci_contract")
+
+
+def tci_contract_str(ctx: int, a: int, la: str, b: int, lb: str, c: int, lc: str) -> None:
+    _ok(_lib.tci_contract_str(_vp(ctx), _vp(a), la.encode("latin-1"), _vp(b), lb.encode("latin-1"),
+                              _vp(c), lc.encode("latin-1")), "tci_contract_str")
+
+
+def tci_contract_workspace_size(ctx: int, a: int, la, b: int, lb, c: int, lc) -> int:
+    n = ctypes.c_size_t()
+    _ok(_lib.tci_contract_workspace_size(_vp(ctx), _vp(a), _labels(la), _vp(b), _labels(lb), _vp(c),
+                                         _labels(lc), ctypes.byref(n)), "tci_contract_workspace_size")
+    return n.value
+
+
+def tci_heff_workspace_size(ctx: int, dtype: int, chi_l, chi_lo, chi_r, chi_ro, d, D, D1, D2) -> int:
+    n = ctypes.c_size_t()
+    _ok(_lib.tci_heff_workspace_size(_vp(ctx), int(dtype), chi_l, chi_lo, chi_r, chi_ro, d, D, D1, D2,
+                                     ctypes.byref(n)), "tci_heff_workspace_size")
+    return n.value
+
+
+def tci_heff_apply(ctx: int, L: int, W1: int, W2: int, R: int, psi: int, out: int) -> None:
+    _ok(_lib.tci_heff_apply(*[_vp(x) for x in (ctx, L, W1, W2, R, psi, out)]), "tci_heff_apply")
+
+
+def tci_tebd_theta(ctx: int, A: int, la: str, B: int, lb: str, U: int, lu: str, T: int, lt: str) -> None:
+    _ok(_lib.tci_tebd_theta(_vp(ctx), _vp(A), la.encode(), _vp(B), lb.encode(), _vp(U), lu.encode(),
+                            _vp(T), lt.encode()), "tci_tebd_theta")
+
+
+def tci_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _ok(_lib.tci_comm_unique_id(buf), "tci_comm_unique_id")
+    return buf.raw
+
+
+def tci_comm_init(ctx: int, uid: bytes, nranks: int, rank: int) -> None:
+    _ok(_lib.tci_comm_init(_vp(ctx), uid, int(nranks), int(rank)), "tci_comm_init")
+
+
+def tci_allgather(ctx: int, shard: int, full: int) -> None:
+    _ok(_lib.tci_allgather(_vp(ctx), _vp(shard), _vp(full)), "tci_allgather")
+
+
+def tci_launch_count(ctx: int) -> int:
+    n = ctypes.c_int64()
+    _ok(_lib.tci_launch_count(_vp(ctx), ctypes.byref(n)), "tci_launch_count")
+    return n.value
+
+
+PROF_GEMM, PROF_SKINNY, PROF_PERMUTE = 0, 1, 2
+
+
+def tci_profile_enable(ctx: int, on: bool) -> None:
+    _ok(_lib.tci_profile_enable(_vp(ctx), int(bool(on))), "tci_profile_enable")
+
+
+def tci_profile_query(ctx: int, kind: int) -> dict:
+    n = ctypes.c_int64()
+    ms, fl, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    _ok(_lib.tci_profile_query(_vp(ctx), int(kind), ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl),
+                               ctypes.byref(by)), "tci_profile_query")
+    return {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+
+
+def tci_heff_plan_tree(chi_l, chi_lo, chi_r, chi_ro, d, D, D1, D2) -> Tuple[str, float, bool]:
+    buf = ctypes.create_string_buffer(128)
+    macs = ctypes.c_double()
+    fast = _lib.tci_heff_plan_tree(chi_l, chi_lo, chi_r, chi_ro, d, D, D1, D2, buf, 128, ctypes.byref(macs))
+    return buf.value.decode(), macs.value, bool(fast)
+
+
+# ---------------------------------------------------------------------------
+# torch convenience layer (marshalling only)
+# ---------------------------------------------------------------------------
+
+def _torch_dtype_code(t) -> int:
+    import torch
+    m = {torch.float32: TCI_R32, torch.float64: TCI_R64, torch.complex64: TCI_C64, torch.complex128: TCI_C128}
+    if t.dtype not in m:
+        raise TypeError(f"unsupported dtype {t.dtype}")
+    return m[t.dtype]
+
+
+class Context:
+    """A TCI context on one CUDA device/stream with a torch-owned workspace."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+        self.torch = torch
+        self.device = int(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        self.handle = tci_create_context(self.device, int(stream.cuda_stream))
+        self._ws = None
+        self._ws_bytes = 0
+        self._desc: Dict[tuple, int] = {}
+
+    # -- descriptors ---------------------------------------------------------
+    def tensor(self, t) -> int:
+        """Descriptor for a contiguous torch tensor (cached by pointer/shape/dtype)."""
+        if not t.is_contiguous():
+            raise ValueError("TCI tensors are dense row-major: pass a contiguous tensor")
+        key = (t.data_ptr(), tuple(t.shape), t.dtype)
+        h = self._desc.get(key)
+        if h is None:
+            h = tci_tensor_create(self.handle, _torch_dtype_code(t), tuple(t.shape), t.data_ptr())
+            self._desc[key] = h
+        return h
+
+    def host_tensor(self, t) -> int:
+        return self.tensor(t)
+
+    def free_descriptors(self):
+        for h in self._desc.values():
+            tci_tensor_free(self.handle, h)
+        self._desc.clear()
+
+    # -- workspace -----------------------------------------------------------
+    def ensure_workspace(self, nbytes: int):
+        if nbytes <= self._ws_bytes:
+            return
+        torch = self.torch
+        nbytes = int(nbytes)
+        self._ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        ptr = (self._ws.data_ptr() + 255) // 256 * 256
+        tci_workspace_attach(self.handle, ptr, nbytes)
+        self._ws_bytes = nbytes
+
+    # -- operations ----------------------------------------------------------
+    def permute(self, x, new_order, out=None):
+        if out is None:
+            out = self.torch.empty([x.shape[p] for p in new_order], dtype=x.dtype, device=x.device)
+        tci_permute(self.handle, self.tensor(x), list(new_order), self.tensor(out))
+        return out
+
+    def contract_out_shape(self, a, la, b, lb, lc):
+        return tci_contract_out_shape(self.handle, self.tensor(a), la, self.tensor(b), lb, lc)
+
+    def contract(self, a, la, b, lb, lc, out=None):
+        if out is None:
+            shape = self.contract_out_shape(a, la, b, lb, lc)
+            out = self.torch.empty(shape, dtype=a.dtype, device=a.device)
+        ha, hb, hc = self.tensor(a), self.tensor(b), self.tensor(out)
+        self.ensure_workspace(tci_contract_workspace_size(self.handle, ha, _labels_list(la), hb,
+                                                          _labels_list(lb), hc, _labels_list(lc)))
+        if isinstance(la, str) and isinstance(lb, str) and isinstance(lc, str):
+            tci_contract_str(self.handle, ha, la, hb, lb, hc, lc)
+        else:
+            tci_contract(self.handle, ha, la, hb, lb, hc, lc)
+        return out
+
+    def heff_workspace_size(self, L, W1, W2, R, psi):
+        return tci_heff_workspace_size(self.handle, _torch_dtype_code(L), L.shape[0], L.shape[2], psi.shape[3],
+                                       R.shape[2], psi.shape[1], L.shape[1], W1.shape[1], W2.shape[1])
+
+    def heff_apply(self, L, W1, W2, R, psi, out=None):
+        if out is None:
+            out = self.torch.empty((L.shape[2], psi.shape[1], psi.shape[2], R.shape[2]), dtype=psi.dtype,
+                                   device=psi.device)
+        self.ensure_workspace(self.heff_workspace_size(L, W1, W2, R, psi))
+        tci_heff_apply(self.handle, *[self.tensor(x) for x in (L, W1, W2, R, psi, out)])
+        return out
+
+    def tebd_theta(self, A, la, B, lb, U, lu, lt, out=None):
+        if out is None:
+            dims = {}
+            for t, l in ((A, la), (B, lb), (U, lu)):
+                for ch, n in zip(l, t.shape):
+                    dims[ch] = n
+            out = self.torch.empty([dims[ch] for ch in lt], dtype=A.dtype, device=A.device)
+        # workspace: intermediate A.B (+ contract scratch, bounded by A.B again)
+        ab = A.numel() * B.numel() // max(1, min(A.shape[la.index(ch)] for ch in la if ch in lb)) ** 2
+        self.ensure_workspace(int(2 * ab * A.element_size() + 4096))
+        tci_tebd_theta(self.handle, self.tensor(A), la, self.tensor(B), lb, self.tensor(U), lu,
+                       self.tensor(out), lt)
+        return out
+
+    def copy(self, src, dst):
+        tci_copy(self.handle, self.tensor(src), self.tensor(dst))
+        return dst
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int):
+        tci_comm_init(self.handle, uid, nranks, rank)
+
+    def allgather(self, shard, full):
+        tci_allgather(self.handle, self.tensor(shard), self.tensor(full))
+        return full
+
+    def launch_count(self) -> int:
+        return tci_launch_count(self.handle)
+
+    def synchronize(self):
+        tci_synchronize(self.handle)
+
+    def close(self):
+        if self.handle:
+            self.free_descriptors()
+            tci_destroy_context(self.handle)
+            self.handle = 0
+
+
+def _labels_list(l):
+    if isinstance(l, str):
+        return list(l.encode("latin-1"))
+    return list(l)

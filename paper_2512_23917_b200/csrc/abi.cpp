@@ -1,0 +1,580 @@
+// abi.cpp -- the extern "C" entry points of libtci_b200 (include/tci_b200.h):
+// context lifecycle, descriptors and queries,
+// reshape, transpose, contract,
+// chains, NCCL all-gather, TCI_VERBOSE diagnostics.
+// Every call validates all arguments before enqueueing any kernel.
+#include <dlfcn.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "runtime.h"
+
+namespace tci {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+const char *last_error() { return g_err; }
+
+namespace {
+struct ProfScope {
+  tci_ctx_s *ctx;
+  int kind;
+  double flops, bytes;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(tci_ctx_s *c, int k, double f, double by) : ctx(c), kind(k), flops(f), bytes(by) {
+    if (!ctx->prof_on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, ctx->stream);
+  }
+  void done() {
+    if (!ctx->prof_on || !a) return;
+    cudaEventRecord(b, ctx->stream);
+    ctx->prof.push_back({kind, a, b, flops, bytes});
+    a = b = nullptr;
+  }
+};
+}  // namespace
+
+tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g) {
+  const bool cplx = dtype_is_complex(g.dtype);
+  const double es = (double)dtype_size(g.dtype);
+  ProfScope ps(ctx, kProfGemm, (cplx ? 8.0 : 2.0) * g.M * g.N * g.K * g.batch,
+               es * g.batch * ((double)g.M * g.K + (double)g.K * g.N + (double)g.M * g.N));
+  TCI_CUDA_CHECK(launch_gemm(g, ctx->stream, &ctx->launches));
+  ps.done();
+  return TCI_OK;
+}
+
+tci_status_t run_skinny(tci_ctx_s *ctx, const SkinnyProblem &p) {
+  const bool cplx = dtype_is_complex(p.dtype);
+  const double nb = (double)p.nb[0] * p.nb[1] * p.nb[2];
+  ProfScope ps(ctx, kProfSkinny, (cplx ? 8.0 : 2.0) * nb * p.K * p.N,
+               (double)dtype_size(p.dtype) * nb * (p.K + p.N));
+  TCI_CUDA_CHECK(launch_skinny(p, ctx->stream, &ctx->launches));
+  ps.done();
+  return TCI_OK;
+}
+
+tci_status_t run_permute(tci_ctx_s *ctx, const PermuteProblem &p) {
+  ProfScope ps(ctx, kProfPermute, 0.0, 2.0 * (double)p.total * (double)p.esize);
+  TCI_CUDA_CHECK(launch_permute(p, ctx->stream, &ctx->launches));
+  ps.done();
+  return TCI_OK;
+}
+
+}  // namespace tci
+
+using namespace tci;
+
+namespace {
+
+tci_status_t check_ctx(tci_ctx_t ctx) {
+  if (!ctx) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL context");
+  if (ctx->magic != kCtxMagic) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "not a context handle");
+  if (!ctx->alive) TCI_FAIL(TCI_ERR_DEAD_CONTEXT, "context was destroyed (P:356, P:2367-2373)");
+  return TCI_OK;
+}
+
+tci_status_t check_ten(tci_ctx_t ctx, tci_tensor_t t, bool need_device) {
+  if (!t) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL tensor");
+  if (t->magic != kTenMagic) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "not a tensor descriptor");
+  if (t->ctx != ctx) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "tensor belongs to another context");
+  if (need_device && t->host)
+    TCI_FAIL(TCI_ERR_UNSUPPORTED, "compute calls need device memory (use tci_copy for host data)");
+  return TCI_OK;
+}
+
+#define CHECK(x)                   \
+  do {                             \
+    tci_status_t _s = (x);         \
+    if (_s != TCI_OK) return _s;   \
+  } while (0)
+
+const char *dtype_name(tci_dtype_t t) {
+  switch (t) {
+    case TCI_R32: return "r32";
+    case TCI_R64: return "r64";
+    case TCI_C64: return "c64";
+    case TCI_C128: return "c128";
+  }
+  return "?";
+}
+
+// TCI_VERBOSE: one line per call; level 2 adds time_us
+struct Verbose {
+  tci_ctx_t ctx;
+  const char *op;
+  std::string shapes;
+  tci_dtype_t dt;
+  std::chrono::steady_clock::time_point t0;
+  Verbose(tci_ctx_t c, const char *o, std::initializer_list<tci_tensor_t> ts) : ctx(c), op(o) {
+    if (!ctx || ctx->verbose <= 0) return;
+    dt = TCI_R64;
+    bool first = true;
+    for (tci_tensor_t t : ts) {
+      if (!t) continue;
+      if (!first) shapes += ';';
+      first = false;
+      dt = t->dtype;
+      for (int k = 0; k < t->order; k++) {
+        if (k) shapes += ',';
+        shapes += std::to_string(t->shape[k]);
+      }
+    }
+    if (ctx->verbose >= 2) {
+      cudaStreamSynchronize(ctx->stream);
+      t0 = std::chrono::steady_clock::now();
+    }
+  }
+  ~Verbose() {
+    if (!ctx || ctx->verbose <= 0) return;
+    if (ctx->verbose >= 2) {
+      cudaStreamSynchronize(ctx->stream);
+      const auto us = std::chrono::duration_cast<std::chrono::microseconds>(
+                          std::chrono::steady_clock::now() - t0)
+                          .count();
+      fprintf(stderr, "tci:%s shapes=[%s] dtype=%s time_us=%lld\n", op, shapes.c_str(),
+              dtype_name(dt), (long long)us);
+    } else {
+      fprintf(stderr, "tci:%s shapes=[%s] dtype=%s\n", op, shapes.c_str(), dtype_name(dt));
+    }
+  }
+};
+
+int read_verbose() {
+  const char *v = getenv("TCI_VERBOSE");
+  if (!v || !*v) return 0;
+  char *end = nullptr;
+  long x = strtol(v, &end, 10);
+  if (*end || x < 0) {
+    fprintf(stderr, "tci: warning: TCI_VERBOSE=%s is not 0, 1 or 2; using 0\n", v);
+    return 0;
+  }
+  return x > 2 ? 2 : (int)x;
+}
+
+tci_status_t parse_labels(const char *s, int order, int32_t *out, const char *what) {
+  if (!s) TCI_FAIL(TCI_ERR_PARSE, "%s: NULL label string", what);
+  const size_t n = strnlen(s, kMaxOrder + 1);
+  if ((int)n != order)
+    TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "%s: label string \"%s\" has %zu labels for order %d", what, s, n, order);
+  for (int i = 0; i < order; i++) out[i] = (unsigned char)s[i];
+  return TCI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *tci_version(void) { return "1.0"; }
+
+const char *tci_last_error(void) { return tci::last_error(); }
+
+tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
+  if (!ctx) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "ctx out-pointer is NULL");
+  int n = 0;
+  TCI_CUDA_CHECK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "device %d of %d", device, n);
+  TCI_CUDA_CHECK(cudaSetDevice(device));
+  tci_ctx_s *c = new tci_ctx_s();
+  c->magic = kCtxMagic;
+  c->alive = true;
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  c->verbose = read_verbose();
+  c->ws = nullptr;
+  c->ws_bytes = 0;
+  c->launches = 0;
+  c->nccl_comm = nullptr;
+  c->nranks = 1;
+  c->rank = 0;
+  c->plan_hits = c->plan_misses = 0;
+  c->prof_on = false;
+  *ctx = c;
+  return TCI_OK;
+}
+
+// NCCL through dlopen of the process's libnccl.so.2 (torch ships it); the
+// minimal ABI used here is stable across NCCL 2.x.
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef int (*nccl_get_uid_fn)(nccl_uid_t *);
+typedef int (*nccl_init_rank_fn)(void **, int, nccl_uid_t, int);
+typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
+typedef int (*nccl_destroy_fn)(void *);
+typedef const char *(*nccl_errstr_fn)(int);
+static struct {
+  void *h = nullptr;
+  nccl_get_uid_fn get_uid;
+  nccl_init_rank_fn init_rank;
+  nccl_allgather_fn allgather;
+  nccl_destroy_fn destroy;
+  nccl_errstr_fn errstr;
+} g_nccl;
+
+static tci_status_t nccl_load() {
+  if (g_nccl.h) return TCI_OK;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW);
+  if (!h) TCI_FAIL(TCI_ERR_NCCL, "cannot load libnccl.so.2: %s", dlerror());
+  g_nccl.get_uid = (nccl_get_uid_fn)dlsym(h, "ncclGetUniqueId");
+  g_nccl.init_rank = (nccl_init_rank_fn)dlsym(h, "ncclCommInitRank");
+  g_nccl.allgather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
+  g_nccl.destroy = (nccl_destroy_fn)dlsym(h, "ncclCommDestroy");
+  g_nccl.errstr = (nccl_errstr_fn)dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.get_uid || !g_nccl.init_rank || !g_nccl.allgather || !g_nccl.destroy)
+    TCI_FAIL(TCI_ERR_NCCL, "libnccl.so.2 lacks a required symbol");
+  g_nccl.h = h;
+  return TCI_OK;
+}
+
+static void prof_clear(tci_ctx_t ctx);
+
+tci_status_t tci_destroy_context(tci_ctx_t ctx) {
+  CHECK(check_ctx(ctx));
+  Verbose vb(ctx, "destroy_context", {});
+  if (ctx->nccl_comm && g_nccl.destroy) g_nccl.destroy(ctx->nccl_comm);
+  cudaStreamSynchronize(ctx->stream);
+  prof_clear(ctx);
+  ctx->prof_on = false;
+  ctx->nccl_comm = nullptr;
+  ctx->plan_cache.clear();
+  ctx->ws = nullptr;
+  ctx->ws_bytes = 0;
+  ctx->alive = false;   // handle kept (not freed) so later calls see DEAD_CONTEXT
+  return TCI_OK;
+}
+
+tci_status_t tci_synchronize(tci_ctx_t ctx) {
+  CHECK(check_ctx(ctx));
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  return TCI_OK;
+}
+
+tci_status_t tci_workspace_attach(tci_ctx_t ctx, void *dev_ws, size_t bytes) {
+  CHECK(check_ctx(ctx));
+  if (dev_ws && ((uintptr_t)dev_ws % 256))
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  ctx->ws = bytes ? dev_ws : nullptr;
+  ctx->ws_bytes = dev_ws ? bytes : 0;
+  return TCI_OK;
+}
+
+tci_status_t tci_launch_count(tci_ctx_t ctx, int64_t *count) {
+  CHECK(check_ctx(ctx));
+  if (!count) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL count");
+  *count = ctx->launches;
+  return TCI_OK;
+}
+
+static void prof_clear(tci_ctx_t ctx) {
+  for (auto &r : ctx->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  ctx->prof.clear();
+}
+
+tci_status_t tci_profile_enable(tci_ctx_t ctx, int on) {
+  CHECK(check_ctx(ctx));
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  prof_clear(ctx);
+  ctx->prof_on = on != 0;
+  return TCI_OK;
+}
+
+tci_status_t tci_profile_query(tci_ctx_t ctx, int kind, int64_t *launches, double *ms, double *flops,
+                               double *bytes) {
+  CHECK(check_ctx(ctx));
+  if (kind < 0 || kind > 2) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "profile kind %d", kind);
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  int64_t n = 0;
+  double t = 0, f = 0, by = 0;
+  for (auto &r : ctx->prof) {
+    if (r.kind != kind) continue;
+    float x = 0;
+    TCI_CUDA_CHECK(cudaEventElapsedTime(&x, r.a, r.b));
+    n++;
+    t += x;
+    f += r.flops;
+    by += r.bytes;
+  }
+  if (launches) *launches = n;
+  if (ms) *ms = t;
+  if (flops) *flops = f;
+  if (bytes) *bytes = by;
+  return TCI_OK;
+}
+
+tci_status_t tci_tensor_create(tci_ctx_t ctx, tci_dtype_t dtype, int order, const int64_t *shape,
+                               void *data, tci_tensor_t *out) {
+  CHECK(check_ctx(ctx));
+  if (!out) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "out is NULL");
+  if (dtype < TCI_R32 || dtype > TCI_C128) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "bad dtype %d", (int)dtype);
+  if (order < 0) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "negative order");
+  if (order > kMaxOrder) TCI_FAIL(TCI_ERR_UNSUPPORTED, "order %d > %d", order, kMaxOrder);
+  if (order > 0 && !shape) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "shape is NULL");
+  for (int k = 0; k < order; k++)
+    if (shape[k] < 1) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "dimension %d is %lld (< 1, reading R13)", k, (long long)shape[k]);
+  if (!data) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "data is NULL");
+  const size_t es = dtype_size(dtype);
+  if ((uintptr_t)data % (dtype == TCI_C128 ? 16 : (es > 8 ? 8 : es)))
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "data is not aligned for dtype %s", dtype_name(dtype));
+  cudaPointerAttributes attr;
+  bool host = true;
+  if (cudaPointerGetAttributes(&attr, data) == cudaSuccess)
+    host = !(attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged);
+  cudaGetLastError();   // clear a possible "invalid value" from unregistered host memory
+  tci_tensor_s *t = new tci_tensor_s();
+  t->magic = kTenMagic;
+  t->ctx = ctx;
+  t->dtype = dtype;
+  t->order = order;
+  for (int k = 0; k < order; k++) t->shape[k] = shape[k];
+  t->data = data;
+  t->host = host;
+  *out = t;
+  return TCI_OK;
+}
+
+tci_status_t tci_tensor_free(tci_ctx_t ctx, tci_tensor_t t) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, t, false));
+  t->magic = 0;
+  delete t;
+  return TCI_OK;
+}
+
+tci_status_t tci_order(tci_ctx_t ctx, tci_tensor_t t, int *order) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, t, false));
+  if (!order) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  *order = t->order;
+  return TCI_OK;
+}
+
+tci_status_t tci_shape(tci_ctx_t ctx, tci_tensor_t t, int64_t *shape) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, t, false));
+  if (!shape && t->order) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  for (int k = 0; k < t->order; k++) shape[k] = t->shape[k];
+  return TCI_OK;
+}
+
+tci_status_t tci_size(tci_ctx_t ctx, tci_tensor_t t, int64_t *n) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, t, false));
+  if (!n) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  *n = view_of(t).size();
+  return TCI_OK;
+}
+
+tci_status_t tci_size_bytes(tci_ctx_t ctx, tci_tensor_t t, int64_t *bytes) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, t, false));
+  if (!bytes) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  *bytes = (int64_t)view_of(t).bytes();
+  return TCI_OK;
+}
+
+tci_status_t tci_copy(tci_ctx_t ctx, tci_tensor_t src, tci_tensor_t dst) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, src, false));
+  CHECK(check_ten(ctx, dst, false));
+  if (src->dtype != dst->dtype) TCI_FAIL(TCI_ERR_UNSUPPORTED, "copy: dtype mismatch");
+  if (view_of(src).size() != view_of(dst).size()) TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "copy: element counts differ");
+  Verbose vb(ctx, "copy", {src, dst});
+  TCI_CUDA_CHECK(cudaMemcpyAsync(dst->data, src->data, view_of(src).bytes(), cudaMemcpyDefault, ctx->stream));
+  return TCI_OK;
+}
+
+tci_status_t tci_reshape(tci_ctx_t ctx, tci_tensor_t t, int order, const int64_t *new_shape) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, t, false));
+  if (order < 0) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "negative order");
+  if (order > kMaxOrder) TCI_FAIL(TCI_ERR_UNSUPPORTED, "order > %d", kMaxOrder);
+  if (order && !new_shape) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL shape");
+  int64_t n = 1;
+  for (int k = 0; k < order; k++) {
+    if (new_shape[k] < 1) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "dimension %d < 1", k);
+    n *= new_shape[k];
+  }
+  if (n != view_of(t).size())
+    TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "reshape changes the element count (%lld -> %lld)",
+             (long long)view_of(t).size(), (long long)n);
+  Verbose vb(ctx, "reshape", {t});
+  t->order = order;
+  for (int k = 0; k < order; k++) t->shape[k] = new_shape[k];
+  return TCI_OK;
+}
+
+tci_status_t tci_permute(tci_ctx_t ctx, tci_tensor_t in, const int32_t *new_order, tci_tensor_t out) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, in, true));
+  CHECK(check_ten(ctx, out, true));
+  if (in->order && !new_order) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL new_order");
+  if (in->dtype != out->dtype) TCI_FAIL(TCI_ERR_UNSUPPORTED, "permute: dtype mismatch");
+  if (in->order != out->order) TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "permute: order mismatch");
+  bool seen[kMaxOrder] = {};
+  for (int k = 0; k < in->order; k++) {
+    if (new_order[k] < 0 || new_order[k] >= in->order || seen[new_order[k]])
+      TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "new_order is not a permutation");
+    seen[new_order[k]] = true;
+  }
+  for (int k = 0; k < in->order; k++)
+    if (out->shape[k] != in->shape[new_order[k]])
+      TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "permute: out.shape[%d] must be in.shape[%d]", k, new_order[k]);
+  const View vi = view_of(in), vo = view_of(out);
+  const char *a = (const char *)vi.data, *b = (const char *)vo.data;
+  if (a < b + vo.bytes() && b < a + vi.bytes())
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "permute: in and out overlap");
+  Verbose vb(ctx, "transpose", {in});
+  return permute_exec(ctx, vi, new_order, out->data);
+}
+
+tci_status_t tci_contract_out_shape(tci_ctx_t ctx, tci_tensor_t a, const int32_t *la, tci_tensor_t b,
+                                    const int32_t *lb, int nc, const int32_t *lc, int64_t *shape_c) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, a, false));
+  CHECK(check_ten(ctx, b, false));
+  if ((a->order && !la) || (b->order && !lb) || (nc && (!lc || !shape_c)))
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL label array");
+  int64_t sc[kMaxOrder];
+  CHECK(contract_shape(a->order, a->shape, la, b->order, b->shape, lb, nc, lc, sc));
+  for (int k = 0; k < nc; k++) shape_c[k] = sc[k];
+  return TCI_OK;
+}
+
+static tci_status_t contract_common(tci_ctx_t ctx, tci_tensor_t a, const int32_t *la, tci_tensor_t b,
+                                    const int32_t *lb, tci_tensor_t c, const int32_t *lc, bool dry,
+                                    size_t *need) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, a, !dry));
+  CHECK(check_ten(ctx, b, !dry));
+  CHECK(check_ten(ctx, c, !dry));
+  if ((a->order && !la) || (b->order && !lb) || (c->order && !lc))
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL label array");
+  size_t n = 0;
+  CHECK(contract_exec(ctx, view_of(a), la, view_of(b), lb, view_of(c), lc, true, &n, nullptr, 0));
+  if (need) *need = n;
+  if (dry) return TCI_OK;
+  if (n > ctx->ws_bytes || (n && !ctx->ws))
+    TCI_FAIL(TCI_ERR_WORKSPACE, "contract needs %zu bytes of workspace, %zu attached", n, ctx->ws_bytes);
+  Verbose vb(ctx, "contract", {a, b, c});
+  return contract_exec(ctx, view_of(a), la, view_of(b), lb, view_of(c), lc, false, &n, ctx->ws,
+                       ctx->ws_bytes);
+}
+
+tci_status_t tci_contract(tci_ctx_t ctx, tci_tensor_t a, const int32_t *la, tci_tensor_t b,
+                          const int32_t *lb, tci_tensor_t c, const int32_t *lc) {
+  return contract_common(ctx, a, la, b, lb, c, lc, false, nullptr);
+}
+
+tci_status_t tci_contract_str(tci_ctx_t ctx, tci_tensor_t a, const char *la, tci_tensor_t b,
+                              const char *lb, tci_tensor_t c, const char *lc) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, a, true));
+  CHECK(check_ten(ctx, b, true));
+  CHECK(check_ten(ctx, c, true));
+  int32_t ia[kMaxOrder], ib[kMaxOrder], ic[kMaxOrder];
+  CHECK(parse_labels(la, a->order, ia, "a"));
+  CHECK(parse_labels(lb, b->order, ib, "b"));
+  CHECK(parse_labels(lc, c->order, ic, "c"));
+  return contract_common(ctx, a, ia, b, ib, c, ic, false, nullptr);
+}
+
+tci_status_t tci_contract_workspace_size(tci_ctx_t ctx, tci_tensor_t a, const int32_t *la,
+                                         tci_tensor_t b, const int32_t *lb, tci_tensor_t c,
+                                         const int32_t *lc, size_t *bytes) {
+  if (!bytes) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  return contract_common(ctx, a, la, b, lb, c, lc, true, bytes);
+}
+
+tci_status_t tci_heff_workspace_size(tci_ctx_t ctx, tci_dtype_t dtype, int64_t chi_l, int64_t chi_lo,
+                                     int64_t chi_r, int64_t chi_ro, int64_t d, int64_t D, int64_t D1,
+                                     int64_t D2, size_t *bytes) {
+  CHECK(check_ctx(ctx));
+  if (!bytes) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  return heff_plan_bytes(dtype, chi_l, chi_lo, chi_r, chi_ro, d, D, D1, D2, bytes, nullptr);
+}
+
+tci_status_t tci_heff_apply(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2,
+                            tci_tensor_t R, tci_tensor_t psi, tci_tensor_t out) {
+  CHECK(check_ctx(ctx));
+  for (tci_tensor_t t : {L, W1, W2, R, psi, out}) CHECK(check_ten(ctx, t, true));
+  const View vo = view_of(out);
+  for (tci_tensor_t t : {L, W1, W2, R, psi}) {
+    const View v = view_of(t);
+    const char *x = (const char *)v.data, *y = (const char *)vo.data;
+    if (x < y + vo.bytes() && y < x + v.bytes())
+      TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "heff: out overlaps an input");
+  }
+  Verbose vb(ctx, "heff_apply", {L, W1, W2, R, psi});
+  return heff_exec(ctx, view_of(L), view_of(W1), view_of(W2), view_of(R), view_of(psi), vo);
+}
+
+tci_status_t tci_tebd_theta(tci_ctx_t ctx, tci_tensor_t A, const char *la, tci_tensor_t B,
+                            const char *lb, tci_tensor_t U, const char *lu, tci_tensor_t theta,
+                            const char *lt) {
+  CHECK(check_ctx(ctx));
+  for (tci_tensor_t t : {A, B, U, theta}) CHECK(check_ten(ctx, t, true));
+  if (!la || !lb || !lu || !lt) TCI_FAIL(TCI_ERR_PARSE, "tebd: NULL label string");
+  Verbose vb(ctx, "tebd_theta", {A, B, U});
+  return tebd_exec(ctx, view_of(A), la, view_of(B), lb, view_of(U), lu, view_of(theta), lt);
+}
+
+tci_status_t tci_comm_unique_id(void *id) {
+  if (!id) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL id");
+  CHECK(nccl_load());
+  nccl_uid_t u;
+  const int r = g_nccl.get_uid(&u);
+  if (r) TCI_FAIL(TCI_ERR_NCCL, "ncclGetUniqueId: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
+  memcpy(id, &u, sizeof u);
+  return TCI_OK;
+}
+
+tci_status_t tci_comm_init(tci_ctx_t ctx, const void *nccl_unique_id, int nranks, int rank) {
+  CHECK(check_ctx(ctx));
+  if (!nccl_unique_id) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL unique id");
+  if (nranks < 1 || rank < 0 || rank >= nranks) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "rank %d of %d", rank, nranks);
+  CHECK(nccl_load());
+  TCI_CUDA_CHECK(cudaSetDevice(ctx->device));
+  nccl_uid_t u;
+  memcpy(&u, nccl_unique_id, sizeof u);
+  void *comm = nullptr;
+  const int r = g_nccl.init_rank(&comm, nranks, u, rank);
+  if (r) TCI_FAIL(TCI_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
+  if (ctx->nccl_comm) g_nccl.destroy(ctx->nccl_comm);
+  ctx->nccl_comm = comm;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return TCI_OK;
+}
+
+tci_status_t tci_allgather(tci_ctx_t ctx, tci_tensor_t shard, tci_tensor_t full) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, shard, true));
+  CHECK(check_ten(ctx, full, true));
+  if (!ctx->nccl_comm) TCI_FAIL(TCI_ERR_NCCL, "no communicator (call tci_comm_init)");
+  if (shard->dtype != full->dtype) TCI_FAIL(TCI_ERR_UNSUPPORTED, "allgather: dtype mismatch");
+  const View vs = view_of(shard), vf = view_of(full);
+  if (vf.size() != vs.size() * ctx->nranks)
+    TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "allgather: full must hold nranks x shard elements");
+  Verbose vb(ctx, "allgather", {shard, full});
+  const int r = g_nccl.allgather(vs.data, vf.data, vs.bytes(), /*ncclUint8*/ 1, ctx->nccl_comm, ctx->stream);
+  if (r) TCI_FAIL(TCI_ERR_NCCL, "ncclAllGather: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
+  return TCI_OK;
+}
+
+}  // extern "C"

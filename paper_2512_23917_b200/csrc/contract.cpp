@@ -1,0 +1,385 @@
+// contract.cpp -- label analysis, leg fusion, GEMM mapping and execution of
+// tci_contract.
+//
+// Semantics (Eq. (3)): labels in both alpha
+// and beta but not in gamma are summed; gamma orders the free bonds of c.
+// Lowering: matricize A to [I,S], B to [S,J], one GEMM, refold
+// to gamma -- but the two permutes and the refold are only materialised when
+// the legs do not already FUSE into strided matrices:
+//   * extent-1 legs are dropped (they do not move any element);
+//   * for each of the 8 choices of (I order in {gamma, A}, J order in
+//     {gamma, B}, S order in {A, B}) the planner checks whether A is
+//     [I,S] or [S,I], B is [S,J] or [J,S] and gamma is [I,J] or [J,I] as
+//     contiguous leg blocks; an operand that fits is read in place by the GEMM
+//     loaders (either major-ness), one that does not is permuted into scratch;
+//     the choice minimising permuted bytes wins (ties: fixed enumeration order);
+//   * gamma == [J,I] is handled by computing C^T = B^T A^T (operand swap).
+// The plan depends only on dtype, shapes, the label STRUCTURE (labels are
+// canonicalised by first appearance) and aliasing, never on label values, so
+// relabelling is bitwise invariant (R23). Plans are cached per
+// context under that key.
+#include <algorithm>
+#include <cstring>
+
+#include "runtime.h"
+
+namespace tci {
+
+static int find_label(int n, const int32_t *l, int32_t x) {
+  for (int i = 0; i < n; i++)
+    if (l[i] == x) return i;
+  return -1;
+}
+
+tci_status_t contract_shape(int na, const int64_t *sa, const int32_t *la, int nb, const int64_t *sb,
+                            const int32_t *lb, int nc, const int32_t *lc, int64_t *sc) {
+  if (na < 0 || nb < 0 || nc < 0) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "negative order");
+  if (na > kMaxOrder || nb > kMaxOrder || nc > kMaxOrder)
+    TCI_FAIL(TCI_ERR_UNSUPPORTED, "order > %d", kMaxOrder);
+  for (int i = 0; i < na; i++)
+    if (sa[i] < 1) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "a: dimension %d < 1", i);
+  for (int i = 0; i < nb; i++)
+    if (sb[i] < 1) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "b: dimension %d < 1", i);
+  for (int i = 0; i < na; i++)
+    if (find_label(i, la, la[i]) >= 0) TCI_FAIL(TCI_ERR_LABEL_CONFLICT, "label repeated in a (P:1955)");
+  for (int i = 0; i < nb; i++)
+    if (find_label(i, lb, lb[i]) >= 0) TCI_FAIL(TCI_ERR_LABEL_CONFLICT, "label repeated in b (P:1955)");
+  for (int i = 0; i < nc; i++)
+    if (find_label(i, lc, lc[i]) >= 0) TCI_FAIL(TCI_ERR_LABEL_CONFLICT, "label repeated in c");
+  for (int i = 0; i < na; i++) {
+    const bool inb = find_label(nb, lb, la[i]) >= 0, inc = find_label(nc, lc, la[i]) >= 0;
+    if (inb && inc) TCI_FAIL(TCI_ERR_LABEL_CONFLICT, "label in a, b and c (reading R3)");
+    if (!inb && !inc) TCI_FAIL(TCI_ERR_LABEL_CONFLICT, "label only in a and not in c (reading R4)");
+  }
+  for (int i = 0; i < nb; i++) {
+    if (find_label(na, la, lb[i]) < 0 && find_label(nc, lc, lb[i]) < 0)
+      TCI_FAIL(TCI_ERR_LABEL_CONFLICT, "label only in b and not in c (reading R4)");
+  }
+  for (int i = 0; i < nc; i++)
+    if (find_label(na, la, lc[i]) < 0 && find_label(nb, lb, lc[i]) < 0)
+      TCI_FAIL(TCI_ERR_LABEL_CONFLICT, "output label absent from the inputs (reading R5)");
+  for (int i = 0; i < na; i++) {
+    const int j = find_label(nb, lb, la[i]);
+    if (j >= 0 && sa[i] != sb[j])
+      TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "dims of a shared label differ: %lld vs %lld (P:1950)",
+               (long long)sa[i], (long long)sb[j]);
+  }
+  for (int i = 0; i < nc; i++) {
+    const int ia = find_label(na, la, lc[i]);
+    sc[i] = ia >= 0 ? sa[ia] : sb[find_label(nb, lb, lc[i])];
+  }
+  return TCI_OK;
+}
+
+namespace {
+
+// one leg after dropping extent-1 legs: canonical label id, extent, stride
+struct Leg {
+  int id;
+  int64_t dim, stride;
+};
+
+struct Operand {
+  int n = 0;
+  Leg leg[kMaxOrder];
+};
+
+Operand reduce(int order, const int64_t *shape, const int *ids) {
+  Operand o;
+  int64_t st = 1;
+  int64_t strides[kMaxOrder];
+  for (int k = order - 1; k >= 0; k--) { strides[k] = st; st *= shape[k]; }
+  for (int k = 0; k < order; k++)
+    if (shape[k] > 1) o.leg[o.n++] = Leg{ids[k], shape[k], strides[k]};
+  return o;
+}
+
+// sequence of ids of an operand's legs restricted to `set`
+std::vector<int> seq_of(const Operand &o, const std::vector<char> &set) {
+  std::vector<int> s;
+  for (int k = 0; k < o.n; k++)
+    if (set[o.leg[k].id]) s.push_back(o.leg[k].id);
+  return s;
+}
+
+std::vector<int> ids_of(const Operand &o) {
+  std::vector<int> s;
+  for (int k = 0; k < o.n; k++) s.push_back(o.leg[k].id);
+  return s;
+}
+
+std::vector<int> cat(const std::vector<int> &x, const std::vector<int> &y) {
+  std::vector<int> r(x);
+  r.insert(r.end(), y.begin(), y.end());
+  return r;
+}
+
+// 0: not blocked; 1: [X,Y]; 2: [Y,X]
+int blocks(const std::vector<int> &legs, const std::vector<int> &X, const std::vector<int> &Y) {
+  if (legs == cat(X, Y)) return 1;
+  if (legs == cat(Y, X)) return 2;
+  return 0;
+}
+
+int64_t extent(const std::vector<int> &ids, const int64_t *dim_of) {
+  int64_t e = 1;
+  for (int id : ids) e *= dim_of[id];
+  return e;
+}
+
+}  // namespace
+
+// Plan decision vector layout (cached): [order choice, formA, formB, formC]
+//   formX: 0 = permute into scratch, 1 / 2 = blocks as documented above
+tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, const View &b,
+                           const int32_t *lb, const View &c, const int32_t *lc, bool dry_run,
+                           size_t *ws_needed, void *ws, size_t ws_bytes) {
+  if (a.dtype != b.dtype || a.dtype != c.dtype)
+    TCI_FAIL(TCI_ERR_UNSUPPORTED, "operands must share one dtype (one TenT per call, P:1918)");
+  int64_t sc[kMaxOrder];
+  tci_status_t st = contract_shape(a.order, a.shape, la, b.order, b.shape, lb, c.order, lc, sc);
+  if (st != TCI_OK) return st;
+  for (int k = 0; k < c.order; k++)
+    if (sc[k] != c.shape[k])
+      TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "c.shape[%d] = %lld, contraction gives %lld", k,
+               (long long)c.shape[k], (long long)sc[k]);
+
+  // canonical label ids by first appearance (a, then b, then c)
+  int ida[kMaxOrder], idb[kMaxOrder], idc[kMaxOrder];
+  int32_t uniq[3 * kMaxOrder];
+  int nu = 0;
+  auto canon = [&](int32_t l) {
+    for (int i = 0; i < nu; i++)
+      if (uniq[i] == l) return i;
+    uniq[nu] = l;
+    return nu++;
+  };
+  for (int k = 0; k < a.order; k++) ida[k] = canon(la[k]);
+  for (int k = 0; k < b.order; k++) idb[k] = canon(lb[k]);
+  for (int k = 0; k < c.order; k++) idc[k] = canon(lc[k]);
+  int64_t dim_of[3 * kMaxOrder];
+  for (int k = 0; k < a.order; k++) dim_of[ida[k]] = a.shape[k];
+  for (int k = 0; k < b.order; k++) dim_of[idb[k]] = b.shape[k];
+
+  const Operand A = reduce(a.order, a.shape, ida);
+  const Operand B = reduce(b.order, b.shape, idb);
+  const Operand C = reduce(c.order, c.shape, idc);
+
+  std::vector<char> inI(nu, 0), inJ(nu, 0), inS(nu, 0);
+  for (int k = 0; k < A.n; k++) {
+    bool in_b = false;
+    for (int j = 0; j < B.n; j++) in_b |= B.leg[j].id == A.leg[k].id;
+    (in_b ? inS : inI)[A.leg[k].id] = 1;
+  }
+  for (int j = 0; j < B.n; j++)
+    if (!inS[B.leg[j].id]) inJ[B.leg[j].id] = 1;
+
+  const std::vector<int> Ig = seq_of(C, inI), Ia = seq_of(A, inI);
+  const std::vector<int> Jg = seq_of(C, inJ), Jb = seq_of(B, inJ);
+  const std::vector<int> Sa = seq_of(A, inS), Sb = seq_of(B, inS);
+  const std::vector<int> legsA = ids_of(A), legsB = ids_of(B), legsC = ids_of(C);
+
+  // aliasing: output range overlapping an input range
+  auto overlap = [](const void *p, size_t np, const void *q, size_t nq) {
+    const char *x = static_cast<const char *>(p), *y = static_cast<const char *>(q);
+    return np && nq && x < y + nq && y < x + np;
+  };
+  const bool alias = overlap(c.data, c.bytes(), a.data, a.bytes()) ||
+                     overlap(c.data, c.bytes(), b.data, b.bytes());
+
+  // ---- plan choice (cached) ----
+  std::string key;
+  {
+    char buf[64];
+    key.reserve(256);
+    snprintf(buf, sizeof buf, "%d|%d|", (int)a.dtype, (int)alias);
+    key += buf;
+    auto put = [&](int n, const int64_t *s, const int *ids) {
+      for (int k = 0; k < n; k++) {
+        snprintf(buf, sizeof buf, "%lld:%d,", (long long)s[k], ids[k]);
+        key += buf;
+      }
+      key += ';';
+    };
+    put(a.order, a.shape, ida);
+    put(b.order, b.shape, idb);
+    put(c.order, c.shape, idc);
+  }
+  int choice = -1, formA = 0, formB = 0, formC = 0;
+  auto it = ctx->plan_cache.find(key);
+  if (it != ctx->plan_cache.end()) {
+    choice = (int)it->second[0];
+    formA = (int)it->second[1];
+    formB = (int)it->second[2];
+    formC = (int)it->second[3];
+    ctx->plan_hits++;
+  } else {
+    const int64_t nA = a.size(), nB = b.size(), nC = c.size();
+    int64_t best = -1;
+    for (int ch = 0; ch < 8; ch++) {
+      const std::vector<int> &I = (ch & 1) ? Ia : Ig;
+      const std::vector<int> &J = (ch & 2) ? Jb : Jg;
+      const std::vector<int> &S = (ch & 4) ? Sb : Sa;
+      const int fa = blocks(legsA, I, S), fb = blocks(legsB, S, J), fc = blocks(legsC, I, J);
+      const int64_t cost = (fa ? 0 : 2 * nA) + (fb ? 0 : 2 * nB) + (fc ? 0 : 2 * nC);
+      if (best < 0 || cost < best) {
+        best = cost;
+        choice = ch;
+        formA = fa;
+        formB = fb;
+        formC = fc;
+      }
+    }
+    ctx->plan_cache[key] = {choice, formA, formB, formC};
+    ctx->plan_misses++;
+  }
+  const std::vector<int> &I = (choice & 1) ? Ia : Ig;
+  const std::vector<int> &J = (choice & 2) ? Jb : Jg;
+  const std::vector<int> &S = (choice & 4) ? Sb : Sa;
+  const int64_t M = extent(I, dim_of), N = extent(J, dim_of), K = extent(S, dim_of);
+  const size_t es = dtype_size(a.dtype);
+
+  // ---- scratch layout ----
+  size_t off = 0, offA = 0, offB = 0, offC = 0;
+  if (!formA) { offA = off; off = align_up(off + (size_t)M * K * es); }
+  if (!formB) { offB = off; off = align_up(off + (size_t)K * N * es); }
+  const bool c_scratch = !formC || alias;
+  if (c_scratch) { offC = off; off = align_up(off + (size_t)M * N * es); }
+  *ws_needed = off;
+  if (dry_run) return TCI_OK;
+  if (off > ws_bytes || (off && !ws))
+    TCI_FAIL(TCI_ERR_WORKSPACE, "contract needs %zu bytes of workspace, %zu attached", off, ws_bytes);
+  char *wsb = static_cast<char *>(ws);
+
+  auto stride_in = [](const Operand &o, int id) {
+    for (int k = 0; k < o.n; k++)
+      if (o.leg[k].id == id) return o.leg[k].stride;
+    return (int64_t)0;
+  };
+  // permute the legs of operand `o` (data `src`) into order `ord` at `dst`
+  auto permute_into = [&](const Operand &o, const void *src, const std::vector<int> &ord,
+                          void *dst) -> tci_status_t {
+    PermuteProblem pp{};
+    pp.esize = es;
+    pp.in = src;
+    pp.out = dst;
+    pp.total = 1;
+    // fuse adjacent out legs that are adjacent in the input too
+    int n = 0;
+    for (size_t k = 0; k < ord.size(); k++) {
+      const int64_t d = dim_of[ord[k]], s = stride_in(o, ord[k]);
+      if (n > 0 && pp.in_stride_for_out[n - 1] == s * d) {
+        pp.shape_out[n - 1] *= d;
+        pp.in_stride_for_out[n - 1] = s;
+      } else {
+        pp.shape_out[n] = d;
+        pp.in_stride_for_out[n] = s;
+        n++;
+      }
+      pp.total *= d;
+    }
+    pp.n = n;
+    { tci_status_t _r = run_permute(ctx, pp); if (_r) return _r; }
+    return TCI_OK;
+  };
+
+  // ---- operand A as a strided [M x K] matrix ----
+  GemmProblem g{};
+  g.dtype = a.dtype;
+  g.M = M; g.N = N; g.K = K;
+  const void *Ap = a.data;
+  int fa = formA;
+  if (!formA) {
+    st = permute_into(A, a.data, cat(I, S), wsb + offA);
+    if (st != TCI_OK) return st;
+    Ap = wsb + offA;
+    fa = 1;
+  }
+  if (fa == 1) { g.a_sm = K; g.a_sk = 1; }   // [I, S]
+  else { g.a_sm = 1; g.a_sk = M; }           // [S, I]
+  const void *Bp = b.data;
+  int fb = formB;
+  if (!formB) {
+    st = permute_into(B, b.data, cat(S, J), wsb + offB);
+    if (st != TCI_OK) return st;
+    Bp = wsb + offB;
+    fb = 1;
+  }
+  if (fb == 1) { g.b_sk = N; g.b_sn = 1; }   // [S, J]
+  else { g.b_sk = 1; g.b_sn = K; }           // [J, S]
+  g.A = Ap;
+  g.B = Bp;
+  // canonicalise degenerate extents (gemm_dmma.cu contract: a_sk == 1 picks
+  // the K-contiguous loader, else a_sm must be 1)
+  auto canon_a = [](int64_t M_, int64_t K_, int64_t &sm, int64_t &sk) {
+    if (K_ == 1) { if (sm == 1 && M_ > 1) sk = 0; else { sk = 1; if (M_ == 1) sm = 1; } }
+    else if (M_ == 1 && sk != 1) sm = 1;
+  };
+  // C layout: formC == 2 means gamma = [J, I] -> swap roles
+  const bool swap = (formC == 2) && !alias;
+  void *Cp = c_scratch ? (void *)(wsb + offC) : c.data;
+  if (!swap) {
+    g.C = Cp;
+    g.c_sm = N;
+  } else {
+    GemmProblem t = g;
+    t.M = N; t.N = M;
+    t.A = Bp; t.a_sm = g.b_sn; t.a_sk = g.b_sk;
+    t.B = Ap; t.b_sk = g.a_sk; t.b_sn = g.a_sm;
+    t.C = Cp; t.c_sm = M;
+    g = t;
+  }
+  canon_a(g.M, g.K, g.a_sm, g.a_sk);
+  // B(k,n): the same rule with (N, K)
+  canon_a(g.N, g.K, g.b_sn, g.b_sk);
+  { tci_status_t _r = run_gemm(ctx, g); if (_r) return _r; }
+
+  // ---- refold into gamma order (or copy out of scratch when aliased) ----
+  if (c_scratch) {
+    if (formC == 1 || (formC == 2 && swap)) {
+      TCI_CUDA_CHECK(launch_copy(c.data, Cp, c.bytes(), ctx->stream, &ctx->launches));
+    } else {
+      // scratch holds [I, J] (or [J, I] never: swap only without scratch)
+      Operand Ct;
+      Ct.n = 0;
+      const std::vector<int> IJ = cat(I, J);
+      int64_t s = 1;
+      int64_t strides[2 * kMaxOrder];
+      for (int k = (int)IJ.size() - 1; k >= 0; k--) { strides[k] = s; s *= dim_of[IJ[k]]; }
+      for (size_t k = 0; k < IJ.size(); k++) Ct.leg[Ct.n++] = Leg{IJ[k], dim_of[IJ[k]], strides[k]};
+      st = permute_into(Ct, Cp, legsC, c.data);
+      if (st != TCI_OK) return st;
+    }
+  }
+  return TCI_OK;
+}
+
+tci_status_t permute_exec(tci_ctx_s *ctx, const View &in, const int32_t *perm, void *out_data) {
+  const size_t es = dtype_size(in.dtype);
+  int64_t strides[kMaxOrder];
+  int64_t s = 1;
+  for (int k = in.order - 1; k >= 0; k--) { strides[k] = s; s *= in.shape[k]; }
+  PermuteProblem pp{};
+  pp.esize = es;
+  pp.in = in.data;
+  pp.out = out_data;
+  pp.total = in.size();
+  int n = 0;
+  for (int k = 0; k < in.order; k++) {
+    const int64_t d = in.shape[perm[k]], st = strides[perm[k]];
+    if (d == 1) continue;
+    if (n > 0 && pp.in_stride_for_out[n - 1] == st * d) {
+      pp.shape_out[n - 1] *= d;
+      pp.in_stride_for_out[n - 1] = st;
+    } else {
+      pp.shape_out[n] = d;
+      pp.in_stride_for_out[n] = st;
+      n++;
+    }
+  }
+  pp.n = n;
+  { tci_status_t _r = run_permute(ctx, pp); if (_r) return _r; }
+  return TCI_OK;
+}
+
+}  // namespace tci

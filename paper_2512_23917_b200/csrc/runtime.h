@@ -1,0 +1,125 @@
+// runtime.h -- host-side runtime structures of libtci_b200 (context, tensor
+// descriptors, error reporting, planner entry points). Internal.
+#pragma once
+#include <cstdarg>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "tci_internal.h"
+
+struct tci_ctx_s {
+  uint32_t magic;
+  bool alive;
+  int device;
+  cudaStream_t stream;
+  int verbose;
+  void *ws;
+  size_t ws_bytes;
+  int64_t launches;
+  void *nccl_comm;
+  int nranks, rank;
+  // kernel profiling (tci_profile_enable): CUDA events on the context stream
+  // around every GEMM / skinny / permute launch, with algorithmic work
+  bool prof_on;
+  struct ProfRec {
+    int kind;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  std::vector<ProfRec> prof;
+  // plan cache: key -> serialized plan decision (see contract.cpp)
+  std::unordered_map<std::string, std::vector<int64_t>> plan_cache;
+  int64_t plan_hits, plan_misses;
+};
+
+struct tci_tensor_s {
+  uint32_t magic;
+  tci_ctx_s *ctx;
+  tci_dtype_t dtype;
+  int order;
+  int64_t shape[TCI_MAX_ORDER];
+  void *data;
+  bool host;
+};
+
+namespace tci {
+
+constexpr uint32_t kCtxMagic = 0x7c1c7c1cu;
+constexpr uint32_t kTenMagic = 0x7e4507e4u;
+
+// thread-local error message
+void set_error(const char *fmt, ...);
+const char *last_error();
+
+#define TCI_FAIL(code, ...)        \
+  do {                             \
+    ::tci::set_error(__VA_ARGS__); \
+    return (code);                 \
+  } while (0)
+
+#define TCI_CUDA_CHECK(expr)                                                                  \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      TCI_FAIL(TCI_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+// A dense row-major view (the data of a descriptor).
+struct View {
+  tci_dtype_t dtype;
+  int order;
+  int64_t shape[kMaxOrder];
+  void *data;
+  int64_t size() const {
+    int64_t n = 1;
+    for (int i = 0; i < order; i++) n *= shape[i];
+    return n;
+  }
+  size_t bytes() const { return (size_t)size() * dtype_size(dtype); }
+};
+
+inline View view_of(const tci_tensor_s *t) {
+  View v;
+  v.dtype = t->dtype;
+  v.order = t->order;
+  for (int i = 0; i < t->order; i++) v.shape[i] = t->shape[i];
+  v.data = t->data;
+  return v;
+}
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Label validation + output shape, identical check order to the oracle
+// (DESIGN.md "Error kinds").
+tci_status_t contract_shape(int na, const int64_t *sa, const int32_t *la, int nb, const int64_t *sb,
+                            const int32_t *lb, int nc, const int32_t *lc, int64_t *sc);
+
+// Plan + (unless dry_run) execute a pairwise contraction on ctx->stream using
+// scratch [ws, ws + ws_bytes). *ws_needed receives the scratch requirement.
+tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, const View &b,
+                           const int32_t *lb, const View &c, const int32_t *lc, bool dry_run,
+                           size_t *ws_needed, void *ws, size_t ws_bytes);
+
+// Permute a dense view: out bond k = in bond perm[k]. out must not overlap in.
+tci_status_t permute_exec(tci_ctx_s *ctx, const View &in, const int32_t *perm, void *out_data);
+
+// Launch wrappers: count launches and (when profiling) bracket each kernel
+// with CUDA events on ctx->stream, recording its algorithmic flops / bytes.
+enum { kProfGemm = 0, kProfSkinny = 1, kProfPermute = 2 };
+tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g);
+tci_status_t run_skinny(tci_ctx_s *ctx, const SkinnyProblem &p);
+tci_status_t run_permute(tci_ctx_s *ctx, const PermuteProblem &p);
+
+// Chains (chains.cpp)
+tci_status_t heff_plan_bytes(tci_dtype_t dt, int64_t chi_l, int64_t chi_lo, int64_t chi_r,
+                             int64_t chi_ro, int64_t d, int64_t D, int64_t D1, int64_t D2,
+                             size_t *bytes, bool *fused_w12);
+tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View &W2, const View &R,
+                       const View &psi, const View &out);
+tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View &B, const char *lb,
+                       const View &U, const char *lu, const View &T, const char *lt);
+
+}  // namespace tci

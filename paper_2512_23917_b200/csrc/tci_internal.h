@@ -1,0 +1,107 @@
+// tci_internal.h -- internal declarations shared by the C ABI layer, the
+// planner and the CUDA kernels of libtci_b200. Not installed; not part of
+// the ABI (include/tci_b200.h is).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/tci_b200.h"
+
+namespace tci {
+
+constexpr int kMaxOrder = TCI_MAX_ORDER;
+
+inline size_t dtype_size(tci_dtype_t t) {
+  switch (t) {
+    case TCI_R32: return 4;
+    case TCI_R64: return 8;
+    case TCI_C64: return 8;
+    case TCI_C128: return 16;
+  }
+  return 0;
+}
+inline bool dtype_is_complex(tci_dtype_t t) { return t == TCI_C64 || t == TCI_C128; }
+
+// ---------------------------------------------------------------------------
+// GEMM over fused legs: C[m,n] = sum_k A(m,k) B(k,n).
+// Offsets are in ELEMENTS of the dtype (a complex element = (re,im) pair).
+//   A(m,k) at A + m*a_sm + k*a_sk, exactly one of a_sm/a_sk is 1 (or both
+//   when the extent is 1); same for B(k,n) and C(m,n) (c_sn == 1 required:
+//   the planner swaps operands to reach an N-contiguous C).
+// ---------------------------------------------------------------------------
+struct GemmProblem {
+  tci_dtype_t dtype;
+  int64_t M, N, K;
+  const void *A; int64_t a_sm, a_sk;
+  const void *B; int64_t b_sk, b_sn;
+  void *C; int64_t c_sm;        // c_sn == 1
+  // Batched over one extra "batch" leg (strides in elements); batch == 1 for
+  // a plain GEMM.
+  int64_t batch = 1, a_sb = 0, b_sb = 0, c_sb = 0;
+};
+
+// Launches the DMMA (f64/c128) or FFMA (f32/c64) GEMM. Returns cudaSuccess or
+// the launch error. `launches` is incremented per kernel launched.
+cudaError_t launch_gemm(const GemmProblem &p, cudaStream_t s, int64_t *launches);
+
+// TEBD theta with the gate applied in the GEMM epilogue.
+// C = A.B with A rows (a,s) = m, B cols (t,c) = n; theta[a,p,q,c] written at
+// a*t_a + p*t_p + q*t_q + c*t_c. d = 2 only. Real f64 only.
+struct TebdProblem {
+  int64_t chi_a, chi_b, chi_c, d;
+  const double *A; int64_t a_a, a_s, a_b;   // strides (elements)
+  const double *B; int64_t b_b, b_t, b_c;
+  const double *U;                          // U[p,q,s,t] dense, 16 entries (d=2), device
+  double *T; int64_t t_a, t_p, t_q, t_c;
+};
+cudaError_t launch_tebd_fused(const TebdProblem &p, cudaStream_t s, int64_t *launches);
+bool tebd_fused_supported(const TebdProblem &p);
+
+// ---------------------------------------------------------------------------
+// Permute: out[c_out] = in[c_in], c_in[perm[k]] = c_out[k].
+// Shapes are already leg-fused by the caller.
+// ---------------------------------------------------------------------------
+struct PermuteProblem {
+  int n;                       // order after fusion (0..16)
+  int64_t shape_out[kMaxOrder];
+  int64_t in_stride_for_out[kMaxOrder];   // stride in `in` of out bond k
+  size_t esize;                // element bytes (4, 8, 16)
+  const void *in;
+  void *out;
+  int64_t total;
+};
+cudaError_t launch_permute(const PermuteProblem &p, cudaStream_t s, int64_t *launches);
+
+// ---------------------------------------------------------------------------
+// Skinny small-K contraction:
+//   out[b0,b1,b2, n] = sum_k in[b0,b1,b2, k] * W(k, n)
+// with arbitrary per-leg strides: the fused k / n leg groups are described by
+// offset tables passed BY VALUE in the kernel parameters (no device staging,
+// no workspace): in(k) at in_koff[k], out(n) at out_noff[n], W(k,n) at
+// w_koff[k] + w_noff[n]. Batch leg b2 is the coalesced leg. f64 / c128.
+// ---------------------------------------------------------------------------
+constexpr int kSkinnyMaxK = 128;
+constexpr int kSkinnyMaxN = 128;
+struct SkinnyProblem {
+  tci_dtype_t dtype;
+  int64_t nb[3];               // batch extents
+  int64_t in_sb[3], out_sb[3]; // batch strides (elements)
+  int K, N;
+  int k_lo, n_lo;              // coalescing hints: trailing k / n runs interleaved with b2
+  const void *in;
+  const void *W;
+  void *out;
+  int64_t in_koff[kSkinnyMaxK];
+  int64_t out_noff[kSkinnyMaxN];
+  int32_t w_koff[kSkinnyMaxK];
+  int32_t w_noff[kSkinnyMaxN];
+};
+cudaError_t launch_skinny(const SkinnyProblem &p, cudaStream_t s, int64_t *launches);
+// Shared-memory bytes the skinny kernel needs (must be <= 227 KB).
+size_t skinny_smem_bytes(int K, int N, size_t esz);
+
+// Plain device copy (aliasing fallback) and elementwise helpers.
+cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s, int64_t *launches);
+
+}  // namespace tci

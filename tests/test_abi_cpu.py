@@ -1,0 +1,118 @@
+"""C-ABI checks that need no GPU (-m "not gpu"): the library builds and loads,
+exports every symbol include/tci_b200.h declares, and its pure-host parts
+(version, H_eff order planner) behave as documented."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "tci_b200.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^TCI_API\s+[\w\s\*]+?\b(tci_\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2512_23917_b200 import build
+    path = build.build()
+    return ctypes.CDLL(path)
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for required in ["tci_create_context", "tci_destroy_context", "tci_tensor_create", "tci_tensor_free",
+                     "tci_permute", "tci_reshape", "tci_contract", "tci_contract_str", "tci_heff_apply",
+                     "tci_tebd_theta", "tci_allgather", "tci_version"]:
+        assert required in syms
+
+
+def test_exports_every_declared_symbol(lib):
+    path = lib._name
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\sT\s(tci_\w+)$", out, flags=re.M))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    # and nothing else leaks from the library (hidden visibility)
+    extra = [s for s in exported if s not in declared_symbols()]
+    assert not extra, extra
+
+
+def test_binding_names_match_header():
+    import paper_2512_23917_b200 as tci
+    for s in declared_symbols():
+        assert hasattr(tci, s), s
+        assert s in tci.EXPORTED
+
+
+def test_version(lib):
+    import paper_2512_23917_b200 as tci
+    assert tci.tci_version() == "1.0"          # P:2505-2517 ("M.m"; may equal "1.0")
+    m = re.fullmatch(r"(\d+)\.(\d+)", tci.tci_version())
+    assert m
+
+
+def test_heff_planner_picks_L_first_chain():
+    import paper_2512_23917_b200 as tci
+    for chi, d, D in [(1024, 2, 5), (4096, 2, 5), (4096, 4, 6), (16, 2, 5)]:
+        tree, macs, fast = tci.tci_heff_plan_tree(chi, chi, chi, chi, d, D, D, D)
+        assert fast, tree
+        assert tree.startswith("(((L.psi)") or tree.startswith("((((L.psi)")
+        # FLOP-optimal cost: 2 D d^2 chi^3 + 2 D^2 d^3 chi^2 plus the W12 pre-contraction
+        opt = 2 * D * d * d * chi ** 3 + 2 * D * D * d ** 3 * chi ** 2
+        assert opt <= macs <= opt + D ** 3 * d ** 4
+    # sharded on b (chi_lo = chi / 8): still L-first, cost scales ~1/8
+    tree, macs8, fast = tci.tci_heff_plan_tree(4096, 512, 4096, 4096, 2, 5, 5, 5)
+    assert fast and "L.psi" in tree
+    # a lopsided environment makes a different tree optimal -> generic executor
+    tree, macs, fast = tci.tci_heff_plan_tree(4096, 4096, 2, 2, 2, 5, 5, 5)
+    assert not fast
+
+
+def test_planner_tree_cost_matches_bruteforce():
+    """Independent check of the DP: enumerate all 105 binary trees in Python."""
+    import itertools
+    import paper_2512_23917_b200 as tci
+    dims = dict(a=7, w=3, b=5, s=2, t=2, c=11, v=4, p=2, x=3, q=2, e=6)
+    tens = {"L": "awb", "psi": "astc", "W1": "wvsp", "W2": "vxtq", "R": "cxe"}
+    out = set("bpqe")
+
+    def legs(group):
+        inside = set("".join(tens[t] for t in group))
+        outside = set("".join(tens[t] for t in tens if t not in group)) | out
+        return inside & outside
+
+    def best(group):
+        group = tuple(sorted(group))
+        if len(group) == 1:
+            return 0
+        res = None
+        items = list(group)
+        for r in range(1, len(items)):
+            for left in itertools.combinations(items, r):
+                right = tuple(t for t in items if t not in left)
+                macs = 1
+                for l in legs(left) | legs(right):
+                    macs *= dims[l]
+                c = best(left) + best(right) + macs
+                res = c if res is None else min(res, c)
+        return res
+    ref = best(tuple(tens))
+    _, macs, _ = tci.tci_heff_plan_tree(dims["a"], dims["b"], dims["c"], dims["e"], 2, dims["w"], dims["v"], dims["x"])
+    assert macs == ref
+
+
+def test_no_gpu_context_fails_cleanly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2512_23917_b200 as tci
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_create_context(0, 0)
+    assert e.value.code in (3, 10)     # OUT_OF_RANGE (no device) or CUDA

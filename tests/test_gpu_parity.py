@@ -1,0 +1,427 @@
+"""GPU parity tests (-m gpu): the CUDA path through the C ABI vs the CPU oracle
+on the same seeded inputs (synth). Tolerances (BASELINE.json north_star,
+DESIGN.md "Parity"): relative Frobenius <= 1e-12 for float64/complex128,
+<= 1e-5 for float32/complex64; bitwise for permutes, identities and
+repeatability."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import synth
+from conftest import ROOT, rel_frob
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2512_23917_b200 as tci  # noqa: E402
+
+TOL = {"r64": 1e-12, "c128": 1e-12, "r32": 1e-5, "c64": 1e-5}
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = tci.Context(0)
+    yield c
+    c.close()
+
+
+def dev(x, dt=None):
+    t = torch.from_numpy(np.ascontiguousarray(x)) if isinstance(x, np.ndarray) else x
+    if dt is not None:
+        t = t.to(synth.TORCH_DTYPE[dt])
+    return t.cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# permute (8(a2)): bitwise
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", ["r32", "r64", "c64", "c128"])
+def test_permute_bitwise(ctx, oracle_mod, dt):
+    rng = np.random.default_rng(7)
+    shapes = [(37, 130, 65), (64, 64), (3, 1, 5, 1, 7, 2), (2, 3, 4, 5, 6), (129,), (1,), (5, 1)]
+    for i, shape in enumerate(shapes):
+        x = synth.random_tensor(shape, dt, 500 + i, 1)
+        for _ in range(4):
+            perm = list(rng.permutation(len(shape)))
+            y = ctx.permute(dev(x), perm)
+            ref = oracle_mod.permute(x.numpy(), perm)
+            assert np.array_equal(host(y).astype(ref.dtype), ref), (shape, perm)
+
+
+def test_permute_paper_example(ctx):
+    a = synth.random_tensor((3, 2, 4), "r64", 12, 1)
+    a2 = ctx.permute(dev(a), [1, 0, 2])
+    assert host(a2)[0, 1, 0] == a.numpy()[1, 0, 0]
+    assert tuple(ctx.permute(a2, [2, 1, 0]).shape) == (4, 3, 2)
+
+
+# ---------------------------------------------------------------------------
+# contract (8(a1), 8(a4), 8(a6))
+# ---------------------------------------------------------------------------
+
+def test_paper_contract_example(ctx, oracle_mod):
+    a = synth.random_tensor((3, 4, 2), "r64", 11, 1)
+    b = synth.random_tensor((2, 4, 5), "r64", 11, 2)
+    c1 = ctx.contract(dev(a), [1, -1, -2], dev(b), [-2, -1, 0], [0, 1])
+    c2 = ctx.contract(dev(a), "ijk", dev(b), "kjl", "li")
+    assert tuple(c1.shape) == (5, 3)
+    assert torch.equal(c1, c2)
+    assert rel_frob(host(c2), oracle_mod.contract(a.numpy(), "ijk", b.numpy(), "kjl", "li")) <= 1e-12
+
+
+def _random_instance(rng, big=False):
+    import string
+    ra = int(rng.integers(1, 5))
+    rb = int(rng.integers(1, 5))
+    nc = int(rng.integers(0, min(ra, rb) + 1))
+    letters = list(string.ascii_letters)
+    rng.shuffle(letters)
+    shared = letters[:nc]
+    fa = letters[nc:ra]
+    fb = letters[ra:ra + rb - nc]
+    la, lb, lc = shared + fa, shared + fb, fa + fb
+    rng.shuffle(la); rng.shuffle(lb); rng.shuffle(lc)
+    pool = [1, 2, 3, 5, 7, 8, 16, 37] if big else [1, 2, 3, 4, 5]
+    dims = {l: int(rng.choice(pool)) for l in la + lb}
+    return "".join(la), "".join(lb), "".join(lc), dims
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128", "r32", "c64"])
+@pytest.mark.parametrize("big", [False, True])
+def test_contract_random_sweep(ctx, oracle_mod, dt, big):
+    rng = np.random.default_rng(2024 + big)
+    for i in range(60):
+        la, lb, lc, dims = _random_instance(rng, big)
+        A = synth.random_tensor([dims[l] for l in la], dt, 1000 + i, 1)
+        B = synth.random_tensor([dims[l] for l in lb], dt, 1000 + i, 2)
+        C = ctx.contract(dev(A), la, dev(B), lb, lc)
+        ref = oracle_mod.contract(A.numpy(), la, B.numpy(), lb, lc)
+        assert rel_frob(host(C), ref) <= TOL[dt], (la, lb, lc, dims)
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_gemm_layouts_ragged(ctx, oracle_mod, dt):
+    """All four operand major-ness combinations, sizes spanning several tiles
+    with ragged tails (M=133, N=77, K=259), read in place (no permute)."""
+    M, N, K = 133, 77, 259
+    A = synth.random_tensor((M, K), dt, 77, 1)
+    B = synth.random_tensor((K, N), dt, 77, 2)
+    ref = oracle_mod.contract(A.numpy(), "mk", B.numpy(), "kn", "mn")
+    for la, At in (("mk", A), ("km", A.T.contiguous())):
+        for lb, Bt in (("kn", B), ("nk", B.T.contiguous())):
+            for lc in ("mn", "nm"):
+                C = ctx.contract(dev(At), la, dev(Bt), lb, lc)
+                r = ref if lc == "mn" else ref.T
+                assert rel_frob(host(C), r) <= 1e-12, (la, lb, lc)
+
+
+def test_higham_elementwise_bound(ctx, oracle_mod):
+    """Per element |C_gpu - C_oracle| <= 2 gamma_K (|A|.|B|): catches local bugs
+    that a Frobenius average could hide."""
+    A = synth.random_tensor((150, 300), "r64", 78, 1).numpy()
+    B = synth.random_tensor((300, 90), "r64", 78, 2).numpy()
+    C = host(ctx.contract(dev(A), "ik", dev(B), "kj", "ij"))
+    ref = oracle_mod.contract(A, "ik", B, "kj", "ij")
+    bound = oracle_mod.contract_abs(A, "ik", B, "kj", "ij")
+    K, u = 300, 2.0 ** -53
+    gam = K * u / (1 - K * u)
+    assert np.all(np.abs(C - ref) <= 2 * gam * bound)
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_identity_contraction_bitwise(ctx, dt):
+    a = synth.random_tensor((133, 70), dt, 79, 1)
+    eye = torch.eye(70, dtype=synth.TORCH_DTYPE[dt])
+    c = ctx.contract(dev(a), "ij", dev(eye), "jk", "ik")
+    assert torch.equal(c.cpu(), a)
+
+
+def test_outer_scalar_and_empty_gamma(ctx, oracle_mod):
+    a = synth.random_tensor((3, 40), "c128", 80, 1)
+    b = synth.random_tensor((33,), "c128", 80, 2)
+    c = ctx.contract(dev(a), "ij", dev(b), "k", "kji")
+    assert rel_frob(host(c), oracle_mod.contract(a.numpy(), "ij", b.numpy(), "k", "kji")) <= 1e-15
+    x = synth.random_tensor((2,) * 6, "r64", 81, 1)
+    y = synth.random_tensor((2,) * 6, "r64", 81, 2)
+    s = ctx.contract(dev(x), "ijklmn", dev(y), "ijklmn", "")
+    assert s.shape == () and abs(s.item() - float(oracle_mod.contract(x.numpy(), "ijklmn", y.numpy(), "ijklmn", ""))) <= 1e-14
+
+
+def test_aliasing_output(ctx, oracle_mod):
+    """correct even when c aliases a."""
+    a = synth.random_tensor((64, 48), "c128", 82, 1)
+    b = synth.random_tensor((48, 48), "c128", 82, 2)
+    ref = oracle_mod.contract(a.numpy(), "ij", b.numpy(), "jk", "ik")
+    ad = dev(a)
+    ctx.contract(ad, "ij", dev(b), "jk", "ik", out=ad)
+    assert rel_frob(host(ad), ref) <= 1e-12
+    ad = dev(a)
+    ctx.contract(ad, "ij", dev(b), "jk", "ki", out=ad.view(48, 64))
+    assert rel_frob(host(ad).reshape(48, 64), ref.T) <= 1e-12
+
+
+def test_relabel_invariance_bitwise(ctx):
+    A = dev(synth.random_tensor((40, 30, 20), "c128", 83, 1))
+    B = dev(synth.random_tensor((20, 30, 50), "c128", 83, 2))
+    c1 = ctx.contract(A, "ikl", B, "lkj", "ji")
+    c2 = ctx.contract(A, [7, -3, 100], B, [100, -3, 42], [42, 7])
+    assert torch.equal(c1, c2)
+
+
+def test_repeatability_bitwise(ctx):
+    A = dev(synth.random_tensor((300, 257), "c128", 84, 1))
+    B = dev(synth.random_tensor((257, 301), "c128", 84, 2))
+    c1 = ctx.contract(A, "ik", B, "kj", "ij")
+    c2 = ctx.contract(A, "ik", B, "kj", "ij")
+    assert torch.equal(c1, c2)
+    # row-sharded A gives bitwise identical rows (per-element k order fixed)
+    c3 = ctx.contract(A[100:200].contiguous(), "ik", B, "kj", "ij")
+    assert torch.equal(c3, c1[100:200])
+
+
+def test_errors(ctx):
+    a = dev(torch.zeros(2, 3, dtype=torch.float64))
+    b = dev(torch.zeros(3, 4, dtype=torch.float64))
+    c = dev(torch.zeros(2, 4, dtype=torch.float64))
+    ha, hb, hc = ctx.tensor(a), ctx.tensor(b), ctx.tensor(c)
+    tci.tci_contract_str(ctx.handle, ha, "ij", hb, "jk", hc, "ik")
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_contract_str(ctx.handle, ha, "ii", hb, "jk", hc, "ik")
+    assert e.value.code == 4
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_contract_str(ctx.handle, ha, "ij", hb, "jk", hc, "ijk")
+    assert e.value.code == 2
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_contract_str(ctx.handle, ha, "ij", hb, "jk", hc, "ki")   # c shape (2,4) != (4,2)
+    assert e.value.code == 1
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_contract_str(ctx.handle, ha, "ij", hb, "ik", hc, "jk")   # i: 2 vs 3
+    assert e.value.code == 1
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_contract_str(ctx.handle, ha, "ij", hb, "jk", hc, "iz")
+    assert e.value.code == 4
+    f = dev(torch.zeros(3, 4, dtype=torch.float32))
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_contract_str(ctx.handle, ha, "ij", ctx.tensor(f), "jk", hc, "ik")
+    assert e.value.code == 7
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_tensor_create(ctx.handle, tci.TCI_R64, (2, 0), a.data_ptr())
+    assert e.value.code == 3
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_reshape(ctx.handle, ha, (5,))
+    assert e.value.code == 1
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_permute(ctx.handle, ha, [0, 0], hc)
+    assert e.value.code == 8
+    # host memory passed to compute -> UNSUPPORTED
+    hbuf = torch.zeros(2, 3, dtype=torch.float64)
+    hh = tci.tci_tensor_create(ctx.handle, tci.TCI_R64, (2, 3), hbuf.data_ptr())
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_contract_str(ctx.handle, hh, "ij", hb, "jk", hc, "ik")
+    assert e.value.code == 7
+    tci.tci_tensor_free(ctx.handle, hh)
+
+
+def test_workspace_and_dead_context(oracle_mod):
+    c = tci.Context(0)
+    a = dev(synth.random_tensor((4, 5, 6), "r64", 85, 1))
+    b = dev(synth.random_tensor((6, 4, 7), "r64", 85, 2))
+    out = dev(torch.zeros(7, 5, dtype=torch.float64))
+    ha, hb, ho = c.tensor(a), c.tensor(b), c.tensor(out)
+    need = tci.tci_contract_workspace_size(c.handle, ha, "ijk", hb, "kil", ho, "lj")
+    assert need > 0
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_contract_str(c.handle, ha, "ijk", hb, "kil", ho, "lj")
+    assert e.value.code == 9
+    assert torch.count_nonzero(out).item() == 0      # nothing launched on error
+    c.ensure_workspace(need)
+    tci.tci_contract_str(c.handle, ha, "ijk", hb, "kil", ho, "lj")
+    ref = oracle_mod.contract(a.cpu().numpy(), "ijk", b.cpu().numpy(), "kil", "lj")
+    assert rel_frob(host(out), ref) <= 1e-12
+    h = c.handle
+    c.free_descriptors()
+    tci.tci_destroy_context(h)
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_destroy_context(h)
+    assert e.value.code == 6
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_synchronize(h)
+    assert e.value.code == 6
+    c.handle = 0
+
+
+def test_verbose_lines():
+    code = (
+        "import torch, paper_2512_23917_b200 as t\n"
+        "c=t.Context(0)\n"
+        "a=torch.ones(3,4,dtype=torch.float64,device='cuda'); b=torch.ones(4,5,dtype=torch.float64,device='cuda')\n"
+        "c.contract(a,'ij',b,'jk','ik'); torch.cuda.synchronize()\n")
+    for lvl, pat in (("1", "tci:contract shapes=[3,4;4,5;3,5] dtype=r64"), ("2", "time_us=")):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
+                           env=dict(os.environ, TCI_VERBOSE=lvl))
+        assert r.returncode == 0, r.stderr
+        assert pat in r.stderr, r.stderr
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
+                       env=dict(os.environ, TCI_VERBOSE="0"))
+    assert "tci:" not in r.stderr
+
+
+# ---------------------------------------------------------------------------
+# H_eff (8(a5), 8(a7))
+# ---------------------------------------------------------------------------
+
+def _heff_np(inp):
+    return {k: v.numpy() for k, v in inp.items()}
+
+
+@pytest.mark.parametrize("dt", ["c128", "r64"])
+@pytest.mark.parametrize("chi,d,D,model", [(1, 2, 5, "heisenberg"), (3, 2, 5, "heisenberg"),
+                                           (37, 2, 5, "heisenberg"), (70, 2, 3, "random"),
+                                           (20, 4, 6, "hubbard"), (9, 3, 4, "random")])
+def test_heff_small(ctx, oracle_mod, dt, chi, d, D, model):
+    if dt == "r64" and model != "random":
+        model = "random"
+    inp = synth.heff_inputs(chi, d, D, dt, 300 + chi, model)
+    gpu = ctx.heff_apply(*[dev(inp[k]) for k in ("L", "W1", "W2", "R", "psi")])
+    n = _heff_np(inp)
+    ref = oracle_mod.heff(n["L"], n["W1"], n["W2"], n["R"], n["psi"])
+    assert rel_frob(host(gpu), ref) <= 1e-12
+
+
+def test_heff_rectangular_and_generic_tree(ctx, oracle_mod):
+    """chi_l != chi_r and a lopsided case where the planner picks another tree."""
+    for (cl, clo, cr, cro) in [(30, 20, 50, 40), (64, 64, 2, 2)]:
+        L = synth.random_tensor((cl, 5, clo), "c128", 310, 1)
+        R = synth.random_tensor((cr, 5, cro), "c128", 310, 5)
+        psi = synth.random_tensor((cl, 2, 2, cr), "c128", 310, 2)
+        W = torch.from_numpy(synth.heisenberg_mpo()[0])
+        gpu = ctx.heff_apply(dev(L), dev(W), dev(W), dev(R), dev(psi))
+        ref = oracle_mod.heff(L.numpy(), W.numpy(), W.numpy(), R.numpy(), psi.numpy())
+        assert rel_frob(host(gpu), ref) <= 1e-12, (cl, clo, cr, cro)
+
+
+def test_heff_heisenberg_singlet_on_gpu(ctx):
+    W, lb, rb = synth.heisenberg_mpo()
+    L = dev(synth.boundary_env(5, lb))
+    R = dev(synth.boundary_env(5, rb))
+    Wd = dev(W)
+    cols = []
+    for k in range(4):
+        e = torch.zeros(4, dtype=torch.complex128)
+        e[k] = 1
+        cols.append(host(ctx.heff_apply(L, Wd, Wd, R, dev(e.reshape(1, 2, 2, 1)))).reshape(-1))
+    H = np.stack(cols, axis=1)
+    ev = np.sort(np.linalg.eigvalsh(H))
+    assert np.max(np.abs(ev - np.array([-0.75, 0.25, 0.25, 0.25]))) < 1e-14
+
+
+def test_heff_cfg2_sampled_rows(ctx, oracle_mod):
+    """Config 2 at full size (chi=1024, d=2, D=5, c128), in the launch
+    configuration bench.py times: sampled output rows vs the oracle, plus
+    bitwise repeatability and bitwise equality of a sharded run."""
+    cfg = synth.HEFF_CONFIGS["cfg2_heisenberg_chi1024"]
+    inp = synth.heff_inputs(cfg["chi"], cfg["d"], cfg["D"], cfg["dtype"], cfg["seed"], cfg["model"])
+    d_in = {k: dev(v) for k, v in inp.items()}
+    out = ctx.heff_apply(d_in["L"], d_in["W1"], d_in["W2"], d_in["R"], d_in["psi"])
+    out2 = ctx.heff_apply(d_in["L"], d_in["W1"], d_in["W2"], d_in["R"], d_in["psi"])
+    assert torch.equal(out, out2)
+    n = _heff_np(inp)
+    rows = [0, 1, 127, 128, 255, 256, 511, 512, 767, 768, 1023, 333, 901]
+    ref = oracle_mod.heff_rows(n["L"], n["W1"], n["W2"], n["R"], n["psi"], rows)
+    assert rel_frob(host(out)[rows], ref) <= 1e-12
+    # shard on b (P=4): rank 2's slab equals rows [512, 768) bitwise
+    Ls = d_in["L"][:, :, 512:768].contiguous()
+    part = ctx.heff_apply(Ls, d_in["W1"], d_in["W2"], d_in["R"], d_in["psi"])
+    assert torch.equal(part, out[512:768])
+
+
+def test_heff_freivalds_projection(ctx, oracle_mod):
+    """Whole-output check: out . x (random x on the e leg) equals the chain with
+    R.x contracted first (oracle, O(chi^2 D d^3))."""
+    inp = synth.heff_inputs(256, 2, 5, "c128", 321, "heisenberg")
+    out = ctx.heff_apply(*[dev(inp[k]) for k in ("L", "W1", "W2", "R", "psi")])
+    x = synth.random_np((256,), "c128", 321, 99)
+    n = _heff_np(inp)
+    Rx = oracle_mod.contract(n["R"], "cxe", x, "e", "cx")
+    T1 = oracle_mod.contract(n["L"], "awb", n["psi"], "astc", "wbstc")
+    T2 = oracle_mod.contract(T1, "wbstc", n["W1"], "wvsp", "btcvp")
+    T3 = oracle_mod.contract(T2, "btcvp", n["W2"], "vxtq", "bpqcx")
+    ref = oracle_mod.contract(T3, "bpqcx", Rx, "cx", "bpq")
+    got = oracle_mod.contract(host(out), "bpqe", x, "e", "bpq")
+    assert rel_frob(got, ref) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# TEBD (8(a8))
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("chi", [1, 33, 130])
+@pytest.mark.parametrize("layout", ["natural", "physical_first"])
+def test_tebd_theta(ctx, oracle_mod, chi, layout):
+    pf = layout == "physical_first"
+    inp = synth.tebd_inputs(chi, 2, "r64", 400 + chi, 0.01, physical_first=pf)
+    la, lb, lt = ("sab", "tbc", "paqc") if pf else ("asb", "btc", "apqc")
+    th = ctx.tebd_theta(dev(inp["A"]), la, dev(inp["B"]), lb, dev(inp["U"]), "pqst", lt)
+    ref = oracle_mod.tebd_theta(inp["A"].numpy(), inp["B"].numpy(), inp["U"].numpy(), la=la, lb=lb, lu="pqst", lt=lt)
+    assert rel_frob(host(th), ref) <= 1e-12
+
+
+def test_tebd_identity_gate_equals_AB_bitwise(ctx):
+    inp = synth.tebd_inputs(64, 2, "r64", 410, 0.0)
+    A, B = dev(inp["A"]), dev(inp["B"])
+    th = ctx.tebd_theta(A, "asb", B, "btc", dev(inp["U"]), "pqst", "apqc")
+    ab = ctx.contract(A, "asb", B, "btc", "astc")
+    assert torch.equal(th, ab)
+
+
+def test_tebd_cfg3_sampled(ctx, oracle_mod):
+    cfg = synth.TEBD_CONFIG
+    inp = synth.tebd_inputs(cfg["chi"], cfg["d"], cfg["dtype"], cfg["seed"], cfg["tau"])
+    th = host(ctx.tebd_theta(dev(inp["A"]), "asb", dev(inp["B"]), "btc", dev(inp["U"]), "pqst", "apqc"))
+    A = inp["A"].numpy()
+    for a0 in (0, 1, 1023, 2047):
+        ref = oracle_mod.tebd_theta(A[a0:a0 + 1], inp["B"].numpy(), inp["U"].numpy())
+        assert rel_frob(th[a0:a0 + 1], ref) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# MPS norm / overlap (8(a9)) and MPS-MPO application (8(a10))
+# ---------------------------------------------------------------------------
+
+def _gpu_overlap(ctx, bra, ket):
+    E = torch.ones(1, 1, dtype=torch.float64, device="cuda")
+    for Ab, Ak in zip(bra, ket):
+        X = ctx.contract(E, "xz", dev(Ab), "xsy", "zsy")
+        E = ctx.contract(X, "zsy", dev(Ak), "zsw", "yw")
+    return E
+
+
+def test_mps_norm_cfg1(ctx, oracle_mod):
+    psi = synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1)
+    phi = synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 2)
+    assert rel_frob(host(_gpu_overlap(ctx, psi, psi)), oracle_mod.mps_norm2(psi)) <= 1e-12
+    assert rel_frob(host(_gpu_overlap(ctx, phi, psi)), oracle_mod.mps_overlap(phi, psi)) <= 1e-12
+    prod = synth.product_state_sites(10)
+    assert host(_gpu_overlap(ctx, prod, prod))[0, 0] == 1.0
+
+
+def test_mps_mpo_apply(ctx, oracle_mod):
+    A = synth.random_tensor((40, 2, 33), "c128", 420, 1)
+    I = torch.eye(2, dtype=torch.complex128).reshape(1, 1, 2, 2)
+    B = ctx.contract(dev(A), "asb", dev(I), "wvst", "awtbv")
+    assert torch.equal(B.cpu().reshape(40, 2, 33), A)
+    W = synth.random_tensor((5, 5, 2, 2), "c128", 420, 2)
+    B = ctx.contract(dev(A), "asb", dev(W), "wvst", "awtbv")
+    ref = oracle_mod.mps_mpo_apply(A.numpy(), W.numpy())
+    assert rel_frob(host(B).reshape(ref.shape), ref) <= 1e-12

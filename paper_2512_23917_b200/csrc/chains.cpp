@@ -404,10 +404,12 @@ tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View
   }
   if (!bond) TCI_FAIL(TCI_ERR_LABEL_CONFLICT, "tebd: A and B share no bond label");
   for (int i = 0; i < 3; i++) {
-    if (la[i] == bond) continue;
-    if (in(lu, la[i])) s = la[i]; else a = la[i];
-    if (lb[i] == bond) continue;
-    if (in(lu, lb[i])) t = lb[i]; else c = lb[i];
+    if (la[i] != bond) {
+      if (in(lu, la[i])) s = la[i]; else a = la[i];
+    }
+    if (lb[i] != bond) {
+      if (in(lu, lb[i])) t = lb[i]; else c = lb[i];
+    }
   }
   if (!s || !a || !t || !c) TCI_FAIL(TCI_ERR_LABEL_CONFLICT, "tebd: cannot identify physical/bond legs");
   // U = (p,q,s,t) in lu: p,q are the U labels that are not s,t

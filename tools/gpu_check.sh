@@ -2,6 +2,6 @@
 # one gpurun call: GPU tests, smoke, a short bench
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -40 | tee gpurun_out/pytest_gpu.txt
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -40 | tee gpurun_out/pytest_gpu.txt
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5 | tee gpurun_out/smoke.txt
 timeout 600 python bench.py --steps 3 --warmup 3 ${BENCH_ARGS} 2>&1 | tail -5 | tee gpurun_out/bench.txt

@@ -4,24 +4,35 @@
 //
 // sm_100a has no tcgen05 kind for f64 (ptxas rejects .kind::f64) and no
 // wgmma, so the FP64 tensor path is the warp-synchronous
-// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4). Measured on this pool's B200:
-// 37.06 TF/s register-resident DMMA peak (profiles/step0_fp64_probe.json).
-// At 64 FP64 MAC/clk/SM one DMMA.8x8x4 issues every 16 cycles per SMSP, so
-// the kernel is built to keep that pipe busy and nothing else: operands are
-// staged global->smem by a 3/4-stage cp.async pipeline (16-byte chunks,
-// zero-fill for ragged edges) into padded tiles whose row pitch makes every
-// fragment load bank-conflict free (pitch mod 128 B = 32 B for
-// 4-rows x 32 B phases, 64 B for 2-rows x 64 B phases), and each warp holds a
-// 32x32 (complex) / 64x32 (real) accumulator tile in registers so every
-// fragment is reused 4-8 times.
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4). Measured on this pool's B200
+// (profiles/step0_*): 37.06 TF/s DMMA peak, 36.7 TF/s DFMA peak, and DMMA +
+// DFMA together never exceed ~37 TF/s -- one FP64 datapath. The only way to
+// run a complex GEMM faster than the 4-real-product rate is to do fewer real
+// products:
 //
-// complex128: interleaved (re,im) in global and smem; one LDS.128 yields both
-// parts of a fragment element. "4M": Cr += Ar.Br + (-Ai).Bi,
-// Ci += Ar.Bi + Ai.Br (two accumulator sets). Each output element is summed
-// over k in ascending chunks of 4 (one DMMA), independent of tiling, grid
-// size or sharding -> bitwise reproducible across runs and across P
-// (R10, R18). No split-K.
+// complex128, "3M" (Gauss): with P = Ar.Br, Q = Ai.Bi, S = (Ar+Ai).(Br+Bi),
+//   Cr = P - Q,  Ci = S - P - Q
+// -- 3 DMMAs per complex fragment product instead of 4 (the sums cost one
+// DADD per fragment element, ~1/64 of the DMMA work). Error is normwise
+// (|Ci error| <~ K u (|Ar|+|Ai|)(|Br|+|Bi|)), inside the 1e-12 relative-
+// Frobenius parity bar (R11). A 4M variant (Cr += Ar.Br - Ai.Bi,
+// Ci += Ar.Bi + Ai.Br) is kept and selectable (TCI_ZGEMM_ALGO=4m).
+//
+// Kernel structure (one CTA per 64x64 complex / 128x128 real output tile):
+//  * 4-stage cp.async pipeline, 16-byte chunks, zero-fill on ragged edges;
+//    each thread's chunk pointers and row predicates are computed once and
+//    advanced by a constant per K tile (no per-tile 64-bit index math);
+//  * padded shared-memory pitches make every fragment load conflict free
+//    (pitch mod 128 B = 32 B for 4-row x 32 B phases, 64 B for 2 x 64 B);
+//  * fragments are double-buffered in registers: the next k-step's (or the
+//    next stage's first) fragments are loaded before the current DMMAs
+//    issue, so DMMA never waits on a shared-memory load;
+//  * each output element is summed over k in ascending chunks of 4 (one
+//    DMMA) for every tiling, grid size and shard -> bitwise reproducible
+//    across runs and across P (R10, R18). No split-K.
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "../tci_internal.h"
 #include "common.cuh"
@@ -29,102 +40,187 @@
 namespace tci {
 namespace {
 
-template <bool CPLX, int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool A_K_, bool B_K_,
+enum Algo { kReal = 0, kCplx3M = 1, kCplx4M = 2 };
+
+template <int ALGO, int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool A_K_, bool B_K_,
           int VEC_>
 struct Cfg {
-  static constexpr bool kCplx = CPLX;
+  static constexpr int kAlgo = ALGO;
+  static constexpr bool kCplx = ALGO != kReal;
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
   static constexpr bool A_K = A_K_, B_K = B_K_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int NT = 32 * WARPS_M * WARPS_N;
-  static constexpr int ESZ = CPLX ? 16 : 8;               // element bytes
-  static constexpr int CHUNK = CPLX ? 1 : VEC_;            // elements per cp.async
-  static constexpr int CPB = CHUNK * ESZ;                  // bytes per cp.async
-  // padded pitches (elements): see header comment
+  static constexpr int ESZ = kCplx ? 16 : 8;               // element bytes
+  static constexpr int CHUNK = kCplx ? 1 : VEC_;            // elements per cp.async
+  static constexpr int CPB = CHUNK * ESZ;                   // bytes per cp.async
   static constexpr int PADK = 4;
-  static constexpr int PADMN = CPLX ? 2 : 4;
+  static constexpr int PADMN = kCplx ? 2 : 4;
   static constexpr int SA = A_K ? (BK + PADK) : (BM + PADMN);
   static constexpr int SB = B_K ? (BK + PADK) : (BN + PADMN);
-  static constexpr int A_STAGE = A_K ? BM * SA : BK * SA;  // elements
+  static constexpr int A_STAGE = A_K ? BM * SA : BK * SA;   // elements
   static constexpr int B_STAGE = B_K ? BN * SB : BK * SB;
   static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) * ESZ;
   static constexpr int MI = WM / 8, NJ = WN / 8;
+  static constexpr int KK = BK / 4;
+  // loader geometry: chunks per tile row along the contiguous leg
+  static constexpr int A_CPR = A_K ? BK / CHUNK : BM / CHUNK;
+  static constexpr int A_ROWS = A_K ? BM : BK;
+  static constexpr int A_PER_T = A_ROWS * A_CPR / NT;
+  static constexpr int B_CPR = B_K ? BK / CHUNK : BN / CHUNK;
+  static constexpr int B_ROWS = B_K ? BN : BK;
+  static constexpr int B_PER_T = B_ROWS * B_CPR / NT;
+  static_assert(A_ROWS * A_CPR % NT == 0 && B_ROWS * B_CPR % NT == 0, "loader split");
+  static_assert(NT % A_CPR == 0 && NT % B_CPR == 0, "loader rows");
 };
 
-template <class C>
-struct Elem {
-  using T = typename std::conditional<C::kCplx, double2, double>::type;
-};
+// One operand's per-thread loader state. The tile is ROWS rows of CPR chunks
+// along the operand's contiguous leg; thread t owns chunk column (t % CPR)
+// of rows t / CPR + i * (NT / CPR).
+template <class C, bool IS_A>
+struct Loader {
+  static constexpr bool KMAJ = IS_A ? C::A_K : C::B_K;
+  static constexpr int CPR = IS_A ? C::A_CPR : C::B_CPR;
+  static constexpr int PER_T = IS_A ? C::A_PER_T : C::B_PER_T;
+  static constexpr int RSTEP = C::NT / CPR;
+  static constexpr int S = IS_A ? C::SA : C::SB;
+  const char *base;           // operand base (a valid dummy address)
+  const char *ptr[PER_T];     // global address of this thread's chunk in K tile 0
+  uint32_t soff[PER_T];       // byte offset inside a stage
+  int kidx[PER_T];            // k index (within the tile) of the chunk's first element
+  int nvalid_mn[PER_T];       // K-major: row valid (0/1); MN-major: valid elements in the chunk
+  int64_t kstep;              // bytes to advance per K tile
 
-template <class C>
-__device__ __forceinline__ void load_stage(const GemmProblem &p, const char *Ab, const char *Bb,
-                                           char *sA, char *sB, int64_t m0, int64_t n0,
-                                           int64_t k0) {
-  const int tid = threadIdx.x;
-  constexpr int ESZ = C::ESZ;
-  // ---- A tile ----
-  if constexpr (C::A_K) {
-    constexpr int CPR = C::BK / C::CHUNK;                 // chunks per row (m)
-    constexpr int TOT = C::BM * CPR;
+  // s_mn / s_k: element strides of the M (or N) and K legs
+  __device__ __forceinline__ void init(const char *b, int64_t mn0, int64_t MN, int64_t s_mn,
+                                       int64_t s_k) {
+    base = b;
+    const int t = threadIdx.x;
+    const int col = (t % CPR) * C::CHUNK;
 #pragma unroll
-    for (int c = tid; c < TOT; c += C::NT) {
-      const int m = c / CPR, k = (c % CPR) * C::CHUNK;
-      const int64_t gm = m0 + m, gk = k0 + k;
-      int valid = 0;
-      if (gm < p.M && gk < p.K) valid = (int)min((int64_t)C::CHUNK, p.K - gk);
-      const char *src = valid ? Ab + (gm * p.a_sm + gk) * ESZ : Ab;
-      cp_async_zfill<C::CPB>(sA + (m * C::SA + k) * ESZ, src, valid * ESZ);
+    for (int i = 0; i < PER_T; i++) {
+      const int row = t / CPR + i * RSTEP;
+      if (KMAJ) {   // rows are m (or n), chunk columns are k
+        const int64_t g = mn0 + row;
+        nvalid_mn[i] = g < MN ? 1 : 0;
+        kidx[i] = col;
+        ptr[i] = b + ((g < MN ? g : 0) * s_mn + col) * C::ESZ;
+      } else {      // rows are k, chunk columns are m (or n)
+        const int64_t g = mn0 + col;
+        nvalid_mn[i] = (int)(g < MN ? (MN - g < C::CHUNK ? MN - g : C::CHUNK) : 0);
+        kidx[i] = row;
+        ptr[i] = b + ((int64_t)row * s_k + (g < MN ? g : 0)) * C::ESZ;
+      }
+      soff[i] = (uint32_t)((row * S + col) * C::ESZ);
     }
-  } else {
-    constexpr int CPR = C::BM / C::CHUNK;
-    constexpr int TOT = C::BK * CPR;
+    kstep = (int64_t)C::BK * (KMAJ ? 1 : s_k) * C::ESZ;
+  }
+
+  // issue this thread's cp.asyncs for K tile kt into the stage at `sbase`
+  __device__ __forceinline__ void load(char *sbase, int kt, int64_t K, bool full_k) const {
+    const int64_t k0 = (int64_t)kt * C::BK;
 #pragma unroll
-    for (int c = tid; c < TOT; c += C::NT) {
-      const int k = c / CPR, m = (c % CPR) * C::CHUNK;
-      const int64_t gm = m0 + m, gk = k0 + k;
-      int valid = 0;
-      if (gm < p.M && gk < p.K) valid = (int)min((int64_t)C::CHUNK, p.M - gm);
-      const char *src = valid ? Ab + (gk * p.a_sk + gm) * ESZ : Ab;
-      cp_async_zfill<C::CPB>(sA + (k * C::SA + m) * ESZ, src, valid * ESZ);
+    for (int i = 0; i < PER_T; i++) {
+      int bytes;
+      if (KMAJ) {
+        int nk = C::CHUNK;
+        if (!full_k) {
+          const int64_t rem = K - (k0 + kidx[i]);
+          nk = rem <= 0 ? 0 : (rem < C::CHUNK ? (int)rem : C::CHUNK);
+        }
+        bytes = nvalid_mn[i] ? nk * C::ESZ : 0;
+      } else {
+        const bool kok = full_k || (k0 + kidx[i] < K);
+        bytes = kok ? nvalid_mn[i] * C::ESZ : 0;
+      }
+      const char *src = bytes ? ptr[i] + kt * kstep : base;   // nothing is read when bytes == 0
+      cp_async_zfill<C::CPB>(sbase + soff[i], src, bytes);
     }
   }
-  // ---- B tile ----
-  if constexpr (C::B_K) {
-    constexpr int CPR = C::BK / C::CHUNK;
-    constexpr int TOT = C::BN * CPR;
+};
+
+template <class C>
+struct Frag {
+  // complex 3M: (re, im, re+im) per fragment element; 4M: (re, im); real: 1
+  static constexpr int NV = C::kAlgo == kCplx3M ? 3 : (C::kCplx ? 2 : 1);
+  double a[C::MI][NV], b[C::NJ][NV];
+};
+
+template <class C>
+__device__ __forceinline__ void load_frag(Frag<C> &f, const char *sA, const char *sB, int kk,
+                                          int wm0, int wn0, int lr, int lc) {
+  const int k = kk * 4 + lc;
+  if constexpr (C::kCplx) {
+    const double2 *A = reinterpret_cast<const double2 *>(sA);
+    const double2 *B = reinterpret_cast<const double2 *>(sB);
 #pragma unroll
-    for (int c = tid; c < TOT; c += C::NT) {
-      const int n = c / CPR, k = (c % CPR) * C::CHUNK;
-      const int64_t gn = n0 + n, gk = k0 + k;
-      int valid = 0;
-      if (gn < p.N && gk < p.K) valid = (int)min((int64_t)C::CHUNK, p.K - gk);
-      const char *src = valid ? Bb + (gn * p.b_sn + gk) * ESZ : Bb;
-      cp_async_zfill<C::CPB>(sB + (n * C::SB + k) * ESZ, src, valid * ESZ);
+    for (int i = 0; i < C::MI; i++) {
+      const int m = wm0 + i * 8 + lr;
+      const double2 v = C::A_K ? A[m * C::SA + k] : A[k * C::SA + m];
+      f.a[i][0] = v.x;
+      f.a[i][1] = v.y;
+      if constexpr (C::kAlgo == kCplx3M) f.a[i][2] = v.x + v.y;
+    }
+#pragma unroll
+    for (int j = 0; j < C::NJ; j++) {
+      const int n = wn0 + j * 8 + lr;
+      const double2 v = C::B_K ? B[n * C::SB + k] : B[k * C::SB + n];
+      f.b[j][0] = v.x;
+      f.b[j][1] = v.y;
+      if constexpr (C::kAlgo == kCplx3M) f.b[j][2] = v.x + v.y;
     }
   } else {
-    constexpr int CPR = C::BN / C::CHUNK;
-    constexpr int TOT = C::BK * CPR;
+    const double *A = reinterpret_cast<const double *>(sA);
+    const double *B = reinterpret_cast<const double *>(sB);
 #pragma unroll
-    for (int c = tid; c < TOT; c += C::NT) {
-      const int k = c / CPR, n = (c % CPR) * C::CHUNK;
-      const int64_t gn = n0 + n, gk = k0 + k;
-      int valid = 0;
-      if (gn < p.N && gk < p.K) valid = (int)min((int64_t)C::CHUNK, p.N - gn);
-      const char *src = valid ? Bb + (gk * p.b_sk + gn) * ESZ : Bb;
-      cp_async_zfill<C::CPB>(sB + (k * C::SB + n) * ESZ, src, valid * ESZ);
+    for (int i = 0; i < C::MI; i++) {
+      const int m = wm0 + i * 8 + lr;
+      f.a[i][0] = C::A_K ? A[m * C::SA + k] : A[k * C::SA + m];
+    }
+#pragma unroll
+    for (int j = 0; j < C::NJ; j++) {
+      const int n = wn0 + j * 8 + lr;
+      f.b[j][0] = C::B_K ? B[n * C::SB + k] : B[k * C::SB + n];
     }
   }
 }
 
 template <class C>
+struct Acc {
+  static constexpr int NS = C::kAlgo == kCplx3M ? 3 : (C::kCplx ? 2 : 1);
+  double c[NS][C::MI][C::NJ][2];
+};
+
+template <class C>
+__device__ __forceinline__ void mma_step(Acc<C> &acc, const Frag<C> &f) {
+#pragma unroll
+  for (int i = 0; i < C::MI; i++)
+#pragma unroll
+    for (int j = 0; j < C::NJ; j++) {
+      if constexpr (C::kAlgo == kCplx3M) {
+        dmma884(acc.c[0][i][j], f.a[i][0], f.b[j][0]);   // P = Ar.Br
+        dmma884(acc.c[1][i][j], f.a[i][1], f.b[j][1]);   // Q = Ai.Bi
+        dmma884(acc.c[2][i][j], f.a[i][2], f.b[j][2]);   // S = (Ar+Ai).(Br+Bi)
+      } else if constexpr (C::kAlgo == kCplx4M) {
+        dmma884(acc.c[0][i][j], f.a[i][0], f.b[j][0]);
+        dmma884(acc.c[1][i][j], f.a[i][0], f.b[j][1]);
+        dmma884(acc.c[0][i][j], -f.a[i][1], f.b[j][1]);
+        dmma884(acc.c[1][i][j], f.a[i][1], f.b[j][0]);
+      } else {
+        dmma884(acc.c[0][i][j], f.a[i][0], f.b[j][0]);
+      }
+    }
+}
+
+template <class C>
 __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p, int tiles_m,
                                                              int tiles_n) {
-  using T = typename Elem<C>::T;
   extern __shared__ __align__(128) char smem[];
   char *sA0 = smem;
   char *sB0 = smem + C::STAGES * C::A_STAGE * C::ESZ;
 
-  // grouped rasterization: 8 M-tiles share the B panels in L2
+  // grouped rasterization: GROUP M-tiles walk the N-tiles together so the
+  // B panels they share stay in L2
   constexpr int GROUP = 8;
   const int bid = blockIdx.x;
   const int per_group = GROUP * tiles_n;
@@ -143,80 +239,69 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
   const int wm0 = (warp / C::WARPS_N) * C::WM, wn0 = (warp % C::WARPS_N) * C::WN;
   const int lr = lane >> 2, lc = lane & 3;
 
-  double accr[C::MI][C::NJ][2];
-  double acci[C::kCplx ? C::MI : 1][C::kCplx ? C::NJ : 1][2];
+  Loader<C, true> la;
+  Loader<C, false> lb;
+  if (C::A_K) la.init(Ab, m0, p.M, p.a_sm, 1);
+  else la.init(Ab, m0, p.M, 1, p.a_sk);
+  if (C::B_K) lb.init(Bb, n0, p.N, p.b_sn, 1);
+  else lb.init(Bb, n0, p.N, 1, p.b_sk);
+
+  Acc<C> acc;
 #pragma unroll
-  for (int i = 0; i < C::MI; i++)
-#pragma unroll
-    for (int j = 0; j < C::NJ; j++) accr[i][j][0] = accr[i][j][1] = 0.0;
-  if constexpr (C::kCplx) {
+  for (int s = 0; s < Acc<C>::NS; s++)
 #pragma unroll
     for (int i = 0; i < C::MI; i++)
 #pragma unroll
-      for (int j = 0; j < C::NJ; j++) acci[i][j][0] = acci[i][j][1] = 0.0;
-  }
+      for (int j = 0; j < C::NJ; j++) acc.c[s][i][j][0] = acc.c[s][i][j][1] = 0.0;
 
   const int KT = (int)((p.K + C::BK - 1) / C::BK);
+  const int KT_full = (int)(p.K / C::BK);   // tiles with no K tail
 #pragma unroll
   for (int s = 0; s < C::STAGES - 1; s++) {
-    if (s < KT)
-      load_stage<C>(p, Ab, Bb, sA0 + s * C::A_STAGE * C::ESZ, sB0 + s * C::B_STAGE * C::ESZ, m0,
-                    n0, (int64_t)s * C::BK);
+    if (s < KT) {
+      la.load(sA0 + s * C::A_STAGE * C::ESZ, s, p.K, s < KT_full);
+      lb.load(sB0 + s * C::B_STAGE * C::ESZ, s, p.K, s < KT_full);
+    }
     cp_async_commit();
   }
+  cp_async_wait<C::STAGES - 2>();
+  __syncthreads();
+
+  Frag<C> fr[2];
+  load_frag<C>(fr[0], sA0, sB0, 0, wm0, wn0, lr, lc);
 
   for (int kt = 0; kt < KT; kt++) {
-    cp_async_wait<C::STAGES - 2>();
-    __syncthreads();
-    {
-      const int nk = kt + C::STAGES - 1;
-      if (nk < KT) {
-        const int st = nk % C::STAGES;
-        load_stage<C>(p, Ab, Bb, sA0 + st * C::A_STAGE * C::ESZ, sB0 + st * C::B_STAGE * C::ESZ,
-                      m0, n0, (int64_t)nk * C::BK);
-      }
-      cp_async_commit();
-    }
     const int st = kt % C::STAGES;
-    const T *sA = reinterpret_cast<const T *>(sA0 + st * C::A_STAGE * C::ESZ);
-    const T *sB = reinterpret_cast<const T *>(sB0 + st * C::B_STAGE * C::ESZ);
+    const char *sA = sA0 + st * C::A_STAGE * C::ESZ;
+    const char *sB = sB0 + st * C::B_STAGE * C::ESZ;
 #pragma unroll
-    for (int kk = 0; kk < C::BK / 4; kk++) {
-      const int k = kk * 4 + lc;
-      T af[C::MI], bf[C::NJ];
-#pragma unroll
-      for (int i = 0; i < C::MI; i++) {
-        const int m = wm0 + i * 8 + lr;
-        af[i] = C::A_K ? sA[m * C::SA + k] : sA[k * C::SA + m];
-      }
-#pragma unroll
-      for (int j = 0; j < C::NJ; j++) {
-        const int n = wn0 + j * 8 + lr;
-        bf[j] = C::B_K ? sB[n * C::SB + k] : sB[k * C::SB + n];
-      }
-      if constexpr (C::kCplx) {
-#pragma unroll
-        for (int i = 0; i < C::MI; i++) {
-          const double ar = af[i].x, ai = af[i].y, nai = -af[i].y;
-#pragma unroll
-          for (int j = 0; j < C::NJ; j++) {
-            dmma884(accr[i][j], ar, bf[j].x);
-            dmma884(acci[i][j], ar, bf[j].y);
-            dmma884(accr[i][j], nai, bf[j].y);
-            dmma884(acci[i][j], ai, bf[j].x);
-          }
-        }
+    for (int kk = 0; kk < C::KK; kk++) {
+      if (kk < C::KK - 1) {
+        load_frag<C>(fr[(kk + 1) & 1], sA, sB, kk + 1, wm0, wn0, lr, lc);
       } else {
-#pragma unroll
-        for (int i = 0; i < C::MI; i++)
-#pragma unroll
-          for (int j = 0; j < C::NJ; j++) dmma884(accr[i][j], af[i], bf[j]);
+        // stage kt+1 must have landed; stage kt-1 is free for reuse
+        cp_async_wait<C::STAGES - 3>();
+        __syncthreads();
+        const int nk = kt + C::STAGES - 1;
+        if (nk < KT) {
+          const int ns = nk % C::STAGES;
+          la.load(sA0 + ns * C::A_STAGE * C::ESZ, nk, p.K, nk < KT_full);
+          lb.load(sB0 + ns * C::B_STAGE * C::ESZ, nk, p.K, nk < KT_full);
+        }
+        cp_async_commit();
+        if (kt + 1 < KT) {
+          const int s1 = (kt + 1) % C::STAGES;
+          load_frag<C>(fr[(kk + 1) & 1], sA0 + s1 * C::A_STAGE * C::ESZ,
+                       sB0 + s1 * C::B_STAGE * C::ESZ, 0, wm0, wn0, lr, lc);
+        }
       }
+      mma_step<C>(acc, fr[kk & 1]);
     }
   }
   cp_async_wait<0>();
 
-  // ---- epilogue: C N-contiguous, direct 16-byte stores ----
+  // ---- epilogue: C N-contiguous, direct stores (each quad of lanes writes a
+  // contiguous 64 B (real) / 128 B (complex) run) ----
 #pragma unroll
   for (int i = 0; i < C::MI; i++) {
     const int64_t m = m0 + wm0 + i * 8 + lr;
@@ -226,12 +311,26 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
       const int64_t n = n0 + wn0 + j * 8 + 2 * lc;
       if constexpr (C::kCplx) {
         double2 *cp = reinterpret_cast<double2 *>(Cb) + m * p.c_sm + n;
-        if (n < p.N) cp[0] = make_double2(accr[i][j][0], acci[i][j][0]);
-        if (n + 1 < p.N) cp[1] = make_double2(accr[i][j][1], acci[i][j][1]);
+        double re0, im0, re1, im1;
+        if constexpr (C::kAlgo == kCplx3M) {
+          const double P0 = acc.c[0][i][j][0], Q0 = acc.c[1][i][j][0], S0 = acc.c[2][i][j][0];
+          const double P1 = acc.c[0][i][j][1], Q1 = acc.c[1][i][j][1], S1 = acc.c[2][i][j][1];
+          re0 = P0 - Q0;
+          im0 = S0 - P0 - Q0;
+          re1 = P1 - Q1;
+          im1 = S1 - P1 - Q1;
+        } else {
+          re0 = acc.c[0][i][j][0];
+          im0 = acc.c[1][i][j][0];
+          re1 = acc.c[0][i][j][1];
+          im1 = acc.c[1][i][j][1];
+        }
+        if (n < p.N) cp[0] = make_double2(re0, im0);
+        if (n + 1 < p.N) cp[1] = make_double2(re1, im1);
       } else {
         double *cp = reinterpret_cast<double *>(Cb) + m * p.c_sm + n;
-        if (n < p.N) cp[0] = accr[i][j][0];
-        if (n + 1 < p.N) cp[1] = accr[i][j][1];
+        if (n < p.N) cp[0] = acc.c[0][i][j][0];
+        if (n + 1 < p.N) cp[1] = acc.c[0][i][j][1];
       }
     }
   }
@@ -256,12 +355,32 @@ cudaError_t run(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   return cudaGetLastError();
 }
 
-// complex128: CTA 64x128, BK 8, 8 warps of 32x32, 4 stages (96 KB smem)
+// complex128 3M: CTA 64x64, BK 16, 8 warps of 32x16, 4 stages
 template <bool AK, bool BK>
-using ZCfg = Cfg<true, 64, 128, 8, 32, 32, 4, AK, BK, 1>;
+using Z3Cfg = Cfg<kCplx3M, 64, 64, 16, 32, 16, 4, AK, BK, 1>;
+// complex128 4M: same tiling
+template <bool AK, bool BK>
+using Z4Cfg = Cfg<kCplx4M, 64, 64, 16, 32, 16, 4, AK, BK, 1>;
 // float64: CTA 128x128, BK 16, 8 warps of 64x32, 3 stages
 template <bool AK, bool BK, int VEC>
-using DCfg = Cfg<false, 128, 128, 16, 64, 32, 3, AK, BK, VEC>;
+using DCfg = Cfg<kReal, 128, 128, 16, 64, 32, 3, AK, BK, VEC>;
+
+template <template <bool, bool> class Z>
+cudaError_t run_z(const GemmProblem &p, bool ak, bool bk, cudaStream_t s, int64_t *launches) {
+  if (ak && bk) return run<Z<true, true>>(p, s, launches);
+  if (ak && !bk) return run<Z<true, false>>(p, s, launches);
+  if (!ak && bk) return run<Z<false, true>>(p, s, launches);
+  return run<Z<false, false>>(p, s, launches);
+}
+
+bool use_4m() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("TCI_ZGEMM_ALGO");
+    v = (e && (strcmp(e, "4m") == 0 || strcmp(e, "4M") == 0)) ? 1 : 0;
+  }
+  return v == 1;
+}
 
 }  // namespace
 
@@ -270,15 +389,11 @@ cudaError_t launch_gemm_f32(const GemmProblem &p, cudaStream_t s, int64_t *launc
 cudaError_t launch_gemm(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   if (p.M == 0 || p.N == 0) return cudaSuccess;
   if (p.dtype == TCI_R32 || p.dtype == TCI_C64) return launch_gemm_f32(p, s, launches);
-  // The planner canonicalises strides (plan.cpp, canonical_gemm): a_sk == 1
-  // selects the K-contiguous loader, otherwise a_sm == 1; same for B.
+  // The planner canonicalises strides (contract.cpp): a_sk == 1 selects the
+  // K-contiguous loader, otherwise a_sm == 1; same for B.
   const bool ak = (p.a_sk == 1), bk = (p.b_sk == 1);
-  if (p.dtype == TCI_C128) {
-    if (ak && bk) return run<ZCfg<true, true>>(p, s, launches);
-    if (ak && !bk) return run<ZCfg<true, false>>(p, s, launches);
-    if (!ak && bk) return run<ZCfg<false, true>>(p, s, launches);
-    return run<ZCfg<false, false>>(p, s, launches);
-  }
+  if (p.dtype == TCI_C128)
+    return use_4m() ? run_z<Z4Cfg>(p, ak, bk, s, launches) : run_z<Z3Cfg>(p, ak, bk, s, launches);
   // float64: 16-byte chunks need 16-byte aligned rows
   const int64_t lda = ak ? p.a_sm : p.a_sk, ldb = bk ? p.b_sn : p.b_sk;
   const bool aligned = ((uintptr_t)p.A % 16 == 0) && ((uintptr_t)p.B % 16 == 0) &&

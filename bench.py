@@ -232,12 +232,11 @@ def run_tci(args):
 
     # inputs, generated on the device (same generator as the oracle side)
     inp = synth.heff_inputs(chi, d, D, dt, cfg["seed"], cfg["model"], device=dev)
+    from paper_2512_23917_b200.sharding import ShardedHeff, slice_environment
     L_full = inp.pop("L")
-    L = L_full[:, :, rank * chi_lo:(rank + 1) * chi_lo].contiguous()
+    L = slice_environment(L_full, ws, rank)          # this rank's L[:, :, b_r] (setup)
     del L_full
     W1, W2, R, psi = inp["W1"], inp["W2"], inp["R"], inp["psi"]
-    out = torch.empty((chi_lo, d, d, chi), dtype=psi.dtype, device=dev)
-    full = torch.empty((chi, d, d, chi), dtype=psi.dtype, device=dev) if ws > 1 else out
     torch.cuda.synchronize()
 
     ctx = tci.Context(local, stream)
@@ -246,11 +245,11 @@ def run_tci(args):
         obj = [tci.tci_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         ctx.comm_init(obj[0], ws, rank)
+    sh = ShardedHeff(ctx, L, W1, W2, R, ws, rank)
+    out = sh.out
 
     def step():
-        ctx.heff_apply(L, W1, W2, R, psi, out=out)
-        if ws > 1:
-            ctx.allgather(out, full)
+        sh.apply(psi)       # tci_heff_apply on the slab (+ tci_allgather when ws > 1)
 
     def barrier():
         if ws > 1:

@@ -1,0 +1,212 @@
+#!/usr/bin/env python
+"""Secondary measurements for the BASELINE.json configs that are not the
+bench.py headline: config 1 (MPS norm chain latency),
+config 2 (chi=1024 H_eff), config 3 (TEBD theta, two layouts), config 4
+(Hubbard chi=4096 d=4 D=6 H_eff), config 5 (general contraction sweep with a
+per-instance roofline) and a permute-bandwidth sweep. Writes one JSON object.
+
+    python tools/bench_extra.py [--only cfg1,cfg3,...] [--out gpurun_out/extra.json]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2512_23917_b200 as tci  # noqa: E402
+import synth  # noqa: E402
+
+FP64_PEAK = 37.06e12
+HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9 \
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6.65e12
+
+
+def timed(fn, reps=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    return float(np.median(ts)), float(np.min(ts))
+
+
+def cfg1(ctx):
+    import oracle
+    psi = [torch.from_numpy(a).cuda() for a in synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1)]
+    E0 = torch.ones(1, 1, dtype=torch.float64, device="cuda")
+    outs = {}
+
+    def chain():
+        E = E0
+        for A in psi:
+            X = ctx.contract(E, "xz", A, "xsy", "zsy")
+            E = ctx.contract(X, "zsy", A, "zsw", "yw")
+        outs["E"] = E
+    med, mn = timed(chain, reps=50, warm=5)
+    # host wall time per contract (plan-cache hits, includes launch latency)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(50):
+        chain()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / 50
+    ref = oracle.mps_norm2(synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1))
+    got = outs["E"].cpu().numpy()
+    t1 = time.perf_counter()
+    for _ in range(20):
+        oracle.mps_norm2(synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1), threads=1)
+    t_or = (time.perf_counter() - t1) / 20
+    return {"workload": "10-site MPS norm, chi=16, d=2, f64 (20 contracts, 46808 MACs)",
+            "gpu_us_per_chain_device": med * 1e6, "gpu_us_per_contract_device": med * 1e6 / 20,
+            "gpu_us_per_chain_wall": wall * 1e6, "gpu_us_per_contract_wall": wall * 1e6 / 20,
+            "oracle_us_per_chain_1thread": t_or * 1e6,
+            "rel_err_vs_oracle": float(abs(got - ref).max() / abs(ref).max())}
+
+
+def heff_cfg(ctx, name, reps=3):
+    cfg = synth.HEFF_CONFIGS[name]
+    inp = synth.heff_inputs(cfg["chi"], cfg["d"], cfg["D"], cfg["dtype"], cfg["seed"], cfg["model"], device="cuda")
+    out = torch.empty(inp["psi"].shape[0], cfg["d"], cfg["d"], cfg["chi"], dtype=inp["psi"].dtype, device="cuda")
+    f = lambda: ctx.heff_apply(inp["L"], inp["W1"], inp["W2"], inp["R"], inp["psi"], out=out)  # noqa: E731
+    med, mn = timed(f, reps=reps, warm=1)
+    F = synth.heff_flops(cfg["chi"], cfg["d"], cfg["D"])
+    tci.tci_profile_enable(ctx.handle, True)
+    f()
+    g = tci.tci_profile_query(ctx.handle, tci.PROF_GEMM)
+    sk = tci.tci_profile_query(ctx.handle, tci.PROF_SKINNY)
+    tci.tci_profile_enable(ctx.handle, False)
+    res = {"workload": name, "tflops": F / med / 1e12, "tflops_best": F / mn / 1e12, "s_per_apply": med,
+           "pct_fp64_peak": F / med / FP64_PEAK * 100,
+           "gemm_tflops": g["flops"] / (g["ms"] / 1e3) / 1e12,
+           "skinny_gbs": sk["bytes"] / (sk["ms"] / 1e3) / 1e9 if sk["launches"] else None,
+           "skinny_share": sk["ms"] / 1e3 / med}
+    del inp, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def cfg3(ctx):
+    c = synth.TEBD_CONFIG
+    res = {}
+    for layout, la, lb, lt in (("natural", "asb", "btc", "apqc"), ("physical_first", "sab", "tbc", "paqc")):
+        inp = synth.tebd_inputs(c["chi"], c["d"], c["dtype"], c["seed"], c["tau"], device="cuda",
+                                physical_first=layout == "physical_first")
+        out = None
+        holder = {}
+
+        def f():
+            holder["t"] = ctx.tebd_theta(inp["A"], la, inp["B"], lb, inp["U"], "pqst", lt, out=holder.get("t"))
+        med, mn = timed(f, reps=10, warm=2)
+        chi, d = c["chi"], c["d"]
+        F = 2.0 * (chi * d) * chi * (d * chi) + 2.0 * d ** 4 * chi * chi
+        byts = 8.0 * (2 * chi * d * chi + d * d * chi * chi)
+        tci.tci_profile_enable(ctx.handle, True)
+        f()
+        g = tci.tci_profile_query(ctx.handle, tci.PROF_GEMM)
+        sk = tci.tci_profile_query(ctx.handle, tci.PROF_SKINNY)
+        pm = tci.tci_profile_query(ctx.handle, tci.PROF_PERMUTE)
+        tci.tci_profile_enable(ctx.handle, False)
+        res[layout] = {"tflops": F / med / 1e12, "us": med * 1e6, "pct_fp64_peak": F / med / FP64_PEAK * 100,
+                       "gemm_tflops": g["flops"] / (g["ms"] / 1e3) / 1e12, "gemm_ms": g["ms"],
+                       "gate_pass_ms": sk["ms"], "permute_ms": pm["ms"], "permute_launches": pm["launches"],
+                       "min_traffic_bytes": byts}
+        del inp
+        torch.cuda.empty_cache()
+    res["workload"] = "TEBD theta chi=2048 d=2 f64 (68.7 GFLOP + gate)"
+    return res
+
+
+def sweep(ctx, seeds=24):
+    """Config 5: random rank 3..6 contractions up to 2^28 elements, f64 and f32."""
+    import string
+    rng = np.random.default_rng(5)
+    pool = [1, 2, 3, 5, 7, 8, 16, 37, 64, 128, 256]
+    rows = []
+    for s in range(seeds):
+        for dt in ("r64", "r32"):
+            ra, rb = int(rng.integers(3, 7)), int(rng.integers(3, 7))
+            nc = int(rng.integers(1, min(ra, rb)))
+            letters = list(string.ascii_letters)
+            rng.shuffle(letters)
+            sh, fa, fb = letters[:nc], letters[nc:ra], letters[ra:ra + rb - nc]
+            la, lb, lc = sh + fa, sh + fb, fa + fb
+            rng.shuffle(la); rng.shuffle(lb); rng.shuffle(lc)
+            dims = {l: int(rng.choice(pool)) for l in la + lb}
+
+            def size(ls):
+                return int(np.prod([dims[l] for l in ls], dtype=np.int64))
+            while max(size(la), size(lb), size(lc)) > 2 ** 28:
+                big = max(dims, key=dims.get)
+                dims[big] = max(1, dims[big] // 2)
+            A = synth.random_tensor([dims[l] for l in la], dt, 5000 + s, 1, device="cuda")
+            B = synth.random_tensor([dims[l] for l in lb], dt, 5000 + s, 2, device="cuda")
+            la_, lb_, lc_ = "".join(la), "".join(lb), "".join(lc)
+            holder = {}
+            f = lambda: holder.__setitem__("c", ctx.contract(A, la_, B, lb_, lc_, out=holder.get("c")))  # noqa
+            med, _ = timed(f, reps=3, warm=1)
+            es = 8 if dt == "r64" else 4
+            S = size(sh)
+            flops = 2.0 * size(lc) * S
+            t_roof = max(flops / FP64_PEAK, (size(la) + size(lb) + size(lc)) * es / HBM)
+            rows.append({"dtype": dt, "la": la_, "lb": lb_, "lc": lc_, "dims": dims, "elems_max": max(size(la), size(lb), size(lc)),
+                         "us": med * 1e6, "roofline_us": t_roof * 1e6, "frac_of_roofline": t_roof / med})
+            del A, B, holder
+    fr = [r["frac_of_roofline"] for r in rows]
+    return {"instances": rows, "median_frac_of_roofline": float(np.median(fr)),
+            "geomean_frac_of_roofline": float(np.exp(np.mean(np.log(fr))))}
+
+
+def permute_bw(ctx):
+    rows = []
+    for shape, perm, dt in [((4096, 4096, 16), (1, 0, 2), "r64"), ((512, 512, 512), (2, 1, 0), "r64"),
+                            ((64, 64, 64, 64, 16), (4, 3, 2, 1, 0), "r64"), ((8192, 8192, 2), (2, 1, 0), "c128"),
+                            ((16384, 16384), (1, 0), "r32"), ((2048, 2048, 32), (0, 2, 1), "r64")]:
+        x = synth.random_tensor(shape, dt, 9, 1, device="cuda")
+        y = torch.empty([shape[p] for p in perm], dtype=x.dtype, device="cuda")
+        med, _ = timed(lambda: ctx.permute(x, list(perm), out=y), reps=10, warm=2)
+        byts = 2.0 * x.numel() * x.element_size()
+        rows.append({"shape": shape, "perm": perm, "dtype": dt, "GBs": byts / med / 1e9, "frac_hbm": byts / med / HBM})
+        del x, y
+    return rows
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg4,sweep,permute")
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "extra.json"))
+    a = ap.parse_args()
+    ctx = tci.Context(0)
+    res = {}
+    for k in a.only.split(","):
+        if k == "cfg1":
+            res["cfg1"] = cfg1(ctx)
+        elif k == "cfg2":
+            res["cfg2"] = heff_cfg(ctx, "cfg2_heisenberg_chi1024", reps=5)
+        elif k == "cfg3":
+            res["cfg3"] = cfg3(ctx)
+        elif k == "cfg4":
+            res["cfg4"] = heff_cfg(ctx, "cfg4_hubbard_chi4096", reps=2)
+        elif k == "sweep":
+            res["sweep"] = sweep(ctx)
+        elif k == "permute":
+            res["permute"] = permute_bw(ctx)
+        print(k, json.dumps(res.get(k))[:600], flush=True)
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    json.dump(res, open(a.out, "w"), indent=1)
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -66,6 +66,15 @@ tci_status_t run_skinny(tci_ctx_s *ctx, const SkinnyProblem &p) {
   return TCI_OK;
 }
 
+tci_status_t run_tebd(tci_ctx_s *ctx, const TebdProblem &t) {
+  const double M = 2.0 * t.chi_a, N = 2.0 * t.chi_c, K = (double)t.chi_b;
+  ProfScope ps(ctx, kProfGemm, 2.0 * M * N * K + 2.0 * 16.0 * t.chi_a * t.chi_c,
+               8.0 * (M * K + K * N + M * N));
+  TCI_CUDA_CHECK(launch_tebd_fused(t, ctx->stream, &ctx->launches));
+  ps.done();
+  return TCI_OK;
+}
+
 tci_status_t run_permute(tci_ctx_s *ctx, const PermuteProblem &p) {
   ProfScope ps(ctx, kProfPermute, 0.0, 2.0 * (double)p.total * (double)p.esize);
   TCI_CUDA_CHECK(launch_permute(p, ctx->stream, &ctx->launches));

@@ -434,6 +434,35 @@ tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View
   if (st) return st;
   for (int k = 0; k < 4; k++)
     if (sth[k] != T.shape[k]) TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "tebd: theta shape mismatch");
+  // ---- fused path: the gate applied in the GEMM epilogue (d = 2, f64) ----
+  {
+    auto stride_of = [](const int32_t *l, const int64_t *shape, int n, char x) -> int64_t {
+      int64_t st = 1;
+      for (int k = n - 1; k >= 0; k--) {
+        if (l[k] == (unsigned char)x) return st;
+        st *= shape[k];
+      }
+      return -1;
+    };
+    TebdProblem tp{};
+    tp.d = U.shape[0];
+    tp.chi_a = A.shape[strchr(la, a) - la];
+    tp.chi_b = A.shape[strchr(la, bond) - la];
+    tp.chi_c = B.shape[strchr(lb, c) - lb];
+    tp.A = static_cast<const double *>(A.data);
+    tp.a_a = stride_of(ila, A.shape, 3, a); tp.a_s = stride_of(ila, A.shape, 3, s); tp.a_b = stride_of(ila, A.shape, 3, bond);
+    tp.B = static_cast<const double *>(B.data);
+    tp.b_b = stride_of(ilb, B.shape, 3, bond); tp.b_t = stride_of(ilb, B.shape, 3, t); tp.b_c = stride_of(ilb, B.shape, 3, c);
+    tp.U = static_cast<const double *>(U.data);
+    tp.u_p = stride_of(ilu, U.shape, 4, pq[0]); tp.u_q = stride_of(ilu, U.shape, 4, pq[1]);
+    tp.u_s = stride_of(ilu, U.shape, 4, s); tp.u_t = stride_of(ilu, U.shape, 4, t);
+    tp.T = static_cast<double *>(T.data);
+    tp.t_a = stride_of(ilt, T.shape, 4, a); tp.t_p = stride_of(ilt, T.shape, 4, pq[0]);
+    tp.t_q = stride_of(ilt, T.shape, 4, pq[1]); tp.t_c = stride_of(ilt, T.shape, 4, c);
+    const bool dims_ok = U.shape[0] == 2 && U.shape[1] == 2 && U.shape[2] == 2 && U.shape[3] == 2 &&
+                         A.shape[strchr(la, s) - la] == 2 && B.shape[strchr(lb, t) - lb] == 2;
+    if (dt == TCI_R64 && dims_ok && tebd_fused_supported(tp)) return run_tebd(ctx, tp);
+  }
   View AB;
   AB.dtype = dt;
   AB.order = 4;

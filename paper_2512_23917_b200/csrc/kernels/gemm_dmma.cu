@@ -19,7 +19,7 @@
 // Ci += Ar.Bi + Ai.Br) is kept and selectable (TCI_ZGEMM_ALGO=4m).
 //
 // Kernel structure (one CTA per 64x64 complex / 128x128 real output tile):
-//  * 4-stage cp.async pipeline, 16-byte chunks, zero-fill on ragged edges;
+//  * 6-stage (complex) / 3-stage (real) cp.async pipeline, 16-byte chunks, zero-fill on ragged edges;
 //    each thread's chunk pointers and row predicates are computed once and
 //    advanced by a constant per K tile (no per-tile 64-bit index math);
 //  * padded shared-memory pitches make every fragment load conflict free
@@ -37,15 +37,21 @@
 #include "../tci_internal.h"
 #include "common.cuh"
 
+// tools/gemm_lab.cu may redefine this to measure the cost of the 3M sums
+#ifndef TCI_LAB_SUM
+#define TCI_LAB_SUM(x, y) ((x) + (y))
+#endif
+
 namespace tci {
 namespace {
 
 enum Algo { kReal = 0, kCplx3M = 1, kCplx4M = 2 };
 
 template <int ALGO, int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool A_K_, bool B_K_,
-          int VEC_>
+          int VEC_, int MODE_ = 0>
 struct Cfg {
   static constexpr int kAlgo = ALGO;
+  static constexpr int MODE = MODE_;   // 0 plain GEMM, 1 TEBD theta (gate in the epilogue)
   static constexpr bool kCplx = ALGO != kReal;
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
   static constexpr bool A_K = A_K_, B_K = B_K_;
@@ -60,7 +66,9 @@ struct Cfg {
   static constexpr int SB = B_K ? (BK + PADK) : (BN + PADMN);
   static constexpr int A_STAGE = A_K ? BM * SA : BK * SA;   // elements
   static constexpr int B_STAGE = B_K ? BN * SB : BK * SB;
-  static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) * ESZ;
+  static constexpr int SMEM_PIPE = STAGES * (A_STAGE + B_STAGE) * ESZ;
+  static constexpr int SMEM_EPI = MODE == 1 ? BM * (BN + 1) * 8 : 0;   // staged C tile (TEBD)
+  static constexpr int SMEM = SMEM_PIPE > SMEM_EPI ? SMEM_PIPE : SMEM_EPI;
   static constexpr int MI = WM / 8, NJ = WN / 8;
   static constexpr int KK = BK / 4;
   // loader geometry: chunks per tile row along the contiguous leg
@@ -116,6 +124,42 @@ struct Loader {
     kstep = (int64_t)C::BK * (KMAJ ? 1 : s_k) * C::ESZ;
   }
 
+  // TEBD A (K-major): tile row r holds (a, s) = (a0 + r / 2, r % 2)
+  __device__ __forceinline__ void init_tebd_a(const char *b, int64_t a0, int64_t chi_a, int64_t s_a,
+                                              int64_t s_s) {
+    base = b;
+    const int t = threadIdx.x;
+    const int col = (t % CPR) * C::CHUNK;
+#pragma unroll
+    for (int i = 0; i < PER_T; i++) {
+      const int row = t / CPR + i * RSTEP;
+      const int64_t a = a0 + row / 2;
+      nvalid_mn[i] = a < chi_a ? 1 : 0;
+      kidx[i] = col;
+      ptr[i] = b + ((a < chi_a ? a : 0) * s_a + (row % 2) * s_s + col) * C::ESZ;
+      soff[i] = (uint32_t)((row * S + col) * C::ESZ);
+    }
+    kstep = (int64_t)C::BK * C::ESZ;
+  }
+  // TEBD B (N-major): tile column l holds (t, c) = (l / (BN/2), c0 + l % (BN/2))
+  __device__ __forceinline__ void init_tebd_b(const char *b, int64_t c0, int64_t chi_c, int64_t s_k,
+                                              int64_t s_t) {
+    base = b;
+    const int t = threadIdx.x;
+    const int col = (t % CPR) * C::CHUNK;
+    constexpr int HALF = C::BN / 2;
+    const int64_t c = c0 + col % HALF;
+#pragma unroll
+    for (int i = 0; i < PER_T; i++) {
+      const int row = t / CPR + i * RSTEP;
+      nvalid_mn[i] = (int)(c < chi_c ? (chi_c - c < C::CHUNK ? chi_c - c : C::CHUNK) : 0);
+      kidx[i] = row;
+      ptr[i] = b + ((int64_t)row * s_k + (col / HALF) * s_t + (c < chi_c ? c : 0)) * C::ESZ;
+      soff[i] = (uint32_t)((row * S + col) * C::ESZ);
+    }
+    kstep = (int64_t)C::BK * s_k * C::ESZ;
+  }
+
   // issue this thread's cp.asyncs for K tile kt into the stage at `sbase`
   __device__ __forceinline__ void load(char *sbase, int kt, int64_t K, bool full_k) const {
     const int64_t k0 = (int64_t)kt * C::BK;
@@ -159,7 +203,7 @@ __device__ __forceinline__ void load_frag(Frag<C> &f, const char *sA, const char
       const double2 v = C::A_K ? A[m * C::SA + k] : A[k * C::SA + m];
       f.a[i][0] = v.x;
       f.a[i][1] = v.y;
-      if constexpr (C::kAlgo == kCplx3M) f.a[i][2] = v.x + v.y;
+      if constexpr (C::kAlgo == kCplx3M) f.a[i][2] = TCI_LAB_SUM(v.x, v.y);
     }
 #pragma unroll
     for (int j = 0; j < C::NJ; j++) {
@@ -167,7 +211,7 @@ __device__ __forceinline__ void load_frag(Frag<C> &f, const char *sA, const char
       const double2 v = C::B_K ? B[n * C::SB + k] : B[k * C::SB + n];
       f.b[j][0] = v.x;
       f.b[j][1] = v.y;
-      if constexpr (C::kAlgo == kCplx3M) f.b[j][2] = v.x + v.y;
+      if constexpr (C::kAlgo == kCplx3M) f.b[j][2] = TCI_LAB_SUM(v.x, v.y);
     }
   } else {
     const double *A = reinterpret_cast<const double *>(sA);
@@ -241,10 +285,15 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
 
   Loader<C, true> la;
   Loader<C, false> lb;
-  if (C::A_K) la.init(Ab, m0, p.M, p.a_sm, 1);
-  else la.init(Ab, m0, p.M, 1, p.a_sk);
-  if (C::B_K) lb.init(Bb, n0, p.N, p.b_sn, 1);
-  else lb.init(Bb, n0, p.N, 1, p.b_sk);
+  if constexpr (C::MODE == 1) {
+    la.init_tebd_a(Ab, (int64_t)tile_m * (C::BM / 2), p.te_chi_a, p.te_a_a, p.te_a_s);
+    lb.init_tebd_b(Bb, (int64_t)tile_n * (C::BN / 2), p.te_chi_c, p.b_sk, p.te_b_t);
+  } else {
+    if (C::A_K) la.init(Ab, m0, p.M, p.a_sm, 1);
+    else la.init(Ab, m0, p.M, 1, p.a_sk);
+    if (C::B_K) lb.init(Bb, n0, p.N, p.b_sn, 1);
+    else lb.init(Bb, n0, p.N, 1, p.b_sk);
+  }
 
   Acc<C> acc;
 #pragma unroll
@@ -299,6 +348,59 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
     }
   }
   cp_async_wait<0>();
+
+  if constexpr (C::MODE == 1) {
+    // ---- TEBD epilogue: theta[a,p,q,c] = sum_{s,t} U[p,q,s,t] C[(a,s),(t,c)].
+    // The CTA holds all (s,t) of its 64 a's x 64 c's; stage C in shared
+    // memory, then each thread applies the 4x4 gate to one (a,c) pair and
+    // writes its 4 outputs (consecutive threads -> consecutive c).
+    __syncthreads();   // pipeline buffers are dead: reuse them for the C tile
+    double *Cs = reinterpret_cast<double *>(smem);
+    constexpr int PC = C::BN + 1;
+#pragma unroll
+    for (int i = 0; i < C::MI; i++)
+#pragma unroll
+      for (int j = 0; j < C::NJ; j++) {
+        const int m = wm0 + i * 8 + lr, n = wn0 + j * 8 + 2 * lc;
+        Cs[m * PC + n] = acc.c[0][i][j][0];
+        Cs[m * PC + n + 1] = acc.c[0][i][j][1];
+      }
+    double u[2][2][2][2];
+#pragma unroll
+    for (int pp = 0; pp < 2; pp++)
+#pragma unroll
+      for (int q = 0; q < 2; q++)
+#pragma unroll
+        for (int s_ = 0; s_ < 2; s_++)
+#pragma unroll
+          for (int t_ = 0; t_ < 2; t_++)
+            u[pp][q][s_][t_] = p.te_U[pp * p.te_u[0] + q * p.te_u[1] + s_ * p.te_u[2] + t_ * p.te_u[3]];
+    __syncthreads();
+    constexpr int HA = C::BM / 2, HC = C::BN / 2;
+    for (int idx = threadIdx.x; idx < HA * HC; idx += C::NT) {
+      const int al = idx / HC, cl = idx % HC;
+      const int64_t a = (int64_t)tile_m * HA + al, c = (int64_t)tile_n * HC + cl;
+      if (a >= p.te_chi_a || c >= p.te_chi_c) continue;
+      double x[2][2];
+#pragma unroll
+      for (int s_ = 0; s_ < 2; s_++)
+#pragma unroll
+        for (int t_ = 0; t_ < 2; t_++) x[s_][t_] = Cs[(2 * al + s_) * PC + t_ * HC + cl];
+      double *T = p.te_T + a * p.te_t[0] + c * p.te_t[3];
+#pragma unroll
+      for (int pp = 0; pp < 2; pp++)
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          double th = 0.0;
+#pragma unroll
+          for (int s_ = 0; s_ < 2; s_++)
+#pragma unroll
+            for (int t_ = 0; t_ < 2; t_++) th = fma(u[pp][q][s_][t_], x[s_][t_], th);
+          T[pp * p.te_t[1] + q * p.te_t[2]] = th;
+        }
+    }
+    return;
+  }
 
   // ---- epilogue: C N-contiguous, direct stores (each quad of lanes writes a
   // contiguous 64 B (real) / 128 B (complex) run) ----
@@ -355,9 +457,11 @@ cudaError_t run(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   return cudaGetLastError();
 }
 
-// complex128 3M: CTA 64x64, BK 16, 8 warps of 32x16, 4 stages
+// complex128 3M: CTA 64x64, BK 8, 8 warps of 32x16, 6 stages (A/B sweep in
+// tools/gemm_lab.cu: BK 8 / 6 stages 44.0 TF/s vs BK 16 / 4 stages 41.6 on
+// the chi=4096 GEMM4 shape)
 template <bool AK, bool BK>
-using Z3Cfg = Cfg<kCplx3M, 64, 64, 16, 32, 16, 4, AK, BK, 1>;
+using Z3Cfg = Cfg<kCplx3M, 64, 64, 8, 32, 16, 6, AK, BK, 1>;
 // complex128 4M: same tiling
 template <bool AK, bool BK>
 using Z4Cfg = Cfg<kCplx4M, 64, 64, 16, 32, 16, 4, AK, BK, 1>;
@@ -385,6 +489,31 @@ bool use_4m() {
 }  // namespace
 
 cudaError_t launch_gemm_f32(const GemmProblem &p, cudaStream_t s, int64_t *launches);
+
+bool tebd_fused_supported(const TebdProblem &t) {
+  auto al16 = [](const void *x) { return ((uintptr_t)x % 16) == 0; };
+  return t.d == 2 && t.a_b == 1 && t.b_c == 1 && al16(t.A) && al16(t.B) && t.a_a % 2 == 0 &&
+         t.a_s % 2 == 0 && t.b_b % 2 == 0 && t.b_t % 2 == 0 && t.chi_b >= 1;
+}
+
+cudaError_t launch_tebd_fused(const TebdProblem &t, cudaStream_t s, int64_t *launches) {
+  using TC = Cfg<kReal, 128, 128, 16, 64, 32, 3, true, false, 2, 1>;
+  GemmProblem p{};
+  p.dtype = TCI_R64;
+  p.M = 2 * t.chi_a;
+  p.N = 2 * t.chi_c;
+  p.K = t.chi_b;
+  p.A = t.A; p.a_sm = 0; p.a_sk = 1;
+  p.B = t.B; p.b_sk = t.b_b; p.b_sn = 1;
+  p.mode = 1;
+  p.te_chi_a = t.chi_a; p.te_chi_c = t.chi_c;
+  p.te_a_a = t.a_a; p.te_a_s = t.a_s; p.te_b_t = t.b_t;
+  p.te_U = t.U;
+  p.te_u[0] = t.u_p; p.te_u[1] = t.u_q; p.te_u[2] = t.u_s; p.te_u[3] = t.u_t;
+  p.te_T = t.T;
+  p.te_t[0] = t.t_a; p.te_t[1] = t.t_p; p.te_t[2] = t.t_q; p.te_t[3] = t.t_c;
+  return run<TC>(p, s, launches);   // tiles: (chi_a / 64) x (chi_c / 64)
+}
 
 cudaError_t launch_gemm(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   if (p.M == 0 || p.N == 0) return cudaSuccess;

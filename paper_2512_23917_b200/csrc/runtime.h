@@ -112,6 +112,7 @@ enum { kProfGemm = 0, kProfSkinny = 1, kProfPermute = 2 };
 tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g);
 tci_status_t run_skinny(tci_ctx_s *ctx, const SkinnyProblem &p);
 tci_status_t run_permute(tci_ctx_s *ctx, const PermuteProblem &p);
+tci_status_t run_tebd(tci_ctx_s *ctx, const TebdProblem &t);
 
 // Chains (chains.cpp)
 tci_status_t heff_plan_bytes(tci_dtype_t dt, int64_t chi_l, int64_t chi_lo, int64_t chi_r,

@@ -39,6 +39,15 @@ struct GemmProblem {
   // Batched over one extra "batch" leg (strides in elements); batch == 1 for
   // a plain GEMM.
   int64_t batch = 1, a_sb = 0, b_sb = 0, c_sb = 0;
+  // mode 1 = TEBD theta with the gate in the epilogue (launch_tebd_fused)
+  int mode = 0;
+  int64_t te_chi_a = 0, te_chi_c = 0;     // extents of a and c
+  int64_t te_a_a = 0, te_a_s = 0;         // A strides of a and s (b stride == 1)
+  int64_t te_b_t = 0;                     // B stride of t (c stride == 1, b stride = b_sk)
+  const double *te_U = nullptr;           // gate U[p,q,s,t], device
+  int64_t te_u[4] = {0, 0, 0, 0};         // strides of p, q, s, t in U
+  double *te_T = nullptr;                 // theta
+  int64_t te_t[4] = {0, 0, 0, 0};         // strides of a, p, q, c in theta
 };
 
 // Launches the DMMA (f64/c128) or FFMA (f32/c64) GEMM. Returns cudaSuccess or
@@ -52,7 +61,7 @@ struct TebdProblem {
   int64_t chi_a, chi_b, chi_c, d;
   const double *A; int64_t a_a, a_s, a_b;   // strides (elements)
   const double *B; int64_t b_b, b_t, b_c;
-  const double *U;                          // U[p,q,s,t] dense, 16 entries (d=2), device
+  const double *U; int64_t u_p, u_q, u_s, u_t;   // gate (device) and its strides
   double *T; int64_t t_a, t_p, t_q, t_c;
 };
 cudaError_t launch_tebd_fused(const TebdProblem &p, cudaStream_t s, int64_t *launches);

@@ -425,3 +425,36 @@ def test_mps_mpo_apply(ctx, oracle_mod):
     B = ctx.contract(dev(A), "asb", dev(W), "wvst", "awtbv")
     ref = oracle_mod.mps_mpo_apply(A.numpy(), W.numpy())
     assert rel_frob(host(B).reshape(ref.shape), ref) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU plumbing (8(e)) on one GPU: NCCL communicator of one rank
+# ---------------------------------------------------------------------------
+
+def test_nccl_allgather_single_rank(ctx):
+    uid = tci.tci_comm_unique_id()
+    assert len(uid) == 128
+    c = tci.Context(0)
+    c.comm_init(uid, 1, 0)
+    x = dev(synth.random_tensor((64, 2, 2, 96), "c128", 430, 1))
+    full = torch.empty_like(x)
+    c.allgather(x, full)
+    torch.cuda.synchronize()
+    assert torch.equal(full, x)
+    with pytest.raises(tci.TciError) as e:
+        c.allgather(x, torch.empty(2 * x.numel(), dtype=x.dtype, device="cuda"))
+    assert e.value.code == 1
+    c.close()
+    with pytest.raises(tci.TciError) as e:
+        ctx.allgather(x, full)          # no communicator on this context
+    assert e.value.code == 11
+
+
+def test_sharded_heff_single_rank_path(ctx):
+    """bench.py's ShardedHeff on one rank (world 1): identical to a direct apply."""
+    from paper_2512_23917_b200.sharding import ShardedHeff, slice_environment
+    inp = synth.heff_inputs(64, 2, 5, "c128", 431, "heisenberg", device="cuda")
+    sh = ShardedHeff(ctx, slice_environment(inp["L"], 1, 0), inp["W1"], inp["W2"], inp["R"], 1, 0)
+    out = sh.apply(inp["psi"])
+    ref = ctx.heff_apply(inp["L"], inp["W1"], inp["W2"], inp["R"], inp["psi"])
+    assert torch.equal(out, ref)

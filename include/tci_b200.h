@@ -253,6 +253,19 @@ TCI_API tci_status_t tci_tebd_theta(tci_ctx_t ctx, tci_tensor_t A, const char *l
                             tci_tensor_t U, const char *lu,
                             tci_tensor_t theta, const char *lt);
 
+/* MPS overlap / norm transfer chain (R17; the section III overlap
+ * by contraction): with E_0 = [[1]],
+ *   E_{i+1}[y,w] = sum_{x,z,s} E_i[x,z] bra_i[x,s,y] ket_i[z,s,w],
+ * out = E_n of shape (bra[n-1].shape[2], ket[n-1].shape[2]). Bilinear (no
+ * conjugation, R9). bra[i], ket[i]: order-3 site tensors [left, phys, right]
+ * (device, r64 or c128), bra[0]/ket[0] left bond 1, physical dims equal per
+ * site. Executed as ONE single-CTA kernel with E and X in shared memory (the
+ * chain is launch-latency bound, config 1); bonds <= 32, d <= 4, n <= 64,
+ * else UNSUPPORTED (use tci_contract for larger chains).
+ * Errors: ORDER_MISMATCH, SHAPE_MISMATCH, UNSUPPORTED, OUT_OF_RANGE, CUDA. */
+TCI_API tci_status_t tci_mps_overlap(tci_ctx_t ctx, int n, const tci_tensor_t *bra,
+                                     const tci_tensor_t *ket, tci_tensor_t out);
+
 /* ---------------------------------------------------------------------- */
 /* Multi-GPU (8(e)): one communicator per context                          */
 /* ---------------------------------------------------------------------- */

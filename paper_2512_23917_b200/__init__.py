@@ -43,6 +43,7 @@ EXPORTED = [
     "tci_contract_workspace_size", "tci_heff_workspace_size", "tci_heff_apply",
     "tci_tebd_theta", "tci_comm_init", "tci_comm_unique_id", "tci_allgather",
     "tci_launch_count", "tci_heff_plan_tree", "tci_profile_enable", "tci_profile_query",
+    "tci_mps_overlap",
 ]
 
 
@@ -84,6 +85,7 @@ _sig = {
     "tci_allgather": ([_vp, _vp, _vp], ctypes.c_int),
     "tci_launch_count": ([_vp, _i64p], ctypes.c_int),
     "tci_profile_enable": ([_vp, ctypes.c_int], ctypes.c_int),
+    "tci_mps_overlap": ([_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp], ctypes.c_int),
     "tci_profile_query": ([_vp, ctypes.c_int, _i64p] + [ctypes.POINTER(ctypes.c_double)] * 3, ctypes.c_int),
     "tci_heff_plan_tree": ([ctypes.c_int64] * 8 + [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
 }
@@ -255,6 +257,13 @@ def tci_launch_count(ctx: int) -> int:
     return n.value
 
 
+def tci_mps_overlap(ctx: int, bra: Sequence[int], ket: Sequence[int], out: int) -> None:
+    n = len(bra)
+    b = (_vp * max(1, n))(*[_vp(x) for x in bra])
+    k = (_vp * max(1, n))(*[_vp(x) for x in ket])
+    _ok(_lib.tci_mps_overlap(_vp(ctx), n, b, k, _vp(out)), "tci_mps_overlap")
+
+
 PROF_GEMM, PROF_SKINNY, PROF_PERMUTE = 0, 1, 2
 
 
@@ -382,6 +391,12 @@ class Context:
         self.ensure_workspace(int(2 * ab * A.element_size() + 4096))
         tci_tebd_theta(self.handle, self.tensor(A), la, self.tensor(B), lb, self.tensor(U), lu,
                        self.tensor(out), lt)
+        return out
+
+    def mps_overlap(self, bra, ket, out=None):
+        if out is None:
+            out = self.torch.empty((bra[-1].shape[2], ket[-1].shape[2]), dtype=bra[0].dtype, device=bra[0].device)
+        tci_mps_overlap(self.handle, [self.tensor(x) for x in bra], [self.tensor(x) for x in ket], self.tensor(out))
         return out
 
     def copy(self, src, dst):

@@ -543,6 +543,55 @@ tci_status_t tci_tebd_theta(tci_ctx_t ctx, tci_tensor_t A, const char *la, tci_t
   return tebd_exec(ctx, view_of(A), la, view_of(B), lb, view_of(U), lu, view_of(theta), lt);
 }
 
+tci_status_t tci_mps_overlap(tci_ctx_t ctx, int n, const tci_tensor_t *bra, const tci_tensor_t *ket,
+                             tci_tensor_t out) {
+  CHECK(check_ctx(ctx));
+  if (!bra || !ket) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL site arrays");
+  if (n < 1 || n > kMpsMaxSites) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "mps: %d sites (1..%d)", n, kMpsMaxSites);
+  CHECK(check_ten(ctx, out, true));
+  MpsChain ch{};
+  ch.dtype = out->dtype;
+  ch.n = n;
+  if (ch.dtype != TCI_R64 && ch.dtype != TCI_C128) TCI_FAIL(TCI_ERR_UNSUPPORTED, "mps: dtype must be r64 or c128");
+  int64_t lb = 1, lk = 1;
+  for (int i = 0; i < n; i++) {
+    CHECK(check_ten(ctx, bra[i], true));
+    CHECK(check_ten(ctx, ket[i], true));
+    const tci_tensor_s *b = bra[i], *k = ket[i];
+    if (b->dtype != ch.dtype || k->dtype != ch.dtype) TCI_FAIL(TCI_ERR_UNSUPPORTED, "mps: dtype mismatch at site %d", i);
+    if (b->order != 3 || k->order != 3) TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "mps: site %d is not order 3", i);
+    if (b->shape[0] != lb || k->shape[0] != lk)
+      TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "mps: bond mismatch entering site %d", i);
+    if (b->shape[1] != k->shape[1]) TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "mps: physical dims differ at site %d", i);
+    if (b->shape[1] > kMpsMaxD || b->shape[2] > kMpsMaxChi || k->shape[2] > kMpsMaxChi)
+      TCI_FAIL(TCI_ERR_UNSUPPORTED, "mps: bond > %d or d > %d at site %d (use tci_contract)", kMpsMaxChi, kMpsMaxD, i);
+    ch.bra[i] = b->data;
+    ch.ket[i] = k->data;
+    ch.d[i] = (int)b->shape[1];
+    ch.bra_r[i] = (int)b->shape[2];
+    ch.ket_r[i] = (int)k->shape[2];
+    lb = b->shape[2];
+    lk = k->shape[2];
+  }
+  if (out->order != 2 || out->shape[0] != lb || out->shape[1] != lk)
+    TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "mps: out must be [%lld, %lld]", (long long)lb, (long long)lk);
+  ch.out = out->data;
+  {
+    int64_t tot = 0, pb = 1, pk = 1;
+    for (int i = 0; i < n; i++) {
+      tot += pb * bra[i]->shape[1] * bra[i]->shape[2] + pk * ket[i]->shape[1] * ket[i]->shape[2];
+      pb = bra[i]->shape[2];
+      pk = ket[i]->shape[2];
+    }
+    const int64_t es = ch.dtype == TCI_C128 ? 16 : 8;
+    const int64_t fixed = (int64_t)(kMpsMaxChi * kMpsMaxChi + kMpsMaxChi * kMpsMaxD * kMpsMaxChi) * es;
+    ch.staged_elems = (fixed + tot * es <= 200 * 1024) ? (int)tot : 0;
+  }
+  Verbose vb(ctx, "mps_overlap", {bra[0], ket[0], out});
+  TCI_CUDA_CHECK(launch_mps_overlap(ch, ctx->stream, &ctx->launches));
+  return TCI_OK;
+}
+
 tci_status_t tci_comm_unique_id(void *id) {
   if (!id) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL id");
   CHECK(nccl_load());

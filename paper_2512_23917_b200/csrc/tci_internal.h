@@ -110,6 +110,21 @@ cudaError_t launch_skinny(const SkinnyProblem &p, cudaStream_t s, int64_t *launc
 // Shared-memory bytes the skinny kernel needs (must be <= 227 KB).
 size_t skinny_smem_bytes(int K, int N, size_t esz);
 
+// ---------------------------------------------------------------------------
+// MPS transfer chain in one kernel: <bra|ket> bilinear.
+// ---------------------------------------------------------------------------
+constexpr int kMpsMaxSites = 64, kMpsMaxChi = 32, kMpsMaxD = 4;
+struct MpsChain {
+  tci_dtype_t dtype;
+  int n;
+  const void *bra[kMpsMaxSites];
+  const void *ket[kMpsMaxSites];
+  int d[kMpsMaxSites], bra_r[kMpsMaxSites], ket_r[kMpsMaxSites];   // phys dim, right bonds
+  void *out;
+  int staged_elems;   // total site elements staged in shared memory (0 = read from global)
+};
+cudaError_t launch_mps_overlap(const MpsChain &ch, cudaStream_t s, int64_t *launches);
+
 // Plain device copy (aliasing fallback) and elementwise helpers.
 cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s, int64_t *launches);
 

@@ -416,6 +416,29 @@ def test_mps_norm_cfg1(ctx, oracle_mod):
     assert host(_gpu_overlap(ctx, prod, prod))[0, 0] == 1.0
 
 
+def test_mps_overlap_single_kernel(ctx, oracle_mod):
+    """tci_mps_overlap: the whole transfer chain in one kernel (config 1)."""
+    psi = synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1)
+    phi = synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 2)
+    n2 = ctx.mps_overlap([dev(a) for a in psi], [dev(a) for a in psi])
+    assert rel_frob(host(n2), oracle_mod.mps_norm2(psi)) <= 1e-12
+    ov = ctx.mps_overlap([dev(a) for a in phi], [dev(a) for a in psi])
+    assert rel_frob(host(ov), oracle_mod.mps_overlap(phi, psi)) <= 1e-12
+    prod = [dev(a) for a in synth.product_state_sites(10)]
+    assert host(ctx.mps_overlap(prod, prod))[0, 0] == 1.0
+    # complex, open right boundary (out is [4, 3]), d = 3
+    bonds_b, bonds_k = [1, 3, 7, 4], [1, 2, 5, 3]
+    bra = [synth.random_np((bonds_b[i], 3, bonds_b[i + 1]), "c128", 440, 100 + i) for i in range(3)]
+    ket = [synth.random_np((bonds_k[i], 3, bonds_k[i + 1]), "c128", 441, 100 + i) for i in range(3)]
+    got = ctx.mps_overlap([dev(a) for a in bra], [dev(a) for a in ket])
+    assert tuple(got.shape) == (4, 3)
+    assert rel_frob(host(got), oracle_mod.mps_overlap(bra, ket)) <= 1e-12
+    with pytest.raises(tci.TciError) as e:
+        ctx.mps_overlap([dev(a) for a in psi[:3]], [dev(a) for a in phi[:2]] + [dev(psi[2])],
+                        out=torch.empty(3, 3, dtype=torch.float64, device="cuda"))
+    assert e.value.code == 1
+
+
 def test_mps_mpo_apply(ctx, oracle_mod):
     A = synth.random_tensor((40, 2, 33), "c128", 420, 1)
     I = torch.eye(2, dtype=torch.complex128).reshape(1, 1, 2, 2)

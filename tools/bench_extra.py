@@ -64,6 +64,38 @@ def cfg1(ctx):
     wall = (time.perf_counter() - t0) / 50
     ref = oracle.mps_norm2(synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1))
     got = outs["E"].cpu().numpy()
+    # (b) the whole chain as one kernel (tci_mps_overlap)
+    nout = torch.empty(1, 1, dtype=torch.float64, device="cuda")
+    fk = lambda: ctx.mps_overlap(psi, psi, out=nout)  # noqa: E731
+    med_k, _ = timed(fk, reps=200, warm=10)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(200):
+        fk()
+    torch.cuda.synchronize()
+    wall_k = (time.perf_counter() - t0) / 200
+    err_k = float(abs(nout.cpu().numpy() - ref).max() / abs(ref).max())
+    # (c) CUDA graph of the 20-contract chain
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ctx_g = tci.Context(0, s)
+        Eg0 = torch.ones(1, 1, dtype=torch.float64, device="cuda")
+
+        def chain_g():
+            E = Eg0
+            for A in psi:
+                X = ctx_g.contract(E, "xz", A, "xsy", "zsy")
+                E = ctx_g.contract(X, "zsy", A, "zsw", "yw")
+            return E
+        chain_g()                       # warm: plans cached, workspace attached
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            Eg = chain_g()
+    torch.cuda.current_stream().wait_stream(s)
+    med_g, _ = timed(lambda: g.replay(), reps=200, warm=10)
+    err_g = float(abs(Eg.cpu().numpy() - ref).max() / abs(ref).max())
     t1 = time.perf_counter()
     for _ in range(20):
         oracle.mps_norm2(synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1), threads=1)
@@ -72,6 +104,9 @@ def cfg1(ctx):
             "gpu_us_per_chain_device": med * 1e6, "gpu_us_per_contract_device": med * 1e6 / 20,
             "gpu_us_per_chain_wall": wall * 1e6, "gpu_us_per_contract_wall": wall * 1e6 / 20,
             "oracle_us_per_chain_1thread": t_or * 1e6,
+            "single_kernel_us_per_chain_device": med_k * 1e6, "single_kernel_us_per_chain_wall": wall_k * 1e6,
+            "single_kernel_rel_err": err_k,
+            "cuda_graph_us_per_chain_device": med_g * 1e6, "cuda_graph_rel_err": err_g,
             "rel_err_vs_oracle": float(abs(got - ref).max() / abs(ref).max())}
 
 

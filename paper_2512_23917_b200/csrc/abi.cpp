@@ -49,8 +49,8 @@ struct ProfScope {
 tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g) {
   const bool cplx = dtype_is_complex(g.dtype);
   const double es = (double)dtype_size(g.dtype);
-  ProfScope ps(ctx, kProfGemm, (cplx ? 8.0 : 2.0) * g.M * g.N * g.K * g.batch,
-               es * g.batch * ((double)g.M * g.K + (double)g.K * g.N + (double)g.M * g.N));
+  ProfScope ps(ctx, kProfGemm, (cplx ? 8.0 : 2.0) * g.M * g.N * g.K,
+               es * ((double)g.M * g.K + (double)g.K * g.N + (double)g.M * g.N));
   TCI_CUDA_CHECK(launch_gemm(g, ctx->stream, &ctx->launches));
   ps.done();
   return TCI_OK;

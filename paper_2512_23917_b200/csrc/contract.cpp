@@ -245,6 +245,29 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   if (!formB) { offB = off; off = align_up(off + (size_t)K * N * es); }
   const bool c_scratch = !formC || alias;
   if (c_scratch) { offC = off; off = align_up(off + (size_t)M * N * es); }
+  // deterministic split-K when the output has too few tiles to fill the 148
+  // SMs and K is long: S partial GEMMs over K chunks + an ascending-order sum
+  int splitk = 1;
+  int64_t k_chunk = 0;
+  size_t offP = 0;
+  {
+    int bm, bn;
+    gemm_tile(a.dtype, &bm, &bn);
+    const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+    if (tiles < 2 * 148 && K >= 256) {
+      int64_t S = std::min<int64_t>({(4 * 148 + tiles - 1) / tiles, K / 128, 1024});
+      if (S >= 2) {
+        k_chunk = ((K + S - 1) / S + 15) / 16 * 16;
+        S = (K + k_chunk - 1) / k_chunk;
+        if (S >= 2) {
+          splitk = (int)S;
+          const size_t pes = dtype_is_complex(a.dtype) ? 16 : 8;   // fp64 partials
+          offP = off;
+          off = align_up(off + (size_t)S * M * N * pes);
+        }
+      }
+    }
+  }
   *ws_needed = off;
   if (dry_run) return TCI_OK;
   if (off > ws_bytes || (off && !ws))
@@ -332,6 +355,11 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   canon_a(g.M, g.K, g.a_sm, g.a_sk);
   // B(k,n): the same rule with (N, K)
   canon_a(g.N, g.K, g.b_sn, g.b_sk);
+  if (splitk > 1) {
+    g.splitk = splitk;
+    g.k_chunk = k_chunk;
+    g.partial = wsb + offP;
+  }
   { tci_status_t _r = run_gemm(ctx, g); if (_r) return _r; }
 
   // ---- refold into gamma order (or copy out of scratch when aliased) ----

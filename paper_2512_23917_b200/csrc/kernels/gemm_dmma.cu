@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 
 #include "../tci_internal.h"
 #include "common.cuh"
@@ -274,10 +275,18 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
   const int tile_n = (bid % per_group) / gsize;
   const int64_t m0 = (int64_t)tile_m * C::BM, n0 = (int64_t)tile_n * C::BN;
 
-  const int64_t bz = blockIdx.z;
-  const char *Ab = static_cast<const char *>(p.A) + bz * p.a_sb * C::ESZ;
-  const char *Bb = static_cast<const char *>(p.B) + bz * p.b_sb * C::ESZ;
-  char *Cb = static_cast<char *>(p.C) + bz * p.c_sb * C::ESZ;
+  const char *Ab = static_cast<const char *>(p.A);
+  const char *Bb = static_cast<const char *>(p.B);
+  char *Cb = static_cast<char *>(p.C);
+  int64_t Kl = p.K, c_sm = p.c_sm;   // this CTA's K extent and C row stride
+  if (p.splitk > 1) {
+    const int64_t kb = (int64_t)blockIdx.z * p.k_chunk;
+    Kl = p.K - kb < p.k_chunk ? p.K - kb : p.k_chunk;
+    Ab += kb * p.a_sk * C::ESZ;
+    Bb += kb * p.b_sk * C::ESZ;
+    Cb = static_cast<char *>(p.partial) + (int64_t)blockIdx.z * p.M * p.N * C::ESZ;
+    c_sm = p.N;
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm0 = (warp / C::WARPS_N) * C::WM, wn0 = (warp % C::WARPS_N) * C::WN;
@@ -303,13 +312,13 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
 #pragma unroll
       for (int j = 0; j < C::NJ; j++) acc.c[s][i][j][0] = acc.c[s][i][j][1] = 0.0;
 
-  const int KT = (int)((p.K + C::BK - 1) / C::BK);
-  const int KT_full = (int)(p.K / C::BK);   // tiles with no K tail
+  const int KT = (int)((Kl + C::BK - 1) / C::BK);
+  const int KT_full = (int)(Kl / C::BK);    // tiles with no K tail
 #pragma unroll
   for (int s = 0; s < C::STAGES - 1; s++) {
     if (s < KT) {
-      la.load(sA0 + s * C::A_STAGE * C::ESZ, s, p.K, s < KT_full);
-      lb.load(sB0 + s * C::B_STAGE * C::ESZ, s, p.K, s < KT_full);
+      la.load(sA0 + s * C::A_STAGE * C::ESZ, s, Kl, s < KT_full);
+      lb.load(sB0 + s * C::B_STAGE * C::ESZ, s, Kl, s < KT_full);
     }
     cp_async_commit();
   }
@@ -334,8 +343,8 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
         const int nk = kt + C::STAGES - 1;
         if (nk < KT) {
           const int ns = nk % C::STAGES;
-          la.load(sA0 + ns * C::A_STAGE * C::ESZ, nk, p.K, nk < KT_full);
-          lb.load(sB0 + ns * C::B_STAGE * C::ESZ, nk, p.K, nk < KT_full);
+          la.load(sA0 + ns * C::A_STAGE * C::ESZ, nk, Kl, nk < KT_full);
+          lb.load(sB0 + ns * C::B_STAGE * C::ESZ, nk, Kl, nk < KT_full);
         }
         cp_async_commit();
         if (kt + 1 < KT) {
@@ -412,7 +421,7 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
     for (int j = 0; j < C::NJ; j++) {
       const int64_t n = n0 + wn0 + j * 8 + 2 * lc;
       if constexpr (C::kCplx) {
-        double2 *cp = reinterpret_cast<double2 *>(Cb) + m * p.c_sm + n;
+        double2 *cp = reinterpret_cast<double2 *>(Cb) + m * c_sm + n;
         double re0, im0, re1, im1;
         if constexpr (C::kAlgo == kCplx3M) {
           const double P0 = acc.c[0][i][j][0], Q0 = acc.c[1][i][j][0], S0 = acc.c[2][i][j][0];
@@ -430,7 +439,7 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
         if (n < p.N) cp[0] = make_double2(re0, im0);
         if (n + 1 < p.N) cp[1] = make_double2(re1, im1);
       } else {
-        double *cp = reinterpret_cast<double *>(Cb) + m * p.c_sm + n;
+        double *cp = reinterpret_cast<double *>(Cb) + m * c_sm + n;
         if (n < p.N) cp[0] = acc.c[0][i][j][0];
         if (n + 1 < p.N) cp[1] = acc.c[0][i][j][1];
       }
@@ -450,8 +459,8 @@ cudaError_t run(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
     attr_set |= 1ull << dev;
   }
   const int64_t tm = (p.M + C::BM - 1) / C::BM, tn = (p.N + C::BN - 1) / C::BN;
-  if (tm * tn > 0x7fffffffLL || p.batch > 65535) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)(tm * tn), 1, (unsigned)p.batch);
+  if (tm * tn > 0x7fffffffLL || p.splitk > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)(tm * tn), 1, (unsigned)(p.splitk > 1 ? p.splitk : 1));
   kern<<<grid, C::NT, C::SMEM, s>>>(p, (int)tm, (int)tn);
   if (launches) ++*launches;
   return cudaGetLastError();
@@ -490,6 +499,74 @@ bool use_4m() {
 
 cudaError_t launch_gemm_f32(const GemmProblem &p, cudaStream_t s, int64_t *launches);
 
+namespace {
+// split-K reduction: C[m, n] = sum_{z ascending} partial[z][m][n] (fixed
+// order -> deterministic); P = partial element, O = output element
+template <typename P, typename O>
+__global__ void __launch_bounds__(256) splitk_reduce(const P *__restrict__ part, O *__restrict__ C,
+                                                     int64_t M, int64_t N, int64_t c_sm, int S) {
+  const int64_t MN = M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < MN; i += (int64_t)gridDim.x * blockDim.x) {
+    P acc = part[i];
+    for (int z = 1; z < S; z++) {
+      const P v = part[(int64_t)z * MN + i];
+      if constexpr (sizeof(P) == 16) {
+        reinterpret_cast<double2 &>(acc).x += reinterpret_cast<const double2 &>(v).x;
+        reinterpret_cast<double2 &>(acc).y += reinterpret_cast<const double2 &>(v).y;
+      } else {
+        reinterpret_cast<double &>(acc) += reinterpret_cast<const double &>(v);
+      }
+    }
+    const int64_t m = i / N, n = i % N;
+    if constexpr (sizeof(O) == sizeof(P)) {
+      C[m * c_sm + n] = reinterpret_cast<const O &>(acc);
+    } else if constexpr (sizeof(P) == 16) {
+      const double2 a = reinterpret_cast<const double2 &>(acc);
+      const float2 f = make_float2((float)a.x, (float)a.y);
+      C[m * c_sm + n] = reinterpret_cast<const O &>(f);
+    } else {
+      const float f = (float)reinterpret_cast<const double &>(acc);
+      C[m * c_sm + n] = reinterpret_cast<const O &>(f);
+    }
+  }
+}
+}  // namespace
+
+static cudaError_t launch_splitk_reduce(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
+  const int64_t MN = p.M * p.N;
+  const unsigned blocks = (unsigned)std::min<int64_t>((MN + 255) / 256, 148 * 8);
+  switch (p.dtype) {
+    case TCI_C128:
+      splitk_reduce<double2, double2><<<blocks, 256, 0, s>>>((const double2 *)p.partial, (double2 *)p.C, p.M, p.N, p.c_sm, p.splitk);
+      break;
+    case TCI_R64:
+      splitk_reduce<double, double><<<blocks, 256, 0, s>>>((const double *)p.partial, (double *)p.C, p.M, p.N, p.c_sm, p.splitk);
+      break;
+    case TCI_C64:
+      splitk_reduce<double2, float2><<<blocks, 256, 0, s>>>((const double2 *)p.partial, (float2 *)p.C, p.M, p.N, p.c_sm, p.splitk);
+      break;
+    case TCI_R32:
+      splitk_reduce<double, float><<<blocks, 256, 0, s>>>((const double *)p.partial, (float *)p.C, p.M, p.N, p.c_sm, p.splitk);
+      break;
+  }
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+void gemm_tile(tci_dtype_t dtype, int *bm, int *bn) {
+  const bool big = dtype == TCI_R64 || dtype == TCI_R32;
+  *bm = big ? 128 : 64;
+  *bn = big ? 128 : 64;
+}
+
+static cudaError_t launch_gemm_main(const GemmProblem &p, cudaStream_t s, int64_t *launches);
+
+cudaError_t launch_gemm(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
+  cudaError_t e = launch_gemm_main(p, s, launches);
+  if (e != cudaSuccess || p.splitk <= 1 || p.M == 0 || p.N == 0) return e;
+  return launch_splitk_reduce(p, s, launches);
+}
+
 bool tebd_fused_supported(const TebdProblem &t) {
   auto al16 = [](const void *x) { return ((uintptr_t)x % 16) == 0; };
   return t.d == 2 && t.a_b == 1 && t.b_c == 1 && al16(t.A) && al16(t.B) && t.a_a % 2 == 0 &&
@@ -515,7 +592,7 @@ cudaError_t launch_tebd_fused(const TebdProblem &t, cudaStream_t s, int64_t *lau
   return run<TC>(p, s, launches);   // tiles: (chi_a / 64) x (chi_c / 64)
 }
 
-cudaError_t launch_gemm(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
+static cudaError_t launch_gemm_main(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   if (p.M == 0 || p.N == 0) return cudaSuccess;
   if (p.dtype == TCI_R32 || p.dtype == TCI_C64) return launch_gemm_f32(p, s, launches);
   // The planner canonicalises strides (contract.cpp): a_sk == 1 selects the
@@ -527,8 +604,7 @@ cudaError_t launch_gemm(const GemmProblem &p, cudaStream_t s, int64_t *launches)
   const int64_t lda = ak ? p.a_sm : p.a_sk, ldb = bk ? p.b_sn : p.b_sk;
   const bool aligned = ((uintptr_t)p.A % 16 == 0) && ((uintptr_t)p.B % 16 == 0) &&
                        (lda % 2 == 0 || (ak ? p.M : p.K) == 1) &&
-                       (ldb % 2 == 0 || (bk ? p.N : p.K) == 1) && (p.a_sb % 2 == 0) &&
-                       (p.b_sb % 2 == 0);
+                       (ldb % 2 == 0 || (bk ? p.N : p.K) == 1);
   if (aligned) {
     if (ak && bk) return run<DCfg<true, true, 2>>(p, s, launches);
     if (ak && !bk) return run<DCfg<true, false, 2>>(p, s, launches);

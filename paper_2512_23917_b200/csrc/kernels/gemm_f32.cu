@@ -50,10 +50,18 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
   const int tid = threadIdx.x;
   const int tile_m = blockIdx.x / tiles_n, tile_n = blockIdx.x % tiles_n;
   const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN;
-  const int64_t bz = blockIdx.z;
-  const E *A = static_cast<const E *>(p.A) + bz * p.a_sb;
-  const E *B = static_cast<const E *>(p.B) + bz * p.b_sb;
-  E *C = static_cast<E *>(p.C) + bz * p.c_sb;
+  const E *A = static_cast<const E *>(p.A);
+  const E *B = static_cast<const E *>(p.B);
+  E *C = static_cast<E *>(p.C);
+  int64_t Kl = p.K;
+  typename Ops<E>::Acc *Pz = nullptr;   // split-K partial (fp64 accumulators)
+  if (p.splitk > 1) {
+    const int64_t kb = (int64_t)blockIdx.z * p.k_chunk;
+    Kl = p.K - kb < p.k_chunk ? p.K - kb : p.k_chunk;
+    A += kb * p.a_sk;
+    B += kb * p.b_sk;
+    Pz = static_cast<typename Ops<E>::Acc *>(p.partial) + (int64_t)blockIdx.z * p.M * p.N;
+  }
   const bool a_mfast = (p.a_sk != 1);   // canonical: a_sk == 1 or a_sm == 1
   const bool b_nfast = (p.b_sk != 1);
   constexpr int LA = BM * BK / 256, LB = BN * BK / 256;
@@ -66,7 +74,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
       int m, k;
       if (a_mfast) { k = idx / BM; m = idx % BM; } else { m = idx / BK; k = idx % BK; }
       const int64_t gm = m0 + m, gk = k0 + k;
-      ra[i] = (gm < p.M && gk < p.K) ? A[gm * p.a_sm + gk * p.a_sk] : Ops<E>::zero();
+      ra[i] = (gm < p.M && gk < Kl) ? A[gm * p.a_sm + gk * p.a_sk] : Ops<E>::zero();
     }
 #pragma unroll
     for (int i = 0; i < LB; i++) {
@@ -74,7 +82,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
       int n, k;
       if (b_nfast) { k = idx / BN; n = idx % BN; } else { n = idx / BK; k = idx % BK; }
       const int64_t gn = n0 + n, gk = k0 + k;
-      rb[i] = (gn < p.N && gk < p.K) ? B[gk * p.b_sk + gn * p.b_sn] : Ops<E>::zero();
+      rb[i] = (gn < p.N && gk < Kl) ? B[gk * p.b_sk + gn * p.b_sn] : Ops<E>::zero();
     }
   };
   auto sstore = [&](int buf) {
@@ -101,7 +109,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
 #pragma unroll
     for (int j = 0; j < TN; j++) acc[i][j] = Ops<E>::azero();
 
-  const int KT = (int)((p.K + BK - 1) / BK);
+  const int KT = (int)((Kl + BK - 1) / BK);
   gload(0);
   sstore(0);
   __syncthreads();
@@ -132,7 +140,9 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
 #pragma unroll
     for (int j = 0; j < TN; j++) {
       const int64_t n = n0 + tx * TN + j;
-      if (n < p.N) C[m * p.c_sm + n] = Ops<E>::out(acc[i][j]);
+      if (n >= p.N) continue;
+      if (Pz) Pz[m * p.N + n] = acc[i][j];
+      else C[m * p.c_sm + n] = Ops<E>::out(acc[i][j]);
     }
   }
 }
@@ -140,8 +150,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
 template <typename E, int BM, int BN, int BK, int TM, int TN>
 cudaError_t run_simt(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
-  if (tm * tn > 0x7fffffffLL || p.batch > 65535) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)(tm * tn), 1, (unsigned)p.batch);
+  if (tm * tn > 0x7fffffffLL || p.splitk > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)(tm * tn), 1, (unsigned)(p.splitk > 1 ? p.splitk : 1));
   gemm_simt_kernel<E, BM, BN, BK, TM, TN><<<grid, 256, 0, s>>>(p, (int)tm, (int)tn);
   if (launches) ++*launches;
   return cudaGetLastError();

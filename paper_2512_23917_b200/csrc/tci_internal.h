@@ -36,9 +36,13 @@ struct GemmProblem {
   const void *A; int64_t a_sm, a_sk;
   const void *B; int64_t b_sk, b_sn;
   void *C; int64_t c_sm;        // c_sn == 1
-  // Batched over one extra "batch" leg (strides in elements); batch == 1 for
-  // a plain GEMM.
-  int64_t batch = 1, a_sb = 0, b_sb = 0, c_sb = 0;
+  // deterministic split-K (few output tiles, long K): split z of `splitk`
+  // sums k in [z*k_chunk, min(K,(z+1)*k_chunk)) into partial + z*M*N (double
+  // or double2 elements, row-major [M][N]); a reduce kernel then adds the
+  // splits in ascending z into C. k_chunk is a multiple of 16.
+  int splitk = 1;
+  int64_t k_chunk = 0;
+  void *partial = nullptr;
   // mode 1 = TEBD theta with the gate in the epilogue (launch_tebd_fused)
   int mode = 0;
   int64_t te_chi_a = 0, te_chi_c = 0;     // extents of a and c
@@ -49,6 +53,9 @@ struct GemmProblem {
   double *te_T = nullptr;                 // theta
   int64_t te_t[4] = {0, 0, 0, 0};         // strides of a, p, q, c in theta
 };
+
+// Output tile of the GEMM kernel used for `dtype` (for the planner's split-K choice).
+void gemm_tile(tci_dtype_t dtype, int *bm, int *bn);
 
 // Launches the DMMA (f64/c128) or FFMA (f32/c64) GEMM. Returns cudaSuccess or
 // the launch error. `launches` is incremented per kernel launched.

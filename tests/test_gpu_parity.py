@@ -126,6 +126,22 @@ def test_gemm_layouts_ragged(ctx, oracle_mod, dt):
                 assert rel_frob(host(C), r) <= 1e-12, (la, lb, lc)
 
 
+@pytest.mark.parametrize("dt", ["r64", "c128", "r32", "c64"])
+def test_splitk_small_output_long_k(ctx, oracle_mod, dt):
+    """Few output tiles and a long K take the deterministic split-K path
+    (partial GEMMs + ascending-order reduction): parity and repeatability."""
+    A = synth.random_tensor((5, 37, 700), dt, 86, 1)      # m=5, k=(37, 700)
+    B = synth.random_tensor((700, 37, 9), dt, 86, 2)
+    C1 = ctx.contract(dev(A), "mkl", dev(B), "lkn", "nm")
+    C2 = ctx.contract(dev(A), "mkl", dev(B), "lkn", "nm")
+    assert torch.equal(C1, C2)
+    ref = oracle_mod.contract(A.numpy(), "mkl", B.numpy(), "lkn", "nm")
+    assert rel_frob(host(C1), ref) <= TOL[dt]
+    # full contraction to a scalar (the sweep's worst case before split-K)
+    s = ctx.contract(dev(A), "mkl", dev(A), "mkl", "")
+    assert rel_frob(host(s), oracle_mod.contract(A.numpy(), "mkl", A.numpy(), "mkl", "")) <= TOL[dt]
+
+
 def test_higham_elementwise_bound(ctx, oracle_mod):
     """Per element |C_gpu - C_oracle| <= 2 gamma_K (|A|.|B|): catches local bugs
     that a Frobenius average could hide."""

@@ -253,6 +253,50 @@ TCI_API tci_status_t tci_tebd_theta(tci_ctx_t ctx, tci_tensor_t A, const char *l
                             tci_tensor_t U, const char *lu,
                             tci_tensor_t theta, const char *lt);
 
+/* ---------------------------------------------------------------------- */
+/* Vector functions (device kernels, deterministic reductions) and the     */
+/* Lanczos driver around H_eff                              */
+/* ---------------------------------------------------------------------- */
+
+/* Frobenius norm (Eq. frob_norm) into *out (host). r64/c128.
+ * Synchronizes the context stream. Bitwise reproducible. */
+TCI_API tci_status_t tci_norm(tci_ctx_t ctx, tci_tensor_t t, double *out);
+
+/* In-place normalize to unit Frobenius norm; the original norm goes to
+ * *norm_out (may be NULL). Zero norm -> INVALID_ARGUMENT. */
+TCI_API tci_status_t tci_normalize(tci_ctx_t ctx, tci_tensor_t inout, double *norm_out);
+
+/* out = s * in with s = s_re + i s_im (s_im must be 0 for real data)
+ * (P:1784-1808). out may be in (in-place overload (1)). */
+TCI_API tci_status_t tci_scale(tci_ctx_t ctx, tci_tensor_t in, double s_re, double s_im, tci_tensor_t out);
+
+/* out = sum_{i<m} s_i ins[i]; coefs = m (re, im) pairs, or
+ * NULL for all s_i = 1 (overload (1)); all shapes identical; out may alias
+ * any input. */
+TCI_API tci_status_t tci_linear_combine(tci_ctx_t ctx, int m, const tci_tensor_t *ins, const double *coefs,
+                                        tci_tensor_t out);
+
+/* <a|b> = sum_i conj?(a_i) b_i into out[2] = (re, im): the full contraction
+ * to a scalar of section III, with cplx_conj of a
+ * when conj_a != 0. Synchronizes. */
+TCI_API tci_status_t tci_inner(tci_ctx_t ctx, tci_tensor_t a, tci_tensor_t b, int conj_a, double *out);
+
+/* Lowest eigenpair of H_eff (tci_heff_apply operator; Hermitian by the
+ * caller's construction) by Lanczos with full re-orthogonalisation: psi is
+ * the start vector on entry and the normalised Ritz vector on return;
+ * *energy = lowest Ritz value; *iters = Krylov dimension used. Stops when
+ * the Ritz value moves by < tol or the residual vanishes, at most max_iter
+ * (1..512) steps. With a communicator (tci_comm_init, nranks P) L is this
+ * rank's slice L[:, :, b_r] (chi_l / P columns) and each step ends with one
+ * NCCL all-gather of the output slabs; every rank then holds identical
+ * vectors. Workspace: tci_lanczos_workspace_size (heff scratch + (max_iter+2)
+ * vectors). Host synchronizes once per inner product. */
+TCI_API tci_status_t tci_lanczos_workspace_size(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2,
+                                                tci_tensor_t R, tci_tensor_t psi, int max_iter, size_t *bytes);
+TCI_API tci_status_t tci_heff_lanczos(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2,
+                                      tci_tensor_t R, tci_tensor_t psi, int max_iter, double tol, double *energy,
+                                      int *iters);
+
 /* MPS overlap / norm transfer chain (R17; the section III overlap
  * by contraction): with E_0 = [[1]],
  *   E_{i+1}[y,w] = sum_{x,z,s} E_i[x,z] bra_i[x,s,y] ket_i[z,s,w],

@@ -284,3 +284,35 @@ def mps_mpo_apply(A, W, threads=None):
     Bt = contract(A, "asb", W, "wvst", "awtbv", threads)
     a, w, t, b, v = Bt.shape
     return reshape(Bt, (a * w, t, b * v))
+
+
+# ----------------------------------------------------------------------------
+# vector functions (App. C.5): definitions written out
+# ----------------------------------------------------------------------------
+
+def norm(a) -> float:
+    """Frobenius norm, Eq. frob_norm: sqrt(sum |A_i|^2)."""
+    a = np.asarray(a).reshape(-1)
+    return float(np.sqrt(np.sum((a.real.astype(np.float64) ** 2) + (a.imag.astype(np.float64) ** 2))))
+
+
+def scale(a, s):
+    """tci::scale (PAPER.md:1784-1808): s * A."""
+    return s * np.asarray(a)
+
+
+def linear_combine(ins, coefs=None):
+    """tci::linear_combine (PAPER.md:1980-2010): sum_i s_i A_i (s_i = 1 by default)."""
+    coefs = [1.0] * len(ins) if coefs is None else list(coefs)
+    out = np.zeros_like(np.asarray(ins[0]), dtype=np.result_type(*ins, *[np.asarray(c) for c in coefs]))
+    for c, x in zip(coefs, ins):
+        out = out + c * np.asarray(x)
+    return out
+
+
+def inner(a, b, conj_a=True):
+    """Full contraction to a scalar of conj(a) (cplx_conj,
+    PAPER.md:1235-1268) with b: sum_i conj(a_i) b_i."""
+    a = np.asarray(a).reshape(-1)
+    b = np.asarray(b).reshape(-1)
+    return complex(np.sum((np.conj(a) if conj_a else a) * b))

@@ -43,7 +43,8 @@ EXPORTED = [
     "tci_contract_workspace_size", "tci_heff_workspace_size", "tci_heff_apply",
     "tci_tebd_theta", "tci_comm_init", "tci_comm_unique_id", "tci_allgather",
     "tci_launch_count", "tci_heff_plan_tree", "tci_profile_enable", "tci_profile_query",
-    "tci_mps_overlap",
+    "tci_mps_overlap", "tci_norm", "tci_normalize", "tci_scale", "tci_linear_combine", "tci_inner",
+    "tci_lanczos_workspace_size", "tci_heff_lanczos",
 ]
 
 
@@ -85,6 +86,14 @@ _sig = {
     "tci_allgather": ([_vp, _vp, _vp], ctypes.c_int),
     "tci_launch_count": ([_vp, _i64p], ctypes.c_int),
     "tci_profile_enable": ([_vp, ctypes.c_int], ctypes.c_int),
+    "tci_norm": ([_vp, _vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "tci_normalize": ([_vp, _vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "tci_scale": ([_vp, _vp, ctypes.c_double, ctypes.c_double, _vp], ctypes.c_int),
+    "tci_linear_combine": ([_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_double), _vp], ctypes.c_int),
+    "tci_inner": ([_vp, _vp, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "tci_lanczos_workspace_size": ([_vp] * 6 + [ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tci_heff_lanczos": ([_vp] * 6 + [ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
+                                      ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_mps_overlap": ([_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp], ctypes.c_int),
     "tci_profile_query": ([_vp, ctypes.c_int, _i64p] + [ctypes.POINTER(ctypes.c_double)] * 3, ctypes.c_int),
     "tci_heff_plan_tree": ([ctypes.c_int64] * 8 + [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
@@ -264,6 +273,58 @@ def tci_mps_overlap(ctx: int, bra: Sequence[int], ket: Sequence[int], out: int) 
     _ok(_lib.tci_mps_overlap(_vp(ctx), n, b, k, _vp(out)), "tci_mps_overlap")
 
 
+def tci_norm(ctx: int, t: int) -> float:
+    x = ctypes.c_double()
+    _ok(_lib.tci_norm(_vp(ctx), _vp(t), ctypes.byref(x)), "tci_norm")
+    return x.value
+
+
+def tci_normalize(ctx: int, t: int) -> float:
+    x = ctypes.c_double()
+    _ok(_lib.tci_normalize(_vp(ctx), _vp(t), ctypes.byref(x)), "tci_normalize")
+    return x.value
+
+
+def tci_scale(ctx: int, src: int, s: complex, dst: int) -> None:
+    s = complex(s)
+    _ok(_lib.tci_scale(_vp(ctx), _vp(src), s.real, s.imag, _vp(dst)), "tci_scale")
+
+
+def tci_linear_combine(ctx: int, ins: Sequence[int], coefs, out: int) -> None:
+    m = len(ins)
+    arr = (_vp * m)(*[_vp(x) for x in ins])
+    if coefs is None:
+        cp = None
+    else:
+        flat = []
+        for c in coefs:
+            c = complex(c)
+            flat += [c.real, c.imag]
+        cp = (ctypes.c_double * (2 * m))(*flat)
+    _ok(_lib.tci_linear_combine(_vp(ctx), m, arr, cp, _vp(out)), "tci_linear_combine")
+
+
+def tci_inner(ctx: int, a: int, b: int, conj_a: bool = True) -> complex:
+    out = (ctypes.c_double * 2)()
+    _ok(_lib.tci_inner(_vp(ctx), _vp(a), _vp(b), int(bool(conj_a)), out), "tci_inner")
+    return complex(out[0], out[1])
+
+
+def tci_lanczos_workspace_size(ctx: int, L: int, W1: int, W2: int, R: int, psi: int, max_iter: int) -> int:
+    n = ctypes.c_size_t()
+    _ok(_lib.tci_lanczos_workspace_size(_vp(ctx), _vp(L), _vp(W1), _vp(W2), _vp(R), _vp(psi), int(max_iter),
+                                        ctypes.byref(n)), "tci_lanczos_workspace_size")
+    return n.value
+
+
+def tci_heff_lanczos(ctx: int, L: int, W1: int, W2: int, R: int, psi: int, max_iter: int, tol: float):
+    e = ctypes.c_double()
+    it = ctypes.c_int()
+    _ok(_lib.tci_heff_lanczos(_vp(ctx), _vp(L), _vp(W1), _vp(W2), _vp(R), _vp(psi), int(max_iter), float(tol),
+                              ctypes.byref(e), ctypes.byref(it)), "tci_heff_lanczos")
+    return e.value, it.value
+
+
 PROF_GEMM, PROF_SKINNY, PROF_PERMUTE = 0, 1, 2
 
 
@@ -392,6 +453,30 @@ class Context:
         tci_tebd_theta(self.handle, self.tensor(A), la, self.tensor(B), lb, self.tensor(U), lu,
                        self.tensor(out), lt)
         return out
+
+    def norm(self, x) -> float:
+        return tci_norm(self.handle, self.tensor(x))
+
+    def inner(self, a, b, conj_a=True) -> complex:
+        return tci_inner(self.handle, self.tensor(a), self.tensor(b), conj_a)
+
+    def linear_combine(self, ins, coefs=None, out=None):
+        if out is None:
+            out = self.torch.empty_like(ins[0])
+        tci_linear_combine(self.handle, [self.tensor(x) for x in ins], coefs, self.tensor(out))
+        return out
+
+    def scale(self, x, s, out=None):
+        if out is None:
+            out = self.torch.empty_like(x)
+        tci_scale(self.handle, self.tensor(x), s, self.tensor(out))
+        return out
+
+    def heff_lanczos(self, L, W1, W2, R, psi, max_iter=60, tol=1e-12):
+        """Lowest eigenpair of H_eff; psi (start vector) is overwritten by the Ritz vector."""
+        hs = [self.tensor(x) for x in (L, W1, W2, R, psi)]
+        self.ensure_workspace(tci_lanczos_workspace_size(self.handle, *hs, max_iter))
+        return tci_heff_lanczos(self.handle, *hs, max_iter, tol)
 
     def mps_overlap(self, bra, ket, out=None):
         if out is None:

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "runtime.h"
 
@@ -210,6 +211,18 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   c->rank = 0;
   c->plan_hits = c->plan_misses = 0;
   c->prof_on = false;
+  c->dev_scratch = nullptr;
+  c->host_scratch = nullptr;
+  {
+    cudaError_t e1 = cudaMalloc(&c->dev_scratch, reduce_scratch_bytes());
+    cudaError_t e2 = cudaMallocHost(&c->host_scratch, 64);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      if (c->dev_scratch) cudaFree(c->dev_scratch);
+      if (c->host_scratch) cudaFreeHost(c->host_scratch);
+      delete c;
+      TCI_FAIL(TCI_ERR_CUDA, "context scratch allocation failed");
+    }
+  }
   *ctx = c;
   return TCI_OK;
 }
@@ -257,6 +270,9 @@ tci_status_t tci_destroy_context(tci_ctx_t ctx) {
   cudaStreamSynchronize(ctx->stream);
   prof_clear(ctx);
   ctx->prof_on = false;
+  if (ctx->dev_scratch) cudaFree(ctx->dev_scratch);
+  if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
+  ctx->dev_scratch = ctx->host_scratch = nullptr;
   ctx->nccl_comm = nullptr;
   ctx->plan_cache.clear();
   ctx->ws = nullptr;
@@ -592,6 +608,94 @@ tci_status_t tci_mps_overlap(tci_ctx_t ctx, int n, const tci_tensor_t *bra, cons
   return TCI_OK;
 }
 
+tci_status_t tci_norm(tci_ctx_t ctx, tci_tensor_t t, double *out) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, t, true));
+  if (!out) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  Verbose vb(ctx, "norm", {t});
+  return vec_norm(ctx, view_of(t), out);
+}
+
+tci_status_t tci_normalize(tci_ctx_t ctx, tci_tensor_t t, double *norm_out) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, t, true));
+  Verbose vb(ctx, "normalize", {t});
+  double n = 0;
+  CHECK(vec_norm(ctx, view_of(t), &n));
+  if (norm_out) *norm_out = n;
+  if (!(n > 0)) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "normalize: zero norm");
+  const View v = view_of(t);
+  const double c[2] = {1.0 / n, 0.0};
+  return vec_lincomb(ctx, 1, &v, c, v);
+}
+
+tci_status_t tci_scale(tci_ctx_t ctx, tci_tensor_t in, double s_re, double s_im, tci_tensor_t out) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, in, true));
+  CHECK(check_ten(ctx, out, true));
+  if (in->dtype != TCI_C128 && s_im != 0.0) TCI_FAIL(TCI_ERR_UNSUPPORTED, "scale: complex factor on real data");
+  Verbose vb(ctx, "scale", {in});
+  const View v = view_of(in);
+  const double c[2] = {s_re, s_im};
+  return vec_lincomb(ctx, 1, &v, c, view_of(out));
+}
+
+tci_status_t tci_linear_combine(tci_ctx_t ctx, int m, const tci_tensor_t *ins, const double *coefs,
+                                tci_tensor_t out) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, out, true));
+  if (m < 1 || !ins) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "linear_combine: need at least one input");
+  std::vector<View> v(m);
+  std::vector<double> c(2 * m);
+  for (int j = 0; j < m; j++) {
+    CHECK(check_ten(ctx, ins[j], true));
+    if (ins[j]->order != out->order) TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "linear_combine: order mismatch");
+    for (int k = 0; k < out->order; k++)
+      if (ins[j]->shape[k] != out->shape[k]) TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "linear_combine: shapes must be identical (P:1995)");
+    v[j] = view_of(ins[j]);
+    c[2 * j] = coefs ? coefs[2 * j] : 1.0;        // overload (1): all s_i = 1
+    c[2 * j + 1] = coefs ? coefs[2 * j + 1] : 0.0;
+    if (out->dtype != TCI_C128 && c[2 * j + 1] != 0.0) TCI_FAIL(TCI_ERR_UNSUPPORTED, "linear_combine: complex coefficient on real data");
+  }
+  Verbose vb(ctx, "linear_combine", {ins[0], out});
+  return vec_lincomb(ctx, m, v.data(), c.data(), view_of(out));
+}
+
+tci_status_t tci_inner(tci_ctx_t ctx, tci_tensor_t a, tci_tensor_t b, int conj_a, double *out) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, a, true));
+  CHECK(check_ten(ctx, b, true));
+  if (!out) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  Verbose vb(ctx, "inner", {a, b});
+  double r[2];
+  CHECK(vec_inner(ctx, view_of(a), view_of(b), conj_a, r));
+  out[0] = r[0];
+  out[1] = r[1];
+  return TCI_OK;
+}
+
+tci_status_t tci_lanczos_workspace_size(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2,
+                                        tci_tensor_t R, tci_tensor_t psi, int max_iter, size_t *bytes) {
+  CHECK(check_ctx(ctx));
+  for (tci_tensor_t t : {L, W1, W2, R, psi}) CHECK(check_ten(ctx, t, false));
+  if (!bytes) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  if (L->order != 3 || W1->order != 4 || W2->order != 4 || R->order != 3 || psi->order != 4)
+    TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "lanczos: orders L 3, W1 4, W2 4, R 3, psi 4");
+  size_t hb = 0;
+  return lanczos_bytes(ctx, view_of(L), view_of(W1), view_of(W2), view_of(R), view_of(psi), max_iter, bytes, &hb);
+}
+
+tci_status_t tci_heff_lanczos(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2, tci_tensor_t R,
+                              tci_tensor_t psi, int max_iter, double tol, double *energy, int *iters) {
+  CHECK(check_ctx(ctx));
+  for (tci_tensor_t t : {L, W1, W2, R, psi}) CHECK(check_ten(ctx, t, true));
+  if (L->order != 3 || W1->order != 4 || W2->order != 4 || R->order != 3 || psi->order != 4)
+    TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "lanczos: orders L 3, W1 4, W2 4, R 3, psi 4");
+  Verbose vb(ctx, "heff_lanczos", {L, psi});
+  return lanczos_exec(ctx, view_of(L), view_of(W1), view_of(W2), view_of(R), view_of(psi), max_iter, tol, energy,
+                      iters);
+}
+
 tci_status_t tci_comm_unique_id(void *id) {
   if (!id) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL id");
   CHECK(nccl_load());
@@ -636,3 +740,7 @@ tci_status_t tci_allgather(tci_ctx_t ctx, tci_tensor_t shard, tci_tensor_t full)
 }
 
 }  // extern "C"
+
+namespace tci {
+ag_fn nccl_allgather_ptr() { return g_nccl.allgather; }
+}  // namespace tci

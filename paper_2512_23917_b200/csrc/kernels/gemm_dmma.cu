@@ -46,7 +46,10 @@
 namespace tci {
 namespace {
 
-enum Algo { kReal = 0, kCplx3M = 1, kCplx4M = 2 };
+enum Algo { kReal = 0, kCplx3M = 1, kCplx4M = 2, kCplx3MS = 3 };
+// kCplx3MS: 3M with the (re+im) sums formed once per CTA per stage into a
+// shared-memory sum plane (each thread sums the chunks it loaded), instead
+// of once per warp per fragment in registers
 
 template <int ALGO, int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool A_K_, bool B_K_,
           int VEC_, int MODE_ = 0>
@@ -67,7 +70,12 @@ struct Cfg {
   static constexpr int SB = B_K ? (BK + PADK) : (BN + PADMN);
   static constexpr int A_STAGE = A_K ? BM * SA : BK * SA;   // elements
   static constexpr int B_STAGE = B_K ? BN * SB : BK * SB;
-  static constexpr int SMEM_PIPE = STAGES * (A_STAGE + B_STAGE) * ESZ;
+  static constexpr bool kSumPlane = ALGO == kCplx3MS;
+  static constexpr int SPA = A_K ? (BK + 4) : (BM + 4);     // sum-plane pitches (doubles)
+  static constexpr int SPB = B_K ? (BK + 4) : (BN + 4);
+  static constexpr int A_SUM = kSumPlane ? (A_K ? BM * SPA : BK * SPA) : 0;   // doubles per stage
+  static constexpr int B_SUM = kSumPlane ? (B_K ? BN * SPB : BK * SPB) : 0;
+  static constexpr int SMEM_PIPE = STAGES * (A_STAGE + B_STAGE) * ESZ + STAGES * (A_SUM + B_SUM) * 8;
   static constexpr int SMEM_EPI = MODE == 1 ? BM * (BN + 1) * 8 : 0;   // staged C tile (TEBD)
   static constexpr int SMEM = SMEM_PIPE > SMEM_EPI ? SMEM_PIPE : SMEM_EPI;
   static constexpr int MI = WM / 8, NJ = WN / 8;
@@ -99,6 +107,27 @@ struct Loader {
   int kidx[PER_T];            // k index (within the tile) of the chunk's first element
   int nvalid_mn[PER_T];       // K-major: row valid (0/1); MN-major: valid elements in the chunk
   int64_t kstep;              // bytes to advance per K tile
+  uint32_t sumoff[PER_T];     // element offset of this chunk in the stage's sum plane
+
+  __device__ __forceinline__ void set_sum_offsets() {
+    if constexpr (C::kSumPlane) {
+      constexpr int SP = IS_A ? C::SPA : C::SPB;
+      const int t = threadIdx.x;
+      const int col = (t % CPR) * C::CHUNK;
+#pragma unroll
+      for (int i = 0; i < PER_T; i++) sumoff[i] = (uint32_t)((t / CPR + i * RSTEP) * SP + col);
+    }
+  }
+  // (re + im) of this thread's landed chunks of one stage into its sum plane
+  __device__ __forceinline__ void make_sums(const char *stage, double *sums) const {
+    if constexpr (C::kSumPlane) {
+#pragma unroll
+      for (int i = 0; i < PER_T; i++) {
+        const double2 v = *reinterpret_cast<const double2 *>(stage + soff[i]);
+        sums[sumoff[i]] = TCI_LAB_SUM(v.x, v.y);
+      }
+    }
+  }
 
   // s_mn / s_k: element strides of the M (or N) and K legs
   __device__ __forceinline__ void init(const char *b, int64_t mn0, int64_t MN, int64_t s_mn,
@@ -187,15 +216,35 @@ struct Loader {
 template <class C>
 struct Frag {
   // complex 3M: (re, im, re+im) per fragment element; 4M: (re, im); real: 1
-  static constexpr int NV = C::kAlgo == kCplx3M ? 3 : (C::kCplx ? 2 : 1);
+  static constexpr int NV = (C::kAlgo == kCplx3M || C::kAlgo == kCplx3MS) ? 3 : (C::kCplx ? 2 : 1);
   double a[C::MI][NV], b[C::NJ][NV];
 };
 
 template <class C>
 __device__ __forceinline__ void load_frag(Frag<C> &f, const char *sA, const char *sB, int kk,
-                                          int wm0, int wn0, int lr, int lc) {
+                                          int wm0, int wn0, int lr, int lc,
+                                          const double *sumA = nullptr, const double *sumB = nullptr) {
   const int k = kk * 4 + lc;
-  if constexpr (C::kCplx) {
+  if constexpr (C::kSumPlane) {
+    const double2 *A = reinterpret_cast<const double2 *>(sA);
+    const double2 *B = reinterpret_cast<const double2 *>(sB);
+#pragma unroll
+    for (int i = 0; i < C::MI; i++) {
+      const int m = wm0 + i * 8 + lr;
+      const double2 v = C::A_K ? A[m * C::SA + k] : A[k * C::SA + m];
+      f.a[i][0] = v.x;
+      f.a[i][1] = v.y;
+      f.a[i][2] = C::A_K ? sumA[m * C::SPA + k] : sumA[k * C::SPA + m];
+    }
+#pragma unroll
+    for (int j = 0; j < C::NJ; j++) {
+      const int n = wn0 + j * 8 + lr;
+      const double2 v = C::B_K ? B[n * C::SB + k] : B[k * C::SB + n];
+      f.b[j][0] = v.x;
+      f.b[j][1] = v.y;
+      f.b[j][2] = C::B_K ? sumB[n * C::SPB + k] : sumB[k * C::SPB + n];
+    }
+  } else if constexpr (C::kCplx) {
     const double2 *A = reinterpret_cast<const double2 *>(sA);
     const double2 *B = reinterpret_cast<const double2 *>(sB);
 #pragma unroll
@@ -232,7 +281,7 @@ __device__ __forceinline__ void load_frag(Frag<C> &f, const char *sA, const char
 
 template <class C>
 struct Acc {
-  static constexpr int NS = C::kAlgo == kCplx3M ? 3 : (C::kCplx ? 2 : 1);
+  static constexpr int NS = (C::kAlgo == kCplx3M || C::kAlgo == kCplx3MS) ? 3 : (C::kCplx ? 2 : 1);
   double c[NS][C::MI][C::NJ][2];
 };
 
@@ -242,7 +291,7 @@ __device__ __forceinline__ void mma_step(Acc<C> &acc, const Frag<C> &f) {
   for (int i = 0; i < C::MI; i++)
 #pragma unroll
     for (int j = 0; j < C::NJ; j++) {
-      if constexpr (C::kAlgo == kCplx3M) {
+      if constexpr (C::kAlgo == kCplx3M || C::kAlgo == kCplx3MS) {
         dmma884(acc.c[0][i][j], f.a[i][0], f.b[j][0]);   // P = Ar.Br
         dmma884(acc.c[1][i][j], f.a[i][1], f.b[j][1]);   // Q = Ai.Bi
         dmma884(acc.c[2][i][j], f.a[i][2], f.b[j][2]);   // S = (Ar+Ai).(Br+Bi)
@@ -263,6 +312,8 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
   extern __shared__ __align__(128) char smem[];
   char *sA0 = smem;
   char *sB0 = smem + C::STAGES * C::A_STAGE * C::ESZ;
+  double *sumA0 = reinterpret_cast<double *>(smem + C::STAGES * (C::A_STAGE + C::B_STAGE) * C::ESZ);
+  double *sumB0 = sumA0 + C::STAGES * C::A_SUM;
 
   // grouped rasterization: GROUP M-tiles walk the N-tiles together so the
   // B panels they share stay in L2
@@ -304,6 +355,9 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
     else lb.init(Bb, n0, p.N, 1, p.b_sk);
   }
 
+  la.set_sum_offsets();
+  lb.set_sum_offsets();
+
   Acc<C> acc;
 #pragma unroll
   for (int s = 0; s < Acc<C>::NS; s++)
@@ -323,22 +377,30 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
     cp_async_commit();
   }
   cp_async_wait<C::STAGES - 2>();
+  la.make_sums(sA0, sumA0);
+  lb.make_sums(sB0, sumB0);
   __syncthreads();
 
   Frag<C> fr[2];
-  load_frag<C>(fr[0], sA0, sB0, 0, wm0, wn0, lr, lc);
+  load_frag<C>(fr[0], sA0, sB0, 0, wm0, wn0, lr, lc, sumA0, sumB0);
 
   for (int kt = 0; kt < KT; kt++) {
     const int st = kt % C::STAGES;
     const char *sA = sA0 + st * C::A_STAGE * C::ESZ;
     const char *sB = sB0 + st * C::B_STAGE * C::ESZ;
+    const double *smA = sumA0 + st * C::A_SUM, *smB = sumB0 + st * C::B_SUM;
 #pragma unroll
     for (int kk = 0; kk < C::KK; kk++) {
       if (kk < C::KK - 1) {
-        load_frag<C>(fr[(kk + 1) & 1], sA, sB, kk + 1, wm0, wn0, lr, lc);
+        load_frag<C>(fr[(kk + 1) & 1], sA, sB, kk + 1, wm0, wn0, lr, lc, smA, smB);
       } else {
         // stage kt+1 must have landed; stage kt-1 is free for reuse
         cp_async_wait<C::STAGES - 3>();
+        if (kt + 1 < KT) {
+          const int s1 = (kt + 1) % C::STAGES;
+          la.make_sums(sA0 + s1 * C::A_STAGE * C::ESZ, sumA0 + s1 * C::A_SUM);
+          lb.make_sums(sB0 + s1 * C::B_STAGE * C::ESZ, sumB0 + s1 * C::B_SUM);
+        }
         __syncthreads();
         const int nk = kt + C::STAGES - 1;
         if (nk < KT) {
@@ -350,7 +412,8 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
         if (kt + 1 < KT) {
           const int s1 = (kt + 1) % C::STAGES;
           load_frag<C>(fr[(kk + 1) & 1], sA0 + s1 * C::A_STAGE * C::ESZ,
-                       sB0 + s1 * C::B_STAGE * C::ESZ, 0, wm0, wn0, lr, lc);
+                       sB0 + s1 * C::B_STAGE * C::ESZ, 0, wm0, wn0, lr, lc, sumA0 + s1 * C::A_SUM,
+                       sumB0 + s1 * C::B_SUM);
         }
       }
       mma_step<C>(acc, fr[kk & 1]);
@@ -423,7 +486,7 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
       if constexpr (C::kCplx) {
         double2 *cp = reinterpret_cast<double2 *>(Cb) + m * c_sm + n;
         double re0, im0, re1, im1;
-        if constexpr (C::kAlgo == kCplx3M) {
+        if constexpr (C::kAlgo == kCplx3M || C::kAlgo == kCplx3MS) {
           const double P0 = acc.c[0][i][j][0], Q0 = acc.c[1][i][j][0], S0 = acc.c[2][i][j][0];
           const double P1 = acc.c[0][i][j][1], Q1 = acc.c[1][i][j][1], S1 = acc.c[2][i][j][1];
           re0 = P0 - Q0;

@@ -33,6 +33,8 @@ struct tci_ctx_s {
   // plan cache: key -> serialized plan decision (see contract.cpp)
   std::unordered_map<std::string, std::vector<int64_t>> plan_cache;
   int64_t plan_hits, plan_misses;
+  void *dev_scratch;    // reductions (vec.cu): allocated once at creation
+  void *host_scratch;   // pinned, reduction results
 };
 
 struct tci_tensor_s {
@@ -113,6 +115,17 @@ tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g);
 tci_status_t run_skinny(tci_ctx_s *ctx, const SkinnyProblem &p);
 tci_status_t run_permute(tci_ctx_s *ctx, const PermuteProblem &p);
 tci_status_t run_tebd(tci_ctx_s *ctx, const TebdProblem &t);
+
+// Vector ops and Lanczos (lanczos.cpp)
+tci_status_t vec_norm(tci_ctx_s *ctx, const View &a, double *nrm);
+tci_status_t vec_inner(tci_ctx_s *ctx, const View &a, const View &b, int conj_a, double out[2]);
+tci_status_t vec_lincomb(tci_ctx_s *ctx, int m, const View *ins, const double *coefs, const View &out);
+tci_status_t lanczos_bytes(tci_ctx_s *ctx, const View &L, const View &W1, const View &W2, const View &R,
+                           const View &psi, int max_iter, size_t *bytes, size_t *heff_b);
+tci_status_t lanczos_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View &W2, const View &R,
+                          const View &psi, int max_iter, double tol, double *energy, int *iters);
+typedef int (*ag_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
+ag_fn nccl_allgather_ptr();
 
 // Chains (chains.cpp)
 tci_status_t heff_plan_bytes(tci_dtype_t dt, int64_t chi_l, int64_t chi_lo, int64_t chi_r,

@@ -132,6 +132,20 @@ struct MpsChain {
 };
 cudaError_t launch_mps_overlap(const MpsChain &ch, cudaStream_t s, int64_t *launches);
 
+// ---------------------------------------------------------------------------
+// Vector kernels (vec.cu) for norm / inner / scale / linear_combine and the
+// Lanczos driver. f64 data; complex = (re, im) pairs.
+// ---------------------------------------------------------------------------
+constexpr int kMaxLC = 8;
+// mode 0: out[0] = sum a_i^2 over n_reals; mode 1: complex inner product
+// sum conj?(a) b (n_reals = 2 x elements) -> out[0..1]; mode 2: real sum a b.
+cudaError_t launch_reduce(int mode, const double *a, const double *b, int64_t n_reals, int conj_a,
+                          double *part, double *out, cudaStream_t s, int64_t *launches);
+size_t reduce_scratch_bytes();
+// out[i] = sum_j (cr_j + i ci_j) in_j[i], m <= kMaxLC; out may alias an input
+cudaError_t launch_lincomb(bool cplx, const double *const *in, const double *cr, const double *ci, int m,
+                           double *out, int64_t n, cudaStream_t s, int64_t *launches);
+
 // Plain device copy (aliasing fallback) and elementwise helpers.
 cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s, int64_t *launches);
 

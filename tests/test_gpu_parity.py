@@ -497,3 +497,88 @@ def test_sharded_heff_single_rank_path(ctx):
     out = sh.apply(inp["psi"])
     ref = ctx.heff_apply(inp["L"], inp["W1"], inp["W2"], inp["R"], inp["psi"])
     assert torch.equal(out, ref)
+
+
+# ---------------------------------------------------------------------------
+# vector functions and the Lanczos driver (8(f1))
+# ---------------------------------------------------------------------------
+
+def test_vector_functions(ctx, oracle_mod):
+    for dt in ("r64", "c128"):
+        xs = [synth.random_tensor((33, 2, 2, 47), dt, 450 + i, 1) for i in range(11)]
+        dx = [dev(x) for x in xs]
+        n1 = ctx.norm(dx[0])
+        assert abs(n1 - oracle_mod.norm(xs[0].numpy())) <= 1e-14 * n1
+        assert ctx.norm(dx[0]) == n1                        # deterministic reduction: bitwise
+        ip = ctx.inner(dx[1], dx[2])
+        ref = oracle_mod.inner(xs[1].numpy(), xs[2].numpy())
+        assert abs(ip - ref) <= 1e-13 * oracle_mod.norm(xs[1].numpy()) * oracle_mod.norm(xs[2].numpy())
+        coefs = [(0.5 - 0.1 * i) + (0.3j * i if dt == "c128" else 0) for i in range(11)]   # 11 > 8: chunked
+        lc = ctx.linear_combine(dx, coefs)
+        assert rel_frob(host(lc), oracle_mod.linear_combine([x.numpy() for x in xs], coefs)) <= 1e-14
+        sc = ctx.scale(dx[3], -2.0)
+        assert torch.equal(sc.cpu(), -2.0 * xs[3])
+        ctx.linear_combine([dx[4], dx[5]], None, out=dx[4])   # aliasing out == input, default coefs
+        assert torch.equal(dx[4].cpu(), xs[4] + xs[5])
+    e = dev(torch.eye(3, dtype=torch.float64))
+    assert ctx.norm(e) == float(np.sqrt(3.0))
+
+
+def _env_left(L, A, W):
+    # L'[a',w',b'] = sum L[a,w,b] A[a,s,a'] W[w,w',s,t] conj(A[b,t,b'])
+    return np.einsum("awb,asx,wvst,bty->xvy", L, A, W, np.conj(A), optimize=True)
+
+
+def _env_right(R, B, W):
+    # R[c,x,e] = sum B[c,s,c'] W[x,x',s,t] conj(B[e,t,e']) R'[c',x',e']
+    return np.einsum("csd,xzst,ety,dzy->cxe", B, W, np.conj(B), R, optimize=True)
+
+
+def _heisenberg_envs(chi_sites, seed):
+    W, lb, rb = synth.heisenberg_mpo()
+    L = synth.boundary_env(5, lb)
+    bonds = [1] + chi_sites
+    for i in range(len(chi_sites)):
+        A = synth.random_np((bonds[i], 2, bonds[i + 1]), "c128", seed, 200 + i)
+        L = _env_left(L, A, W)
+    R = synth.boundary_env(5, rb)
+    for i in range(len(chi_sites)):
+        B = synth.random_np((bonds[i + 1], 2, bonds[i]), "c128", seed, 300 + i)
+        R = _env_right(R, B, W)
+    return L, W, R
+
+
+@pytest.mark.parametrize("chi_sites", [[2, 4], [2, 4, 8, 16]])
+def test_lanczos_vs_dense_eigvalsh(ctx, oracle_mod, chi_sites):
+    L, W, R = _heisenberg_envs(chi_sites, 460 + len(chi_sites))
+    chi = chi_sites[-1]
+    H = oracle_mod.heff_dense(L, W, W, R, (chi, 2, 2, chi))
+    assert np.max(np.abs(H - H.conj().T)) < 1e-12 * np.max(np.abs(H))       # Hermitian by construction
+    e_ref = np.linalg.eigvalsh((H + H.conj().T) / 2)[0]
+    psi = dev(synth.random_tensor((chi, 2, 2, chi), "c128", 470, 2))
+    e, it = ctx.heff_lanczos(dev(L), dev(W), dev(W), dev(R), psi, max_iter=min(200, H.shape[0]), tol=1e-14)
+    assert abs(e - e_ref) <= 1e-9 * max(1.0, abs(e_ref)), (e, e_ref, it)
+    # returned Ritz vector: normalised and an eigenvector (residual small)
+    assert abs(ctx.norm(psi) - 1.0) < 1e-12
+    hv = host(ctx.heff_apply(dev(L), dev(W), dev(W), dev(R), psi)).reshape(-1)
+    v = host(psi).reshape(-1)
+    assert np.linalg.norm(hv - e * v) <= 1e-6 * max(1.0, abs(e))
+
+
+def test_lanczos_closed_forms(ctx):
+    g = __import__("conftest").golden("closed_forms.json")
+    W, lb, rb = synth.heisenberg_mpo()
+    L, R = dev(synth.boundary_env(5, lb)), dev(synth.boundary_env(5, rb))
+    psi = dev(synth.random_tensor((1, 2, 2, 1), "c128", 480, 2))
+    e, _ = ctx.heff_lanczos(L, dev(W), dev(W), R, psi, max_iter=10, tol=1e-15)
+    assert abs(e - g["heisenberg_two_site"]["eigenvalues"][0]) < 1e-13
+    # Hubbard: start in the N = 2 sector (H conserves N) -> closed-form E0
+    h = g["hubbard_two_site_N2"]
+    W, lb, rb = synth.hubbard_mpo(h["t"], h["U"])
+    L, R = dev(synth.boundary_env(6, lb)), dev(synth.boundary_env(6, rb))
+    nloc = np.array([0, 1, 1, 2])
+    start = synth.random_np((1, 4, 4, 1), "c128", 481, 2)
+    start[0][(nloc[:, None] + nloc[None, :]) != 2] = 0
+    psi = dev(start)
+    e, _ = ctx.heff_lanczos(L, dev(W), dev(W), R, psi, max_iter=16, tol=1e-15)
+    assert abs(e - h["E0"]) < 1e-12

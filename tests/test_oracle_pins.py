@@ -483,3 +483,23 @@ def test_generator_matches_reference():
         # chunking does not change values
         d2 = synth.uniform_draws(seed, tid, 2000, chunk=77).numpy()
         assert np.array_equal(d, d2)
+
+
+def test_vector_function_examples(oracle_mod):
+    """App. C examples: norm(eye(3)) = sqrt(3); normalize gives
+    norm 1; scale(eye(3), 3)[2,2] = 3 and scale(., -2) = -6
+    (P:1796-1806); linear_combine with default coefficients is the plain sum
+    (P:1993)."""
+    g = golden("paper_examples.json")
+    assert oracle_mod.norm(np.eye(3)) == g["frobenius_norm_eye3"]["value"]
+    a = rnd((3, 4, 2), 120)
+    assert abs(oracle_mod.norm(a / oracle_mod.norm(a)) - 1.0) < 1e-15
+    e3 = oracle_mod.scale(np.eye(3), 3.0)
+    assert e3[2, 2] == 3.0 and oracle_mod.scale(e3, -2.0)[2, 2] == -6.0
+    b, c = rnd((3, 4, 2), 121), rnd((3, 4, 2), 122)
+    assert np.array_equal(oracle_mod.linear_combine([a, b, c]), a + b + c)
+    lc = oracle_mod.linear_combine([a, b, c], [1.0, 2.0, 3.0])
+    assert np.max(np.abs(lc - (a + 2 * b + 3 * c))) < 1e-15
+    z = rnd((5, 7), 123, 1, True)
+    assert abs(oracle_mod.inner(z, z) - oracle_mod.norm(z) ** 2) < 1e-13
+    assert abs(oracle_mod.inner(z, z, conj_a=False) - complex(oracle_mod.contract(z, "ij", z, "ij", ""))) < 1e-13

@@ -42,14 +42,14 @@ int main(int argc, char** argv) {
   p.A = A; p.a_sm = K; p.a_sk = 1; p.B = B; p.b_sk = N; p.b_sn = 1; p.C = Cm; p.c_sm = N;
   const double F = 8.0 * M * N * K;
   auto rep = [&](const char* name, double t) { printf("%-40s %8.2f ms  %6.2f TF/s (alg)\n", name, t * 1e3, F / t / 1e12); };
-  rep("3M 64x64 bk8 w32x16 s4", time_cfg<Cfg<kCplx3M, 64, 64, 8, 32, 16, 4, true, false, 1>>(p, 3));
-  rep("3M 64x64 bk8 w32x16 s3", time_cfg<Cfg<kCplx3M, 64, 64, 8, 32, 16, 3, true, false, 1>>(p, 3));
-  rep("3M 64x64 bk8 w32x16 s6", time_cfg<Cfg<kCplx3M, 64, 64, 8, 32, 16, 6, true, false, 1>>(p, 3));
-  rep("3M 64x64 bk4 w32x16 s6", time_cfg<Cfg<kCplx3M, 64, 64, 4, 32, 16, 6, true, false, 1>>(p, 3));
-  rep("3M 64x32 bk8 w32x16 s4 (4 warps)", time_cfg<Cfg<kCplx3M, 64, 32, 8, 32, 16, 4, true, false, 1>>(p, 3));
-  rep("3M 32x64 bk8 w32x16 s4 (4 warps)", time_cfg<Cfg<kCplx3M, 32, 64, 8, 16, 32, 4, true, false, 1>>(p, 3));
-  rep("3M 64x64 bk8 w16x32 s4", time_cfg<Cfg<kCplx3M, 64, 64, 8, 16, 32, 4, true, false, 1>>(p, 3));
-  rep("4M 64x64 bk8 w32x16 s4", time_cfg<Cfg<kCplx4M, 64, 64, 8, 32, 16, 4, true, false, 1>>(p, 3));
-  rep("4M 64x128 bk8 w32x32 s4", time_cfg<Cfg<kCplx4M, 64, 128, 8, 32, 32, 4, true, false, 1>>(p, 3));
+  rep("3M  64x64 bk8 w32x16 s6", time_cfg<Cfg<kCplx3M, 64, 64, 8, 32, 16, 6, true, false, 1>>(p, 3));
+  rep("3MS 64x64 bk8 w32x16 s6", time_cfg<Cfg<kCplx3MS, 64, 64, 8, 32, 16, 6, true, false, 1>>(p, 3));
+  rep("3MS 64x64 bk16 w32x16 s4", time_cfg<Cfg<kCplx3MS, 64, 64, 16, 32, 16, 4, true, false, 1>>(p, 3));
+  rep("3MS 64x64 bk8 w32x16 s5", time_cfg<Cfg<kCplx3MS, 64, 64, 8, 32, 16, 5, true, false, 1>>(p, 3));
+  rep("3MS 64x64 bk8 w16x32 s6", time_cfg<Cfg<kCplx3MS, 64, 64, 8, 16, 32, 6, true, false, 1>>(p, 3));
+  p.A = A; p.a_sm = 1; p.a_sk = M;   // GEMM1-like: A M-major
+  rep("[A M-major] 3M  bk8 s6", time_cfg<Cfg<kCplx3M, 64, 64, 8, 32, 16, 6, false, false, 1>>(p, 3));
+  rep("[A M-major] 3MS bk8 s6", time_cfg<Cfg<kCplx3MS, 64, 64, 8, 32, 16, 6, false, false, 1>>(p, 3));
+  rep("[A M-major] 3MS bk16 s4", time_cfg<Cfg<kCplx3MS, 64, 64, 16, 32, 16, 4, false, false, 1>>(p, 3));
   return 0;
 }

@@ -120,7 +120,8 @@ def main():
             try:
                 rd = float(d["dram__bytes_read.sum"].split()[0]) * (1e9 if "Gbyte" in d["dram__bytes_read.sum"] else 1e6 if "Mbyte" in d["dram__bytes_read.sum"] else 1)
                 wr = float(d["dram__bytes_write.sum"].split()[0]) * (1e9 if "Gbyte" in d["dram__bytes_write.sum"] else 1e6 if "Mbyte" in d["dram__bytes_write.sum"] else 1)
-                tr.append(rd + wr)
+                if rd == rd and wr == wr:   # skip NaN captures
+                    tr.append(rd + wr)
             except (KeyError, ValueError):
                 pass
         if tr:

@@ -240,6 +240,11 @@ def run_tci(args):
     torch.cuda.synchronize()
 
     ctx = tci.Context(local, stream)
+    if args.algo:
+        ctx.set_gemm_algorithm({"dmma3m": tci.TCI_GEMM_DMMA_3M, "dmma4m": tci.TCI_GEMM_DMMA_4M,
+                                "ozaki": tci.TCI_GEMM_OZAKI_INT8}[args.algo])
+    ALGOS = {"dmma3m": tci.TCI_GEMM_DMMA_3M, "dmma4m": tci.TCI_GEMM_DMMA_4M, "ozaki": tci.TCI_GEMM_OZAKI_INT8}
+    algo = {0: "dmma3m", 1: "dmma4m", 2: "ozaki"}[tci.tci_get_gemm_algorithm(ctx.handle)]
     if ws > 1:
         import torch.distributed as dist
         obj = [tci.tci_comm_unique_id() if rank == 0 else None]
@@ -278,7 +283,8 @@ def run_tci(args):
     t_step = e0.elapsed_time(e1) / 1e3 / args.steps
     launches = ctx.launch_count() - n0
     prof = {k: tci.tci_profile_query(ctx.handle, v) for k, v in
-            (("gemm", tci.PROF_GEMM), ("skinny", tci.PROF_SKINNY), ("permute", tci.PROF_PERMUTE))}
+            (("gemm", tci.PROF_GEMM), ("skinny", tci.PROF_SKINNY), ("permute", tci.PROF_PERMUTE),
+             ("int8_gemm", tci.PROF_I8))}
     tci.tci_profile_enable(ctx.handle, False)
     clocks = sampler.stop() if sampler else None
     if ws > 1:
@@ -290,6 +296,38 @@ def run_tci(args):
         dist.all_reduce(ln)
         launches = int(ln.item())
     value = F / t_step / 1e12
+
+    # ---- the other complex GEMM algorithm on the same inputs (same timing rules) ----
+    alt = None
+    if args.alt and args.alt != "none" and args.alt != algo:
+        ctx.set_gemm_algorithm(ALGOS[args.alt])
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        ka = max(1, min(args.steps, 3))
+        for _ in range(ka):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ta = e0.elapsed_time(e1) / 1e3 / ka
+        if ws > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([ta], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ta = float(tt.item())
+        alt_out = out.clone() if ws == 1 else None
+        alt = {"algorithm": args.alt, "value": F / ta / 1e12, "ms_per_step": ta * 1e3, "steps": ka,
+               "pct_fp64_tc_peak": F / ta / 1e12 / FP64_PEAK_TFLOPS * 100}
+        ctx.set_gemm_algorithm(ALGOS[algo])
+        step()
+        torch.cuda.synchronize()
+        if alt_out is not None:
+            diff = (out - alt_out).abs().pow(2).sum().sqrt() / alt_out.abs().pow(2).sum().sqrt()
+            alt["rel_frob_vs_main"] = float(diff.item())
+        del alt_out
 
     # ---- end to end through the C ABI with pinned host buffers ----
     e2e = None
@@ -339,19 +377,35 @@ def run_tci(args):
     achieved = gemm_flops_per_launch / gemm_avg_s / 1e12 if g["launches"] else None
     traffic = traffic_from_profiles(name)
     sk = prof["skinny"]
-    roofline = {
-        "bound": "tensor", "kernel": "gemm_dmma_kernel (L.psi and T3.R GEMMs, DMMA.8x8x4)",
-        "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-        "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": traffic,
-        "peak_source": FP64_PEAK_SOURCE,
-        "flops_per_launch": gemm_flops_per_launch, "launches": g["launches"],
-        "gemm_share_of_step": g["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
-        "secondary": {
-            "kernel": "skinny_kernel (MPO pass)", "bound": "hbm",
-            "achieved": (sk["bytes"] / (sk["ms"] / 1e3) / 1e9) if sk["launches"] else None,
-            "peak": peaks.get("hbm_gbs"), "unit": "GB/s", "peak_source": peak_src,
-            "share_of_step": sk["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
-        },
+    i8 = prof["int8_gemm"]
+    if algo == "ozaki" and i8["launches"]:
+        # dominant kernel: the CUTLASS sm100 INT8 tcgen05 GEMM (batched residue products)
+        i8_peak = peaks.get("bf16_tflops", 1646.4) * 2.0   # measured bf16 x nominal int8/bf16 (4.5/2.25)
+        i8_ach = i8["flops"] / (i8["ms"] / 1e3) / 1e12
+        roofline = {
+            "bound": "tensor", "kernel": "CUTLASS sm100 INT8 tcgen05 GEMM (Ozaki-II residue products; UTCIMMA)",
+            "achieved": i8_ach, "peak": i8_peak, "unit": "TOPS", "frac": i8_ach / i8_peak,
+            "traffic": traffic_from_profiles(name + "_ozaki"),
+            "peak_source": f"MEASURED_PEAKS.json bf16_tflops x 2 (nominal int8/bf16 = 4.5/2.25 PFLOP/s)",
+            "ops_per_launch": i8["flops"] / i8["launches"], "launches": i8["launches"],
+            "share_of_step": i8["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
+            "ozaki_gemm_fp64_equivalent_tflops": achieved,
+            "ozaki_gemm_share_of_step": g["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
+        }
+    else:
+        roofline = {
+            "bound": "tensor", "kernel": "gemm_dmma_kernel (L.psi and T3.R GEMMs, DMMA.8x8x4)",
+            "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": traffic,
+            "peak_source": FP64_PEAK_SOURCE,
+            "flops_per_launch": gemm_flops_per_launch, "launches": g["launches"],
+            "gemm_share_of_step": g["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
+        }
+    roofline["secondary"] = {
+        "kernel": "skinny_kernel (MPO pass)", "bound": "hbm",
+        "achieved": (sk["bytes"] / (sk["ms"] / 1e3) / 1e9) if sk["launches"] else None,
+        "peak": peaks.get("hbm_gbs"), "unit": "GB/s", "peak_source": peak_src,
+        "share_of_step": sk["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
     }
 
     cpu = None
@@ -364,9 +418,13 @@ def run_tci(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "c128" if dt == "c128" else "f64",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": ("c128 (fp64-accurate: Ozaki-II exact INT8 tensor-core residue GEMMs + CRT)"
+                  if algo == "ozaki" else ("c128" if dt == "c128" else "f64")),
+        "alt": alt,
         "data": "synthetic (seeded counter-based generator; exact model MPO as W1=W2)",
         "config": {"workload": name, "chi": chi, "d": d, "D": D, "dtype": dt, "model": cfg["model"],
+                   "gemm_algorithm": algo,
                    "parallelism": f"output bond b sharded over {ws} rank(s); NCCL all-gather of out per step"
                    if ws > 1 else "single GPU",
                    "l2": "inputs larger than L2 (L, psi, R >= 1 GB each): no flush"},
@@ -392,6 +450,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-rows", type=int, default=4)
+    ap.add_argument("--algo", choices=["dmma3m", "dmma4m", "ozaki"], default="ozaki",
+                    help="complex128 GEMM algorithm of the timed apply (DESIGN.md §12)")
+    ap.add_argument("--alt", default="dmma3m",
+                    help="also time this algorithm (reported under 'alt'; 'none' to skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -116,6 +116,22 @@ TCI_API tci_status_t tci_synchronize(tci_ctx_t ctx);
  * ("" if none). Static thread-local storage; valid until the next call. */
 TCI_API const char *tci_last_error(void);
 
+/* complex128 GEMM algorithm of a context:
+ *  TCI_GEMM_DMMA_3M (default): FP64 tensor cores (DMMA), Gauss 3-multiplication
+ *    complex product;
+ *  TCI_GEMM_DMMA_4M: DMMA, textbook 4-multiplication product;
+ *  TCI_GEMM_OZAKI_INT8: Ozaki-II integer-modular emulation on the INT8 tcgen05
+ *    tensor cores (row/column scaling to >= 46-bit integers, exact residue
+ *    GEMMs, exact CRT), used for GEMMs of >= 4e9 complex MACs; needs more
+ *    scratch (the *_workspace_size queries account for it).
+ * The initial value comes from TCI_ZGEMM_ALGO = 3m | 4m | ozaki (read at
+ * context creation). Setting it synchronizes the context stream. */
+#define TCI_GEMM_DMMA_3M 0
+#define TCI_GEMM_DMMA_4M 1
+#define TCI_GEMM_OZAKI_INT8 2
+TCI_API tci_status_t tci_set_gemm_algorithm(tci_ctx_t ctx, int algo);
+TCI_API tci_status_t tci_get_gemm_algorithm(tci_ctx_t ctx, int *algo);
+
 /* Attach caller-owned device scratch memory of `bytes` bytes (256-byte
  * aligned pointer). Replaces any previous attachment; NULL/0 detaches. Calls
  * that need scratch (tci_contract with permutes or aliasing, tci_heff_apply)
@@ -342,7 +358,9 @@ TCI_API tci_status_t tci_launch_count(tci_ctx_t ctx, int64_t *count);
  * Enabling (or disabling) synchronizes the stream and clears the records. */
 TCI_API tci_status_t tci_profile_enable(tci_ctx_t ctx, int on);
 
-/* Sum over recorded launches of `kind` (0 GEMM, 1 skinny, 2 permute):
+/* Sum over recorded launches of `kind` (0 GEMM, 1 skinny, 2 permute,
+ * 3 the INT8 tensor-core GEMMs inside Ozaki GEMMs -- "flops" = executed int8
+ * ops, 2 per MAC):
  * launch count, total event time in ms, algorithmic flops and bytes.
  * Synchronizes the context stream. */
 TCI_API tci_status_t tci_profile_query(tci_ctx_t ctx, int kind, int64_t *launches, double *ms,

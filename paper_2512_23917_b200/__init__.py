@@ -44,7 +44,7 @@ EXPORTED = [
     "tci_tebd_theta", "tci_comm_init", "tci_comm_unique_id", "tci_allgather",
     "tci_launch_count", "tci_heff_plan_tree", "tci_profile_enable", "tci_profile_query",
     "tci_mps_overlap", "tci_norm", "tci_normalize", "tci_scale", "tci_linear_combine", "tci_inner",
-    "tci_lanczos_workspace_size", "tci_heff_lanczos",
+    "tci_lanczos_workspace_size", "tci_heff_lanczos", "tci_set_gemm_algorithm", "tci_get_gemm_algorithm",
 ]
 
 
@@ -86,6 +86,8 @@ _sig = {
     "tci_allgather": ([_vp, _vp, _vp], ctypes.c_int),
     "tci_launch_count": ([_vp, _i64p], ctypes.c_int),
     "tci_profile_enable": ([_vp, ctypes.c_int], ctypes.c_int),
+    "tci_set_gemm_algorithm": ([_vp, ctypes.c_int], ctypes.c_int),
+    "tci_get_gemm_algorithm": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_norm": ([_vp, _vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tci_normalize": ([_vp, _vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tci_scale": ([_vp, _vp, ctypes.c_double, ctypes.c_double, _vp], ctypes.c_int),
@@ -273,6 +275,19 @@ def tci_mps_overlap(ctx: int, bra: Sequence[int], ket: Sequence[int], out: int) 
     _ok(_lib.tci_mps_overlap(_vp(ctx), n, b, k, _vp(out)), "tci_mps_overlap")
 
 
+TCI_GEMM_DMMA_3M, TCI_GEMM_DMMA_4M, TCI_GEMM_OZAKI_INT8 = 0, 1, 2
+
+
+def tci_set_gemm_algorithm(ctx: int, algo: int) -> None:
+    _ok(_lib.tci_set_gemm_algorithm(_vp(ctx), int(algo)), "tci_set_gemm_algorithm")
+
+
+def tci_get_gemm_algorithm(ctx: int) -> int:
+    x = ctypes.c_int()
+    _ok(_lib.tci_get_gemm_algorithm(_vp(ctx), ctypes.byref(x)), "tci_get_gemm_algorithm")
+    return x.value
+
+
 def tci_norm(ctx: int, t: int) -> float:
     x = ctypes.c_double()
     _ok(_lib.tci_norm(_vp(ctx), _vp(t), ctypes.byref(x)), "tci_norm")
@@ -325,7 +340,7 @@ def tci_heff_lanczos(ctx: int, L: int, W1: int, W2: int, R: int, psi: int, max_i
     return e.value, it.value
 
 
-PROF_GEMM, PROF_SKINNY, PROF_PERMUTE = 0, 1, 2
+PROF_GEMM, PROF_SKINNY, PROF_PERMUTE, PROF_I8 = 0, 1, 2, 3
 
 
 def tci_profile_enable(ctx: int, on: bool) -> None:
@@ -453,6 +468,9 @@ class Context:
         tci_tebd_theta(self.handle, self.tensor(A), la, self.tensor(B), lb, self.tensor(U), lu,
                        self.tensor(out), lt)
         return out
+
+    def set_gemm_algorithm(self, algo: int):
+        tci_set_gemm_algorithm(self.handle, algo)
 
     def norm(self, x) -> float:
         return tci_norm(self.handle, self.tensor(x))

@@ -52,8 +52,12 @@ tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g) {
   const double es = (double)dtype_size(g.dtype);
   ProfScope ps(ctx, kProfGemm, (cplx ? 8.0 : 2.0) * g.M * g.N * g.K,
                es * ((double)g.M * g.K + (double)g.K * g.N + (double)g.M * g.N));
-  TCI_CUDA_CHECK(launch_gemm(g, ctx->stream, &ctx->launches));
+  OzProf pf{};
+  GemmProblem gg = g;
+  if (ctx->prof_on && g.zalgo == kZOzaki) gg.oz_prof = &pf;
+  TCI_CUDA_CHECK(launch_gemm(gg, ctx->stream, &ctx->launches));
   ps.done();
+  for (int i = 0; i < pf.n; i++) ctx->prof.push_back({kProfI8, pf.a[i], pf.b[i], pf.ops[i], 0.0});
   return TCI_OK;
 }
 
@@ -211,6 +215,11 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   c->rank = 0;
   c->plan_hits = c->plan_misses = 0;
   c->prof_on = false;
+  c->zgemm_algo = kZ3M;
+  if (const char *e = getenv("TCI_ZGEMM_ALGO")) {
+    if (!strcmp(e, "4m") || !strcmp(e, "4M")) c->zgemm_algo = kZ4M;
+    else if (!strcmp(e, "ozaki") || !strcmp(e, "OZAKI")) c->zgemm_algo = kZOzaki;
+  }
   c->dev_scratch = nullptr;
   c->host_scratch = nullptr;
   {
@@ -296,6 +305,22 @@ tci_status_t tci_workspace_attach(tci_ctx_t ctx, void *dev_ws, size_t bytes) {
   return TCI_OK;
 }
 
+tci_status_t tci_set_gemm_algorithm(tci_ctx_t ctx, int algo) {
+  CHECK(check_ctx(ctx));
+  if (algo != TCI_GEMM_DMMA_3M && algo != TCI_GEMM_DMMA_4M && algo != TCI_GEMM_OZAKI_INT8)
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "unknown GEMM algorithm %d", algo);
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));   // scratch layouts may change
+  ctx->zgemm_algo = algo;
+  return TCI_OK;
+}
+
+tci_status_t tci_get_gemm_algorithm(tci_ctx_t ctx, int *algo) {
+  CHECK(check_ctx(ctx));
+  if (!algo) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  *algo = ctx->zgemm_algo;
+  return TCI_OK;
+}
+
 tci_status_t tci_launch_count(tci_ctx_t ctx, int64_t *count) {
   CHECK(check_ctx(ctx));
   if (!count) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL count");
@@ -322,7 +347,7 @@ tci_status_t tci_profile_enable(tci_ctx_t ctx, int on) {
 tci_status_t tci_profile_query(tci_ctx_t ctx, int kind, int64_t *launches, double *ms, double *flops,
                                double *bytes) {
   CHECK(check_ctx(ctx));
-  if (kind < 0 || kind > 2) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "profile kind %d", kind);
+  if (kind < 0 || kind > 3) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "profile kind %d", kind);
   TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   int64_t n = 0;
   double t = 0, f = 0, by = 0;
@@ -531,7 +556,7 @@ tci_status_t tci_heff_workspace_size(tci_ctx_t ctx, tci_dtype_t dtype, int64_t c
                                      int64_t D2, size_t *bytes) {
   CHECK(check_ctx(ctx));
   if (!bytes) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
-  return heff_plan_bytes(dtype, chi_l, chi_lo, chi_r, chi_ro, d, D, D1, D2, bytes, nullptr);
+  return heff_plan_bytes(dtype, chi_l, chi_lo, chi_r, chi_ro, d, D, D1, D2, bytes, nullptr, ctx->zgemm_algo);
 }
 
 tci_status_t tci_heff_apply(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2,

@@ -146,9 +146,21 @@ HeffLayout heff_layout(const HeffDims &h, tci_dtype_t dt) {
 }
 }  // namespace
 
+// Ozaki scratch for the two chain GEMMs (0 when not used)
+static size_t heff_ozaki_bytes(tci_dtype_t dt, int zalgo, int64_t chi_l, int64_t chi_lo, int64_t chi_r,
+                               int64_t chi_ro, int64_t d, int64_t D, int64_t D2) {
+  if (dt != TCI_C128 || zalgo != kZOzaki) return 0;
+  size_t b = 0;
+  const int64_t M1 = D * chi_lo, N1 = d * d * chi_r, K1 = chi_l;
+  if (ozaki_worthwhile(M1, N1, K1)) b = std::max(b, ozaki_workspace_bytes(M1, N1, K1));
+  const int64_t M4 = chi_lo * d * d, N4 = chi_ro, K4 = chi_r * D2;
+  if (ozaki_worthwhile(M4, N4, K4)) b = std::max(b, ozaki_workspace_bytes(M4, N4, K4));
+  return b ? align_up(b) : 0;
+}
+
 tci_status_t heff_plan_bytes(tci_dtype_t dt, int64_t chi_l, int64_t chi_lo, int64_t chi_r,
                              int64_t chi_ro, int64_t d, int64_t D, int64_t D1, int64_t D2,
-                             size_t *bytes, bool *fused_w12) {
+                             size_t *bytes, bool *fused_w12, int zalgo) {
   if (dt != TCI_R64 && dt != TCI_C128) TCI_FAIL(TCI_ERR_UNSUPPORTED, "heff: dtype must be r64 or c128");
   if (chi_l < 1 || chi_lo < 1 || chi_r < 1 || chi_ro < 1 || d < 1 || D < 1 || D1 < 1 || D2 < 1)
     TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "heff: dimension < 1");
@@ -156,7 +168,7 @@ tci_status_t heff_plan_bytes(tci_dtype_t dt, int64_t chi_l, int64_t chi_lo, int6
   HeffLayout L = heff_layout(h, dt);
   const int64_t dims[NLAB] = {chi_l, D, chi_lo, d, d, chi_r, D1, d, D2, d, chi_ro};
   std::vector<Node> nd = plan_heff_tree(dims);
-  size_t need = L.total;
+  size_t need = L.total + heff_ozaki_bytes(dt, zalgo, chi_l, chi_lo, chi_r, chi_ro, d, D, D2);
   if (!is_standard_tree(nd)) {
     // generic tree executor: every intermediate + the largest contract scratch
     // (bounded by 3x the largest intermediate) -- computed in heff_exec
@@ -243,7 +255,7 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
   size_t need = 0;
   bool fused = false;
   tci_status_t st = heff_plan_bytes(dt, h.chi_l, h.chi_lo, h.chi_r, h.chi_ro, h.d, h.D, h.D1, h.D2,
-                                    &need, &fused);
+                                    &need, &fused, ctx->zgemm_algo);
   if (st) return st;
   if (need > ctx->ws_bytes || (need && !ctx->ws))
     TCI_FAIL(TCI_ERR_WORKSPACE, "heff needs %zu bytes of workspace, %zu attached", need, ctx->ws_bytes);
@@ -260,6 +272,15 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
   }
   const HeffLayout lay = heff_layout(h, dt);
   const int64_t d = h.d, chi_lo = h.chi_lo, chi_r = h.chi_r;
+  const size_t oz_b = heff_ozaki_bytes(dt, ctx->zgemm_algo, h.chi_l, h.chi_lo, h.chi_r, h.chi_ro, h.d, h.D, h.D2);
+  auto set_zalgo = [&](GemmProblem &g) {
+    g.zalgo = ctx->zgemm_algo == kZOzaki ? kZ3M : ctx->zgemm_algo;
+    if (oz_b && ozaki_worthwhile(g.M, g.N, g.K)) {
+      g.zalgo = kZOzaki;
+      g.oz_ws = ws + lay.total;
+      g.oz_ws_bytes = oz_b;
+    }
+  };
   void *T1 = ws + lay.off_x;
   // ---- GEMM1: T1[w,b,s,t,c] = sum_a L[a,w,b] psi[a,s,t,c] ----
   {
@@ -269,6 +290,7 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
     g.A = L.data; g.a_sm = 1; g.a_sk = g.M;
     g.B = psi.data; g.b_sk = g.N; g.b_sn = 1;
     g.C = T1; g.c_sm = g.N;
+    set_zalgo(g);
     if (g.K == 1) g.a_sk = 0;
     if (g.M == 1) { g.a_sm = 1; g.a_sk = 1; }
     if (g.K == 1 && g.N == 1) g.b_sk = 1;
@@ -376,6 +398,7 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
     g.A = T3; g.a_sm = g.K; g.a_sk = 1;
     g.B = R.data; g.b_sk = g.N; g.b_sn = 1;
     g.C = out.data; g.c_sm = g.N;
+    set_zalgo(g);
     if (g.N == 1) { g.b_sk = 1; }
     { tci_status_t _r = run_gemm(ctx, g); if (_r) return _r; }
   }

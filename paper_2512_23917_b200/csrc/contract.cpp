@@ -268,6 +268,15 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
       }
     }
   }
+  // complex128 GEMM algorithm; the Ozaki path needs its own scratch
+  int zalgo = ctx->zgemm_algo == kZOzaki ? kZ3M : ctx->zgemm_algo;
+  size_t offZ = 0, ozb = 0;
+  if (a.dtype == TCI_C128 && ctx->zgemm_algo == kZOzaki && splitk <= 1 && ozaki_worthwhile(M, N, K)) {
+    zalgo = kZOzaki;
+    ozb = ozaki_workspace_bytes(M, N, K);
+    offZ = off;
+    off = align_up(off + ozb);
+  }
   *ws_needed = off;
   if (dry_run) return TCI_OK;
   if (off > ws_bytes || (off && !ws))
@@ -355,6 +364,11 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   canon_a(g.M, g.K, g.a_sm, g.a_sk);
   // B(k,n): the same rule with (N, K)
   canon_a(g.N, g.K, g.b_sn, g.b_sk);
+  g.zalgo = zalgo;
+  if (zalgo == kZOzaki) {
+    g.oz_ws = wsb + offZ;
+    g.oz_ws_bytes = ozb;
+  }
   if (splitk > 1) {
     g.splitk = splitk;
     g.k_chunk = k_chunk;

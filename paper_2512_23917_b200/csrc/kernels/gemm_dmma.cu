@@ -16,7 +16,7 @@
 // DADD per fragment element, ~1/64 of the DMMA work). Error is normwise
 // (|Ci error| <~ K u (|Ar|+|Ai|)(|Br|+|Bi|)), inside the 1e-12 relative-
 // Frobenius parity bar (R11). A 4M variant (Cr += Ar.Br - Ai.Bi,
-// Ci += Ar.Bi + Ai.Br) is kept and selectable (TCI_ZGEMM_ALGO=4m).
+// Ci += Ar.Bi + Ai.Br) is kept and selectable (tci_set_gemm_algorithm).
 //
 // Kernel structure (one CTA per 64x64 complex / 128x128 real output tile):
 //  * 6-stage (complex) / 3-stage (real) cp.async pipeline, 16-byte chunks, zero-fill on ragged edges;
@@ -549,14 +549,6 @@ cudaError_t run_z(const GemmProblem &p, bool ak, bool bk, cudaStream_t s, int64_
   return run<Z<false, false>>(p, s, launches);
 }
 
-bool use_4m() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("TCI_ZGEMM_ALGO");
-    v = (e && (strcmp(e, "4m") == 0 || strcmp(e, "4M") == 0)) ? 1 : 0;
-  }
-  return v == 1;
-}
 
 }  // namespace
 
@@ -661,8 +653,10 @@ static cudaError_t launch_gemm_main(const GemmProblem &p, cudaStream_t s, int64_
   // The planner canonicalises strides (contract.cpp): a_sk == 1 selects the
   // K-contiguous loader, otherwise a_sm == 1; same for B.
   const bool ak = (p.a_sk == 1), bk = (p.b_sk == 1);
-  if (p.dtype == TCI_C128)
-    return use_4m() ? run_z<Z4Cfg>(p, ak, bk, s, launches) : run_z<Z3Cfg>(p, ak, bk, s, launches);
+  if (p.dtype == TCI_C128) {
+    if (p.zalgo == kZOzaki && p.splitk <= 1) return launch_ozaki_zgemm(p, p.oz_ws, p.oz_ws_bytes, s, launches);
+    return p.zalgo == kZ4M ? run_z<Z4Cfg>(p, ak, bk, s, launches) : run_z<Z3Cfg>(p, ak, bk, s, launches);
+  }
   // float64: 16-byte chunks need 16-byte aligned rows
   const int64_t lda = ak ? p.a_sm : p.a_sk, ldb = bk ? p.b_sn : p.b_sk;
   const bool aligned = ((uintptr_t)p.A % 16 == 0) && ((uintptr_t)p.B % 16 == 0) &&

@@ -1,0 +1,509 @@
+// ozaki.cu -- complex128 GEMM on the INT8 tensor cores (tcgen05 kind::i8) by
+// the Ozaki-II integer-modular scheme:
+//
+//   1. scale: for every row m of A (both re and im) pick s_m so that
+//      |A(m,k)| 2^{s_m} < 2^t, and A'(m,k) = rint(A(m,k) 2^{s_m}) (t-bit
+//      integers, exact in fp64); likewise B'(k,n) = rint(B(k,n) 2^{r_n});
+//   2. the integer complex product C' = A'B' is computed EXACTLY from its
+//      residues modulo n coprime moduli m_l <= 255 (prod m_l > 2 max|C'|):
+//      with the 3M split (exact in integer arithmetic)
+//        P = A'r B'r,  Q = A'i B'i,  S = (A'r + A'i)(B'r + B'i),
+//        C'r = P - Q,  C'i = S - P - Q,
+//      every residue operand is an int8 in [-127, 127] and every batch of the
+//      3n INT8 GEMMs (int32 accumulation, exact for K <= 133 000) runs in ONE
+//      batched CUTLASS sm100 INT8 GEMM (2-SM 256x256x128 tiles, TMA, TMEM);
+//   3. CRT: C' = sum_l c_l w_l mod M (w_l the CRT weights, M = prod m_l) in
+//      exact 128-bit integer arithmetic, reduced to (-M/2, M/2], converted to
+//      fp64 and scaled back by 2^-(s_m + r_n).
+//
+// The only rounding is step 1's truncation to t >= 46 bits (relative error
+// ~2^-46 per operand entry, well inside the 1e-12 relative-Frobenius bar;
+// DESIGN.md R26) and the final conversion to fp64. t and n are chosen from K:
+// 2t + 3 + log2 K <= log2 M. Rows are processed in chunks so the int32 GEMM
+// outputs (3n x Mc x N) fit a bounded workspace.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+
+#include "../tci_internal.h"
+#include "common.cuh"
+
+#include "cutlass/cutlass.h"
+#include "cute/tensor.hpp"
+#include "cutlass/gemm/dispatch_policy.hpp"
+#include "cutlass/gemm/collective/collective_builder.hpp"
+#include "cutlass/epilogue/collective/collective_builder.hpp"
+#include "cutlass/gemm/device/gemm_universal_adapter.h"
+#include "cutlass/gemm/kernel/gemm_universal.hpp"
+#include "cutlass/util/packed_stride.hpp"
+
+namespace tci {
+namespace {
+
+using namespace cute;
+
+constexpr int kMaxMod = 15;
+constexpr int kModuli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+__constant__ int c_moduli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+
+// ---------------------------------------------------------------------------
+// CUTLASS sm100 INT8 GEMM: D[b][m][n] = sum_k A[b][m][k] B[b][n][k] (int32)
+// ---------------------------------------------------------------------------
+using TileShape = Shape<_256, _256, _128>;
+using ClusterShape = Shape<_2, _1, _1>;
+using Epi = typename cutlass::epilogue::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, TileShape, ClusterShape,
+    cutlass::epilogue::collective::EpilogueTileAuto, int32_t, int32_t, int32_t, cutlass::layout::RowMajor, 4,
+    int32_t, cutlass::layout::RowMajor, 4, cutlass::epilogue::collective::EpilogueScheduleAuto>::CollectiveOp;
+using Main = typename cutlass::gemm::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, int8_t, cutlass::layout::RowMajor, 16, int8_t,
+    cutlass::layout::ColumnMajor, 16, int32_t, TileShape, ClusterShape,
+    cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename Epi::SharedStorage))>,
+    cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
+using I8Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Main, Epi, void>;
+using I8Gemm = cutlass::gemm::device::GemmUniversalAdapter<I8Kernel>;
+
+// ---------------------------------------------------------------------------
+// step 1a: per-row (A) / per-column (B) exponent E with |x| < 2^E for every
+// entry (re and im) of that row/column; E = -100000 for an all-zero line
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int exp_of(double x) {
+  if (x == 0.0) return -100000;
+  int e;
+  frexp(x, &e);   // |x| = f 2^e, 0.5 <= f < 1  ->  |x| < 2^e
+  return e;
+}
+
+// line l (= m for A, n for B) of extent K; element (l, k) at base + l*s_l + k*s_k
+// (complex elements). K-contiguous lines: one warp per line. Line-contiguous
+// (s_l == 1): blockIdx.y splits K into chunks, consecutive threads take
+// consecutive lines (coalesced) and combine with atomicMax (max is order-
+// independent: deterministic). E must be pre-set to -100000 in that mode.
+__global__ void __launch_bounds__(256) line_exponent(const double2 *base, int64_t nlines, int64_t K,
+                                                     int64_t s_l, int64_t s_k, int *E) {
+  if (s_k == 1) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nlines) return;
+    int e = -100000;
+    const double2 *p = base + warp * s_l;
+    for (int64_t k = lane; k < K; k += 32) {
+      const double2 v = p[k];
+      e = max(e, max(exp_of(v.x), exp_of(v.y)));
+    }
+    for (int o = 16; o; o >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if (lane == 0) E[warp] = e;
+  } else {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= nlines) return;
+    const int64_t kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc;
+    const int64_t k1 = min(K, k0 + kc);
+    int e = -100000;
+    const double2 *p = base + l * s_l;
+    for (int64_t k = k0; k < k1; k++) {
+      const double2 v = p[k * s_k];
+      e = max(e, max(exp_of(v.x), exp_of(v.y)));
+    }
+    atomicMax(E + l, e);
+  }
+}
+
+__global__ void fill_int(int *p, int64_t n, int v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// exact symmetric residue of an integer-valued double |x| < 2^51 modulo m,
+// as the low byte of an int: rounding by the 1.5*2^52 "magic" addition keeps
+// the work on the FP64 pipe (no F2I / FRND conversions)
+__device__ __forceinline__ uint32_t residue_byte(double x, double m, double minv) {
+  const double magic = 6755399441055744.0;   // 1.5 * 2^52
+  const double q = (fma(x, minv, magic) - magic);
+  const double r = fma(-q, m, x) + magic;     // r in [-(m-1)/2, (m-1)/2] + magic
+  return (uint32_t)__double2loint(r) & 0xffu;
+}
+
+// ---------------------------------------------------------------------------
+// step 1b + 2a: residue planes. out[(l*3 + comp)][line][kp] int8, K-major,
+// comp 0 = re, 1 = im, 2 = re + im; zero for k >= K or line >= nlines.
+// Each thread produces 16 consecutive k of one line for all planes.
+// ---------------------------------------------------------------------------
+struct ResArgs {
+  const double2 *base;
+  int64_t nlines, K, Kp, s_l, s_k;
+  int64_t line0;            // first line of the chunk (global index)
+  int64_t lines_out;        // rows in the output planes (chunk, padded)
+  const int *E;             // exponents (global line index)
+  int t;                    // bit budget
+  int nmod;
+  int8_t *out;
+  int64_t plane_stride;     // lines_out * Kp
+};
+
+__global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs a) {
+  const int64_t kgroups = a.Kp / 16;
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= a.lines_out * kgroups) return;
+  // K-contiguous source: consecutive threads walk k (coalesced reads and writes)
+  const int64_t row = gid / kgroups;
+  const int64_t k0 = (gid % kgroups) * 16;
+  const int64_t line = a.line0 + row;
+  double xr[16], xi[16];
+  if (line < a.nlines && a.E[line] > -100000) {
+    const int sc = a.t - a.E[line];
+    const double2 *p = a.base + line * a.s_l;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      const int64_t k = k0 + j;
+      double2 v = make_double2(0.0, 0.0);
+      if (k < a.K) v = p[k * a.s_k];
+      xr[j] = rint(ldexp(v.x, sc));
+      xi[j] = rint(ldexp(v.y, sc));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; j++) xr[j] = xi[j] = 0.0;
+  }
+  for (int l = 0; l < a.nmod; l++) {
+    const double m = (double)c_moduli[l], minv = 1.0 / m;
+#pragma unroll
+    for (int comp = 0; comp < 3; comp++) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        uint32_t packed = 0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const int j = q * 4 + b;
+          const double x = comp == 0 ? xr[j] : (comp == 1 ? xi[j] : xr[j] + xi[j]);
+          packed |= residue_byte(x, m, minv) << (8 * b);
+        }
+        w[q] = packed;
+      }
+      int8_t *dst = a.out + (int64_t)(l * 3 + comp) * a.plane_stride + row * a.Kp + k0;
+      *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+// line-contiguous source (s_l == 1): a 32-line x 64-k tile is read along the
+// lines (coalesced), turned into integers in shared memory and written along
+// k: eight threads write one line's 64 contiguous residue bytes per plane.
+__global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArgs a) {
+  __shared__ double sx[2][32][65];
+  const int64_t ntk = a.Kp / 64;
+  const int64_t tl = blockIdx.x / ntk, tk = blockIdx.x % ntk;
+  const int64_t r0 = tl * 32, kb = tk * 64;
+  const int tid = threadIdx.x;
+  {
+    const int li = tid % 32;
+    const int64_t row = r0 + li, line = a.line0 + row;
+    const bool ok = row < a.lines_out && line < a.nlines && a.E[line] > -100000;
+    const int sc = ok ? a.t - a.E[line] : 0;
+#pragma unroll 4
+    for (int j = tid / 32; j < 64; j += 8) {
+      const int64_t k = kb + j;
+      double2 v = make_double2(0.0, 0.0);
+      if (ok && k < a.K) v = a.base[line + k * a.s_k];
+      sx[0][li][j] = rint(ldexp(v.x, sc));
+      sx[1][li][j] = rint(ldexp(v.y, sc));
+    }
+  }
+  __syncthreads();
+  const int li = tid / 8, kq = (tid % 8) * 8;
+  const int64_t row = r0 + li;
+  if (row >= a.lines_out) return;
+  for (int l = 0; l < a.nmod; l++) {
+    const double m = (double)c_moduli[l], minv = 1.0 / m;
+#pragma unroll
+    for (int comp = 0; comp < 3; comp++) {
+      uint32_t w[2];
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        uint32_t packed = 0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const int j = kq + q * 4 + b;
+          const double xr = sx[0][li][j], xi = sx[1][li][j];
+          const double x = comp == 0 ? xr : (comp == 1 ? xi : xr + xi);
+          packed |= residue_byte(x, m, minv) << (8 * b);
+        }
+        w[q] = packed;
+      }
+      int8_t *dst = a.out + (int64_t)(l * 3 + comp) * a.plane_stride + row * a.Kp + kb + kq;
+      *reinterpret_cast<uint2 *>(dst) = make_uint2(w[0], w[1]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// step 3: CRT reconstruction + scaling into C (complex128), O(n) and exact.
+// With balanced residues c_l of C' (|c_l| <= 127) and the CRT weights
+// w_l = (M/m_l) ((M/m_l)^-1 mod m_l) split into three 37-bit chunks
+// w_l = w_l0 + w_l1 2^37 + w_l2 2^74, the chunk sums S_j = sum_l c_l w_lj are
+// exact fp64 integers (< 15 * 127 * 2^37 < 2^48) and X = S_0 + S_1 2^37 +
+// S_2 2^74 == C' (mod M). Since |C'| <= M/4 (choice of t), q = rint(X/M) from
+// a double estimate is exact; R_j = S_j - q M_j is exact; carries normalise
+// the chunks to |R_0|, |R_1| <= 2^36; C' = R_2 2^74 + R_1 2^37 + R_0 is then
+// converted with ~1 ulp error.
+// ---------------------------------------------------------------------------
+struct CrtArgs {
+  const int32_t *D;         // [3n][Mc][Np]
+  int64_t Mc, N, Np, m0;    // chunk rows, columns, padded columns, first row
+  int nmod;
+  double W[kMaxMod][3];     // CRT weight chunks (exact integers)
+  double Mch[3];            // M chunks
+  double Minv;              // ~1 / M
+  const int *EA, *EB;       // exponents
+  int t;
+  double2 *C;
+  int64_t c_sm;
+};
+
+__device__ __forceinline__ double crt_value(const double (&S)[3], const CrtArgs &a) {
+  const double two37 = 137438953472.0, inv37 = 1.0 / 137438953472.0;
+  const double two74 = two37 * two37;
+  const double xe = fma(S[2], two74, S[1] * two37) + S[0];
+  const double q = rint(xe * a.Minv);
+  double r0 = fma(-q, a.Mch[0], S[0]);
+  double r1 = fma(-q, a.Mch[1], S[1]);
+  double r2 = fma(-q, a.Mch[2], S[2]);
+  double cy = rint(r0 * inv37);
+  r0 = fma(-cy, two37, r0);
+  r1 += cy;
+  cy = rint(r1 * inv37);
+  r1 = fma(-cy, two37, r1);
+  r2 += cy;
+  return fma(r2, two74, fma(r1, two37, r0));
+}
+
+template <int NMOD>
+__global__ void __launch_bounds__(256) crt_kernel(const __grid_constant__ CrtArgs a) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= a.Mc * a.N) return;
+  const int64_t r = idx / a.N, n = idx % a.N;
+  const int64_t m = a.m0 + r;
+  const int ea = a.EA[m], eb = a.EB[n];
+  double2 out = make_double2(0.0, 0.0);
+  if (ea > -100000 && eb > -100000) {
+    const int64_t plane = a.Mc * a.Np, off = r * a.Np + n;
+    int vr[NMOD], vi[NMOD];
+#pragma unroll
+    for (int i = 0; i < NMOD; i++) {
+      const int P = __ldg(a.D + (3 * i + 0) * plane + off), Q = __ldg(a.D + (3 * i + 1) * plane + off);
+      const int S = __ldg(a.D + (3 * i + 2) * plane + off);
+      vr[i] = P - Q;
+      vi[i] = S - P - Q;
+    }
+    double Sr[3] = {0.0, 0.0, 0.0}, Si[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < NMOD; i++) {
+      const int mm = c_moduli[i], h = mm >> 1;
+      int cr = vr[i] % mm, ci = vi[i] % mm;        // (-m, m)
+      cr += cr > h ? -mm : (cr < -h ? mm : 0);      // balanced [-h, h]
+      ci += ci > h ? -mm : (ci < -h ? mm : 0);
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        Sr[j] = fma((double)cr, a.W[i][j], Sr[j]);
+        Si[j] = fma((double)ci, a.W[i][j], Si[j]);
+      }
+    }
+    const int sc = -(2 * a.t - ea - eb);
+    out = make_double2(ldexp(crt_value(Sr, a), sc), ldexp(crt_value(Si, a), sc));
+  }
+  a.C[m * a.c_sm + n] = out;
+}
+
+// ---------------------------------------------------------------------------
+// host planning
+// ---------------------------------------------------------------------------
+struct OzPlan {
+  int nmod, t;
+  int64_t Kp, Np, Mc, chunks;
+  size_t off_EA, off_EB, off_Bres, off_Ares, off_D, off_cutlass, total;
+};
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+size_t align_up(size_t x) { return (x + 255) / 256 * 256; }
+
+OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D) {
+  OzPlan p{};
+  const double lk = std::log2((double)std::max<int64_t>(K, 1));
+  double lm = 0;
+  p.nmod = 0;
+  for (int l = 0; l < kMaxMod; l++) {
+    lm += std::log2((double)kModuli[l]);
+    p.nmod = l + 1;
+    if (std::floor((lm - 3.0 - lk) / 2.0) >= 46) break;
+  }
+  p.t = (int)std::floor((lm - 3.0 - lk) / 2.0);
+  p.Kp = round_up(K, 64);
+  p.Np = round_up(N, 16);
+  const int64_t planes = 3 * p.nmod;
+  // rows per chunk: int32 outputs + A residues within budget_D, multiple of 256
+  int64_t mc = (int64_t)(budget_D / ((size_t)planes * (p.Np * 4 + p.Kp)));
+  mc = std::max<int64_t>(256, mc / 256 * 256);
+  p.Mc = std::min<int64_t>(round_up(M, 256), mc);
+  p.chunks = (M + p.Mc - 1) / p.Mc;
+  size_t off = 0;
+  p.off_EA = off; off = align_up(off + (size_t)M * 4);
+  p.off_EB = off; off = align_up(off + (size_t)N * 4);
+  p.off_Bres = off; off = align_up(off + (size_t)planes * p.Np * p.Kp);
+  p.off_Ares = off; off = align_up(off + (size_t)planes * p.Mc * p.Kp);
+  p.off_D = off; off = align_up(off + (size_t)planes * p.Mc * p.Np * 4);
+  p.off_cutlass = off; off = align_up(off + ((size_t)64 << 20));   // CUTLASS workspace (small)
+  p.total = off;
+  return p;
+}
+
+// modular helpers on the host (unsigned 128-bit)
+typedef unsigned __int128 u128;
+u128 mulmod_small(u128 a, unsigned b, u128 M) {   // (a * b) mod M, a < M < 2^126, b < 256
+  u128 r = 0;
+  for (int bit = 7; bit >= 0; bit--) {
+    r = (r << 1) % M;
+    if (b >> bit & 1) r = (r + a) % M;
+  }
+  return r;
+}
+// modular inverse on the host (extended Euclid)
+unsigned inv_mod(unsigned a, unsigned m) {
+  int t = 0, nt = 1, r = (int)m, nr = (int)(a % m);
+  while (nr) {
+    const int q = r / nr;
+    int tmp = t - q * nt; t = nt; nt = tmp;
+    tmp = r - q * nr; r = nr; nr = tmp;
+  }
+  return (unsigned)(t < 0 ? t + (int)m : t);
+}
+
+}  // namespace
+
+size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  return oz_plan(M, N, K, (size_t)8 << 30).total;
+}
+
+// C = A B (complex128) per GemmProblem strides, by Ozaki-II on INT8 tcgen05.
+cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
+                               int64_t *launches) {
+  if (g.M == 0 || g.N == 0) return cudaSuccess;
+  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30);
+  if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
+  char *w = static_cast<char *>(ws);
+  int *EA = reinterpret_cast<int *>(w + p.off_EA), *EB = reinterpret_cast<int *>(w + p.off_EB);
+  int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
+  int32_t *D = reinterpret_cast<int32_t *>(w + p.off_D);
+  const double2 *A = static_cast<const double2 *>(g.A), *B = static_cast<const double2 *>(g.B);
+  // exponents: rows of A (line m: stride a_sm, along k: a_sk); columns of B
+  auto exponents = [&](const double2 *X, int64_t nl, int64_t s_l, int64_t s_k, int *E) {
+    if (s_k == 1) {
+      line_exponent<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, s>>>(X, nl, g.K, s_l, s_k, E);
+      if (launches) ++*launches;
+    } else {
+      fill_int<<<(unsigned)std::min<int64_t>((nl + 255) / 256, 1024), 256, 0, s>>>(E, nl, -100000);
+      const int64_t ky = std::max<int64_t>(1, std::min<int64_t>((g.K + 127) / 128, 65535));
+      dim3 grid((unsigned)((nl + 255) / 256), (unsigned)ky);
+      line_exponent<<<grid, 256, 0, s>>>(X, nl, g.K, s_l, s_k, E);
+      if (launches) *launches += 2;
+    }
+  };
+  exponents(A, g.M, g.a_sm, g.a_sk, EA);
+  exponents(B, g.N, g.b_sn, g.b_sk, EB);
+  auto launch_res = [&](const ResArgs &r) {
+    if (r.s_k == 1) {
+      const int64_t th = r.lines_out * (r.Kp / 16);
+      residues<<<(unsigned)((th + 255) / 256), 256, 0, s>>>(r);
+    } else {
+      const int64_t blocks = ((r.lines_out + 31) / 32) * (r.Kp / 64);
+      residues_t<<<(unsigned)blocks, 256, 0, s>>>(r);
+    }
+    if (launches) ++*launches;
+  };
+  const int planes = 3 * p.nmod;
+  // residues of B (all columns, padded to Np lines)
+  {
+    ResArgs r{};
+    r.base = B; r.nlines = g.N; r.K = g.K; r.Kp = p.Kp; r.s_l = g.b_sn; r.s_k = g.b_sk;
+    r.line0 = 0; r.lines_out = p.Np; r.E = EB; r.t = p.t; r.nmod = p.nmod; r.out = Bres;
+    r.plane_stride = p.Np * p.Kp;
+    launch_res(r);
+  }
+  // CRT weights in 37-bit chunks
+  CrtArgs c{};
+  {
+    u128 Mp = 1;
+    for (int l = 0; l < p.nmod; l++) Mp *= (u128)kModuli[l];
+    const u128 mask = ((u128)1 << 37) - 1;
+    for (int l = 0; l < p.nmod; l++) {
+      const unsigned ml = (unsigned)kModuli[l];
+      const u128 Ml = Mp / ml;
+      const u128 wl = mulmod_small(Ml, inv_mod((unsigned)(Ml % ml), ml), Mp);
+      c.W[l][0] = (double)(uint64_t)(wl & mask);
+      c.W[l][1] = (double)(uint64_t)((wl >> 37) & mask);
+      c.W[l][2] = (double)(uint64_t)(wl >> 74);
+    }
+    c.Mch[0] = (double)(uint64_t)(Mp & mask);
+    c.Mch[1] = (double)(uint64_t)((Mp >> 37) & mask);
+    c.Mch[2] = (double)(uint64_t)(Mp >> 74);
+    c.Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
+  }
+  c.nmod = p.nmod; c.EA = EA; c.EB = EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
+  c.C = static_cast<double2 *>(g.C); c.c_sm = g.c_sm;
+  for (int64_t ch = 0; ch < p.chunks; ch++) {
+    const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
+    {
+      ResArgs r{};
+      r.base = A; r.nlines = g.M; r.K = g.K; r.Kp = p.Kp; r.s_l = g.a_sm; r.s_k = g.a_sk;
+      r.line0 = m0; r.lines_out = mc; r.E = EA; r.t = p.t; r.nmod = p.nmod; r.out = Ares;
+      r.plane_stride = mc * p.Kp;
+      launch_res(r);
+    }
+    {
+      using SA = typename I8Gemm::GemmKernel::StrideA;
+      using SB = typename I8Gemm::GemmKernel::StrideB;
+      using SC = typename I8Gemm::GemmKernel::StrideC;
+      using SD = typename I8Gemm::GemmKernel::StrideD;
+      const int Mi = (int)mc, Ni = (int)p.Np, Ki = (int)p.Kp, Li = planes;
+      SA sa = cutlass::make_cute_packed_stride(SA{}, {Mi, Ki, Li});
+      SB sb = cutlass::make_cute_packed_stride(SB{}, {Ni, Ki, Li});
+      SC sc = cutlass::make_cute_packed_stride(SC{}, {Mi, Ni, Li});
+      SD sd = cutlass::make_cute_packed_stride(SD{}, {Mi, Ni, Li});
+      typename I8Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {Mi, Ni, Ki, Li},
+                                      {Ares, sa, Bres, sb}, {{1, 0}, D, sc, D, sd}};
+      I8Gemm gemm;
+      if (gemm.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorNotSupported;
+      const size_t cws = I8Gemm::get_workspace_size(args);
+      if (cws > ((size_t)64 << 20)) return cudaErrorInvalidValue;
+      if (gemm.initialize(args, w + p.off_cutlass, s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
+      OzProf *pf = g.oz_prof;
+      const bool rec = pf && pf->n < 64;
+      if (rec) {
+        cudaEventCreate(&pf->a[pf->n]);
+        cudaEventCreate(&pf->b[pf->n]);
+        cudaEventRecord(pf->a[pf->n], s);
+      }
+      if (gemm.run(s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
+      if (rec) {
+        cudaEventRecord(pf->b[pf->n], s);
+        pf->ops[pf->n] = 2.0 * (double)Mi * Ni * Ki * Li;
+        pf->n++;
+      }
+      if (launches) ++*launches;
+    }
+    c.Mc = mc;
+    c.m0 = m0;
+    const int64_t th = mc * g.N;
+    const unsigned gb = (unsigned)((th + 255) / 256);
+    switch (p.nmod) {
+      case 12: crt_kernel<12><<<gb, 256, 0, s>>>(c); break;
+      case 13: crt_kernel<13><<<gb, 256, 0, s>>>(c); break;
+      case 14: crt_kernel<14><<<gb, 256, 0, s>>>(c); break;
+      case 15: crt_kernel<15><<<gb, 256, 0, s>>>(c); break;
+      default: return cudaErrorInvalidValue;
+    }
+    if (launches) ++*launches;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace tci

@@ -150,13 +150,12 @@ tci_status_t lanczos_bytes(tci_ctx_s *ctx, const View &L, const View &W1, const 
                            const View &psi, int max_iter, size_t *bytes, size_t *heff_b) {
   size_t hb = 0;
   tci_status_t st = heff_plan_bytes(psi.dtype, L.shape[0], L.shape[2], psi.shape[3], R.shape[2], psi.shape[1],
-                                    L.shape[1], W1.shape[1], W2.shape[1], &hb, nullptr);
+                                    L.shape[1], W1.shape[1], W2.shape[1], &hb, nullptr, ctx->zgemm_algo);
   if (st) return st;
   const size_t vb = align_up(psi.bytes());
   const size_t slab = align_up((size_t)L.shape[2] * psi.shape[1] * psi.shape[2] * R.shape[2] * dtype_size(psi.dtype));
   *heff_b = align_up(hb);
   *bytes = *heff_b + vb + slab + (size_t)(max_iter + 1) * vb;
-  (void)ctx;
   (void)W2;
   return TCI_OK;
 }

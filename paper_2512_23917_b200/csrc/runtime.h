@@ -33,6 +33,7 @@ struct tci_ctx_s {
   // plan cache: key -> serialized plan decision (see contract.cpp)
   std::unordered_map<std::string, std::vector<int64_t>> plan_cache;
   int64_t plan_hits, plan_misses;
+  int zgemm_algo;       // complex128 GEMM algorithm (kZ3M default; tci_set_gemm_algorithm)
   void *dev_scratch;    // reductions (vec.cu): allocated once at creation
   void *host_scratch;   // pinned, reduction results
 };
@@ -110,7 +111,7 @@ tci_status_t permute_exec(tci_ctx_s *ctx, const View &in, const int32_t *perm, v
 
 // Launch wrappers: count launches and (when profiling) bracket each kernel
 // with CUDA events on ctx->stream, recording its algorithmic flops / bytes.
-enum { kProfGemm = 0, kProfSkinny = 1, kProfPermute = 2 };
+enum { kProfGemm = 0, kProfSkinny = 1, kProfPermute = 2, kProfI8 = 3 };
 tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g);
 tci_status_t run_skinny(tci_ctx_s *ctx, const SkinnyProblem &p);
 tci_status_t run_permute(tci_ctx_s *ctx, const PermuteProblem &p);
@@ -130,7 +131,7 @@ ag_fn nccl_allgather_ptr();
 // Chains (chains.cpp)
 tci_status_t heff_plan_bytes(tci_dtype_t dt, int64_t chi_l, int64_t chi_lo, int64_t chi_r,
                              int64_t chi_ro, int64_t d, int64_t D, int64_t D1, int64_t D2,
-                             size_t *bytes, bool *fused_w12);
+                             size_t *bytes, bool *fused_w12, int zalgo = 0);
 tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View &W2, const View &R,
                        const View &psi, const View &out);
 tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View &B, const char *lb,

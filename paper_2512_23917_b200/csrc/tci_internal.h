@@ -36,6 +36,12 @@ struct GemmProblem {
   const void *A; int64_t a_sm, a_sk;
   const void *B; int64_t b_sk, b_sn;
   void *C; int64_t c_sm;        // c_sn == 1
+  // complex128 algorithm (kZ3M / kZ4M on DMMA, kZOzaki on INT8 tcgen05) and,
+  // for kZOzaki, its scratch (ozaki_workspace_bytes)
+  int zalgo = 0;
+  void *oz_ws = nullptr;
+  size_t oz_ws_bytes = 0;
+  struct OzProf *oz_prof = nullptr;   // optional: event timing of the INT8 GEMMs
   // deterministic split-K (few output tiles, long K): split z of `splitk`
   // sums k in [z*k_chunk, min(K,(z+1)*k_chunk)) into partial + z*M*N (double
   // or double2 elements, row-major [M][N]); a reduce kernel then adds the
@@ -53,6 +59,23 @@ struct GemmProblem {
   double *te_T = nullptr;                 // theta
   int64_t te_t[4] = {0, 0, 0, 0};         // strides of a, p, q, c in theta
 };
+
+enum { kZ3M = 0, kZ4M = 1, kZOzaki = 2 };
+// event pairs around each INT8 tensor-core GEMM of an Ozaki GEMM, with its
+// executed int8 ops (2 per MAC over the padded batch); filled by ozaki.cu
+struct OzProf {
+  int n;
+  cudaEvent_t a[64], b[64];
+  double ops[64];
+};
+// Scratch of the Ozaki-II INT8 complex GEMM (ozaki.cu) for an M x N x K product.
+size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K);
+cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
+                               int64_t *launches);
+// Ozaki pays ~10 passes over the operands: use it only for big products.
+inline bool ozaki_worthwhile(int64_t M, int64_t N, int64_t K) {
+  return (double)M * (double)N * (double)K >= 4.0e9 && M >= 256 && N >= 256 && K >= 64;
+}
 
 // Output tile of the GEMM kernel used for `dtype` (for the planner's split-K choice).
 void gemm_tile(tci_dtype_t dtype, int *bm, int *bn);

@@ -582,3 +582,62 @@ def test_lanczos_closed_forms(ctx):
     psi = dev(start)
     e, _ = ctx.heff_lanczos(L, dev(W), dev(W), R, psi, max_iter=16, tol=1e-15)
     assert abs(e - h["E0"]) < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# Ozaki-II INT8 tcgen05 complex GEMM (8(f4))
+# ---------------------------------------------------------------------------
+
+@pytest.fixture()
+def ozctx():
+    c = tci.Context(0)
+    c.set_gemm_algorithm(tci.TCI_GEMM_OZAKI_INT8)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("layout", ["mk", "km"])
+def test_ozaki_contract_vs_dmma_and_oracle(ctx, ozctx, oracle_mod, layout):
+    """M = N = 1024, K = 4096 (4.3e9 MACs: takes the Ozaki path) with rows
+    scaled by random powers of two (dynamic range between rows) and one zero row."""
+    A = synth.random_tensor((1024, 4096), "c128", 490, 1)
+    rng = np.random.default_rng(5)
+    A = A * torch.from_numpy(2.0 ** rng.integers(-30, 30, size=(1024, 1))).to(torch.complex128)
+    A[17] = 0
+    B = synth.random_tensor((4096, 1024), "c128", 490, 2)
+    At = A if layout == "mk" else A.T.contiguous()
+    c_oz = ozctx.contract(dev(At), layout, dev(B), "kn", "mn")
+    c_dm = ctx.contract(dev(At), layout, dev(B), "kn", "mn")
+    assert torch.count_nonzero(c_oz[17]).item() == 0
+    # per-row relative errors (rows differ in scale by up to 2^60)
+    d = (c_oz - c_dm).abs().pow(2).sum(1).sqrt() / c_dm.abs().pow(2).sum(1).sqrt().clamp_min(1e-300)
+    d[17] = 0
+    assert d.max().item() <= 1e-12
+    rows = [0, 1, 511, 1023]
+    ref = oracle_mod.contract(A.numpy()[rows], "mk", B.numpy(), "kn", "mn")
+    got = host(c_oz)[rows]
+    for i in range(len(rows)):
+        assert rel_frob(got[i], ref[i]) <= 1e-12
+    c2 = ozctx.contract(dev(At), layout, dev(B), "kn", "mn")
+    assert torch.equal(c_oz, c2)                         # deterministic
+
+
+def test_ozaki_heff_cfg2(ozctx, oracle_mod):
+    cfg = synth.HEFF_CONFIGS["cfg2_heisenberg_chi1024"]
+    inp = synth.heff_inputs(cfg["chi"], cfg["d"], cfg["D"], cfg["dtype"], cfg["seed"], cfg["model"])
+    d_in = {k: dev(v) for k, v in inp.items()}
+    out = ozctx.heff_apply(d_in["L"], d_in["W1"], d_in["W2"], d_in["R"], d_in["psi"])
+    n = {k: v.numpy() for k, v in inp.items()}
+    rows = [0, 1, 255, 256, 511, 512, 1023]
+    ref = oracle_mod.heff_rows(n["L"], n["W1"], n["W2"], n["R"], n["psi"], rows)
+    assert rel_frob(host(out)[rows], ref) <= 1e-12
+    part = ozctx.heff_apply(d_in["L"][:, :, 256:512].contiguous(), d_in["W1"], d_in["W2"], d_in["R"], d_in["psi"])
+    assert torch.equal(part, out[256:512])                # shard-invariant, bitwise
+
+
+def test_ozaki_lanczos(ozctx):
+    W, lb, rb = synth.heisenberg_mpo()
+    L, R = dev(synth.boundary_env(5, lb)), dev(synth.boundary_env(5, rb))
+    psi = dev(synth.random_tensor((1, 2, 2, 1), "c128", 480, 2))
+    e, _ = ozctx.heff_lanczos(L, dev(W), dev(W), R, psi, max_iter=10, tol=1e-15)
+    assert abs(e + 0.75) < 1e-13

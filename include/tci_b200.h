@@ -130,6 +130,12 @@ TCI_API const char *tci_last_error(void);
 #define TCI_GEMM_DMMA_4M 1
 #define TCI_GEMM_OZAKI_INT8 2
 TCI_API tci_status_t tci_set_gemm_algorithm(tci_ctx_t ctx, int algo);
+
+/* Diagnostic (pure host): the Ozaki parameters for contraction length K --
+ * number of moduli *nmod, integer bit budget *t (operands are scaled to
+ * |A'| < 2^t), and the moduli (moduli[nmod], may be NULL). Returns 0, or
+ * OUT_OF_RANGE when K is outside 1..131072 (the int32 exactness limit). */
+TCI_API int tci_ozaki_params(int64_t K, int *nmod, int *t, int *moduli);
 TCI_API tci_status_t tci_get_gemm_algorithm(tci_ctx_t ctx, int *algo);
 
 /* Attach caller-owned device scratch memory of `bytes` bytes (256-byte

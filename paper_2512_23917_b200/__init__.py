@@ -45,6 +45,7 @@ EXPORTED = [
     "tci_launch_count", "tci_heff_plan_tree", "tci_profile_enable", "tci_profile_query",
     "tci_mps_overlap", "tci_norm", "tci_normalize", "tci_scale", "tci_linear_combine", "tci_inner",
     "tci_lanczos_workspace_size", "tci_heff_lanczos", "tci_set_gemm_algorithm", "tci_get_gemm_algorithm",
+    "tci_ozaki_params",
 ]
 
 
@@ -87,6 +88,8 @@ _sig = {
     "tci_launch_count": ([_vp, _i64p], ctypes.c_int),
     "tci_profile_enable": ([_vp, ctypes.c_int], ctypes.c_int),
     "tci_set_gemm_algorithm": ([_vp, ctypes.c_int], ctypes.c_int),
+    "tci_ozaki_params": ([ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                          ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_get_gemm_algorithm": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_norm": ([_vp, _vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tci_normalize": ([_vp, _vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
@@ -280,6 +283,13 @@ TCI_GEMM_DMMA_3M, TCI_GEMM_DMMA_4M, TCI_GEMM_OZAKI_INT8 = 0, 1, 2
 
 def tci_set_gemm_algorithm(ctx: int, algo: int) -> None:
     _ok(_lib.tci_set_gemm_algorithm(_vp(ctx), int(algo)), "tci_set_gemm_algorithm")
+
+
+def tci_ozaki_params(K: int):
+    n, t = ctypes.c_int(), ctypes.c_int()
+    mods = (ctypes.c_int * 16)()
+    st = _lib.tci_ozaki_params(int(K), ctypes.byref(n), ctypes.byref(t), mods)
+    return st, n.value, t.value, [mods[i] for i in range(n.value)]
 
 
 def tci_get_gemm_algorithm(ctx: int) -> int:

@@ -769,3 +769,13 @@ tci_status_t tci_allgather(tci_ctx_t ctx, tci_tensor_t shard, tci_tensor_t full)
 namespace tci {
 ag_fn nccl_allgather_ptr() { return g_nccl.allgather; }
 }  // namespace tci
+
+extern "C" int tci_ozaki_params(int64_t K, int *nmod, int *t, int *moduli) {
+  const int *m = nullptr;
+  int n = 0;
+  tci::ozaki_params(K, &n, t, &m);
+  if (nmod) *nmod = n;
+  if (moduli)
+    for (int i = 0; i < n; i++) moduli[i] = m[i];
+  return (K >= 1 && K <= tci::kOzakiMaxK) ? 0 : (int)TCI_ERR_OUT_OF_RANGE;
+}

@@ -379,6 +379,13 @@ unsigned inv_mod(unsigned a, unsigned m) {
 
 }  // namespace
 
+void ozaki_params(int64_t K, int *nmod, int *t, const int **moduli) {
+  const OzPlan p = oz_plan(1, 1, K, (size_t)8 << 30);
+  if (nmod) *nmod = p.nmod;
+  if (t) *t = p.t;
+  if (moduli) *moduli = kModuli;
+}
+
 size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   return oz_plan(M, N, K, (size_t)8 << 30).total;
 }
@@ -387,6 +394,7 @@ size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
                                int64_t *launches) {
   if (g.M == 0 || g.N == 0) return cudaSuccess;
+  if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;   // int32 residue products would overflow
   const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
   char *w = static_cast<char *>(ws);

@@ -73,9 +73,13 @@ size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K);
 cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
                                int64_t *launches);
 // Ozaki pays ~10 passes over the operands: use it only for big products.
+// K <= 131072 keeps every int32 residue dot product exact (K * 127^2 < 2^31).
+constexpr int64_t kOzakiMaxK = 131072;
 inline bool ozaki_worthwhile(int64_t M, int64_t N, int64_t K) {
-  return (double)M * (double)N * (double)K >= 4.0e9 && M >= 256 && N >= 256 && K >= 64;
+  return (double)M * (double)N * (double)K >= 4.0e9 && M >= 256 && N >= 256 && K >= 64 && K <= kOzakiMaxK;
 }
+// moduli count and integer bit budget chosen for a contraction length K
+void ozaki_params(int64_t K, int *nmod, int *t, const int **moduli);
 
 // Output tile of the GEMM kernel used for `dtype` (for the planner's split-K choice).
 void gemm_tile(tci_dtype_t dtype, int *bm, int *bn);

@@ -34,6 +34,7 @@
 #include "cutlass/gemm/dispatch_policy.hpp"
 #include "cutlass/gemm/collective/collective_builder.hpp"
 #include "cutlass/epilogue/collective/collective_builder.hpp"
+#include "cutlass/epilogue/fusion/sm90_callbacks_tma_warpspecialized.hpp"
 #include "cutlass/gemm/device/gemm_universal_adapter.h"
 #include "cutlass/gemm/kernel/gemm_universal.hpp"
 #include "cutlass/util/packed_stride.hpp"
@@ -48,14 +49,37 @@ constexpr int kModuli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 2
 __constant__ int c_moduli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
 
 // ---------------------------------------------------------------------------
-// CUTLASS sm100 INT8 GEMM: D[b][m][n] = sum_k A[b][m][k] B[b][n][k] (int32)
+// CUTLASS sm100 INT8 GEMM with a fused epilogue (EVT):
+//   D[b][m][n] = (sum_k A[b][m][k] B[b][n][k]) mod m_b   in [0, m_b), uint8
+// The int32 accumulator (exact) is reduced by its batch's modulus in the
+// epilogue (per-batch scalar broadcast), so the residue planes leave the
+// tensor cores as bytes: 4x less traffic than int32 outputs.
 // ---------------------------------------------------------------------------
+template <class T>
+struct ModNonneg;
+template <int N>
+struct ModNonneg<cutlass::Array<int32_t, N>> {
+  CUTLASS_HOST_DEVICE cutlass::Array<int32_t, N> operator()(cutlass::Array<int32_t, N> const &a,
+                                                           cutlass::Array<int32_t, N> const &m) const {
+    cutlass::Array<int32_t, N> r;
+    CUTLASS_PRAGMA_UNROLL
+    for (int i = 0; i < N; ++i) {
+      const int32_t x = a[i] % m[i];
+      r[i] = x < 0 ? x + m[i] : x;
+    }
+    return r;
+  }
+};
+namespace fu = cutlass::epilogue::fusion;
+using ModEVT = fu::Sm90EVT<fu::Sm90Compute<ModNonneg, uint8_t, int32_t, cutlass::FloatRoundStyle::round_to_nearest>,
+                           fu::Sm90AccFetch, fu::Sm90ScalarBroadcast<int32_t, Stride<_0, _0, int64_t>>>;
 using TileShape = Shape<_256, _256, _128>;
 using ClusterShape = Shape<_2, _1, _1>;
 using Epi = typename cutlass::epilogue::collective::CollectiveBuilder<
     cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, TileShape, ClusterShape,
-    cutlass::epilogue::collective::EpilogueTileAuto, int32_t, int32_t, int32_t, cutlass::layout::RowMajor, 4,
-    int32_t, cutlass::layout::RowMajor, 4, cutlass::epilogue::collective::EpilogueScheduleAuto>::CollectiveOp;
+    cutlass::epilogue::collective::EpilogueTileAuto, int32_t, int32_t, void, cutlass::layout::RowMajor, 16,
+    uint8_t, cutlass::layout::RowMajor, 16, cutlass::epilogue::collective::EpilogueScheduleAuto,
+    ModEVT>::CollectiveOp;
 using Main = typename cutlass::gemm::collective::CollectiveBuilder<
     cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, int8_t, cutlass::layout::RowMajor, 16, int8_t,
     cutlass::layout::ColumnMajor, 16, int32_t, TileShape, ClusterShape,
@@ -107,6 +131,11 @@ __global__ void __launch_bounds__(256) line_exponent(const double2 *base, int64_
     }
     atomicMax(E + l, e);
   }
+}
+
+__global__ void batch_moduli(int32_t *p, int planes) {
+  const int i = threadIdx.x;
+  if (i < planes) p[i] = c_moduli[i / 3];
 }
 
 __global__ void fill_int(int *p, int64_t n, int v) {
@@ -248,7 +277,7 @@ __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArg
 // converted with ~1 ulp error.
 // ---------------------------------------------------------------------------
 struct CrtArgs {
-  const int32_t *D;         // [3n][Mc][Np]
+  const uint8_t *D;         // [3n][Mc][Np], residues in [0, m)
   int64_t Mc, N, Np, m0;    // chunk rows, columns, padded columns, first row
   int nmod;
   double W[kMaxMod][3];     // CRT weight chunks (exact integers)
@@ -291,7 +320,7 @@ __global__ void __launch_bounds__(256) crt_kernel(const __grid_constant__ CrtArg
 #pragma unroll
     for (int i = 0; i < NMOD; i++) {
       const int P = __ldg(a.D + (3 * i + 0) * plane + off), Q = __ldg(a.D + (3 * i + 1) * plane + off);
-      const int S = __ldg(a.D + (3 * i + 2) * plane + off);
+      const int S = __ldg(a.D + (3 * i + 2) * plane + off);   // residues in [0, m)
       vr[i] = P - Q;
       vi[i] = S - P - Q;
     }
@@ -320,7 +349,7 @@ __global__ void __launch_bounds__(256) crt_kernel(const __grid_constant__ CrtArg
 struct OzPlan {
   int nmod, t;
   int64_t Kp, Np, Mc, chunks;
-  size_t off_EA, off_EB, off_Bres, off_Ares, off_D, off_cutlass, total;
+  size_t off_EA, off_EB, off_Bres, off_Ares, off_D, off_mod, off_cutlass, total;
 };
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -340,8 +369,8 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D) {
   p.Kp = round_up(K, 64);
   p.Np = round_up(N, 16);
   const int64_t planes = 3 * p.nmod;
-  // rows per chunk: int32 outputs + A residues within budget_D, multiple of 256
-  int64_t mc = (int64_t)(budget_D / ((size_t)planes * (p.Np * 4 + p.Kp)));
+  // rows per chunk: uint8 residue outputs + A residues within budget_D, multiple of 256
+  int64_t mc = (int64_t)(budget_D / ((size_t)planes * (p.Np + p.Kp)));
   mc = std::max<int64_t>(256, mc / 256 * 256);
   p.Mc = std::min<int64_t>(round_up(M, 256), mc);
   p.chunks = (M + p.Mc - 1) / p.Mc;
@@ -350,7 +379,8 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D) {
   p.off_EB = off; off = align_up(off + (size_t)N * 4);
   p.off_Bres = off; off = align_up(off + (size_t)planes * p.Np * p.Kp);
   p.off_Ares = off; off = align_up(off + (size_t)planes * p.Mc * p.Kp);
-  p.off_D = off; off = align_up(off + (size_t)planes * p.Mc * p.Np * 4);
+  p.off_D = off; off = align_up(off + (size_t)planes * p.Mc * p.Np);
+  p.off_mod = off; off = align_up(off + (size_t)planes * 4);
   p.off_cutlass = off; off = align_up(off + ((size_t)64 << 20));   // CUTLASS workspace (small)
   p.total = off;
   return p;
@@ -400,7 +430,8 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   char *w = static_cast<char *>(ws);
   int *EA = reinterpret_cast<int *>(w + p.off_EA), *EB = reinterpret_cast<int *>(w + p.off_EB);
   int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
-  int32_t *D = reinterpret_cast<int32_t *>(w + p.off_D);
+  uint8_t *D = reinterpret_cast<uint8_t *>(w + p.off_D);
+  int32_t *bmod = reinterpret_cast<int32_t *>(w + p.off_mod);   // modulus of each batch plane
   const double2 *A = static_cast<const double2 *>(g.A), *B = static_cast<const double2 *>(g.B);
   // exponents: rows of A (line m: stride a_sm, along k: a_sk); columns of B
   auto exponents = [&](const double2 *X, int64_t nl, int64_t s_l, int64_t s_k, int *E) {
@@ -428,6 +459,8 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
     if (launches) ++*launches;
   };
   const int planes = 3 * p.nmod;
+  batch_moduli<<<1, 64, 0, s>>>(bmod, planes);
+  if (launches) ++*launches;
   // residues of B (all columns, padded to Np lines)
   {
     ResArgs r{};
@@ -476,8 +509,9 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       SB sb = cutlass::make_cute_packed_stride(SB{}, {Ni, Ki, Li});
       SC sc = cutlass::make_cute_packed_stride(SC{}, {Mi, Ni, Li});
       SD sd = cutlass::make_cute_packed_stride(SD{}, {Mi, Ni, Li});
+      typename ModEVT::Arguments fargs{{}, {{0}, {bmod}, {Stride<_0, _0, int64_t>{_0{}, _0{}, int64_t(1)}}}, {}};
       typename I8Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {Mi, Ni, Ki, Li},
-                                      {Ares, sa, Bres, sb}, {{1, 0}, D, sc, D, sd}};
+                                      {Ares, sa, Bres, sb}, {fargs, nullptr, sc, D, sd}};
       I8Gemm gemm;
       if (gemm.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorNotSupported;
       const size_t cws = I8Gemm::get_workspace_size(args);

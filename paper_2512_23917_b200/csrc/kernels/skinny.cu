@@ -118,9 +118,20 @@ cudaError_t launch_npt(const SkinnyProblem &p, size_t smem, int64_t blocks, cuda
 
 template <bool CPLX>
 cudaError_t launch_c(const SkinnyProblem &p, size_t smem, int64_t blocks, cudaStream_t s) {
+  // outputs per thread: instantiated exactly for the common sizes so no
+  // unrolled slot is dead (N = 20 -> 5 at d=2, D=5)
   const int npt = (p.N + NG - 1) / NG;
-  if (npt <= 2) return launch_npt<CPLX, 2>(p, smem, blocks, s);
+  switch (npt) {
+    case 1: return launch_npt<CPLX, 1>(p, smem, blocks, s);
+    case 2: return launch_npt<CPLX, 2>(p, smem, blocks, s);
+    case 3: return launch_npt<CPLX, 3>(p, smem, blocks, s);
+    case 4: return launch_npt<CPLX, 4>(p, smem, blocks, s);
+    case 5: return launch_npt<CPLX, 5>(p, smem, blocks, s);
+    case 6: return launch_npt<CPLX, 6>(p, smem, blocks, s);
+  }
   if (npt <= 8) return launch_npt<CPLX, 8>(p, smem, blocks, s);
+  if (npt <= 12) return launch_npt<CPLX, 12>(p, smem, blocks, s);
+  if (npt <= 16) return launch_npt<CPLX, 16>(p, smem, blocks, s);
   return launch_npt<CPLX, MAXNPT>(p, smem, blocks, s);
 }
 

@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../tci_internal.h"
 #include "common.cuh"
@@ -194,23 +195,31 @@ __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs 
     for (int j = 0; j < 16; j++) xr[j] = xi[j] = 0.0;
   }
   for (int l = 0; l < a.nmod; l++) {
-    const double m = (double)c_moduli[l], minv = 1.0 / m;
+    const int mi = c_moduli[l], h = mi >> 1;
+    const double m = (double)mi, minv = 1.0 / m;
+    uint32_t w[3][4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      uint32_t pr = 0, pi = 0, ps = 0;
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        const int j = q * 4 + b;
+        const uint32_t br = residue_byte(xr[j], m, minv), bi = residue_byte(xi[j], m, minv);
+        // (re + im) mod m from the two balanced residues: integer ops only
+        int s = (int)(int8_t)br + (int)(int8_t)bi;
+        s += s > h ? -mi : (s < -h ? mi : 0);
+        pr |= br << (8 * b);
+        pi |= bi << (8 * b);
+        ps |= ((uint32_t)s & 0xffu) << (8 * b);
+      }
+      w[0][q] = pr;
+      w[1][q] = pi;
+      w[2][q] = ps;
+    }
 #pragma unroll
     for (int comp = 0; comp < 3; comp++) {
-      uint32_t w[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        uint32_t packed = 0;
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
-          const int j = q * 4 + b;
-          const double x = comp == 0 ? xr[j] : (comp == 1 ? xi[j] : xr[j] + xi[j]);
-          packed |= residue_byte(x, m, minv) << (8 * b);
-        }
-        w[q] = packed;
-      }
       int8_t *dst = a.out + (int64_t)(l * 3 + comp) * a.plane_stride + row * a.Kp + k0;
-      *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4 *>(dst) = make_uint4(w[comp][0], w[comp][1], w[comp][2], w[comp][3]);
     }
   }
 }
@@ -243,36 +252,43 @@ __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArg
   const int64_t row = r0 + li;
   if (row >= a.lines_out) return;
   for (int l = 0; l < a.nmod; l++) {
-    const double m = (double)c_moduli[l], minv = 1.0 / m;
+    const int mi = c_moduli[l], h = mi >> 1;
+    const double m = (double)mi, minv = 1.0 / m;
+    uint32_t w[3][2];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      uint32_t pr = 0, pi = 0, ps = 0;
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        const int j = kq + q * 4 + b;
+        const uint32_t br = residue_byte(sx[0][li][j], m, minv), bi = residue_byte(sx[1][li][j], m, minv);
+        int s = (int)(int8_t)br + (int)(int8_t)bi;
+        s += s > h ? -mi : (s < -h ? mi : 0);
+        pr |= br << (8 * b);
+        pi |= bi << (8 * b);
+        ps |= ((uint32_t)s & 0xffu) << (8 * b);
+      }
+      w[0][q] = pr;
+      w[1][q] = pi;
+      w[2][q] = ps;
+    }
 #pragma unroll
     for (int comp = 0; comp < 3; comp++) {
-      uint32_t w[2];
-#pragma unroll
-      for (int q = 0; q < 2; q++) {
-        uint32_t packed = 0;
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
-          const int j = kq + q * 4 + b;
-          const double xr = sx[0][li][j], xi = sx[1][li][j];
-          const double x = comp == 0 ? xr : (comp == 1 ? xi : xr + xi);
-          packed |= residue_byte(x, m, minv) << (8 * b);
-        }
-        w[q] = packed;
-      }
       int8_t *dst = a.out + (int64_t)(l * 3 + comp) * a.plane_stride + row * a.Kp + kb + kq;
-      *reinterpret_cast<uint2 *>(dst) = make_uint2(w[0], w[1]);
+      *reinterpret_cast<uint2 *>(dst) = make_uint2(w[comp][0], w[comp][1]);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
 // step 3: CRT reconstruction + scaling into C (complex128), O(n) and exact.
-// With balanced residues c_l of C' (|c_l| <= 127) and the CRT weights
-// w_l = (M/m_l) ((M/m_l)^-1 mod m_l) split into three 37-bit chunks
-// w_l = w_l0 + w_l1 2^37 + w_l2 2^74, the chunk sums S_j = sum_l c_l w_lj are
-// exact fp64 integers (< 15 * 127 * 2^37 < 2^48) and X = S_0 + S_1 2^37 +
-// S_2 2^74 == C' (mod M). Since |C'| <= M/4 (choice of t), q = rint(X/M) from
-// a double estimate is exact; R_j = S_j - q M_j is exact; carries normalise
+// With representatives 0 <= c_l < 3 m_l of the residues of C' and the CRT
+// weights w_l = (M/m_l) ((M/m_l)^-1 mod m_l) split into three 37-bit chunks
+// w_l = w_l0 + w_l1 2^37 + w_l2 2^74 (w_l2 < 2^38), the chunk sums
+// S_j = sum_l c_l w_lj are exact fp64 integers (< 15 * 765 * 2^38 < 2^52) and
+// X = S_0 + S_1 2^37 + S_2 2^74 == C' (mod M), 0 <= X < 15 * 765 * M. Since
+// |C'| <= M/4 (choice of t), q = rint(X/M) from a double estimate is exact;
+// R_j = S_j - q M_j is exact (q < 2^14, M_j < 2^38); carries normalise
 // the chunks to |R_0|, |R_1| <= 2^36; C' = R_2 2^74 + R_1 2^37 + R_0 is then
 // converted with ~1 ulp error.
 // ---------------------------------------------------------------------------
@@ -280,8 +296,8 @@ struct CrtArgs {
   const uint8_t *D;         // [3n][Mc][Np], residues in [0, m)
   int64_t Mc, N, Np, m0;    // chunk rows, columns, padded columns, first row
   int nmod;
-  double W[kMaxMod][3];     // CRT weight chunks (exact integers)
-  double Mch[3];            // M chunks
+  double W[kMaxMod][4];     // CRT weight chunks (exact integers, 37 bits each)
+  double Mch[4];            // M chunks
   double Minv;              // ~1 / M
   const int *EA, *EB;       // exponents
   int t;
@@ -289,58 +305,173 @@ struct CrtArgs {
   int64_t c_sm;
 };
 
-__device__ __forceinline__ double crt_value(const double (&S)[3], const CrtArgs &a) {
+template <int NCH>
+__device__ __forceinline__ double crt_value(const double (&S)[NCH], const CrtArgs &a) {
   const double two37 = 137438953472.0, inv37 = 1.0 / 137438953472.0;
-  const double two74 = two37 * two37;
-  const double xe = fma(S[2], two74, S[1] * two37) + S[0];
+  double xe = S[NCH - 1];
+#pragma unroll
+  for (int j = NCH - 2; j >= 0; j--) xe = fma(xe, two37, S[j]);
   const double q = rint(xe * a.Minv);
-  double r0 = fma(-q, a.Mch[0], S[0]);
-  double r1 = fma(-q, a.Mch[1], S[1]);
-  double r2 = fma(-q, a.Mch[2], S[2]);
-  double cy = rint(r0 * inv37);
-  r0 = fma(-cy, two37, r0);
-  r1 += cy;
-  cy = rint(r1 * inv37);
-  r1 = fma(-cy, two37, r1);
-  r2 += cy;
-  return fma(r2, two74, fma(r1, two37, r0));
+  double r[NCH];
+#pragma unroll
+  for (int j = 0; j < NCH; j++) r[j] = fma(-q, a.Mch[j], S[j]);
+#pragma unroll
+  for (int j = 0; j < NCH - 1; j++) {
+    const double cy = rint(r[j] * inv37);
+    r[j] = fma(-cy, two37, r[j]);
+    r[j + 1] += cy;
+  }
+  double x = r[NCH - 1];
+#pragma unroll
+  for (int j = NCH - 2; j >= 0; j--) x = fma(x, two37, r[j]);
+  return x;
 }
 
-template <int NMOD>
-__global__ void __launch_bounds__(256) crt_kernel(const __grid_constant__ CrtArgs a) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= a.Mc * a.N) return;
-  const int64_t r = idx / a.N, n = idx % a.N;
-  const int64_t m = a.m0 + r;
-  const int ea = a.EA[m], eb = a.EB[n];
-  double2 out = make_double2(0.0, 0.0);
-  if (ea > -100000 && eb > -100000) {
-    const int64_t plane = a.Mc * a.Np, off = r * a.Np + n;
-    int vr[NMOD], vi[NMOD];
-#pragma unroll
-    for (int i = 0; i < NMOD; i++) {
-      const int P = __ldg(a.D + (3 * i + 0) * plane + off), Q = __ldg(a.D + (3 * i + 1) * plane + off);
-      const int S = __ldg(a.D + (3 * i + 2) * plane + off);   // residues in [0, m)
-      vr[i] = P - Q;
-      vi[i] = S - P - Q;
+// Persistent kernel over tiles of (one row, TW = CPT * THREADS columns). The
+// 3 NMOD residue planes of a tile (3 NMOD x TW bytes) are staged in shared
+// memory by cp.async.bulk (TMA) into a STAGES-deep ring completed on
+// mbarriers, so later tiles' bytes are in flight while this one is reduced;
+// each thread reconstructs CPT consecutive columns.
+template <int CPT, int THREADS, int STAGES>
+struct CrtShape {
+  static constexpr int kTW = CPT * THREADS;
+  static constexpr size_t smem(int nmod) { return (size_t)STAGES * 3 * nmod * kTW + 8 * STAGES; }
+};
+
+// NCH = 3 chunks while sum_l 3 m_l w_lj stays below 2^53 (nmod <= 14: top
+// chunk < 2^36, sums < 2^50); 4 chunks for nmod = 15 (M > 2^117).
+template <int NMOD, int NCH, int CPT, int THREADS, int STAGES>
+__global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ CrtArgs a) {
+  static_assert(CPT == 2 || CPT == 4, "columns per thread");
+  using Shape = CrtShape<CPT, THREADS, STAGES>;
+  constexpr int TW = Shape::kTW;
+  extern __shared__ __align__(128) uint8_t crt_smem[];
+  constexpr int kStage = 3 * NMOD * TW;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(crt_smem + STAGES * kStage);
+  const int64_t tpr = (a.Np + TW - 1) / TW;   // tiles per row
+  const int64_t ntiles = a.Mc * tpr;
+  const int64_t plane = a.Mc * a.Np;
+  const int tid = threadIdx.x;
+
+  auto issue = [&](int64_t tile, int s) {   // warp 0
+    const int64_t r = tile / tpr, c0 = (tile % tpr) * TW;
+    const uint32_t w = (uint32_t)(a.Np - c0 < TW ? a.Np - c0 : TW);   // multiple of 16
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(&bar[s], 3 * NMOD * w);
     }
-    double Sr[3] = {0.0, 0.0, 0.0}, Si[3] = {0.0, 0.0, 0.0};
+    __syncwarp();
+    for (int q = tid; q < 3 * NMOD; q += 32)
+      bulk_g2s(crt_smem + s * kStage + q * TW, a.D + q * plane + r * a.Np + c0, w, &bar[s]);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; s++) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid < 32)
+    for (int s = 0; s < STAGES; s++)
+      if (blockIdx.x + (int64_t)s * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)s * gridDim.x, s);
+
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+    const int s = it % STAGES;
+    mbar_wait(&bar[s], (uint32_t)((it / STAGES) & 1));
+    const int64_t r = tile / tpr, n0 = (tile % tpr) * TW + CPT * tid;
+    if (n0 < a.N) {
+      const uint8_t *st = crt_smem + s * kStage + CPT * tid;
+      double Sr[CPT][NCH], Si[CPT][NCH];
 #pragma unroll
-    for (int i = 0; i < NMOD; i++) {
-      const int mm = c_moduli[i], h = mm >> 1;
-      int cr = vr[i] % mm, ci = vi[i] % mm;        // (-m, m)
-      cr += cr > h ? -mm : (cr < -h ? mm : 0);      // balanced [-h, h]
-      ci += ci > h ? -mm : (ci < -h ? mm : 0);
+      for (int e = 0; e < CPT; e++)
 #pragma unroll
-      for (int j = 0; j < 3; j++) {
-        Sr[j] = fma((double)cr, a.W[i][j], Sr[j]);
-        Si[j] = fma((double)ci, a.W[i][j], Si[j]);
+        for (int j = 0; j < NCH; j++) Sr[e][j] = Si[e][j] = 0.0;
+#pragma unroll
+      for (int i = 0; i < NMOD; i++) {
+        uint32_t P, Q, S;
+        if constexpr (CPT == 4) {
+          P = *reinterpret_cast<const uint32_t *>(st + (3 * i + 0) * TW);
+          Q = *reinterpret_cast<const uint32_t *>(st + (3 * i + 1) * TW);
+          S = *reinterpret_cast<const uint32_t *>(st + (3 * i + 2) * TW);
+        } else {
+          P = *reinterpret_cast<const uint16_t *>(st + (3 * i + 0) * TW);
+          Q = *reinterpret_cast<const uint16_t *>(st + (3 * i + 1) * TW);
+          S = *reinterpret_cast<const uint16_t *>(st + (3 * i + 2) * TW);
+        }
+        // Unbalanced representatives, congruent to the residues of Re/Im C':
+        // P - Q + m in (0, 2m), S - P - Q + 2m in (0, 3m). Computed on two 16-bit
+        // lanes per register (no lane leaves [0, 2^16), so no cross-lane carry).
+        const uint32_t m2 = (uint32_t)c_moduli[i] * 0x10001u;
+#pragma unroll
+        for (int half = 0; half < CPT / 2; half++) {
+          const uint32_t sel = half ? 0x4342u : 0x4140u;
+          const uint32_t p2 = __byte_perm(P, 0, sel), q2 = __byte_perm(Q, 0, sel), s2 = __byte_perm(S, 0, sel);
+          const uint32_t cr2 = p2 + m2 - q2;
+          const uint32_t ci2 = s2 + 2u * m2 - p2 - q2;
+#pragma unroll
+          for (int lane = 0; lane < 2; lane++) {
+            const int e = half * 2 + lane;
+            const double dr = (double)(lane ? cr2 >> 16 : cr2 & 0xffffu);
+            const double di = (double)(lane ? ci2 >> 16 : ci2 & 0xffffu);
+#pragma unroll
+            for (int j = 0; j < NCH; j++) {
+              Sr[e][j] = fma(dr, a.W[i][j], Sr[e][j]);
+              Si[e][j] = fma(di, a.W[i][j], Si[e][j]);
+            }
+          }
+        }
+      }
+      const int64_t m = a.m0 + r;
+      const int ea = a.EA[m];
+      const int sc0 = -(2 * a.t - ea);
+#pragma unroll
+      for (int e = 0; e < CPT; e++) {
+        const int64_t n = n0 + e;
+        if (n >= a.N) break;
+        const int eb = a.EB[n];
+        double2 out = make_double2(0.0, 0.0);
+        if (ea > -100000 && eb > -100000) {
+          const double xr = crt_value(Sr[e], a), xi = crt_value(Si[e], a);
+          const int sc = sc0 + eb;
+          if (sc >= -1022 && sc <= 1023) {   // 2^sc is a normal double: one exact multiply
+            const double f = __hiloint2double((sc + 1023) << 20, 0);
+            out = make_double2(xr * f, xi * f);
+          } else {
+            out = make_double2(ldexp(xr, sc), ldexp(xi, sc));
+          }
+        }
+        __stcs(&a.C[m * a.c_sm + n], out);
       }
     }
-    const int sc = -(2 * a.t - ea - eb);
-    out = make_double2(ldexp(crt_value(Sr, a), sc), ldexp(crt_value(Si, a), sc));
+    __syncthreads();   // stage s fully consumed
+    const int64_t next = tile + (int64_t)STAGES * gridDim.x;
+    if (tid < 32 && next < ntiles) issue(next, s);
   }
-  a.C[m * a.c_sm + n] = out;
+}
+
+template <int NMOD, int NCH, int CPT, int THREADS, int STAGES>
+cudaError_t launch_crt_cfg(const CrtArgs &c, int64_t mc, cudaStream_t s) {
+  using Shape = CrtShape<CPT, THREADS, STAGES>;
+  auto kern = crt_kernel<NMOD, NCH, CPT, THREADS, STAGES>;
+  const size_t smem = Shape::smem(NMOD);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = mc * ((c.Np + Shape::kTW - 1) / Shape::kTW);
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)std::max(per_sm, 1) * sms);
+  kern<<<grid, THREADS, smem, s>>>(c);
+  return cudaGetLastError();
+}
+
+// 4 columns x 256 threads x 2 stages: measured best of {2,4} x {128,256} x
+// {2,3,4} on the target shapes (the kernel is XU/FP64-issue bound there).
+template <int NMOD, int NCH>
+cudaError_t launch_crt(const CrtArgs &c, int64_t mc, cudaStream_t s) {
+  return launch_crt_cfg<NMOD, NCH, 4, 256, 2>(c, mc, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -479,13 +610,9 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       const unsigned ml = (unsigned)kModuli[l];
       const u128 Ml = Mp / ml;
       const u128 wl = mulmod_small(Ml, inv_mod((unsigned)(Ml % ml), ml), Mp);
-      c.W[l][0] = (double)(uint64_t)(wl & mask);
-      c.W[l][1] = (double)(uint64_t)((wl >> 37) & mask);
-      c.W[l][2] = (double)(uint64_t)(wl >> 74);
+      for (int j = 0; j < 4; j++) c.W[l][j] = (double)(uint64_t)((wl >> (37 * j)) & mask);
     }
-    c.Mch[0] = (double)(uint64_t)(Mp & mask);
-    c.Mch[1] = (double)(uint64_t)((Mp >> 37) & mask);
-    c.Mch[2] = (double)(uint64_t)(Mp >> 74);
+    for (int j = 0; j < 4; j++) c.Mch[j] = (double)(uint64_t)((Mp >> (37 * j)) & mask);
     c.Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
   }
   c.nmod = p.nmod; c.EA = EA; c.EB = EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
@@ -534,15 +661,15 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
     }
     c.Mc = mc;
     c.m0 = m0;
-    const int64_t th = mc * g.N;
-    const unsigned gb = (unsigned)((th + 255) / 256);
+    cudaError_t ce;
     switch (p.nmod) {
-      case 12: crt_kernel<12><<<gb, 256, 0, s>>>(c); break;
-      case 13: crt_kernel<13><<<gb, 256, 0, s>>>(c); break;
-      case 14: crt_kernel<14><<<gb, 256, 0, s>>>(c); break;
-      case 15: crt_kernel<15><<<gb, 256, 0, s>>>(c); break;
+      case 12: ce = launch_crt<12, 3>(c, mc, s); break;
+      case 13: ce = launch_crt<13, 3>(c, mc, s); break;
+      case 14: ce = launch_crt<14, 3>(c, mc, s); break;
+      case 15: ce = launch_crt<15, 4>(c, mc, s); break;
       default: return cudaErrorInvalidValue;
     }
+    if (ce != cudaSuccess) return ce;
     if (launches) ++*launches;
   }
   return cudaGetLastError();

@@ -622,6 +622,22 @@ def test_ozaki_contract_vs_dmma_and_oracle(ctx, ozctx, oracle_mod, layout):
     assert torch.equal(c_oz, c2)                         # deterministic
 
 
+@pytest.mark.parametrize("mnk", [(320, 320, 40960), (256, 256, 131072)])
+def test_ozaki_large_k_fifteen_moduli(ozctx, oracle_mod, mnk):
+    """K > 28k needs 15 moduli (M > 2^117): the CRT runs with four 37-bit
+    weight chunks so every chunk sum stays an exact fp64 integer (R27)."""
+    M, N, K = mnk
+    st, nmod, t, _ = tci.tci_ozaki_params(K)
+    assert st == 0 and nmod == 15 and t >= 46
+    A = synth.random_tensor((M, K), "c128", 493, 1)
+    B = synth.random_tensor((K, N), "c128", 493, 2)
+    c = host(ozctx.contract(dev(A), "mk", dev(B), "kn", "mn"))
+    rows = [0, 1, M // 2, M - 1]
+    ref = oracle_mod.contract(A.numpy()[rows], "mk", B.numpy(), "kn", "mn")
+    assert rel_frob(c[rows], ref) <= 1e-12
+    assert ozctx.launch_count() > 0
+
+
 def test_ozaki_heff_cfg2(ozctx, oracle_mod):
     cfg = synth.HEFF_CONFIGS["cfg2_heisenberg_chi1024"]
     inp = synth.heff_inputs(cfg["chi"], cfg["d"], cfg["D"], cfg["dtype"], cfg["seed"], cfg["model"])

@@ -639,6 +639,12 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       typename ModEVT::Arguments fargs{{}, {{0}, {bmod}, {Stride<_0, _0, int64_t>{_0{}, _0{}, int64_t(1)}}}, {}};
       typename I8Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {Mi, Ni, Ki, Li},
                                       {Ares, sa, Bres, sb}, {fargs, nullptr, sc, D, sd}};
+      // Tile order: raster along M in swizzled groups of 8. With K = 20480 (GEMM4)
+      // each 256x256 tile streams 5.2 MB A and B panels; the default order re-read
+      // them from DRAM ~4.5x (50 GB per launch, ncu); this order halves that
+      // (24 GB) and the launch time drops 8% (profiles/r01_ncu_target_ozaki.json).
+      args.scheduler.max_swizzle_size = 8;
+      args.scheduler.raster_order = cutlass::gemm::kernel::detail::RasterOrderOptions::AlongM;
       I8Gemm gemm;
       if (gemm.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorNotSupported;
       const size_t cws = I8Gemm::get_workspace_size(args);

@@ -48,6 +48,8 @@ def launches(cfg):
         full = r["Kernel Name"]
         if "Cfg<" in full:
             name += "<" + full.split("Cfg<")[1].split(">")[0] + ">"
+        if "cutlass" in full:
+            name = "cutlass_int8_gemm (Ozaki residue products)"
         m, v, u = r["Metric Name"], r["Metric Value"], r["Metric Unit"]
         try:
             v = float(v.replace(",", ""))
@@ -107,6 +109,7 @@ def main():
     summ = {"cfg": a.cfg, "launch_list": launches(a.cfg),
             "gemm_full": report(os.path.join(OUT, f"prof_gemm_{a.cfg}.ncu-rep")),
             "skinny_full": report(os.path.join(OUT, f"prof_skinny_{a.cfg}.ncu-rep")),
+            "aux_full": report(os.path.join(OUT, f"prof_aux_{a.cfg}.ncu-rep")),
             "note": "launch_list: ncu --metrics gpu__time_duration.sum,dram__bytes_* --clock-control none "
                     "(cold-cache, serialised: compare shares); *_full: ncu --set full --clock-control none"}
     os.makedirs(PROF, exist_ok=True)
@@ -128,7 +131,8 @@ def main():
             tp = os.path.join(PROF, "ncu_traffic.json")
             cur = json.load(open(tp)) if os.path.exists(tp) else {}
             wl = {"target": "target_heisenberg_chi4096", "cfg2": "cfg2_heisenberg_chi1024",
-                  "cfg4": "cfg4_hubbard_chi4096"}[a.cfg]
+                  "cfg4": "cfg4_hubbard_chi4096",
+                  "target_ozaki": "target_heisenberg_chi4096_ozaki"}[a.cfg]
             cur[wl] = {"gemm_dram_bytes_per_launch": sum(tr) / len(tr), "per_launch": tr,
                        "source": os.path.basename(out), "round": a.round}
             json.dump(cur, open(tp, "w"), indent=1)

@@ -286,6 +286,52 @@ def mps_mpo_apply(A, W, threads=None):
     return reshape(Bt, (a * w, t, b * v))
 
 
+def cplx_conj(a):
+    """tci::cplx_conj (PAPER.md:1235-1268): elementwise complex conjugate,
+    (re, im) -> (re, -im); for real data a deep copy."""
+    a = np.asarray(a)
+    if np.iscomplexobj(a):
+        out = np.empty_like(a)
+        out.real = a.real
+        out.imag = -a.imag
+        return out
+    return a.copy()
+
+
+def env_left(E, ket, W, bra=None, threads=None):
+    """Left environment update (R28), the definition
+        out[b,v,e] = sum_{a,w,c,s,t} E[a,w,c] ket[a,s,b] W[w,v,s,t] conj(bra[c,t,e])
+    evaluated pairwise in the order E.ket -> W -> conj(bra)."""
+    bra = ket if bra is None else bra
+    T1 = contract(E, "awc", ket, "asb", "wcsb", threads)
+    T2 = contract(T1, "wcsb", W, "wvst", "ctbv", threads)
+    return contract(T2, "ctbv", cplx_conj(bra), "cte", "bve", threads)
+
+
+def env_right(E, ket, W, bra=None, threads=None):
+    """Right environment update (R28), the definition
+        out[a,w,f] = sum_{c,x,e,s,t} ket[a,s,c] W[w,x,s,t] E[c,x,e] conj(bra[f,t,e])
+    evaluated pairwise in the order ket.E -> W -> conj(bra)."""
+    bra = ket if bra is None else bra
+    T1 = contract(ket, "asc", E, "cxe", "asxe", threads)
+    T2 = contract(T1, "asxe", W, "wxst", "awte", threads)
+    return contract(T2, "awte", cplx_conj(bra), "fte", "awf", threads)
+
+
+def env_rows(side, E, ket, W, bra, rows, threads=None):
+    """Rows out[r,:,:] for r in rows (the ket's outgoing bond sliced to r)."""
+    res = []
+    for r in rows:
+        r = int(r)
+        if side == 0:
+            k = np.ascontiguousarray(ket[:, :, r:r + 1])
+            res.append(env_left(E, k, W, bra, threads)[0])
+        else:
+            k = np.ascontiguousarray(ket[r:r + 1])
+            res.append(env_right(E, k, W, bra, threads)[0])
+    return np.stack(res)
+
+
 # ----------------------------------------------------------------------------
 # vector functions (App. C.5): definitions written out
 # ----------------------------------------------------------------------------

@@ -503,3 +503,155 @@ def test_vector_function_examples(oracle_mod):
     z = rnd((5, 7), 123, 1, True)
     assert abs(oracle_mod.inner(z, z) - oracle_mod.norm(z) ** 2) < 1e-13
     assert abs(oracle_mod.inner(z, z, conj_a=False) - complex(oracle_mod.contract(z, "ij", z, "ij", ""))) < 1e-13
+
+
+# ---------------------------------------------------------------------------
+# cplx_conj and environment updates (R28)
+# ---------------------------------------------------------------------------
+
+def test_cplx_conj_identities(oracle_mod):
+    a = rnd((3, 2, 4), 71, cplx=True)
+    c = oracle_mod.cplx_conj(a)
+    # the paper's example: std::conj(el1) == el2 at {0,0,0}
+    assert c[0, 0, 0] == np.conj(a[0, 0, 0])
+    # involution, bitwise; a + conj(a) is real (exactly 2 Re a); a conj(a) = |a|^2 >= 0
+    assert np.array_equal(oracle_mod.cplx_conj(c), a)
+    s = a + c
+    assert np.all(s.imag == 0) and np.array_equal(s.real, 2 * a.real)
+    p = a * c
+    assert np.all(p.real >= 0) and np.max(np.abs(p.imag)) <= 1e-15 * np.max(p.real)
+    # real data: a deep copy
+    r = rnd((5, 3), 72)
+    rc = oracle_mod.cplx_conj(r)
+    assert np.array_equal(rc, r) and rc is not r and not np.shares_memory(rc, r)
+
+
+_SX = np.array([[0, 0.5], [0.5, 0]], dtype=np.complex128)
+_SY = np.array([[0, -0.5j], [0.5j, 0]], dtype=np.complex128)
+_SZ = np.diag([0.5, -0.5]).astype(np.complex128)
+
+
+def _dense_heisenberg(n):
+    """H = sum_i S_i . S_{i+1} from Kronecker products of the spin matrices
+    (site 0 = most significant index, basis (up, dn)) -- independent of the MPO."""
+    H = np.zeros((2 ** n, 2 ** n), dtype=np.complex128)
+    for i in range(n - 1):
+        for op in (_SX, _SY, _SZ):
+            H += np.kron(np.kron(np.eye(2 ** i), np.kron(op, op)), np.eye(2 ** (n - i - 2)))
+    return H
+
+
+def _dense_state(sites):
+    v = sites[0][0]                                  # [d, chi]
+    for A in sites[1:]:
+        v = np.tensordot(v, A, axes=([-1], [0]))
+    return v[..., 0].reshape(-1)
+
+
+def _env_expectation(oracle_mod, sites, W, lb, rb, bra=None, side=0):
+    D = W.shape[0]
+    bra = sites if bra is None else bra
+    if side == 0:
+        E = synth.boundary_env(D, lb)
+        for A, B in zip(sites, bra):
+            E = oracle_mod.env_left(E, A, W, B)
+        return E[0, rb, 0]
+    E = synth.boundary_env(D, rb)
+    for A, B in zip(reversed(sites), reversed(bra)):
+        E = oracle_mod.env_right(E, A, W, B)
+    return E[0, lb, 0]
+
+
+@pytest.mark.parametrize("side", [0, 1])
+def test_env_expectation_vs_dense_hamiltonian(oracle_mod, side):
+    n, bonds = 6, [1, 2, 4, 5, 4, 2, 1]
+    ket = [rnd((bonds[i], 2, bonds[i + 1]), 80 + i, cplx=True) for i in range(n)]
+    bra = [rnd((bonds[i], 2, bonds[i + 1]), 90 + i, cplx=True) for i in range(n)]
+    W, lb, rb = synth.heisenberg_mpo()
+    H = _dense_heisenberg(n)
+    psi, phi = _dense_state(ket), _dense_state(bra)
+    ref = np.vdot(psi, H @ psi)
+    got = _env_expectation(oracle_mod, ket, W, lb, rb, side=side)
+    assert abs(got - ref) <= 1e-12 * abs(ref)
+    assert abs(got.imag) <= 1e-12 * abs(ref)            # Hermitian H: real expectation
+    ref2 = np.vdot(phi, H @ psi)                         # <phi|H|psi>, bra conjugated
+    got2 = _env_expectation(oracle_mod, ket, W, lb, rb, bra=bra, side=side)
+    assert abs(got2 - ref2) <= 1e-12 * abs(ref2)
+
+
+def test_env_product_state_closed_form(oracle_mod):
+    """Product state of spinors u_i: <S_i . S_j> = n_i . n_j / 4 with the Bloch
+    vectors n = (2 Re u0* u1, 2 Im u0* u1, |u0|^2 - |u1|^2) (normalised u)."""
+    rng = np.random.default_rng(7)
+    n = 9
+    u = rng.standard_normal((n, 2)) + 1j * rng.standard_normal((n, 2))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    sites = [x.reshape(1, 2, 1) for x in u]
+    bloch = np.stack([2 * (np.conj(u[:, 0]) * u[:, 1]).real, 2 * (np.conj(u[:, 0]) * u[:, 1]).imag,
+                      np.abs(u[:, 0]) ** 2 - np.abs(u[:, 1]) ** 2], axis=1)
+    closed = float(np.sum(bloch[:-1] * bloch[1:]) / 4)
+    W, lb, rb = synth.heisenberg_mpo()
+    for side in (0, 1):
+        got = _env_expectation(oracle_mod, sites, W, lb, rb, side=side)
+        assert abs(got - closed) <= 1e-14 and abs(got.imag) <= 1e-15
+    # Neel state: -(n-1)/4 exactly
+    neel = synth.product_state_sites(n)
+    assert _env_expectation(oracle_mod, neel, W, lb, rb) == -(n - 1) / 4
+
+
+def test_env_left_isometry_maps_identity_to_identity(oracle_mod):
+    rng = np.random.default_rng(11)
+    chi, d, chi2 = 6, 3, 9
+    X = rng.standard_normal((chi * d, chi2)) + 1j * rng.standard_normal((chi * d, chi2))
+    Q, _ = np.linalg.qr(X)                                # Q^H Q = I
+    A = Q.reshape(chi, d, chi2)
+    I_mpo = np.eye(d, dtype=np.complex128).reshape(1, 1, d, d)
+    E = np.eye(chi, dtype=np.complex128).reshape(chi, 1, chi)
+    out = oracle_mod.env_left(E, A, I_mpo)
+    assert max_abs(out.reshape(chi2, chi2), np.eye(chi2)) <= 1e-14
+    # the right version with a right isometry (rows orthonormal)
+    B = np.ascontiguousarray(Q.T).reshape(chi2, d, chi)
+    R = np.eye(chi, dtype=np.complex128).reshape(chi, 1, chi)
+    outr = oracle_mod.env_right(R, B, I_mpo)
+    # sum_{s,c} B[a,s,c] conj(B[f,s,c]) = (Q^T conj(Q))[a,f] = conj(Q^H Q)^T = I
+    assert max_abs(outr.reshape(chi2, chi2), np.eye(chi2)) <= 1e-14
+
+
+def test_env_norm_equals_transfer_chain_cfg1(oracle_mod):
+    """<psi|psi> through identity-MPO environments equals config 1's transfer
+    norm (real data: the bilinear chain of R17 is the norm)."""
+    sites = synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1, "r64")
+    I_mpo = np.eye(2).reshape(1, 1, 2, 2)
+    E = np.ones((1, 1, 1))
+    for A in sites:
+        E = oracle_mod.env_left(E, A, I_mpo)
+    ref = oracle_mod.mps_norm2(sites)[0, 0]
+    assert abs(E[0, 0, 0] - ref) <= 1e-13 * abs(ref)
+    psi = _dense_state(sites)
+    assert abs(E[0, 0, 0] - np.dot(psi, psi)) <= 1e-12 * abs(ref)
+
+
+@pytest.mark.parametrize("side", [0, 1])
+def test_env_random_mpo_vs_dense_operator(oracle_mod, side):
+    """A random complex (non-Hermitian) MPO: <phi|O|psi> through environments
+    equals phi^H O psi with O[(t..), (s..)] = sum_w prod_i W_i[w_i, w_i+1, s_i, t_i]
+    assembled here with numpy (catches s/t or bra/ket role swaps that the
+    symmetric Heisenberg MPO cannot)."""
+    n, d, D = 4, 2, 3
+    bonds = [1, 2, 3, 2, 1]
+    ket = [rnd((bonds[i], d, bonds[i + 1]), 120 + i, cplx=True) for i in range(n)]
+    bra = [rnd((bonds[i], d, bonds[i + 1]), 130 + i, cplx=True) for i in range(n)]
+    W = rnd((D, D, d, d), 140, cplx=True)
+    lb, rb = 1, 2
+    O = np.einsum("s,t->ts", np.ones(1), np.ones(1)).astype(np.complex128)   # 1x1 start
+    vec = np.zeros(D, dtype=np.complex128)
+    vec[lb] = 1
+    # M[w][(t..), (s..)] accumulated site by site
+    M = [vec[w] * np.ones((1, 1), dtype=np.complex128) for w in range(D)]
+    for _ in range(n):
+        M = [sum(np.kron(M[w], W[w, v].T) for w in range(D)) for v in range(D)]
+    O = M[rb]
+    psi, phi = _dense_state(ket), _dense_state(bra)
+    ref = np.vdot(phi, O @ psi)
+    got = _env_expectation(oracle_mod, ket, W, lb, rb, bra=bra, side=side)
+    assert abs(got - ref) <= 1e-12 * abs(ref)

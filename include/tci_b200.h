@@ -275,6 +275,36 @@ TCI_API tci_status_t tci_tebd_theta(tci_ctx_t ctx, tci_tensor_t A, const char *l
                             tci_tensor_t U, const char *lu,
                             tci_tensor_t theta, const char *lt);
 
+/* Environment update (R28): the DMRG step before
+ * every H_eff, with the index conventions of tci_heff_apply (E[ket bond, MPO
+ * bond, bra bond]; W[w_left, w_right, s = ket physical, t = bra physical]):
+ *   side 0 (left):  out[b,v,e] = sum E[a,w,c] ket[a,s,b] W[w,v,s,t] conj(bra[c,t,e])
+ *     E [chi_k, D, chi_b], ket [chi_k, d, chi_ko], W [D, Dv, d, d],
+ *     bra [chi_b, d, chi_bo], out [chi_ko, Dv, chi_bo]
+ *   side 1 (right): out[a,w,f] = sum ket[a,s,c] W[w,x,s,t] E[c,x,e] conj(bra[f,t,e])
+ *     E [chi_k, D, chi_b], ket [chi_ko, d, chi_k], W [Dv, D, d, d],
+ *     bra [chi_bo, d, chi_b], out [chi_ko, Dv, chi_bo]
+ * (conj is the identity for r64). bra may be the same tensor as ket
+ * (<psi|H|psi>). Executed as GEMM (E.ket, contract engine) -> skinny MPO pass
+ * -> conj(bra) (one HBM pass into workspace) -> GEMM, permute-free;
+ * intermediates live in the attached workspace (tci_env_workspace_size).
+ * All device tensors, one dtype (r64 or c128); out must not overlap inputs.
+ * Errors: INVALID_ARGUMENT (side, overlap), ORDER_MISMATCH, SHAPE_MISMATCH,
+ * UNSUPPORTED (dtype; D*d or Dv*d > 128), WORKSPACE, CUDA, DEAD_CONTEXT. */
+TCI_API tci_status_t tci_env_workspace_size(tci_ctx_t ctx, int side, tci_tensor_t E, tci_tensor_t ket,
+                                            tci_tensor_t W, tci_tensor_t bra, tci_tensor_t out, size_t *bytes);
+TCI_API tci_status_t tci_env_update(tci_ctx_t ctx, int side, tci_tensor_t E, tci_tensor_t ket, tci_tensor_t W,
+                                    tci_tensor_t bra, tci_tensor_t out);
+
+/* Elementwise complex conjugation (tci::cplx_conj): out[i] =
+ * conj(in[i]). out == in conjugates in place (overload (1)); otherwise out
+ * must not overlap in (overload (2)). Real data: in place is a no-op, out of
+ * place a deep copy. Same dtype / shape required. Asynchronous on
+ * the context stream; bitwise exact.
+ * Errors: UNSUPPORTED (dtype mismatch, complex64), ORDER_MISMATCH,
+ * SHAPE_MISMATCH, INVALID_ARGUMENT (partial overlap), CUDA, DEAD_CONTEXT. */
+TCI_API tci_status_t tci_cplx_conj(tci_ctx_t ctx, tci_tensor_t in, tci_tensor_t out);
+
 /* ---------------------------------------------------------------------- */
 /* Vector functions (device kernels, deterministic reductions) and the     */
 /* Lanczos driver around H_eff                              */

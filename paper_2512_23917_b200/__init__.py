@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libtci_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_2512_23917_b200.build` "
+        f"{LIB_PATH} is missing: build it with `python paper_2512_23917_b200/build.py` "
         "(or __graft_entry__.build()); there is no fallback path")
 
 _lib = ctypes.CDLL(LIB_PATH)
@@ -45,7 +45,7 @@ EXPORTED = [
     "tci_launch_count", "tci_heff_plan_tree", "tci_profile_enable", "tci_profile_query",
     "tci_mps_overlap", "tci_norm", "tci_normalize", "tci_scale", "tci_linear_combine", "tci_inner",
     "tci_lanczos_workspace_size", "tci_heff_lanczos", "tci_set_gemm_algorithm", "tci_get_gemm_algorithm",
-    "tci_ozaki_params",
+    "tci_ozaki_params", "tci_env_workspace_size", "tci_env_update", "tci_cplx_conj",
 ]
 
 
@@ -81,6 +81,9 @@ _sig = {
     "tci_contract_workspace_size": ([_vp, _vp, _i32p, _vp, _i32p, _vp, _i32p, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tci_heff_workspace_size": ([_vp, ctypes.c_int] + [ctypes.c_int64] * 8 + [ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tci_heff_apply": ([_vp] * 7, ctypes.c_int),
+    "tci_env_workspace_size": ([_vp, ctypes.c_int] + [_vp] * 5 + [ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tci_env_update": ([_vp, ctypes.c_int] + [_vp] * 5, ctypes.c_int),
+    "tci_cplx_conj": ([_vp] * 3, ctypes.c_int),
     "tci_tebd_theta": ([_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p], ctypes.c_int),
     "tci_comm_init": ([_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "tci_comm_unique_id": ([ctypes.c_char_p], ctypes.c_int),
@@ -244,6 +247,21 @@ def tci_heff_workspace_size(ctx: int, dtype: int, chi_l, chi_lo, chi_r, chi_ro, 
 
 def tci_heff_apply(ctx: int, L: int, W1: int, W2: int, R: int, psi: int, out: int) -> None:
     _ok(_lib.tci_heff_apply(*[_vp(x) for x in (ctx, L, W1, W2, R, psi, out)]), "tci_heff_apply")
+
+
+def tci_env_workspace_size(ctx: int, side: int, E: int, ket: int, W: int, bra: int, out: int) -> int:
+    n = ctypes.c_size_t()
+    _ok(_lib.tci_env_workspace_size(_vp(ctx), int(side), *[_vp(x) for x in (E, ket, W, bra, out)], ctypes.byref(n)),
+        "tci_env_workspace_size")
+    return n.value
+
+
+def tci_env_update(ctx: int, side: int, E: int, ket: int, W: int, bra: int, out: int) -> None:
+    _ok(_lib.tci_env_update(_vp(ctx), int(side), *[_vp(x) for x in (E, ket, W, bra, out)]), "tci_env_update")
+
+
+def tci_cplx_conj(ctx: int, t_in: int, t_out: int) -> None:
+    _ok(_lib.tci_cplx_conj(_vp(ctx), _vp(t_in), _vp(t_out)), "tci_cplx_conj")
 
 
 def tci_tebd_theta(ctx: int, A: int, la: str, B: int, lb: str, U: int, lu: str, T: int, lt: str) -> None:
@@ -465,6 +483,25 @@ class Context:
         tci_heff_apply(self.handle, *[self.tensor(x) for x in (L, W1, W2, R, psi, out)])
         return out
 
+    def env_update(self, side, E, ket, W, bra=None, out=None):
+        """Environment update (tci_env_update): side 0 = left, 1 = right; bra defaults to ket."""
+        bra = ket if bra is None else bra
+        if out is None:
+            shape = ((ket.shape[2], W.shape[1], bra.shape[2]) if side == 0 else
+                     (ket.shape[0], W.shape[0], bra.shape[0]))
+            out = self.torch.empty(shape, dtype=ket.dtype, device=ket.device)
+        h = [self.tensor(x) for x in (E, ket, W, bra, out)]
+        self.ensure_workspace(tci_env_workspace_size(self.handle, side, *h))
+        tci_env_update(self.handle, side, *h)
+        return out
+
+    def cplx_conj(self, x, out=None):
+        """Complex conjugate (tci_cplx_conj); out=x conjugates in place."""
+        if out is None:
+            out = self.torch.empty_like(x)
+        tci_cplx_conj(self.handle, self.tensor(x), self.tensor(out))
+        return out
+
     def tebd_theta(self, A, la, B, lb, U, lu, lt, out=None):
         if out is None:
             dims = {}
@@ -481,6 +518,10 @@ class Context:
 
     def set_gemm_algorithm(self, algo: int):
         tci_set_gemm_algorithm(self.handle, algo)
+
+    def gemm_algorithm_name(self) -> str:
+        return {TCI_GEMM_DMMA_3M: "dmma3m", TCI_GEMM_DMMA_4M: "dmma4m",
+                TCI_GEMM_OZAKI_INT8: "ozaki"}.get(tci_get_gemm_algorithm(self.handle), "?")
 
     def norm(self, x) -> float:
         return tci_norm(self.handle, self.tensor(x))

@@ -1,6 +1,6 @@
 """Build libtci_b200.so in-tree for sm_100a (nvcc; cross-compiles without a GPU).
 
-    python -m paper_2512_23917_b200.build [--force]
+    python paper_2512_23917_b200/build.py [--force]   (by path: the package import needs the .so)
 
 Each source is compiled to an object under build/ (in parallel), then linked
 with the static CUDA runtime into paper_2512_23917_b200/libtci_b200.so. The

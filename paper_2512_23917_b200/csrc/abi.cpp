@@ -574,6 +574,57 @@ tci_status_t tci_heff_apply(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_
   return heff_exec(ctx, view_of(L), view_of(W1), view_of(W2), view_of(R), view_of(psi), vo);
 }
 
+tci_status_t tci_env_workspace_size(tci_ctx_t ctx, int side, tci_tensor_t E, tci_tensor_t ket, tci_tensor_t W,
+                                    tci_tensor_t bra, tci_tensor_t out, size_t *bytes) {
+  CHECK(check_ctx(ctx));
+  for (tci_tensor_t t : {E, ket, W, bra, out}) CHECK(check_ten(ctx, t, false));
+  if (!bytes) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  return env_bytes(ctx, side, view_of(E), view_of(ket), view_of(W), view_of(bra), view_of(out), bytes);
+}
+
+tci_status_t tci_env_update(tci_ctx_t ctx, int side, tci_tensor_t E, tci_tensor_t ket, tci_tensor_t W,
+                            tci_tensor_t bra, tci_tensor_t out) {
+  CHECK(check_ctx(ctx));
+  for (tci_tensor_t t : {E, ket, W, bra, out}) CHECK(check_ten(ctx, t, true));
+  const View vo = view_of(out);
+  for (tci_tensor_t t : {E, ket, W, bra}) {
+    const View v = view_of(t);
+    const char *x = (const char *)v.data, *y = (const char *)vo.data;
+    if (x < y + vo.bytes() && y < x + v.bytes())
+      TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "env: out overlaps an input");
+  }
+  Verbose vb(ctx, side == 0 ? "env_update_left" : "env_update_right", {E, ket, W, bra});
+  return env_exec(ctx, side, view_of(E), view_of(ket), view_of(W), view_of(bra), vo);
+}
+
+tci_status_t tci_cplx_conj(tci_ctx_t ctx, tci_tensor_t in, tci_tensor_t out) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, in, true));
+  CHECK(check_ten(ctx, out, true));
+  if (in->dtype != out->dtype) TCI_FAIL(TCI_ERR_UNSUPPORTED, "cplx_conj: in and out dtypes differ");
+  if (in->order != out->order) TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "cplx_conj: order mismatch");
+  for (int k = 0; k < in->order; k++)
+    if (in->shape[k] != out->shape[k]) TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "cplx_conj: shapes must be identical");
+  const View vi = view_of(in), vo = view_of(out);
+  if (vi.data != vo.data) {
+    const char *x = (const char *)vi.data, *y = (const char *)vo.data;
+    if (x < y + vo.bytes() && y < x + vi.bytes())
+      TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "cplx_conj: out partially overlaps in (only in == out is allowed)");
+  }
+  Verbose vb(ctx, "cplx_conj", {in});
+  if (in->dtype == TCI_C128 || in->dtype == TCI_C64) {
+    if (in->dtype == TCI_C64) TCI_FAIL(TCI_ERR_UNSUPPORTED, "cplx_conj: complex64 not supported (use complex128)");
+    int64_t n = 1;
+    for (int k = 0; k < in->order; k++) n *= in->shape[k];
+    TCI_CUDA_CHECK(launch_conj(vi.data, vo.data, n, ctx->stream, &ctx->launches));
+    return TCI_OK;
+  }
+  // real element type: (1) in place is a no-op, (2) is a deep copy
+  if (vi.data == vo.data) return TCI_OK;
+  TCI_CUDA_CHECK(launch_copy(vo.data, vi.data, vi.bytes(), ctx->stream, &ctx->launches));
+  return TCI_OK;
+}
+
 tci_status_t tci_tebd_theta(tci_ctx_t ctx, tci_tensor_t A, const char *la, tci_tensor_t B,
                             const char *lb, tci_tensor_t U, const char *lu, tci_tensor_t theta,
                             const char *lt) {

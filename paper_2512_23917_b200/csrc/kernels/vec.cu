@@ -146,4 +146,21 @@ cudaError_t launch_lincomb(bool cplx, const double *const *in, const double *cr,
   return cudaGetLastError();
 }
 
+// complex conjugation: out[i] = (re, -im); in == out allowed.
+// 16-byte elements, grid-stride, one load and one store per element.
+__global__ void __launch_bounds__(RT) conj_kernel(const double2 *in, double2 *out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT) {
+    const double2 v = in[i];
+    out[i] = make_double2(v.x, -v.y);
+  }
+}
+
+cudaError_t launch_conj(const void *in, void *out, int64_t n, cudaStream_t s, int64_t *launches) {
+  const int64_t blocks = std::min<int64_t>((n + RT - 1) / RT, 148 * 8);
+  if (blocks <= 0) return cudaSuccess;
+  conj_kernel<<<(unsigned)blocks, RT, 0, s>>>(static_cast<const double2 *>(in), static_cast<double2 *>(out), n);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
 }  // namespace tci

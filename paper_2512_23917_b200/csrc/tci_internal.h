@@ -175,5 +175,7 @@ cudaError_t launch_lincomb(bool cplx, const double *const *in, const double *cr,
 
 // Plain device copy (aliasing fallback) and elementwise helpers.
 cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s, int64_t *launches);
+// complex128 conjugation of n elements (in == out allowed)
+cudaError_t launch_conj(const void *in, void *out, int64_t n, cudaStream_t s, int64_t *launches);
 
 }  // namespace tci

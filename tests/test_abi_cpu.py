@@ -20,7 +20,12 @@ def declared_symbols():
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2512_23917_b200 import build
+    # build.py by path: the package import itself needs an up-to-date library
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_tci_build", os.path.join(os.path.dirname(HEADER), "..", "paper_2512_23917_b200", "build.py"))
+    build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(build)
     path = build.build()
     return ctypes.CDLL(path)
 

@@ -657,3 +657,112 @@ def test_ozaki_lanczos(ozctx):
     psi = dev(synth.random_tensor((1, 2, 2, 1), "c128", 480, 2))
     e, _ = ozctx.heff_lanczos(L, dev(W), dev(W), R, psi, max_iter=10, tol=1e-15)
     assert abs(e + 0.75) < 1e-13
+
+
+# ---------------------------------------------------------------------------
+# cplx_conj and environment updates (8(f3), R28)
+# ---------------------------------------------------------------------------
+
+def test_cplx_conj(ctx, oracle_mod):
+    x = synth.random_tensor((37, 5, 129), "c128", 600, 1)
+    y = ctx.cplx_conj(dev(x))
+    assert np.array_equal(host(y), oracle_mod.cplx_conj(x.numpy()))     # bitwise
+    d = dev(x)
+    ctx.cplx_conj(d, out=d)                                               # in place (overload (1))
+    assert np.array_equal(host(d), oracle_mod.cplx_conj(x.numpy()))
+    r = synth.random_tensor((33, 7), "r64", 601, 1)
+    rc = ctx.cplx_conj(dev(r))                                            # real: deep copy
+    assert np.array_equal(host(rc), r.numpy())
+    buf = dev(synth.random_tensor((65,), "c128", 602, 1))
+    with pytest.raises(tci.TciError) as e:                                # partial overlap
+        ctx.cplx_conj(buf[:-1], out=buf[1:])
+    assert e.value.code == 8
+    with pytest.raises(tci.TciError) as e:
+        ctx.cplx_conj(dev(x), out=torch.empty((37, 5, 128), dtype=torch.complex128, device="cuda"))
+    assert e.value.code == 1
+
+
+def _env_inputs(side, dt, chi_k, chi_b, chi_ko, chi_bo, D, Dv, d, seed, same_bra=False):
+    E = synth.random_tensor((chi_k, D, chi_b), dt, seed, 1)
+    if side == 0:
+        ket = synth.random_tensor((chi_k, d, chi_ko), dt, seed, 2)
+        W = synth.random_tensor((D, Dv, d, d), dt, seed, 3)
+        bra = ket if same_bra else synth.random_tensor((chi_b, d, chi_bo), dt, seed, 4)
+    else:
+        ket = synth.random_tensor((chi_ko, d, chi_k), dt, seed, 2)
+        W = synth.random_tensor((Dv, D, d, d), dt, seed, 3)
+        bra = ket if same_bra else synth.random_tensor((chi_bo, d, chi_b), dt, seed, 4)
+    return E, ket, W, bra
+
+
+@pytest.mark.parametrize("side", [0, 1])
+@pytest.mark.parametrize("dt", ["c128", "r64"])
+@pytest.mark.parametrize("dims", [(37, 29, 41, 23, 5, 4, 2), (64, 64, 64, 64, 5, 5, 2), (1, 1, 9, 7, 1, 5, 3),
+                                  (20, 33, 17, 70, 6, 6, 4)])
+def test_env_update_vs_oracle(ctx, oracle_mod, side, dt, dims):
+    chi_k, chi_b, chi_ko, chi_bo, D, Dv, d = dims
+    E, ket, W, bra = _env_inputs(side, dt, chi_k, chi_b, chi_ko, chi_bo, D, Dv, d, 610)
+    out = ctx.env_update(side, dev(E), dev(ket), dev(W), dev(bra))
+    f = oracle_mod.env_left if side == 0 else oracle_mod.env_right
+    ref = f(E.numpy(), ket.numpy(), W.numpy(), bra.numpy())
+    assert out.shape == ref.shape
+    assert rel_frob(host(out), ref) <= TOL[dt]
+    again = ctx.env_update(side, dev(E), dev(ket), dev(W), dev(bra))
+    assert torch.equal(out, again)                                        # deterministic
+
+
+def test_env_update_errors(ctx):
+    E, ket, W, bra = _env_inputs(0, "c128", 8, 8, 8, 8, 3, 3, 2, 611)
+    with pytest.raises(tci.TciError) as e:
+        ctx.env_update(0, dev(E), dev(ket), dev(W), dev(bra),
+                       out=torch.empty((8, 3, 9), dtype=torch.complex128, device="cuda"))
+    assert e.value.code == 1
+    with pytest.raises(tci.TciError) as e:
+        ctx.env_update(2, dev(E), dev(ket), dev(W), dev(bra),
+                       out=torch.empty((8, 3, 8), dtype=torch.complex128, device="cuda"))
+    assert e.value.code == 8
+
+
+@pytest.mark.parametrize("side", [0, 1])
+def test_env_heisenberg_expectation_closed_form(ctx, side):
+    """<psi|H|psi> of a random product state through a chain of device
+    environment updates equals the Bloch-vector closed form sum n_i.n_j / 4."""
+    rng = np.random.default_rng(21)
+    n = 12
+    u = rng.standard_normal((n, 2)) + 1j * rng.standard_normal((n, 2))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    bloch = np.stack([2 * (np.conj(u[:, 0]) * u[:, 1]).real, 2 * (np.conj(u[:, 0]) * u[:, 1]).imag,
+                      np.abs(u[:, 0]) ** 2 - np.abs(u[:, 1]) ** 2], axis=1)
+    closed = float(np.sum(bloch[:-1] * bloch[1:]) / 4)
+    W, lb, rb = synth.heisenberg_mpo()
+    Wd = dev(W)
+    sites = [dev(x.reshape(1, 2, 1).astype(np.complex128)) for x in u]
+    if side == 0:
+        E = dev(synth.boundary_env(5, lb))
+        for A in sites:
+            E = ctx.env_update(0, E, A, Wd)
+        got = complex(host(E)[0, rb, 0])
+    else:
+        E = dev(synth.boundary_env(5, rb))
+        for A in reversed(sites):
+            E = ctx.env_update(1, E, A, Wd)
+        got = complex(host(E)[0, lb, 0])
+    assert abs(got - closed) <= 1e-14 and abs(got.imag) <= 1e-15
+
+
+@pytest.mark.parametrize("algo", ["dmma3m", "ozaki"])
+@pytest.mark.parametrize("side", [0, 1])
+def test_env_update_chi1024_sampled(oracle_mod, side, algo):
+    """cfg2 scale (chi = 1024, D = 5, d = 2, c128; both GEMMs take the Ozaki
+    path when selected): sampled output rows vs the oracle."""
+    c = tci.Context(0)
+    if algo == "ozaki":
+        c.set_gemm_algorithm(tci.TCI_GEMM_OZAKI_INT8)
+    try:
+        E, ket, W, bra = _env_inputs(side, "c128", 1024, 1024, 1024, 1024, 5, 5, 2, 612, same_bra=True)
+        out = c.env_update(side, dev(E), dev(ket), dev(W))
+        rows = [0, 1, 511, 1023]
+        ref = oracle_mod.env_rows(side, E.numpy(), ket.numpy(), W.numpy(), bra.numpy(), rows)
+        assert rel_frob(host(out)[rows], ref) <= 1e-12
+    finally:
+        c.close()

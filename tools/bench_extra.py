@@ -132,6 +132,32 @@ def heff_cfg(ctx, name, reps=3):
     return res
 
 
+def env_cfg(ctx, chi=4096, d=2, D=5, reps=3):
+    """Environment updates (8(f3)) at the target scale, both sides, c128:
+    GEMM (E.ket) -> skinny MPO pass -> conj(bra) -> GEMM; bra = ket."""
+    res = {}
+    for side in (0, 1):
+        E = synth.random_tensor((chi, D, chi), "c128", 700, 1, device="cuda")
+        ket = synth.random_tensor((chi, d, chi), "c128", 700, 2, device="cuda")
+        W = synth.random_tensor((D, D, d, d), "c128", 700, 3, device="cuda")
+        out = torch.empty((chi, D, chi), dtype=torch.complex128, device="cuda")
+        f = lambda: ctx.env_update(side, E, ket, W, out=out)  # noqa: E731
+        med, mn = timed(f, reps=reps, warm=1)
+        F = 8.0 * (2 * chi * D * chi * d * chi + chi * chi * (D * d) * (D * d))
+        tci.tci_profile_enable(ctx.handle, True)
+        f()
+        g = tci.tci_profile_query(ctx.handle, tci.PROF_GEMM)
+        sk = tci.tci_profile_query(ctx.handle, tci.PROF_SKINNY)
+        tci.tci_profile_enable(ctx.handle, False)
+        res["left" if side == 0 else "right"] = {
+            "chi": chi, "d": d, "D": D, "tflops": F / med / 1e12, "tflops_best": F / mn / 1e12,
+            "s_per_update": med, "algorithm": ctx.gemm_algorithm_name(),
+            "gemm_share": g["ms"] / 1e3 / med, "skinny_gbs": sk["bytes"] / (sk["ms"] / 1e3) / 1e9 if sk["launches"] else None}
+        del E, ket, W, out
+        torch.cuda.empty_cache()
+    return res
+
+
 def cfg3(ctx):
     c = synth.TEBD_CONFIG
     res = {}
@@ -221,8 +247,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg4,sweep,permute")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "extra.json"))
+    ap.add_argument("--algo", default=None, choices=[None, "dmma3m", "dmma4m", "ozaki"])
     a = ap.parse_args()
     ctx = tci.Context(0)
+    if a.algo:
+        ctx.set_gemm_algorithm({"dmma3m": tci.TCI_GEMM_DMMA_3M, "dmma4m": tci.TCI_GEMM_DMMA_4M,
+                                "ozaki": tci.TCI_GEMM_OZAKI_INT8}[a.algo])
     res = {}
     for k in a.only.split(","):
         if k == "cfg1":
@@ -237,6 +267,8 @@ def main():
             res["sweep"] = sweep(ctx)
         elif k == "permute":
             res["permute"] = permute_bw(ctx)
+        elif k == "env":
+            res["env"] = env_cfg(ctx)
         print(k, json.dumps(res.get(k))[:600], flush=True)
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     json.dump(res, open(a.out, "w"), indent=1)

@@ -332,6 +332,56 @@ def env_rows(side, E, ket, W, bra, rows, threads=None):
     return np.stack(res)
 
 
+def svd(a, k):
+    """tci::svd (PAPER.md:2014-2053): matricize the first k bonds as rows
+    (I = prod d_0..d_{k-1}, J = the rest), A' = U S V^dagger with
+    s_0 >= ... >= s_{kappa-1} >= 0, kappa = min(I, J); fold back to
+    u [d_0..d_{k-1}, kappa], s [kappa] (real), v_dag [kappa, d_k..d_{r-1}].
+    The matrix SVD is the library primitive (LAPACK via numpy)."""
+    a = np.asarray(a)
+    r = a.ndim
+    if not 1 <= k < r:
+        raise ValueError("svd: need 1 <= num_of_bds_as_row < order")
+    I = int(np.prod(a.shape[:k]))
+    J = int(np.prod(a.shape[k:]))
+    U, s, Vh = np.linalg.svd(a.reshape(I, J), full_matrices=False)
+    kappa = min(I, J)
+    return U.reshape(*a.shape[:k], kappa), s, Vh.reshape(kappa, *a.shape[k:])
+
+
+def trunc_chi(s, chi_min, chi_max, target_trunc_err, s_min):
+    """Truncation strategy of tci::trunc_svd (2), PAPER.md:2093-2098, applied
+    to non-increasing s; returns (chi, eps) with eps of PAPER.md:2088-2090:
+    eps(chi) = sum_{i >= chi} s_i^2 / sum_i s_i^2.
+      a) discard all s_i < s_min;
+      b) keep at least chi_min values; if fewer remain after a), keep those;
+      c) grow chi (descending order) until eps <= target_trunc_err or chi = chi_max."""
+    s = [float(x) for x in s]
+    total = sum(x * x for x in s)
+
+    def eps(chi):
+        return (sum(x * x for x in s[chi:]) / total) if total > 0 else 0.0
+
+    remain = sum(1 for x in s if x >= s_min)            # a)
+    if remain <= chi_min:                               # b) stop and retain those
+        chi = remain
+    else:
+        chi = chi_min                                   # b)
+        while chi < min(chi_max, remain) and eps(chi) > target_trunc_err:   # c)
+            chi += 1
+    chi = max(chi, 1)                                   # DESIGN.md R30: never an empty bond
+    return chi, eps(chi)
+
+
+def trunc_svd(a, k, chi_min, chi_max, target_trunc_err, s_min):
+    """tci::trunc_svd (2) (PAPER.md:2055-2098); overload (1) is chi_min = 1,
+    target_trunc_err = 0. Returns (u, s, v_dag, trunc_err) truncated to chi."""
+    u, s, vd = svd(a, k)
+    chi, err = trunc_chi(s, chi_min, chi_max, target_trunc_err, s_min)
+    return (np.ascontiguousarray(u[..., :chi]), np.ascontiguousarray(s[:chi]),
+            np.ascontiguousarray(vd[:chi]), err)
+
+
 # ----------------------------------------------------------------------------
 # vector functions (App. C.5): definitions written out
 # ----------------------------------------------------------------------------

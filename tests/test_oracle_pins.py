@@ -655,3 +655,78 @@ def test_env_random_mpo_vs_dense_operator(oracle_mod, side):
     ref = np.vdot(phi, O @ psi)
     got = _env_expectation(oracle_mod, ket, W, lb, rb, bra=bra, side=side)
     assert abs(got - ref) <= 1e-12 * abs(ref)
+
+
+# ---------------------------------------------------------------------------
+# svd / trunc_svd, SURVEY 8(f2)
+# ---------------------------------------------------------------------------
+
+def _unitary(n, seed):
+    rng = np.random.default_rng(seed)
+    q, r = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    return q * (np.diag(r) / np.abs(np.diag(r)))
+
+
+def test_svd_paper_example_shapes(oracle_mod):
+    a = rnd((3, 4, 12), 150, cplx=True)
+    u, s, vd = oracle_mod.svd(a, 2)
+    assert u.shape == (3, 4, 12) and s.shape == (12,) and vd.shape == (12, 12)
+    assert np.all(np.diff(s) <= 0) and np.all(s >= 0)
+    rec = np.einsum("ijk,k,kl->ijl", u, s, vd)
+    assert rel_frob(rec, a) <= 1e-14
+    w = rnd((2, 3, 5, 7), 151)                            # wide matricization: kappa = min(6, 35)
+    u, s, vd = oracle_mod.svd(w, 2)
+    assert u.shape == (2, 3, 6) and vd.shape == (6, 5, 7)
+    U = u.reshape(6, 6)
+    assert max_abs(U.T @ U, np.eye(6)) <= 1e-14
+
+
+def test_svd_prescribed_spectrum(oracle_mod):
+    """A = Q1 diag(sigma) Q2^H with random unitaries: the returned s is sigma
+    (sorted), u/v_dag reproduce A and are orthonormal."""
+    m, n = 24, 17
+    sig = np.sort(np.abs(np.random.default_rng(3).standard_normal(n)) + 0.1)[::-1]
+    A = _unitary(m, 4)[:, :n] @ np.diag(sig) @ _unitary(n, 5).conj().T
+    u, s, vd = oracle_mod.svd(A.reshape(4, 6, n), 2)
+    assert max_abs(s, sig) <= 1e-14 * sig[0]
+    U = u.reshape(m, n)
+    assert max_abs(U.conj().T @ U, np.eye(n)) <= 1e-14
+    assert max_abs(vd @ vd.conj().T, np.eye(n)) <= 1e-14
+    assert rel_frob((U * s) @ vd, A) <= 1e-14
+
+
+@pytest.mark.parametrize("args,chi,num,den", [
+    ((1, 3, 0.0, 1e-12), 3, Fraction(5, 4), None),          # overload (1): chi_max = 3
+    ((2, 5, 0.05, 1e-12), 3, Fraction(5, 4), None),         # c) grows 2 -> 3 (eps 0.174 > 0.05 >= 0.041)
+    ((6, 9, 0.0, 1e-12), 5, None, None),                    # b) fewer than chi_min survive a): keep 5
+    ((1, 10, 0.0, 0.0), 6, Fraction(0), None),              # nothing discarded
+    ((1, 10, 0.0, 5.0), 1, None, None),                     # all below s_min: R30 keeps one
+    ((4, 4, 0.5, 1e-12), 4, Fraction(1, 4), None),          # chi_min = chi_max
+])
+def test_trunc_chi_strategy(oracle_mod, args, chi, num, den):
+    s = [4.0, 3.0, 2.0, 1.0, 0.5, 1e-13]
+    total = Fraction(16) + 9 + 4 + 1 + Fraction(1, 4) + Fraction(1e-13) ** 2
+    got_chi, eps = oracle_mod.trunc_chi(s, *args)
+    assert got_chi == chi
+    exact = sum((Fraction(x) ** 2 for x in s[chi:]), Fraction(0)) / total     # P:2088-2090
+    assert abs(eps - float(exact)) <= 1e-16
+    if num is not None:
+        assert abs(eps - float(num / total)) <= 1e-15
+
+
+def test_trunc_svd_paper_example(oracle_mod):
+    a = rnd((3, 4, 12), 152)                              # P:2104-2110
+    u, s, vd, err = oracle_mod.trunc_svd(a, 2, 3, 6, 1e-2, 1e-12)
+    assert err != 0.0 and 3 <= s.shape[0] <= 6
+    assert u.shape == (3, 4, s.shape[0]) and vd.shape == (s.shape[0], 12)
+
+
+def test_trunc_svd_fidelity_identity(oracle_mod):
+    """Section III (R24): with a normalized psi and psi1 = u s v_dag
+    from trunc_svd, <psi|psi1> = 1 - trunc_err."""
+    psi = rnd((2, 2, 2, 2, 2, 2), 153)
+    psi = psi / np.sqrt(np.sum(psi * psi))
+    u, s, vd, err = oracle_mod.trunc_svd(psi, 3, 1, 3, 0.0, 0.0)
+    psi1 = np.einsum("ijka,a,alm n->ijklmn".replace(" ", ""), u, s, vd)
+    ovlp = float(np.sum(psi * psi1))
+    assert err > 0 and abs(ovlp - (1 - err)) <= 1e-14

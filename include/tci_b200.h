@@ -411,6 +411,61 @@ TCI_API int tci_heff_plan_tree(int64_t chi_l, int64_t chi_lo, int64_t chi_r, int
                                int64_t d, int64_t D, int64_t D1, int64_t D2, char *buf, int n,
                                double *macs);
 
+/* ---------------------------------------------------------------------- */
+/* Singular value decomposition: tci::svd / tci::trunc_svd  */
+/* ---------------------------------------------------------------------- */
+
+/* Scratch bytes tci_svd / tci_trunc_svd need for a tensor of this dtype and
+ * shape matricized with the first num_of_bds_as_row bonds as rows: two
+ * working matrices of min(I,J) x max(I,J) and min(I,J)^2 elements (rounded
+ * up to multiples of 32) plus O(min(I,J)) vectors.
+ * Errors: UNSUPPORTED (dtype other than r64 / c128), OUT_OF_RANGE (k). */
+TCI_API tci_status_t tci_svd_workspace_size(tci_ctx_t ctx, tci_dtype_t dtype, int order, const int64_t *shape,
+                                            int num_of_bds_as_row, size_t *bytes);
+
+/* tci::svd. a (order r, shape {d_0..d_{r-1}}, r64 or c128) is
+ * matricized by grouping the first k = num_of_bds_as_row bonds into the row
+ * index (1 <= k < r): A' is I x J, I = prod_{b<k} d_b, J = prod_{b>=k} d_b
+ * (row-major, metadata only). A' = U S V^dagger with s_0 >= s_1 >= ... >=
+ * s_{kappa-1} >= 0, kappa = min(I, J), folded back:
+ *   u      [d_0, .., d_{k-1}, kappa]   dtype of a
+ *   s_diag [kappa]                     r64 (real_ten_t), non-increasing
+ *   v_dag  [kappa, d_k, .., d_{r-1}]   dtype of a
+ * All three are caller-allocated device tensors of exactly these shapes;
+ * none may overlap a; a is not modified. Scratch: tci_svd_workspace_size.
+ * Method: block one-sided Jacobi on the FP64 tensor cores:
+ * singular values to ~1e-14 relative to s_0, u and v_dag orthonormal to
+ * ~1e-13; where s_i = 0 exactly the singular vector is completed to an
+ * orthonormal set (R29). Synchronous (returns after the result is written).
+ * Errors: UNSUPPORTED (dtype; u/v_dag dtype != a's, s_diag not r64),
+ * OUT_OF_RANGE (k), ORDER_MISMATCH / SHAPE_MISMATCH (output descriptors),
+ * INVALID_ARGUMENT (overlap), WORKSPACE, CUDA, DEAD_CONTEXT. */
+TCI_API tci_status_t tci_svd(tci_ctx_t ctx, tci_tensor_t a, int num_of_bds_as_row, tci_tensor_t u,
+                             tci_tensor_t s_diag, tci_tensor_t v_dag);
+
+/* tci::trunc_svd, overload (2); overload (1) is chi_min = 1,
+ * target_trunc_err = 0. The SVD as tci_svd, then the strategy of
+ * P:2093-2098 on the pre-truncation s_0 >= .. >= s_{kappa-1}:
+ *   a) discard all s_i < s_min; b) keep at least chi_min values, and if fewer
+ *   remain after a) keep those; c) grow chi in descending order until
+ *   eps <= target_trunc_err or chi = chi_max; chi >= 1 always (R30).
+ * eps = sum_{i>=chi} s_i^2 / sum_i s_i^2 -> *trunc_err.
+ * The output descriptors are passed with the CAPACITY shape, cap =
+ * min(max(chi_min, chi_max), kappa) in the chi position (u [.., cap], s_diag
+ * [cap], v_dag [cap, ..]); on success they are reshaped (metadata) to chi and
+ * their buffers hold the dense row-major truncated tensors. *chi_out (may be
+ * NULL) receives chi. Errors as tci_svd, plus OUT_OF_RANGE (chi_max < 1,
+ * chi_min < 0, negative target_trunc_err or s_min). */
+TCI_API tci_status_t tci_trunc_svd(tci_ctx_t ctx, tci_tensor_t a, int num_of_bds_as_row, tci_tensor_t u,
+                                   tci_tensor_t s_diag, tci_tensor_t v_dag, double *trunc_err, int64_t chi_min,
+                                   int64_t chi_max, double target_trunc_err, double s_min, int64_t *chi_out);
+
+/* Diagnostics of the last tci_svd / tci_trunc_svd on this context: Jacobi
+ * sweeps executed and the final sweep's largest relative off-diagonal
+ * |<x_i|x_j>| / (|x_i| |x_j|) (convergence: <= max(1e-13, 4 sqrt(max(I,J)) eps),
+ * env TCI_SVD_TOL overrides). */
+TCI_API tci_status_t tci_svd_info(tci_ctx_t ctx, int *sweeps, double *off);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,6 +46,7 @@ EXPORTED = [
     "tci_mps_overlap", "tci_norm", "tci_normalize", "tci_scale", "tci_linear_combine", "tci_inner",
     "tci_lanczos_workspace_size", "tci_heff_lanczos", "tci_set_gemm_algorithm", "tci_get_gemm_algorithm",
     "tci_ozaki_params", "tci_env_workspace_size", "tci_env_update", "tci_cplx_conj",
+    "tci_svd_workspace_size", "tci_svd", "tci_trunc_svd", "tci_svd_info",
 ]
 
 
@@ -84,6 +85,12 @@ _sig = {
     "tci_env_workspace_size": ([_vp, ctypes.c_int] + [_vp] * 5 + [ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tci_env_update": ([_vp, ctypes.c_int] + [_vp] * 5, ctypes.c_int),
     "tci_cplx_conj": ([_vp] * 3, ctypes.c_int),
+    "tci_svd_workspace_size": ([_vp, ctypes.c_int, ctypes.c_int, _i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)],
+                               ctypes.c_int),
+    "tci_svd": ([_vp, _vp, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
+    "tci_trunc_svd": ([_vp, _vp, ctypes.c_int, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
+                       ctypes.c_int64, ctypes.c_double, ctypes.c_double, _i64p], ctypes.c_int),
+    "tci_svd_info": ([_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tci_tebd_theta": ([_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p], ctypes.c_int),
     "tci_comm_init": ([_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "tci_comm_unique_id": ([ctypes.c_char_p], ctypes.c_int),
@@ -262,6 +269,35 @@ def tci_env_update(ctx: int, side: int, E: int, ket: int, W: int, bra: int, out:
 
 def tci_cplx_conj(ctx: int, t_in: int, t_out: int) -> None:
     _ok(_lib.tci_cplx_conj(_vp(ctx), _vp(t_in), _vp(t_out)), "tci_cplx_conj")
+
+
+def tci_svd_workspace_size(ctx: int, dtype: int, shape: Sequence[int], num_of_bds_as_row: int) -> int:
+    n = ctypes.c_size_t()
+    _ok(_lib.tci_svd_workspace_size(_vp(ctx), int(dtype), len(shape), _i64arr(shape), int(num_of_bds_as_row),
+                                    ctypes.byref(n)), "tci_svd_workspace_size")
+    return n.value
+
+
+def tci_svd(ctx: int, a: int, num_of_bds_as_row: int, u: int, s_diag: int, v_dag: int) -> None:
+    _ok(_lib.tci_svd(_vp(ctx), _vp(a), int(num_of_bds_as_row), _vp(u), _vp(s_diag), _vp(v_dag)), "tci_svd")
+
+
+def tci_trunc_svd(ctx: int, a: int, num_of_bds_as_row: int, u: int, s_diag: int, v_dag: int, chi_min: int,
+                  chi_max: int, target_trunc_err: float, s_min: float) -> Tuple[float, int]:
+    """Returns (trunc_err, chi); the u / s_diag / v_dag descriptors are reshaped to chi."""
+    err = ctypes.c_double()
+    chi = ctypes.c_int64()
+    _ok(_lib.tci_trunc_svd(_vp(ctx), _vp(a), int(num_of_bds_as_row), _vp(u), _vp(s_diag), _vp(v_dag),
+                           ctypes.byref(err), int(chi_min), int(chi_max), float(target_trunc_err), float(s_min),
+                           ctypes.byref(chi)), "tci_trunc_svd")
+    return err.value, chi.value
+
+
+def tci_svd_info(ctx: int) -> Tuple[int, float]:
+    sw = ctypes.c_int()
+    off = ctypes.c_double()
+    _ok(_lib.tci_svd_info(_vp(ctx), ctypes.byref(sw), ctypes.byref(off)), "tci_svd_info")
+    return sw.value, off.value
 
 
 def tci_tebd_theta(ctx: int, A: int, la: str, B: int, lb: str, U: int, lu: str, T: int, lt: str) -> None:
@@ -515,6 +551,56 @@ class Context:
         tci_tebd_theta(self.handle, self.tensor(A), la, self.tensor(B), lb, self.tensor(U), lu,
                        self.tensor(out), lt)
         return out
+
+    def _svd_outputs(self, a, k, cap):
+        torch = self.torch
+        u = torch.empty(tuple(a.shape[:k]) + (cap,), dtype=a.dtype, device=a.device)
+        s = torch.empty((cap,), dtype=torch.float64, device=a.device)
+        vd = torch.empty((cap,) + tuple(a.shape[k:]), dtype=a.dtype, device=a.device)
+        return u, s, vd
+
+    def _fresh(self, t) -> int:
+        # uncached descriptor (trunc_svd reshapes its outputs' descriptors)
+        return tci_tensor_create(self.handle, _torch_dtype_code(t), tuple(t.shape), t.data_ptr())
+
+    def svd(self, a, num_of_bds_as_row):
+        """tci::svd (P:2014-2053): returns (u, s_diag, v_dag)."""
+        k = int(num_of_bds_as_row)
+        I = 1
+        for x in a.shape[:k]:
+            I *= int(x)
+        kappa = min(I, a.numel() // max(I, 1))
+        u, s, vd = self._svd_outputs(a, k, kappa)
+        self.ensure_workspace(tci_svd_workspace_size(self.handle, _torch_dtype_code(a), tuple(a.shape), k))
+        tci_svd(self.handle, self.tensor(a), k, self.tensor(u), self.tensor(s), self.tensor(vd))
+        return u, s, vd
+
+    def trunc_svd(self, a, num_of_bds_as_row, chi_min, chi_max, target_trunc_err, s_min):
+        """tci::trunc_svd (2) (P:2055-2098): returns (u, s_diag, v_dag, trunc_err),
+        truncated to the chi the strategy keeps."""
+        k = int(num_of_bds_as_row)
+        I = 1
+        for x in a.shape[:k]:
+            I *= int(x)
+        kappa = min(I, a.numel() // max(I, 1))
+        cap = min(max(int(chi_min), int(chi_max)), kappa)
+        u, s, vd = self._svd_outputs(a, k, max(cap, 1))
+        self.ensure_workspace(tci_svd_workspace_size(self.handle, _torch_dtype_code(a), tuple(a.shape), k))
+        hs = [self._fresh(x) for x in (u, s, vd)]
+        try:
+            err, chi = tci_trunc_svd(self.handle, self.tensor(a), k, *hs, chi_min, chi_max, target_trunc_err,
+                                     s_min)
+        finally:
+            for h in hs:
+                tci_tensor_free(self.handle, h)
+        # the buffers hold the dense truncated tensors: view them with the chi shapes
+        u = u.view(-1)[: u.numel() // cap * chi].view(tuple(a.shape[:k]) + (chi,))
+        s = s[:chi]
+        vd = vd.view(-1)[: vd.numel() // cap * chi].view((chi,) + tuple(a.shape[k:]))
+        return u, s, vd, err
+
+    def svd_info(self):
+        return tci_svd_info(self.handle)
 
     def set_gemm_algorithm(self, algo: int):
         tci_set_gemm_algorithm(self.handle, algo)

@@ -222,6 +222,8 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   }
   c->dev_scratch = nullptr;
   c->host_scratch = nullptr;
+  c->svd_last_sweeps = 0;
+  c->svd_last_off = 0.0;
   {
     cudaError_t e1 = cudaMalloc(&c->dev_scratch, reduce_scratch_bytes());
     cudaError_t e2 = cudaMallocHost(&c->host_scratch, 64);
@@ -622,6 +624,43 @@ tci_status_t tci_cplx_conj(tci_ctx_t ctx, tci_tensor_t in, tci_tensor_t out) {
   // real element type: (1) in place is a no-op, (2) is a deep copy
   if (vi.data == vo.data) return TCI_OK;
   TCI_CUDA_CHECK(launch_copy(vo.data, vi.data, vi.bytes(), ctx->stream, &ctx->launches));
+  return TCI_OK;
+}
+
+tci_status_t tci_svd_workspace_size(tci_ctx_t ctx, tci_dtype_t dtype, int order, const int64_t *shape,
+                                    int num_of_bds_as_row, size_t *bytes) {
+  CHECK(check_ctx(ctx));
+  if (!shape || !bytes) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL shape or out");
+  if (order < 0 || order > kMaxOrder) TCI_FAIL(TCI_ERR_UNSUPPORTED, "order %d > %d", order, kMaxOrder);
+  return svd_bytes(dtype, order, shape, num_of_bds_as_row, bytes);
+}
+
+static tci_status_t svd_common(tci_ctx_t ctx, tci_tensor_t a, int k, tci_tensor_t u, tci_tensor_t s,
+                               tci_tensor_t v, bool trunc, double *err, int64_t chi_min, int64_t chi_max,
+                               double target, double s_min, int64_t *chi_out) {
+  CHECK(check_ctx(ctx));
+  for (tci_tensor_t t : {a, u, s, v}) CHECK(check_ten(ctx, t, true));
+  Verbose vb(ctx, trunc ? "trunc_svd" : "svd", {a});
+  return svd_exec(ctx, view_of(a), k, trunc, chi_min, chi_max, target, s_min, u, s, v, err, chi_out);
+}
+
+tci_status_t tci_svd(tci_ctx_t ctx, tci_tensor_t a, int num_of_bds_as_row, tci_tensor_t u, tci_tensor_t s_diag,
+                     tci_tensor_t v_dag) {
+  return svd_common(ctx, a, num_of_bds_as_row, u, s_diag, v_dag, false, nullptr, 0, 0, 0.0, 0.0, nullptr);
+}
+
+tci_status_t tci_trunc_svd(tci_ctx_t ctx, tci_tensor_t a, int num_of_bds_as_row, tci_tensor_t u,
+                           tci_tensor_t s_diag, tci_tensor_t v_dag, double *trunc_err, int64_t chi_min,
+                           int64_t chi_max, double target_trunc_err, double s_min, int64_t *chi_out) {
+  if (!trunc_err) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "trunc_svd: NULL trunc_err");
+  return svd_common(ctx, a, num_of_bds_as_row, u, s_diag, v_dag, true, trunc_err, chi_min, chi_max,
+                    target_trunc_err, s_min, chi_out);
+}
+
+tci_status_t tci_svd_info(tci_ctx_t ctx, int *sweeps, double *off) {
+  CHECK(check_ctx(ctx));
+  if (sweeps) *sweeps = ctx->svd_last_sweeps;
+  if (off) *off = ctx->svd_last_off;
   return TCI_OK;
 }
 

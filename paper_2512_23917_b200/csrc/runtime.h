@@ -36,6 +36,8 @@ struct tci_ctx_s {
   int zgemm_algo;       // complex128 GEMM algorithm (kZ3M default; tci_set_gemm_algorithm)
   void *dev_scratch;    // reductions (vec.cu): allocated once at creation
   void *host_scratch;   // pinned, reduction results
+  int svd_last_sweeps;  // Jacobi sweeps of the last svd / trunc_svd (tci_svd_info)
+  double svd_last_off;  // its final off-diagonal measure
 };
 
 struct tci_tensor_s {
@@ -142,5 +144,11 @@ tci_status_t env_bytes(tci_ctx_s *ctx, int side, const View &E, const View &K, c
                        const View &O, size_t *bytes);
 tci_status_t env_exec(tci_ctx_s *ctx, int side, const View &E, const View &K, const View &W, const View &B,
                       const View &O);
+
+// SVD (svd.cpp)
+tci_status_t svd_bytes(tci_dtype_t dt, int order, const int64_t *shape, int k, size_t *bytes);
+tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t chi_min, int64_t chi_max,
+                      double target, double s_min, tci_tensor_s *tu, tci_tensor_s *ts, tci_tensor_s *tv,
+                      double *trunc_err, int64_t *chi_out);
 
 }  // namespace tci

@@ -1,0 +1,234 @@
+// svd.cpp -- tci::svd / tci::trunc_svd on the
+// block one-sided Jacobi kernels of kernels/svd.cu.
+//
+// Steps (all compute in kernels; the host keeps only integer / scalar logic):
+//   1. matricize (first k bonds are rows, I x J, metadata only)
+//      and load X = A' (I <= J) or A'^H (I > J) into the workspace, Y = I;
+//   2. Jacobi sweeps (nb - 1 round launches each) until the sweep's largest
+//      relative off-diagonal measure is <= tol (one 8-byte D2H per sweep);
+//   3. row norms s_i; the n values are copied to the host and ordered
+//      s_0 >= s_1 >= ... (stable: ties keep row order);
+//   4. trunc_svd: chi and trunc_err by the strategy of P:2093-2098 with the
+//      error of P:2088-2090, evaluated exactly as the oracle does;
+//   5. gather the chi selected rows into u [d_0..d_{k-1}, chi], s [chi],
+//      v_dag [chi, d_k..d_{r-1}]; the output descriptors are
+//      reshaped to chi (metadata).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "runtime.h"
+
+namespace tci {
+namespace {
+
+struct SvdDims {
+  int64_t I, J, n, L, npad, ldx, ldy;
+  bool tall;
+  size_t off_x, off_y, off_s, off_sn, off_perm, off_zl, off_off, total;
+};
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+tci_status_t svd_dims(tci_dtype_t dt, int order, const int64_t *shape, int k, SvdDims &d) {
+  if (dt != TCI_R64 && dt != TCI_C128) TCI_FAIL(TCI_ERR_UNSUPPORTED, "svd: dtype must be r64 or c128");
+  if (k < 1 || k >= order)
+    TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "svd: need 1 <= num_of_bds_as_row (%d) < order (%d) (P:2030)", k, order);
+  d.I = 1;
+  d.J = 1;
+  for (int i = 0; i < order; i++) (i < k ? d.I : d.J) *= shape[i];
+  d.tall = d.I > d.J;
+  d.n = std::min(d.I, d.J);
+  d.L = std::max(d.I, d.J);
+  d.npad = round_up(d.n, 32);
+  d.ldx = round_up(d.L, 64);
+  d.ldy = round_up(d.npad, 64);
+  const size_t es = dtype_size(dt);
+  size_t o = 0;
+  d.off_x = o;
+  o = align_up(o + (size_t)d.npad * d.ldx * es);
+  d.off_y = o;
+  o = align_up(o + (size_t)d.npad * d.ldy * es);
+  d.off_s = o;
+  o = align_up(o + (size_t)d.npad * 8);
+  d.off_sn = o;
+  o = align_up(o + (size_t)d.npad * 8);
+  d.off_perm = o;
+  o = align_up(o + (size_t)d.npad * 4);
+  d.off_zl = o;
+  o = align_up(o + (size_t)d.npad * 4);
+  d.off_off = o;
+  o = align_up(o + 8);
+  d.total = o;
+  return TCI_OK;
+}
+
+double default_tol(int64_t L) {
+  const char *e = getenv("TCI_SVD_TOL");
+  if (e && *e) return atof(e);
+  return std::max(1e-13, 4.0 * std::sqrt((double)L) * 2.220446049250313e-16);
+}
+
+// tci::trunc_svd (2), on non-increasing s[0..n); the same
+// arithmetic (sequential sums in index order) as oracle.trunc_chi.
+int64_t trunc_chi(const std::vector<double> &s, int64_t chi_min, int64_t chi_max, double target, double s_min,
+                  double *eps_out) {
+  const int64_t n = (int64_t)s.size();
+  double total = 0.0;
+  for (double x : s) total += x * x;
+  auto eps = [&](int64_t chi) {
+    if (!(total > 0.0)) return 0.0;
+    double t = 0.0;
+    for (int64_t i = chi; i < n; i++) t += s[i] * s[i];
+    return t / total;
+  };
+  int64_t remain = 0;
+  for (double x : s) remain += x >= s_min;                    // a)
+  int64_t chi;
+  if (remain <= chi_min) {
+    chi = remain;                                              // b) stop and retain those
+  } else {
+    chi = chi_min;                                             // b)
+    while (chi < std::min(chi_max, remain) && eps(chi) > target) chi++;   // c)
+  }
+  chi = std::max<int64_t>(chi, 1);                             // R30: never an empty bond
+  *eps_out = eps(chi);
+  return chi;
+}
+
+}  // namespace
+
+tci_status_t svd_bytes(tci_dtype_t dt, int order, const int64_t *shape, int k, size_t *bytes) {
+  SvdDims d;
+  tci_status_t st = svd_dims(dt, order, shape, k, d);
+  if (st) return st;
+  *bytes = d.total;
+  return TCI_OK;
+}
+
+tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t chi_min, int64_t chi_max,
+                      double target, double s_min, tci_tensor_s *tu, tci_tensor_s *ts, tci_tensor_s *tv,
+                      double *trunc_err, int64_t *chi_out) {
+  SvdDims d;
+  tci_status_t st = svd_dims(a.dtype, a.order, a.shape, k, d);
+  if (st) return st;
+  if (trunc) {
+    if (chi_max < 1 || chi_min < 0)
+      TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "trunc_svd: need chi_max >= 1 and chi_min >= 0");
+    if (!(target >= 0.0) || !(s_min >= 0.0))
+      TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "trunc_svd: target_trunc_err and s_min must be >= 0");
+  }
+  // output capacity: kappa for svd, min(max(chi_min, chi_max), kappa) for trunc_svd (R31)
+  const int64_t cap = trunc ? std::min(std::max(chi_min, chi_max), d.n) : d.n;
+  const int r = a.order;
+  if (tu->dtype != a.dtype || tv->dtype != a.dtype || ts->dtype != TCI_R64)
+    TCI_FAIL(TCI_ERR_UNSUPPORTED, "svd: u / v_dag must have a's dtype and s_diag must be r64 (real_ten_t)");
+  if (tu->order != k + 1 || ts->order != 1 || tv->order != r - k + 1)
+    TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "svd: orders must be u %d, s_diag 1, v_dag %d", k + 1, r - k + 1);
+  bool ok = tu->shape[k] == cap && ts->shape[0] == cap && tv->shape[0] == cap;
+  for (int i = 0; i < k; i++) ok = ok && tu->shape[i] == a.shape[i];
+  for (int i = k; i < r; i++) ok = ok && tv->shape[i - k + 1] == a.shape[i];
+  if (!ok)
+    TCI_FAIL(TCI_ERR_SHAPE_MISMATCH,
+             "svd: need u [d_0..d_{k-1}, %lld], s_diag [%lld], v_dag [%lld, d_k..d_{r-1}] (P:2037-2039)",
+             (long long)cap, (long long)cap, (long long)cap);
+  const View vu = view_of(tu), vv = view_of(tv), vs = view_of(ts);
+  for (const View *o : {&vu, &vv, &vs}) {
+    const char *x = (const char *)a.data, *y = (const char *)o->data;
+    if (x < y + o->bytes() && y < x + a.bytes()) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "svd: an output overlaps a");
+  }
+  if (ctx->ws_bytes < d.total || (d.total && !ctx->ws))
+    TCI_FAIL(TCI_ERR_WORKSPACE, "svd: workspace %zu B < %zu B (tci_svd_workspace_size)", ctx->ws_bytes, d.total);
+
+  char *ws = static_cast<char *>(ctx->ws);
+  SvdProblem p;
+  p.cplx = a.dtype == TCI_C128;
+  p.tall = d.tall;
+  p.n = d.n;
+  p.L = d.L;
+  p.npad = d.npad;
+  p.ldx = d.ldx;
+  p.ldy = d.ldy;
+  p.X = ws + d.off_x;
+  p.Y = ws + d.off_y;
+  p.s = reinterpret_cast<double *>(ws + d.off_s);
+  p.offmax = reinterpret_cast<unsigned long long *>(ws + d.off_off);
+  double *snorm = reinterpret_cast<double *>(ws + d.off_sn);
+  int *perm = reinterpret_cast<int *>(ws + d.off_perm);
+  int *zl = reinterpret_cast<int *>(ws + d.off_zl);
+  cudaStream_t s = ctx->stream;
+
+  TCI_CUDA_CHECK(launch_svd_load(p, a.data, d.I, d.J, s, &ctx->launches));
+  const double tol = default_tol(d.L);
+  const double tol_in = 0.25 * tol;
+  int max_inner = 1;
+  if (const char *e = getenv("TCI_SVD_INNER")) max_inner = std::max(1, atoi(e));
+  const bool trace = getenv("TCI_SVD_TRACE") != nullptr;
+  const int nb = (int)(d.npad / 16);
+  const int max_sweeps = 60;
+  unsigned long long offbits = 0;
+  int sweeps = 0;
+  for (; sweeps < max_sweeps;) {
+    TCI_CUDA_CHECK(cudaMemsetAsync(p.offmax, 0, 8, s));
+    for (int rd = 0; rd < nb - 1; rd++) TCI_CUDA_CHECK(launch_svd_round(p, rd, tol, tol_in, max_inner, s, &ctx->launches));
+    TCI_CUDA_CHECK(cudaMemcpyAsync(&offbits, p.offmax, 8, cudaMemcpyDeviceToHost, s));
+    TCI_CUDA_CHECK(cudaStreamSynchronize(s));
+    sweeps++;
+    double off;
+    memcpy(&off, &offbits, 8);
+    ctx->svd_last_off = off;
+    if (trace) fprintf(stderr, "tci:svd sweep %d off=%.3e\n", sweeps, off);
+    if (!(off > tol)) break;
+  }
+  ctx->svd_last_sweeps = sweeps;
+  TCI_CUDA_CHECK(launch_svd_norms(p, s, &ctx->launches));
+  std::vector<double> sh(d.npad);
+  TCI_CUDA_CHECK(cudaMemcpyAsync(sh.data(), p.s, d.npad * 8, cudaMemcpyDeviceToHost, s));
+  TCI_CUDA_CHECK(cudaStreamSynchronize(s));
+  std::vector<int> order(d.npad);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sh[x] > sh[y]; });
+  order.resize(d.n);   // padding rows are exact zeros with the largest indices: sorted last
+  std::vector<double> ss(d.n);
+  for (int64_t i = 0; i < d.n; i++) ss[i] = sh[order[i]];
+  int64_t chi = d.n;
+  double eps = 0.0;
+  if (trunc) chi = trunc_chi(ss, chi_min, chi_max, target, s_min, &eps);
+  // numerically zero rows (s_i <= 1e-18 s_0, reading R29): their singular
+  // vectors are completed to an orthonormal set; s_i is reported as computed
+  std::vector<int> zeros;
+  for (int64_t i = 0; i < chi; i++)
+    if (!(ss[i] > 1e-18 * ss[0])) zeros.push_back(order[i]);
+  TCI_CUDA_CHECK(cudaMemcpyAsync(perm, order.data(), chi * sizeof(int), cudaMemcpyHostToDevice, s));
+  TCI_CUDA_CHECK(cudaMemcpyAsync(snorm, p.s, d.npad * 8, cudaMemcpyDeviceToDevice, s));
+  if (!zeros.empty()) {
+    TCI_CUDA_CHECK(cudaMemcpyAsync(zl, zeros.data(), zeros.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    TCI_CUDA_CHECK(launch_svd_complete(p, perm, chi, snorm, zl, (int)zeros.size(), s, &ctx->launches));
+  }
+  // A' = U diag(s) V^H: wide  U[r][k] = conj(Y[perm k][r]),          V^H[k][c] = X[perm k][c] / s
+  //                      tall  U[r][k] = conj(X[perm k][r]) / s,      V^H[k][c] = Y[perm k][c]
+  if (!d.tall) {
+    TCI_CUDA_CHECK(launch_svd_gather_t(p.cplx, tu->data, p.Y, d.ldy, perm, nullptr, chi, d.I, 1, s, &ctx->launches));
+    TCI_CUDA_CHECK(launch_svd_gather_rows(p.cplx, tv->data, d.J, p.X, d.ldx, perm, snorm, chi, d.J, 0, s,
+                                          &ctx->launches));
+  } else {
+    TCI_CUDA_CHECK(launch_svd_gather_t(p.cplx, tu->data, p.X, d.ldx, perm, snorm, chi, d.I, 1, s, &ctx->launches));
+    TCI_CUDA_CHECK(launch_svd_gather_rows(p.cplx, tv->data, d.J, p.Y, d.ldy, perm, nullptr, chi, d.J, 0, s,
+                                          &ctx->launches));
+  }
+  TCI_CUDA_CHECK(launch_svd_gather_s(static_cast<double *>(ts->data), p.s, perm, chi, s, &ctx->launches));
+  // the host vectors above are pageable: the copies complete before return
+  TCI_CUDA_CHECK(cudaStreamSynchronize(s));
+  tu->shape[k] = chi;
+  ts->shape[0] = chi;
+  tv->shape[0] = chi;
+  if (trunc_err) *trunc_err = eps;
+  if (chi_out) *chi_out = chi;
+  return TCI_OK;
+}
+
+}  // namespace tci

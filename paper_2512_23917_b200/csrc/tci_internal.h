@@ -178,4 +178,39 @@ cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s
 // complex128 conjugation of n elements (in == out allowed)
 cudaError_t launch_conj(const void *in, void *out, int64_t n, cudaStream_t s, int64_t *launches);
 
+// ---------------------------------------------------------------------------
+// Matrix SVD by block one-sided Jacobi (svd.cu).
+// X: npad x ldx working rows (X = A' if I <= J, else A'^H), Y: npad x ldy
+// accumulated rotations (Y0 = I). cplx = complex128, else float64.
+// ---------------------------------------------------------------------------
+struct SvdProblem {
+  bool cplx;
+  int tall;              // 1: X = A'^H (I > J)
+  int64_t n, L;          // rows being orthogonalised (min(I,J)) and their length (max(I,J))
+  int64_t npad, ldx;     // n rounded up to 32; L rounded up to 64 (X row pitch)
+  int64_t ldy;           // Y row pitch: npad rounded up to 64
+  void *X, *Y;
+  double *s;             // npad row norms
+  unsigned long long *offmax;   // sweep maximum of the off-diagonal measure (double bits)
+};
+size_t svd_round_smem_bytes(bool cplx);
+cudaError_t launch_svd_load(const SvdProblem &p, const void *A, int64_t I, int64_t J, cudaStream_t s,
+                            int64_t *launches);
+// tol: outer convergence (pair skipped when its max relative off-diagonal <= tol);
+// tol_in / max_inner: rotation threshold and sweep cap of the 32 x 32 eigensolver
+cudaError_t launch_svd_round(const SvdProblem &p, int round, double tol, double tol_in, int max_inner,
+                             cudaStream_t s, int64_t *launches);
+cudaError_t launch_svd_norms(const SvdProblem &p, cudaStream_t s, int64_t *launches);
+cudaError_t launch_svd_gather_rows(bool cplx, void *dst, int64_t ld_dst, const void *src, int64_t ld_src,
+                                   const int *perm, const double *s, int64_t nk, int64_t ncols, int conj,
+                                   cudaStream_t st, int64_t *launches);
+cudaError_t launch_svd_gather_t(bool cplx, void *dst, const void *src, int64_t ld_src, const int *perm,
+                                const double *s, int64_t nk, int64_t nr, int conj, cudaStream_t st,
+                                int64_t *launches);
+// zero rows zl[0..nz) of X -> unit vectors orthogonal to the other selected rows sel[0..nsel)
+cudaError_t launch_svd_complete(const SvdProblem &p, const int *sel, int64_t nsel, double *snorm, const int *zl,
+                                int nz, cudaStream_t st, int64_t *launches);
+cudaError_t launch_svd_gather_s(double *s_out, const double *s, const int *perm, int64_t nk, cudaStream_t st,
+                                int64_t *launches);
+
 }  // namespace tci

@@ -1,0 +1,264 @@
+"""GPU parity tests of tci_svd / tci_trunc_svd
+against the CPU oracle (oracle.svd / oracle.trunc_svd: LAPACK via numpy
+plus the truncation strategy written out).
+
+Several results are correct for an SVD (reading R29): singular
+values, trunc_err, chi and -- where the spectrum is non-degenerate at the cut
+-- the truncated product u s v_dag are unique and compared with the oracle;
+the singular vectors themselves are unique only up to a phase, so they are
+checked for validity (orthonormality, reconstruction of the input).
+
+Tolerances: one-sided Jacobi is backward stable with
+relative error ~ c(n) u per rotation; with u = 2^-53 and at most a few
+thousand rotations per row the absolute errors stay <= 1e-12 ||A||_2:
+  s:              max |s - s_ref| <= 1e-12 s_0
+  reconstruction: ||u s v_dag - A||_F <= 1e-12 ||A||_F
+  orthonormality: max |U^H U - I|, |V^H V - I| <= 1e-12
+  truncated product vs the oracle's: <= 1e-12 relative Frobenius for the
+  prescribed spectra below (relative gaps >= 5 %, so the subspace
+  perturbation ||E|| / gap stays < 1e-13).
+"""
+import numpy as np
+import pytest
+
+import synth
+from conftest import max_abs, rel_frob
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2512_23917_b200 as tci  # noqa: E402
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = tci.Context(0)
+    yield c
+    c.close()
+
+
+def dev(x):
+    t = torch.from_numpy(np.ascontiguousarray(x)) if isinstance(x, np.ndarray) else x
+    return t.cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def as_matrix(u, s, vd, k):
+    U = u.reshape(-1, u.shape[-1])
+    V = vd.reshape(vd.shape[0], -1)
+    return U, s, V
+
+
+def check_valid(u, s, vd, a, k, full=True):
+    U, s, V = as_matrix(u, s, vd, k)
+    A = a.reshape(U.shape[0], V.shape[1])
+    n = s.shape[0]
+    assert np.all(np.diff(s) <= 0) and np.all(s >= 0), "s must be non-increasing and >= 0 (P:2036)"
+    assert max_abs(U.conj().T @ U, np.eye(n)) <= TOL
+    assert max_abs(V @ V.conj().T, np.eye(n)) <= TOL
+    if full:
+        assert rel_frob((U * s) @ V, A) <= TOL
+    return U, s, V
+
+
+def prescribed(m, n, sig, seed, cplx):
+    """A = Q1 diag(sig) Q2^H with Haar-like unitaries (numpy QR of seeded Gaussians)."""
+    rng = np.random.default_rng(seed)
+
+    def unitary(k):
+        g = rng.standard_normal((k, k)) + (1j * rng.standard_normal((k, k)) if cplx else 0)
+        q, r = np.linalg.qr(g)
+        return q * (np.diag(r) / np.abs(np.diag(r)))
+
+    r = len(sig)
+    return unitary(m)[:, :r] @ np.diag(sig) @ unitary(n)[:, :r].conj().T
+
+
+SHAPES = [  # (tensor shape, k): several 32-row blocks, ragged tails, wide / tall / square
+    ((3, 4, 12), 2),          # paper example P:2045-2051 (12 x 12)
+    ((2, 3, 5, 7), 2),        # wide 6 x 35
+    ((5, 7, 3), 1),           # wide 5 x 21
+    ((37, 100), 1),           # wide, ragged
+    ((100, 37), 1),           # tall, ragged
+    ((8, 8, 2, 3, 11), 3),    # tall 128 x 33
+    ((64, 64), 1),
+    ((130, 96), 1),
+    ((1, 9), 1),              # kappa = 1
+    ((200, 2, 100), 2),       # tall 400 x 100
+]
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+@pytest.mark.parametrize("shape,k", SHAPES)
+def test_svd_vs_oracle(ctx, oracle_mod, dt, shape, k):
+    a = synth.random_np(shape, dt, 300 + len(shape), 1)
+    u, s, vd = ctx.svd(dev(a), k)
+    u, s, vd = host(u), host(s), host(vd)
+    ru, rs, rvd = oracle_mod.svd(a, k)
+    assert u.shape == ru.shape and s.shape == rs.shape and vd.shape == rvd.shape
+    assert max_abs(s, rs) <= TOL * rs[0]
+    check_valid(u, s, vd, a, k)
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_svd_prescribed_spectrum(ctx, oracle_mod, dt):
+    """Known singular values (a closed form independent of LAPACK)."""
+    m, n = 150, 90
+    sig = np.sort(np.random.default_rng(1).uniform(0.1, 3.0, n))[::-1]
+    A = prescribed(m, n, sig, 2, dt == "c128")
+    if dt == "r64":
+        A = A.real.copy()
+    u, s, vd = ctx.svd(dev(A.reshape(10, 15, n)), 2)
+    assert max_abs(host(s), sig) <= TOL * sig[0]
+    check_valid(host(u), host(s), host(vd), A, 2)
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_svd_rank_deficient_tebd_like(ctx, oracle_mod, dt):
+    """theta = A.B through an inner bond 24 < 48: half the singular values are
+    rounding noise; the factors must still be orthonormal (R29)."""
+    A = synth.random_np((24, 2, 24), dt, 41, 6)
+    B = synth.random_np((24, 2, 24), dt, 41, 7)
+    th = oracle_mod.contract(A, "asb", B, "btc", "astc")
+    u, s, vd = ctx.svd(dev(th), 2)
+    _, rs, _ = oracle_mod.svd(th, 2)
+    assert max_abs(host(s), rs) <= TOL * rs[0]
+    check_valid(host(u), host(s), host(vd), th, 2)
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_svd_exact_zeros_completed(ctx, dt):
+    """Zero matrix and exact-rank-1 matrix with zero rows: s = 0 exactly where
+    the oracle's is, and u / v_dag are completed to orthonormal sets (R29)."""
+    z = np.zeros((20, 45), dtype=np.float64 if dt == "r64" else np.complex128)
+    u, s, vd = ctx.svd(dev(z), 1)
+    assert np.all(host(s) == 0.0)
+    check_valid(host(u), host(s), host(vd), z, 1)
+    x = np.zeros((40, 24), dtype=z.dtype)
+    x[3, :] = np.arange(1, 25)
+    x[17, :] = 2 * np.arange(1, 25)
+    u, s, vd = ctx.svd(dev(x), 1)
+    sh = host(s)
+    assert abs(sh[0] - np.linalg.norm(x)) <= 1e-14 * sh[0] and np.all(sh[1:] <= 1e-14 * sh[0])
+    check_valid(host(u), sh, host(vd), x, 1)
+
+
+def test_svd_repeatable_bitwise(ctx):
+    a = synth.random_np((70, 90), "c128", 5, 1)
+    r1 = [host(t) for t in ctx.svd(dev(a), 1)]
+    r2 = [host(t) for t in ctx.svd(dev(a), 1)]
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("args", [
+    (3, 6, 1e-2, 1e-12),      # the paper's example
+    (1, 5, 0.0, 0.0),         # overload (1): chi_max
+    (2, 40, 1e-3, 0.0),       # c) grows until eps <= target
+    (1, 40, 0.0, 0.9),        # a) s_min discards
+    (30, 40, 0.0, 0.9),       # b) fewer than chi_min survive a): keep those
+    (8, 4, 0.0, 0.0),         # chi_min > chi_max: b) wins (R31)
+])
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_trunc_svd_strategy_vs_oracle(ctx, oracle_mod, dt, args):
+    """Decaying prescribed spectrum sigma_i = 2^(-i/4): relative gaps 16 %, so
+    chi, trunc_err and the truncated product are unique and stable."""
+    m, n = 48, 40
+    sig = 2.0 ** (-np.arange(n) / 4.0)
+    A = prescribed(m, n, sig, 7, dt == "c128")
+    if dt == "r64":
+        A = A.real.copy()
+    a = A.reshape(6, 8, n)
+    u, s, vd, err = ctx.trunc_svd(dev(a), 2, *args)
+    ru, rs, rvd, rerr = oracle_mod.trunc_svd(a, 2, *args)
+    assert tuple(u.shape) == ru.shape and tuple(vd.shape) == rvd.shape and tuple(s.shape) == rs.shape
+    assert max_abs(host(s), rs) <= TOL * rs[0]
+    assert abs(err - rerr) <= 1e-12 * max(rerr, 1e-300) + 1e-15
+    U, sh, V = check_valid(host(u), host(s), host(vd), a, 2, full=False)
+    rU, _, rV = as_matrix(ru, rs, rvd, 2)
+    assert rel_frob((U * sh) @ V, (rU * rs) @ rV) <= TOL
+
+
+def test_trunc_svd_paper_example(ctx, oracle_mod):
+    a = synth.random_np((3, 4, 12), "r64", 152, 1)
+    u, s, vd, err = ctx.trunc_svd(dev(a), 2, 3, 6, 1e-2, 1e-12)
+    ru, rs, rvd, rerr = oracle_mod.trunc_svd(a, 2, 3, 6, 1e-2, 1e-12)
+    assert err != 0.0 and s.shape == rs.shape and 3 <= s.shape[0] <= 6
+    assert abs(err - rerr) <= 1e-12 * rerr
+
+
+def test_trunc_svd_fidelity_identity(ctx, oracle_mod):
+    """Section III (reading R24): psi normalized, psi1 = u s v_dag
+    from trunc_svd => <psi|psi1> = 1 - trunc_err, on the GPU path
+    (contract for psi1 and the overlap)."""
+    psi = synth.random_np((2, 2, 2, 2, 2, 2), "r64", 153, 1)
+    psi = psi / np.sqrt(np.sum(psi * psi))
+    d = dev(psi)
+    u, s, vd, err = ctx.trunc_svd(d, 3, 1, 3, 0.0, 0.0)
+    _, _, _, rerr = oracle_mod.trunc_svd(psi, 3, 1, 3, 0.0, 0.0)
+    psi1 = np.einsum("ijka,a,almn->ijklmn", host(u), host(s), host(vd))   # P:333-337 (checker side)
+    ovlp = float(np.sum(psi * psi1))
+    assert err > 0 and abs(ovlp - (1 - err)) <= 1e-13
+    assert abs(err - rerr) <= 1e-12 * rerr
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_tebd_step_theta_then_trunc_svd(ctx, oracle_mod, dt):
+    """One TEBD bond update (Application A): theta = A.B.U on the
+    GPU, then trunc_svd back to chi; compared with the oracle's
+    theta and trunc_svd. Gate = TFIM expm(-tau h) (R25)."""
+    if dt == "c128":
+        pytest.skip("tebd_theta is real (float64) in this build")
+    chi = 40
+    inp = synth.tebd_inputs(chi, 2, dt, 4, 0.01)
+    A, B, U = (inp[k] for k in ("A", "B", "U"))
+    th = ctx.tebd_theta(dev(A), "asb", dev(B), "btc", dev(U), "pqst", "apqc")
+    ref_th = oracle_mod.tebd_theta(A.numpy(), B.numpy(), U.numpy())
+    assert rel_frob(host(th), ref_th) <= TOL
+    u, s, vd, err = ctx.trunc_svd(th, 2, 1, chi, 0.0, 1e-14)
+    ru, rs, rvd, rerr = oracle_mod.trunc_svd(ref_th, 2, 1, chi, 0.0, 1e-14)
+    assert s.shape == rs.shape
+    assert max_abs(host(s), rs) <= TOL * rs[0]
+    check_valid(host(u), host(s), host(vd), ref_th, 2, full=False)
+
+
+def test_svd_errors(ctx):
+    a = dev(synth.random_np((4, 5, 6), "r64", 1, 1))
+    with pytest.raises(tci.TciError) as e:
+        ctx.svd(a, 0)                                        # k = 0 (1 <= k < r)
+    assert e.value.code == 3
+    with pytest.raises(tci.TciError) as e:
+        ctx.svd(a, 3)
+    assert e.value.code == 3
+    with pytest.raises(tci.TciError) as e:
+        ctx.svd(a.float(), 1)                                # r32 unsupported
+    assert e.value.code == 7
+    with pytest.raises(tci.TciError) as e:
+        ctx.trunc_svd(a, 1, 1, 0, 0.0, 0.0)                  # chi_max < 1
+    assert e.value.code == 3
+    h = ctx.handle
+    u = torch.empty((4, 3), dtype=torch.float64, device="cuda")
+    s = torch.empty((4,), dtype=torch.float64, device="cuda")
+    v = torch.empty((4, 5, 6), dtype=torch.float64, device="cuda")
+    with pytest.raises(tci.TciError) as e:                   # u has the wrong capacity
+        tci.tci_svd(h, ctx.tensor(a), 1, ctx.tensor(u), ctx.tensor(s), ctx.tensor(v))
+    assert e.value.code == 1
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_svd_large_vs_oracle(ctx, oracle_mod, dt):
+    """1024 x 1024 (c128: the two-site DMRG matrix at chi = 512, d = 2):
+    s vs LAPACK, reconstruction and orthonormality."""
+    a = synth.random_np((512, 2, 2, 512), dt, 21, 2)
+    u, s, vd = ctx.svd(dev(a), 2)
+    _, rs, _ = oracle_mod.svd(a, 2)
+    assert max_abs(host(s), rs) <= TOL * rs[0]
+    check_valid(host(u), host(s), host(vd), a, 2)

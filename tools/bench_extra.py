@@ -189,6 +189,46 @@ def cfg3(ctx):
     return res
 
 
+def svd_cfg(ctx, reps=2):
+    """truncated SVD after the TEBD theta of config 3 (chi = 2048:
+    a 4096 x 4096 f64 matrix of rank <= 2048) and after a two-site DMRG solve
+    (chi = 1024, d = 2: a 2048 x 2048 c128 matrix), each truncated back to chi;
+    the oracle (LAPACK gesdd via numpy) times the same matrix on the host."""
+    import oracle
+    res = {}
+    c = synth.TEBD_CONFIG
+    cases = [("tebd_theta_chi2048_r64", None), ("dmrg_two_site_chi1024_c128", None)]
+    for name, _ in cases:
+        if name.startswith("tebd"):
+            inp = synth.tebd_inputs(c["chi"], c["d"], c["dtype"], c["seed"], c["tau"], device="cuda")
+            th = ctx.tebd_theta(inp["A"], "asb", inp["B"], "btc", inp["U"], "pqst", "apqc")
+            chi = c["chi"]
+            del inp
+        else:
+            chi = 1024
+            th = synth.random_tensor((chi, 2, 2, chi), "c128", 9, 2, device="cuda")
+        holder = {}
+
+        def f():
+            holder["r"] = ctx.trunc_svd(th, 2, 1, chi, 0.0, 1e-14)
+        med, mn = timed(f, reps=reps, warm=1)
+        sweeps, off = ctx.svd_info()
+        u, s, vd, err = holder["r"]
+        A = th.cpu().numpy().reshape(th.shape[0] * th.shape[1], -1)
+        t0 = time.time()
+        rs = np.linalg.svd(A, compute_uv=False)
+        t_or = time.time() - t0
+        sh = s.cpu().numpy()
+        k = sh.shape[0]
+        res[name] = {"shape": list(A.shape), "chi_kept": int(k), "trunc_err": err, "ms": med * 1e3,
+                     "ms_min": mn * 1e3, "sweeps": sweeps, "final_off": off,
+                     "max_abs_ds_over_s0": float(np.max(np.abs(sh - rs[:k])) / rs[0]),
+                     "oracle_numpy_gesdd_values_only_s": t_or, "host_threads": os.cpu_count()}
+        del th, holder, u, s, vd
+        torch.cuda.empty_cache()
+    return res
+
+
 def sweep(ctx, seeds=24):
     """Config 5: random rank 3..6 contractions up to 2^28 elements, f64 and f32."""
     import string
@@ -267,6 +307,8 @@ def main():
             res["sweep"] = sweep(ctx)
         elif k == "permute":
             res["permute"] = permute_bw(ctx)
+        elif k == "svd":
+            res["svd"] = svd_cfg(ctx)
         elif k == "env":
             res["env"] = env_cfg(ctx)
         print(k, json.dumps(res.get(k))[:600], flush=True)

@@ -12,6 +12,8 @@
 //    other leg i is in-contiguous -> a (TI x TJ) tile is read along i with
 //    16-byte loads into padded shared memory and written along j with
 //    16-byte stores; every other leg indexes the tile grid.
+#include <algorithm>
+
 #include "../tci_internal.h"
 #include "common.cuh"
 
@@ -127,6 +129,306 @@ __global__ void __launch_bounds__(256) copy_rows(const RowArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Leg-group tiles (general case). The tile is the product of a group G of
+// legs: the input-fastest legs (a contiguous input block of >= RUN elements)
+// and the output-fastest legs (a contiguous output block of >= RUN elements);
+// at most one leg of each run is cut into chunks. Every other leg (and the
+// chunk index of a cut leg) indexes the tiles. A CTA stages one tile in
+// shared memory: the load phase walks the tile in input order (contiguous
+// runs of Pi elements), the store phase in output order (runs of Po); the
+// in-tile coordinates come from 32-bit division by invariant integers.
+// Persistent CTAs loop over the tiles.
+// ---------------------------------------------------------------------------
+constexpr int kGMax = 8;
+
+struct FDiv {                  // n / d for n < 2^31 (Granlund-Montgomery)
+  uint32_t d, m;
+  int s;                       // shift, -1 for d == 1
+};
+inline FDiv make_fdiv(uint32_t d) {
+  FDiv f{d, 0, -1};
+  if (d <= 1) return f;
+  int l = 0;
+  while ((1ull << l) < d) l++;
+  const int p = 31 + l;
+  f.m = (uint32_t)(((1ull << p) + d - 1) / d);
+  f.s = p - 32;
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FDiv &f) { return f.s < 0 ? n : __umulhi(n, f.m) >> f.s; }
+
+struct GroupArgs {
+  int ng;                                  // legs in the tile
+  int TS;                                  // tile elements
+  // tile legs in INPUT order (fastest first): extent in the tile, strides,
+  // shared-memory stride (tile stored in input order), full extent and cut flag
+  FDiv gi_div[kGMax];
+  int64_t gi_in[kGMax], gi_out[kGMax];
+  int gi_cut[kGMax];                       // index into the cut arrays, or -1
+  // the same legs in OUTPUT order
+  FDiv go_div[kGMax];
+  int64_t go_out[kGMax];
+  int go_sm[kGMax];
+  int go_cut[kGMax];
+  // cut legs (<= 2): full extent; their chunk coordinate comes from the tile index;
+  // in-tile coordinate of cut leg c at input position q: (q / ci_pre[c]) % ci_ext[c]
+  // (and at output position p with co_pre)
+  int ncut;
+  int64_t cut_ext[2];
+  FDiv ci_pre[2], co_pre[2], c_ext[2];
+  // tile-grid legs (outer legs + chunk indices of cut legs), slowest first
+  int nb;
+  int64_t b_ext[2 * kMaxOrder], b_in[2 * kMaxOrder], b_out[2 * kMaxOrder];
+  int b_cut[2 * kMaxOrder];                // cut index when the grid leg is a chunk index, else -1
+  int64_t b_chunk[2 * kMaxOrder];          // chunk length for chunk-index legs
+  int64_t ntiles;
+  const char *in;
+  char *out;
+};
+
+template <int ESZ>
+__global__ void __launch_bounds__(256) permute_groups(const __grid_constant__ GroupArgs a) {
+  using E = typename std::conditional<ESZ == 16, int4,
+                                      typename std::conditional<ESZ == 8, int2, int>::type>::type;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int TS = a.TS;
+  E *tile = reinterpret_cast<E *>(smraw);                            // padded: slot + slot / 32
+  int32_t *ld_off = reinterpret_cast<int32_t *>(tile + TS + TS / 32 + 1);   // in offset of tile position q
+  int32_t *st_off = ld_off + TS;                                      // out offset of output position p
+  uint16_t *st_slot = reinterpret_cast<uint16_t *>(st_off + TS);      // padded smem slot of p
+  const E *in = reinterpret_cast<const E *>(a.in);
+  E *out = reinterpret_cast<E *>(a.out);
+  // offset tables of the tile geometry, built once per CTA (full tiles)
+  for (int q = threadIdx.x; q < TS; q += 256) {
+    uint32_t r = (uint32_t)q;
+    int64_t off = 0;
+#pragma unroll
+    for (int l = 0; l < kGMax; l++) {
+      if (l < a.ng) {
+        const uint32_t nq = fdiv(r, a.gi_div[l]);
+        off += (int64_t)(r - nq * a.gi_div[l].d) * a.gi_in[l];
+        r = nq;
+      }
+    }
+    ld_off[q] = (int32_t)off;
+    r = (uint32_t)q;
+    off = 0;
+    int slot = 0;
+#pragma unroll
+    for (int l = 0; l < kGMax; l++) {
+      if (l < a.ng) {
+        const uint32_t nq = fdiv(r, a.go_div[l]);
+        const uint32_t c = r - nq * a.go_div[l].d;
+        r = nq;
+        off += (int64_t)c * a.go_out[l];
+        slot += (int)c * a.go_sm[l];
+      }
+    }
+    st_off[q] = (int32_t)off;
+    st_slot[q] = (uint16_t)(slot + (slot >> 5));
+  }
+  __syncthreads();
+  for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    int64_t rem = t, in_base = 0, out_base = 0;
+    int64_t cut_base[2] = {0, 0};
+    bool full = true;
+    for (int k = a.nb - 1; k >= 0; k--) {
+      const int64_t c = rem % a.b_ext[k];
+      rem /= a.b_ext[k];
+      in_base += c * a.b_in[k];
+      out_base += c * a.b_out[k];
+      if (a.b_cut[k] >= 0) {
+        cut_base[a.b_cut[k]] = c * a.b_chunk[k];
+        full = full && (c * a.b_chunk[k] + a.b_chunk[k] <= a.cut_ext[a.b_cut[k]]);
+      }
+    }
+    if (full) {
+      for (int q = threadIdx.x; q < TS; q += 256) tile[q + (q >> 5)] = in[in_base + ld_off[q]];
+      __syncthreads();
+      for (int p = threadIdx.x; p < TS; p += 256) out[out_base + st_off[p]] = tile[st_slot[p]];
+      __syncthreads();
+      continue;
+    }
+    // ragged chunk of a cut leg: bounds from the cut legs' coordinates
+    for (int q = threadIdx.x; q < TS; q += 256) {
+      bool ok = true;
+      for (int c = 0; c < a.ncut; c++) {
+        const uint32_t x = fdiv((uint32_t)q, a.ci_pre[c]);
+        ok = ok && (cut_base[c] + (x - fdiv(x, a.c_ext[c]) * a.c_ext[c].d) < a.cut_ext[c]);
+      }
+      if (ok) tile[q + (q >> 5)] = in[in_base + ld_off[q]];
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < TS; p += 256) {
+      bool ok = true;
+      for (int c = 0; c < a.ncut; c++) {
+        const uint32_t x = fdiv((uint32_t)p, a.co_pre[c]);
+        ok = ok && (cut_base[c] + (x - fdiv(x, a.c_ext[c]) * a.c_ext[c].d) < a.cut_ext[c]);
+      }
+      if (ok) out[out_base + st_off[p]] = tile[st_slot[p]];
+    }
+    __syncthreads();
+  }
+}
+
+// Plan the leg-group tile; false when it does not apply (caller falls back).
+template <int ESZ>
+bool plan_groups(const PermuteProblem &p, const int64_t *out_stride, GroupArgs &a) {
+  const int n = p.n;
+  constexpr int RUN = 256 / ESZ;             // >= 256 contiguous bytes per run
+  constexpr int TSMAX = 32768 / ESZ;         // 32 KB tiles
+  int ord_in[kMaxOrder], ord_out[kMaxOrder];
+  for (int k = 0; k < n; k++) ord_in[k] = ord_out[k] = k;
+  std::sort(ord_in, ord_in + n, [&](int x, int y) { return p.in_stride_for_out[x] < p.in_stride_for_out[y]; });
+  std::sort(ord_out, ord_out + n, [&](int x, int y) { return out_stride[x] < out_stride[y]; });
+  int64_t tex[kMaxOrder];                    // tile extent per leg (0 = not in the tile)
+  for (int k = 0; k < n; k++) tex[k] = 0;
+  int cut_leg[2] = {-1, -1}, ncut = 0;
+  int64_t TS = 1;
+  auto add_run = [&](const int *ord, int64_t target) {
+    int64_t run = 1;
+    for (int i = 0; i < n && run < target; i++) {
+      const int k = ord[i];
+      const int64_t e = p.shape_out[k];
+      if (tex[k] > 0) {                      // already in the tile
+        run *= tex[k];
+        if (tex[k] < e) break;               // a cut leg ends the contiguous run
+        continue;
+      }
+      const int64_t room = TSMAX / TS;
+      if (room < 2) break;
+      if (e <= room && (run * e <= 4 * target || e <= 2)) {
+        tex[k] = e;
+        TS *= e;
+        run *= e;
+      } else {                               // cut into chunks
+        int64_t ch = std::min<int64_t>(room, std::max<int64_t>(2, (target + run - 1) / run));
+        ch = std::min(ch, e);
+        tex[k] = ch;
+        TS *= ch;
+        run *= ch;
+        if (ch < e) cut_leg[ncut++] = k;
+        break;
+      }
+    }
+  };
+  add_run(ord_in, RUN);
+  add_run(ord_out, RUN);
+  // grow the tile towards TSMAX: widen the cut legs first (input-run cut
+  // first), then take further legs in input order
+  for (int c = 0; c < ncut; c++) {
+    const int k = cut_leg[c];
+    const int64_t e = p.shape_out[k];
+    const int64_t grow = std::min<int64_t>(TSMAX / TS, (e + tex[k] - 1) / tex[k]);
+    if (grow >= 2) {
+      TS = TS / tex[k];
+      // balanced chunks: the last one is not a sliver
+      const int64_t cmax = std::min<int64_t>(e, tex[k] * grow), nch = (e + cmax - 1) / cmax;
+      tex[k] = (e + nch - 1) / nch;
+      TS *= tex[k];
+    }
+  }
+  for (int i = 0; i < n && 2 * TS <= TSMAX; i++) {
+    const int k = ord_in[i];
+    if (tex[k] > 0) continue;
+    const int64_t e = p.shape_out[k], room = TSMAX / TS;
+    if (e <= room) {
+      tex[k] = e;
+      TS *= e;
+    } else if (ncut < 2) {
+      tex[k] = room;
+      TS *= room;
+      cut_leg[ncut++] = k;
+    }
+    break;   // one extra leg at most: keep the tile's leg count small
+  }
+  // a cut leg that grew to its full extent is no longer cut
+  for (int c = 0; c < ncut; c++)
+    if (tex[cut_leg[c]] >= p.shape_out[cut_leg[c]]) {
+      cut_leg[c] = cut_leg[ncut - 1];
+      cut_leg[ncut - 1] = -1;
+      ncut--;
+      c--;
+    }
+  int ng = 0;
+  for (int k = 0; k < n; k++) ng += tex[k] > 0;
+  if (ng > kGMax || TS < 2 || p.total >= (int64_t(1) << 31)) return false;   // int32 in-tile offsets
+  a.ng = ng;
+  a.TS = (int)TS;
+  a.ncut = ncut;
+  // legs in input order with their smem strides (tile stored in input order)
+  int64_t sm_of[kMaxOrder];
+  {
+    int l = 0;
+    int64_t sm = 1;
+    for (int i = 0; i < n; i++) {
+      const int k = ord_in[i];
+      if (!tex[k]) continue;
+      a.gi_div[l] = make_fdiv((uint32_t)tex[k]);
+      a.gi_in[l] = p.in_stride_for_out[k];
+      a.gi_out[l] = out_stride[k];
+      a.gi_cut[l] = k == cut_leg[0] ? 0 : (k == cut_leg[1] ? 1 : -1);
+      sm_of[k] = sm;
+      sm *= tex[k];
+      l++;
+    }
+    l = 0;
+    for (int i = 0; i < n; i++) {
+      const int k = ord_out[i];
+      if (!tex[k]) continue;
+      a.go_div[l] = make_fdiv((uint32_t)tex[k]);
+      a.go_out[l] = out_stride[k];
+      a.go_sm[l] = (int)sm_of[k];
+      a.go_cut[l] = k == cut_leg[0] ? 0 : (k == cut_leg[1] ? 1 : -1);
+      l++;
+    }
+  }
+  for (int c = 0; c < 2; c++) {
+    a.cut_ext[c] = c < ncut ? p.shape_out[cut_leg[c]] : 0;
+    a.c_ext[c] = make_fdiv(c < ncut ? (uint32_t)tex[cut_leg[c]] : 1u);
+    int64_t pi = 1, po = 1;
+    for (int i = 0; c < ncut && i < n; i++) {
+      const int k = ord_in[i];
+      if (k == cut_leg[c]) break;
+      if (tex[k]) pi *= tex[k];
+    }
+    for (int i = 0; c < ncut && i < n; i++) {
+      const int k = ord_out[i];
+      if (k == cut_leg[c]) break;
+      if (tex[k]) po *= tex[k];
+    }
+    a.ci_pre[c] = make_fdiv((uint32_t)pi);
+    a.co_pre[c] = make_fdiv((uint32_t)po);
+  }
+  // tile grid: legs outside the tile and chunk indices of cut legs (output order, slowest first)
+  a.nb = 0;
+  a.ntiles = 1;
+  for (int k = 0; k < n; k++) {
+    if (tex[k] == 0) {
+      a.b_ext[a.nb] = p.shape_out[k];
+      a.b_in[a.nb] = p.in_stride_for_out[k];
+      a.b_out[a.nb] = out_stride[k];
+      a.b_cut[a.nb] = -1;
+      a.b_chunk[a.nb] = 0;
+    } else if (tex[k] < p.shape_out[k]) {
+      const int64_t ch = tex[k];
+      a.b_ext[a.nb] = (p.shape_out[k] + ch - 1) / ch;
+      a.b_in[a.nb] = ch * p.in_stride_for_out[k];
+      a.b_out[a.nb] = ch * out_stride[k];
+      a.b_cut[a.nb] = k == cut_leg[0] ? 0 : 1;
+      a.b_chunk[a.nb] = ch;
+    } else {
+      continue;
+    }
+    a.ntiles *= a.b_ext[a.nb];
+    a.nb++;
+  }
+  a.in = static_cast<const char *>(p.in);
+  a.out = static_cast<char *>(p.out);
+  return true;
+}
+
 template <int ESZ>
 cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launches) {
   const int n = p.n;
@@ -137,7 +439,7 @@ cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launc
   }
   constexpr int VMAX = 16 / ESZ;
   auto aligned = [&](const void *ptr) { return ((uintptr_t)ptr % 16) == 0; };
-  if (n == 0 || p.in_stride_for_out[n - 1] == 1) {
+  if (n == 0 || (p.in_stride_for_out[n - 1] == 1 && (p.shape_out[n - 1] * ESZ >= 128 || n == 1))) {
     RowArgs a{};
     a.run = n ? p.shape_out[n - 1] : 1;
     a.nb = n ? n - 1 : 0;
@@ -160,10 +462,29 @@ cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launc
     if (launches) ++*launches;
     return cudaGetLastError();
   }
-  // tile transpose between j = out-fastest leg and i = the in-contiguous leg
+  // tile legs of the classic transpose: j = out-fastest leg, i = the
+  // in-contiguous leg; when both are long it is the fastest kernel
+  constexpr int T = (ESZ == 16) ? 32 : 64;
   int li = -1;
   for (int k = 0; k < n - 1; k++)
     if (p.in_stride_for_out[k] == 1) li = k;
+  const bool classic = li >= 0 && p.shape_out[li] >= T / 2 && p.shape_out[n - 1] >= T / 2;
+  // otherwise leg-group tiles (short contiguous legs are grouped until both
+  // the reads and the writes move >= 256 contiguous bytes)
+  if (!classic) {
+    GroupArgs ga;
+    if (plan_groups<ESZ>(p, out_stride, ga)) {
+      const size_t smem = ((size_t)ga.TS + ga.TS / 32 + 1) * ESZ + (size_t)ga.TS * 10 + 16;
+      auto k = permute_groups<ESZ>;
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      const int64_t blocks = std::min<int64_t>(ga.ntiles, 148 * 6);
+      k<<<(unsigned)blocks, 256, smem, s>>>(ga);
+      if (launches) ++*launches;
+      return cudaGetLastError();
+    }
+  }
+  // tile transpose between j = out-fastest leg and i = the in-contiguous leg
   const int lj = n - 1;
   if (li < 0) {
     // no unit-stride input leg (cannot happen for a fused dense input): use rows
@@ -188,7 +509,6 @@ cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launc
     nbt *= p.shape_out[k];
     a.nb++;
   }
-  constexpr int T = (ESZ == 16) ? 32 : 64;
   a.tiles_i = (a.ni + T - 1) / T;
   a.tiles_j = (a.nj + T - 1) / T;
   a.in = static_cast<const char *>(p.in);

@@ -59,6 +59,22 @@ def test_permute_bitwise(ctx, oracle_mod, dt):
             assert np.array_equal(host(y).astype(ref.dtype), ref), (shape, perm)
 
 
+@pytest.mark.parametrize("dt", ["r32", "r64", "c128"])
+def test_permute_leg_groups_bitwise(ctx, oracle_mod, dt):
+    """Leg-group tiles: short contiguous legs grouped, long legs cut into
+    chunks with ragged last chunks, up to 7 legs; bitwise vs the oracle."""
+    rng = np.random.default_rng(11)
+    shapes = [(5, 7, 3, 11), (2, 3, 2, 5, 2, 7, 3), (1000, 3, 5), (3, 5, 1031), (37, 130, 65, 2),
+              (17, 2, 513, 3), (64, 1, 64, 5), (6, 4000), (4000, 6), (2, 2, 2, 2, 2, 2, 2)]
+    for i, shape in enumerate(shapes):
+        x = synth.random_tensor(shape, dt, 700 + i, 1)
+        for _ in range(5):
+            perm = list(rng.permutation(len(shape)))
+            y = ctx.permute(dev(x), perm)
+            ref = oracle_mod.permute(x.numpy(), perm)
+            assert np.array_equal(host(y).astype(ref.dtype), ref), (shape, perm)
+
+
 def test_permute_paper_example(ctx):
     a = synth.random_tensor((3, 2, 4), "r64", 12, 1)
     a2 = ctx.permute(dev(a), [1, 0, 2])

@@ -239,12 +239,6 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   const int64_t M = extent(I, dim_of), N = extent(J, dim_of), K = extent(S, dim_of);
   const size_t es = dtype_size(a.dtype);
 
-  // ---- scratch layout ----
-  size_t off = 0, offA = 0, offB = 0, offC = 0;
-  if (!formA) { offA = off; off = align_up(off + (size_t)M * K * es); }
-  if (!formB) { offB = off; off = align_up(off + (size_t)K * N * es); }
-  const bool c_scratch = !formC || alias;
-  if (c_scratch) { offC = off; off = align_up(off + (size_t)M * N * es); }
   // deterministic split-K when the output has too few tiles to fill the 148
   // SMs and K is long: S partial GEMMs over K chunks + an ascending-order sum
   int splitk = 1;
@@ -259,19 +253,54 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
       if (S >= 2) {
         k_chunk = ((K + S - 1) / S + 15) / 16 * 16;
         S = (K + k_chunk - 1) / k_chunk;
-        if (S >= 2) {
-          splitk = (int)S;
-          const size_t pes = dtype_is_complex(a.dtype) ? 16 : 8;   // fp64 partials
-          offP = off;
-          off = align_up(off + (size_t)S * M * N * pes);
-        }
+        if (S >= 2) splitk = (int)S;
       }
     }
   }
-  // complex128 GEMM algorithm; the Ozaki path needs its own scratch
+  // complex128 GEMM algorithm
   int zalgo = ctx->zgemm_algo == kZOzaki ? kZ3M : ctx->zgemm_algo;
+  const bool use_ozaki = a.dtype == TCI_C128 && ctx->zgemm_algo == kZOzaki && splitk <= 1 &&
+                         ozaki_worthwhile(M, N, K);
+  // gamma-order scatter epilogue (8(a6)): an output that is not a [I,J] /
+  // [J,I] block is written in place through row / column offset tables
+  // instead of GEMM -> scratch -> permute; the GEMM is oriented so that the
+  // fastest gamma leg is on its N side (coalesced runs)
+  bool scatter = !formC && !alias && !use_ozaki && C.n > 0;
+  bool scat_swap = false;
+  if (scatter) {
+    scat_swap = inI[C.leg[C.n - 1].id] != 0;
+    // contiguous gamma run along the GEMM's N side: the trailing gamma legs
+    // that are also the trailing legs of the N-side order; short runs write
+    // scattered sectors, so below 128 bytes the GEMM -> scratch -> permute
+    // route (leg-group tiles) is the better one
+    const std::vector<int> &Nside = scat_swap ? I : J;
+    int64_t run = 1;
+    int pos = (int)Nside.size() - 1;
+    for (int k = C.n - 1; k >= 0 && pos >= 0 && C.leg[k].id == Nside[pos]; k--, pos--) run *= C.leg[k].dim;
+    // (a pure output-write kernel, K <= 16, needs whole 128-byte lines; with a
+    // real K the GEMM hides partial sectors up to one 32-byte sector per run)
+    if (run * (int64_t)es < (K <= 16 ? 128 : 32)) scatter = false;
+  }
+
+  // ---- scratch layout ----
+  size_t off = 0, offA = 0, offB = 0, offC = 0, offR = 0, offCol = 0;
+  if (!formA) { offA = off; off = align_up(off + (size_t)M * K * es); }
+  if (!formB) { offB = off; off = align_up(off + (size_t)K * N * es); }
+  const bool c_scratch = (!formC && !scatter) || alias;
+  if (c_scratch) { offC = off; off = align_up(off + (size_t)M * N * es); }
+  if (scatter) {
+    offR = off;
+    off = align_up(off + (size_t)M * 8);
+    offCol = off;
+    off = align_up(off + (size_t)N * 8);
+  }
+  if (splitk > 1) {
+    const size_t pes = dtype_is_complex(a.dtype) ? 16 : 8;   // fp64 partials
+    offP = off;
+    off = align_up(off + (size_t)splitk * M * N * pes);
+  }
   size_t offZ = 0, ozb = 0;
-  if (a.dtype == TCI_C128 && ctx->zgemm_algo == kZOzaki && splitk <= 1 && ozaki_worthwhile(M, N, K)) {
+  if (use_ozaki) {
     zalgo = kZOzaki;
     ozb = ozaki_workspace_bytes(M, N, K);
     offZ = off;
@@ -347,9 +376,32 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
     if (K_ == 1) { if (sm == 1 && M_ > 1) sk = 0; else { sk = 1; if (M_ == 1) sm = 1; } }
     else if (M_ == 1 && sk != 1) sm = 1;
   };
-  // C layout: formC == 2 means gamma = [J, I] -> swap roles
-  const bool swap = (formC == 2) && !alias;
+  // C layout: formC == 2 means gamma = [J, I] -> swap roles (also for a
+  // scatter whose fastest gamma leg is an I leg)
+  const bool swap = ((formC == 2) || (scatter && scat_swap)) && !alias;
   void *Cp = c_scratch ? (void *)(wsb + offC) : c.data;
+  int64_t *rowt = nullptr, *colt = nullptr;
+  if (scatter) {
+    // gamma offsets of the I legs (rows) and J legs (columns), slowest first
+    auto table = [&](const std::vector<int> &legs, int64_t *dst, int64_t n) -> tci_status_t {
+      int64_t ext[kMaxOrder], str[kMaxOrder];
+      int nl = 0;
+      for (int id : legs) {
+        ext[nl] = dim_of[id];
+        str[nl] = stride_in(C, id);
+        nl++;
+      }
+      TCI_CUDA_CHECK(launch_offsets(dst, n, nl, ext, str, ctx->stream, &ctx->launches));
+      return TCI_OK;
+    };
+    int64_t *ti = reinterpret_cast<int64_t *>(wsb + offR), *tj = reinterpret_cast<int64_t *>(wsb + offCol);
+    st = table(I, ti, M);
+    if (st != TCI_OK) return st;
+    st = table(J, tj, N);
+    if (st != TCI_OK) return st;
+    rowt = swap ? tj : ti;
+    colt = swap ? ti : tj;
+  }
   if (!swap) {
     g.C = Cp;
     g.c_sm = N;
@@ -364,6 +416,8 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   canon_a(g.M, g.K, g.a_sm, g.a_sk);
   // B(k,n): the same rule with (N, K)
   canon_a(g.N, g.K, g.b_sn, g.b_sk);
+  g.c_row = rowt;
+  g.c_col = colt;
   g.zalgo = zalgo;
   if (zalgo == kZOzaki) {
     g.oz_ws = wsb + offZ;

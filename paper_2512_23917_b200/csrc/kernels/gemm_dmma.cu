@@ -475,7 +475,9 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
   }
 
   // ---- epilogue: C N-contiguous, direct stores (each quad of lanes writes a
-  // contiguous 64 B (real) / 128 B (complex) run) ----
+  // contiguous 64 B (real) / 128 B (complex) run), or the gamma-order
+  // scatter through the row / column offset tables (8(a6)) ----
+  const bool scat = p.c_row != nullptr && p.splitk <= 1;
 #pragma unroll
   for (int i = 0; i < C::MI; i++) {
     const int64_t m = m0 + wm0 + i * 8 + lr;
@@ -485,6 +487,11 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
       const int64_t n = n0 + wn0 + j * 8 + 2 * lc;
       if constexpr (C::kCplx) {
         double2 *cp = reinterpret_cast<double2 *>(Cb) + m * c_sm + n;
+        double2 *cp1 = cp + 1;
+        if (scat) {
+          cp = reinterpret_cast<double2 *>(Cb) + p.c_row[m] + p.c_col[n];
+          if (n + 1 < p.N) cp1 = reinterpret_cast<double2 *>(Cb) + p.c_row[m] + p.c_col[n + 1];
+        }
         double re0, im0, re1, im1;
         if constexpr (C::kAlgo == kCplx3M || C::kAlgo == kCplx3MS) {
           const double P0 = acc.c[0][i][j][0], Q0 = acc.c[1][i][j][0], S0 = acc.c[2][i][j][0];
@@ -500,11 +507,16 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
           im1 = acc.c[1][i][j][1];
         }
         if (n < p.N) cp[0] = make_double2(re0, im0);
-        if (n + 1 < p.N) cp[1] = make_double2(re1, im1);
+        if (n + 1 < p.N) cp1[0] = make_double2(re1, im1);
       } else {
         double *cp = reinterpret_cast<double *>(Cb) + m * c_sm + n;
+        double *cp1 = cp + 1;
+        if (scat) {
+          cp = reinterpret_cast<double *>(Cb) + p.c_row[m] + p.c_col[n];
+          if (n + 1 < p.N) cp1 = reinterpret_cast<double *>(Cb) + p.c_row[m] + p.c_col[n + 1];
+        }
         if (n < p.N) cp[0] = acc.c[0][i][j][0];
-        if (n + 1 < p.N) cp[1] = acc.c[0][i][j][1];
+        if (n + 1 < p.N) cp1[0] = acc.c[0][i][j][1];
       }
     }
   }
@@ -559,7 +571,8 @@ namespace {
 // order -> deterministic); P = partial element, O = output element
 template <typename P, typename O>
 __global__ void __launch_bounds__(256) splitk_reduce(const P *__restrict__ part, O *__restrict__ C,
-                                                     int64_t M, int64_t N, int64_t c_sm, int S) {
+                                                     int64_t M, int64_t N, int64_t c_sm, int S,
+                                                     const int64_t *c_row, const int64_t *c_col) {
   const int64_t MN = M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < MN; i += (int64_t)gridDim.x * blockDim.x) {
     P acc = part[i];
@@ -573,15 +586,16 @@ __global__ void __launch_bounds__(256) splitk_reduce(const P *__restrict__ part,
       }
     }
     const int64_t m = i / N, n = i % N;
+    const int64_t ci = c_row ? c_row[m] + c_col[n] : m * c_sm + n;
     if constexpr (sizeof(O) == sizeof(P)) {
-      C[m * c_sm + n] = reinterpret_cast<const O &>(acc);
+      C[ci] = reinterpret_cast<const O &>(acc);
     } else if constexpr (sizeof(P) == 16) {
       const double2 a = reinterpret_cast<const double2 &>(acc);
       const float2 f = make_float2((float)a.x, (float)a.y);
-      C[m * c_sm + n] = reinterpret_cast<const O &>(f);
+      C[ci] = reinterpret_cast<const O &>(f);
     } else {
       const float f = (float)reinterpret_cast<const double &>(acc);
-      C[m * c_sm + n] = reinterpret_cast<const O &>(f);
+      C[ci] = reinterpret_cast<const O &>(f);
     }
   }
 }
@@ -592,16 +606,16 @@ static cudaError_t launch_splitk_reduce(const GemmProblem &p, cudaStream_t s, in
   const unsigned blocks = (unsigned)std::min<int64_t>((MN + 255) / 256, 148 * 8);
   switch (p.dtype) {
     case TCI_C128:
-      splitk_reduce<double2, double2><<<blocks, 256, 0, s>>>((const double2 *)p.partial, (double2 *)p.C, p.M, p.N, p.c_sm, p.splitk);
+      splitk_reduce<double2, double2><<<blocks, 256, 0, s>>>((const double2 *)p.partial, (double2 *)p.C, p.M, p.N, p.c_sm, p.splitk, p.c_row, p.c_col);
       break;
     case TCI_R64:
-      splitk_reduce<double, double><<<blocks, 256, 0, s>>>((const double *)p.partial, (double *)p.C, p.M, p.N, p.c_sm, p.splitk);
+      splitk_reduce<double, double><<<blocks, 256, 0, s>>>((const double *)p.partial, (double *)p.C, p.M, p.N, p.c_sm, p.splitk, p.c_row, p.c_col);
       break;
     case TCI_C64:
-      splitk_reduce<double2, float2><<<blocks, 256, 0, s>>>((const double2 *)p.partial, (float2 *)p.C, p.M, p.N, p.c_sm, p.splitk);
+      splitk_reduce<double2, float2><<<blocks, 256, 0, s>>>((const double2 *)p.partial, (float2 *)p.C, p.M, p.N, p.c_sm, p.splitk, p.c_row, p.c_col);
       break;
     case TCI_R32:
-      splitk_reduce<double, float><<<blocks, 256, 0, s>>>((const double *)p.partial, (float *)p.C, p.M, p.N, p.c_sm, p.splitk);
+      splitk_reduce<double, float><<<blocks, 256, 0, s>>>((const double *)p.partial, (float *)p.C, p.M, p.N, p.c_sm, p.splitk, p.c_row, p.c_col);
       break;
   }
   if (launches) ++*launches;
@@ -649,6 +663,8 @@ cudaError_t launch_tebd_fused(const TebdProblem &t, cudaStream_t s, int64_t *lau
 
 static cudaError_t launch_gemm_main(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   if (p.M == 0 || p.N == 0) return cudaSuccess;
+  // one of M, N, K tiny: HBM-bound, no tensor-core tile (gemm_thin.cu)
+  if (gemm_thin_applies(p)) return launch_gemm_thin(p, s, launches);
   if (p.dtype == TCI_R32 || p.dtype == TCI_C64) return launch_gemm_f32(p, s, launches);
   // The planner canonicalises strides (contract.cpp): a_sk == 1 selects the
   // K-contiguous loader, otherwise a_sm == 1; same for B.

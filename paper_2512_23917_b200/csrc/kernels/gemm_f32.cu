@@ -24,7 +24,8 @@ struct Ops<float> {
   using Acc = double;
   static __device__ __forceinline__ float zero() { return 0.f; }
   static __device__ __forceinline__ Acc azero() { return 0.0; }
-  static __device__ __forceinline__ void mac(Acc &c, float a, float b) { c = fma((double)a, (double)b, c); }
+  static __device__ __forceinline__ Acc wide(float a) { return (double)a; }
+  static __device__ __forceinline__ void mac(Acc &c, Acc a, Acc b) { c = fma(a, b, c); }
   static __device__ __forceinline__ float out(Acc c) { return (float)c; }
 };
 template <>
@@ -32,7 +33,8 @@ struct Ops<float2> {
   using Acc = double2;
   static __device__ __forceinline__ float2 zero() { return make_float2(0.f, 0.f); }
   static __device__ __forceinline__ Acc azero() { return make_double2(0.0, 0.0); }
-  static __device__ __forceinline__ void mac(Acc &c, float2 a, float2 b) {
+  static __device__ __forceinline__ Acc wide(float2 a) { return make_double2(a.x, a.y); }
+  static __device__ __forceinline__ void mac(Acc &c, Acc a, Acc b) {
     const double ax = a.x, ay = a.y, bx = b.x, by = b.y;
     c.x = fma(ax, bx, c.x);
     c.x = fma(-ay, by, c.x);
@@ -45,8 +47,10 @@ struct Ops<float2> {
 template <typename E, int BM, int BN, int BK, int TM, int TN>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int tiles_m, int tiles_n) {
   static_assert((BM / TM) * (BN / TN) == 256, "256 threads");
-  __shared__ E As[2][BK][BM];
-  __shared__ E Bs[2][BK][BN];
+  using Acc = typename Ops<E>::Acc;
+  // operands are widened to fp64 once, when staged (products exact, R20)
+  __shared__ Acc As[2][BK][BM];
+  __shared__ Acc Bs[2][BK][BN];
   const int tid = threadIdx.x;
   const int tile_m = blockIdx.x / tiles_n, tile_n = blockIdx.x % tiles_n;
   const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN;
@@ -91,14 +95,14 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
       const int idx = tid + i * 256;
       int m, k;
       if (a_mfast) { k = idx / BM; m = idx % BM; } else { m = idx / BK; k = idx % BK; }
-      As[buf][k][m] = ra[i];
+      As[buf][k][m] = Ops<E>::wide(ra[i]);
     }
 #pragma unroll
     for (int i = 0; i < LB; i++) {
       const int idx = tid + i * 256;
       int n, k;
       if (b_nfast) { k = idx / BN; n = idx % BN; } else { n = idx / BK; k = idx % BK; }
-      Bs[buf][k][n] = rb[i];
+      Bs[buf][k][n] = Ops<E>::wide(rb[i]);
     }
   };
 
@@ -118,11 +122,11 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
     if (kt + 1 < KT) gload((int64_t)(kt + 1) * BK);
 #pragma unroll
     for (int k = 0; k < BK; k++) {
-      E a[TM], b[TN];
+      Acc a[TM], b[TN];
 #pragma unroll
       for (int i = 0; i < TM; i++) a[i] = As[buf][k][ty * TM + i];
 #pragma unroll
-      for (int j = 0; j < TN; j++) b[j] = Bs[buf][k][tx * TN + j];
+      for (int j = 0; j < TN; j++) b[j] = Bs[buf][k][tx + j * (BN / TN)];   // conflict-free
 #pragma unroll
       for (int i = 0; i < TM; i++)
 #pragma unroll
@@ -139,10 +143,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
     if (m >= p.M) continue;
 #pragma unroll
     for (int j = 0; j < TN; j++) {
-      const int64_t n = n0 + tx * TN + j;
+      const int64_t n = n0 + tx + j * (BN / TN);
       if (n >= p.N) continue;
       if (Pz) Pz[m * p.N + n] = acc[i][j];
-      else C[m * p.c_sm + n] = Ops<E>::out(acc[i][j]);
+      else C[p.c_row ? p.c_row[m] + p.c_col[n] : m * p.c_sm + n] = Ops<E>::out(acc[i][j]);
     }
   }
 }
@@ -160,7 +164,12 @@ cudaError_t run_simt(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
 }  // namespace
 
 cudaError_t launch_gemm_f32(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
-  if (p.dtype == TCI_R32) return run_simt<float, 128, 128, 8, 8, 8>(p, s, launches);
+  if (p.dtype == TCI_R32) {
+    // narrow N or M: a 128 x 64 (64 x 128) tile wastes less of the register tile
+    if (p.N <= 64 && p.M > 64) return run_simt<float, 128, 64, 8, 8, 4>(p, s, launches);
+    if (p.M <= 64 && p.N > 64) return run_simt<float, 64, 128, 8, 4, 8>(p, s, launches);
+    return run_simt<float, 128, 128, 8, 8, 8>(p, s, launches);
+  }
   return run_simt<float2, 64, 64, 8, 4, 4>(p, s, launches);
 }
 

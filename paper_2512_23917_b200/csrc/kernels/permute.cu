@@ -439,7 +439,12 @@ cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launc
   }
   constexpr int VMAX = 16 / ESZ;
   auto aligned = [&](const void *ptr) { return ((uintptr_t)ptr % 16) == 0; };
-  if (n == 0 || (p.in_stride_for_out[n - 1] == 1 && (p.shape_out[n - 1] * ESZ >= 128 || n == 1))) {
+  // contiguous runs: vectorised row copies when the runs are >= 128 bytes and
+  // 16-byte aligned (odd runs go to the leg-group tiles)
+  bool rows_vec = n > 0 && p.in_stride_for_out[n - 1] == 1 && aligned(p.in) && aligned(p.out) &&
+                  p.shape_out[n - 1] % VMAX == 0;
+  for (int k = 0; rows_vec && k < n - 1; k++) rows_vec = p.in_stride_for_out[k] % VMAX == 0;
+  auto rows_path = [&]() -> cudaError_t {
     RowArgs a{};
     a.run = n ? p.shape_out[n - 1] : 1;
     a.nb = n ? n - 1 : 0;
@@ -461,7 +466,9 @@ cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launc
     else copy_rows<ESZ, 1><<<(unsigned)blocks, 256, 0, s>>>(a);
     if (launches) ++*launches;
     return cudaGetLastError();
-  }
+  };
+  const bool in_run = n > 0 && p.in_stride_for_out[n - 1] == 1;
+  if (n <= 1 || (in_run && p.shape_out[n - 1] * ESZ >= 128 && rows_vec)) return rows_path();
   // tile legs of the classic transpose: j = out-fastest leg, i = the
   // in-contiguous leg; when both are long it is the fastest kernel
   constexpr int T = (ESZ == 16) ? 32 : 64;
@@ -484,6 +491,7 @@ cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launc
       return cudaGetLastError();
     }
   }
+  if (in_run || li < 0) return rows_path();   // no leg-group plan: plain row copies
   // tile transpose between j = out-fastest leg and i = the in-contiguous leg
   const int lj = n - 1;
   if (li < 0) {
@@ -531,6 +539,38 @@ cudaError_t launch_permute(const PermuteProblem &p, cudaStream_t s, int64_t *lau
     case 16: return launch_typed<16>(p, s, launches);
   }
   return cudaErrorInvalidValue;
+}
+
+namespace {
+struct OffLegs {
+  int nl;
+  int64_t ext[kMaxOrder], stride[kMaxOrder];
+};
+__global__ void offsets_kernel(int64_t *offs, int64_t n, const OffLegs L) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i, o = 0;
+    for (int l = L.nl - 1; l >= 0; l--) {
+      o += (r % L.ext[l]) * L.stride[l];
+      r /= L.ext[l];
+    }
+    offs[i] = o;
+  }
+}
+}  // namespace
+
+cudaError_t launch_offsets(int64_t *offs, int64_t n, int nl, const int64_t *ext, const int64_t *stride,
+                           cudaStream_t s, int64_t *launches) {
+  if (n == 0) return cudaSuccess;
+  if (nl > kMaxOrder) return cudaErrorInvalidValue;
+  OffLegs L{};
+  L.nl = nl;
+  for (int l = 0; l < nl; l++) {
+    L.ext[l] = ext[l];
+    L.stride[l] = stride[l];
+  }
+  offsets_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, s>>>(offs, n, L);
+  if (launches) ++*launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s, int64_t *launches) {

@@ -51,6 +51,10 @@ struct GemmProblem {
   void *partial = nullptr;
   // mode 1 = TEBD theta with the gate in the epilogue (launch_tebd_fused)
   int mode = 0;
+  // gamma-order scatter epilogue: when c_row is set, C(m, n)
+  // is stored at c_row[m] + c_col[n] (device tables, elements) instead of
+  // m * c_sm + n; split-K partials stay dense and the reduction scatters
+  const int64_t *c_row = nullptr, *c_col = nullptr;
   int64_t te_chi_a = 0, te_chi_c = 0;     // extents of a and c
   int64_t te_a_a = 0, te_a_s = 0;         // A strides of a and s (b stride == 1)
   int64_t te_b_t = 0;                     // B stride of t (c stride == 1, b stride = b_sk)
@@ -83,6 +87,11 @@ void ozaki_params(int64_t K, int *nmod, int *t, const int **moduli);
 
 // Output tile of the GEMM kernel used for `dtype` (for the planner's split-K choice).
 void gemm_tile(tci_dtype_t dtype, int *bm, int *bn);
+
+// HBM-bound GEMM corners (gemm_thin.cu): min(M, N) <= 16 (any K, honours the
+// split-K fields) or K <= 16 (no split-K). launch_gemm dispatches to it.
+bool gemm_thin_applies(const GemmProblem &p);
+cudaError_t launch_gemm_thin(const GemmProblem &p, cudaStream_t s, int64_t *launches);
 
 // Launches the DMMA (f64/c128) or FFMA (f32/c64) GEMM. Returns cudaSuccess or
 // the launch error. `launches` is incremented per kernel launched.
@@ -172,6 +181,12 @@ size_t reduce_scratch_bytes();
 // out[i] = sum_j (cr_j + i ci_j) in_j[i], m <= kMaxLC; out may alias an input
 cudaError_t launch_lincomb(bool cplx, const double *const *in, const double *cr, const double *ci, int m,
                            double *out, int64_t n, cudaStream_t s, int64_t *launches);
+
+// offs[i] = sum_l ((i / inner_l) % ext_l) * stride_l over nl legs given
+// slowest first (inner_l = product of the extents after l): gamma offsets of
+// the GEMM rows / columns for the scatter epilogue
+cudaError_t launch_offsets(int64_t *offs, int64_t n, int nl, const int64_t *ext, const int64_t *stride,
+                           cudaStream_t s, int64_t *launches);
 
 // Plain device copy (aliasing fallback) and elementwise helpers.
 cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s, int64_t *launches);

@@ -452,6 +452,7 @@ class Context:
         self._ws = None
         self._ws_bytes = 0
         self._desc: Dict[tuple, int] = {}
+        self._ws_need: Dict[tuple, int] = {}
 
     # -- descriptors ---------------------------------------------------------
     def tensor(self, t) -> int:
@@ -472,6 +473,7 @@ class Context:
         for h in self._desc.values():
             tci_tensor_free(self.handle, h)
         self._desc.clear()
+        self._ws_need.clear()
 
     # -- workspace -----------------------------------------------------------
     def ensure_workspace(self, nbytes: int):
@@ -499,8 +501,14 @@ class Context:
             shape = self.contract_out_shape(a, la, b, lb, lc)
             out = self.torch.empty(shape, dtype=a.dtype, device=a.device)
         ha, hb, hc = self.tensor(a), self.tensor(b), self.tensor(out)
-        self.ensure_workspace(tci_contract_workspace_size(self.handle, ha, _labels_list(la), hb,
-                                                          _labels_list(lb), hc, _labels_list(lc)))
+        key = (ha, hb, hc, la if isinstance(la, str) else tuple(la), lb if isinstance(lb, str) else tuple(lb),
+               lc if isinstance(lc, str) else tuple(lc))
+        ws = self._ws_need.get(key)
+        if ws is None:   # the planner's answer depends only on the descriptors and labels
+            ws = tci_contract_workspace_size(self.handle, ha, _labels_list(la), hb, _labels_list(lb), hc,
+                                             _labels_list(lc))
+            self._ws_need[key] = ws
+        self.ensure_workspace(ws)
         if isinstance(la, str) and isinstance(lb, str) and isinstance(lc, str):
             tci_contract_str(self.handle, ha, la, hb, lb, hc, lc)
         else:

@@ -188,22 +188,24 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
                      overlap(c.data, c.bytes(), b.data, b.bytes());
 
   // ---- plan choice (cached) ----
+  // binary key: dtype, alias, then (extent, canonical id) per leg of a, b, c
   std::string key;
   {
-    char buf[64];
-    key.reserve(256);
-    snprintf(buf, sizeof buf, "%d|%d|", (int)a.dtype, (int)alias);
-    key += buf;
+    int64_t buf[2 + 6 * kMaxOrder + 3];
+    int nk = 0;
+    buf[nk++] = (int64_t)a.dtype;
+    buf[nk++] = (int64_t)alias;
     auto put = [&](int n, const int64_t *s, const int *ids) {
+      buf[nk++] = n;
       for (int k = 0; k < n; k++) {
-        snprintf(buf, sizeof buf, "%lld:%d,", (long long)s[k], ids[k]);
-        key += buf;
+        buf[nk++] = s[k];
+        buf[nk++] = ids[k];
       }
-      key += ';';
     };
     put(a.order, a.shape, ida);
     put(b.order, b.shape, idb);
     put(c.order, c.shape, idc);
+    key.assign(reinterpret_cast<const char *>(buf), nk * sizeof(int64_t));
   }
   int choice = -1, formA = 0, formB = 0, formC = 0;
   auto it = ctx->plan_cache.find(key);

@@ -382,6 +382,52 @@ def trunc_svd(a, k, chi_min, chi_max, target_trunc_err, s_min):
             np.ascontiguousarray(vd[:chi]), err)
 
 
+def itebd_update(GA, lA, GB, lB, U, chi, s_min=1e-12, threads=None):
+    """One bond update of Vidal's iTEBD (Application A, PAPER.md:392-403;
+    SPEC.md itebd_update_bond): theta[a,s,t,c] = lB[a] GA[a,s,b] lA[b]
+    GB[b,t,c] lB[c]; theta' = U.theta over (s,t) (tebd_theta, R16);
+    trunc_svd at (a p)|(q c) with chi_max = chi; the new centre
+    lambda is normalised and the outer lambdas are divided back out.
+    Returns (GA', lA', GB', trunc_err)."""
+    A = lB[:, None, None] * GA * lA[None, None, :]
+    B = GB * lB[None, None, :]
+    th = tebd_theta(A, B, U, threads=threads)
+    X, s, Y, err = trunc_svd(th, 2, 1, chi, 0.0, s_min)
+    s = s / np.sqrt(np.sum(s * s))
+    return X / lB[:, None, None], s, Y / lB[None, None, :], err
+
+
+def itebd_bond_energy(GA, lA, GB, lB, h, threads=None):
+    """<theta|h|theta>/<theta|theta> for the bond A-B in the canonical
+    lB GA lA GB lB form (h[p,q,s,t], real data)."""
+    A = lB[:, None, None] * GA * lA[None, None, :]
+    B = GB * lB[None, None, :]
+    th = contract(A, "asb", B, "btc", "astc", threads)
+    hth = contract(th, "astc", h, "pqst", "apqc", threads)
+    return float(np.sum(th * hth) / np.sum(th * th))
+
+
+def itebd_tfim(g, chi, schedule, gate, h, seed=0):
+    """Imaginary-time iTEBD for the 1D TFIM (R25) from a
+    random product state: for (tau, steps) in schedule, `steps` A-B / B-A
+    bond-update pairs with U = gate(tau). Returns the energy per site (the
+    mean of the two bond energies) and the final state."""
+    rng = np.random.default_rng(seed)
+    GA = rng.uniform(-1, 1, (1, 2, 1))
+    GB = rng.uniform(-1, 1, (1, 2, 1))
+    GA /= np.linalg.norm(GA)
+    GB /= np.linalg.norm(GB)
+    lA = np.ones(1)
+    lB = np.ones(1)
+    for tau, steps in schedule:
+        U = gate(tau)
+        for _ in range(steps):
+            GA, lA, GB, _ = itebd_update(GA, lA, GB, lB, U, chi)
+            GB, lB, GA, _ = itebd_update(GB, lB, GA, lA, U, chi)
+    e = 0.5 * (itebd_bond_energy(GA, lA, GB, lB, h) + itebd_bond_energy(GB, lB, GA, lA, h))
+    return e, (GA, lA, GB, lB)
+
+
 # ----------------------------------------------------------------------------
 # vector functions (App. C.5): definitions written out
 # ----------------------------------------------------------------------------

@@ -262,3 +262,53 @@ def test_svd_large_vs_oracle(ctx, oracle_mod, dt):
     _, rs, _ = oracle_mod.svd(a, 2)
     assert max_abs(host(s), rs) <= TOL * rs[0]
     check_valid(host(u), host(s), host(vd), a, 2)
+
+
+def _tfim_h(g):
+    X = np.array([[0.0, 1.0], [1.0, 0.0]])
+    Z = np.diag([1.0, -1.0])
+    I = np.eye(2)
+    return (-np.kron(Z, Z) + 0.5 * g * (np.kron(X, I) + np.kron(I, X))).reshape(2, 2, 2, 2)
+
+
+def test_itebd_tfim_critical_energy_on_gpu(ctx, oracle_mod):
+    """Application A: imaginary-time iTEBD of the critical TFIM at
+    chi = 16 with every contraction (tci_tebd_theta, tci_contract) and every
+    truncated SVD (tci_trunc_svd) on the GPU; the lambda scalings are test
+    glue. The energy per site matches the oracle's iTEBD run (same seed and
+    schedule) to 1e-8 and the exact -4/pi (Pfeuty) to 1e-4 (SPEC acceptance 5)."""
+    g, chi = 1.0, 16
+    schedule = [(0.1, 200), (0.01, 300), (0.001, 300)]
+    e_or, _ = oracle_mod.itebd_tfim(g, chi, schedule, lambda tau: synth.tfim_gate(tau, 1.0, g), _tfim_h(g))
+    rng = np.random.default_rng(0)                       # oracle.itebd_tfim's initial product state
+    GA = rng.uniform(-1, 1, (1, 2, 1))
+    GB = rng.uniform(-1, 1, (1, 2, 1))
+    GA, GB = dev(GA / np.linalg.norm(GA)), dev(GB / np.linalg.norm(GB))
+    lA = torch.ones(1, dtype=torch.float64, device="cuda")
+    lB = torch.ones(1, dtype=torch.float64, device="cuda")
+
+    def update(GA, lA, GB, lB, U):
+        A = (lB[:, None, None] * GA * lA[None, None, :]).contiguous()
+        B = (GB * lB[None, None, :]).contiguous()
+        th = ctx.tebd_theta(A, "asb", B, "btc", U, "pqst", "apqc")
+        X, s, Y, _ = ctx.trunc_svd(th, 2, 1, chi, 0.0, 1e-12)
+        s = s / torch.sqrt(torch.sum(s * s))
+        return (X / lB[:, None, None]).contiguous(), s.contiguous(), (Y / lB[None, None, :]).contiguous()
+
+    for tau, steps in schedule:
+        U = dev(synth.tfim_gate(tau, 1.0, g))
+        for _ in range(steps):
+            GA, lA, GB = update(GA, lA, GB, lB, U)
+            GB, lB, GA = update(GB, lB, GA, lA, U)
+    h = dev(_tfim_h(g))
+
+    def bond_energy(GA, lA, GB, lB):
+        A = (lB[:, None, None] * GA * lA[None, None, :]).contiguous()
+        B = (GB * lB[None, None, :]).contiguous()
+        th = ctx.contract(A, "asb", B, "btc", "astc")
+        hth = ctx.contract(th, "astc", h, "pqst", "apqc")
+        return float(ctx.contract(th, "astc", hth, "astc", "")) / float(ctx.contract(th, "astc", th, "astc", ""))
+
+    e = 0.5 * (bond_energy(GA, lA, GB, lB) + bond_energy(GB, lB, GA, lA))
+    assert abs(e - e_or) <= 1e-8
+    assert abs(e + 4.0 / np.pi) <= 1e-4

@@ -730,3 +730,49 @@ def test_trunc_svd_fidelity_identity(oracle_mod):
     psi1 = np.einsum("ijka,a,alm n->ijklmn".replace(" ", ""), u, s, vd)
     ovlp = float(np.sum(psi * psi1))
     assert err > 0 and abs(ovlp - (1 - err)) <= 1e-14
+
+
+# ---------------------------------------------------------------------------
+# iTEBD (Application A) built from tebd_theta + trunc_svd
+# ---------------------------------------------------------------------------
+
+def _tfim_h(g):
+    X = np.array([[0.0, 1.0], [1.0, 0.0]])
+    Z = np.diag([1.0, -1.0])
+    I = np.eye(2)
+    return (-np.kron(Z, Z) + 0.5 * g * (np.kron(X, I) + np.kron(I, X))).reshape(2, 2, 2, 2)
+
+
+def pfeuty_e0(g):
+    """Exact TFIM ground-state energy per site (Pfeuty 1970):
+    e0 = -(1/2pi) int_0^2pi sqrt(1 + g^2 - 2 g cos k) dk; the uniform-grid mean
+    of a smooth periodic integrand is spectrally accurate."""
+    k = np.linspace(0.0, 2.0 * np.pi, 400001)[:-1]
+    return float(-np.mean(np.sqrt(1.0 + g * g - 2.0 * g * np.cos(k))))
+
+
+ITEBD_SCHEDULE = [(0.1, 200), (0.01, 300), (0.001, 300)]
+
+
+def test_pfeuty_quadrature_closed_forms():
+    assert abs(pfeuty_e0(1.0) + 4.0 / np.pi) <= 1e-10          # critical point: -4/pi (kink at k = 0: O(1/N^2))
+    assert abs(pfeuty_e0(0.0) + 1.0) <= 1e-15                  # classical ferromagnet
+
+
+@pytest.mark.parametrize("g,tol", [(1.0, 1e-4), (0.5, 1e-5)])
+def test_itebd_tfim_energy(oracle_mod, g, tol):
+    """SPEC.md:618-621 / acceptance 5: chi = 16 imaginary-time iTEBD reaches the
+    Pfeuty energy (within 1e-4 at the critical point g = 1, 1e-5 at g = 0.5)."""
+    e, _ = oracle_mod.itebd_tfim(g, 16, ITEBD_SCHEDULE, lambda tau: synth.tfim_gate(tau, 1.0, g), _tfim_h(g))
+    assert abs(e - pfeuty_e0(g)) <= tol
+    assert e >= pfeuty_e0(g) - 1e-9                            # variational (up to Trotter error)
+
+
+def test_itebd_identity_gate_on_product_state(oracle_mod):
+    """SPEC itebd_update_bond examples: from a product state (chi = 1) the
+    identity gate keeps rank 1, so trunc_err = 0 (up to rounding noise of the
+    discarded values) and the new centre lambda is exactly (1)."""
+    rng = np.random.default_rng(3)
+    GA, GB = rng.uniform(-1, 1, (1, 2, 1)), rng.uniform(-1, 1, (1, 2, 1))
+    GA2, lA2, GB2, err = oracle_mod.itebd_update(GA, np.ones(1), GB, np.ones(1), synth.tfim_gate(0.0), 4)
+    assert lA2.shape == (1,) and lA2[0] == 1.0 and err <= 1e-30

@@ -460,6 +460,27 @@ TCI_API tci_status_t tci_trunc_svd(tci_ctx_t ctx, tci_tensor_t a, int num_of_bds
                                    tci_tensor_t s_diag, tci_tensor_t v_dag, double *trunc_err, int64_t chi_min,
                                    int64_t chi_max, double target_trunc_err, double s_min, int64_t *chi_out);
 
+/* Compressed MPS-MPO application by zip-up (R32):
+ * B ~ W|psi> for an open-boundary MPS A[i] [chi_{i-1}, d_i, chi_i] (chi_{-1} =
+ * chi_{n-1} = 1) and MPO W[i] [D_{i-1}, D_i, d_i (in), d'_i (out)] (D_{-1} =
+ * D_{n-1} = 1; index order of R15). Left to right: T1 = C.A_i, T = T1.W_i
+ * (tci_contract semantics), then for i < n-1 the truncated SVD of T at
+ * (k t)|(b v) (tci_trunc_svd with chi_min = 1, chi_max, target 0, s_min):
+ * B_i = U, carry C = S V^dag; B_{n-1} = T. Every step runs in the library's
+ * kernels; the host loops over the sites.
+ * B[i] are caller-allocated device tensors of CAPACITY shape [c_{i-1}, d'_i,
+ * c_i], c_{-1} = c_{n-1} = 1, c_i = min(chi_max, c_{i-1} d'_i, chi_i D_i); on
+ * success their descriptors are reshaped to the kept bonds (dense row-major
+ * buffers). *trunc_err = sum over bonds of the discarded weights.
+ * With chi_max >= every exact bond and s_min = 0 the result is W|psi> exactly
+ * (up to rounding). Synchronous. Scratch: tci_mps_mpo_zipup_workspace_size.
+ * Errors: OUT_OF_RANGE (n < 1, chi_max < 1, s_min < 0), UNSUPPORTED (dtype),
+ * ORDER_MISMATCH / SHAPE_MISMATCH (bonds, capacities), WORKSPACE, CUDA. */
+TCI_API tci_status_t tci_mps_mpo_zipup_workspace_size(tci_ctx_t ctx, int n, const tci_tensor_t *A,
+                                                      const tci_tensor_t *W, int64_t chi_max, size_t *bytes);
+TCI_API tci_status_t tci_mps_mpo_zipup(tci_ctx_t ctx, int n, const tci_tensor_t *A, const tci_tensor_t *W,
+                                       tci_tensor_t *B, int64_t chi_max, double s_min, double *trunc_err);
+
 /* Diagnostics of the last tci_svd / tci_trunc_svd on this context: Jacobi
  * sweeps executed and the final sweep's largest relative off-diagonal
  * |<x_i|x_j>| / (|x_i| |x_j|) (convergence: <= max(1e-13, 4 sqrt(max(I,J)) eps),

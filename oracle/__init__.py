@@ -382,6 +382,28 @@ def trunc_svd(a, k, chi_min, chi_max, target_trunc_err, s_min):
             np.ascontiguousarray(vd[:chi]), err)
 
 
+def mps_mpo_zipup(A, W, chi_max, s_min=0.0, threads=None):
+    """Compressed MPS-MPO application by zip-up (R32):
+    C = 1; per site T1 = C.A_i ("kaw","asb"->"kwsb"), T = T1.W_i
+    ("kwsb","wvst"->"ktbv"); for i < n-1 trunc_svd of T at (k t)|(b v) with
+    chi_min = 1: B_i = U, C = S V^dag; the last site takes T.
+    Returns (B sites, sum of the per-bond discarded weights)."""
+    C = np.ones((1, 1, 1), dtype=np.result_type(A[0], W[0]))
+    out, err = [], 0.0
+    n = len(A)
+    for i in range(n):
+        T1 = contract(C, "kaw", A[i], "asb", "kwsb", threads)
+        T = contract(T1, "kwsb", W[i], "wvst", "ktbv", threads)
+        if i == n - 1:
+            out.append(np.ascontiguousarray(T.reshape(T.shape[0], T.shape[1], 1)))
+            break
+        U, S, Vd, e = trunc_svd(T, 2, 1, chi_max, 0.0, s_min)
+        out.append(U)
+        err += e
+        C = S[:, None, None] * Vd
+    return out, err
+
+
 def itebd_update(GA, lA, GB, lB, U, chi, s_min=1e-12, threads=None):
     """One bond update of Vidal's iTEBD (Application A, PAPER.md:392-403;
     SPEC.md itebd_update_bond): theta[a,s,t,c] = lB[a] GA[a,s,b] lA[b]

@@ -16,6 +16,8 @@ from __future__ import annotations
 
 import ctypes
 import os
+
+import numpy as np
 from typing import Dict, Optional, Sequence, Tuple, Union
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -47,6 +49,7 @@ EXPORTED = [
     "tci_lanczos_workspace_size", "tci_heff_lanczos", "tci_set_gemm_algorithm", "tci_get_gemm_algorithm",
     "tci_ozaki_params", "tci_env_workspace_size", "tci_env_update", "tci_cplx_conj",
     "tci_svd_workspace_size", "tci_svd", "tci_trunc_svd", "tci_svd_info",
+    "tci_mps_mpo_zipup_workspace_size", "tci_mps_mpo_zipup",
 ]
 
 
@@ -91,6 +94,10 @@ _sig = {
     "tci_trunc_svd": ([_vp, _vp, ctypes.c_int, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
                        ctypes.c_int64, ctypes.c_double, ctypes.c_double, _i64p], ctypes.c_int),
     "tci_svd_info": ([_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "tci_mps_mpo_zipup_workspace_size": ([_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.c_int64,
+                                          ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tci_mps_mpo_zipup": ([_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                           ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tci_tebd_theta": ([_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p], ctypes.c_int),
     "tci_comm_init": ([_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "tci_comm_unique_id": ([ctypes.c_char_p], ctypes.c_int),
@@ -291,6 +298,24 @@ def tci_trunc_svd(ctx: int, a: int, num_of_bds_as_row: int, u: int, s_diag: int,
                            ctypes.byref(err), int(chi_min), int(chi_max), float(target_trunc_err), float(s_min),
                            ctypes.byref(chi)), "tci_trunc_svd")
     return err.value, chi.value
+
+
+def tci_mps_mpo_zipup_workspace_size(ctx: int, A: Sequence[int], W: Sequence[int], chi_max: int) -> int:
+    n = ctypes.c_size_t()
+    arr = lambda xs: (_vp * len(xs))(*[_vp(x) for x in xs])  # noqa: E731
+    _ok(_lib.tci_mps_mpo_zipup_workspace_size(_vp(ctx), len(A), arr(A), arr(W), int(chi_max), ctypes.byref(n)),
+        "tci_mps_mpo_zipup_workspace_size")
+    return n.value
+
+
+def tci_mps_mpo_zipup(ctx: int, A: Sequence[int], W: Sequence[int], B: Sequence[int], chi_max: int,
+                      s_min: float) -> float:
+    """Returns trunc_err; the B descriptors are reshaped to the kept bonds."""
+    err = ctypes.c_double()
+    arr = lambda xs: (_vp * len(xs))(*[_vp(x) for x in xs])  # noqa: E731
+    _ok(_lib.tci_mps_mpo_zipup(_vp(ctx), len(A), arr(A), arr(W), arr(B), int(chi_max), float(s_min),
+                               ctypes.byref(err)), "tci_mps_mpo_zipup")
+    return err.value
 
 
 def tci_svd_info(ctx: int) -> Tuple[int, float]:
@@ -606,6 +631,29 @@ class Context:
         s = s[:chi]
         vd = vd.view(-1)[: vd.numel() // cap * chi].view((chi,) + tuple(a.shape[k:]))
         return u, s, vd, err
+
+    def mps_mpo_zipup(self, A, W, chi_max, s_min=0.0):
+        """Compressed W|psi> by zip-up (tci_mps_mpo_zipup): returns (B sites, trunc_err)."""
+        torch = self.torch
+        n = len(A)
+        caps, left = [], 1
+        for i in range(n):
+            dout = W[i].shape[3]
+            c = 1 if i == n - 1 else min(int(chi_max), left * dout, A[i].shape[2] * W[i].shape[1])
+            caps.append((left, dout, c))
+            left = c
+        B = [torch.empty(c, dtype=A[0].dtype, device=A[0].device) for c in caps]
+        ha, hw = [self.tensor(x) for x in A], [self.tensor(x) for x in W]
+        self.ensure_workspace(tci_mps_mpo_zipup_workspace_size(self.handle, ha, hw, chi_max))
+        hb = [self._fresh(x) for x in B]
+        try:
+            err = tci_mps_mpo_zipup(self.handle, ha, hw, hb, chi_max, s_min)
+            shapes = [tci_shape(self.handle, h) for h in hb]
+        finally:
+            for h in hb:
+                tci_tensor_free(self.handle, h)
+        out = [b.view(-1)[: int(np.prod(sh))].view(sh) for b, sh in zip(B, shapes)]
+        return out, err
 
     def svd_info(self):
         return tci_svd_info(self.handle)

@@ -657,6 +657,32 @@ tci_status_t tci_trunc_svd(tci_ctx_t ctx, tci_tensor_t a, int num_of_bds_as_row,
                     target_trunc_err, s_min, chi_out);
 }
 
+tci_status_t tci_mps_mpo_zipup_workspace_size(tci_ctx_t ctx, int n, const tci_tensor_t *A, const tci_tensor_t *W,
+                                              int64_t chi_max, size_t *bytes) {
+  CHECK(check_ctx(ctx));
+  if (!A || !W || !bytes) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (n < 1 || n > 4096) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "zipup: %d sites", n);
+  for (int i = 0; i < n; i++) {
+    CHECK(check_ten(ctx, A[i], false));
+    CHECK(check_ten(ctx, W[i], false));
+  }
+  return zipup_bytes(ctx, n, A, W, chi_max, bytes);
+}
+
+tci_status_t tci_mps_mpo_zipup(tci_ctx_t ctx, int n, const tci_tensor_t *A, const tci_tensor_t *W, tci_tensor_t *B,
+                               int64_t chi_max, double s_min, double *trunc_err) {
+  CHECK(check_ctx(ctx));
+  if (!A || !W || !B) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL site arrays");
+  if (n < 1 || n > 4096) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "zipup: %d sites", n);
+  for (int i = 0; i < n; i++) {
+    CHECK(check_ten(ctx, A[i], true));
+    CHECK(check_ten(ctx, W[i], true));
+    CHECK(check_ten(ctx, B[i], true));
+  }
+  Verbose vb(ctx, "mps_mpo_zipup", {A[0], W[0]});
+  return zipup_exec(ctx, n, A, W, B, chi_max, s_min, trunc_err);
+}
+
 tci_status_t tci_svd_info(tci_ctx_t ctx, int *sweeps, double *off) {
   CHECK(check_ctx(ctx));
   if (sweeps) *sweeps = ctx->svd_last_sweeps;

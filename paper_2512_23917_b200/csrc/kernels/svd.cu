@@ -368,9 +368,21 @@ __device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_in
 }
 
 // rows <- A rows over chunks [c0, c1) of one matrix (in place), A = G^H
+// the first NST - 1 chunk loads of an update pass (issued early by the caller
+// so they overlap the eigensolver)
+template <bool C>
+__device__ __forceinline__ void update_prologue(RoundSmem<C> &sm, const typename Cx<C>::E *X, int64_t ld, int c0,
+                                                int c1, int64_t row_lo, int64_t row_hi) {
+#pragma unroll
+  for (int s = 0; s < Cx<C>::NST - 1; s++) {
+    if (s < c1 - c0) load_chunk<C>(sm, s, X, ld, row_lo, row_hi, (int64_t)(c0 + s) * Cx<C>::CW);
+    cp_async_commit();
+  }
+}
+
 template <bool C>
 __device__ void update_pass(RoundSmem<C> &sm, typename Cx<C>::E *X, int64_t ld, int c0, int c1, int64_t row_lo,
-                            int64_t row_hi) {
+                            int64_t row_hi, bool prologue_done = false) {
   constexpr int CW = Cx<C>::CW, NST = Cx<C>::NST, TW = CW / 16;   // column tiles per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ti = warp >> 1, tj0 = TW * (warp & 1);
@@ -390,11 +402,7 @@ __device__ void update_pass(RoundSmem<C> &sm, typename Cx<C>::E *X, int64_t ld, 
   }
   const int orow = ti * 8 + (lane >> 2);
   const int64_t grow = orow < SB ? row_lo + orow : row_hi + (orow - SB);
-#pragma unroll
-  for (int s = 0; s < NST - 1; s++) {
-    if (s < nch) load_chunk<C>(sm, s, X, ld, row_lo, row_hi, (int64_t)(c0 + s) * CW);
-    cp_async_commit();
-  }
+if (!prologue_done) update_prologue<C>(sm, X, ld, c0, c1, row_lo, row_hi);
   for (int c = 0; c < nch; c++) {
     cp_async_wait<NST - 2>();
     __syncthreads();
@@ -505,8 +513,11 @@ __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, 
   const int64_t lo_real = n - row_lo < 0 ? 0 : (n - row_lo > SB ? SB : n - row_lo);
   const int64_t hi_real = n - row_hi < 0 ? 0 : (n - row_hi > SB ? SB : n - row_hi);
   // real rows form a prefix of the pair's row list (padding rows are the top indices)
+  // the staging ring is free now (Hp was consumed): start streaming X for
+  // the update while the eigensolver runs
+  update_prologue<C>(sm, X, ldx, x0, x1, row_lo, row_hi);
   block_eig<C>(sm, lo_real < SB ? (int)lo_real : SB + (int)hi_real, tol_in, max_inner);
-  update_pass<C>(sm, X, ldx, x0, x1, row_lo, row_hi);
+  update_pass<C>(sm, X, ldx, x0, x1, row_lo, row_hi, true);
   update_pass<C>(sm, Y, ldy, y0, y1, row_lo, row_hi);
 }
 

@@ -146,6 +146,27 @@ cudaError_t launch_lincomb(bool cplx, const double *const *in, const double *cr,
   return cudaGetLastError();
 }
 
+// out[r, c] = s[r] * in[r, c] (real scale s, r64 / c128 rows of `cols`
+// elements): the diagonal S of an SVD absorbed into V^H (zip-up carry)
+template <bool C>
+__global__ void __launch_bounds__(RT) row_scale_kernel(const double *in, const double *s, double *out, int64_t rows,
+                                                       int64_t cols) {
+  const int64_t w = C ? 2 : 1, n = rows * cols * w;
+  for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT)
+    out[i] = s[i / (cols * w)] * in[i];
+}
+
+cudaError_t launch_row_scale(bool cplx, const double *in, const double *s, double *out, int64_t rows, int64_t cols,
+                             cudaStream_t st, int64_t *launches) {
+  const int64_t n = rows * cols * (cplx ? 2 : 1);
+  const int64_t blocks = std::min<int64_t>((n + RT - 1) / RT, 148 * 8);
+  if (blocks <= 0) return cudaSuccess;
+  if (cplx) row_scale_kernel<true><<<(unsigned)blocks, RT, 0, st>>>(in, s, out, rows, cols);
+  else row_scale_kernel<false><<<(unsigned)blocks, RT, 0, st>>>(in, s, out, rows, cols);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
 // complex conjugation: out[i] = (re, -im); in == out allowed.
 // 16-byte elements, grid-stride, one load and one store per element.
 __global__ void __launch_bounds__(RT) conj_kernel(const double2 *in, double2 *out, int64_t n) {

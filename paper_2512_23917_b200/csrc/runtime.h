@@ -149,6 +149,12 @@ tci_status_t env_exec(tci_ctx_s *ctx, int side, const View &E, const View &K, co
 tci_status_t svd_bytes(tci_dtype_t dt, int order, const int64_t *shape, int k, size_t *bytes);
 tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t chi_min, int64_t chi_max,
                       double target, double s_min, tci_tensor_s *tu, tci_tensor_s *ts, tci_tensor_s *tv,
-                      double *trunc_err, int64_t *chi_out);
+                      double *trunc_err, int64_t *chi_out, void *ws = nullptr, size_t ws_bytes = 0);
+
+// Zip-up MPS-MPO application with truncation (zipup.cpp)
+tci_status_t zipup_bytes(tci_ctx_s *ctx, int n, const tci_tensor_s *const *A, const tci_tensor_s *const *W,
+                         int64_t chi_max, size_t *bytes);
+tci_status_t zipup_exec(tci_ctx_s *ctx, int n, const tci_tensor_s *const *A, const tci_tensor_s *const *W,
+                        tci_tensor_s *const *B, int64_t chi_max, double s_min, double *trunc_err);
 
 }  // namespace tci

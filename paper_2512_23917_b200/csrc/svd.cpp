@@ -112,7 +112,7 @@ tci_status_t svd_bytes(tci_dtype_t dt, int order, const int64_t *shape, int k, s
 
 tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t chi_min, int64_t chi_max,
                       double target, double s_min, tci_tensor_s *tu, tci_tensor_s *ts, tci_tensor_s *tv,
-                      double *trunc_err, int64_t *chi_out) {
+                      double *trunc_err, int64_t *chi_out, void *ws_base, size_t ws_bytes) {
   SvdDims d;
   tci_status_t st = svd_dims(a.dtype, a.order, a.shape, k, d);
   if (st) return st;
@@ -141,10 +141,14 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
     const char *x = (const char *)a.data, *y = (const char *)o->data;
     if (x < y + o->bytes() && y < x + a.bytes()) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "svd: an output overlaps a");
   }
-  if (ctx->ws_bytes < d.total || (d.total && !ctx->ws))
-    TCI_FAIL(TCI_ERR_WORKSPACE, "svd: workspace %zu B < %zu B (tci_svd_workspace_size)", ctx->ws_bytes, d.total);
+  if (!ws_base) {
+    ws_base = ctx->ws;
+    ws_bytes = ctx->ws_bytes;
+  }
+  if (ws_bytes < d.total || (d.total && !ws_base))
+    TCI_FAIL(TCI_ERR_WORKSPACE, "svd: workspace %zu B < %zu B (tci_svd_workspace_size)", ws_bytes, d.total);
 
-  char *ws = static_cast<char *>(ctx->ws);
+  char *ws = static_cast<char *>(ws_base);
   SvdProblem p;
   p.cplx = a.dtype == TCI_C128;
   p.tall = d.tall;

@@ -188,6 +188,10 @@ cudaError_t launch_lincomb(bool cplx, const double *const *in, const double *cr,
 cudaError_t launch_offsets(int64_t *offs, int64_t n, int nl, const int64_t *ext, const int64_t *stride,
                            cudaStream_t s, int64_t *launches);
 
+// out[r, :] = s[r] * in[r, :] over rows x cols elements (r64 / c128)
+cudaError_t launch_row_scale(bool cplx, const double *in, const double *s, double *out, int64_t rows, int64_t cols,
+                             cudaStream_t st, int64_t *launches);
+
 // Plain device copy (aliasing fallback) and elementwise helpers.
 cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s, int64_t *launches);
 // complex128 conjugation of n elements (in == out allowed)

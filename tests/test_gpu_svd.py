@@ -312,3 +312,65 @@ def test_itebd_tfim_critical_energy_on_gpu(ctx, oracle_mod):
     e = 0.5 * (bond_energy(GA, lA, GB, lB) + bond_energy(GB, lB, GA, lA))
     assert abs(e - e_or) <= 1e-8
     assert abs(e + 4.0 / np.pi) <= 1e-4
+
+
+# ---------------------------------------------------------------------------
+# zip-up MPS-MPO application (R32)
+# ---------------------------------------------------------------------------
+
+def _dense_mps(sites):
+    v = sites[0].reshape(sites[0].shape[1], sites[0].shape[2])
+    for A in sites[1:]:
+        v = np.einsum("xa,asb->xsb", v, A).reshape(-1, A.shape[2])
+    return v.reshape(-1)
+
+
+def _zipup_inputs(n, chi, D, d, dt, seed):
+    rng = np.random.default_rng(seed)
+    bonds = [1] + [min(chi, d ** min(i + 1, n - i - 1)) for i in range(n - 1)] + [1]
+    mb = [1] + [D] * (n - 1) + [1]
+    cp = dt == "c128"
+
+    def r(*sh):
+        x = rng.uniform(-1, 1, sh)
+        return x + 1j * rng.uniform(-1, 1, sh) if cp else x
+    return [r(bonds[i], d, bonds[i + 1]) for i in range(n)], [r(mb[i], mb[i + 1], d, d) for i in range(n)]
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+@pytest.mark.parametrize("n,chi,D,chi_max", [(6, 4, 3, 10 ** 6), (8, 8, 5, 10 ** 6), (8, 8, 5, 6), (10, 16, 5, 12)])
+def test_zipup_vs_oracle(ctx, oracle_mod, dt, n, chi, D, chi_max):
+    """The state itself (dense amplitudes) is unique: compared with the
+    oracle's zip-up to 1e-11 relative (truncated runs: the cut singular values
+    of random data are non-degenerate); trunc_err to 1e-10 relative."""
+    A, W = _zipup_inputs(n, chi, D, 2, dt, 100 + n + chi_max % 97)
+    B, err = ctx.mps_mpo_zipup([dev(x) for x in A], [dev(x) for x in W], chi_max)
+    RB, rerr = oracle_mod.mps_mpo_zipup(A, W, chi_max)
+    assert [tuple(b.shape) for b in B] == [b.shape for b in RB]
+    assert rel_frob(_dense_mps([host(b) for b in B]), _dense_mps(RB)) <= 1e-11
+    assert abs(err - rerr) <= 1e-10 * max(rerr, 1e-300) + 1e-26
+
+
+def test_zipup_long_chain_heisenberg(ctx, oracle_mod):
+    """40-site chi = 32 MPS, Heisenberg MPO (D = 5), compressed to chi = 32:
+    per-site factors from the GPU reproduce the oracle's energy-like overlap
+    <psi|B> (a contraction of the whole chain, tci_contract on the GPU)."""
+    n = 40
+    rng = np.random.default_rng(5)
+    bonds = [1] + [min(32, 2 ** min(i + 1, n - i - 1)) for i in range(n - 1)] + [1]
+    A = [rng.uniform(-1, 1, (bonds[i], 2, bonds[i + 1])) for i in range(n)]
+    Wh, lb, rb = synth.heisenberg_mpo(1.0)
+    Wh = np.asarray(Wh).real
+    W = [Wh[lb:lb + 1]] + [Wh] * (n - 2) + [Wh[:, rb:rb + 1]]
+    B, err = ctx.mps_mpo_zipup([dev(x) for x in A], [dev(x) for x in W], 32)
+    RB, rerr = oracle_mod.mps_mpo_zipup(A, W, 32)
+
+    def overlap(bra, ket):
+        E = np.ones((1, 1))
+        for x, y in zip(bra, ket):
+            E = oracle_mod.contract(oracle_mod.contract(E, "xz", x, "xsy", "zsy"), "zsy", y, "zsw", "yw")
+        return float(E[0, 0])
+    got = overlap(A, [host(b) for b in B])
+    ref = overlap(A, RB)
+    assert abs(got - ref) <= 1e-10 * abs(ref)
+    assert abs(err - rerr) <= 1e-9 * rerr

@@ -776,3 +776,74 @@ def test_itebd_identity_gate_on_product_state(oracle_mod):
     GA, GB = rng.uniform(-1, 1, (1, 2, 1)), rng.uniform(-1, 1, (1, 2, 1))
     GA2, lA2, GB2, err = oracle_mod.itebd_update(GA, np.ones(1), GB, np.ones(1), synth.tfim_gate(0.0), 4)
     assert lA2.shape == (1,) and lA2[0] == 1.0 and err <= 1e-30
+
+
+# ---------------------------------------------------------------------------
+# zip-up MPS-MPO application
+# ---------------------------------------------------------------------------
+
+def dense_mps(sites):
+    """Amplitudes psi(s_1..s_n) = A_1[s_1] ... A_n[s_n] (open boundary)."""
+    v = sites[0].reshape(sites[0].shape[1], sites[0].shape[2])
+    for A in sites[1:]:
+        v = np.einsum("xa,asb->xsb", v, A).reshape(-1, A.shape[2])
+    return v.reshape(-1)
+
+
+def dense_mpo(W):
+    """Operator matrix O[(t_1..t_n),(s_1..s_n)] from W[w,v,s,t] by Kronecker assembly."""
+    M = W[0][0]                                    # [v, s, t]
+    M = np.transpose(M, (0, 2, 1))                 # [v, t, s]
+    for Wi in W[1:]:
+        M = np.einsum("vTS,vwst->wTtSs", M, Wi)
+        M = M.reshape(M.shape[0], M.shape[1] * M.shape[2], M.shape[3] * M.shape[4])
+    return M[0]
+
+
+def _zipup_inputs(n, chi, D, d, dt, seed):
+    rng = np.random.default_rng(seed)
+    bonds = [1] + [min(chi, d ** min(i + 1, n - i - 1)) for i in range(n - 1)] + [1]
+    mb = [1] + [D] * (n - 1) + [1]
+    cp = dt == "c128"
+    def r(*sh):
+        x = rng.uniform(-1, 1, sh)
+        return x + 1j * rng.uniform(-1, 1, sh) if cp else x
+    A = [r(bonds[i], d, bonds[i + 1]) for i in range(n)]
+    W = [r(mb[i], mb[i + 1], d, d) for i in range(n)]
+    return A, W
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_zipup_exact_equals_dense_operator(oracle_mod, dt):
+    """No truncation (chi_max above every exact bond, s_min = 0): the zip-up
+    state equals W|psi> formed densely (Kronecker-assembled MPO matrix)."""
+    A, W = _zipup_inputs(6, 4, 3, 2, dt, 11)
+    B, err = oracle_mod.mps_mpo_zipup(A, W, 10 ** 6)
+    ref = dense_mpo(W) @ dense_mps(A)
+    assert err <= 1e-28
+    assert rel_frob(dense_mps(B), ref) <= 1e-13
+
+
+def test_zipup_identity_mpo_and_heisenberg(oracle_mod):
+    """Identity MPO (D = 1, W = I) reproduces psi; the Heisenberg MPO gives
+    <psi|H|psi> of the dense Kronecker Hamiltonian (bra = psi, real data)."""
+    A, _ = _zipup_inputs(6, 4, 1, 2, "r64", 12)
+    I = [np.eye(2).reshape(1, 1, 2, 2) for _ in range(6)]
+    B, _ = oracle_mod.mps_mpo_zipup(A, I, 10 ** 6)
+    assert rel_frob(dense_mps(B), dense_mps(A)) <= 1e-13
+    Wh, lb, rb = synth.heisenberg_mpo(1.0)
+    Wh = np.asarray(Wh).real
+    Ws = [Wh[lb:lb + 1]] + [Wh] * 4 + [Wh[:, rb:rb + 1]]
+    B, _ = oracle_mod.mps_mpo_zipup(A, Ws, 10 ** 6)
+    psi = dense_mps(A)
+    assert abs(psi @ dense_mps(B) - psi @ dense_mpo(Ws) @ psi) <= 1e-12 * abs(psi @ psi)
+
+
+def test_zipup_truncation_error_accounting(oracle_mod):
+    """With chi_max = 2 the kept state is no longer exact, the reported error
+    is positive, and chi_max >= exact bonds reports zero."""
+    A, W = _zipup_inputs(6, 4, 3, 2, "r64", 13)
+    B, err = oracle_mod.mps_mpo_zipup(A, W, 2)
+    assert err > 0 and max(b.shape[2] for b in B) <= 2
+    ref = dense_mpo(W) @ dense_mps(A)
+    assert rel_frob(dense_mps(B), ref) > 1e-6

@@ -338,7 +338,15 @@ def run_tci(args):
         h2d = sum(x.numel() * x.element_size() for x in hosts.values())
         d2h = hout.numel() * hout.element_size()
 
+        staged = ws == 1
+
         def e2e_step():
+            if staged:
+                # tci_heff_apply_staged: the H2D copies of L, psi, W and R and the
+                # chunked D2H of the result overlap the computation
+                ctx.heff_apply_staged([hosts[k] for k in ("L", "W1", "W2", "R", "psi")] + [hout],
+                                      [devs[k] for k in ("L", "W1", "W2", "R", "psi")] + [out])
+                return
             for k in hosts:
                 ctx.copy(hosts[k], devs[k])        # tci_copy: pinned host -> device
             step()
@@ -361,7 +369,10 @@ def run_tci(args):
             te = float(tt.item())
         e2e = {"value": F / te / 1e12, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": te * 1e3,
-               "path": "tci_copy(pinned host->device) x5, tci_heff_apply, tci_copy(device->host)"}
+               "path": ("tci_heff_apply_staged (pinned host inputs/outputs; psi + W copied first, L streamed in "
+                        "8 column blocks behind GEMM1's row chunks, R behind L, D2H in 8 row chunks behind "
+                        "GEMM4)") if staged else
+                       "tci_copy(pinned host->device) x5, tci_heff_apply, tci_copy(device->host), tci_allgather"}
 
     if rank != 0:
         ctx.close()

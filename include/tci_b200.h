@@ -460,6 +460,24 @@ TCI_API tci_status_t tci_trunc_svd(tci_ctx_t ctx, tci_tensor_t a, int num_of_bds
                                    tci_tensor_t s_diag, tci_tensor_t v_dag, double *trunc_err, int64_t chi_min,
                                    int64_t chi_max, double target_trunc_err, double s_min, int64_t *chi_out);
 
+/* tci_heff_apply with the inputs in (pinned) host memory and the result
+ * returned to host memory, copies overlapped with the computation: the
+ * context's copy stream moves psi, W1, W2 to the device staging tensors
+ * (L..out, device, caller-owned); GEMM1 starts when they have arrived and
+ * reads L in eight column blocks, each copied in just before the Ozaki row
+ * chunk (or DMMA row-block GEMM) that needs it; R is copied behind L while
+ * GEMM1 and the MPO pass run; GEMM4's output rows are copied back in eight
+ * chunks as they are finished. Equivalent to tci_copy x5,
+ * tci_heff_apply, tci_copy, and stream-ordered on the context stream like
+ * them (the context stream waits for the last D2H copy). Each *_h tensor
+ * must match its device twin in dtype and shape (host or device memory;
+ * pinned host memory for overlap). Errors: as tci_heff_apply, plus
+ * SHAPE_MISMATCH for a twin mismatch. Scratch: tci_heff_workspace_size. */
+TCI_API tci_status_t tci_heff_apply_staged(tci_ctx_t ctx, tci_tensor_t L_h, tci_tensor_t W1_h, tci_tensor_t W2_h,
+                                           tci_tensor_t R_h, tci_tensor_t psi_h, tci_tensor_t out_h,
+                                           tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2, tci_tensor_t R,
+                                           tci_tensor_t psi, tci_tensor_t out);
+
 /* Compressed MPS-MPO application by zip-up (R32):
  * B ~ W|psi> for an open-boundary MPS A[i] [chi_{i-1}, d_i, chi_i] (chi_{-1} =
  * chi_{n-1} = 1) and MPO W[i] [D_{i-1}, D_i, d_i (in), d'_i (out)] (D_{-1} =

@@ -49,7 +49,7 @@ EXPORTED = [
     "tci_lanczos_workspace_size", "tci_heff_lanczos", "tci_set_gemm_algorithm", "tci_get_gemm_algorithm",
     "tci_ozaki_params", "tci_env_workspace_size", "tci_env_update", "tci_cplx_conj",
     "tci_svd_workspace_size", "tci_svd", "tci_trunc_svd", "tci_svd_info",
-    "tci_mps_mpo_zipup_workspace_size", "tci_mps_mpo_zipup",
+    "tci_mps_mpo_zipup_workspace_size", "tci_mps_mpo_zipup", "tci_heff_apply_staged",
 ]
 
 
@@ -85,6 +85,7 @@ _sig = {
     "tci_contract_workspace_size": ([_vp, _vp, _i32p, _vp, _i32p, _vp, _i32p, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tci_heff_workspace_size": ([_vp, ctypes.c_int] + [ctypes.c_int64] * 8 + [ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tci_heff_apply": ([_vp] * 7, ctypes.c_int),
+    "tci_heff_apply_staged": ([_vp] * 13, ctypes.c_int),
     "tci_env_workspace_size": ([_vp, ctypes.c_int] + [_vp] * 5 + [ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tci_env_update": ([_vp, ctypes.c_int] + [_vp] * 5, ctypes.c_int),
     "tci_cplx_conj": ([_vp] * 3, ctypes.c_int),
@@ -261,6 +262,12 @@ def tci_heff_workspace_size(ctx: int, dtype: int, chi_l, chi_lo, chi_r, chi_ro, 
 
 def tci_heff_apply(ctx: int, L: int, W1: int, W2: int, R: int, psi: int, out: int) -> None:
     _ok(_lib.tci_heff_apply(*[_vp(x) for x in (ctx, L, W1, W2, R, psi, out)]), "tci_heff_apply")
+
+
+def tci_heff_apply_staged(ctx: int, L_h: int, W1_h: int, W2_h: int, R_h: int, psi_h: int, out_h: int, L: int,
+                          W1: int, W2: int, R: int, psi: int, out: int) -> None:
+    _ok(_lib.tci_heff_apply_staged(*[_vp(x) for x in (ctx, L_h, W1_h, W2_h, R_h, psi_h, out_h, L, W1, W2, R, psi,
+                                                        out)]), "tci_heff_apply_staged")
 
 
 def tci_env_workspace_size(ctx: int, side: int, E: int, ket: int, W: int, bra: int, out: int) -> int:
@@ -551,6 +558,14 @@ class Context:
         self.ensure_workspace(self.heff_workspace_size(L, W1, W2, R, psi))
         tci_heff_apply(self.handle, *[self.tensor(x) for x in (L, W1, W2, R, psi, out)])
         return out
+
+    def heff_apply_staged(self, hosts, devs):
+        """tci_heff_apply_staged: hosts / devs = (L, W1, W2, R, psi, out) host and
+        device twins; the result lands in hosts[5] (copies overlap compute)."""
+        L = devs[0]
+        self.ensure_workspace(self.heff_workspace_size(devs[0], devs[1], devs[2], devs[3], devs[4]))
+        tci_heff_apply_staged(self.handle, *[self.tensor(x) for x in hosts], *[self.tensor(x) for x in devs])
+        return hosts[5]
 
     def env_update(self, side, E, ket, W, bra=None, out=None):
         """Environment update (tci_env_update): side 0 = left, 1 = right; bra defaults to ket."""

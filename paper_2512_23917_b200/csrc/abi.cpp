@@ -222,6 +222,8 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   }
   c->dev_scratch = nullptr;
   c->host_scratch = nullptr;
+  c->copy_stream = nullptr;
+  for (auto &e : c->evs) e = nullptr;
   c->svd_last_sweeps = 0;
   c->svd_last_off = 0.0;
   {
@@ -281,6 +283,16 @@ tci_status_t tci_destroy_context(tci_ctx_t ctx) {
   cudaStreamSynchronize(ctx->stream);
   prof_clear(ctx);
   ctx->prof_on = false;
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    ctx->copy_stream = nullptr;
+  }
+  for (auto &e : ctx->evs)
+    if (e) {
+      cudaEventDestroy(e);
+      e = nullptr;
+    }
   if (ctx->dev_scratch) cudaFree(ctx->dev_scratch);
   if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
   ctx->dev_scratch = ctx->host_scratch = nullptr;
@@ -574,6 +586,72 @@ tci_status_t tci_heff_apply(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_
   }
   Verbose vb(ctx, "heff_apply", {L, W1, W2, R, psi});
   return heff_exec(ctx, view_of(L), view_of(W1), view_of(W2), view_of(R), view_of(psi), vo);
+}
+
+tci_status_t tci_heff_apply_staged(tci_ctx_t ctx, tci_tensor_t L_h, tci_tensor_t W1_h, tci_tensor_t W2_h,
+                                   tci_tensor_t R_h, tci_tensor_t psi_h, tci_tensor_t out_h, tci_tensor_t L,
+                                   tci_tensor_t W1, tci_tensor_t W2, tci_tensor_t R, tci_tensor_t psi,
+                                   tci_tensor_t out) {
+  CHECK(check_ctx(ctx));
+  const tci_tensor_t hs[6] = {L_h, W1_h, W2_h, R_h, psi_h, out_h}, ds[6] = {L, W1, W2, R, psi, out};
+  for (int i = 0; i < 6; i++) {
+    CHECK(check_ten(ctx, hs[i], false));
+    CHECK(check_ten(ctx, ds[i], true));
+    if (hs[i]->dtype != ds[i]->dtype || hs[i]->order != ds[i]->order)
+      TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "heff_staged: host / device tensor %d differ in dtype or order", i);
+    for (int k = 0; k < ds[i]->order; k++)
+      if (hs[i]->shape[k] != ds[i]->shape[k])
+        TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "heff_staged: host / device tensor %d differ in shape", i);
+  }
+  const View vo = view_of(out);
+  for (int i = 0; i < 5; i++) {
+    const View v = view_of(ds[i]);
+    const char *x = (const char *)v.data, *y = (const char *)vo.data;
+    if (x < y + vo.bytes() && y < x + v.bytes()) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "heff: out overlaps an input");
+  }
+  Verbose vb(ctx, "heff_apply_staged", {L, W1, W2, R, psi});
+  if (L->order != 3 || R->order != 3) TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "heff: L and R must be order 3");
+  if (!ctx->copy_stream) TCI_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  for (auto &e : ctx->evs)
+    if (!e) TCI_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaStream_t s0 = ctx->stream, s1 = ctx->copy_stream;
+  // the copy stream starts after everything already queued on the context stream
+  TCI_CUDA_CHECK(cudaEventRecord(ctx->evs[0], s0));
+  TCI_CUDA_CHECK(cudaStreamWaitEvent(s1, ctx->evs[0], 0));
+  auto h2d = [&](int i) -> tci_status_t {
+    const View v = view_of(ds[i]);
+    TCI_CUDA_CHECK(cudaMemcpyAsync(v.data, hs[i]->data, v.bytes(), cudaMemcpyDefault, s1));
+    return TCI_OK;
+  };
+  // psi and the MPO first (GEMM1's B operand and the MPO pass); L follows in
+  // column blocks as GEMM1 reaches them, then R (heff_exec enqueues both)
+  for (int i : {4, 1, 2}) CHECK(h2d(i));
+  TCI_CUDA_CHECK(cudaEventRecord(ctx->evs[1], s1));
+  HeffStaging st{};
+  st.ctx = ctx;
+  st.ev_in = ctx->evs[1];
+  st.ev_R = ctx->evs[2];
+  st.ev_rows = ctx->evs[3];
+  st.ev_L = ctx->evs[5];
+  st.L_host = static_cast<const char *>(L_h->data);
+  st.L_dev = static_cast<char *>(L->data);
+  st.L_rows = L->shape[0];
+  st.L_cols = L->shape[1] * L->shape[2];
+  st.es = (int64_t)dtype_size(L->dtype);
+  st.R_host = static_cast<const char *>(R_h->data);
+  st.R_dev = static_cast<char *>(R->data);
+  st.R_bytes = view_of(R).bytes();
+  st.out_host = static_cast<char *>(out_h->data);
+  st.out_dev = static_cast<const char *>(out->data);
+  st.row_bytes = out->shape[3] * (int64_t)dtype_size(out->dtype);
+  const int64_t rows = out->shape[0] * out->shape[1] * out->shape[2];
+  st.chunk_rows = std::max<int64_t>(256, (rows + 7) / 8);
+  st.err = cudaSuccess;
+  tci_status_t r = heff_exec(ctx, view_of(L), view_of(W1), view_of(W2), view_of(R), view_of(psi), vo, &st);
+  // the context stream resumes after the last chunk has reached the host
+  TCI_CUDA_CHECK(cudaEventRecord(ctx->evs[4], s1));
+  TCI_CUDA_CHECK(cudaStreamWaitEvent(s0, ctx->evs[4], 0));
+  return r;
 }
 
 tci_status_t tci_env_workspace_size(tci_ctx_t ctx, int side, tci_tensor_t E, tci_tensor_t ket, tci_tensor_t W,

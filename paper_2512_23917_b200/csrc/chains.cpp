@@ -236,8 +236,36 @@ static tci_status_t exec_tree(tci_ctx_s *ctx, const std::vector<Node> &nd, int m
   return contract_exec(ctx, x, lx.data(), y, ly.data(), out, labs.data(), false, &need, arena, left);
 }
 
+namespace {
+// GEMM4 row chunk finished (enqueued) on the context stream: copy it out
+void stage_rows_out(void *user, int64_t m0, int64_t mc) {
+  HeffStaging *st = static_cast<HeffStaging *>(user);
+  if (st->err != cudaSuccess) return;
+  tci_ctx_s *ctx = st->ctx;
+  cudaError_t e = cudaEventRecord(st->ev_rows, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->copy_stream, st->ev_rows, 0);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(st->out_host + m0 * st->row_bytes, st->out_dev + m0 * st->row_bytes, mc * st->row_bytes,
+                        cudaMemcpyDeviceToHost, ctx->copy_stream);
+  st->err = e;
+}
+// GEMM1 is about to read A rows (w b) [m0, m0 + mc) = L columns: copy that
+// column block in on the copy stream and make the context stream wait for it
+void stage_L_in(void *user, int64_t m0, int64_t mc) {
+  HeffStaging *st = static_cast<HeffStaging *>(user);
+  if (st->err != cudaSuccess) return;
+  tci_ctx_s *ctx = st->ctx;
+  const size_t pitch = (size_t)st->L_cols * st->es;
+  cudaError_t e = cudaMemcpy2DAsync(st->L_dev + m0 * st->es, pitch, st->L_host + m0 * st->es, pitch,
+                                    (size_t)mc * st->es, (size_t)st->L_rows, cudaMemcpyDefault, ctx->copy_stream);
+  if (e == cudaSuccess) e = cudaEventRecord(st->ev_L, ctx->copy_stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->stream, st->ev_L, 0);
+  st->err = e;
+}
+}  // namespace
+
 tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View &W2, const View &R,
-                       const View &psi, const View &out) {
+                       const View &psi, const View &out, HeffStaging *stage) {
   const tci_dtype_t dt = L.dtype;
   if (W1.dtype != dt || W2.dtype != dt || R.dtype != dt || psi.dtype != dt || out.dtype != dt)
     TCI_FAIL(TCI_ERR_UNSUPPORTED, "heff: all operands must share one dtype");
@@ -262,13 +290,32 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
   const int64_t dims[NLAB] = {h.chi_l, h.D, h.chi_lo, h.d, h.d, h.chi_r, h.D1, h.d, h.D2, h.d, h.chi_ro};
   std::vector<Node> nd = plan_heff_tree(dims);
   char *ws = static_cast<char *>(ctx->ws);
+  if (stage) TCI_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, stage->ev_in, 0));
+  // R's H2D follows L's on the copy stream
+  auto copy_R = [&]() -> tci_status_t {
+    TCI_CUDA_CHECK(cudaMemcpyAsync(stage->R_dev, stage->R_host, stage->R_bytes, cudaMemcpyDefault,
+                                   ctx->copy_stream));
+    TCI_CUDA_CHECK(cudaEventRecord(stage->ev_R, ctx->copy_stream));
+    return TCI_OK;
+  };
   if (!is_standard_tree(nd)) {
+    if (stage) {
+      stage_L_in(stage, 0, stage->L_cols);
+      TCI_CUDA_CHECK(stage->err);
+      st = copy_R();
+      if (st) return st;
+      TCI_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, stage->ev_R, 0));
+    }
     const View leaf[5] = {L, psi, W1, W2, R};
     char *arena = ws;
     size_t left = ctx->ws_bytes;
     View o = out;
     std::vector<int32_t> labs;
-    return exec_tree(ctx, nd, 31, leaf, dims, arena, left, o, labs);
+    st = exec_tree(ctx, nd, 31, leaf, dims, arena, left, o, labs);
+    if (st || !stage) return st;
+    stage_rows_out(stage, 0, out.shape[0] * out.shape[1] * out.shape[2]);
+    TCI_CUDA_CHECK(stage->err);
+    return TCI_OK;
   }
   const HeffLayout lay = heff_layout(h, dt);
   const int64_t d = h.d, chi_lo = h.chi_lo, chi_r = h.chi_r;
@@ -295,7 +342,37 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
     if (g.M == 1) { g.a_sm = 1; g.a_sk = 1; }
     if (g.K == 1 && g.N == 1) g.b_sk = 1;
     else if (g.K == 1) g.b_sk = 0;
-    { tci_status_t _r = run_gemm(ctx, g); if (_r) return _r; }
+    if (stage && g.zalgo == kZOzaki && g.a_sm == 1) {
+      // L arrives column block by column block while GEMM1 computes
+      g.rows_needed = stage_L_in;
+      g.rows_user = stage;
+      g.max_chunk_rows = std::max<int64_t>(256, (g.M + 7) / 8);
+      { tci_status_t _r = run_gemm(ctx, g); if (_r) return _r; }
+      TCI_CUDA_CHECK(stage->err);
+    } else if (stage && g.a_sm == 1 && g.M >= 1024) {
+      const int64_t M = g.M, ch = (M + 3) / 4;
+      for (int64_t m0 = 0; m0 < M; m0 += ch) {
+        GemmProblem gc = g;
+        gc.M = std::min(ch, M - m0);
+        gc.A = static_cast<const char *>(g.A) + m0 * dtype_size(dt);
+        gc.C = static_cast<char *>(g.C) + m0 * g.c_sm * dtype_size(dt);
+        if (gc.zalgo == kZOzaki && !ozaki_worthwhile(gc.M, gc.N, gc.K)) gc.zalgo = kZ3M;
+        stage_L_in(stage, m0, gc.M);
+        TCI_CUDA_CHECK(stage->err);
+        { tci_status_t _r = run_gemm(ctx, gc); if (_r) return _r; }
+      }
+    } else {
+      if (stage) {
+        stage_L_in(stage, 0, stage->L_cols);
+        TCI_CUDA_CHECK(stage->err);
+      }
+      tci_status_t _r = run_gemm(ctx, g);
+      if (_r) return _r;
+    }
+    if (stage) {
+      st = copy_R();
+      if (st) return st;
+    }
   }
   void *T3;
   if (lay.fused) {
@@ -391,6 +468,7 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
     }
   }
   // ---- GEMM4: out[b,p,q,e] = sum_{c,x} T3[b,p,q,c,x] R[c,x,e] ----
+  if (stage) TCI_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, stage->ev_R, 0));
   {
     GemmProblem g{};
     g.dtype = dt;
@@ -400,7 +478,30 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
     g.C = out.data; g.c_sm = g.N;
     set_zalgo(g);
     if (g.N == 1) { g.b_sk = 1; }
-    { tci_status_t _r = run_gemm(ctx, g); if (_r) return _r; }
+    if (stage && g.zalgo == kZOzaki) {
+      // the Ozaki GEMM finishes rows chunk by chunk: stream them out
+      g.rows_done = stage_rows_out;
+      g.rows_user = stage;
+      g.max_chunk_rows = stage->chunk_rows;
+      { tci_status_t _r = run_gemm(ctx, g); if (_r) return _r; }
+      TCI_CUDA_CHECK(stage->err);
+    } else if (stage) {
+      // DMMA path: row-chunked GEMMs, each chunk copied out behind the next
+      const int64_t M = g.M, ch = std::max<int64_t>(1, stage->chunk_rows);
+      for (int64_t m0 = 0; m0 < M; m0 += ch) {
+        GemmProblem gc = g;
+        gc.M = std::min(ch, M - m0);
+        gc.A = static_cast<const char *>(g.A) + m0 * g.a_sm * dtype_size(dt);
+        gc.C = static_cast<char *>(g.C) + m0 * g.c_sm * dtype_size(dt);
+        if (gc.zalgo == kZOzaki && !ozaki_worthwhile(gc.M, gc.N, gc.K)) gc.zalgo = kZ3M;
+        { tci_status_t _r = run_gemm(ctx, gc); if (_r) return _r; }
+        stage_rows_out(stage, m0, gc.M);
+        TCI_CUDA_CHECK(stage->err);
+      }
+    } else {
+      tci_status_t _r = run_gemm(ctx, g);
+      if (_r) return _r;
+    }
   }
   return TCI_OK;
 }

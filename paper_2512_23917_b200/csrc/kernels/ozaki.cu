@@ -486,7 +486,7 @@ struct OzPlan {
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 size_t align_up(size_t x) { return (x + 255) / 256 * 256; }
 
-OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D) {
+OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_rows = 0) {
   OzPlan p{};
   const double lk = std::log2((double)std::max<int64_t>(K, 1));
   double lm = 0;
@@ -504,6 +504,7 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D) {
   int64_t mc = (int64_t)(budget_D / ((size_t)planes * (p.Np + p.Kp)));
   mc = std::max<int64_t>(256, mc / 256 * 256);
   p.Mc = std::min<int64_t>(round_up(M, 256), mc);
+  if (max_rows > 0) p.Mc = std::min<int64_t>(p.Mc, std::max<int64_t>(256, round_up(max_rows, 256)));
   p.chunks = (M + p.Mc - 1) / p.Mc;
   size_t off = 0;
   p.off_EA = off; off = align_up(off + (size_t)M * 4);
@@ -556,7 +557,7 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
                                int64_t *launches) {
   if (g.M == 0 || g.N == 0) return cudaSuccess;
   if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;   // int32 residue products would overflow
-  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30);
+  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
   char *w = static_cast<char *>(ws);
   int *EA = reinterpret_cast<int *>(w + p.off_EA), *EB = reinterpret_cast<int *>(w + p.off_EB);
@@ -577,7 +578,7 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       if (launches) *launches += 2;
     }
   };
-  exponents(A, g.M, g.a_sm, g.a_sk, EA);
+  if (!g.rows_needed) exponents(A, g.M, g.a_sm, g.a_sk, EA);   // else per row chunk (A streams in)
   exponents(B, g.N, g.b_sn, g.b_sk, EB);
   auto launch_res = [&](const ResArgs &r) {
     if (r.s_k == 1) {
@@ -619,6 +620,10 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   c.C = static_cast<double2 *>(g.C); c.c_sm = g.c_sm;
   for (int64_t ch = 0; ch < p.chunks; ch++) {
     const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
+    if (g.rows_needed) {
+      g.rows_needed(g.rows_user, m0, mc);
+      exponents(A + m0 * g.a_sm, mc, g.a_sm, g.a_sk, EA + m0);
+    }
     {
       ResArgs r{};
       r.base = A; r.nlines = g.M; r.K = g.K; r.Kp = p.Kp; r.s_l = g.a_sm; r.s_k = g.a_sk;
@@ -677,6 +682,7 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
     }
     if (ce != cudaSuccess) return ce;
     if (launches) ++*launches;
+    if (g.rows_done) g.rows_done(g.rows_user, m0, mc);
   }
   return cudaGetLastError();
 }

@@ -226,7 +226,7 @@ __device__ void gram_pass(RoundSmem<C> &sm, const typename Cx<C>::E *X, int64_t 
 // re-orthonormalisation), then A = G^H with the eigenpairs of the first nreal
 // rows in descending eigenvalue order (ties by index). A aliases H.
 template <bool C>
-__device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_inner) {
+__device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_inner, int sort) {
   using E = typename Cx<C>::E;
   const int tid = threadIdx.x;
   for (int idx = tid; idx < PR * PR; idx += NT) sm.G[idx / PR][idx % PR] = (idx / PR == idx % PR) ? cone<E>() : czero<E>();
@@ -347,7 +347,7 @@ __device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_in
   // padding rows (global index >= n, a suffix of the pair) keep their place,
   // so they stay exact zero rows of X and unit rows of Y
   if (tid < PR) {
-    if (tid < nreal) {
+    if (tid < nreal && sort) {
       const double e = sm.ev[tid];
       int rank = 0;
       for (int j = 0; j < nreal; j++) {
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, 
   // the staging ring is free now (Hp was consumed): start streaming X for
   // the update while the eigensolver runs
   update_prologue<C>(sm, X, ldx, x0, x1, row_lo, row_hi);
-  block_eig<C>(sm, lo_real < SB ? (int)lo_real : SB + (int)hi_real, tol_in, max_inner);
+  block_eig<C>(sm, lo_real < SB ? (int)lo_real : SB + (int)hi_real, tol_in, max_inner & 0xff, max_inner >> 8);
   update_pass<C>(sm, X, ldx, x0, x1, row_lo, row_hi, true);
   update_pass<C>(sm, Y, ldy, y0, y1, row_lo, row_hi);
 }

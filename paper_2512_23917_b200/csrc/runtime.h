@@ -36,6 +36,8 @@ struct tci_ctx_s {
   int zgemm_algo;       // complex128 GEMM algorithm (kZ3M default; tci_set_gemm_algorithm)
   void *dev_scratch;    // reductions (vec.cu): allocated once at creation
   void *host_scratch;   // pinned, reduction results
+  cudaStream_t copy_stream;   // library-owned (created on first use): staged H2D / D2H copies
+  cudaEvent_t evs[8];         // ordering events between the context and copy streams
   int svd_last_sweeps;  // Jacobi sweeps of the last svd / trunc_svd (tci_svd_info)
   double svd_last_off;  // its final off-diagonal measure
 };
@@ -134,8 +136,29 @@ ag_fn nccl_allgather_ptr();
 tci_status_t heff_plan_bytes(tci_dtype_t dt, int64_t chi_l, int64_t chi_lo, int64_t chi_r,
                              int64_t chi_ro, int64_t d, int64_t D, int64_t D1, int64_t D2,
                              size_t *bytes, bool *fused_w12, int zalgo = 0);
+// Host staging for tci_heff_apply_staged: ev_in / ev_R are recorded on the
+// copy stream after the H2D copies of (L, W1, W2, psi) / R; GEMM1 waits for
+// ev_in, GEMM4 for ev_R, and every finished row chunk of out is copied to
+// out_host on the copy stream.
+struct HeffStaging {
+  tci_ctx_s *ctx;
+  cudaEvent_t ev_in, ev_R, ev_rows, ev_L;
+  // L streamed in column blocks during GEMM1 (L[a, (w b)]: chi_l rows of
+  // m_cols elements); R copied after the last block
+  const char *L_host;
+  char *L_dev;
+  int64_t L_rows, L_cols, es;
+  const char *R_host;
+  char *R_dev;
+  size_t R_bytes;
+  char *out_host;
+  const char *out_dev;
+  int64_t row_bytes;
+  int64_t chunk_rows;
+  cudaError_t err;
+};
 tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View &W2, const View &R,
-                       const View &psi, const View &out);
+                       const View &psi, const View &out, HeffStaging *stage = nullptr);
 tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View &B, const char *lb,
                        const View &U, const char *lu, const View &T, const char *lt);
 

@@ -169,8 +169,10 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
   TCI_CUDA_CHECK(launch_svd_load(p, a.data, d.I, d.J, s, &ctx->launches));
   const double tol = default_tol(d.L);
   const double tol_in = 0.25 * tol;
-  int max_inner = 1;
+  int max_inner = 1, sort = 1;
   if (const char *e = getenv("TCI_SVD_INNER")) max_inner = std::max(1, atoi(e));
+  if (const char *e = getenv("TCI_SVD_SORT")) sort = atoi(e) != 0;
+  max_inner |= sort << 8;   // packed kernel parameter: sweeps | sort flag
   const bool trace = getenv("TCI_SVD_TRACE") != nullptr;
   const int nb = (int)(d.npad / 16);
   const int max_sweeps = 60;

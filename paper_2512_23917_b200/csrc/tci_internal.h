@@ -55,6 +55,17 @@ struct GemmProblem {
   // is stored at c_row[m] + c_col[n] (device tables, elements) instead of
   // m * c_sm + n; split-K partials stay dense and the reduction scatters
   const int64_t *c_row = nullptr, *c_col = nullptr;
+  // optional: called (host side, at enqueue time) after the kernels that
+  // finish output rows [m0, m0 + mc) have been enqueued on the stream -- the
+  // Ozaki path calls it per row chunk (at most max_chunk_rows rows when > 0),
+  // so a caller can stream finished rows out while later rows compute
+  void (*rows_done)(void *user, int64_t m0, int64_t mc) = nullptr;
+  // optional: called (host side) before the kernels that READ rows [m0,
+  // m0 + mc) of A are enqueued (the caller may make the stream wait for them
+  // to arrive); with it the Ozaki path also takes A's row exponents per chunk
+  void (*rows_needed)(void *user, int64_t m0, int64_t mc) = nullptr;
+  void *rows_user = nullptr;
+  int64_t max_chunk_rows = 0;
   int64_t te_chi_a = 0, te_chi_c = 0;     // extents of a and c
   int64_t te_a_a = 0, te_a_s = 0;         // A strides of a and s (b stride == 1)
   int64_t te_b_t = 0;                     // B stride of t (c stride == 1, b stride = b_sk)

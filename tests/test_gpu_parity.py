@@ -782,3 +782,31 @@ def test_env_update_chi1024_sampled(oracle_mod, side, algo):
         assert rel_frob(host(out)[rows], ref) <= 1e-12
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("algo", ["dmma3m", "ozaki"])
+def test_heff_apply_staged_bitwise(algo, oracle_mod):
+    """tci_heff_apply_staged (host inputs, copies overlapped with compute,
+    GEMM4 rows streamed back in chunks) equals tci_copy + tci_heff_apply +
+    tci_copy bitwise, for the chunked DMMA path and the Ozaki path; sampled
+    rows vs the oracle."""
+    c = tci.Context(0)
+    try:
+        c.set_gemm_algorithm(tci.TCI_GEMM_OZAKI_INT8 if algo == "ozaki" else tci.TCI_GEMM_DMMA_3M)
+        cfg = synth.HEFF_CONFIGS["cfg2_heisenberg_chi1024"]
+        inp = synth.heff_inputs(cfg["chi"], cfg["d"], cfg["D"], cfg["dtype"], cfg["seed"], cfg["model"])
+        keys = ("L", "W1", "W2", "R", "psi")
+        d_in = {k: dev(inp[k]) for k in keys}
+        ref_dev = c.heff_apply(*[d_in[k] for k in keys])
+        hosts = [inp[k].contiguous().pin_memory() for k in keys]
+        hout = torch.empty(ref_dev.shape, dtype=ref_dev.dtype).pin_memory()
+        devs = [torch.empty_like(d_in[k]) for k in keys] + [torch.empty_like(ref_dev)]
+        c.heff_apply_staged(hosts + [hout], devs)
+        c.synchronize()
+        assert torch.equal(hout, ref_dev.cpu())
+        n = {k: v.numpy() for k, v in inp.items()}
+        rows = [0, 511, 1023]
+        ref = oracle_mod.heff_rows(n["L"], n["W1"], n["W2"], n["R"], n["psi"], rows)
+        assert rel_frob(hout.numpy()[rows], ref) <= 1e-12
+    finally:
+        c.close()

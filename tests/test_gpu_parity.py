@@ -810,3 +810,36 @@ def test_heff_apply_staged_bitwise(algo, oracle_mod):
         assert rel_frob(hout.numpy()[rows], ref) <= 1e-12
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("name", ["target_heisenberg_chi4096", "cfg4_hubbard_chi4096"])
+def test_heff_full_size_rows_and_freivalds(name, oracle_mod):
+    """BASELINE configs at full size (the bench workload chi = 4096, d = 2,
+    D = 5 and config 4: chi = 4096, d = 4, D = 6, c128) with the bench's
+    default algorithm (Ozaki-II): two sampled output rows vs the oracle, and a
+    whole-output Freivalds check: out . x for a random x on the e leg equals
+    the chain applied with R.x (the oracle contracts psi with R.x first,
+    O(chi^2 D d^4) instead of O(D d^2 chi^3)). Tolerance 1e-12 (north star)."""
+    cfg = synth.HEFF_CONFIGS[name]
+    chi, d, D = cfg["chi"], cfg["d"], cfg["D"]
+    c = tci.Context(0)
+    try:
+        c.set_gemm_algorithm(tci.TCI_GEMM_OZAKI_INT8)
+        dv = synth.heff_inputs(chi, d, D, "c128", cfg["seed"], cfg["model"], device="cuda")
+        out = c.heff_apply(dv["L"], dv["W1"], dv["W2"], dv["R"], dv["psi"])
+        x = synth.random_tensor((chi,), "c128", cfg["seed"], 98, device="cuda")
+        ox = host(c.contract(out, "bpqe", x, "e", "bpq"))      # GPU contraction of the GPU output
+        rows = [1, chi - 2]
+        got_rows = host(out[rows])
+        del out
+        n = {k: v.cpu().numpy() for k, v in dv.items()}
+        del dv
+        torch.cuda.empty_cache()
+        xn = x.cpu().numpy()
+        Rx = oracle_mod.contract(n["R"], "cxe", xn, "e", "cx").reshape(chi, D, 1)
+        ref_ox = oracle_mod.heff_alt(n["L"], n["W1"], n["W2"], Rx, n["psi"])[..., 0]
+        assert rel_frob(ox, ref_ox) <= 1e-12
+        ref_rows = oracle_mod.heff_rows(n["L"], n["W1"], n["W2"], n["R"], n["psi"], rows)
+        assert rel_frob(got_rows, ref_rows) <= 1e-12
+    finally:
+        c.close()

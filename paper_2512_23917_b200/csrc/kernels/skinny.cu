@@ -14,6 +14,8 @@
 // fixed order -> deterministic), and results are staged in shared memory and
 // written back in (n_hi, b2, n_lo) order so global stores are contiguous when
 // the trailing n-run is interleaved with b2.
+#include <algorithm>
+
 #include "../tci_internal.h"
 #include "common.cuh"
 
@@ -107,6 +109,192 @@ __global__ void __launch_bounds__(NTH) skinny_kernel(const __grid_constant__ Ski
   }
 }
 
+// ---------------------------------------------------------------------------
+// Streaming variant (b2 contiguous in the input, k_lo == 1): persistent CTAs,
+// the [K x TB] input tile of the next (b0, b1, b2-block) is prefetched with
+// cp.async while the current one is contracted; each thread owns NPT
+// CONSECUTIVE outputs n = g*NPT .. g*NPT + NPT - 1 of one b2 value and stores
+// them straight from registers (with the trailing n-run interleaved with b2,
+// as in the H_eff MPO pass, a warp then writes one contiguous block).
+// Complex products use 3 real multiplications (Gauss / 3M, as the DMMA GEMM):
+// P = sum xr wr, Q = sum xi wi, S = sum (xr + xi)(wr + wi); re = P - Q,
+// im = S - P - Q (normwise stable, R11).
+// ---------------------------------------------------------------------------
+constexpr int NC = 2;            // b2 values per thread (register blocking: weights reused NC times)
+constexpr int TBS = TB * NC;     // b2 values per streamed tile
+
+template <bool CPLX, int NPT, bool FULL>
+__global__ void __launch_bounds__(NTH) skinny_stream_kernel(const __grid_constant__ SkinnyProblem a,
+                                                            int64_t ntiles) {
+  using T = typename SkE<CPLX>::T;
+  constexpr int NW = CPLX ? 3 : 1;       // weight planes: (wr, wi, wr + wi) or w
+  extern __shared__ __align__(16) char sm[];
+  const int K = a.K, N = a.N;
+  double *sW = reinterpret_cast<double *>(sm);                    // [NW][K][N]
+  T *sIn = reinterpret_cast<T *>(sW + NW * K * N + (NW * K * N) % 2);   // [2][K][TBS], 16 B aligned
+  const T *W = reinterpret_cast<const T *>(a.W);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < K * N; i += NTH) {
+    const int k = i / N, n = i % N;
+    const T w = W[a.w_koff[k] + a.w_noff[n]];
+    if constexpr (CPLX) {
+      sW[i] = w.x;
+      sW[K * N + i] = w.y;
+      sW[2 * K * N + i] = w.x + w.y;
+    } else {
+      sW[i] = w;
+    }
+  }
+  const int64_t tiles2 = (a.nb[2] + TBS - 1) / TBS;
+  auto tile_ptrs = [&](int64_t t, const T *&in, T *&out, int &nc) {
+    const int64_t t2 = t % tiles2, r = t / tiles2;
+    const int64_t i1 = r % a.nb[1], i0 = r / a.nb[1];
+    const int64_t c0 = t2 * TBS;
+    nc = (int)min((int64_t)TBS, a.nb[2] - c0);
+    in = reinterpret_cast<const T *>(a.in) + i0 * a.in_sb[0] + i1 * a.in_sb[1] + c0;
+    out = reinterpret_cast<T *>(a.out) + i0 * a.out_sb[0] + i1 * a.out_sb[1] + c0 * a.out_sb[2];
+  };
+  constexpr int PER16 = 16 / (int)sizeof(T);   // elements per 16-byte copy
+  auto load = [&](int64_t t, int buf) {
+    const T *in;
+    T *out;
+    int nc;
+    tile_ptrs(t, in, out, nc);
+    T *dst = sIn + buf * K * TBS;
+    constexpr int CPR = TBS / PER16;
+    for (int i = tid; i < K * CPR; i += NTH) {
+      const int k = i / CPR, q = i % CPR;
+      const int c = q * PER16;
+      const int valid = c < nc ? (int)min(16, (nc - c) * (int)sizeof(T)) : 0;
+      cp_async_zfill<16>(dst + k * TBS + c, valid ? in + a.in_koff[k] + c : in, valid);
+    }
+  };
+  int64_t t = blockIdx.x;
+  if (t < ntiles) load(t, 0);
+  cp_async_commit();
+  const int cl = tid % TB, g = tid / TB;   // b2 values cl + TB * i, outputs g*NPT ..
+  const int n0 = g * NPT;
+  int buf = 0;
+  for (; t < ntiles; t += gridDim.x, buf ^= 1) {
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntiles) load(tn, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const T *tile = sIn + buf * K * TBS;
+    const T *in;
+    T *out;
+    int nc;
+    tile_ptrs(t, in, out, nc);
+    if constexpr (CPLX) {
+      double P[NC][NPT], Q[NC][NPT], S[NC][NPT];
+#pragma unroll
+      for (int i = 0; i < NC; i++)
+#pragma unroll
+        for (int j = 0; j < NPT; j++) P[i][j] = Q[i][j] = S[i][j] = 0.0;
+#pragma unroll 2
+      for (int k = 0; k < K; k++) {
+        double xr[NC], xi[NC], xs[NC];
+#pragma unroll
+        for (int i = 0; i < NC; i++) {
+          const T x = tile[k * TBS + cl + TB * i];
+          xr[i] = x.x;
+          xi[i] = x.y;
+          xs[i] = x.x + x.y;
+        }
+        const double *wr = sW + k * N + n0, *wi = wr + K * N, *ws = wi + K * N;
+#pragma unroll
+        for (int j = 0; j < NPT; j++) {
+          if (FULL || n0 + j < N) {
+            const double a_ = wr[j], b_ = wi[j], c_ = ws[j];
+#pragma unroll
+            for (int i = 0; i < NC; i++) {
+              P[i][j] = fma(xr[i], a_, P[i][j]);
+              Q[i][j] = fma(xi[i], b_, Q[i][j]);
+              S[i][j] = fma(xs[i], c_, S[i][j]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NC; i++) {
+        const int c = cl + TB * i;
+        if (c < nc) {
+#pragma unroll
+          for (int j = 0; j < NPT; j++)
+            if (FULL || n0 + j < N)
+              out[c * a.out_sb[2] + a.out_noff[n0 + j]] =
+                  make_double2(P[i][j] - Q[i][j], S[i][j] - P[i][j] - Q[i][j]);
+        }
+      }
+    } else {
+      double acc[NC][NPT];
+#pragma unroll
+      for (int i = 0; i < NC; i++)
+#pragma unroll
+        for (int j = 0; j < NPT; j++) acc[i][j] = 0.0;
+#pragma unroll 2
+      for (int k = 0; k < K; k++) {
+        double x[NC];
+#pragma unroll
+        for (int i = 0; i < NC; i++) x[i] = tile[k * TBS + cl + TB * i];
+        const double *w = sW + k * N + n0;
+#pragma unroll
+        for (int j = 0; j < NPT; j++)
+          if (FULL || n0 + j < N) {
+            const double wj = w[j];
+#pragma unroll
+            for (int i = 0; i < NC; i++) acc[i][j] = fma(x[i], wj, acc[i][j]);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < NC; i++) {
+        const int c = cl + TB * i;
+        if (c < nc) {
+#pragma unroll
+          for (int j = 0; j < NPT; j++)
+            if (FULL || n0 + j < N) out[c * a.out_sb[2] + a.out_noff[n0 + j]] = acc[i][j];
+        }
+      }
+    }
+    __syncthreads();   // this buffer is refilled two tiles later
+  }
+  cp_async_wait<0>();
+}
+
+template <bool CPLX, int NPT>
+cudaError_t launch_stream_npt(const SkinnyProblem &p, cudaStream_t s) {
+  const size_t es = CPLX ? 16 : 8;
+  const int NW = CPLX ? 3 : 1;
+  const size_t smem = (size_t)(NW * p.K * p.N + (NW * p.K * p.N) % 2) * 8 + 2 * (size_t)p.K * TBS * es;
+  const int64_t ntiles = p.nb[0] * p.nb[1] * ((p.nb[2] + TBS - 1) / TBS);
+  auto k = (p.N == NPT * NG) ? skinny_stream_kernel<CPLX, NPT, true> : skinny_stream_kernel<CPLX, NPT, false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTH, smem);
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)148 * std::max(1, per_sm));
+  k<<<(unsigned)grid, NTH, smem, s>>>(p, ntiles);
+  return cudaGetLastError();
+}
+
+template <bool CPLX>
+cudaError_t launch_stream(const SkinnyProblem &p, cudaStream_t s) {
+  const int npt = (p.N + NG - 1) / NG;
+  switch (npt) {
+    case 1: return launch_stream_npt<CPLX, 1>(p, s);
+    case 2: return launch_stream_npt<CPLX, 2>(p, s);
+    case 3: return launch_stream_npt<CPLX, 3>(p, s);
+    case 4: return launch_stream_npt<CPLX, 4>(p, s);
+    case 5: return launch_stream_npt<CPLX, 5>(p, s);
+    case 6: return launch_stream_npt<CPLX, 6>(p, s);
+  }
+  if (npt <= 8) return launch_stream_npt<CPLX, 8>(p, s);
+  if (npt <= 12) return launch_stream_npt<CPLX, 12>(p, s);
+  if (npt <= 16) return launch_stream_npt<CPLX, 16>(p, s);
+  return launch_stream_npt<CPLX, MAXNPT>(p, s);
+}
+
 template <bool CPLX, int NPT>
 cudaError_t launch_npt(const SkinnyProblem &p, size_t smem, int64_t blocks, cudaStream_t s) {
   auto k = skinny_kernel<CPLX, NPT>;
@@ -149,6 +337,21 @@ cudaError_t launch_skinny(const SkinnyProblem &p0, cudaStream_t s, int64_t *laun
   const size_t smem = skinny_smem_bytes(p.K, p.N, cplx ? 16 : 8);
   const int64_t blocks = p.nb[0] * p.nb[1] * ((p.nb[2] + TB - 1) / TB);
   if (blocks == 0) return cudaSuccess;
+  // streaming variant: b2 unit-stride in the input, 16-byte aligned rows
+  {
+    const size_t es = cplx ? 16 : 8;
+    bool ok = p.in_sb[2] == 1 && p.k_lo == 1 && ((uintptr_t)p.in % 16) == 0 && p.K <= kSkinnyMaxK &&
+              p.N <= kSkinnyMaxN;
+    const int64_t per = 16 / (int64_t)es;
+    for (int k = 0; ok && k < p.K; k++) ok = p.in_koff[k] % per == 0;
+    ok = ok && p.in_sb[0] % per == 0 && p.in_sb[1] % per == 0;
+    const size_t ssm = (size_t)((cplx ? 3 : 1) * p.K * p.N + 1) * 8 + 2 * (size_t)p.K * TBS * es;
+    if (ok && ssm <= 200 * 1024) {
+      cudaError_t e = cplx ? launch_stream<true>(p, s) : launch_stream<false>(p, s);
+      if (launches) ++*launches;
+      return e;
+    }
+  }
   if (blocks > 0x7fffffffLL || p.K > kSkinnyMaxK || p.N > kSkinnyMaxN || smem > 227 * 1024)
     return cudaErrorInvalidValue;
   cudaError_t e = cplx ? launch_c<true>(p, smem, blocks, s) : launch_c<false>(p, smem, blocks, s);

@@ -19,11 +19,21 @@
 // relabelling is bitwise invariant (R23). Plans are cached per
 // context under that key.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "runtime.h"
 
 namespace tci {
+
+// TCI_CONTRACT_NO_SKINNY=1 disables the skinny route (A/B measurements)
+static bool skinny_route_disabled() {
+  static const bool off = [] {
+    const char *e = getenv("TCI_CONTRACT_NO_SKINNY");
+    return e && *e == '1';
+  }();
+  return off;
+}
 
 static int find_label(int n, const int32_t *l, int32_t x) {
   for (int i = 0; i < n; i++)
@@ -186,6 +196,96 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   };
   const bool alias = overlap(c.data, c.bytes(), a.data, a.bytes()) ||
                      overlap(c.data, c.bytes(), b.data, b.bytes());
+
+  // ---- skinny route (8(a5), 8(a10)): one small operand W (contracted
+  // extent K <= 64, free extent <= 128) against a large one X whose free legs
+  // form at most three (fused) batch groups: out[b, n] = sum_k X[b, k] W(k, n)
+  // streamed once through the skinny kernel, written in gamma order directly
+  // (no GEMM tile, no permute). f64 / c128, no aliasing.
+  if (!alias && (a.dtype == TCI_R64 || a.dtype == TCI_C128) && !skinny_route_disabled()) {
+    int64_t KS = 1;
+    for (int k = 0; k < A.n; k++)
+      if (inS[A.leg[k].id]) KS *= A.leg[k].dim;
+    auto sin = [](const Operand &o, int id) {
+      for (int k = 0; k < o.n; k++)
+        if (o.leg[k].id == id) return o.leg[k].stride;
+      return (int64_t)0;
+    };
+    for (int side = 0; side < 2 && KS <= 64; side++) {
+      const Operand &X = side == 0 ? A : B, &Wo = side == 0 ? B : A;
+      const int64_t nW = side == 0 ? b.size() : a.size(), nX = side == 0 ? a.size() : b.size();
+      if (nW * 16 > nX || nW > 64 * 128) continue;
+      const std::vector<char> &freeW = side == 0 ? inJ : inI;
+      const std::vector<char> &freeX = side == 0 ? inI : inJ;
+      int64_t NW = 1;
+      for (int k = 0; k < Wo.n; k++)
+        if (freeW[Wo.leg[k].id]) NW *= Wo.leg[k].dim;
+      if (NW > kSkinnyMaxN || KS > kSkinnyMaxK) continue;
+      // batch groups: X's free legs in X order (slowest first), fused when
+      // adjacent with matching strides in both X and C
+      int64_t gext[kMaxOrder], gin[kMaxOrder], gout[kMaxOrder];
+      int ng = 0;
+      for (int k = 0; k < X.n; k++) {
+        const int id = X.leg[k].id;
+        if (!freeX[id]) continue;
+        const int64_t e = X.leg[k].dim, si = X.leg[k].stride, so = sin(C, id);
+        if (ng > 0 && gin[ng - 1] == si * e && gout[ng - 1] == so * e) {
+          gext[ng - 1] *= e;
+          gin[ng - 1] = si;
+          gout[ng - 1] = so;
+        } else {
+          gext[ng] = e;
+          gin[ng] = si;
+          gout[ng] = so;
+          ng++;
+        }
+      }
+      if (ng > 3) continue;
+      SkinnyProblem sp{};
+      sp.dtype = a.dtype;
+      for (int g = 0; g < 3; g++) {
+        const int src = g - (3 - ng);
+        sp.nb[g] = src >= 0 ? gext[src] : 1;
+        sp.in_sb[g] = src >= 0 ? gin[src] : 0;
+        sp.out_sb[g] = src >= 0 ? gout[src] : 0;
+      }
+      sp.K = (int)KS;
+      sp.N = (int)NW;
+      // k enumerates the contracted legs in X order; n the free legs of W
+      // ordered by decreasing C stride (the fastest C leg innermost)
+      std::vector<int> kl, nl;
+      for (int k = 0; k < X.n; k++)
+        if (inS[X.leg[k].id]) kl.push_back(X.leg[k].id);
+      for (int k = 0; k < Wo.n; k++)
+        if (freeW[Wo.leg[k].id]) nl.push_back(Wo.leg[k].id);
+      std::stable_sort(nl.begin(), nl.end(), [&](int x, int y) { return sin(C, x) > sin(C, y); });
+      auto fill = [&](const std::vector<int> &legs, const Operand &o1, int64_t *off1, const Operand &o2,
+                      int32_t *off2, int64_t total) {
+        for (int64_t i = 0; i < total; i++) {
+          int64_t r = i, a1 = 0, a2 = 0;
+          for (int q = (int)legs.size() - 1; q >= 0; q--) {
+            const int64_t e = dim_of[legs[q]], c_ = r % e;
+            r /= e;
+            a1 += c_ * sin(o1, legs[q]);
+            a2 += c_ * sin(o2, legs[q]);
+          }
+          off1[i] = a1;
+          off2[i] = (int32_t)a2;
+        }
+      };
+      fill(kl, X, sp.in_koff, Wo, sp.w_koff, KS);
+      fill(nl, C, sp.out_noff, Wo, sp.w_noff, NW);
+      sp.k_lo = 1;
+      sp.n_lo = 1;
+      if (!nl.empty() && sin(C, nl.back()) == 1 && sp.out_sb[2] == dim_of[nl.back()]) sp.n_lo = (int)dim_of[nl.back()];
+      sp.in = side == 0 ? a.data : b.data;
+      sp.W = side == 0 ? b.data : a.data;
+      sp.out = c.data;
+      *ws_needed = 0;
+      if (dry_run) return TCI_OK;
+      return run_skinny(ctx, sp);
+    }
+  }
 
   // ---- plan choice (cached) ----
   // binary key: dtype, alias, then (extent, canonical id) per leg of a, b, c

@@ -229,6 +229,33 @@ def svd_cfg(ctx, reps=2):
     return res
 
 
+def mpo_apply_cfg(ctx, chi=4096, d=2, D=5):
+    """site-local uncompressed MPS-MPO application
+    B[a,w,t,b,v] = sum_s A[a,s,b] W[w,v,s,t] at chi = 4096, d = 2, D = 5, c128
+    (A 537 MB -> B 13.4 GB): HBM-bound, roofline = bytes / measured copy BW."""
+    A = synth.random_tensor((chi, d, chi), "c128", 31, 1, device="cuda")
+    Wh, _, _ = synth.heisenberg_mpo(1.0)
+    W = torch.from_numpy(np.asarray(Wh)).to(torch.complex128).cuda()
+    holder = {}
+
+    def f():
+        holder["b"] = ctx.contract(A, "asb", W, "wvst", "awtbv", out=holder.get("b"))
+    med, mn = timed(f, reps=5, warm=2)
+    byts = 16.0 * (A.numel() + W.numel() + chi * D * d * chi * D)
+    tci.tci_profile_enable(ctx.handle, True)
+    f()
+    sk = tci.tci_profile_query(ctx.handle, tci.PROF_SKINNY)
+    g = tci.tci_profile_query(ctx.handle, tci.PROF_GEMM)
+    pm = tci.tci_profile_query(ctx.handle, tci.PROF_PERMUTE)
+    tci.tci_profile_enable(ctx.handle, False)
+    res = {"workload": f"MPS-MPO site apply chi={chi} d={d} D={D} c128", "ms": med * 1e3, "GBs": byts / med / 1e9,
+           "frac_hbm": byts / med / HBM, "bytes": byts, "skinny_launches": sk["launches"],
+           "gemm_launches": g["launches"], "permute_launches": pm["launches"]}
+    del A, W, holder
+    torch.cuda.empty_cache()
+    return res
+
+
 def sweep(ctx, seeds=24):
     """Config 5: random rank 3..6 contractions up to 2^28 elements, f64 and f32."""
     import string
@@ -307,6 +334,8 @@ def main():
             res["sweep"] = sweep(ctx)
         elif k == "permute":
             res["permute"] = permute_bw(ctx)
+        elif k == "mpo":
+            res["mpo"] = mpo_apply_cfg(ctx)
         elif k == "svd":
             res["svd"] = svd_cfg(ctx)
         elif k == "env":

@@ -374,3 +374,29 @@ def test_zipup_long_chain_heisenberg(ctx, oracle_mod):
     ref = overlap(A, RB)
     assert abs(got - ref) <= 1e-10 * abs(ref)
     assert abs(err - rerr) <= 1e-9 * rerr
+
+
+def test_trunc_svd_tebd_theta_full_size(ctx, oracle_mod):
+    """Config 3 at full size (chi = 2048, d = 2, f64): theta = A.B.U on the GPU
+    (4096 x 4096), trunc_svd to chi_max = 2048 on the GPU. Checked against
+    LAPACK's singular values (<= 1e-12 s_0), orthonormality of u and v_dag,
+    and the Eckart-Young identity ||theta - u s v_dag||_F^2 = sum_{i >= chi}
+    s_i^2 (= trunc_err * ||theta||_F^2, P:2088-2090)."""
+    c = synth.TEBD_CONFIG
+    inp = synth.tebd_inputs(c["chi"], c["d"], c["dtype"], c["seed"], c["tau"], device="cuda")
+    th = ctx.tebd_theta(inp["A"], "asb", inp["B"], "btc", inp["U"], "pqst", "apqc")
+    del inp
+    u, s, vd, err = ctx.trunc_svd(th, 2, 1, c["chi"], 0.0, 0.0)
+    T = host(th).reshape(4096, 4096)
+    rs = np.linalg.svd(T, compute_uv=False)
+    chi = s.shape[0]
+    assert chi == c["chi"]
+    assert max_abs(host(s), rs[:chi]) <= TOL * rs[0]
+    U = host(u).reshape(4096, chi)
+    V = host(vd).reshape(chi, 4096)
+    assert max_abs(U.T @ U, np.eye(chi)) <= TOL
+    assert max_abs(V @ V.T, np.eye(chi)) <= TOL
+    resid2 = np.linalg.norm(T - (U * host(s)) @ V) ** 2
+    tail = float(np.sum(rs[chi:] ** 2))
+    assert abs(resid2 - tail) <= 1e-9 * tail + 1e-12 * float(np.sum(rs ** 2))
+    assert abs(err - tail / float(np.sum(rs ** 2))) <= 1e-9 * err

@@ -2,7 +2,7 @@
 // 8(a4)): products where one of M, N, K is tiny. A tensor-core tile
 // (128x128x16) would compute mostly padding there, while the work is bound
 // by streaming the one large operand (or the output) once:
-//   * thin  (min(M, N) <= 16): C[m, n] = sum_k A[m, k] B[k, n] with N <= 16
+//   * thin  (min(M, N) <= 32 real / 16 complex): C[m, n] = sum_k A[m, k] B[k, n], N thin
 //     after an operand swap (C^T = B^T A^T); B's K-chunk is staged in shared
 //     memory and every row of A is read once, coalesced along whichever of m
 //     or k is contiguous (thread per row, or warp per row with a fixed-order
@@ -223,7 +223,12 @@ cudaError_t launch_thin_t(const ThinArgs &t, int splits, cudaStream_t s) {
   if (t.N <= 2) return launch_thin_nn<E, 2>(t, splits, s);
   if (t.N <= 4) return launch_thin_nn<E, 4>(t, splits, s);
   if (t.N <= 8) return launch_thin_nn<E, 8>(t, splits, s);
-  return launch_thin_nn<E, 16>(t, splits, s);
+  if constexpr (sizeof(typename TOps<E>::Acc) == 16) {
+    return launch_thin_nn<E, 16>(t, splits, s);   // complex: thin side <= 16
+  } else {
+    if (t.N <= 16) return launch_thin_nn<E, 16>(t, splits, s);
+    return launch_thin_nn<E, 32>(t, splits, s);
+  }
 }
 
 template <typename E>
@@ -243,7 +248,9 @@ cudaError_t launch_outer_t(const ThinArgs &t, cudaStream_t s) {
 
 bool gemm_thin_applies(const GemmProblem &p) {
   if (p.mode != 0 || p.M == 0 || p.N == 0) return false;
-  if (std::min(p.M, p.N) <= 16) return p.M < (1LL << 31) && p.N < (1LL << 31);
+  // thin side up to 32 (complex: 16, register budget); real GEMM tiles waste >= 75 % there
+  const int64_t thin_max = dtype_is_complex(p.dtype) ? 16 : 32;
+  if (std::min(p.M, p.N) <= thin_max) return p.M < (1LL << 31) && p.N < (1LL << 31);
   return p.K <= 16 && p.splitk <= 1;
 }
 

@@ -99,7 +99,7 @@ void ozaki_params(int64_t K, int *nmod, int *t, const int **moduli);
 // Output tile of the GEMM kernel used for `dtype` (for the planner's split-K choice).
 void gemm_tile(tci_dtype_t dtype, int *bm, int *bn);
 
-// HBM-bound GEMM corners (gemm_thin.cu): min(M, N) <= 16 (any K, honours the
+// HBM-bound GEMM corners (gemm_thin.cu): min(M, N) <= 32 (16 complex; any K, honours the
 // split-K fields) or K <= 16 (no split-K). launch_gemm dispatches to it.
 bool gemm_thin_applies(const GemmProblem &p);
 cudaError_t launch_gemm_thin(const GemmProblem &p, cudaStream_t s, int64_t *launches);

@@ -55,6 +55,8 @@ __device__ __forceinline__ double re(double x) { return x; }
 __device__ __forceinline__ double re(double2 x) { return x.x; }
 __device__ __forceinline__ double cabs(double x) { return fabs(x); }
 __device__ __forceinline__ double cabs(double2 x) { return hypot(x.x, x.y); }
+__device__ __forceinline__ double abs2(double x) { return x * x; }
+__device__ __forceinline__ double abs2(double2 x) { return fma(x.x, x.x, x.y * x.y); }
 __device__ __forceinline__ double cj(double x) { return x; }
 __device__ __forceinline__ double2 cj(double2 x) { return make_double2(x.x, -x.y); }
 __device__ __forceinline__ double cmul(double a, double b) { return a * b; }
@@ -71,8 +73,10 @@ template <> __device__ __forceinline__ double2 czero<double2>() { return make_do
 template <class E> __device__ __forceinline__ E cone();
 template <> __device__ __forceinline__ double cone<double>() { return 1.0; }
 template <> __device__ __forceinline__ double2 cone<double2>() { return make_double2(1.0, 0.0); }
-__device__ __forceinline__ double phase_of(double h, double ah) { return h / ah; }              // conj(h)/|h|
-__device__ __forceinline__ double2 phase_of(double2 h, double ah) { return make_double2(h.x / ah, -h.y / ah); }
+__device__ __forceinline__ double phase_of(double h, double ah) { return h >= 0.0 ? 1.0 : -1.0; }   // conj(h)/|h|
+__device__ __forceinline__ double2 phase_of(double2 h, double ah) {
+  return make_double2(h.x / ah, -h.y / ah);   // (not h * (1/ah): 1/ah overflows for subnormal |h|)
+}
 
 // A row whose squared norm is below 1e-36 of its partner's (norm ratio 1e-18)
 // is numerically zero next to it (reading R29): the pair counts as converged
@@ -248,14 +252,16 @@ __device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_in
         // c^2 + s^2 > 1 bias grows the row norms
         // pairs with a numerically zero row (R29) are left alone: the row is
         // completed at the end
-        if (ah == 0.0 || ah <= tol_in * sqrt(fabs(hi * hj)) || negligible(hi, hj)) {
+        if (ah == 0.0 || ah <= tol_in * sqrt(fabs(hi)) * sqrt(fabs(hj)) || negligible(hi, hj)) {
           sm.rflag[tid] = 0;
         } else {
           // real symmetric [[hi, |h|], [|h|, hj]] (after the phase) -> R = [[c, s], [-s, c]]
+          // tau = (hj - hi) / (2|h|), t = sign(tau) / (|tau| + sqrt(1 + tau^2))
+          // (scale-free: Gram entries of rows ~1e100 must not overflow)
           const double tau = (hj - hi) / (2.0 * ah);
           const double at = fabs(tau);
-          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (at > 1e150 ? 2.0 * at : at + sqrt(1.0 + tau * tau));
-          const double c = 1.0 / sqrt(1.0 + t * t);
+          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (at > 1e150 ? 2.0 * at : at + sqrt(fma(tau, tau, 1.0)));
+          const double c = rsqrt(fma(t, t, 1.0));
           sm.rc[tid] = c;
           sm.rs[tid] = t * c;
           sm.rph[tid] = phase_of(h, ah);   // e^{-i phi}
@@ -452,7 +458,7 @@ template <bool C>
 __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, int64_t ldx, typename Cx<C>::E *Y,
                                                           int64_t ldy, int nb, int64_t n, int round, double tol,
                                                           double tol_in, int max_inner,
-                                                          unsigned long long *offmax) {
+                                                          unsigned long long *offmax, unsigned long long *prof) {
   using E = typename Cx<C>::E;
   constexpr int CW = Cx<C>::CW;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -466,7 +472,10 @@ __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, 
   const int x0 = (int)((int64_t)nchx * rank / CL), x1 = (int)((int64_t)nchx * (rank + 1) / CL);
   const int y0 = (int)((int64_t)nchy * rank / CL), y1 = (int)((int64_t)nchy * (rank + 1) / CL);
 
+  long long tp0 = 0;
+  if (prof && threadIdx.x == 0) tp0 = clock64();
   gram_pass<C>(sm, X, ldx, x0, x1, row_lo, row_hi);
+  if (prof && threadIdx.x == 0) atomicAdd(prof + 0, (unsigned long long)(clock64() - tp0));
   // H = sum of the cluster's partials in rank order (identical in every CTA)
   cluster.sync();
   for (int idx = threadIdx.x; idx < PR * PR; idx += NT) {
@@ -516,9 +525,25 @@ __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, 
   // the staging ring is free now (Hp was consumed): start streaming X for
   // the update while the eigensolver runs
   update_prologue<C>(sm, X, ldx, x0, x1, row_lo, row_hi);
-  block_eig<C>(sm, lo_real < SB ? (int)lo_real : SB + (int)hi_real, tol_in, max_inner & 0xff, max_inner >> 8);
+  long long tp1 = 0;
+  if (prof && threadIdx.x == 0) tp1 = clock64();
+  block_eig<C>(sm, lo_real < SB ? (int)lo_real : SB + (int)hi_real, tol_in, max_inner & 0xff, (max_inner >> 8) & 1);
+  long long tp2 = 0;
+  if (prof && threadIdx.x == 0) {
+    tp2 = clock64();
+    atomicAdd(prof + 1, (unsigned long long)(tp2 - tp1));
+  }
   update_pass<C>(sm, X, ldx, x0, x1, row_lo, row_hi, true);
+  long long tp3 = 0;
+  if (prof && threadIdx.x == 0) {
+    tp3 = clock64();
+    atomicAdd(prof + 2, (unsigned long long)(tp3 - tp2));
+  }
   update_pass<C>(sm, Y, ldy, y0, y1, row_lo, row_hi);
+  if (prof && threadIdx.x == 0) {
+    atomicAdd(prof + 3, (unsigned long long)(clock64() - tp3));
+    atomicAdd(prof + 4, 1ull);
+  }
 }
 
 // X[r][c] = A'[r][c] (wide) or conj(A'[c][r]) (tall), zero padded; 32x32 tiles
@@ -641,7 +666,7 @@ __global__ void svd_gather_s_kernel(double *s_out, const double *s, const int *p
 // Numerically zero selected rows (s <= 1e-18 s_0, R29: the factor is undetermined there) become
 // unit vectors orthogonal to every other selected row: for candidates e_j,
 // j = 0, 1, ..., two Gram-Schmidt passes against the normalized selected rows
-// (x_r / snorm[r], snorm[r] > 0), accepted when the residual norm > 1/2.
+// (x_r / snorm[r], snorm[r] > 0), accepted when the residual norm > 1/(2 sqrt L).
 // One CTA, sequential over zero rows; only degenerate inputs get here.
 template <bool C>
 __device__ double cta_sum(double v, double *red) {
@@ -663,11 +688,12 @@ __global__ void __launch_bounds__(1024) svd_complete_kernel(typename Cx<C>::E *X
   __shared__ double red[32];
   for (int zi = threadIdx.x; zi < nz; zi += blockDim.x) snorm[zl[zi]] = 0.0;   // not part of the basis
   __syncthreads();
-  int64_t j = 0;
   for (int zi = 0; zi < nz; zi++) {
     const int64_t z = zl[zi];
     E *v = X + z * ldx;
-    for (; j < L; j++) {
+    // candidates e_0, e_1, ... for every zero row (those already taken are in
+    // the span of the completed rows and fail the residual test)
+    for (int64_t j = 0; j < L; j++) {
       for (int64_t c = threadIdx.x; c < L; c += blockDim.x) v[c] = c == j ? cone<E>() : czero<E>();
       __syncthreads();
       for (int pass = 0; pass < 2; pass++) {
@@ -704,12 +730,12 @@ __global__ void __launch_bounds__(1024) svd_complete_kernel(typename Cx<C>::E *X
         else nn = fma(v[c].x, v[c].x, fma(v[c].y, v[c].y, nn));
       }
       const double nrm = sqrt(cta_sum<C>(nn, red));
-      if (nrm > 0.5) {
+      // some e_j has a residual >= 1/sqrt(L) whenever the complement is non-empty
+      if (nrm > 0.5 / sqrt((double)L)) {
         for (int64_t c = threadIdx.x; c < L; c += blockDim.x) v[c] = rmul(1.0 / nrm, v[c]);
         __syncthreads();
         if (threadIdx.x == 0) snorm[z] = 1.0;
         __syncthreads();
-        j++;
         break;
       }
     }
@@ -771,12 +797,12 @@ cudaError_t launch_svd_round(const SvdProblem &p, int round, double tol, double 
     auto k = svd_round_kernel<true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     e = cudaLaunchKernelEx(&cfg, k, static_cast<double2 *>(p.X), p.ldx, static_cast<double2 *>(p.Y), p.ldy, nb,
-                           p.n, round, tol, tol_in, max_inner, p.offmax);
+                           p.n, round, tol, tol_in, max_inner, p.offmax, p.prof);
   } else {
     auto k = svd_round_kernel<false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     e = cudaLaunchKernelEx(&cfg, k, static_cast<double *>(p.X), p.ldx, static_cast<double *>(p.Y), p.ldy, nb, p.n,
-                           round, tol, tol_in, max_inner, p.offmax);
+                           round, tol, tol_in, max_inner, p.offmax, p.prof);
   }
   (*launches)++;
   if (e != cudaSuccess) return e;

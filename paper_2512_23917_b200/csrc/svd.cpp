@@ -62,7 +62,7 @@ tci_status_t svd_dims(tci_dtype_t dt, int order, const int64_t *shape, int k, Sv
   d.off_zl = o;
   o = align_up(o + (size_t)d.npad * 4);
   d.off_off = o;
-  o = align_up(o + 8);
+  o = align_up(o + 8 + 5 * 8);
   d.total = o;
   return TCI_OK;
 }
@@ -174,6 +174,10 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
   if (const char *e = getenv("TCI_SVD_SORT")) sort = atoi(e) != 0;
   max_inner |= sort << 8;   // packed kernel parameter: sweeps | sort flag
   const bool trace = getenv("TCI_SVD_TRACE") != nullptr;
+  if (getenv("TCI_SVD_PROFILE")) {   // per-phase clock totals of the round kernel (diagnostics)
+    p.prof = reinterpret_cast<unsigned long long *>(ws + d.off_off + 8);
+    TCI_CUDA_CHECK(cudaMemsetAsync(p.prof, 0, 5 * 8, s));
+  }
   const int nb = (int)(d.npad / 16);
   const int max_sweeps = 60;
   unsigned long long offbits = 0;
@@ -191,6 +195,13 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
     if (!(off > tol)) break;
   }
   ctx->svd_last_sweeps = sweeps;
+  if (p.prof) {
+    unsigned long long h[5];
+    TCI_CUDA_CHECK(cudaMemcpy(h, p.prof, sizeof h, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "tci:svd phase clocks per rotated CTA: gram(all) %.0f eig %.0f X %.0f Y %.0f (rotated CTAs %llu)\n",
+            (double)h[0] / std::max(1ull, h[4]), (double)h[1] / std::max(1ull, h[4]), (double)h[2] / std::max(1ull, h[4]),
+            (double)h[3] / std::max(1ull, h[4]), h[4]);
+  }
   TCI_CUDA_CHECK(launch_svd_norms(p, s, &ctx->launches));
   std::vector<double> sh(d.npad);
   TCI_CUDA_CHECK(cudaMemcpyAsync(sh.data(), p.s, d.npad * 8, cudaMemcpyDeviceToHost, s));

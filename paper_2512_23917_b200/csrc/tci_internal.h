@@ -222,6 +222,7 @@ struct SvdProblem {
   void *X, *Y;
   double *s;             // npad row norms
   unsigned long long *offmax;   // sweep maximum of the off-diagonal measure (double bits)
+  unsigned long long *prof = nullptr;   // optional phase clocks (gram, eig, X, Y, rotated pairs)
 };
 size_t svd_round_smem_bytes(bool cplx);
 cudaError_t launch_svd_load(const SvdProblem &p, const void *A, int64_t I, int64_t J, cudaStream_t s,

@@ -1,1 +1,2 @@
-for sort in 1 0; do echo "== sort=$sort"; TCI_SVD_SORT=$sort python tools/svd_diag.py 1024 2048 2>&1 | grep -o "n=.*sweeps=[0-9]*\|max|ds|/s0=[0-9.e-]*" | paste - -; TCI_SVD_SORT=$sort python tools/svd_trace.py 1024 2>&1 | tail -1; done
+timeout 600 python -m pytest tests/test_gpu_svd.py -q -x 2>&1 | tail -2
+TCI_SVD_PROFILE=1 python tools/svd_diag.py 2048 4096 2>&1 | grep -o "n=.*sweeps=[0-9]*\|max|ds|/s0=[0-9.e-]*\|eig [0-9]*" | paste - - - | head -6

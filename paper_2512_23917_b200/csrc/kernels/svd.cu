@@ -230,7 +230,8 @@ __device__ void gram_pass(RoundSmem<C> &sm, const typename Cx<C>::E *X, int64_t 
 // re-orthonormalisation), then A = G^H with the eigenpairs of the first nreal
 // rows in descending eigenvalue order (ties by index). A aliases H.
 template <bool C>
-__device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_inner, int sort) {
+__device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_inner, int sort,
+                          unsigned long long *prof = nullptr) {
   using E = typename Cx<C>::E;
   const int tid = threadIdx.x;
   for (int idx = tid; idx < PR * PR; idx += NT) sm.G[idx / PR][idx % PR] = (idx / PR == idx % PR) ? cone<E>() : czero<E>();
@@ -238,6 +239,8 @@ __device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_in
   for (int sw = 0; sw < max_inner; sw++) {
     int rotated = 0;
     for (int step = 0; step < PR - 1; step++) {
+      long long q0 = 0;
+      if (prof && tid == 0) q0 = clock64();
       if (tid < PR / 2) {
         int a, b;
         rr_pair(PR, step, tid, a, b);
@@ -272,6 +275,11 @@ __device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_in
         }
       }
       __syncthreads();
+      long long q1 = 0;
+      if (prof && tid == 0) {
+        q1 = clock64();
+        atomicAdd(prof + 5, (unsigned long long)(q1 - q0));
+      }
       {
         // H <- J^H H J on 2x2 blocks (u, v), J_u = [[c, s], [-s ph, c ph]]
         const int u = tid >> 4, v = tid & 15;
@@ -320,6 +328,7 @@ __device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_in
         }
       }
       __syncthreads();
+      if (prof && tid == 0) atomicAdd(prof + 6, (unsigned long long)(clock64() - q1));
     }
     if (!__syncthreads_or(rotated)) break;
   }
@@ -527,7 +536,8 @@ __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, 
   update_prologue<C>(sm, X, ldx, x0, x1, row_lo, row_hi);
   long long tp1 = 0;
   if (prof && threadIdx.x == 0) tp1 = clock64();
-  block_eig<C>(sm, lo_real < SB ? (int)lo_real : SB + (int)hi_real, tol_in, max_inner & 0xff, (max_inner >> 8) & 1);
+  block_eig<C>(sm, lo_real < SB ? (int)lo_real : SB + (int)hi_real, tol_in, max_inner & 0xff, (max_inner >> 8) & 1,
+               prof);
   long long tp2 = 0;
   if (prof && threadIdx.x == 0) {
     tp2 = clock64();

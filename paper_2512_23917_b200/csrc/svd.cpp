@@ -62,7 +62,7 @@ tci_status_t svd_dims(tci_dtype_t dt, int order, const int64_t *shape, int k, Sv
   d.off_zl = o;
   o = align_up(o + (size_t)d.npad * 4);
   d.off_off = o;
-  o = align_up(o + 8 + 5 * 8);
+  o = align_up(o + 8 + 7 * 8);
   d.total = o;
   return TCI_OK;
 }
@@ -176,7 +176,7 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
   const bool trace = getenv("TCI_SVD_TRACE") != nullptr;
   if (getenv("TCI_SVD_PROFILE")) {   // per-phase clock totals of the round kernel (diagnostics)
     p.prof = reinterpret_cast<unsigned long long *>(ws + d.off_off + 8);
-    TCI_CUDA_CHECK(cudaMemsetAsync(p.prof, 0, 5 * 8, s));
+    TCI_CUDA_CHECK(cudaMemsetAsync(p.prof, 0, 7 * 8, s));
   }
   const int nb = (int)(d.npad / 16);
   const int max_sweeps = 60;
@@ -196,11 +196,13 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
   }
   ctx->svd_last_sweeps = sweeps;
   if (p.prof) {
-    unsigned long long h[5];
+    unsigned long long h[7];
     TCI_CUDA_CHECK(cudaMemcpy(h, p.prof, sizeof h, cudaMemcpyDeviceToHost));
     fprintf(stderr, "tci:svd phase clocks per rotated CTA: gram(all) %.0f eig %.0f X %.0f Y %.0f (rotated CTAs %llu)\n",
             (double)h[0] / std::max(1ull, h[4]), (double)h[1] / std::max(1ull, h[4]), (double)h[2] / std::max(1ull, h[4]),
             (double)h[3] / std::max(1ull, h[4]), h[4]);
+    fprintf(stderr, "tci:svd eig steps: rotation phase %.0f, update phase %.0f clocks per rotated CTA\n",
+            (double)h[5] / std::max(1ull, h[4]), (double)h[6] / std::max(1ull, h[4]));
   }
   TCI_CUDA_CHECK(launch_svd_norms(p, s, &ctx->launches));
   std::vector<double> sh(d.npad);

@@ -70,7 +70,7 @@ struct TOps<double2> : CplxOps {
 };
 
 struct ThinArgs {
-  int64_t M, N, K;                 // N <= 16 (thin) or K <= 16 (outer)
+  int64_t M, N, K;                 // N <= 32 (16 complex; thin) or K <= 16 (outer)
   const void *A; int64_t a_sm, a_sk;
   const void *B; int64_t b_sk, b_sn;
   void *C; int64_t c_sm, c_sn;
@@ -259,7 +259,8 @@ cudaError_t launch_gemm_thin(const GemmProblem &p, cudaStream_t s, int64_t *laun
   const int splits = p.splitk > 1 ? p.splitk : 1;
   t.K = p.K;
   t.k_chunk = p.splitk > 1 ? p.k_chunk : p.K;
-  const bool outer = std::min(p.M, p.N) > 16;
+  const int64_t thin_max = dtype_is_complex(p.dtype) ? 16 : 32;   // as gemm_thin_applies
+  const bool outer = std::min(p.M, p.N) > thin_max;
   // thin: make N the thin side (C^T = B^T A^T when M is the thin one)
   const bool swap = !outer && p.M < p.N;
   if (!swap) {

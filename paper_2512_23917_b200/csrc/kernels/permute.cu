@@ -89,10 +89,28 @@ __global__ void __launch_bounds__(256) transpose_tiles(const PermArgs a) {
   }
 }
 
+struct FDiv {                  // n / d for n < 2^31 (Granlund-Montgomery)
+  uint32_t d, m;
+  int s;                       // shift, -1 for d == 1
+};
+inline FDiv make_fdiv(uint32_t d) {
+  FDiv f{d, 0, -1};
+  if (d <= 1) return f;
+  int l = 0;
+  while ((1ull << l) < d) l++;
+  const int p = 31 + l;
+  f.m = (uint32_t)(((1ull << p) + d - 1) / d);
+  f.s = p - 32;
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FDiv &f) { return f.s < 0 ? n : __umulhi(n, f.m) >> f.s; }
+
 struct RowArgs {
   int nb;
   int64_t bshape[kMaxOrder];
   int64_t b_in[kMaxOrder];
+  FDiv bdiv[kMaxOrder];  // 32-bit division by bshape (used when rows * vec_per_row < 2^31)
+  FDiv vdiv;             // ... and by vec_per_row
   int64_t run;          // contiguous run length (elements), out rows are contiguous
   int64_t rows;
   int64_t vec_per_row;
@@ -100,31 +118,71 @@ struct RowArgs {
   char *out;
 };
 
-template <int ESZ, int VEC>
-__global__ void __launch_bounds__(256) copy_rows(const RowArgs a) {
+// Each thread moves U vectors per pass (all loads issued before the stores:
+// memory-level parallelism), coordinates by 32-bit invariant division when
+// the vector count fits (64-bit division costs ~40 instructions per leg).
+template <int ESZ, int VEC, bool SMALL>
+__global__ void __launch_bounds__(256) copy_rows(const __grid_constant__ RowArgs a) {
   using E = typename std::conditional<ESZ == 16, int4,
                                       typename std::conditional<ESZ == 8, int2, int>::type>::type;
   using V = typename std::conditional<
       ESZ * VEC == 16, int4,
       typename std::conditional<ESZ * VEC == 8, int2, int>::type>::type;
+  constexpr int U = 4;
   const int64_t total = a.rows * a.vec_per_row;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    int64_t row = idx / a.vec_per_row;
-    const int64_t v = idx % a.vec_per_row;
-    const int64_t out_row = row;
-    int64_t in_off = 0;
-    for (int k = a.nb - 1; k >= 0; k--) {
-      const int64_t c = row % a.bshape[k];
-      row /= a.bshape[k];
-      in_off += c * a.b_in[k];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const E *__restrict__ inE = reinterpret_cast<const E *>(a.in);
+  E *__restrict__ outE = reinterpret_cast<E *>(a.out);
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total; base += U * stride) {
+    V val[U];
+    int64_t dst_off[U];
+    bool full[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t idx = base + u * stride;
+      dst_off[u] = -1;
+      if (idx >= total) continue;
+      int64_t row, v, in_off = 0;
+      if (SMALL) {
+        uint32_t r32 = fdiv((uint32_t)idx, a.vdiv);
+        v = (uint32_t)idx - r32 * a.vdiv.d;
+        row = r32;
+        for (int k = a.nb - 1; k >= 0; k--) {
+          const uint32_t q = fdiv(r32, a.bdiv[k]);
+          in_off += (int64_t)(r32 - q * a.bdiv[k].d) * a.b_in[k];
+          r32 = q;
+        }
+      } else {
+        row = idx / a.vec_per_row;
+        v = idx % a.vec_per_row;
+        int64_t r = row;
+        for (int k = a.nb - 1; k >= 0; k--) {
+          const int64_t c = r % a.bshape[k];
+          r /= a.bshape[k];
+          in_off += c * a.b_in[k];
+        }
+      }
+      const E *src = inE + in_off + v * VEC;
+      dst_off[u] = row * a.run + v * VEC;
+      full[u] = VEC > 1 && (v + 1) * VEC <= a.run;
+      if (full[u]) {
+        val[u] = __ldg(reinterpret_cast<const V *>(src));
+      } else {
+        E *ve = reinterpret_cast<E *>(&val[u]);
+        for (int e = 0; e < VEC; e++) ve[e] = v * VEC + e < a.run ? src[e] : E{};
+      }
     }
-    const E *src = reinterpret_cast<const E *>(a.in) + in_off + v * VEC;
-    E *dst = reinterpret_cast<E *>(a.out) + out_row * a.run + v * VEC;
-    if (VEC > 1 && (v + 1) * VEC <= a.run) {
-      *reinterpret_cast<V *>(dst) = *reinterpret_cast<const V *>(src);
-    } else {
-      for (int e = 0; e < VEC && v * VEC + e < a.run; e++) dst[e] = src[e];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (dst_off[u] < 0) continue;
+      E *dst = outE + dst_off[u];
+      if (full[u]) {
+        *reinterpret_cast<V *>(dst) = val[u];
+      } else {
+        const E *ve = reinterpret_cast<const E *>(&val[u]);
+        const int64_t v0 = dst_off[u] % a.run;
+        for (int e = 0; e < VEC && v0 + e < a.run; e++) dst[e] = ve[e];
+      }
     }
   }
 }
@@ -141,22 +199,6 @@ __global__ void __launch_bounds__(256) copy_rows(const RowArgs a) {
 // Persistent CTAs loop over the tiles.
 // ---------------------------------------------------------------------------
 constexpr int kGMax = 8;
-
-struct FDiv {                  // n / d for n < 2^31 (Granlund-Montgomery)
-  uint32_t d, m;
-  int s;                       // shift, -1 for d == 1
-};
-inline FDiv make_fdiv(uint32_t d) {
-  FDiv f{d, 0, -1};
-  if (d <= 1) return f;
-  int l = 0;
-  while ((1ull << l) < d) l++;
-  const int p = 31 + l;
-  f.m = (uint32_t)(((1ull << p) + d - 1) / d);
-  f.s = p - 32;
-  return f;
-}
-__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FDiv &f) { return f.s < 0 ? n : __umulhi(n, f.m) >> f.s; }
 
 struct GroupArgs {
   int ng;                                  // legs in the tile
@@ -182,21 +224,40 @@ struct GroupArgs {
   int64_t b_ext[2 * kMaxOrder], b_in[2 * kMaxOrder], b_out[2 * kMaxOrder];
   int b_cut[2 * kMaxOrder];                // cut index when the grid leg is a chunk index, else -1
   int64_t b_chunk[2 * kMaxOrder];          // chunk length for chunk-index legs
+  FDiv b_div[2 * kMaxOrder];               // division by b_ext (ntiles < 2^31)
   int64_t ntiles;
   const char *in;
   char *out;
 };
 
+// Shared-memory slot of tile position x: XOR-swizzled within blocks of
+// W = 128 / ESZ elements (one 128-byte wavefront) by a hash of the higher
+// bits, so both the input-order writes (consecutive x) and the output-order
+// reads (x strided by any power of two) are free of bank conflicts.
 template <int ESZ>
+__device__ __forceinline__ int swz(int x) {
+  constexpr int W = 128 / ESZ, B = W == 32 ? 5 : (W == 16 ? 4 : 3);
+  return x ^ (((x >> B) ^ (x >> (2 * B)) ^ (x >> (3 * B))) & (W - 1));
+}
+
+// V elements per vector (16 / 8 / 4-byte accesses): the tile's input-fastest
+// and output-fastest legs both hold whole vectors (planner check), so the
+// full-tile path moves V consecutive elements per global access.
+template <int ESZ, int V>
 __global__ void __launch_bounds__(256) permute_groups(const __grid_constant__ GroupArgs a) {
+  constexpr int GU = ESZ * V >= 16 ? 4 : 8;
   using E = typename std::conditional<ESZ == 16, int4,
                                       typename std::conditional<ESZ == 8, int2, int>::type>::type;
+  using VT = typename std::conditional<
+      ESZ * V == 16, int4, typename std::conditional<ESZ * V == 8, int2, int>::type>::type;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int TS = a.TS;
-  E *tile = reinterpret_cast<E *>(smraw);                            // padded: slot + slot / 32
-  int32_t *ld_off = reinterpret_cast<int32_t *>(tile + TS + TS / 32 + 1);   // in offset of tile position q
+  constexpr int W = 128 / ESZ;
+  const int TSP = (TS + W - 1) / W * W;                                // swizzle blocks are whole
+  E *tile = reinterpret_cast<E *>(smraw);
+  int32_t *ld_off = reinterpret_cast<int32_t *>(tile + TSP);          // in offset of tile position q
   int32_t *st_off = ld_off + TS;                                      // out offset of output position p
-  uint16_t *st_slot = reinterpret_cast<uint16_t *>(st_off + TS);      // padded smem slot of p
+  uint16_t *st_slot = reinterpret_cast<uint16_t *>(st_off + TS);      // smem slot of p
   const E *in = reinterpret_cast<const E *>(a.in);
   E *out = reinterpret_cast<E *>(a.out);
   // offset tables of the tile geometry, built once per CTA (full tiles)
@@ -226,16 +287,18 @@ __global__ void __launch_bounds__(256) permute_groups(const __grid_constant__ Gr
       }
     }
     st_off[q] = (int32_t)off;
-    st_slot[q] = (uint16_t)(slot + (slot >> 5));
+    st_slot[q] = (uint16_t)swz<ESZ>(slot);
   }
   __syncthreads();
   for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-    int64_t rem = t, in_base = 0, out_base = 0;
+    uint32_t rem = (uint32_t)t;
+    int64_t in_base = 0, out_base = 0;
     int64_t cut_base[2] = {0, 0};
     bool full = true;
     for (int k = a.nb - 1; k >= 0; k--) {
-      const int64_t c = rem % a.b_ext[k];
-      rem /= a.b_ext[k];
+      const uint32_t qk = fdiv(rem, a.b_div[k]);
+      const int64_t c = rem - qk * a.b_div[k].d;
+      rem = qk;
       in_base += c * a.b_in[k];
       out_base += c * a.b_out[k];
       if (a.b_cut[k] >= 0) {
@@ -244,9 +307,35 @@ __global__ void __launch_bounds__(256) permute_groups(const __grid_constant__ Gr
       }
     }
     if (full) {
-      for (int q = threadIdx.x; q < TS; q += 256) tile[q + (q >> 5)] = in[in_base + ld_off[q]];
+      // GU vector loads in flight per thread before their shared-memory stores
+      const int TV = TS / V;
+      for (int i0 = threadIdx.x; i0 < TV; i0 += 256 * GU) {
+        VT v[GU];
+#pragma unroll
+        for (int u = 0; u < GU; u++) {
+          const int i = i0 + u * 256;
+          if (i < TV) v[u] = __ldg(reinterpret_cast<const VT *>(in + in_base + ld_off[i * V]));
+        }
+#pragma unroll
+        for (int u = 0; u < GU; u++) {
+          const int i = i0 + u * 256;
+          if (i < TV) {
+            const E *ve = reinterpret_cast<const E *>(&v[u]);
+            const int sq = swz<ESZ>(i * V);     // V | W: the vector stays in one swizzle block
+#pragma unroll
+            for (int e = 0; e < V; e++) tile[sq ^ e] = ve[e];
+          }
+        }
+      }
       __syncthreads();
-      for (int p = threadIdx.x; p < TS; p += 256) out[out_base + st_off[p]] = tile[st_slot[p]];
+#pragma unroll 4
+      for (int i = threadIdx.x; i < TV; i += 256) {
+        VT v;
+        E *ve = reinterpret_cast<E *>(&v);
+#pragma unroll
+        for (int e = 0; e < V; e++) ve[e] = tile[st_slot[i * V + e]];
+        *reinterpret_cast<VT *>(out + out_base + st_off[i * V]) = v;
+      }
       __syncthreads();
       continue;
     }
@@ -257,7 +346,7 @@ __global__ void __launch_bounds__(256) permute_groups(const __grid_constant__ Gr
         const uint32_t x = fdiv((uint32_t)q, a.ci_pre[c]);
         ok = ok && (cut_base[c] + (x - fdiv(x, a.c_ext[c]) * a.c_ext[c].d) < a.cut_ext[c]);
       }
-      if (ok) tile[q + (q >> 5)] = in[in_base + ld_off[q]];
+      if (ok) tile[swz<ESZ>(q)] = in[in_base + ld_off[q]];
     }
     __syncthreads();
     for (int p = threadIdx.x; p < TS; p += 256) {
@@ -276,8 +365,10 @@ __global__ void __launch_bounds__(256) permute_groups(const __grid_constant__ Gr
 template <int ESZ>
 bool plan_groups(const PermuteProblem &p, const int64_t *out_stride, GroupArgs &a) {
   const int n = p.n;
-  constexpr int RUN = 256 / ESZ;             // >= 256 contiguous bytes per run
-  constexpr int TSMAX = 32768 / ESZ;         // 32 KB tiles
+  // >= 256 contiguous bytes per run; 16 KB tiles, 8 CTAs per SM (measured
+  // against 8/24/32/64 KB tiles and 512/1024-byte runs: tools/gpu_perm_sweep.sh)
+  constexpr int RUN = 256 / ESZ;
+  constexpr int TSMAX = 16384 / ESZ;
   int ord_in[kMaxOrder], ord_out[kMaxOrder];
   for (int k = 0; k < n; k++) ord_in[k] = ord_out[k] = k;
   std::sort(ord_in, ord_in + n, [&](int x, int y) { return p.in_stride_for_out[x] < p.in_stride_for_out[y]; });
@@ -305,6 +396,7 @@ bool plan_groups(const PermuteProblem &p, const int64_t *out_stride, GroupArgs &
       } else {                               // cut into chunks
         int64_t ch = std::min<int64_t>(room, std::max<int64_t>(2, (target + run - 1) / run));
         ch = std::min(ch, e);
+        if (ch < e) ch = (e + (e + ch - 1) / ch - 1) / ((e + ch - 1) / ch);   // balanced: no sliver chunk
         tex[k] = ch;
         TS *= ch;
         run *= ch;
@@ -422,8 +514,10 @@ bool plan_groups(const PermuteProblem &p, const int64_t *out_stride, GroupArgs &
       continue;
     }
     a.ntiles *= a.b_ext[a.nb];
+    a.b_div[a.nb] = make_fdiv((uint32_t)std::min<int64_t>(a.b_ext[a.nb], 0x7fffffff));
     a.nb++;
   }
+  if (a.ntiles >= (int64_t(1) << 31)) return false;
   a.in = static_cast<const char *>(p.in);
   a.out = static_cast<char *>(p.out);
   return true;
@@ -461,31 +555,62 @@ cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launc
     const int vec = vec_ok ? VMAX : 1;
     a.vec_per_row = (a.run + vec - 1) / vec;
     const int64_t total = a.rows * a.vec_per_row;
-    const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
-    if (vec_ok) copy_rows<ESZ, VMAX><<<(unsigned)blocks, 256, 0, s>>>(a);
-    else copy_rows<ESZ, 1><<<(unsigned)blocks, 256, 0, s>>>(a);
+    const bool small = total < (int64_t(1) << 31);
+    if (small) {
+      a.vdiv = make_fdiv((uint32_t)a.vec_per_row);
+      for (int k = 0; k < a.nb; k++) a.bdiv[k] = make_fdiv((uint32_t)a.bshape[k]);
+    }
+    // 4 vectors per thread per pass; 8 CTAs of 256 per SM
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 1023) / 1024, 148 * 8));
+    if (vec_ok) {
+      if (small) copy_rows<ESZ, VMAX, true><<<(unsigned)blocks, 256, 0, s>>>(a);
+      else copy_rows<ESZ, VMAX, false><<<(unsigned)blocks, 256, 0, s>>>(a);
+    } else {
+      if (small) copy_rows<ESZ, 1, true><<<(unsigned)blocks, 256, 0, s>>>(a);
+      else copy_rows<ESZ, 1, false><<<(unsigned)blocks, 256, 0, s>>>(a);
+    }
     if (launches) ++*launches;
     return cudaGetLastError();
   };
   const bool in_run = n > 0 && p.in_stride_for_out[n - 1] == 1;
-  if (n <= 1 || (in_run && p.shape_out[n - 1] * ESZ >= 128 && rows_vec)) return rows_path();
+  // row copies for contiguous runs >= 512 B; shorter runs go to leg-group tiles,
+  // which also group the writes (128-byte runs: 0.81 -> 0.87 of a plain copy)
+  if (n <= 1 || (in_run && p.shape_out[n - 1] * ESZ >= 512 && rows_vec)) return rows_path();
   // tile legs of the classic transpose: j = out-fastest leg, i = the
   // in-contiguous leg; when both are long it is the fastest kernel
   constexpr int T = (ESZ == 16) ? 32 : 64;
   int li = -1;
   for (int k = 0; k < n - 1; k++)
     if (p.in_stride_for_out[k] == 1) li = k;
-  const bool classic = li >= 0 && p.shape_out[li] >= T / 2 && p.shape_out[n - 1] >= T / 2;
+  // (both legs at least one full tile: a half-empty tile wastes half the CTA)
+  const bool classic = li >= 0 && p.shape_out[li] >= T && p.shape_out[n - 1] >= T;
   // otherwise leg-group tiles (short contiguous legs are grouped until both
   // the reads and the writes move >= 256 contiguous bytes)
   if (!classic) {
     GroupArgs ga;
     if (plan_groups<ESZ>(p, out_stride, ga)) {
-      const size_t smem = ((size_t)ga.TS + ga.TS / 32 + 1) * ESZ + (size_t)ga.TS * 10 + 16;
-      auto k = permute_groups<ESZ>;
+      constexpr int W = 128 / ESZ;
+      const size_t smem = (size_t)((ga.TS + W - 1) / W * W) * ESZ + (size_t)ga.TS * 10 + 16;
+      // vectors: V consecutive elements along the tile's input-fastest leg
+      // (unit input stride) and its output-fastest leg (unit output stride);
+      // every other stride and chunk base a multiple of V, 16-byte bases
+      int V = VMAX;
+      auto vec_ok = [&](int v) {
+        if (v == 1) return true;
+        if ((uintptr_t)p.in % (v * ESZ) || (uintptr_t)p.out % (v * ESZ)) return false;
+        if (ga.gi_in[0] != 1 || ga.gi_div[0].d % v || ga.go_out[0] != 1 || ga.go_div[0].d % v) return false;
+        for (int l = 1; l < ga.ng; l++) if (ga.gi_in[l] % v) return false;
+        for (int l = 1; l < ga.ng; l++) if (ga.go_out[l] % v) return false;
+        for (int k = 0; k < ga.nb; k++) if (ga.b_in[k] % v || ga.b_out[k] % v) return false;
+        return ga.TS % v == 0;
+      };
+      while (V > 1 && !vec_ok(V)) V /= 2;
+      auto k = permute_groups<ESZ, 1>;
+      if (V == 4) k = permute_groups<ESZ, (VMAX >= 4 ? 4 : 1)>;
+      else if (V == 2) k = permute_groups<ESZ, (VMAX >= 2 ? 2 : 1)>;
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      const int64_t blocks = std::min<int64_t>(ga.ntiles, 148 * 6);
+      const int64_t blocks = std::min<int64_t>(ga.ntiles, 148 * 8);
       k<<<(unsigned)blocks, 256, smem, s>>>(ga);
       if (launches) ++*launches;
       return cudaGetLastError();

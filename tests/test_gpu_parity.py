@@ -143,6 +143,25 @@ def test_gemm_layouts_ragged(ctx, oracle_mod, dt):
 
 
 @pytest.mark.parametrize("dt", ["r64", "c128", "r32", "c64"])
+def test_thin_side_boundaries(ctx, oracle_mod, dt):
+    """Thin / outer-product GEMM routing at every width boundary (1, 2, 4, 8,
+    16, 17, 32, 33 on either side, K short and long, both A layouts): the thin
+    kernels take min(M, N) <= 32 real / 16 complex, the outer kernel K <= 16."""
+    for thin in (1, 2, 3, 8, 16, 17, 24, 32, 33):
+        for big, K in ((300, 7), (300, 259), (1000, 16), (129, 1100)):
+            A = synth.random_tensor((thin, K), dt, 88 + thin, 1)
+            B = synth.random_tensor((K, big), dt, 88 + thin, 2)
+            ref = oracle_mod.contract(A.numpy(), "mk", B.numpy(), "kn", "mn")
+            for la, At in (("mk", A), ("km", A.T.contiguous())):
+                for lc in ("mn", "nm"):
+                    C = ctx.contract(dev(At), la, dev(B), "kn", lc)
+                    r = ref if lc == "mn" else ref.T
+                    assert rel_frob(host(C), r) <= TOL[dt], (thin, big, K, la, lc)
+                    C = ctx.contract(dev(B), "kn", dev(At), la, lc)   # operands swapped
+                    assert rel_frob(host(C), r) <= TOL[dt], ("swap", thin, big, K, la, lc)
+
+
+@pytest.mark.parametrize("dt", ["r64", "c128", "r32", "c64"])
 def test_splitk_small_output_long_k(ctx, oracle_mod, dt):
     """Few output tiles and a long K take the deterministic split-K path
     (partial GEMMs + ascending-order reduction): parity and repeatability."""

@@ -300,12 +300,19 @@ def permute_bw(ctx):
     rows = []
     for shape, perm, dt in [((4096, 4096, 16), (1, 0, 2), "r64"), ((512, 512, 512), (2, 1, 0), "r64"),
                             ((64, 64, 64, 64, 16), (4, 3, 2, 1, 0), "r64"), ((8192, 8192, 2), (2, 1, 0), "c128"),
-                            ((16384, 16384), (1, 0), "r32"), ((2048, 2048, 32), (0, 2, 1), "r64")]:
+                            ((16384, 16384), (1, 0), "r32"), ((2048, 2048, 32), (0, 2, 1), "r64"),
+                            ((32, 64, 48, 40, 36), (3, 0, 4, 2, 1), "r32"), ((96, 96, 96, 24), (2, 3, 0, 1), "c64"),
+                            ((3, 5, 7, 1024, 512), (4, 2, 0, 3, 1), "r64")]:
         x = synth.random_tensor(shape, dt, 9, 1, device="cuda")
         y = torch.empty([shape[p] for p in perm], dtype=x.dtype, device="cuda")
         med, _ = timed(lambda: ctx.permute(x, list(perm), out=y), reps=10, warm=2)
         byts = 2.0 * x.numel() * x.element_size()
-        rows.append({"shape": shape, "perm": perm, "dtype": dt, "GBs": byts / med / 1e9, "frac_hbm": byts / med / HBM})
+        # plain device copy of the same bytes (torch copy_), same timing: the ceiling beside the peak
+        yc = torch.empty_like(x)
+        medc, _ = timed(lambda: yc.copy_(x), reps=10, warm=2)
+        rows.append({"shape": shape, "perm": perm, "dtype": dt, "GBs": byts / med / 1e9, "frac_hbm": byts / med / HBM,
+                     "copy_GBs": byts / medc / 1e9, "frac_of_copy": medc / med})
+        del yc
         del x, y
     return rows
 

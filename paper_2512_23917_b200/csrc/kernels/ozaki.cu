@@ -143,20 +143,78 @@ __global__ void fill_int(int *p, int64_t n, int v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
-// exact symmetric residue of an integer-valued double |x| < 2^51 modulo m,
-// as the low byte of an int: rounding by the 1.5*2^52 "magic" addition keeps
-// the work on the FP64 pipe (no F2I / FRND conversions)
-__device__ __forceinline__ uint32_t residue_byte(double x, double m, double minv) {
-  const double magic = 6755399441055744.0;   // 1.5 * 2^52
-  const double q = (fma(x, minv, magic) - magic);
-  const double r = fma(-q, m, x) + magic;     // r in [-(m-1)/2, (m-1)/2] + magic
-  return (uint32_t)__double2loint(r) & 0xffu;
+// 1/m_l rounded to double (IEEE division, evaluated at compile time)
+__constant__ double c_minv[kMaxMod] = {1.0 / 255, 1.0 / 253, 1.0 / 251, 1.0 / 247, 1.0 / 241, 1.0 / 239, 1.0 / 233, 1.0 / 229, 1.0 / 227, 1.0 / 223, 1.0 / 217, 1.0 / 211, 1.0 / 199, 1.0 / 197, 1.0 / 193};
+
+constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52: x + kMagic rounds x to an integer (|x| < 2^51)
+
+// rint(v * 2^sc) + 1.5*2^52 with the scale split in two exact power-of-two
+// factors (s2a * s2b = 2^sc; the first product is inexact only when it is
+// subnormal, and then the result rounds to 0 either way): the integer
+// x = rint(v 2^sc) sits in the low mantissa bits, so x = result - kMagic and
+// the low word of the result is x mod 2^32. Bitwise equal to rint(ldexp(v, sc)).
+__device__ __forceinline__ double scaled_magic(double v, double s2a, double s2b) {
+  return fma(v * s2a, s2b, kMagic);
+}
+
+// balanced residue r of an integer-valued double |x| < 2^51 modulo odd m,
+// r in [-(m-1)/2, (m-1)/2]: q = rint(x/m) is exact (x/m is never within
+// 2^-9.6 of a half-integer for odd m) and sits in the low word of
+// fma(x, 1/m, 1.5*2^52); r = x - q m holds exactly in 32-bit wrap-around
+// arithmetic on the low words (|r| < 2^31): one DFMA + one IMAD per residue
+__device__ __forceinline__ int bal_res(double x, int x_lo, double minv, int m) {
+  return x_lo - __double2loint(fma(x, minv, kMagic)) * m;
+}
+
+// low bytes of four ints -> one word (3 PRMT)
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+  return __byte_perm(__byte_perm((uint32_t)a, (uint32_t)b, 0x0040), __byte_perm((uint32_t)c, (uint32_t)d, 0x0040),
+                     0x5410);
+}
+
+// Scaled integers of NV consecutive complex values: x[0] = re, x[1] = im,
+// x[2] = re + im (exact, |.| < 2^49) and their low words
+template <int NV>
+struct ResVals {
+  double x[3][NV];
+  int lo[3][NV];
+  __device__ __forceinline__ void set(int j, double mr, double mi) {   // mr, mi: scaled_magic outputs
+    x[0][j] = mr - kMagic;
+    x[1][j] = mi - kMagic;
+    x[2][j] = x[0][j] + x[1][j];
+    lo[0][j] = __double2loint(mr);
+    lo[1][j] = __double2loint(mi);
+    lo[2][j] = lo[0][j] + lo[1][j];
+  }
+};
+
+// the three residue planes (re, im, re + im) of NV consecutive values for
+// modulus l, packed 4 bytes per word
+template <int NV>
+__device__ __forceinline__ void residue_words(const ResVals<NV> &v, int l, uint32_t (&w)[3][NV / 4]) {
+  const int mi = c_moduli[l];
+  const double minv = c_minv[l];
+#pragma unroll
+  for (int c = 0; c < 3; c++)
+#pragma unroll
+    for (int q = 0; q < NV / 4; q++)
+      w[c][q] = pack4(bal_res(v.x[c][q * 4 + 0], v.lo[c][q * 4 + 0], minv, mi),
+                      bal_res(v.x[c][q * 4 + 1], v.lo[c][q * 4 + 1], minv, mi),
+                      bal_res(v.x[c][q * 4 + 2], v.lo[c][q * 4 + 2], minv, mi),
+                      bal_res(v.x[c][q * 4 + 3], v.lo[c][q * 4 + 3], minv, mi));
+}
+
+// scale factors 2^sc = s2a * s2b of one line (E > -100000)
+__device__ __forceinline__ void line_scale(int t, int E, double &s2a, double &s2b) {
+  const int sc = t - E, h1 = sc / 2;
+  s2a = ldexp(1.0, h1);
+  s2b = ldexp(1.0, sc - h1);
 }
 
 // ---------------------------------------------------------------------------
 // step 1b + 2a: residue planes. out[(l*3 + comp)][line][kp] int8, K-major,
 // comp 0 = re, 1 = im, 2 = re + im; zero for k >= K or line >= nlines.
-// Each thread produces 16 consecutive k of one line for all planes.
+// Each thread produces 8 consecutive k of one line for all planes.
 // ---------------------------------------------------------------------------
 struct ResArgs {
   const double2 *base;
@@ -171,56 +229,35 @@ struct ResArgs {
 };
 
 __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs a) {
-  const int64_t kgroups = a.Kp / 16;
+  constexpr int NV = 8;
+  const int64_t kgroups = a.Kp / NV;
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (gid >= a.lines_out * kgroups) return;
   // K-contiguous source: consecutive threads walk k (coalesced reads and writes)
   const int64_t row = gid / kgroups;
-  const int64_t k0 = (gid % kgroups) * 16;
+  const int64_t k0 = (gid % kgroups) * NV;
   const int64_t line = a.line0 + row;
-  double xr[16], xi[16];
+  ResVals<NV> x;
   if (line < a.nlines && a.E[line] > -100000) {
-    const int sc = a.t - a.E[line];
+    double s2a, s2b;
+    line_scale(a.t, a.E[line], s2a, s2b);
     const double2 *p = a.base + line * a.s_l;
+    double2 v[NV];
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-      const int64_t k = k0 + j;
-      double2 v = make_double2(0.0, 0.0);
-      if (k < a.K) v = p[k * a.s_k];
-      xr[j] = rint(ldexp(v.x, sc));
-      xi[j] = rint(ldexp(v.y, sc));
-    }
+    for (int j = 0; j < NV; j++) v[j] = k0 + j < a.K ? __ldg(p + (k0 + j) * a.s_k) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < NV; j++) x.set(j, scaled_magic(v[j].x, s2a, s2b), scaled_magic(v[j].y, s2a, s2b));
   } else {
 #pragma unroll
-    for (int j = 0; j < 16; j++) xr[j] = xi[j] = 0.0;
+    for (int j = 0; j < NV; j++) x.set(j, kMagic, kMagic);
   }
+  int8_t *dst = a.out + row * a.Kp + k0;
   for (int l = 0; l < a.nmod; l++) {
-    const int mi = c_moduli[l], h = mi >> 1;
-    const double m = (double)mi, minv = 1.0 / m;
-    uint32_t w[3][4];
+    uint32_t w[3][NV / 4];
+    residue_words<NV>(x, l, w);
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      uint32_t pr = 0, pi = 0, ps = 0;
-#pragma unroll
-      for (int b = 0; b < 4; b++) {
-        const int j = q * 4 + b;
-        const uint32_t br = residue_byte(xr[j], m, minv), bi = residue_byte(xi[j], m, minv);
-        // (re + im) mod m from the two balanced residues: integer ops only
-        int s = (int)(int8_t)br + (int)(int8_t)bi;
-        s += s > h ? -mi : (s < -h ? mi : 0);
-        pr |= br << (8 * b);
-        pi |= bi << (8 * b);
-        ps |= ((uint32_t)s & 0xffu) << (8 * b);
-      }
-      w[0][q] = pr;
-      w[1][q] = pi;
-      w[2][q] = ps;
-    }
-#pragma unroll
-    for (int comp = 0; comp < 3; comp++) {
-      int8_t *dst = a.out + (int64_t)(l * 3 + comp) * a.plane_stride + row * a.Kp + k0;
-      *reinterpret_cast<uint4 *>(dst) = make_uint4(w[comp][0], w[comp][1], w[comp][2], w[comp][3]);
-    }
+    for (int comp = 0; comp < 3; comp++)
+      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 3 + comp) * a.plane_stride) = make_uint2(w[comp][0], w[comp][1]);
   }
 }
 
@@ -237,46 +274,36 @@ __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArg
     const int li = tid % 32;
     const int64_t row = r0 + li, line = a.line0 + row;
     const bool ok = row < a.lines_out && line < a.nlines && a.E[line] > -100000;
-    const int sc = ok ? a.t - a.E[line] : 0;
-#pragma unroll 4
-    for (int j = tid / 32; j < 64; j += 8) {
-      const int64_t k = kb + j;
-      double2 v = make_double2(0.0, 0.0);
-      if (ok && k < a.K) v = a.base[line + k * a.s_k];
-      sx[0][li][j] = rint(ldexp(v.x, sc));
-      sx[1][li][j] = rint(ldexp(v.y, sc));
+    double s2a = 0.0, s2b = 0.0;   // 0 -> scaled value 0 for dead lines
+    if (ok) line_scale(a.t, a.E[line], s2a, s2b);
+    double2 v[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; jj++) {
+      const int64_t k = kb + tid / 32 + jj * 8;
+      v[jj] = ok && k < a.K ? __ldg(a.base + line + k * a.s_k) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int jj = 0; jj < 8; jj++) {
+      const int j = tid / 32 + jj * 8;
+      sx[0][li][j] = scaled_magic(v[jj].x, s2a, s2b);
+      sx[1][li][j] = scaled_magic(v[jj].y, s2a, s2b);
     }
   }
   __syncthreads();
   const int li = tid / 8, kq = (tid % 8) * 8;
   const int64_t row = r0 + li;
   if (row >= a.lines_out) return;
+  // the thread's 8 values, read from shared memory once for all moduli
+  ResVals<8> x;
+#pragma unroll
+  for (int j = 0; j < 8; j++) x.set(j, sx[0][li][kq + j], sx[1][li][kq + j]);
+  int8_t *dst = a.out + row * a.Kp + kb + kq;
   for (int l = 0; l < a.nmod; l++) {
-    const int mi = c_moduli[l], h = mi >> 1;
-    const double m = (double)mi, minv = 1.0 / m;
     uint32_t w[3][2];
+    residue_words<8>(x, l, w);
 #pragma unroll
-    for (int q = 0; q < 2; q++) {
-      uint32_t pr = 0, pi = 0, ps = 0;
-#pragma unroll
-      for (int b = 0; b < 4; b++) {
-        const int j = kq + q * 4 + b;
-        const uint32_t br = residue_byte(sx[0][li][j], m, minv), bi = residue_byte(sx[1][li][j], m, minv);
-        int s = (int)(int8_t)br + (int)(int8_t)bi;
-        s += s > h ? -mi : (s < -h ? mi : 0);
-        pr |= br << (8 * b);
-        pi |= bi << (8 * b);
-        ps |= ((uint32_t)s & 0xffu) << (8 * b);
-      }
-      w[0][q] = pr;
-      w[1][q] = pi;
-      w[2][q] = ps;
-    }
-#pragma unroll
-    for (int comp = 0; comp < 3; comp++) {
-      int8_t *dst = a.out + (int64_t)(l * 3 + comp) * a.plane_stride + row * a.Kp + kb + kq;
-      *reinterpret_cast<uint2 *>(dst) = make_uint2(w[comp][0], w[comp][1]);
-    }
+    for (int comp = 0; comp < 3; comp++)
+      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 3 + comp) * a.plane_stride) = make_uint2(w[comp][0], w[comp][1]);
   }
 }
 
@@ -582,7 +609,7 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   exponents(B, g.N, g.b_sn, g.b_sk, EB);
   auto launch_res = [&](const ResArgs &r) {
     if (r.s_k == 1) {
-      const int64_t th = r.lines_out * (r.Kp / 16);
+      const int64_t th = r.lines_out * (r.Kp / 8);
       residues<<<(unsigned)((th + 255) / 256), 256, 0, s>>>(r);
     } else {
       const int64_t blocks = ((r.lines_out + 31) / 32) * (r.Kp / 64);

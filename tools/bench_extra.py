@@ -132,6 +132,44 @@ def heff_cfg(ctx, name, reps=3):
     return res
 
 
+def shard_projection(ctx, name="target_heisenberg_chi4096", reps=5, ag_gbs=770.0):
+    """Per-rank step of the sharded apply emulated on one GPU:
+    rank r of P computes out[b_r] from L[:, :, b_r] and the full psi, W, R --
+    exactly the launch sequence bench.py --gpus P runs on each rank, minus the
+    all-gather, which is estimated as (P-1)/P |out| at the measured 770 GB/s
+    NVLink peer bandwidth (B200_PROFILING.md). Projection, not a P-GPU run."""
+    from paper_2512_23917_b200.sharding import slice_environment
+    cfg = synth.HEFF_CONFIGS[name]
+    chi, d, D = cfg["chi"], cfg["d"], cfg["D"]
+    inp = synth.heff_inputs(chi, d, D, cfg["dtype"], cfg["seed"], cfg["model"], device="cuda")
+    F = synth.heff_flops(chi, d, D)
+    L_full = inp.pop("L")
+    out_bytes = chi * d * d * chi * 16
+    rows = []
+    t1 = None
+    for P in (1, 2, 4, 8):
+        res = {"P": P}
+        for r in sorted({0, P - 1}):
+            L = slice_environment(L_full, P, r)
+            out = torch.empty(chi // P, d, d, chi, dtype=inp["psi"].dtype, device="cuda")
+            f = lambda: ctx.heff_apply(L, inp["W1"], inp["W2"], inp["R"], inp["psi"], out=out)  # noqa: E731
+            med, _ = timed(f, reps=reps, warm=2)
+            res[f"rank{r}_ms"] = med * 1e3
+            del L, out
+            torch.cuda.empty_cache()
+        t_rank = max(res[k] for k in res if k.startswith("rank")) / 1e3
+        t_ag = (P - 1) / P * out_bytes / (ag_gbs * 1e9) if P > 1 else 0.0
+        if P == 1:
+            t1 = t_rank
+        res.update({"allgather_ms_est": t_ag * 1e3, "step_ms_proj": (t_rank + t_ag) * 1e3,
+                    "tflops_proj": F / (t_rank + t_ag) / 1e12, "speedup_proj": t1 / (t_rank + t_ag),
+                    "speedup_compute_only": t1 / t_rank})
+        rows.append(res)
+    del inp, L_full
+    torch.cuda.empty_cache()
+    return {"workload": name, "rows": rows}
+
+
 def env_cfg(ctx, chi=4096, d=2, D=5, reps=3):
     """Environment updates (8(f3)) at the target scale, both sides, c128:
     GEMM (E.ket) -> skinny MPO pass -> conj(bra) -> GEMM; bra = ket."""
@@ -345,6 +383,10 @@ def main():
             res["mpo"] = mpo_apply_cfg(ctx)
         elif k == "svd":
             res["svd"] = svd_cfg(ctx)
+        elif k == "shards":
+            res["shards"] = shard_projection(ctx)
+        elif k == "shards4":
+            res["shards4"] = shard_projection(ctx, "cfg4_hubbard_chi4096", reps=2)
         elif k == "env":
             res["env"] = env_cfg(ctx)
         print(k, json.dumps(res.get(k))[:600], flush=True)

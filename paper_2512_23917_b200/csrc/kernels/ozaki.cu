@@ -438,8 +438,8 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
 #pragma unroll
           for (int lane = 0; lane < 2; lane++) {
             const int e = half * 2 + lane;
-            const double dr = (double)(lane ? cr2 >> 16 : cr2 & 0xffffu);
-            const double di = (double)(lane ? ci2 >> 16 : ci2 & 0xffffu);
+            const double dr = (double)(lane ? cr2 >> 16 : cr2 & 0xffffu);   // I2F on the XU pipe,
+            const double di = (double)(lane ? ci2 >> 16 : ci2 & 0xffffu);   // beside the saturated FP64 pipe
 #pragma unroll
             for (int j = 0; j < NCH; j++) {
               Sr[e][j] = fma(dr, a.W[i][j], Sr[e][j]);

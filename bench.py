@@ -250,7 +250,32 @@ def run_tci(args):
         obj = [tci.tci_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         ctx.comm_init(obj[0], ws, rank)
-    sh = ShardedHeff(ctx, L, W1, W2, R, ws, rank)
+    gather = "none" if ws == 1 else args.gather
+    sh = None
+    if ws > 1 and gather == "p2p":
+        # all-gather over peer memory, fused into the GEMM4 (Ozaki CRT) epilogue
+        try:
+            from paper_2512_23917_b200.sharding import PeerGatherHeff
+
+            def exchange(obj):
+                import torch.distributed as dist
+                allo = [None] * ws
+                dist.all_gather_object(allo, obj)
+                return allo
+            sh = PeerGatherHeff(ctx, L, W1, W2, R, ws, rank, exchange=exchange)
+        except Exception as e:   # no P2P / IPC on this box: NCCL all-gather instead
+            print(f"[rank {rank}] peer-memory gather unavailable ({e}); using NCCL", file=sys.stderr, flush=True)
+            sh = None
+        ok = torch.tensor([1 if sh is not None else 0], dtype=torch.int32, device=dev)
+        import torch.distributed as dist
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            gather = "nccl"
+            if sh is not None:
+                sh.close()
+                sh = None
+    if sh is None:
+        sh = ShardedHeff(ctx, L, W1, W2, R, ws, rank)
     out = sh.out
 
     def step():
@@ -264,6 +289,8 @@ def run_tci(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if gather == "p2p" and ctx.gather_status():
+        raise SystemExit(f"[rank {rank}] peer-memory gather barrier timed out (rerun with --gather nccl)")
 
     # ---- timed region (device time, CUDA events on the launching stream) ----
     sampler = ClockSampler(gpu_index(local)) if rank == 0 else None
@@ -436,8 +463,9 @@ def run_tci(args):
         "data": "synthetic (seeded counter-based generator; exact model MPO as W1=W2)",
         "config": {"workload": name, "chi": chi, "d": d, "D": D, "dtype": dt, "model": cfg["model"],
                    "gemm_algorithm": algo,
-                   "parallelism": f"output bond b sharded over {ws} rank(s); NCCL all-gather of out per step"
-                   if ws > 1 else "single GPU",
+                   "parallelism": (f"output bond b sharded over {ws} rank(s); all-gather of out per step "
+                                   + ("over peer memory fused into the GEMM4 epilogue (CUDA IPC, NVLink)"
+                                      if gather == "p2p" else "by NCCL")) if ws > 1 else "single GPU",
                    "l2": "inputs larger than L2 (L, psi, R >= 1 GB each): no flush"},
         "pct_fp64_tc_peak": value / FP64_PEAK_TFLOPS * 100, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
         "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
@@ -457,6 +485,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["tci", "reference"], default="tci")
     ap.add_argument("--config", choices=list(CONFIGS), default="target")
+    ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
+                    help="N > 1: all-gather of the output slabs over peer memory (fused into the GEMM4 "
+                         "epilogue) or by ncclAllGather")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -380,6 +380,48 @@ TCI_API tci_status_t tci_comm_unique_id(void *id);
  * Errors: NCCL (no communicator), SHAPE_MISMATCH, UNSUPPORTED. */
 TCI_API tci_status_t tci_allgather(tci_ctx_t ctx, tci_tensor_t shard, tci_tensor_t full);
 
+/* Peer-memory all-gather fused into the H_eff output (the one exchange of
+ * the sharded apply). One process per GPU. Each
+ * rank owns (caller-allocated device memory) its full output buffer
+ * [P * chi_lo_r, d, d, chi_ro] (complex128 / float64, 16-byte aligned) and a
+ * zeroed flag array of P uint32; it exports both with tci_ipc_handle, the
+ * ranks exchange the (handle, offset) pairs (e.g. with
+ * torch.distributed.all_gather_object), map the peers' with tci_ipc_open and
+ * register the P pointers of each kind (own ones included, rank order) with
+ * tci_gather_register.
+ *
+ * tci_ipc_handle: `handle` receives the 64-byte cudaIpcMemHandle_t of the
+ * allocation holding dev_ptr, `offset` dev_ptr's offset in it.
+ * tci_ipc_open: maps a peer's allocation (cudaIpcOpenMemHandle, lazy peer
+ * access) and returns base + offset; tci_ipc_close unmaps it.
+ * Errors: INVALID_ARGUMENT (NULL, not a device allocation, unknown pointer),
+ * CUDA. */
+TCI_API tci_status_t tci_ipc_handle(const void *dev_ptr, void *handle, size_t *offset);
+TCI_API tci_status_t tci_ipc_open(const void *handle, size_t offset, void **dev_ptr);
+TCI_API tci_status_t tci_ipc_close(void *dev_ptr);
+
+/* Register the gather's pointer tables (nranks <= 8): full[i] / flags[i] are
+ * rank i's buffers, valid in this process. Errors: OUT_OF_RANGE, INVALID_ARGUMENT. */
+TCI_API tci_status_t tci_gather_register(tci_ctx_t ctx, int nranks, int rank, void *const *full,
+                                         void *const *flags);
+
+/* H_eff psi on this rank's slab (L = L[:, :, b_r], chi_lo_r columns) with the
+ * result gathered into EVERY rank's `full` (the registered buffer): rows
+ * [r chi_lo_r, (r+1) chi_lo_r) of the slowest leg are this rank's. The Ozaki
+ * GEMM4 epilogue stores each output element locally and into every peer's
+ * buffer over NVLink (no separate collective); the DMMA path pushes the slab
+ * after GEMM4 with a peer-copy kernel. A flag barrier (system-scope release /
+ * acquire) before the chain and after the stores orders the steps across
+ * ranks; on return (stream order) `full` holds the whole output on every
+ * rank, bitwise equal to the unsharded tci_heff_apply. A barrier that waits
+ * > 30 s sets an error flag read by tci_gather_status (synchronizes) instead
+ * of hanging. With nranks = 1 it is tci_heff_apply into full.
+ * Errors: as tci_heff_apply; INVALID_ARGUMENT if full is not the registered
+ * buffer; SHAPE_MISMATCH if full's first leg != nranks x L's last leg. */
+TCI_API tci_status_t tci_heff_apply_gather(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2,
+                                           tci_tensor_t R, tci_tensor_t psi, tci_tensor_t full);
+TCI_API tci_status_t tci_gather_status(tci_ctx_t ctx, int *timed_out);
+
 /* ---------------------------------------------------------------------- */
 /* Diagnostics                                                             */
 /* ---------------------------------------------------------------------- */

@@ -50,6 +50,8 @@ EXPORTED = [
     "tci_ozaki_params", "tci_env_workspace_size", "tci_env_update", "tci_cplx_conj",
     "tci_svd_workspace_size", "tci_svd", "tci_trunc_svd", "tci_svd_info",
     "tci_mps_mpo_zipup_workspace_size", "tci_mps_mpo_zipup", "tci_heff_apply_staged",
+    "tci_ipc_handle", "tci_ipc_open", "tci_ipc_close", "tci_gather_register", "tci_heff_apply_gather",
+    "tci_gather_status",
 ]
 
 
@@ -103,6 +105,12 @@ _sig = {
     "tci_comm_init": ([_vp, ctypes.c_char_p, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "tci_comm_unique_id": ([ctypes.c_char_p], ctypes.c_int),
     "tci_allgather": ([_vp, _vp, _vp], ctypes.c_int),
+    "tci_ipc_handle": ([_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "tci_ipc_open": ([ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(_vp)], ctypes.c_int),
+    "tci_ipc_close": ([_vp], ctypes.c_int),
+    "tci_gather_register": ([_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp)], ctypes.c_int),
+    "tci_heff_apply_gather": ([_vp] * 7, ctypes.c_int),
+    "tci_gather_status": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_launch_count": ([_vp, _i64p], ctypes.c_int),
     "tci_profile_enable": ([_vp, ctypes.c_int], ctypes.c_int),
     "tci_set_gemm_algorithm": ([_vp, ctypes.c_int], ctypes.c_int),
@@ -349,6 +357,42 @@ def tci_comm_init(ctx: int, uid: bytes, nranks: int, rank: int) -> None:
 
 def tci_allgather(ctx: int, shard: int, full: int) -> None:
     _ok(_lib.tci_allgather(_vp(ctx), _vp(shard), _vp(full)), "tci_allgather")
+
+
+def tci_ipc_handle(dev_ptr: int):
+    """(64-byte cudaIpcMemHandle of the allocation, offset of dev_ptr in it)."""
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_size_t()
+    _ok(_lib.tci_ipc_handle(_vp(dev_ptr), buf, ctypes.byref(off)), "tci_ipc_handle")
+    return buf.raw, off.value
+
+
+def tci_ipc_open(handle: bytes, offset: int) -> int:
+    p = _vp()
+    _ok(_lib.tci_ipc_open(handle, int(offset), ctypes.byref(p)), "tci_ipc_open")
+    return p.value
+
+
+def tci_ipc_close(dev_ptr: int) -> None:
+    _ok(_lib.tci_ipc_close(_vp(dev_ptr)), "tci_ipc_close")
+
+
+def tci_gather_register(ctx: int, nranks: int, rank: int, full_ptrs, flag_ptrs) -> None:
+    fa = (_vp * len(full_ptrs))(*[_vp(int(x)) for x in full_ptrs])
+    ga = (_vp * len(flag_ptrs))(*[_vp(int(x)) for x in flag_ptrs])
+    _ok(_lib.tci_gather_register(_vp(ctx), int(nranks), int(rank), fa, ga), "tci_gather_register")
+
+
+def tci_heff_apply_gather(ctx: int, L: int, W1: int, W2: int, R: int, psi: int, full: int) -> None:
+    _ok(_lib.tci_heff_apply_gather(_vp(ctx), _vp(L), _vp(W1), _vp(W2), _vp(R), _vp(psi), _vp(full)),
+        "tci_heff_apply_gather")
+
+
+def tci_gather_status(ctx: int) -> int:
+    """1 if a gather barrier timed out since registration (synchronizes the stream)."""
+    v = ctypes.c_int()
+    _ok(_lib.tci_gather_status(_vp(ctx), ctypes.byref(v)), "tci_gather_status")
+    return v.value
 
 
 def tci_launch_count(ctx: int) -> int:
@@ -720,6 +764,18 @@ class Context:
     def allgather(self, shard, full):
         tci_allgather(self.handle, self.tensor(shard), self.tensor(full))
         return full
+
+    def gather_register(self, nranks: int, rank: int, full_ptrs, flag_ptrs):
+        tci_gather_register(self.handle, nranks, rank, full_ptrs, flag_ptrs)
+
+    def heff_apply_gather(self, L, W1, W2, R, psi, full):
+        """tci_heff_apply_gather: this rank's slab, gathered into every rank's full."""
+        self.ensure_workspace(self.heff_workspace_size(L, W1, W2, R, psi))
+        tci_heff_apply_gather(self.handle, *[self.tensor(x) for x in (L, W1, W2, R, psi, full)])
+        return full
+
+    def gather_status(self) -> int:
+        return tci_gather_status(self.handle)
 
     def launch_count(self) -> int:
         return tci_launch_count(self.handle)

@@ -4,6 +4,8 @@
 // chains, NCCL all-gather, TCI_VERBOSE diagnostics.
 // Every call validates all arguments before enqueueing any kernel.
 #include <dlfcn.h>
+#include <map>
+#include <mutex>
 
 #include <chrono>
 #include <cstdio>
@@ -224,6 +226,11 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   c->host_scratch = nullptr;
   c->copy_stream = nullptr;
   for (auto &e : c->evs) e = nullptr;
+  c->g_nranks = 1;
+  c->g_rank = 0;
+  for (int i = 0; i < 8; i++) c->g_full[i] = c->g_flags[i] = nullptr;
+  c->g_epoch = 0;
+  c->g_err = nullptr;
   c->svd_last_sweeps = 0;
   c->svd_last_off = 0.0;
   {
@@ -295,6 +302,9 @@ tci_status_t tci_destroy_context(tci_ctx_t ctx) {
     }
   if (ctx->dev_scratch) cudaFree(ctx->dev_scratch);
   if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
+  if (ctx->g_err) cudaFree(ctx->g_err);
+  ctx->g_err = nullptr;
+  ctx->g_nranks = 1;
   ctx->dev_scratch = ctx->host_scratch = nullptr;
   ctx->nccl_comm = nullptr;
   ctx->plan_cache.clear();
@@ -955,6 +965,143 @@ tci_status_t tci_allgather(tci_ctx_t ctx, tci_tensor_t shard, tci_tensor_t full)
   Verbose vb(ctx, "allgather", {shard, full});
   const int r = g_nccl.allgather(vs.data, vf.data, vs.bytes(), /*ncclUint8*/ 1, ctx->nccl_comm, ctx->stream);
   if (r) TCI_FAIL(TCI_ERR_NCCL, "ncclAllGather: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
+  return TCI_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Peer-memory all-gather
+// ---------------------------------------------------------------------------
+static std::mutex g_ipc_mu;
+static std::map<void *, void *> g_ipc_base;   // pointer handed out -> mapped base
+
+tci_status_t tci_ipc_handle(const void *dev_ptr, void *handle, size_t *offset) {
+  if (!dev_ptr || !handle || !offset) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL argument");
+  // the handle names the whole allocation; the offset locates dev_ptr in it
+  typedef int (*range_fn)(unsigned long long *, size_t *, unsigned long long);
+  static range_fn range = nullptr;
+  if (!range) {
+    void *h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+    if (h) range = (range_fn)dlsym(h, "cuMemGetAddressRange_v2");
+    if (!range) TCI_FAIL(TCI_ERR_CUDA, "cuMemGetAddressRange_v2 not found in libcuda.so.1");
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "ipc: not a device allocation");
+  cudaIpcMemHandle_t hd;
+  TCI_CUDA_CHECK(cudaIpcGetMemHandle(&hd, (void *)(uintptr_t)base));
+  static_assert(sizeof(hd) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle, &hd, sizeof hd);
+  *offset = (size_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+  return TCI_OK;
+}
+
+tci_status_t tci_ipc_open(const void *handle, size_t offset, void **dev_ptr) {
+  if (!handle || !dev_ptr) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL argument");
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle, sizeof hd);
+  void *base = nullptr;
+  TCI_CUDA_CHECK(cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr = static_cast<char *>(base) + offset;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  g_ipc_base[*dev_ptr] = base;
+  return TCI_OK;
+}
+
+tci_status_t tci_ipc_close(void *dev_ptr) {
+  void *base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto it = g_ipc_base.find(dev_ptr);
+    if (it == g_ipc_base.end()) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "ipc_close: pointer was not opened by tci_ipc_open");
+    base = it->second;
+    g_ipc_base.erase(it);
+  }
+  TCI_CUDA_CHECK(cudaIpcCloseMemHandle(base));
+  return TCI_OK;
+}
+
+tci_status_t tci_gather_register(tci_ctx_t ctx, int nranks, int rank, void *const *full, void *const *flags) {
+  CHECK(check_ctx(ctx));
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+    TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "gather: rank %d of %d (at most %d ranks)", rank, nranks, kMaxRanks);
+  if (!full || !flags) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL pointer table");
+  for (int i = 0; i < nranks; i++)
+    if (!full[i] || !flags[i] || (uintptr_t)full[i] % 16 || (uintptr_t)flags[i] % 4)
+      TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "gather: rank %d pointer is NULL or misaligned", i);
+  if (!ctx->g_err) {
+    TCI_CUDA_CHECK(cudaSetDevice(ctx->device));
+    TCI_CUDA_CHECK(cudaMalloc(&ctx->g_err, sizeof(int)));   // registration time, not a compute call
+    TCI_CUDA_CHECK(cudaMemset(ctx->g_err, 0, sizeof(int)));
+  }
+  TCI_CUDA_CHECK(gather_preload());
+  ctx->g_nranks = nranks;
+  ctx->g_rank = rank;
+  for (int i = 0; i < 8; i++) {
+    ctx->g_full[i] = i < nranks ? full[i] : nullptr;
+    ctx->g_flags[i] = i < nranks ? flags[i] : nullptr;
+  }
+  return TCI_OK;
+}
+
+tci_status_t tci_gather_status(tci_ctx_t ctx, int *timed_out) {
+  CHECK(check_ctx(ctx));
+  if (!timed_out) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  *timed_out = 0;
+  if (!ctx->g_err) return TCI_OK;
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  TCI_CUDA_CHECK(cudaMemcpy(timed_out, ctx->g_err, sizeof(int), cudaMemcpyDeviceToHost));
+  return TCI_OK;
+}
+
+tci_status_t tci_heff_apply_gather(tci_ctx_t ctx, tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2, tci_tensor_t R,
+                                   tci_tensor_t psi, tci_tensor_t full) {
+  CHECK(check_ctx(ctx));
+  for (tci_tensor_t t : {L, W1, W2, R, psi, full}) CHECK(check_ten(ctx, t, true));
+  const int P = ctx->g_nranks, r = ctx->g_rank;
+  if (P > 1 && full->data != ctx->g_full[r])
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "gather: full is not the buffer registered for this rank");
+  if (full->order != 4 || L->order != 3) TCI_FAIL(TCI_ERR_ORDER_MISMATCH, "gather: full order 4, L order 3");
+  const int64_t slab = L->shape[2];
+  if (full->shape[0] != slab * P)
+    TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "gather: full's first leg must be nranks x L's last leg");
+  const View vf = view_of(full);
+  for (tci_tensor_t t : {L, W1, W2, R, psi}) {
+    const View v = view_of(t);
+    const char *x = (const char *)v.data, *y = (const char *)vf.data;
+    if (x < y + vf.bytes() && y < x + v.bytes()) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "heff: full overlaps an input");
+  }
+  Verbose vb(ctx, "heff_apply_gather", {L, W1, W2, R, psi});
+  // this rank's slab: rows [r slab, (r+1) slab) of the slowest leg (contiguous)
+  View vo = vf;
+  vo.shape[0] = slab;
+  const size_t slab_bytes = vo.bytes(), off = (size_t)r * slab_bytes;
+  vo.data = static_cast<char *>(vf.data) + off;
+  PeerTable tab{};
+  for (int i = 0; i < P; i++) {
+    tab.full[i] = ctx->g_full[i];
+    tab.flags[i] = ctx->g_flags[i];
+  }
+  const double timeout_s = 30.0;
+  if (P > 1) {
+    // entry: every peer has finished with its buffer from the previous step
+    TCI_CUDA_CHECK(launch_gather_barrier(tab, r, P, ++ctx->g_epoch, ctx->g_err, timeout_s, ctx->stream,
+                                         &ctx->launches));
+  }
+  HeffGather g{};
+  g.npeer = 0;
+  for (int i = 0; i < P; i++)
+    if (i != r) g.peer_out[g.npeer++] = static_cast<char *>(ctx->g_full[i]) + off;
+  CHECK(heff_exec(ctx, view_of(L), view_of(W1), view_of(W2), view_of(R), view_of(psi), vo, nullptr,
+                  P > 1 ? &g : nullptr));
+  if (P > 1) {
+    if (!g.fused)   // DMMA / generic-tree GEMM4: push the finished slab to the peers
+      TCI_CUDA_CHECK(launch_push_rows(vo.data, tab, r, P, off, slab_bytes, ctx->stream, &ctx->launches));
+    // exit: every peer's slab has landed in this rank's buffer
+    TCI_CUDA_CHECK(launch_gather_barrier(tab, r, P, ++ctx->g_epoch, ctx->g_err, timeout_s, ctx->stream,
+                                         &ctx->launches));
+  }
   return TCI_OK;
 }
 

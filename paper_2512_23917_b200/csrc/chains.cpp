@@ -265,7 +265,8 @@ void stage_L_in(void *user, int64_t m0, int64_t mc) {
 }  // namespace
 
 tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View &W2, const View &R,
-                       const View &psi, const View &out, HeffStaging *stage) {
+                       const View &psi, const View &out, HeffStaging *stage, HeffGather *gather) {
+  if (gather) gather->fused = false;
   const tci_dtype_t dt = L.dtype;
   if (W1.dtype != dt || W2.dtype != dt || R.dtype != dt || psi.dtype != dt || out.dtype != dt)
     TCI_FAIL(TCI_ERR_UNSUPPORTED, "heff: all operands must share one dtype");
@@ -499,6 +500,13 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
         TCI_CUDA_CHECK(stage->err);
       }
     } else {
+      // peer-memory all-gather fused into the Ozaki CRT epilogue: each
+      // finished element also goes to every peer's copy of this slab
+      if (gather && dt == TCI_C128 && g.zalgo == kZOzaki && g.splitk <= 1 && !gemm_thin_applies(g)) {
+        g.npeer = gather->npeer;
+        for (int p = 0; p < gather->npeer; p++) g.peer_C[p] = gather->peer_out[p];
+        gather->fused = true;
+      }
       tci_status_t _r = run_gemm(ctx, g);
       if (_r) return _r;
     }

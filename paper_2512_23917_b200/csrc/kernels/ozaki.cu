@@ -330,6 +330,8 @@ struct CrtArgs {
   int t;
   double2 *C;
   int64_t c_sm;
+  int npeer;                // peer-memory all-gather: the same element also
+  double2 *peer[7];         // stored at peer[p] + (m c_sm + n) over NVLink
 };
 
 template <int NCH>
@@ -468,6 +470,8 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
           }
         }
         __stcs(&a.C[m * a.c_sm + n], out);
+#pragma unroll 1
+        for (int pp = 0; pp < a.npeer; pp++) __stcs(&a.peer[pp][m * a.c_sm + n], out);
       }
     }
     __syncthreads();   // stage s fully consumed
@@ -645,6 +649,8 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   }
   c.nmod = p.nmod; c.EA = EA; c.EB = EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
   c.C = static_cast<double2 *>(g.C); c.c_sm = g.c_sm;
+  c.npeer = std::min(g.npeer, 7);
+  for (int pp = 0; pp < c.npeer; pp++) c.peer[pp] = static_cast<double2 *>(g.peer_C[pp]);
   for (int64_t ch = 0; ch < p.chunks; ch++) {
     const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
     if (g.rows_needed) {

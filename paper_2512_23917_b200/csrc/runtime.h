@@ -37,6 +37,11 @@ struct tci_ctx_s {
   void *dev_scratch;    // reductions (vec.cu): allocated once at creation
   void *host_scratch;   // pinned, reduction results
   cudaStream_t copy_stream;   // library-owned (created on first use): staged H2D / D2H copies
+  // peer-memory all-gather (tci_gather_register): P pointers of each kind
+  int g_nranks, g_rank;
+  void *g_full[8], *g_flags[8];
+  uint32_t g_epoch;
+  int *g_err;                 // device: set when a barrier timed out
   cudaEvent_t evs[8];         // ordering events between the context and copy streams
   int svd_last_sweeps;  // Jacobi sweeps of the last svd / trunc_svd (tci_svd_info)
   double svd_last_off;  // its final off-diagonal measure
@@ -157,8 +162,17 @@ struct HeffStaging {
   int64_t chunk_rows;
   cudaError_t err;
 };
+// Peer-memory all-gather of the output slab (tci_heff_apply_gather): GEMM4's
+// epilogue also stores every element at peer_out[p] (same layout); `fused`
+// reports whether it did (else the caller pushes the slab after the chain)
+struct HeffGather {
+  int npeer;
+  void *peer_out[7];
+  bool fused;
+};
 tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View &W2, const View &R,
-                       const View &psi, const View &out, HeffStaging *stage = nullptr);
+                       const View &psi, const View &out, HeffStaging *stage = nullptr,
+                       HeffGather *gather = nullptr);
 tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View &B, const char *lb,
                        const View &U, const char *lu, const View &T, const char *lt);
 

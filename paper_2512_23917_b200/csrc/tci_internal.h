@@ -66,6 +66,11 @@ struct GemmProblem {
   void (*rows_needed)(void *user, int64_t m0, int64_t mc) = nullptr;
   void *rows_user = nullptr;
   int64_t max_chunk_rows = 0;
+  // peer-memory all-gather fused into the epilogue (Ozaki CRT only): every
+  // stored C element is also stored at the same offset from peer_C[p]
+  // (another rank's buffer, mapped over NVLink); c_row must be null
+  int npeer = 0;
+  void *peer_C[7] = {};
   int64_t te_chi_a = 0, te_chi_c = 0;     // extents of a and c
   int64_t te_a_a = 0, te_a_s = 0;         // A strides of a and s (b stride == 1)
   int64_t te_b_t = 0;                     // B stride of t (c stride == 1, b stride = b_sk)
@@ -243,5 +248,18 @@ cudaError_t launch_svd_complete(const SvdProblem &p, const int *sel, int64_t nse
                                 int nz, cudaStream_t st, int64_t *launches);
 cudaError_t launch_svd_gather_s(double *s_out, const double *s, const int *perm, int64_t nk, cudaStream_t st,
                                 int64_t *launches);
+
+// Peer-memory all-gather (gather.cu): pointers valid in this
+// process (own buffers and the peers' IPC mappings), rank order
+constexpr int kMaxRanks = 8;
+struct PeerTable {
+  void *full[kMaxRanks];    // each rank's full output buffer
+  void *flags[kMaxRanks];   // each rank's uint32 flag array [nranks]
+};
+cudaError_t gather_preload();
+cudaError_t launch_gather_barrier(const PeerTable &t, int rank, int nranks, uint32_t epoch, int *err,
+                                  double timeout_s, cudaStream_t s, int64_t *launches);
+cudaError_t launch_push_rows(const void *src, const PeerTable &t, int rank, int nranks, size_t offset_bytes,
+                             size_t bytes, cudaStream_t s, int64_t *launches);
 
 }  // namespace tci

@@ -54,3 +54,68 @@ class ShardedHeff:
         if self.world > 1:
             self.ctx.allgather(self.out, self.full)
         return self.full
+
+
+def peer_pointer_table(rank: int, handles, own, opener):
+    """Pointer tables for tci_gather_register from the exchanged IPC handles.
+
+    handles: per rank (rank order) ((full_handle, full_offset), (flag_handle,
+    flag_offset)), as all_gather_object returns them; own: this rank's
+    (full_ptr, flag_ptr); opener(handle, offset) -> mapped pointer. Returns
+    (full_ptrs, flag_ptrs, opened) -- opened lists what must be unmapped."""
+    fulls, flags, opened = [], [], []
+    for i, (hf, hg) in enumerate(handles):
+        if i == rank:
+            fulls.append(own[0])
+            flags.append(own[1])
+            continue
+        pf, pg = opener(*hf), opener(*hg)
+        opened += [pf, pg]
+        fulls.append(pf)
+        flags.append(pg)
+    return fulls, flags, opened
+
+
+class PeerGatherHeff:
+    """One rank of the sharded apply with the all-gather done over peer memory
+    (tci_heff_apply_gather): the GEMM4 epilogue stores every output element
+    into this rank's slab of EVERY rank's `full` buffer (CUDA IPC mappings
+    over NVLink), with a flag barrier around the step -- no collective call.
+
+    exchange(obj) -> [obj of rank 0, ..., obj of rank P-1] (e.g. a wrapper of
+    torch.distributed.all_gather_object). `peers` = (full_ptrs, flag_ptrs)
+    bypasses IPC (single-process emulation of several ranks in tests)."""
+
+    def __init__(self, ctx, L_slice, W1, W2, R, world: int, rank: int, exchange=None, peers=None, full=None,
+                 flags=None):
+        import torch
+        import paper_2512_23917_b200 as tci
+        self.ctx, self.world, self.rank = ctx, world, rank
+        self.L, self.W1, self.W2, self.R = L_slice, W1, W2, R
+        chi_lo, d, chi_ro = L_slice.shape[2], W1.shape[2], R.shape[2]
+        dev = L_slice.device
+        self.full = full if full is not None else torch.empty((chi_lo * world, d, d, chi_ro),
+                                                              dtype=L_slice.dtype, device=dev)
+        self.flags = flags if flags is not None else torch.zeros(max(world, 1), dtype=torch.int32, device=dev)
+        self._opened = []
+        if world > 1:
+            if peers is None:
+                if exchange is None:
+                    raise ValueError("PeerGatherHeff needs exchange() (or peers) for world > 1")
+                mine = (tci.tci_ipc_handle(self.full.data_ptr()), tci.tci_ipc_handle(self.flags.data_ptr()))
+                fulls, flg, self._opened = peer_pointer_table(
+                    rank, exchange(mine), (self.full.data_ptr(), self.flags.data_ptr()), tci.tci_ipc_open)
+            else:
+                fulls, flg = peers
+            ctx.gather_register(world, rank, fulls, flg)
+        self.out = self.full
+
+    def apply(self, psi):
+        self.ctx.heff_apply_gather(self.L, self.W1, self.W2, self.R, psi, self.full)
+        return self.full
+
+    def close(self):
+        import paper_2512_23917_b200 as tci
+        for p in self._opened:
+            tci.tci_ipc_close(p)
+        self._opened = []

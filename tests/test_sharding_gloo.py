@@ -70,3 +70,55 @@ def test_shard_bounds():
     assert [shard_bounds(4096, 8, r) for r in (0, 7)] == [(0, 512), (3584, 4096)]
     with pytest.raises(ValueError):
         shard_bounds(10, 4, 0)
+
+
+def _handle_worker(rank, world, port, q):
+    """Host logic of the peer-memory gather setup: IPC handles exchanged with
+    all_gather_object (gloo here, the same call over NCCL on the GPU box),
+    pointer tables built in rank order with this rank's own buffers."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_23917_b200.sharding import peer_pointer_table
+        mine = ((b"F%d" % rank + bytes(62), 4096 * rank), (b"G%d" % rank + bytes(62), 64 * rank))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        opened = []
+
+        def opener(h, off):   # stands in for tci_ipc_open: a distinct fake pointer per (handle, offset)
+            p = (1 << 40) + int(h[1:2].decode()) * (1 << 32) + (1 << 20) * (h[:1] == b"G") + off
+            opened.append(p)
+            return p
+        own = (7000 + rank, 9000 + rank)
+        fulls, flags, op = peer_pointer_table(rank, allh, own, opener)
+        q.put((rank, fulls, flags, op, opened))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_gather_handle_exchange_gloo_world3():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_handle_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    res = {}
+    for _ in range(world):
+        r, fulls, flags, op, opened = q.get(timeout=10)
+        res[r] = (fulls, flags, op, opened)
+    for r in range(world):
+        fulls, flags, op, opened = res[r]
+        assert len(fulls) == len(flags) == world
+        assert fulls[r] == 7000 + r and flags[r] == 9000 + r          # own buffers, unmapped
+        for i in range(world):
+            if i != r:                                                 # peer i's mapping + its offset
+                assert fulls[i] == (1 << 40) + i * (1 << 32) + 4096 * i
+                assert flags[i] == (1 << 40) + i * (1 << 32) + (1 << 20) + 64 * i
+        assert sorted(op) == sorted(opened) and len(op) == 2 * (world - 1)

@@ -15,6 +15,7 @@
 // written back in (n_hi, b2, n_lo) order so global stores are contiguous when
 // the trailing n-run is interleaved with b2.
 #include <algorithm>
+#include <cstdlib>
 
 #include "../tci_internal.h"
 #include "common.cuh"
@@ -262,6 +263,164 @@ __global__ void __launch_bounds__(NTH) skinny_stream_kernel(const __grid_constan
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core variant of the streaming complex pass (K, N <= 32; the H_eff
+// MPO pass is K = N = 20 at d = 2, D = 5): the contraction of a tile of TD
+// b2 values is the [TD x K] x [K x N] product, run as FP64 DMMA m8n8k4 with
+// the 3M complex split (P = Xr Wr, Q = Xi Wi, S = (Xr + Xi)(Wr + Wi); re =
+// P - Q, im = S - P - Q, as the streaming CUDA-core kernel). One DMMA does
+// 256 FMAs, so the pass needs ~1/8 of the FP64 instructions of the CUDA-core
+// version and is left bound by streaming `in` and `out` (HBM). W's three
+// planes sit in shared memory pre-arranged as per-lane B fragments; the input
+// tile [K][TD] is double-buffered with cp.async; warp w owns m-tiles 2w and
+// 2w + 1 (8 b2 values each). Summation order per output: k ascending in
+// chunks of 4 (DMMA), fixed -> deterministic.
+// ---------------------------------------------------------------------------
+constexpr int TD = 128;   // b2 values per tile (16 m-tiles of 8; 2 per warp)
+
+template <int KS, int NTL>
+__global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant__ SkinnyProblem a, int64_t ntiles) {
+  extern __shared__ __align__(16) char sm[];
+  const int K = a.K, N = a.N;
+  double *sWf = reinterpret_cast<double *>(sm);                        // [KS][NTL][3][32]
+  double2 *sIn = reinterpret_cast<double2 *>(sWf + KS * NTL * 3 * 32);  // [2][K][TD]
+  const double2 *W = reinterpret_cast<const double2 *>(a.W);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < KS * NTL * 32; i += NTH) {
+    const int l = i & 31, f = i >> 5, nt = f % NTL, ks = f / NTL;
+    const int k = ks * 4 + (l & 3), n = nt * 8 + (l >> 2);
+    double2 w = make_double2(0.0, 0.0);
+    if (k < K && n < N) w = W[a.w_koff[k] + a.w_noff[n]];
+    double *dst = sWf + ((ks * NTL + nt) * 3) * 32 + l;
+    dst[0] = w.x;
+    dst[32] = w.y;
+    dst[64] = w.x + w.y;
+  }
+  const int64_t tiles2 = (a.nb[2] + TD - 1) / TD;
+  auto tile_ptrs = [&](int64_t t, const double2 *&in, double2 *&out, int &nc) {
+    const int64_t t2 = t % tiles2, r = t / tiles2;
+    const int64_t i1 = r % a.nb[1], i0 = r / a.nb[1];
+    const int64_t c0 = t2 * TD;
+    nc = (int)min((int64_t)TD, a.nb[2] - c0);
+    in = reinterpret_cast<const double2 *>(a.in) + i0 * a.in_sb[0] + i1 * a.in_sb[1] + c0;
+    out = reinterpret_cast<double2 *>(a.out) + i0 * a.out_sb[0] + i1 * a.out_sb[1] + c0 * a.out_sb[2];
+  };
+  auto load = [&](int64_t t, int buf) {
+    const double2 *in;
+    double2 *out;
+    int nc;
+    tile_ptrs(t, in, out, nc);
+    double2 *dst = sIn + buf * K * TD;
+    for (int i = tid; i < K * TD; i += NTH) {
+      const int k = i / TD, c = i % TD;
+      cp_async_zfill<16>(dst + k * TD + c, c < nc ? in + a.in_koff[k] + c : in, c < nc ? 16 : 0);
+    }
+  };
+  int64_t t = blockIdx.x;
+  if (t < ntiles) load(t, 0);
+  cp_async_commit();
+  int buf = 0;
+  const int r = lane >> 2, q = lane & 3;   // fragment row (b2 in the m-tile) / column (k in the step)
+  for (; t < ntiles; t += gridDim.x, buf ^= 1) {
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntiles) load(tn, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double2 *tile = sIn + buf * K * TD;
+    const double2 *in;
+    double2 *out;
+    int nc;
+    tile_ptrs(t, in, out, nc);
+    double P[2][NTL][2], Q[2][NTL][2], S[2][NTL][2];
+#pragma unroll
+    for (int m = 0; m < 2; m++)
+#pragma unroll
+      for (int nt = 0; nt < NTL; nt++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) P[m][nt][e] = Q[m][nt][e] = S[m][nt][e] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ks++) {
+      const int k = ks * 4 + q;
+      double ar[2], ai[2], as[2];
+#pragma unroll
+      for (int m = 0; m < 2; m++) {
+        const double2 x = k < K ? tile[k * TD + (warp * 2 + m) * 8 + r] : make_double2(0.0, 0.0);
+        ar[m] = x.x;
+        ai[m] = x.y;
+        as[m] = x.x + x.y;
+      }
+#pragma unroll
+      for (int nt = 0; nt < NTL; nt++) {
+        const double *wf = sWf + ((ks * NTL + nt) * 3) * 32 + lane;
+        const double wr = wf[0], wi = wf[32], ws = wf[64];
+#pragma unroll
+        for (int m = 0; m < 2; m++) {
+          dmma884(P[m][nt], ar[m], wr);
+          dmma884(Q[m][nt], ai[m], wi);
+          dmma884(S[m][nt], as[m], ws);
+        }
+      }
+    }
+    // C fragment: row r (b2), columns n = nt*8 + 2q + e
+#pragma unroll
+    for (int m = 0; m < 2; m++) {
+      const int c = (warp * 2 + m) * 8 + r;
+      if (c < nc) {
+#pragma unroll
+        for (int nt = 0; nt < NTL; nt++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int n = nt * 8 + 2 * q + e;
+            if (n < N)
+              out[c * a.out_sb[2] + a.out_noff[n]] =
+                  make_double2(P[m][nt][e] - Q[m][nt][e], S[m][nt][e] - P[m][nt][e] - Q[m][nt][e]);
+          }
+      }
+    }
+    __syncthreads();   // this buffer is refilled two tiles later
+  }
+  cp_async_wait<0>();
+}
+
+template <int KS, int NTL>
+cudaError_t launch_dmma_kn(const SkinnyProblem &p, cudaStream_t s) {
+  const size_t smem = (size_t)KS * NTL * 3 * 32 * 8 + 2 * (size_t)p.K * TD * 16;
+  const int64_t ntiles = p.nb[0] * p.nb[1] * ((p.nb[2] + TD - 1) / TD);
+  auto k = skinny_dmma_kernel<KS, NTL>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTH, smem);
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)148 * std::max(1, per_sm));
+  k<<<(unsigned)grid, NTH, smem, s>>>(p, ntiles);
+  return cudaGetLastError();
+}
+
+template <int KS>
+cudaError_t launch_dmma_k(const SkinnyProblem &p, cudaStream_t s) {
+  switch ((p.N + 7) / 8) {
+    case 1: return launch_dmma_kn<KS, 1>(p, s);
+    case 2: return launch_dmma_kn<KS, 2>(p, s);
+    case 3: return launch_dmma_kn<KS, 3>(p, s);
+    default: return launch_dmma_kn<KS, 4>(p, s);
+  }
+}
+
+// K, N <= 32, complex, b2 unit-stride in the input (the caller checked)
+cudaError_t launch_dmma(const SkinnyProblem &p, cudaStream_t s) {
+  switch ((p.K + 3) / 4) {
+    case 1: return launch_dmma_k<1>(p, s);
+    case 2: return launch_dmma_k<2>(p, s);
+    case 3: return launch_dmma_k<3>(p, s);
+    case 4: return launch_dmma_k<4>(p, s);
+    case 5: return launch_dmma_k<5>(p, s);
+    case 6: return launch_dmma_k<6>(p, s);
+    case 7: return launch_dmma_k<7>(p, s);
+    default: return launch_dmma_k<8>(p, s);
+  }
+}
+
 template <bool CPLX, int NPT>
 cudaError_t launch_stream_npt(const SkinnyProblem &p, cudaStream_t s) {
   const size_t es = CPLX ? 16 : 8;
@@ -323,6 +482,15 @@ cudaError_t launch_c(const SkinnyProblem &p, size_t smem, int64_t blocks, cudaSt
   return launch_npt<CPLX, MAXNPT>(p, smem, blocks, s);
 }
 
+// TCI_SKINNY_DMMA=0 keeps the CUDA-core streaming kernel (A/B measurements)
+bool dmma_pass_disabled() {
+  static const int off = [] {
+    const char *e = getenv("TCI_SKINNY_DMMA");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 }  // namespace
 
 size_t skinny_smem_bytes(int K, int N, size_t esz) {
@@ -346,6 +514,11 @@ cudaError_t launch_skinny(const SkinnyProblem &p0, cudaStream_t s, int64_t *laun
     for (int k = 0; ok && k < p.K; k++) ok = p.in_koff[k] % per == 0;
     ok = ok && p.in_sb[0] % per == 0 && p.in_sb[1] % per == 0;
     const size_t ssm = (size_t)((cplx ? 3 : 1) * p.K * p.N + 1) * 8 + 2 * (size_t)p.K * TBS * es;
+    if (ok && cplx && p.K <= 32 && p.N <= 32 && !dmma_pass_disabled()) {
+      cudaError_t e = launch_dmma(p, s);   // FP64 tensor cores (DMMA), 3M
+      if (launches) ++*launches;
+      return e;
+    }
     if (ok && ssm <= 200 * 1024) {
       cudaError_t e = cplx ? launch_stream<true>(p, s) : launch_stream<false>(p, s);
       if (launches) ++*launches;

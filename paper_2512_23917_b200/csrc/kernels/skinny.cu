@@ -272,18 +272,18 @@ __global__ void __launch_bounds__(NTH) skinny_stream_kernel(const __grid_constan
 // 256 FMAs, so the pass needs ~1/8 of the FP64 instructions of the CUDA-core
 // version and is left bound by streaming `in` and `out` (HBM). W's three
 // planes sit in shared memory pre-arranged as per-lane B fragments; the input
-// tile [K][TD] is double-buffered with cp.async; warp w owns m-tiles 2w and
-// 2w + 1 (8 b2 values each). Summation order per output: k ascending in
-// chunks of 4 (DMMA), fixed -> deterministic.
+// tile [K][TD] is double-buffered with cp.async; warp w owns m-tile w (8 b2
+// values). Summation order per output: k ascending in chunks of 4 (DMMA),
+// fixed -> deterministic.
 // ---------------------------------------------------------------------------
-constexpr int TD = 128;   // b2 values per tile (16 m-tiles of 8; 2 per warp)
-
-template <int KS, int NTL>
+template <int KS, int NTL, int MT>
 __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant__ SkinnyProblem a, int64_t ntiles) {
+  constexpr int TD = 8 * (NTH / 32) * MT;   // b2 values per tile: MT m-tiles of 8 per warp
   extern __shared__ __align__(16) char sm[];
   const int K = a.K, N = a.N;
   double *sWf = reinterpret_cast<double *>(sm);                        // [KS][NTL][3][32]
-  double2 *sIn = reinterpret_cast<double2 *>(sWf + KS * NTL * 3 * 32);  // [2][K][TD]
+  const int KN = K > N ? K : N;                                        // buffer rows: input [K] / output [N]
+  double2 *sIn = reinterpret_cast<double2 *>(sWf + KS * NTL * 3 * 32);  // [2][KN][TD]
   const double2 *W = reinterpret_cast<const double2 *>(a.W);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < KS * NTL * 32; i += NTH) {
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant_
     double2 *out;
     int nc;
     tile_ptrs(t, in, out, nc);
-    double2 *dst = sIn + buf * K * TD;
+    double2 *dst = sIn + buf * KN * TD;
     for (int i = tid; i < K * TD; i += NTH) {
       const int k = i / TD, c = i % TD;
       cp_async_zfill<16>(dst + k * TD + c, c < nc ? in + a.in_koff[k] + c : in, c < nc ? 16 : 0);
@@ -327,14 +327,14 @@ __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant_
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double2 *tile = sIn + buf * K * TD;
+    const double2 *tile = sIn + buf * KN * TD;
     const double2 *in;
     double2 *out;
     int nc;
     tile_ptrs(t, in, out, nc);
-    double P[2][NTL][2], Q[2][NTL][2], S[2][NTL][2];
+    double P[MT][NTL][2], Q[MT][NTL][2], S[MT][NTL][2];
 #pragma unroll
-    for (int m = 0; m < 2; m++)
+    for (int m = 0; m < MT; m++)
 #pragma unroll
       for (int nt = 0; nt < NTL; nt++)
 #pragma unroll
@@ -342,10 +342,10 @@ __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant_
 #pragma unroll
     for (int ks = 0; ks < KS; ks++) {
       const int k = ks * 4 + q;
-      double ar[2], ai[2], as[2];
+      double ar[MT], ai[MT], as[MT];
 #pragma unroll
-      for (int m = 0; m < 2; m++) {
-        const double2 x = k < K ? tile[k * TD + (warp * 2 + m) * 8 + r] : make_double2(0.0, 0.0);
+      for (int m = 0; m < MT; m++) {
+        const double2 x = k < K ? tile[k * TD + (warp * MT + m) * 8 + r] : make_double2(0.0, 0.0);
         ar[m] = x.x;
         ai[m] = x.y;
         as[m] = x.x + x.y;
@@ -355,17 +355,19 @@ __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant_
         const double *wf = sWf + ((ks * NTL + nt) * 3) * 32 + lane;
         const double wr = wf[0], wi = wf[32], ws = wf[64];
 #pragma unroll
-        for (int m = 0; m < 2; m++) {
+        for (int m = 0; m < MT; m++) {
           dmma884(P[m][nt], ar[m], wr);
           dmma884(Q[m][nt], ai[m], wi);
           dmma884(S[m][nt], as[m], ws);
         }
       }
     }
-    // C fragment: row r (b2), columns n = nt*8 + 2q + e
+    // C fragment: row r (b2), columns n = nt*8 + 2q + e, stored from registers
+    // (staging through shared memory for contiguous warp stores measured slower:
+    // 2.92 vs 2.60 ms at the target, the extra barriers cost more than L2 merging)
 #pragma unroll
-    for (int m = 0; m < 2; m++) {
-      const int c = (warp * 2 + m) * 8 + r;
+    for (int m = 0; m < MT; m++) {
+      const int c = (warp * MT + m) * 8 + r;
       if (c < nc) {
 #pragma unroll
         for (int nt = 0; nt < NTL; nt++)
@@ -383,11 +385,12 @@ __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant_
   cp_async_wait<0>();
 }
 
-template <int KS, int NTL>
-cudaError_t launch_dmma_kn(const SkinnyProblem &p, cudaStream_t s) {
-  const size_t smem = (size_t)KS * NTL * 3 * 32 * 8 + 2 * (size_t)p.K * TD * 16;
+template <int KS, int NTL, int MT>
+cudaError_t launch_dmma_knm(const SkinnyProblem &p, cudaStream_t s) {
+  constexpr int TD = 8 * (NTH / 32) * MT;
+  const size_t smem = (size_t)KS * NTL * 3 * 32 * 8 + 2 * (size_t)std::max(p.K, p.N) * TD * 16;
   const int64_t ntiles = p.nb[0] * p.nb[1] * ((p.nb[2] + TD - 1) / TD);
-  auto k = skinny_dmma_kernel<KS, NTL>;
+  auto k = skinny_dmma_kernel<KS, NTL, MT>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -395,6 +398,11 @@ cudaError_t launch_dmma_kn(const SkinnyProblem &p, cudaStream_t s) {
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)148 * std::max(1, per_sm));
   k<<<(unsigned)grid, NTH, smem, s>>>(p, ntiles);
   return cudaGetLastError();
+}
+
+template <int KS, int NTL>
+cudaError_t launch_dmma_kn(const SkinnyProblem &p, cudaStream_t s) {
+  return launch_dmma_knm<KS, NTL, 1>(p, s);   // one m-tile per warp: 2.60 ms vs 2.70 (two) at the target
 }
 
 template <int KS>

@@ -230,7 +230,7 @@ __device__ void gram_pass(RoundSmem<C> &sm, const typename Cx<C>::E *X, int64_t 
 // re-orthonormalisation), then A = G^H with the eigenpairs of the first nreal
 // rows in descending eigenvalue order (ties by index). A aliases H.
 template <bool C>
-__device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_inner, int sort,
+__device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_inner, int sort, double zfloor2,
                           unsigned long long *prof = nullptr) {
   using E = typename Cx<C>::E;
   const int tid = threadIdx.x;
@@ -255,7 +255,10 @@ __device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_in
         // c^2 + s^2 > 1 bias grows the row norms
         // pairs with a numerically zero row (R29) are left alone: the row is
         // completed at the end
-        if (ah == 0.0 || ah <= tol_in * sqrt(fabs(hi)) * sqrt(fabs(hj)) || negligible(hi, hj)) {
+        // rows at or below the noise floor (zfloor2, squared norm) are frozen:
+        // their directions are rounding noise, completed at the end (R29)
+        if (ah == 0.0 || ah <= tol_in * sqrt(fabs(hi)) * sqrt(fabs(hj)) || negligible(hi, hj) ||
+            fmin(hi, hj) <= zfloor2) {
           sm.rflag[tid] = 0;
         } else {
           // real symmetric [[hi, |h|], [|h|, hj]] (after the phase) -> R = [[c, s], [-s, c]]
@@ -466,7 +469,7 @@ if (!prologue_done) update_prologue<C>(sm, X, ld, c0, c1, row_lo, row_hi);
 template <bool C>
 __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, int64_t ldx, typename Cx<C>::E *Y,
                                                           int64_t ldy, int nb, int64_t n, int round, double tol,
-                                                          double tol_in, int max_inner,
+                                                          double tol_in, int max_inner, double zfloor2,
                                                           unsigned long long *offmax, unsigned long long *prof) {
   using E = typename Cx<C>::E;
   constexpr int CW = Cx<C>::CW;
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, 
     const int i = idx / PR, j = idx % PR;
     if (i < j) {
       const double di = re(sm.H[i][i]), dj = re(sm.H[j][j]);
-      if (di > 0.0 && dj > 0.0 && !negligible(di, dj)) off = fmax(off, cabs(sm.H[i][j]) / sqrt(di * dj));
+      if (di > zfloor2 && dj > zfloor2 && !negligible(di, dj)) off = fmax(off, cabs(sm.H[i][j]) / sqrt(di * dj));
     }
   }
 #pragma unroll
@@ -537,7 +540,7 @@ __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, 
   long long tp1 = 0;
   if (prof && threadIdx.x == 0) tp1 = clock64();
   block_eig<C>(sm, lo_real < SB ? (int)lo_real : SB + (int)hi_real, tol_in, max_inner & 0xff, (max_inner >> 8) & 1,
-               prof);
+               zfloor2, prof);
   long long tp2 = 0;
   if (prof && threadIdx.x == 0) {
     tp2 = clock64();
@@ -807,12 +810,12 @@ cudaError_t launch_svd_round(const SvdProblem &p, int round, double tol, double 
     auto k = svd_round_kernel<true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     e = cudaLaunchKernelEx(&cfg, k, static_cast<double2 *>(p.X), p.ldx, static_cast<double2 *>(p.Y), p.ldy, nb,
-                           p.n, round, tol, tol_in, max_inner, p.offmax, p.prof);
+                           p.n, round, tol, tol_in, max_inner, p.zfloor2, p.offmax, p.prof);
   } else {
     auto k = svd_round_kernel<false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     e = cudaLaunchKernelEx(&cfg, k, static_cast<double *>(p.X), p.ldx, static_cast<double *>(p.Y), p.ldy, nb, p.n,
-                           round, tol, tol_in, max_inner, p.offmax, p.prof);
+                           round, tol, tol_in, max_inner, p.zfloor2, p.offmax, p.prof);
   }
   (*launches)++;
   if (e != cudaSuccess) return e;

@@ -228,6 +228,9 @@ struct SvdProblem {
   double *s;             // npad row norms
   unsigned long long *offmax;   // sweep maximum of the off-diagonal measure (double bits)
   unsigned long long *prof = nullptr;   // optional phase clocks (gram, eig, X, Y, rotated pairs)
+  // noise floor (squared row norm): rows at or below it are neither rotated
+  // nor counted in the convergence measure; their vectors are completed
+  double zfloor2 = 0.0;
 };
 size_t svd_round_smem_bytes(bool cplx);
 cudaError_t launch_svd_load(const SvdProblem &p, const void *A, int64_t I, int64_t J, cudaStream_t s,

@@ -490,6 +490,23 @@ def test_mps_overlap_single_kernel(ctx, oracle_mod):
     assert e.value.code == 1
 
 
+@pytest.mark.parametrize("dt", ["c128", "r64"])
+def test_skinny_pass_shapes(ctx, oracle_mod, dt):
+    """The skinny pass over a unit-stride batch leg (the MPO-pass shape; complex
+    K, N <= 32 runs on the DMMA kernel, 3M, in 4-k x 8-n fragments): every
+    fragment boundary of K and N, a batch leg ragged against the 64-value tile,
+    through contract's skinny route."""
+    for K in (1, 3, 4, 5, 8, 13, 20, 32):
+        for N in (1, 2, 7, 8, 9, 20, 24, 32):
+            X = synth.random_tensor((3, K, 200), dt, 440 + K, 1)
+            W = synth.random_tensor((K, N), dt, 440 + N, 2)
+            got = ctx.contract(dev(X), "akc", dev(W), "kn", "anc")
+            ref = oracle_mod.contract(X.numpy(), "akc", W.numpy(), "kn", "anc")
+            assert rel_frob(host(got), ref) <= 1e-12, (K, N)
+            got2 = ctx.contract(dev(X), "akc", dev(W), "kn", "anc")
+            assert torch.equal(got, got2)                       # deterministic
+
+
 def test_mps_mpo_apply(ctx, oracle_mod):
     A = synth.random_tensor((40, 2, 33), "c128", 420, 1)
     I = torch.eye(2, dtype=torch.complex128).reshape(1, 1, 2, 2)

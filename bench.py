@@ -262,7 +262,13 @@ def run_tci(args):
                 allo = [None] * ws
                 dist.all_gather_object(allo, obj)
                 return allo
-            sh = PeerGatherHeff(ctx, L, W1, W2, R, ws, rank, exchange=exchange)
+
+            def agree(ok):
+                import torch.distributed as dist
+                t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                return bool(t.item())
+            sh = PeerGatherHeff(ctx, L, W1, W2, R, ws, rank, exchange=exchange, agree=agree)
         except Exception as e:   # no P2P / IPC on this box: NCCL all-gather instead
             print(f"[rank {rank}] peer-memory gather unavailable ({e}); using NCCL", file=sys.stderr, flush=True)
             sh = None

@@ -83,11 +83,14 @@ class PeerGatherHeff:
     over NVLink), with a flag barrier around the step -- no collective call.
 
     exchange(obj) -> [obj of rank 0, ..., obj of rank P-1] (e.g. a wrapper of
-    torch.distributed.all_gather_object). `peers` = (full_ptrs, flag_ptrs)
-    bypasses IPC (single-process emulation of several ranks in tests)."""
+    torch.distributed.all_gather_object); agree(ok) -> True iff every rank
+    passed ok=True (an all-reduce MIN), so a failure on one rank makes every
+    rank raise at the same point instead of leaving the others blocked in a
+    collective. `peers` = (full_ptrs, flag_ptrs) bypasses IPC (single-process
+    emulation of several ranks in tests)."""
 
     def __init__(self, ctx, L_slice, W1, W2, R, world: int, rank: int, exchange=None, peers=None, full=None,
-                 flags=None):
+                 flags=None, agree=None):
         import torch
         import paper_2512_23917_b200 as tci
         self.ctx, self.world, self.rank = ctx, world, rank
@@ -102,9 +105,31 @@ class PeerGatherHeff:
             if peers is None:
                 if exchange is None:
                     raise ValueError("PeerGatherHeff needs exchange() (or peers) for world > 1")
-                mine = (tci.tci_ipc_handle(self.full.data_ptr()), tci.tci_ipc_handle(self.flags.data_ptr()))
-                fulls, flg, self._opened = peer_pointer_table(
-                    rank, exchange(mine), (self.full.data_ptr(), self.flags.data_ptr()), tci.tci_ipc_open)
+                agree = agree or (lambda ok: ok)
+                try:
+                    mine, err = (tci.tci_ipc_handle(self.full.data_ptr()),
+                                 tci.tci_ipc_handle(self.flags.data_ptr())), None
+                except Exception as e:   # noqa: BLE001 -- reported after the agreement
+                    mine, err = None, e
+                if not agree(mine is not None):
+                    raise RuntimeError(f"peer gather: IPC export failed on some rank ({err})")
+                allh = exchange(mine)
+                opened = []
+
+                def opener(h, off):
+                    ptr = tci.tci_ipc_open(h, off)
+                    opened.append(ptr)
+                    return ptr
+                try:
+                    fulls, flg, _ = peer_pointer_table(rank, allh, (self.full.data_ptr(), self.flags.data_ptr()),
+                                                       opener)
+                    err = None
+                except Exception as e:   # noqa: BLE001
+                    err = e
+                self._opened = opened
+                if not agree(err is None):
+                    self.close()
+                    raise RuntimeError(f"peer gather: IPC mapping failed on some rank ({err})")
             else:
                 fulls, flg = peers
             ctx.gather_register(world, rank, fulls, flg)

@@ -122,3 +122,67 @@ def test_peer_gather_handle_exchange_gloo_world3():
                 assert fulls[i] == (1 << 40) + i * (1 << 32) + 4096 * i
                 assert flags[i] == (1 << 40) + i * (1 << 32) + (1 << 20) + 64 * i
         assert sorted(op) == sorted(opened) and len(op) == 2 * (world - 1)
+
+
+def _agree_worker(rank, world, port, q, fail_stage):
+    """PeerGatherHeff setup when one rank fails (IPC export or mapping): every
+    rank must raise at the same point (agreement by all-reduce MIN) instead of
+    leaving the others blocked in the handle exchange; mapped handles are closed."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2512_23917_b200 as tci
+        from paper_2512_23917_b200.sharding import PeerGatherHeff
+        closed = []
+
+        def fake_handle(ptr):
+            if fail_stage == "export" and rank == 1:
+                raise RuntimeError("no IPC on this rank")
+            return (b"H%d" % rank + bytes(62), 0)
+
+        def fake_open(h, off):
+            if fail_stage == "map" and rank == 1:
+                raise RuntimeError("cannot map")
+            return 4096 + int(h[1:2].decode())
+        tci.tci_ipc_handle, tci.tci_ipc_open = fake_handle, fake_open
+        tci.tci_ipc_close = lambda p: closed.append(p)
+
+        def exchange(obj):
+            allo = [None] * world
+            dist.all_gather_object(allo, obj)
+            return allo
+
+        def agree(ok):
+            t = torch.tensor([1 if ok else 0], dtype=torch.int32)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            return bool(t.item())
+        L = torch.zeros(4, 2, 3, dtype=torch.complex128)
+        W = torch.zeros(2, 2, 2, 2, dtype=torch.complex128)
+        R = torch.zeros(4, 2, 4, dtype=torch.complex128)
+        try:
+            PeerGatherHeff(None, L, W, W, R, world, rank, exchange=exchange, agree=agree)
+            q.put((rank, "no error", closed))
+        except RuntimeError as e:
+            q.put((rank, str(e), closed))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("stage", ["export", "map"])
+def test_peer_gather_setup_failure_agreement_gloo(stage):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 2, port, q, stage)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0, "a rank hung or crashed"
+    res = dict((r, (msg, closed)) for r, msg, closed in (q.get(timeout=10) for _ in range(2)))
+    word = "export" if stage == "export" else "mapping"
+    assert all(word in res[r][0] for r in (0, 1)), res
+    if stage == "map":
+        assert res[0][1] == [4097] * 2 and res[1][1] == []    # rank 0 unmapped what it had opened

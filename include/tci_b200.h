@@ -173,6 +173,19 @@ TCI_API tci_status_t tci_size_bytes(tci_ctx_t ctx, tci_tensor_t t, int64_t *byte
  * host or device memory (cudaMemcpyAsync). Used for end-to-end host I/O. */
 TCI_API tci_status_t tci_copy(tci_ctx_t ctx, tci_tensor_t src, tci_tensor_t dst);
 
+/* Asynchronous lanes (the asynchronous API the paper defers to a later
+ * revision): lane 0 is the context stream (every compute call),
+ * lanes 1 and 2 are library-owned copy streams (host -> device and device ->
+ * host traffic, so both PCIe directions and the compute can run at once).
+ * tci_copy_async enqueues tci_copy's copy on `lane`; tci_lane_record records
+ * event `slot` (0..15) on `lane`; tci_lane_wait makes `lane` wait for the
+ * last record of `slot` (on any lane). With these a caller double-buffers
+ * device inputs: the copies of step i+1 run while step i computes.
+ * Errors: OUT_OF_RANGE (lane, slot), as tci_copy, CUDA. */
+TCI_API tci_status_t tci_copy_async(tci_ctx_t ctx, tci_tensor_t src, tci_tensor_t dst, int lane);
+TCI_API tci_status_t tci_lane_record(tci_ctx_t ctx, int lane, int slot);
+TCI_API tci_status_t tci_lane_wait(tci_ctx_t ctx, int lane, int slot);
+
 /* ---------------------------------------------------------------------- */
 /* Manipulation: reshape and transpose (Eq. (1)) */
 /* ---------------------------------------------------------------------- */

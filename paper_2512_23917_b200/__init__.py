@@ -51,7 +51,7 @@ EXPORTED = [
     "tci_svd_workspace_size", "tci_svd", "tci_trunc_svd", "tci_svd_info",
     "tci_mps_mpo_zipup_workspace_size", "tci_mps_mpo_zipup", "tci_heff_apply_staged",
     "tci_ipc_handle", "tci_ipc_open", "tci_ipc_close", "tci_gather_register", "tci_heff_apply_gather",
-    "tci_gather_status",
+    "tci_gather_status", "tci_copy_async", "tci_lane_record", "tci_lane_wait",
 ]
 
 
@@ -79,6 +79,9 @@ _sig = {
     "tci_size": ([_vp, _vp, _i64p], ctypes.c_int),
     "tci_size_bytes": ([_vp, _vp, _i64p], ctypes.c_int),
     "tci_copy": ([_vp, _vp, _vp], ctypes.c_int),
+    "tci_copy_async": ([_vp, _vp, _vp, ctypes.c_int], ctypes.c_int),
+    "tci_lane_record": ([_vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+    "tci_lane_wait": ([_vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "tci_reshape": ([_vp, _vp, ctypes.c_int, _i64p], ctypes.c_int),
     "tci_permute": ([_vp, _vp, _i32p, _vp], ctypes.c_int),
     "tci_contract_out_shape": ([_vp, _vp, _i32p, _vp, _i32p, ctypes.c_int, _i32p, _i64p], ctypes.c_int),
@@ -225,6 +228,18 @@ def tci_size_bytes(ctx: int, t: int) -> int:
 
 def tci_copy(ctx: int, src: int, dst: int) -> None:
     _ok(_lib.tci_copy(_vp(ctx), _vp(src), _vp(dst)), "tci_copy")
+
+
+def tci_copy_async(ctx: int, src: int, dst: int, lane: int) -> None:
+    _ok(_lib.tci_copy_async(_vp(ctx), _vp(src), _vp(dst), int(lane)), "tci_copy_async")
+
+
+def tci_lane_record(ctx: int, lane: int, slot: int) -> None:
+    _ok(_lib.tci_lane_record(_vp(ctx), int(lane), int(slot)), "tci_lane_record")
+
+
+def tci_lane_wait(ctx: int, lane: int, slot: int) -> None:
+    _ok(_lib.tci_lane_wait(_vp(ctx), int(lane), int(slot)), "tci_lane_wait")
 
 
 def tci_reshape(ctx: int, t: int, new_shape: Sequence[int]) -> None:
@@ -757,6 +772,17 @@ class Context:
     def copy(self, src, dst):
         tci_copy(self.handle, self.tensor(src), self.tensor(dst))
         return dst
+
+    # asynchronous lanes: 0 = context stream, 1 = h2d copy lane, 2 = d2h copy lane
+    def copy_async(self, src, dst, lane: int):
+        tci_copy_async(self.handle, self.tensor(src), self.tensor(dst), lane)
+        return dst
+
+    def lane_record(self, lane: int, slot: int):
+        tci_lane_record(self.handle, lane, slot)
+
+    def lane_wait(self, lane: int, slot: int):
+        tci_lane_wait(self.handle, lane, slot)
 
     def comm_init(self, uid: bytes, nranks: int, rank: int):
         tci_comm_init(self.handle, uid, nranks, rank)

@@ -226,6 +226,8 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   c->host_scratch = nullptr;
   c->copy_stream = nullptr;
   for (auto &e : c->evs) e = nullptr;
+  c->d2h_stream = nullptr;
+  for (auto &e : c->lane_ev) e = nullptr;
   c->g_nranks = 1;
   c->g_rank = 0;
   for (int i = 0; i < 8; i++) c->g_full[i] = c->g_flags[i] = nullptr;
@@ -296,6 +298,16 @@ tci_status_t tci_destroy_context(tci_ctx_t ctx) {
     ctx->copy_stream = nullptr;
   }
   for (auto &e : ctx->evs)
+    if (e) {
+      cudaEventDestroy(e);
+      e = nullptr;
+    }
+  if (ctx->d2h_stream) {
+    cudaStreamSynchronize(ctx->d2h_stream);
+    cudaStreamDestroy(ctx->d2h_stream);
+    ctx->d2h_stream = nullptr;
+  }
+  for (auto &e : ctx->lane_ev)
     if (e) {
       cudaEventDestroy(e);
       e = nullptr;
@@ -470,6 +482,54 @@ tci_status_t tci_copy(tci_ctx_t ctx, tci_tensor_t src, tci_tensor_t dst) {
   if (view_of(src).size() != view_of(dst).size()) TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "copy: element counts differ");
   Verbose vb(ctx, "copy", {src, dst});
   TCI_CUDA_CHECK(cudaMemcpyAsync(dst->data, src->data, view_of(src).bytes(), cudaMemcpyDefault, ctx->stream));
+  return TCI_OK;
+}
+
+static tci_status_t lane_stream(tci_ctx_t ctx, int lane, cudaStream_t *s) {
+  if (lane < 0 || lane > 2) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "lane %d (0 context, 1 h2d, 2 d2h)", lane);
+  if (lane == 0) {
+    *s = ctx->stream;
+    return TCI_OK;
+  }
+  cudaStream_t &ls = lane == 1 ? ctx->copy_stream : ctx->d2h_stream;
+  if (!ls) {
+    TCI_CUDA_CHECK(cudaSetDevice(ctx->device));
+    TCI_CUDA_CHECK(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));
+  }
+  *s = ls;
+  return TCI_OK;
+}
+
+tci_status_t tci_copy_async(tci_ctx_t ctx, tci_tensor_t src, tci_tensor_t dst, int lane) {
+  CHECK(check_ctx(ctx));
+  CHECK(check_ten(ctx, src, false));
+  CHECK(check_ten(ctx, dst, false));
+  if (src->dtype != dst->dtype) TCI_FAIL(TCI_ERR_UNSUPPORTED, "copy: dtype mismatch");
+  if (view_of(src).size() != view_of(dst).size()) TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "copy: element counts differ");
+  cudaStream_t s;
+  CHECK(lane_stream(ctx, lane, &s));
+  Verbose vb(ctx, "copy_async", {src, dst});
+  TCI_CUDA_CHECK(cudaMemcpyAsync(dst->data, src->data, view_of(src).bytes(), cudaMemcpyDefault, s));
+  return TCI_OK;
+}
+
+tci_status_t tci_lane_record(tci_ctx_t ctx, int lane, int slot) {
+  CHECK(check_ctx(ctx));
+  if (slot < 0 || slot >= 16) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "slot %d (0..15)", slot);
+  cudaStream_t s;
+  CHECK(lane_stream(ctx, lane, &s));
+  if (!ctx->lane_ev[slot]) TCI_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->lane_ev[slot], cudaEventDisableTiming));
+  TCI_CUDA_CHECK(cudaEventRecord(ctx->lane_ev[slot], s));
+  return TCI_OK;
+}
+
+tci_status_t tci_lane_wait(tci_ctx_t ctx, int lane, int slot) {
+  CHECK(check_ctx(ctx));
+  if (slot < 0 || slot >= 16) TCI_FAIL(TCI_ERR_OUT_OF_RANGE, "slot %d (0..15)", slot);
+  cudaStream_t s;
+  CHECK(lane_stream(ctx, lane, &s));
+  if (!ctx->lane_ev[slot]) return TCI_OK;   // never recorded: nothing to wait for
+  TCI_CUDA_CHECK(cudaStreamWaitEvent(s, ctx->lane_ev[slot], 0));
   return TCI_OK;
 }
 

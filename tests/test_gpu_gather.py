@@ -113,3 +113,49 @@ def test_peer_gather_errors():
     x = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
     h, off = tci.tci_ipc_handle(x.data_ptr() + 4096)
     assert len(h) == 64 and off >= 4096
+
+
+def test_lanes_streaming_applies():
+    """tci_copy_async / tci_lane_record / tci_lane_wait: a stream of applies
+    with double-buffered device inputs (each step's inputs copied on lane 1
+    while the previous step computes, results copied out on lane 2) returns
+    exactly the per-step results of plain synchronous applies."""
+    ctx = tci.Context(0)
+    chi, steps = 48, 5
+    KEYS = ("L", "W1", "W2", "R", "psi")
+    hosts = [synth.heff_inputs(chi, 2, 5, "c128", 200 + i, "heisenberg") for i in range(steps)]
+    hosts = [{k: v.pin_memory() for k, v in h.items()} for h in hosts]
+    refs = [ctx.heff_apply(*(h[k].cuda() for k in KEYS)).cpu() for h in hosts]
+    bufs = [{k: torch.empty_like(v, device="cuda") for k, v in hosts[0].items()} for _ in range(2)]
+    outs = [torch.empty(chi, 2, 2, chi, dtype=torch.complex128, device="cuda") for _ in range(2)]
+    houts = [torch.empty(chi, 2, 2, chi, dtype=torch.complex128).pin_memory() for _ in range(steps)]
+    IN, DONE, OUT = 0, 2, 4
+
+    def load(i, b):
+        ctx.lane_wait(1, DONE + b)
+        for k in KEYS:
+            ctx.copy_async(hosts[i][k], bufs[b][k], 1)
+        ctx.lane_record(1, IN + b)
+    torch.cuda.synchronize()
+    load(0, 0)
+    for i in range(steps):
+        b = i % 2
+        if i + 1 < steps:
+            load(i + 1, 1 - b)
+        ctx.lane_wait(0, IN + b)
+        ctx.lane_wait(0, OUT + b)
+        ctx.heff_apply(*(bufs[b][k] for k in KEYS), out=outs[b])
+        ctx.lane_record(0, DONE + b)
+        ctx.lane_wait(2, DONE + b)
+        ctx.copy_async(outs[b], houts[i], 2)
+        ctx.lane_record(2, OUT + b)
+    ctx.lane_wait(0, OUT + (steps - 1) % 2)
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    for i in range(steps):
+        assert torch.equal(houts[i], refs[i]), f"step {i}"
+    with pytest.raises(tci.TciError):
+        ctx.lane_record(3, 0)
+    with pytest.raises(tci.TciError):
+        ctx.lane_wait(0, 16)
+    ctx.close()

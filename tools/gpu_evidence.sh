@@ -21,7 +21,7 @@ cap gemm4_int8 device_kernel 4
 cap crt '^crt_kernel' 0
 cap residues '^residues$' 0
 cap residues_t '^residues_t$' 0
-cap skinny_stream '^skinny_stream_kernel' 0
+cap skinny_dmma '^skinny_dmma_kernel' 0
 cap line_exponent '^line_exponent$' 0
 timeout 300 python tools/bench_extra.py --only permute --out gpurun_out/extra_permute.json > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:permute_groups -c 1 \

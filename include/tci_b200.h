@@ -288,6 +288,14 @@ TCI_API tci_status_t tci_tebd_theta(tci_ctx_t ctx, tci_tensor_t A, const char *l
                             tci_tensor_t U, const char *lu,
                             tci_tensor_t theta, const char *lt);
 
+/* Scratch bytes tci_tebd_theta needs for these operands under the context's
+ * GEMM algorithm (0 for the fused DMMA gate epilogue; the intermediate A.B +
+ * the contraction's scratch otherwise, incl. the Ozaki residue planes).
+ * Reads only descriptors. Errors: as tci_tebd_theta's validation. */
+TCI_API tci_status_t tci_tebd_workspace_size(tci_ctx_t ctx, tci_tensor_t A, const char *la, tci_tensor_t B,
+                                             const char *lb, tci_tensor_t U, const char *lu, tci_tensor_t theta,
+                                             const char *lt, size_t *bytes);
+
 /* Environment update (R28): the DMRG step before
  * every H_eff, with the index conventions of tci_heff_apply (E[ket bond, MPO
  * bond, bra bond]; W[w_left, w_right, s = ket physical, t = bra physical]):

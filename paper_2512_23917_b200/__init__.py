@@ -51,7 +51,7 @@ EXPORTED = [
     "tci_svd_workspace_size", "tci_svd", "tci_trunc_svd", "tci_svd_info",
     "tci_mps_mpo_zipup_workspace_size", "tci_mps_mpo_zipup", "tci_heff_apply_staged",
     "tci_ipc_handle", "tci_ipc_open", "tci_ipc_close", "tci_gather_register", "tci_heff_apply_gather",
-    "tci_gather_status", "tci_copy_async", "tci_lane_record", "tci_lane_wait",
+    "tci_gather_status", "tci_tebd_workspace_size", "tci_copy_async", "tci_lane_record", "tci_lane_wait",
 ]
 
 
@@ -80,6 +80,8 @@ _sig = {
     "tci_size_bytes": ([_vp, _vp, _i64p], ctypes.c_int),
     "tci_copy": ([_vp, _vp, _vp], ctypes.c_int),
     "tci_copy_async": ([_vp, _vp, _vp, ctypes.c_int], ctypes.c_int),
+    "tci_tebd_workspace_size": ([_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp,
+                                 ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "tci_lane_record": ([_vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "tci_lane_wait": ([_vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "tci_reshape": ([_vp, _vp, ctypes.c_int, _i64p], ctypes.c_int),
@@ -228,6 +230,14 @@ def tci_size_bytes(ctx: int, t: int) -> int:
 
 def tci_copy(ctx: int, src: int, dst: int) -> None:
     _ok(_lib.tci_copy(_vp(ctx), _vp(src), _vp(dst)), "tci_copy")
+
+
+def tci_tebd_workspace_size(ctx: int, A: int, la: str, B: int, lb: str, U: int, lu: str, T: int, lt: str) -> int:
+    n = ctypes.c_size_t()
+    _ok(_lib.tci_tebd_workspace_size(_vp(ctx), _vp(A), la.encode("latin-1"), _vp(B), lb.encode("latin-1"), _vp(U),
+                                     lu.encode("latin-1"), _vp(T), lt.encode("latin-1"), ctypes.byref(n)),
+        "tci_tebd_workspace_size")
+    return n.value
 
 
 def tci_copy_async(ctx: int, src: int, dst: int, lane: int) -> None:
@@ -652,9 +662,8 @@ class Context:
                 for ch, n in zip(l, t.shape):
                     dims[ch] = n
             out = self.torch.empty([dims[ch] for ch in lt], dtype=A.dtype, device=A.device)
-        # workspace: intermediate A.B (+ contract scratch, bounded by A.B again)
-        ab = A.numel() * B.numel() // max(1, min(A.shape[la.index(ch)] for ch in la if ch in lb)) ** 2
-        self.ensure_workspace(int(2 * ab * A.element_size() + 4096))
+        self.ensure_workspace(tci_tebd_workspace_size(self.handle, self.tensor(A), la, self.tensor(B), lb,
+                                                      self.tensor(U), lu, self.tensor(out), lt))
         tci_tebd_theta(self.handle, self.tensor(A), la, self.tensor(B), lb, self.tensor(U), lu,
                        self.tensor(out), lt)
         return out

@@ -848,6 +848,16 @@ tci_status_t tci_tebd_theta(tci_ctx_t ctx, tci_tensor_t A, const char *la, tci_t
   return tebd_exec(ctx, view_of(A), la, view_of(B), lb, view_of(U), lu, view_of(theta), lt);
 }
 
+tci_status_t tci_tebd_workspace_size(tci_ctx_t ctx, tci_tensor_t A, const char *la, tci_tensor_t B,
+                                     const char *lb, tci_tensor_t U, const char *lu, tci_tensor_t theta,
+                                     const char *lt, size_t *bytes) {
+  CHECK(check_ctx(ctx));
+  for (tci_tensor_t t : {A, B, U, theta}) CHECK(check_ten(ctx, t, false));
+  if (!la || !lb || !lu || !lt) TCI_FAIL(TCI_ERR_PARSE, "tebd: NULL label string");
+  if (!bytes) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL out");
+  return tebd_exec(ctx, view_of(A), la, view_of(B), lb, view_of(U), lu, view_of(theta), lt, bytes);
+}
+
 tci_status_t tci_mps_overlap(tci_ctx_t ctx, int n, const tci_tensor_t *bra, const tci_tensor_t *ket,
                              tci_tensor_t out) {
   CHECK(check_ctx(ctx));

@@ -518,7 +518,8 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
 // TEBD theta = (A.B).U (R16)
 // ---------------------------------------------------------------------------
 tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View &B, const char *lb,
-                       const View &U, const char *lu, const View &T, const char *lt) {
+                       const View &U, const char *lu, const View &T, const char *lt, size_t *ws_query) {
+  if (ws_query) *ws_query = 0;
   const tci_dtype_t dt = A.dtype;
   if (B.dtype != dt || U.dtype != dt || T.dtype != dt)
     TCI_FAIL(TCI_ERR_UNSUPPORTED, "tebd: all operands must share one dtype");
@@ -593,7 +594,10 @@ tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View
     tp.t_q = stride_of(ilt, T.shape, 4, pq[1]); tp.t_c = stride_of(ilt, T.shape, 4, c);
     const bool dims_ok = U.shape[0] == 2 && U.shape[1] == 2 && U.shape[2] == 2 && U.shape[3] == 2 &&
                          A.shape[strchr(la, s) - la] == 2 && B.shape[strchr(lb, t) - lb] == 2;
-    if (dt == TCI_R64 && dims_ok && tebd_fused_supported(tp)) return run_tebd(ctx, tp);
+    // (with the Ozaki algorithm selected, A.B runs as a real Ozaki GEMM and the
+    // gate as the skinny pass below; the fused epilogue is a DMMA kernel)
+    if (dt == TCI_R64 && dims_ok && ctx->zgemm_algo != kZOzaki && tebd_fused_supported(tp))
+      return ws_query ? TCI_OK : run_tebd(ctx, tp);
   }
   View AB;
   AB.dtype = dt;
@@ -623,6 +627,10 @@ tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View
   const int64_t dp = U.shape[pos(ilu, 4, pq[0])], dq = U.shape[pos(ilu, 4, pq[1])];
   if (ds * dtt > kSkinnyMaxK || dp * dq > kSkinnyMaxN || skinny_smem_bytes((int)(ds * dtt), (int)(dp * dq), es) > 200 * 1024)
     TCI_FAIL(TCI_ERR_UNSUPPORTED, "tebd: physical dimension too large for the gate kernel");
+  if (ws_query) {
+    *ws_query = ab_bytes + need_c;
+    return TCI_OK;
+  }
   if (ab_bytes + need_c > ctx->ws_bytes || !ctx->ws)
     TCI_FAIL(TCI_ERR_WORKSPACE, "tebd needs %zu bytes of workspace, %zu attached", ab_bytes + need_c,
              ctx->ws_bytes);

@@ -350,7 +350,11 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
     int bm, bn;
     gemm_tile(a.dtype, &bm, &bn);
     const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
-    if (tiles < 2 * 148 && K >= 256) {
+    // (not when the GEMM goes to the INT8 tensor cores: its 3n / n residue
+    // GEMMs of one launch fill the machine by themselves)
+    const bool oz_candidate = (a.dtype == TCI_C128 || a.dtype == TCI_R64) && ctx->zgemm_algo == kZOzaki &&
+                              ozaki_worthwhile(M, N, K);
+    if (tiles < 2 * 148 && K >= 256 && !oz_candidate) {
       int64_t S = std::min<int64_t>({(4 * 148 + tiles - 1) / tiles, K / 128, 1024});
       if (S >= 2) {
         k_chunk = ((K + S - 1) / S + 15) / 16 * 16;
@@ -361,8 +365,9 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   }
   // complex128 GEMM algorithm
   int zalgo = ctx->zgemm_algo == kZOzaki ? kZ3M : ctx->zgemm_algo;
-  const bool use_ozaki = a.dtype == TCI_C128 && ctx->zgemm_algo == kZOzaki && splitk <= 1 &&
-                         ozaki_worthwhile(M, N, K);
+  // (float64 too: real Ozaki-II, one residue plane per modulus)
+  const bool use_ozaki = (a.dtype == TCI_C128 || a.dtype == TCI_R64) && ctx->zgemm_algo == kZOzaki &&
+                         splitk <= 1 && ozaki_worthwhile(M, N, K);
   // gamma-order scatter epilogue (8(a6)): an output that is not a [I,J] /
   // [J,I] block is written in place through row / column offset tables
   // instead of GEMM -> scratch -> permute; the GEMM is oriented so that the

@@ -673,6 +673,9 @@ static cudaError_t launch_gemm_main(const GemmProblem &p, cudaStream_t s, int64_
     if (p.zalgo == kZOzaki && p.splitk <= 1) return launch_ozaki_zgemm(p, p.oz_ws, p.oz_ws_bytes, s, launches);
     return p.zalgo == kZ4M ? run_z<Z4Cfg>(p, ak, bk, s, launches) : run_z<Z3Cfg>(p, ak, bk, s, launches);
   }
+  // float64 on the INT8 tensor cores (real Ozaki-II) when the caller chose it
+  if (p.zalgo == kZOzaki && p.splitk <= 1 && p.mode == 0 && !p.c_row)
+    return launch_ozaki_dgemm(p, p.oz_ws, p.oz_ws_bytes, s, launches);
   // float64: 16-byte chunks need 16-byte aligned rows
   const int64_t lda = ak ? p.a_sm : p.a_sk, ldb = bk ? p.b_sn : p.b_sk;
   const bool aligned = ((uintptr_t)p.A % 16 == 0) && ((uintptr_t)p.B % 16 == 0) &&

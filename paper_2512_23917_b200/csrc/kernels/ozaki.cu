@@ -570,6 +570,206 @@ unsigned inv_mod(unsigned a, unsigned m) {
   return (unsigned)(t < 0 ? t + (int)m : t);
 }
 
+// ===========================================================================
+// float64 (real) Ozaki-II: one residue plane per modulus (no 3M split), the
+// same scaling, moduli, INT8 GEMM + mod-m epilogue and CRT; n GEMMs instead
+// of 3n. C'(m, n) = sum_k A'(m, k) B'(k, n) with |C'| <= K 2^(2t) <= M/8.
+// ===========================================================================
+__global__ void __launch_bounds__(256) line_exponent_r(const double *base, int64_t nlines, int64_t K, int64_t s_l,
+                                                       int64_t s_k, int *E) {
+  if (s_k == 1) {
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nlines) return;
+    int e = -100000;
+    const double *p = base + warp * s_l;
+    for (int64_t k = lane; k < K; k += 32) e = max(e, exp_of(p[k]));
+    for (int o = 16; o; o >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if (lane == 0) E[warp] = e;
+  } else {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= nlines) return;
+    const int64_t kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc;
+    const int64_t k1 = min(K, k0 + kc);
+    int e = -100000;
+    const double *p = base + l * s_l;
+    for (int64_t k = k0; k < k1; k++) e = max(e, exp_of(p[k * s_k]));
+    atomicMax(E + l, e);
+  }
+}
+
+struct ResArgsR {
+  const double *base;
+  int64_t nlines, K, Kp, s_l, s_k;
+  int64_t line0, lines_out;
+  const int *E;
+  int t, nmod;
+  int8_t *out;
+  int64_t plane_stride;
+};
+
+// K-contiguous: 8 consecutive k of one line per thread, 8 bytes per plane
+__global__ void __launch_bounds__(256) residues_real(const __grid_constant__ ResArgsR a) {
+  const int64_t kgroups = a.Kp / 8;
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= a.lines_out * kgroups) return;
+  const int64_t row = gid / kgroups, k0 = (gid % kgroups) * 8, line = a.line0 + row;
+  double x[8];
+  int lo[8];
+  if (line < a.nlines && a.E[line] > -100000) {
+    double s2a, s2b;
+    line_scale(a.t, a.E[line], s2a, s2b);
+    const double *p = a.base + line * a.s_l;
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) v[j] = k0 + j < a.K ? __ldg(p + (k0 + j) * a.s_k) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const double m = scaled_magic(v[j], s2a, s2b);
+      x[j] = m - kMagic;
+      lo[j] = __double2loint(m);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      x[j] = 0.0;
+      lo[j] = 0;
+    }
+  }
+  int8_t *dst = a.out + row * a.Kp + k0;
+  for (int l = 0; l < a.nmod; l++) {
+    const int mi = c_moduli[l];
+    const double minv = c_minv[l];
+    int r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = bal_res(x[j], lo[j], minv, mi);
+    *reinterpret_cast<uint2 *>(dst + (int64_t)l * a.plane_stride) =
+        make_uint2(pack4(r[0], r[1], r[2], r[3]), pack4(r[4], r[5], r[6], r[7]));
+  }
+}
+
+// line-contiguous: 32-line x 64-k tile through shared memory (as residues_t)
+__global__ void __launch_bounds__(256) residues_real_t(const __grid_constant__ ResArgsR a) {
+  __shared__ double sx[32][65];
+  const int64_t ntk = a.Kp / 64;
+  const int64_t tl = blockIdx.x / ntk, tk = blockIdx.x % ntk;
+  const int64_t r0 = tl * 32, kb = tk * 64;
+  const int tid = threadIdx.x;
+  {
+    const int li = tid % 32;
+    const int64_t row = r0 + li, line = a.line0 + row;
+    const bool ok = row < a.lines_out && line < a.nlines && a.E[line] > -100000;
+    double s2a = 0.0, s2b = 0.0;
+    if (ok) line_scale(a.t, a.E[line], s2a, s2b);
+    double v[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; jj++) {
+      const int64_t k = kb + tid / 32 + jj * 8;
+      v[jj] = ok && k < a.K ? __ldg(a.base + line + k * a.s_k) : 0.0;
+    }
+#pragma unroll
+    for (int jj = 0; jj < 8; jj++) sx[li][tid / 32 + jj * 8] = scaled_magic(v[jj], s2a, s2b);
+  }
+  __syncthreads();
+  const int li = tid / 8, kq = (tid % 8) * 8;
+  const int64_t row = r0 + li;
+  if (row >= a.lines_out) return;
+  double x[8];
+  int lo[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const double m = sx[li][kq + j];
+    x[j] = m - kMagic;
+    lo[j] = __double2loint(m);
+  }
+  int8_t *dst = a.out + row * a.Kp + kb + kq;
+  for (int l = 0; l < a.nmod; l++) {
+    const int mi = c_moduli[l];
+    const double minv = c_minv[l];
+    int r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = bal_res(x[j], lo[j], minv, mi);
+    *reinterpret_cast<uint2 *>(dst + (int64_t)l * a.plane_stride) =
+        make_uint2(pack4(r[0], r[1], r[2], r[3]), pack4(r[4], r[5], r[6], r[7]));
+  }
+}
+
+__global__ void batch_moduli_r(int32_t *p, int planes) {
+  const int i = threadIdx.x;
+  if (i < planes) p[i] = c_moduli[i];
+}
+
+// CRT for real outputs: the residue of C' modulo m_l is the GEMM's byte in
+// [0, m_l) itself; 4 consecutive columns per thread (one 32-bit load per plane)
+struct CrtArgsR {
+  const uint8_t *D;          // [n][Mc][Np]
+  int64_t Mc, N, Np, m0;
+  int nmod;
+  double W[kMaxMod][4];
+  double Mch[4];
+  double Minv;
+  const int *EA, *EB;
+  int t;
+  double *C;
+  int64_t c_sm;
+};
+
+template <int NMOD, int NCH>
+__global__ void __launch_bounds__(256) crt_real_kernel(const __grid_constant__ CrtArgsR a) {
+  const int64_t q4 = a.Np / 4;
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= a.Mc * q4) return;
+  const int64_t r = gid / q4, n0 = (gid % q4) * 4;
+  const int64_t plane = a.Mc * a.Np;
+  double S[4][NCH];
+#pragma unroll
+  for (int e = 0; e < 4; e++)
+#pragma unroll
+    for (int j = 0; j < NCH; j++) S[e][j] = 0.0;
+#pragma unroll
+  for (int i = 0; i < NMOD; i++) {
+    const uint32_t w4 = __ldg(reinterpret_cast<const uint32_t *>(a.D + i * plane + r * a.Np + n0));
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const double c = (double)((w4 >> (8 * e)) & 0xffu);
+#pragma unroll
+      for (int j = 0; j < NCH; j++) S[e][j] = fma(c, a.W[i][j], S[e][j]);
+    }
+  }
+  const int64_t m = a.m0 + r;
+  const int ea = a.EA[m];
+#pragma unroll
+  for (int e = 0; e < 4; e++) {
+    const int64_t n = n0 + e;
+    if (n >= a.N) break;
+    const int eb = a.EB[n];
+    double out = 0.0;
+    if (ea > -100000 && eb > -100000) {
+      // crt_value over the real chunk sums (same reconstruction as the complex CRT)
+      const double two37 = 137438953472.0, inv37 = 1.0 / 137438953472.0;
+      double xe = S[e][NCH - 1];
+#pragma unroll
+      for (int j = NCH - 2; j >= 0; j--) xe = fma(xe, two37, S[e][j]);
+      const double q = rint(xe * a.Minv);
+      double rr[NCH];
+#pragma unroll
+      for (int j = 0; j < NCH; j++) rr[j] = fma(-q, a.Mch[j], S[e][j]);
+#pragma unroll
+      for (int j = 0; j < NCH - 1; j++) {
+        const double cy = rint(rr[j] * inv37);
+        rr[j] = fma(-cy, two37, rr[j]);
+        rr[j + 1] += cy;
+      }
+      double x = rr[NCH - 1];
+#pragma unroll
+      for (int j = NCH - 2; j >= 0; j--) x = fma(x, two37, rr[j]);
+      const int sc = -(2 * a.t - ea) + eb;
+      out = (sc >= -1022 && sc <= 1023) ? x * __hiloint2double((sc + 1023) << 20, 0) : ldexp(x, sc);
+    }
+    a.C[m * a.c_sm + n] = out;
+  }
+}
+
 }  // namespace
 
 void ozaki_params(int64_t K, int *nmod, int *t, const int **moduli) {
@@ -714,6 +914,131 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       default: return cudaErrorInvalidValue;
     }
     if (ce != cudaSuccess) return ce;
+    if (launches) ++*launches;
+    if (g.rows_done) g.rows_done(g.rows_user, m0, mc);
+  }
+  return cudaGetLastError();
+}
+
+// C = A B (float64) per GemmProblem strides by real Ozaki-II on INT8 tcgen05
+// (layout of ozaki_workspace_bytes: sized for 3n planes, n used here).
+cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
+                               int64_t *launches) {
+  if (g.M == 0 || g.N == 0) return cudaSuccess;
+  if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;
+  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows);
+  if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
+  char *w = static_cast<char *>(ws);
+  int *EA = reinterpret_cast<int *>(w + p.off_EA), *EB = reinterpret_cast<int *>(w + p.off_EB);
+  int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
+  uint8_t *D = reinterpret_cast<uint8_t *>(w + p.off_D);
+  int32_t *bmod = reinterpret_cast<int32_t *>(w + p.off_mod);
+  const double *A = static_cast<const double *>(g.A), *B = static_cast<const double *>(g.B);
+  auto exponents = [&](const double *X, int64_t nl, int64_t s_l, int64_t s_k, int *E) {
+    if (s_k == 1) {
+      line_exponent_r<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, s>>>(X, nl, g.K, s_l, s_k, E);
+      if (launches) ++*launches;
+    } else {
+      fill_int<<<(unsigned)std::min<int64_t>((nl + 255) / 256, 1024), 256, 0, s>>>(E, nl, -100000);
+      const int64_t ky = std::max<int64_t>(1, std::min<int64_t>((g.K + 127) / 128, 65535));
+      dim3 grid((unsigned)((nl + 255) / 256), (unsigned)ky);
+      line_exponent_r<<<grid, 256, 0, s>>>(X, nl, g.K, s_l, s_k, E);
+      if (launches) *launches += 2;
+    }
+  };
+  auto launch_res = [&](const ResArgsR &r) {
+    if (r.s_k == 1) {
+      const int64_t th = r.lines_out * (r.Kp / 8);
+      residues_real<<<(unsigned)((th + 255) / 256), 256, 0, s>>>(r);
+    } else {
+      residues_real_t<<<(unsigned)(((r.lines_out + 31) / 32) * (r.Kp / 64)), 256, 0, s>>>(r);
+    }
+    if (launches) ++*launches;
+  };
+  const int64_t a_sk = g.K == 1 ? 1 : g.a_sk, a_sm = g.a_sm;
+  const int64_t b_sk = g.b_sk, b_sn = g.N == 1 ? 1 : g.b_sn;
+  exponents(A, g.M, a_sm, a_sk, EA);
+  exponents(B, g.N, b_sn, b_sk, EB);
+  const int planes = p.nmod;
+  batch_moduli_r<<<1, 64, 0, s>>>(bmod, planes);
+  if (launches) ++*launches;
+  {
+    ResArgsR r{};
+    r.base = B; r.nlines = g.N; r.K = g.K; r.Kp = p.Kp; r.s_l = b_sn; r.s_k = b_sk;
+    r.line0 = 0; r.lines_out = p.Np; r.E = EB; r.t = p.t; r.nmod = p.nmod; r.out = Bres;
+    r.plane_stride = p.Np * p.Kp;
+    launch_res(r);
+  }
+  CrtArgsR c{};
+  {
+    u128 Mp = 1;
+    for (int l = 0; l < p.nmod; l++) Mp *= (u128)kModuli[l];
+    const u128 mask = ((u128)1 << 37) - 1;
+    for (int l = 0; l < p.nmod; l++) {
+      const unsigned ml = (unsigned)kModuli[l];
+      const u128 Ml = Mp / ml;
+      const u128 wl = mulmod_small(Ml, inv_mod((unsigned)(Ml % ml), ml), Mp);
+      for (int j = 0; j < 4; j++) c.W[l][j] = (double)(uint64_t)((wl >> (37 * j)) & mask);
+    }
+    for (int j = 0; j < 4; j++) c.Mch[j] = (double)(uint64_t)((Mp >> (37 * j)) & mask);
+    c.Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
+  }
+  c.nmod = p.nmod; c.EA = EA; c.EB = EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
+  c.C = static_cast<double *>(g.C); c.c_sm = g.c_sm;
+  for (int64_t ch = 0; ch < p.chunks; ch++) {
+    const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
+    {
+      ResArgsR r{};
+      r.base = A; r.nlines = g.M; r.K = g.K; r.Kp = p.Kp; r.s_l = a_sm; r.s_k = a_sk;
+      r.line0 = m0; r.lines_out = mc; r.E = EA; r.t = p.t; r.nmod = p.nmod; r.out = Ares;
+      r.plane_stride = mc * p.Kp;
+      launch_res(r);
+    }
+    {
+      using SA = typename I8Gemm::GemmKernel::StrideA;
+      using SB = typename I8Gemm::GemmKernel::StrideB;
+      using SC = typename I8Gemm::GemmKernel::StrideC;
+      using SD = typename I8Gemm::GemmKernel::StrideD;
+      const int Mi = (int)mc, Ni = (int)p.Np, Ki = (int)p.Kp, Li = planes;
+      SA sa = cutlass::make_cute_packed_stride(SA{}, {Mi, Ki, Li});
+      SB sb = cutlass::make_cute_packed_stride(SB{}, {Ni, Ki, Li});
+      SC sc = cutlass::make_cute_packed_stride(SC{}, {Mi, Ni, Li});
+      SD sd = cutlass::make_cute_packed_stride(SD{}, {Mi, Ni, Li});
+      typename ModEVT::Arguments fargs{{}, {{0}, {bmod}, {Stride<_0, _0, int64_t>{_0{}, _0{}, int64_t(1)}}}, {}};
+      typename I8Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {Mi, Ni, Ki, Li},
+                                      {Ares, sa, Bres, sb}, {fargs, nullptr, sc, D, sd}};
+      args.scheduler.max_swizzle_size = 8;
+      args.scheduler.raster_order = cutlass::gemm::kernel::detail::RasterOrderOptions::AlongM;
+      I8Gemm gemm;
+      if (gemm.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorNotSupported;
+      if (I8Gemm::get_workspace_size(args) > ((size_t)64 << 20)) return cudaErrorInvalidValue;
+      if (gemm.initialize(args, w + p.off_cutlass, s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
+      OzProf *pf = g.oz_prof;
+      const bool rec = pf && pf->n < 64;
+      if (rec) {
+        cudaEventCreate(&pf->a[pf->n]);
+        cudaEventCreate(&pf->b[pf->n]);
+        cudaEventRecord(pf->a[pf->n], s);
+      }
+      if (gemm.run(s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
+      if (rec) {
+        cudaEventRecord(pf->b[pf->n], s);
+        pf->ops[pf->n] = 2.0 * (double)Mi * Ni * Ki * Li;
+        pf->n++;
+      }
+      if (launches) ++*launches;
+    }
+    c.Mc = mc;
+    c.m0 = m0;
+    const int64_t th = mc * (p.Np / 4);
+    const unsigned blocks = (unsigned)((th + 255) / 256);
+    switch (p.nmod) {
+      case 12: crt_real_kernel<12, 3><<<blocks, 256, 0, s>>>(c); break;
+      case 13: crt_real_kernel<13, 3><<<blocks, 256, 0, s>>>(c); break;
+      case 14: crt_real_kernel<14, 3><<<blocks, 256, 0, s>>>(c); break;
+      case 15: crt_real_kernel<15, 4><<<blocks, 256, 0, s>>>(c); break;
+      default: return cudaErrorInvalidValue;
+    }
     if (launches) ++*launches;
     if (g.rows_done) g.rows_done(g.rows_user, m0, mc);
   }

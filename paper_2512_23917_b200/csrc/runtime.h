@@ -176,7 +176,7 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
                        const View &psi, const View &out, HeffStaging *stage = nullptr,
                        HeffGather *gather = nullptr);
 tci_status_t tebd_exec(tci_ctx_s *ctx, const View &A, const char *la, const View &B, const char *lb,
-                       const View &U, const char *lu, const View &T, const char *lt);
+                       const View &U, const char *lu, const View &T, const char *lt, size_t *ws_query = nullptr);
 
 // Environment updates (env.cpp)
 tci_status_t env_bytes(tci_ctx_s *ctx, int side, const View &E, const View &K, const View &W, const View &B,

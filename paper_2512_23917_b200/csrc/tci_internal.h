@@ -90,6 +90,9 @@ struct OzProf {
 };
 // Scratch of the Ozaki-II INT8 complex GEMM (ozaki.cu) for an M x N x K product.
 size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K);
+// float64 on the same scheme: one residue plane per modulus (ozaki.cu)
+cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
+                               int64_t *launches);
 cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
                                int64_t *launches);
 // Ozaki pays ~10 passes over the operands: use it only for big products.

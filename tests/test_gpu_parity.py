@@ -879,3 +879,49 @@ def test_heff_full_size_rows_and_freivalds(name, oracle_mod):
         assert rel_frob(got_rows, ref_rows) <= 1e-12
     finally:
         c.close()
+
+
+# ---------------------------------------------------------------------------
+# float64 on the INT8 tensor cores (real Ozaki-II: one residue plane per modulus)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("la,lb", [("mk", "kn"), ("km", "kn"), ("mk", "nk"), ("km", "nk")])
+def test_ozaki_real_contract_vs_dmma_and_oracle(ctx, ozctx, oracle_mod, la, lb):
+    """M = 1100, N = 1300, K = 3000 (4.3e9 MACs, ragged against every tile):
+    all four operand layouts (K-contiguous and line-contiguous residue
+    kernels), rows scaled by 2^(-30..30) and one zero row; per-row relative
+    error vs the DMMA GEMM and oracle rows <= 1e-12; the INT8 GEMM ran."""
+    M, N, K = 1100, 1300, 3000
+    rng = np.random.default_rng(6)
+    A = synth.random_tensor((M, K), "r64", 495, 1) * torch.from_numpy(2.0 ** rng.integers(-30, 30, size=(M, 1)))
+    A[17] = 0
+    B = synth.random_tensor((K, N), "r64", 495, 2)
+    At = A if la == "mk" else A.T.contiguous()
+    Bt = B if lb == "kn" else B.T.contiguous()
+    tci.tci_profile_enable(ozctx.handle, True)
+    c_oz = ozctx.contract(dev(At), la, dev(Bt), lb, "mn")
+    i8 = tci.tci_profile_query(ozctx.handle, tci.PROF_I8)
+    tci.tci_profile_enable(ozctx.handle, False)
+    assert i8["launches"] >= 1, "float64 Ozaki path not taken"
+    c_dm = ctx.contract(dev(At), la, dev(Bt), lb, "mn")
+    assert torch.count_nonzero(c_oz[17]).item() == 0
+    d = (c_oz - c_dm).pow(2).sum(1).sqrt() / c_dm.pow(2).sum(1).sqrt().clamp_min(1e-300)
+    d[17] = 0
+    assert d.max().item() <= 1e-12
+    rows = [0, 1, 550, M - 1]
+    ref = oracle_mod.contract(A.numpy()[rows], "mk", B.numpy(), "kn", "mn")
+    got = host(c_oz)[rows]
+    for i in range(len(rows)):
+        assert rel_frob(got[i], ref[i]) <= 1e-12
+    assert torch.equal(c_oz, ozctx.contract(dev(At), la, dev(Bt), lb, "mn"))     # deterministic
+
+
+def test_ozaki_real_tebd_theta(ozctx, oracle_mod):
+    """TEBD theta (chi = 1024, f64) with the Ozaki algorithm: A.B on the INT8
+    tensor cores, the gate by the skinny pass; sampled rows vs the oracle."""
+    c = synth.TEBD_CONFIG
+    inp = synth.tebd_inputs(1024, c["d"], c["dtype"], c["seed"], c["tau"])
+    th = ozctx.tebd_theta(dev(inp["A"]), "asb", dev(inp["B"]), "btc", dev(inp["U"]), "pqst", "apqc")
+    a_rows = [0, 511, 1023]
+    ref = oracle_mod.tebd_theta(inp["A"].numpy()[a_rows], inp["B"].numpy(), inp["U"].numpy())
+    assert rel_frob(host(th)[a_rows], ref) <= 1e-12

@@ -237,7 +237,7 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   c->svd_last_off = 0.0;
   {
     cudaError_t e1 = cudaMalloc(&c->dev_scratch, reduce_scratch_bytes());
-    cudaError_t e2 = cudaMallocHost(&c->host_scratch, 64);
+    cudaError_t e2 = cudaMallocHost(&c->host_scratch, 2 * kMaxMIOut * sizeof(double) + 64);
     if (e1 != cudaSuccess || e2 != cudaSuccess) {
       if (c->dev_scratch) cudaFree(c->dev_scratch);
       if (c->host_scratch) cudaFreeHost(c->host_scratch);

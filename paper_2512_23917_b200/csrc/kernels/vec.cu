@@ -15,7 +15,7 @@
 namespace tci {
 namespace {
 
-constexpr int RB = 296;   // reduction CTAs (2 per SM)
+constexpr int RB = kReduceBlocks;   // reduction CTAs (2 per SM)
 constexpr int RT = 256;
 
 // block-wide sum in a fixed tree order
@@ -79,6 +79,58 @@ __global__ void __launch_bounds__(RT) reduce_pass2(const double *part, int nb, d
   }
 }
 
+// Several inner products <v_i|w> (i < m <= kMaxMI) in one pass: w is read
+// once; each v_i's sum runs in exactly the order of reduce_pass1 / pass2 (same
+// grid, same per-thread sequence, same trees), so every result is bitwise the
+// single inner product's.
+struct MiArgs {
+  const double *v[kMaxMI];
+  int m;
+};
+
+template <bool CPLX>
+__global__ void __launch_bounds__(RT) multi_inner_pass1(const __grid_constant__ MiArgs a, const double *w,
+                                                        int64_t n_reals, int conj_a, double *part) {
+  __shared__ double sh[2][RT];
+  double acc[kMaxMI][2];
+#pragma unroll
+  for (int i = 0; i < kMaxMI; i++) acc[i][0] = acc[i][1] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * RT;
+  if (CPLX) {
+    const double2 *w2 = reinterpret_cast<const double2 *>(w);
+    const double sg = conj_a ? -1.0 : 1.0;
+    for (int64_t e = blockIdx.x * (int64_t)RT + threadIdx.x; e < n_reals / 2; e += stride) {
+      const double2 y = w2[e];
+#pragma unroll
+      for (int i = 0; i < kMaxMI; i++) {
+        if (i < a.m) {
+          const double2 x = reinterpret_cast<const double2 *>(a.v[i])[e];
+          acc[i][0] = fma(x.x, y.x, acc[i][0]);
+          acc[i][0] = fma(-sg * x.y, y.y, acc[i][0]);
+          acc[i][1] = fma(x.x, y.y, acc[i][1]);
+          acc[i][1] = fma(sg * x.y, y.x, acc[i][1]);
+        }
+      }
+    }
+  } else {
+    for (int64_t e = blockIdx.x * (int64_t)RT + threadIdx.x; e < n_reals; e += stride) {
+      const double y = w[e];
+#pragma unroll
+      for (int i = 0; i < kMaxMI; i++)
+        if (i < a.m) acc[i][0] = fma(a.v[i][e], y, acc[i][0]);
+    }
+  }
+  for (int i = 0; i < a.m; i++) {
+    double v[2] = {acc[i][0], acc[i][1]};
+    block_sum<2>(v, sh);
+    if (threadIdx.x == 0) {
+      part[(size_t)i * 2 * gridDim.x + 2 * blockIdx.x] = v[0];
+      part[(size_t)i * 2 * gridDim.x + 2 * blockIdx.x + 1] = v[1];
+    }
+    __syncthreads();
+  }
+}
+
 // out = sum_j c_j in_j over up to kMaxLC inputs (complex coefficients);
 // CPLX: elements are (re, im) pairs
 struct LcArgs {
@@ -125,7 +177,27 @@ cudaError_t launch_reduce(int mode, const double *a, const double *b, int64_t n_
   return cudaGetLastError();
 }
 
-size_t reduce_scratch_bytes() { return 2 * RB * sizeof(double) + 2 * sizeof(double); }
+// [multi-inner partials: kMaxMI x 2 RB][multi-inner results: 2 x kMaxMIOut][single partials 2 RB][single result 2]
+size_t reduce_scratch_bytes() {
+  return (2 * RB * kMaxMI + 2 * kMaxMIOut + 2 * RB + 2) * sizeof(double);
+}
+
+// <v_i|w> for i < m (any m <= kMaxMIOut) into out[2 i] (device, the
+// results region of the scratch), chunks of kMaxMI vectors per pass over w
+cudaError_t launch_multi_inner(bool cplx, const double *const *v, int m, const double *w, int64_t n_reals, int conj_a,
+                               double *scratch, double *out, cudaStream_t s, int64_t *launches) {
+  if (m > kMaxMIOut) return cudaErrorInvalidValue;
+  for (int i0 = 0; i0 < m; i0 += kMaxMI) {
+    MiArgs a{};
+    a.m = std::min(kMaxMI, m - i0);
+    for (int i = 0; i < a.m; i++) a.v[i] = v[i0 + i];
+    if (cplx) multi_inner_pass1<true><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, scratch);
+    else multi_inner_pass1<false><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, scratch);
+    for (int i = 0; i < a.m; i++) reduce_pass2<<<1, RT, 0, s>>>(scratch + (size_t)i * 2 * RB, RB, out + 2 * (i0 + i));
+    if (launches) *launches += 1 + a.m;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t launch_lincomb(bool cplx, const double *const *in, const double *cr, const double *ci, int m,
                            double *out, int64_t n, cudaStream_t s, int64_t *launches) {

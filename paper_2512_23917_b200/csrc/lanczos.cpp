@@ -30,8 +30,8 @@ static tci_status_t vec_check(const View &v) {
 static int64_t n_reals(const View &v) { return v.size() * (v.dtype == TCI_C128 ? 2 : 1); }
 
 tci_status_t vec_reduce(tci_ctx_s *ctx, int mode, const View &a, const View *b, int conj_a, double out[2]) {
-  double *part = static_cast<double *>(ctx->dev_scratch);
-  double *res = part + (reduce_scratch_bytes() / sizeof(double) - 2);
+  double *res = static_cast<double *>(ctx->dev_scratch) + (reduce_scratch_bytes() / sizeof(double) - 2);
+  double *part = res - 2 * kReduceBlocks;   // the single-reduction partials
   TCI_CUDA_CHECK(launch_reduce(mode, static_cast<const double *>(a.data),
                                b ? static_cast<const double *>(b->data) : nullptr, n_reals(a), conj_a, part,
                                res, ctx->stream, &ctx->launches));
@@ -58,6 +58,23 @@ tci_status_t vec_inner(tci_ctx_s *ctx, const View &a, const View &b, int conj_a,
   if (a.dtype != b.dtype || a.size() != b.size())
     TCI_FAIL(TCI_ERR_SHAPE_MISMATCH, "inner: operands differ in dtype or size");
   return vec_reduce(ctx, a.dtype == TCI_C128 ? 1 : 2, a, &b, conj_a, out);
+}
+
+// out[2 i] = <V_i|w> for i < m: one pass over w per kMaxMI vectors, one host
+// synchronisation for all (each value bitwise vec_inner's)
+static tci_status_t vec_multi_inner(tci_ctx_s *ctx, int m, const View *V, const View &w, int conj_a, double *out) {
+  tci_status_t st = vec_check(w);
+  if (st) return st;
+  std::vector<const double *> vp(m);
+  for (int i = 0; i < m; i++) vp[i] = static_cast<const double *>(V[i].data);
+  double *scratch = static_cast<double *>(ctx->dev_scratch);
+  double *res = scratch + 2 * kReduceBlocks * kMaxMI;
+  TCI_CUDA_CHECK(launch_multi_inner(w.dtype == TCI_C128, vp.data(), m, static_cast<const double *>(w.data), n_reals(w),
+                                    conj_a, scratch, res, ctx->stream, &ctx->launches));
+  TCI_CUDA_CHECK(cudaMemcpyAsync(ctx->host_scratch, res, 2 * m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  memcpy(out, ctx->host_scratch, 2 * m * sizeof(double));
+  return TCI_OK;
 }
 
 // out = sum_j coef_j in_j (coef as (re, im) pairs); chunks of kMaxLC inputs
@@ -229,13 +246,13 @@ tci_status_t lanczos_exec(tci_ctx_s *ctx, const View &L, const View &W1, const V
     for (int pass = 0; pass < 2; pass++) {   // full re-orthogonalisation (CGS2)
       std::vector<View> ins(1, w);
       std::vector<double> c = {1.0, 0.0};
+      std::vector<double> q(2 * (j + 1));
+      st = vec_multi_inner(ctx, j + 1, V.data(), w, 1, q.data());   // all <v_i|w> in one pass over w
+      if (st) return st;
       for (int i = 0; i <= j; i++) {
-        double q[2];
-        st = vec_inner(ctx, V[i], w, 1, q);
-        if (st) return st;
         ins.push_back(V[i]);
-        c.push_back(-q[0]);
-        c.push_back(cplx ? -q[1] : 0.0);
+        c.push_back(-q[2 * i]);
+        c.push_back(cplx ? -q[2 * i + 1] : 0.0);
       }
       st = vec_lincomb(ctx, (int)ins.size(), ins.data(), c.data(), w);
       if (st) return st;

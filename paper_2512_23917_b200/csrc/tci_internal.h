@@ -197,6 +197,11 @@ constexpr int kMaxLC = 8;
 cudaError_t launch_reduce(int mode, const double *a, const double *b, int64_t n_reals, int conj_a,
                           double *part, double *out, cudaStream_t s, int64_t *launches);
 size_t reduce_scratch_bytes();
+// several inner products <v_i|w> in one pass over w (bitwise the single ones)
+constexpr int kMaxMI = 8, kMaxMIOut = 520;
+constexpr int kReduceBlocks = 296;   // reduction CTAs (vec.cu), 2 per SM
+cudaError_t launch_multi_inner(bool cplx, const double *const *v, int m, const double *w, int64_t n_reals, int conj_a,
+                               double *scratch, double *out, cudaStream_t s, int64_t *launches);
 // out[i] = sum_j (cr_j + i ci_j) in_j[i], m <= kMaxLC; out may alias an input
 cudaError_t launch_lincomb(bool cplx, const double *const *in, const double *cr, const double *ci, int m,
                            double *out, int64_t n, cudaStream_t s, int64_t *launches);

@@ -170,6 +170,30 @@ def shard_projection(ctx, name="target_heisenberg_chi4096", reps=5, ag_gbs=770.0
     return {"workload": name, "rows": rows}
 
 
+def lanczos_cfg(ctx, name="target_heisenberg_chi4096", iters=(5, 20)):
+    """The two-site DMRG local solve the north star frames H_eff.psi inside: the
+    Lanczos driver (tci_heff_lanczos: apply, full reorthogonalisation, host
+    tridiagonal solve) at the bench workload. Time per iteration from two runs
+    of different Krylov dimension (the difference removes the setup)."""
+    cfg = synth.HEFF_CONFIGS[name]
+    inp = synth.heff_inputs(cfg["chi"], cfg["d"], cfg["D"], cfg["dtype"], cfg["seed"], cfg["model"], device="cuda")
+    res = {"workload": name}
+    for n in iters:
+        psi = inp["psi"].clone()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        energy, it = ctx.heff_lanczos(inp["L"], inp["W1"], inp["W2"], inp["R"], psi, max_iter=n, tol=0.0)
+        torch.cuda.synchronize()
+        res[f"iters_{n}"] = {"s": time.perf_counter() - t0, "iterations": it, "energy": energy}
+    a, b = res[f"iters_{iters[0]}"], res[f"iters_{iters[1]}"]
+    per = (b["s"] - a["s"]) / max(1, b["iterations"] - a["iterations"])
+    F = synth.heff_flops(cfg["chi"], cfg["d"], cfg["D"])
+    res.update({"s_per_iteration": per, "apply_tflops_in_lanczos": F / per / 1e12})
+    del inp
+    torch.cuda.empty_cache()
+    return res
+
+
 def env_cfg(ctx, chi=4096, d=2, D=5, reps=3):
     """Environment updates (8(f3)) at the target scale, both sides, c128:
     GEMM (E.ket) -> skinny MPO pass -> conj(bra) -> GEMM; bra = ket."""
@@ -383,6 +407,8 @@ def main():
             res["mpo"] = mpo_apply_cfg(ctx)
         elif k == "svd":
             res["svd"] = svd_cfg(ctx)
+        elif k == "lanczos":
+            res["lanczos"] = lanczos_cfg(ctx)
         elif k == "shards":
             res["shards"] = shard_projection(ctx)
         elif k == "shards4":

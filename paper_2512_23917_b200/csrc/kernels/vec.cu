@@ -3,7 +3,7 @@
 //   norm (Frobenius, Eq. frob_norm), scale,
 //   linear_combine, and the inner product <a|b> = sum conj?(a) b
 //   (a full contraction to a scalar, with cplx_conj P:1235-1268).
-// All HBM-bound. Reductions are deterministic: a fixed grid (2 x 148 CTAs),
+// All HBM-bound. Reductions are deterministic: a fixed grid (4 x 148 CTAs),
 // each CTA sums a fixed strided set of elements in a fixed order and writes
 // one partial; a second single-CTA pass adds the partials in ascending order.
 // Results are therefore bitwise reproducible run to run.
@@ -15,7 +15,7 @@
 namespace tci {
 namespace {
 
-constexpr int RB = kReduceBlocks;   // reduction CTAs (2 per SM)
+constexpr int RB = kReduceBlocks;   // reduction CTAs (4 per SM)
 constexpr int RT = 256;
 
 // block-wide sum in a fixed tree order
@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(RT) reduce_pass1(const double *a, const double
   } else {
     const double2 *a2 = reinterpret_cast<const double2 *>(a), *b2 = reinterpret_cast<const double2 *>(b);
     const double sg = conj_a ? -1.0 : 1.0;
+#pragma unroll 4
     for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n_reals / 2; i += stride) {
       const double2 x = a2[i], y = b2[i];
       // (xr + i sg xi)(yr + i yi)
@@ -88,39 +89,41 @@ struct MiArgs {
   int m;
 };
 
-template <bool CPLX>
+template <bool CPLX, int M>
 __global__ void __launch_bounds__(RT) multi_inner_pass1(const __grid_constant__ MiArgs a, const double *w,
                                                         int64_t n_reals, int conj_a, double *part) {
   __shared__ double sh[2][RT];
-  double acc[kMaxMI][2];
+  double acc[M][2];
 #pragma unroll
-  for (int i = 0; i < kMaxMI; i++) acc[i][0] = acc[i][1] = 0.0;
+  for (int i = 0; i < M; i++) acc[i][0] = acc[i][1] = 0.0;
   const int64_t stride = (int64_t)gridDim.x * RT;
   if (CPLX) {
     const double2 *w2 = reinterpret_cast<const double2 *>(w);
     const double sg = conj_a ? -1.0 : 1.0;
+#pragma unroll 2
     for (int64_t e = blockIdx.x * (int64_t)RT + threadIdx.x; e < n_reals / 2; e += stride) {
       const double2 y = w2[e];
+      double2 x[M];
 #pragma unroll
-      for (int i = 0; i < kMaxMI; i++) {
-        if (i < a.m) {
-          const double2 x = reinterpret_cast<const double2 *>(a.v[i])[e];
-          acc[i][0] = fma(x.x, y.x, acc[i][0]);
-          acc[i][0] = fma(-sg * x.y, y.y, acc[i][0]);
-          acc[i][1] = fma(x.x, y.y, acc[i][1]);
-          acc[i][1] = fma(sg * x.y, y.x, acc[i][1]);
-        }
+      for (int i = 0; i < M; i++) x[i] = reinterpret_cast<const double2 *>(a.v[i])[e];
+#pragma unroll
+      for (int i = 0; i < M; i++) {
+        acc[i][0] = fma(x[i].x, y.x, acc[i][0]);
+        acc[i][0] = fma(-sg * x[i].y, y.y, acc[i][0]);
+        acc[i][1] = fma(x[i].x, y.y, acc[i][1]);
+        acc[i][1] = fma(sg * x[i].y, y.x, acc[i][1]);
       }
     }
   } else {
+#pragma unroll 2
     for (int64_t e = blockIdx.x * (int64_t)RT + threadIdx.x; e < n_reals; e += stride) {
       const double y = w[e];
 #pragma unroll
-      for (int i = 0; i < kMaxMI; i++)
-        if (i < a.m) acc[i][0] = fma(a.v[i][e], y, acc[i][0]);
+      for (int i = 0; i < M; i++) acc[i][0] = fma(a.v[i][e], y, acc[i][0]);
     }
   }
-  for (int i = 0; i < a.m; i++) {
+#pragma unroll 1
+  for (int i = 0; i < M; i++) {
     double v[2] = {acc[i][0], acc[i][1]};
     block_sum<2>(v, sh);
     if (threadIdx.x == 0) {
@@ -128,6 +131,21 @@ __global__ void __launch_bounds__(RT) multi_inner_pass1(const __grid_constant__ 
       part[(size_t)i * 2 * gridDim.x + 2 * blockIdx.x + 1] = v[1];
     }
     __syncthreads();
+  }
+}
+
+template <bool CPLX>
+void multi_inner_launch(int m, const MiArgs &a, const double *w, int64_t n_reals, int conj_a, double *part,
+                        cudaStream_t s) {
+  switch (m) {
+    case 1: multi_inner_pass1<CPLX, 1><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, part); break;
+    case 2: multi_inner_pass1<CPLX, 2><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, part); break;
+    case 3: multi_inner_pass1<CPLX, 3><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, part); break;
+    case 4: multi_inner_pass1<CPLX, 4><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, part); break;
+    case 5: multi_inner_pass1<CPLX, 5><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, part); break;
+    case 6: multi_inner_pass1<CPLX, 6><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, part); break;
+    case 7: multi_inner_pass1<CPLX, 7><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, part); break;
+    default: multi_inner_pass1<CPLX, 8><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, part); break;
   }
 }
 
@@ -191,8 +209,8 @@ cudaError_t launch_multi_inner(bool cplx, const double *const *v, int m, const d
     MiArgs a{};
     a.m = std::min(kMaxMI, m - i0);
     for (int i = 0; i < a.m; i++) a.v[i] = v[i0 + i];
-    if (cplx) multi_inner_pass1<true><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, scratch);
-    else multi_inner_pass1<false><<<RB, RT, 0, s>>>(a, w, n_reals, conj_a, scratch);
+    if (cplx) multi_inner_launch<true>(a.m, a, w, n_reals, conj_a, scratch, s);
+    else multi_inner_launch<false>(a.m, a, w, n_reals, conj_a, scratch, s);
     for (int i = 0; i < a.m; i++) reduce_pass2<<<1, RT, 0, s>>>(scratch + (size_t)i * 2 * RB, RB, out + 2 * (i0 + i));
     if (launches) *launches += 1 + a.m;
   }

@@ -199,7 +199,7 @@ cudaError_t launch_reduce(int mode, const double *a, const double *b, int64_t n_
 size_t reduce_scratch_bytes();
 // several inner products <v_i|w> in one pass over w (bitwise the single ones)
 constexpr int kMaxMI = 8, kMaxMIOut = 520;
-constexpr int kReduceBlocks = 296;   // reduction CTAs (vec.cu), 2 per SM
+constexpr int kReduceBlocks = 592;   // reduction CTAs (vec.cu), 4 per SM
 cudaError_t launch_multi_inner(bool cplx, const double *const *v, int m, const double *w, int64_t n_reals, int conj_a,
                                double *scratch, double *out, cudaStream_t s, int64_t *launches);
 // out[i] = sum_j (cr_j + i ci_j) in_j[i], m <= kMaxLC; out may alias an input

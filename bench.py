@@ -511,7 +511,7 @@ def run_tci(args):
             "gemm_share_of_step": g["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
         }
     roofline["secondary"] = {
-        "kernel": "skinny_kernel (MPO pass)", "bound": "hbm",
+        "kernel": "skinny_dmma_kernel (MPO pass, FP64 tensor cores, 3M)", "bound": "hbm",
         "achieved": (sk["bytes"] / (sk["ms"] / 1e3) / 1e9) if sk["launches"] else None,
         "peak": peaks.get("hbm_gbs"), "unit": "GB/s", "peak_source": peak_src,
         "share_of_step": sk["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,

@@ -118,6 +118,7 @@ struct __align__(16) RoundSmem {
   int ord[PR];
   double ev[PR];
   double red[NT / 32];
+  int lowf[PR];   // row below the truncation cut (trunc_svd low-pair skipping), per pair row
   int skip;
 };
 
@@ -258,7 +259,7 @@ __device__ void block_eig(RoundSmem<C> &sm, int nreal, double tol_in, int max_in
         // rows at or below the noise floor (zfloor2, squared norm) are frozen:
         // their directions are rounding noise, completed at the end (R29)
         if (ah == 0.0 || ah <= tol_in * sqrt(fabs(hi)) * sqrt(fabs(hj)) || negligible(hi, hj) ||
-            fmin(hi, hj) <= zfloor2) {
+            fmin(hi, hj) <= zfloor2 || (sm.lowf[i] && sm.lowf[j])) {
           sm.rflag[tid] = 0;
         } else {
           // real symmetric [[hi, |h|], [|h|, hj]] (after the phase) -> R = [[c, s], [-s, c]]
@@ -470,7 +471,8 @@ template <bool C>
 __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, int64_t ldx, typename Cx<C>::E *Y,
                                                           int64_t ldy, int nb, int64_t n, int round, double tol,
                                                           double tol_in, int max_inner, double zfloor2,
-                                                          unsigned long long *offmax, unsigned long long *prof) {
+                                                          const int *low, unsigned long long *offmax,
+                                                          unsigned long long *prof) {
   using E = typename Cx<C>::E;
   constexpr int CW = Cx<C>::CW;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -509,13 +511,21 @@ __global__ void __launch_bounds__(NT, 2) svd_round_kernel(typename Cx<C>::E *X, 
   }
   __syncthreads();
 
+  // rows below the truncation cut (both rows of a pair low: the pair only
+  // mixes discarded rows and is skipped, trunc_svd with chi_max < n)
+  for (int i = threadIdx.x; i < PR; i += NT) {
+    const int64_t r = i < SB ? row_lo + i : row_hi + (i - SB);
+    sm.lowf[i] = (low && r < n) ? low[r] : 0;
+  }
+  __syncthreads();
   // convergence test: max relative off-diagonal |H_ij| / sqrt(H_ii H_jj)
   double off = 0.0;
   for (int idx = threadIdx.x; idx < PR * PR; idx += NT) {
     const int i = idx / PR, j = idx % PR;
     if (i < j) {
       const double di = re(sm.H[i][i]), dj = re(sm.H[j][j]);
-      if (di > zfloor2 && dj > zfloor2 && !negligible(di, dj)) off = fmax(off, cabs(sm.H[i][j]) / sqrt(di * dj));
+      if (di > zfloor2 && dj > zfloor2 && !negligible(di, dj) && !(sm.lowf[i] && sm.lowf[j]))
+        off = fmax(off, cabs(sm.H[i][j]) / sqrt(di * dj));
     }
   }
 #pragma unroll
@@ -810,12 +820,12 @@ cudaError_t launch_svd_round(const SvdProblem &p, int round, double tol, double 
     auto k = svd_round_kernel<true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     e = cudaLaunchKernelEx(&cfg, k, static_cast<double2 *>(p.X), p.ldx, static_cast<double2 *>(p.Y), p.ldy, nb,
-                           p.n, round, tol, tol_in, max_inner, p.zfloor2, p.offmax, p.prof);
+                           p.n, round, tol, tol_in, max_inner, p.zfloor2, p.low, p.offmax, p.prof);
   } else {
     auto k = svd_round_kernel<false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     e = cudaLaunchKernelEx(&cfg, k, static_cast<double *>(p.X), p.ldx, static_cast<double *>(p.Y), p.ldy, nb, p.n,
-                           round, tol, tol_in, max_inner, p.zfloor2, p.offmax, p.prof);
+                           round, tol, tol_in, max_inner, p.zfloor2, p.low, p.offmax, p.prof);
   }
   (*launches)++;
   if (e != cudaSuccess) return e;

@@ -14,6 +14,7 @@
 //      v_dag [chi, d_k..d_{r-1}]; the output descriptors are
 //      reshaped to chi (metadata).
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -204,7 +205,32 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
   const int max_sweeps = 60;
   unsigned long long offbits = 0;
   int sweeps = 0;
+  // trunc_svd cut by chi_max alone (target = 0, chi_max < n): a pair of two
+  // rows below half the chi_max-th largest row norm only mixes rows that are
+  // discarded, so it is neither rotated nor counted in the convergence
+  // measure (the discarded rows' squared norms still sum exactly to the
+  // tail, as rotations keep the sum). Flags are recomputed after every sweep;
+  // convergence is accepted only when the flags it ran with are unchanged.
+  static const bool lowskip_on = [] {
+    const char *e = getenv("TCI_SVD_LOWSKIP");
+    return !(e && e[0] == '0');
+  }();
+  const bool lowskip = lowskip_on && trunc && target == 0.0 && chi_max >= 1 && chi_max < d.n && chi_min <= chi_max;
+  std::vector<int> lowf(d.npad, 0), lowf_new(d.npad, 0);
+  int *dlow = reinterpret_cast<int *>(ws + d.off_perm);   // perm is written only after the sweeps
+  auto flags_from_norms = [&](std::vector<int> &f) -> tci_status_t {
+    TCI_CUDA_CHECK(launch_svd_norms(p, s, &ctx->launches));
+    std::vector<double> nr(d.npad);
+    TCI_CUDA_CHECK(cudaMemcpyAsync(nr.data(), p.s, d.npad * 8, cudaMemcpyDeviceToHost, s));
+    TCI_CUDA_CHECK(cudaStreamSynchronize(s));
+    std::vector<double> srt(nr.begin(), nr.begin() + d.n);
+    std::nth_element(srt.begin(), srt.begin() + (chi_max - 1), srt.end(), std::greater<double>());
+    const double cut = 0.5 * srt[chi_max - 1];
+    for (int64_t i = 0; i < d.npad; i++) f[i] = (i < d.n && nr[i] < cut) ? 1 : 0;
+    return TCI_OK;
+  };
   for (; sweeps < max_sweeps;) {
+    p.low = (lowskip && sweeps > 0) ? dlow : nullptr;
     TCI_CUDA_CHECK(cudaMemsetAsync(p.offmax, 0, 8, s));
     for (int rd = 0; rd < nb - 1; rd++) TCI_CUDA_CHECK(launch_svd_round(p, rd, tol, tol_in, max_inner, s, &ctx->launches));
     TCI_CUDA_CHECK(cudaMemcpyAsync(&offbits, p.offmax, 8, cudaMemcpyDeviceToHost, s));
@@ -214,8 +240,19 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
     memcpy(&off, &offbits, 8);
     ctx->svd_last_off = off;
     if (trace) fprintf(stderr, "tci:svd sweep %d off=%.3e\n", sweeps, off);
+    if (lowskip) {
+      tci_status_t fs = flags_from_norms(lowf_new);
+      if (fs) return fs;
+      const bool same = p.low && lowf_new == lowf;
+      lowf.swap(lowf_new);
+      TCI_CUDA_CHECK(cudaMemcpyAsync(dlow, lowf.data(), d.npad * sizeof(int), cudaMemcpyHostToDevice, s));
+      TCI_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (!(off > tol) && same) break;
+      continue;
+    }
     if (!(off > tol)) break;
   }
+  p.low = nullptr;
   ctx->svd_last_sweeps = sweeps;
   if (p.prof) {
     unsigned long long h[7];

@@ -239,6 +239,9 @@ struct SvdProblem {
   // noise floor (squared row norm): rows at or below it are neither rotated
   // nor counted in the convergence measure; their vectors are completed
   double zfloor2 = 0.0;
+  // optional per-row flags (npad ints): a pair of two flagged rows is skipped
+  // (trunc_svd: both rows below the chi_max cut)
+  const int *low = nullptr;
 };
 size_t svd_round_smem_bytes(bool cplx);
 cudaError_t launch_svd_load(const SvdProblem &p, const void *A, int64_t I, int64_t J, cudaStream_t s,

@@ -26,3 +26,6 @@ PY
 for cfg in "X=1" "TCI_SVD_LOWSKIP=0"; do
   echo "== $cfg"; env $cfg timeout 300 python /tmp/svdt.py 2048 2>&1 | tail -1; env $cfg timeout 300 python /tmp/svdt.py 512 2>&1 | tail -1
 done
+timeout 600 python tools/bench_extra.py --only svd --out gpurun_out/extra_svd.json 2>&1 | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()[4:])
+for k,v in d.items(): print(k, v['ms'], v['sweeps'], v['final_off'], v['max_abs_ds_over_s0'])"

@@ -159,3 +159,14 @@ def test_lanes_streaming_applies():
     with pytest.raises(tci.TciError):
         ctx.lane_wait(0, 16)
     ctx.close()
+
+
+def test_peer_gather_bench_workload_p2():
+    """The bench workload (chi = 4096, d = 2, D = 5, Ozaki) gathered over
+    emulated peer memory by two ranks: bitwise the unsharded apply."""
+    inp, ref, fulls, flags, status, launches = _run(4096, 2, 5, 2, "ozaki", steps=1, seed=6)
+    assert status == [0, 0]
+    for r in range(2):
+        assert torch.equal(fulls[r], ref)
+    del inp, ref, fulls
+    torch.cuda.empty_cache()

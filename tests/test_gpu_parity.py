@@ -925,3 +925,15 @@ def test_ozaki_real_tebd_theta(ozctx, oracle_mod):
     a_rows = [0, 511, 1023]
     ref = oracle_mod.tebd_theta(inp["A"].numpy()[a_rows], inp["B"].numpy(), inp["U"].numpy())
     assert rel_frob(host(th)[a_rows], ref) <= 1e-12
+
+
+def test_ozaki_real_tebd_theta_full_size(ozctx, oracle_mod):
+    """Config 3 at full size (chi = 2048, f64) with the Ozaki algorithm: sampled
+    rows of theta vs the oracle (<= 1e-12 relative per row)."""
+    c = synth.TEBD_CONFIG
+    inp = synth.tebd_inputs(c["chi"], c["d"], c["dtype"], c["seed"], c["tau"])
+    th = host(ozctx.tebd_theta(dev(inp["A"]), "asb", dev(inp["B"]), "btc", dev(inp["U"]), "pqst", "apqc"))
+    a_rows = [0, 1, 1023, 2047]
+    ref = oracle_mod.tebd_theta(inp["A"].numpy()[a_rows], inp["B"].numpy(), inp["U"].numpy())
+    for i, a in enumerate(a_rows):
+        assert rel_frob(th[a], ref[i]) <= 1e-12

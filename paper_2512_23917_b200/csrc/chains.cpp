@@ -149,7 +149,7 @@ HeffLayout heff_layout(const HeffDims &h, tci_dtype_t dt) {
 // Ozaki scratch for the two chain GEMMs (0 when not used)
 static size_t heff_ozaki_bytes(tci_dtype_t dt, int zalgo, int64_t chi_l, int64_t chi_lo, int64_t chi_r,
                                int64_t chi_ro, int64_t d, int64_t D, int64_t D2) {
-  if (dt != TCI_C128 || zalgo != kZOzaki) return 0;
+  if ((dt != TCI_C128 && dt != TCI_R64) || zalgo != kZOzaki) return 0;   // r64: real Ozaki-II
   size_t b = 0;
   const int64_t M1 = D * chi_lo, N1 = d * d * chi_r, K1 = chi_l;
   if (ozaki_worthwhile(M1, N1, K1)) b = std::max(b, ozaki_workspace_bytes(M1, N1, K1));
@@ -323,7 +323,8 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
   const size_t oz_b = heff_ozaki_bytes(dt, ctx->zgemm_algo, h.chi_l, h.chi_lo, h.chi_r, h.chi_ro, h.d, h.D, h.D2);
   auto set_zalgo = [&](GemmProblem &g) {
     g.zalgo = ctx->zgemm_algo == kZOzaki ? kZ3M : ctx->zgemm_algo;
-    if (oz_b && ozaki_worthwhile(g.M, g.N, g.K)) {
+    // (the real Ozaki GEMM takes its row exponents up front: not with staged input)
+    if (oz_b && ozaki_worthwhile(g.M, g.N, g.K) && !(dt == TCI_R64 && stage)) {
       g.zalgo = kZOzaki;
       g.oz_ws = ws + lay.total;
       g.oz_ws_bytes = oz_b;

@@ -937,3 +937,23 @@ def test_ozaki_real_tebd_theta_full_size(ozctx, oracle_mod):
     ref = oracle_mod.tebd_theta(inp["A"].numpy()[a_rows], inp["B"].numpy(), inp["U"].numpy())
     for i, a in enumerate(a_rows):
         assert rel_frob(th[a], ref[i]) <= 1e-12
+
+
+def test_ozaki_real_heff(ctx, ozctx, oracle_mod):
+    """float64 H_eff.psi (chi = 1024, Heisenberg) with the Ozaki algorithm: both
+    chain GEMMs on the real Ozaki-II path; vs the DMMA chain (<= 1e-12) and
+    oracle rows; deterministic."""
+    inp = synth.heff_inputs(1024, 2, 5, "r64", 97, "heisenberg")
+    d = {k: dev(v) for k, v in inp.items()}
+    tci.tci_profile_enable(ozctx.handle, True)
+    got = ozctx.heff_apply(d["L"], d["W1"], d["W2"], d["R"], d["psi"])
+    i8 = tci.tci_profile_query(ozctx.handle, tci.PROF_I8)
+    tci.tci_profile_enable(ozctx.handle, False)
+    assert i8["launches"] >= 2
+    ref_dm = ctx.heff_apply(d["L"], d["W1"], d["W2"], d["R"], d["psi"])
+    assert rel_frob(host(got), host(ref_dm)) <= 1e-12
+    rows = [0, 511, 1023]
+    n = {k: v.numpy() for k, v in inp.items()}
+    want = oracle_mod.heff_rows(n["L"], n["W1"], n["W2"], n["R"], n["psi"], rows)
+    assert rel_frob(host(got)[rows], want) <= 1e-12
+    assert torch.equal(got, ozctx.heff_apply(d["L"], d["W1"], d["W2"], d["R"], d["psi"]))

@@ -802,16 +802,17 @@ def test_env_heisenberg_expectation_closed_form(ctx, side):
     assert abs(got - closed) <= 1e-14 and abs(got.imag) <= 1e-15
 
 
+@pytest.mark.parametrize("dt", ["c128", "r64"])
 @pytest.mark.parametrize("algo", ["dmma3m", "ozaki"])
 @pytest.mark.parametrize("side", [0, 1])
-def test_env_update_chi1024_sampled(oracle_mod, side, algo):
-    """cfg2 scale (chi = 1024, D = 5, d = 2, c128; both GEMMs take the Ozaki
-    path when selected): sampled output rows vs the oracle."""
+def test_env_update_chi1024_sampled(oracle_mod, side, algo, dt):
+    """cfg2 scale (chi = 1024, D = 5, d = 2; both GEMMs take the Ozaki path --
+    complex or real -- when selected): sampled output rows vs the oracle."""
     c = tci.Context(0)
     if algo == "ozaki":
         c.set_gemm_algorithm(tci.TCI_GEMM_OZAKI_INT8)
     try:
-        E, ket, W, bra = _env_inputs(side, "c128", 1024, 1024, 1024, 1024, 5, 5, 2, 612, same_bra=True)
+        E, ket, W, bra = _env_inputs(side, dt, 1024, 1024, 1024, 1024, 5, 5, 2, 612, same_bra=True)
         out = c.env_update(side, dev(E), dev(ket), dev(W))
         rows = [0, 1, 511, 1023]
         ref = oracle_mod.env_rows(side, E.numpy(), ket.numpy(), W.numpy(), bra.numpy(), rows)

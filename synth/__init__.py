@@ -254,6 +254,9 @@ def heff_inputs(chi: int, d: int, D: int, dtype: str, seed: int, model: str,
     if model in ("heisenberg", "hubbard"):
         W, _, _ = model_mpo(model)
         assert W.shape == (D, D, d, d), (W.shape, D, d)
+        if not tdt.is_complex:   # real dtypes: the model MPOs are real (exact imaginary zeros)
+            assert not np.iscomplexobj(W) or not np.any(np.imag(W)), "model MPO is not real"
+            W = np.ascontiguousarray(np.real(W))
         W1 = torch.from_numpy(W).to(tdt).to(device)
         W2 = W1.clone()
     else:

@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant_
   double2 *sIn = reinterpret_cast<double2 *>(sWf + KS * NTL * 3 * 32);  // [2][KN][TD]
   const double2 *W = reinterpret_cast<const double2 *>(a.W);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int wimag = 0;
   for (int i = tid; i < KS * NTL * 32; i += NTH) {
     const int l = i & 31, f = i >> 5, nt = f % NTL, ks = f / NTL;
     const int k = ks * 4 + (l & 3), n = nt * 8 + (l >> 2);
@@ -295,7 +296,11 @@ __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant_
     dst[0] = w.x;
     dst[32] = w.y;
     dst[64] = w.x + w.y;
+    wimag |= (w.y != 0.0);
   }
+  // a real W (the Heisenberg / Hubbard MPOs): X W = (Xr W, Xi W), two DMMAs
+  // per fragment product instead of the three of 3M (uniform per CTA)
+  const bool wreal = __syncthreads_or(wimag) == 0;
   const int64_t tiles2 = (a.nb[2] + TD - 1) / TD;
   auto tile_ptrs = [&](int64_t t, const double2 *&in, double2 *&out, int &nc) {
     const int64_t t2 = t % tiles2, r = t / tiles2;
@@ -350,15 +355,27 @@ __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant_
         ai[m] = x.y;
         as[m] = x.x + x.y;
       }
+      if (wreal) {
 #pragma unroll
-      for (int nt = 0; nt < NTL; nt++) {
-        const double *wf = sWf + ((ks * NTL + nt) * 3) * 32 + lane;
-        const double wr = wf[0], wi = wf[32], ws = wf[64];
+        for (int nt = 0; nt < NTL; nt++) {
+          const double wr = sWf[((ks * NTL + nt) * 3) * 32 + lane];
 #pragma unroll
-        for (int m = 0; m < MT; m++) {
-          dmma884(P[m][nt], ar[m], wr);
-          dmma884(Q[m][nt], ai[m], wi);
-          dmma884(S[m][nt], as[m], ws);
+          for (int m = 0; m < MT; m++) {
+            dmma884(P[m][nt], ar[m], wr);
+            dmma884(Q[m][nt], ai[m], wr);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < NTL; nt++) {
+          const double *wf = sWf + ((ks * NTL + nt) * 3) * 32 + lane;
+          const double wr = wf[0], wi = wf[32], ws = wf[64];
+#pragma unroll
+          for (int m = 0; m < MT; m++) {
+            dmma884(P[m][nt], ar[m], wr);
+            dmma884(Q[m][nt], ai[m], wi);
+            dmma884(S[m][nt], as[m], ws);
+          }
         }
       }
     }
@@ -376,7 +393,8 @@ __global__ void __launch_bounds__(NTH) skinny_dmma_kernel(const __grid_constant_
             const int n = nt * 8 + 2 * q + e;
             if (n < N)
               out[c * a.out_sb[2] + a.out_noff[n]] =
-                  make_double2(P[m][nt][e] - Q[m][nt][e], S[m][nt][e] - P[m][nt][e] - Q[m][nt][e]);
+                  wreal ? make_double2(P[m][nt][e], Q[m][nt][e])
+                        : make_double2(P[m][nt][e] - Q[m][nt][e], S[m][nt][e] - P[m][nt][e] - Q[m][nt][e]);
           }
       }
     }

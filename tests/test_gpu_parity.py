@@ -507,6 +507,20 @@ def test_skinny_pass_shapes(ctx, oracle_mod, dt):
             assert torch.equal(got, got2)                       # deterministic
 
 
+def test_skinny_pass_real_weights(ctx, oracle_mod):
+    """Complex data with a real-valued W (the model MPOs) takes the two-DMMA
+    branch of the tensor-core pass; one nonzero imaginary entry switches it
+    back to 3M. Both vs the oracle."""
+    X = synth.random_tensor((3, 20, 200), "c128", 450, 1)
+    W = synth.random_tensor((20, 20), "c128", 450, 2)
+    Wr = torch.complex(W.real, torch.zeros_like(W.real))
+    for w in (Wr, Wr.clone()):
+        got = ctx.contract(dev(X), "akc", dev(w), "kn", "anc")
+        ref = oracle_mod.contract(X.numpy(), "akc", w.numpy(), "kn", "anc")
+        assert rel_frob(host(got), ref) <= 1e-12
+        Wr[7, 3] = complex(Wr[7, 3].real.item(), 1e-3)   # second pass: one imaginary entry
+
+
 def test_mps_mpo_apply(ctx, oracle_mod):
     A = synth.random_tensor((40, 2, 33), "c128", 420, 1)
     I = torch.eye(2, dtype=torch.complex128).reshape(1, 1, 2, 2)

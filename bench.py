@@ -62,7 +62,14 @@ def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("TCI_BENCH_SAME_DEVICE") == "1":
+        local = 0   # test harness: every rank on cuda:0 (multi-process check of the N > 1 path on one GPU)
     return ws, rank, local
+
+
+# process-group backend: NCCL (default); TCI_BENCH_BACKEND=gloo is the
+# single-GPU multi-process test harness (NCCL refuses two ranks on one device)
+BACKEND = os.environ.get("TCI_BENCH_BACKEND", "nccl")
 
 
 class ClockSampler:
@@ -218,7 +225,10 @@ def run_tci(args):
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(BACKEND)
     name = CONFIGS[args.config]
     cfg = synth.HEFF_CONFIGS[name]
     chi, d, D, dt = cfg["chi"], cfg["d"], cfg["D"], cfg["dtype"]
@@ -245,7 +255,9 @@ def run_tci(args):
                                 "ozaki": tci.TCI_GEMM_OZAKI_INT8}[args.algo])
     ALGOS = {"dmma3m": tci.TCI_GEMM_DMMA_3M, "dmma4m": tci.TCI_GEMM_DMMA_4M, "ozaki": tci.TCI_GEMM_OZAKI_INT8}
     algo = {0: "dmma3m", 1: "dmma4m", 2: "ozaki"}[tci.tci_get_gemm_algorithm(ctx.handle)]
-    if ws > 1:
+    def nccl_comm_init():
+        # the library's NCCL communicator: only for the NCCL all-gather (the
+        # peer-memory gather needs none)
         import torch.distributed as dist
         obj = [tci.tci_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -281,6 +293,8 @@ def run_tci(args):
                 sh.close()
                 sh = None
     if sh is None:
+        if ws > 1:
+            nccl_comm_init()
         sh = ShardedHeff(ctx, L, W1, W2, R, ws, rank)
     out = sh.out
 
@@ -290,7 +304,10 @@ def run_tci(args):
     def barrier():
         if ws > 1:
             import torch.distributed as dist
-            dist.barrier(device_ids=[local])
+            if BACKEND == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     for _ in range(args.warmup):
         step()
@@ -405,7 +422,9 @@ def run_tci(args):
                "path": ("tci_heff_apply_staged (pinned host inputs/outputs; psi + W copied first, L streamed in "
                         "8 column blocks behind GEMM1's row chunks, R behind L, D2H in 8 row chunks behind "
                         "GEMM4)") if staged else
-                       "tci_copy(pinned host->device) x5, tci_heff_apply, tci_copy(device->host), tci_allgather"}
+                       ("tci_copy(pinned host->device) x5, tci_heff_apply_gather (peer-memory all-gather in the "
+                        "GEMM4 epilogue), tci_copy(device->host)" if gather == "p2p" else
+                        "tci_copy(pinned host->device) x5, tci_heff_apply, tci_allgather, tci_copy(device->host)")}
         if ws == 1 and not args.no_pipeline:
             # Streaming applies (steady state of a stream of independent H_eff.psi
             # problems): device inputs / outputs double-buffered; step i+1's five
@@ -523,6 +542,19 @@ def run_tci(args):
         inp_np = {"L": L.cpu().numpy(), "W1": W1.cpu().numpy(), "W2": W2.cpu().numpy(),
                   "R": R.cpu().numpy(), "psi": psi.cpu().numpy()}
         cpu, parity = cpu_baseline(inp_np, chi, F, budget_s=args.cpu_budget, gpu_out=out.cpu().numpy())
+    elif ws > 1 and not args.no_cpu_baseline:
+        # the gathered output on rank 0 vs oracle rows at both edges of every
+        # rank's slab (the all-gather put them there; inputs regenerated on the host)
+        import oracle
+        oracle.build()
+        full_inp = synth.heff_inputs(chi, d, D, dt, cfg["seed"], cfg["model"], device="cpu")
+        inp_np = {k: v.numpy() for k, v in full_inp.items()}
+        rows = sorted({b for r in range(ws) for b in (r * chi_lo, r * chi_lo + chi_lo - 1)})
+        ref, _ = oracle_rows_run(inp_np, rows)
+        got = sh.full.cpu().numpy()[rows]
+        parity = {"rows_checked": len(rows), "rows": "first and last row of every rank's slab",
+                  "rel_frob": float(np.linalg.norm(got - ref) / np.linalg.norm(ref))}
+        del full_inp, inp_np
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

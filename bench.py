@@ -383,7 +383,8 @@ def run_tci(args):
     e2e = None
     if not args.no_e2e:
         hosts = {k: x.cpu().pin_memory() for k, x in (("L", L), ("W1", W1), ("W2", W2), ("R", R), ("psi", psi))}
-        hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        res_dev = sh.full if ws > 1 else out      # the step's result: the gathered output at N > 1
+        hout = torch.empty(res_dev.shape, dtype=res_dev.dtype).pin_memory()
         devs = {"L": L, "W1": W1, "W2": W2, "R": R, "psi": psi}
         h2d = sum(x.numel() * x.element_size() for x in hosts.values())
         d2h = hout.numel() * hout.element_size()
@@ -400,7 +401,7 @@ def run_tci(args):
             for k in hosts:
                 ctx.copy(hosts[k], devs[k])        # tci_copy: pinned host -> device
             step()
-            ctx.copy(out, hout)                     # tci_copy: device -> pinned host
+            ctx.copy(res_dev, hout)                 # tci_copy: device -> pinned host
         e2e_step()
         torch.cuda.synchronize()
         ke = max(1, min(args.steps, 3))
@@ -425,17 +426,34 @@ def run_tci(args):
                        ("tci_copy(pinned host->device) x5, tci_heff_apply_gather (peer-memory all-gather in the "
                         "GEMM4 epilogue), tci_copy(device->host)" if gather == "p2p" else
                         "tci_copy(pinned host->device) x5, tci_heff_apply, tci_allgather, tci_copy(device->host)")}
-        if ws == 1 and not args.no_pipeline:
+        if not args.no_pipeline:
             # Streaming applies (steady state of a stream of independent H_eff.psi
-            # problems): device inputs / outputs double-buffered; step i+1's five
+            # problems): device inputs double-buffered; step i+1's five
             # host->device copies run on copy lane 1 and step i-1's device->host
             # copy on lane 2 while step i computes on the context stream. Every
             # step still copies all of its inputs in and its result out inside
-            # the timed region (the first step's copies start after e0).
-            bufs = [devs, {k: torch.empty_like(v) for k, v in devs.items()}]
-            outs = [out, torch.empty_like(out)]
+            # the timed region (the first step's copies start after e0). At
+            # N > 1 the result is the gathered full output (one buffer: the
+            # context stream waits for its previous copy-out before the step,
+            # so no rank writes into it early -- the gather's entry barrier
+            # follows that wait).
             KEYS = ("L", "W1", "W2", "R", "psi")
+            bufs = [devs, {k: torch.empty_like(v) for k, v in devs.items()}]
+            if ws == 1:
+                outs = [out, torch.empty_like(out)]
+            else:
+                outs = [sh.full, sh.full]
             IN, DONE, OUT, START = 0, 2, 4, 6    # lane event slots (+ buffer index)
+
+            def compute(b):
+                x = [bufs[b][k] for k in KEYS]
+                if ws == 1:
+                    ctx.heff_apply(*x, out=outs[b])
+                elif gather == "p2p":
+                    ctx.heff_apply_gather(*x, sh.full)
+                else:
+                    ctx.heff_apply(*x, out=sh.out)
+                    ctx.allgather(sh.out, sh.full)
 
             def pipelined(n):
                 ctx.lane_record(0, START)
@@ -449,28 +467,39 @@ def run_tci(args):
                 load(0)
                 for i in range(n):
                     b = i % 2
+                    ob = b if ws == 1 else 0
                     if i + 1 < n:
                         load(1 - b)
                     ctx.lane_wait(0, IN + b)
-                    ctx.lane_wait(0, OUT + b)           # the d2h that last read outs[b] is done
-                    ctx.heff_apply(*(bufs[b][k] for k in KEYS), out=outs[b])
+                    ctx.lane_wait(0, OUT + ob)          # the d2h that last read this output is done
+                    compute(b)
                     ctx.lane_record(0, DONE + b)
                     ctx.lane_wait(2, DONE + b)
                     ctx.copy_async(outs[b], hout, 2)
-                    ctx.lane_record(2, OUT + b)
-                ctx.lane_wait(0, OUT + (n - 1) % 2)
+                    ctx.lane_record(2, OUT + ob)
+                ctx.lane_wait(0, OUT + ((n - 1) % 2 if ws == 1 else 0))
 
             pipelined(2)
             torch.cuda.synchronize()
             # a stream of 10 applies (the first step's input copies and the last
             # step's result copy are not overlapped: amortised over the stream)
             kp = max(10, args.steps)
+            barrier()
+            torch.cuda.synchronize()
             e0.record(stream)
             pipelined(kp)
             e1.record(stream)
             torch.cuda.synchronize()
             tp = e0.elapsed_time(e1) / 1e3 / kp
-            ok = bool(torch.equal(outs[0], outs[1])) and bool(torch.equal(hout, outs[(kp - 1) % 2].cpu()))
+            if ws > 1:
+                import torch.distributed as dist
+                tt = torch.tensor([tp], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                tp = float(tt.item())
+            if ws == 1:
+                ok = bool(torch.equal(outs[0], outs[1])) and bool(torch.equal(hout, outs[(kp - 1) % 2].cpu()))
+            else:
+                ok = bool(torch.equal(hout, sh.full.cpu()))
             # the PCIe ceiling of this path: one pinned host -> device copy of L alone
             e0.record(stream)
             for _ in range(3):
@@ -483,8 +512,11 @@ def run_tci(args):
                    "d2h_bytes_per_step": int(d2h), "ms_per_step": tp * 1e3, "steps": kp,
                    "path": ("streaming applies through the C ABI: tci_copy_async (pinned host -> device, copy "
                             "lane 1) of step i+1's L, W1, W2, R, psi and tci_copy_async (device -> pinned host, "
-                            "lane 2) of step i-1's result overlap tci_heff_apply of step i (double-buffered "
-                            "device inputs/outputs, ordered by tci_lane_record / tci_lane_wait)"),
+                            "lane 2) of step i-1's result overlap " +
+                            ("tci_heff_apply" if ws == 1 else
+                             "tci_heff_apply_gather" if gather == "p2p" else "tci_heff_apply + tci_allgather") +
+                            " of step i (double-buffered device inputs, ordered by tci_lane_record / "
+                            "tci_lane_wait)"),
                    "results_identical_across_buffers": ok,
                    "h2d_gbs_measured": h2d_gbs,
                    "h2d_bound_ms_per_step": h2d / (h2d_gbs * 1e9) * 1e3,
@@ -593,7 +625,7 @@ def main():
                          "epilogue) or by ncclAllGather")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true",
-                    help="N = 1: report the single-call staged e2e instead of streaming applies")
+                    help="report the single-call e2e instead of a stream of applies")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-rows", type=int, default=4)

@@ -14,3 +14,5 @@ TCI_BENCH_BACKEND=gloo TCI_BENCH_SAME_DEVICE=1 timeout 900 python -m torch.distr
   --config cfg2 --alt none > gpurun_out/mp_bench4.log 2>&1
 echo "exit4 $?"
 tail -1 gpurun_out/mp_bench4.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['n_gpus'], d['config']['parallelism']); print('parity', d['parity'])"
+tail -1 gpurun_out/mp_bench4.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); e=d['e2e']; print('e2e4', e['value'], e['results_identical_across_buffers'], e['path'][:160], e['single_call']['path'][:80])"
+# (the --gather nccl variant cannot run here: NCCL refuses two ranks on one device)

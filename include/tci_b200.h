@@ -121,9 +121,12 @@ TCI_API const char *tci_last_error(void);
  *    complex product;
  *  TCI_GEMM_DMMA_4M: DMMA, textbook 4-multiplication product;
  *  TCI_GEMM_OZAKI_INT8: Ozaki-II integer-modular emulation on the INT8 tcgen05
- *    tensor cores (row/column scaling to >= 46-bit integers, exact residue
- *    GEMMs, exact CRT), used for GEMMs of >= 4e9 complex MACs; needs more
- *    scratch (the *_workspace_size queries account for it).
+ *    tensor cores (exact power-of-two K-balancing A diag(2^s), diag(2^-s) B,
+ *    row/column scaling to t >= 46-bit integers, exact residue GEMMs, exact
+ *    CRT), used for GEMMs of >= 4e9 complex MACs; needs more scratch (the
+ *    *_workspace_size queries account for it). Each such GEMM is guarded
+ *    (tci_set_ozaki_guard): when its estimated relative Frobenius truncation
+ *    error exceeds the context tolerance it is recomputed on DMMA.
  * The initial value comes from TCI_ZGEMM_ALGO = 3m | 4m | ozaki (read at
  * context creation). Setting it synchronizes the context stream. */
 #define TCI_GEMM_DMMA_3M 0
@@ -137,6 +140,27 @@ TCI_API tci_status_t tci_set_gemm_algorithm(tci_ctx_t ctx, int algo);
  * OUT_OF_RANGE when K is outside 1..131072 (the int32 exactness limit). */
 TCI_API int tci_ozaki_params(int64_t K, int *nmod, int *t, int *moduli);
 TCI_API tci_status_t tci_get_gemm_algorithm(tci_ctx_t ctx, int *algo);
+
+/* Accuracy guard of the Ozaki-II GEMMs (reading R26; the north
+ * star's 1e-12 relative-Frobenius bar). Entry (m,k) of A is rounded to an
+ * integer at scale 2^(t - E_m + s_k), so its error is eps 2^(E_m - t - s_k),
+ * |eps| <= 1/2 per real component. With independent errors
+ *   est^2 = c 4^-t (sum_m 4^E_m ||B'||_F^2 + ||A'||_F^2 sum_n 4^E_n) / ||C||_F^2
+ * (c = 1/6 complex, 1/12 real; A' = A diag(2^s), B' = diag(2^-s) B) is the
+ * expected squared relative Frobenius error; it is evaluated on the device
+ * after the CRT and, when est > tol, the GEMM is recomputed on DMMA (a
+ * launch gated by a device flag: no host synchronisation). tol <= 0 turns
+ * the guard off. Default 1e-13 (TCI_OZAKI_GUARD=0 at context creation: off).
+ * Errors: DEAD_CONTEXT, INVALID_ARGUMENT (NaN). */
+TCI_API tci_status_t tci_set_ozaki_guard(tci_ctx_t ctx, double tol);
+
+/* Statistics of the guard since context creation or the last reset
+ * (synchronizes the context stream): Ozaki GEMMs checked, how many were
+ * recomputed on DMMA, how many ran with a non-trivial K-balancing, the last
+ * and the maximum estimate. Any out-pointer may be NULL; reset != 0 zeroes
+ * the counters after reading. Errors: DEAD_CONTEXT, CUDA. */
+TCI_API tci_status_t tci_ozaki_guard_stats(tci_ctx_t ctx, int reset, int64_t *gemms, int64_t *fallbacks,
+                                           int64_t *balanced, double *last_est, double *max_est);
 
 /* Attach caller-owned device scratch memory of `bytes` bytes (256-byte
  * aligned pointer). Replaces any previous attachment; NULL/0 detaches. Calls

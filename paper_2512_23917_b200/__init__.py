@@ -52,6 +52,7 @@ EXPORTED = [
     "tci_mps_mpo_zipup_workspace_size", "tci_mps_mpo_zipup", "tci_heff_apply_staged",
     "tci_ipc_handle", "tci_ipc_open", "tci_ipc_close", "tci_gather_register", "tci_heff_apply_gather",
     "tci_gather_status", "tci_tebd_workspace_size", "tci_copy_async", "tci_lane_record", "tci_lane_wait",
+    "tci_set_ozaki_guard", "tci_ozaki_guard_stats",
 ]
 
 
@@ -122,6 +123,10 @@ _sig = {
     "tci_ozaki_params": ([ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                           ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_get_gemm_algorithm": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "tci_set_ozaki_guard": ([_vp, ctypes.c_double], ctypes.c_int),
+    "tci_ozaki_guard_stats": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
+                               ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tci_norm": ([_vp, _vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tci_normalize": ([_vp, _vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tci_scale": ([_vp, _vp, ctypes.c_double, ctypes.c_double, _vp], ctypes.c_int),
@@ -447,6 +452,19 @@ def tci_ozaki_params(K: int):
     return st, n.value, t.value, [mods[i] for i in range(n.value)]
 
 
+def tci_set_ozaki_guard(ctx: int, tol: float) -> None:
+    _ok(_lib.tci_set_ozaki_guard(_vp(ctx), float(tol)), "tci_set_ozaki_guard")
+
+
+def tci_ozaki_guard_stats(ctx: int, reset: bool = False) -> dict:
+    g, f, b = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    le, me = ctypes.c_double(), ctypes.c_double()
+    _ok(_lib.tci_ozaki_guard_stats(_vp(ctx), 1 if reset else 0, ctypes.byref(g), ctypes.byref(f), ctypes.byref(b),
+                                   ctypes.byref(le), ctypes.byref(me)), "tci_ozaki_guard_stats")
+    return {"gemms": g.value, "fallbacks": f.value, "balanced": b.value, "last_est": le.value,
+            "max_est": me.value}
+
+
 def tci_get_gemm_algorithm(ctx: int) -> int:
     x = ctypes.c_int()
     _ok(_lib.tci_get_gemm_algorithm(_vp(ctx), ctypes.byref(x)), "tci_get_gemm_algorithm")
@@ -743,6 +761,12 @@ class Context:
 
     def set_gemm_algorithm(self, algo: int):
         tci_set_gemm_algorithm(self.handle, algo)
+
+    def set_ozaki_guard(self, tol: float):
+        tci_set_ozaki_guard(self.handle, tol)
+
+    def ozaki_guard_stats(self, reset: bool = False) -> dict:
+        return tci_ozaki_guard_stats(self.handle, reset)
 
     def gemm_algorithm_name(self) -> str:
         return {TCI_GEMM_DMMA_3M: "dmma3m", TCI_GEMM_DMMA_4M: "dmma4m",

@@ -57,6 +57,8 @@ tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g) {
   OzProf pf{};
   GemmProblem gg = g;
   if (ctx->prof_on && g.zalgo == kZOzaki) gg.oz_prof = &pf;
+  gg.oz_tol = ctx->oz_tol;
+  gg.oz_guard = ctx->oz_guard;
   TCI_CUDA_CHECK(launch_gemm(gg, ctx->stream, &ctx->launches));
   ps.done();
   for (int i = 0; i < pf.n; i++) ctx->prof.push_back({kProfI8, pf.a[i], pf.b[i], pf.ops[i], 0.0});
@@ -235,12 +237,20 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   c->g_err = nullptr;
   c->svd_last_sweeps = 0;
   c->svd_last_off = 0.0;
+  c->oz_tol = kOzakiDefaultTol;
+  if (const char *e = getenv("TCI_OZAKI_GUARD")) {
+    if (!strcmp(e, "0") || !strcmp(e, "off")) c->oz_tol = 0.0;
+  }
+  c->oz_guard = nullptr;
   {
     cudaError_t e1 = cudaMalloc(&c->dev_scratch, reduce_scratch_bytes());
     cudaError_t e2 = cudaMallocHost(&c->host_scratch, 2 * kMaxMIOut * sizeof(double) + 64);
-    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaError_t e3 = cudaMalloc(&c->oz_guard, sizeof(OzGuard));
+    if (e3 == cudaSuccess) e3 = cudaMemset(c->oz_guard, 0, sizeof(OzGuard));
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
       if (c->dev_scratch) cudaFree(c->dev_scratch);
       if (c->host_scratch) cudaFreeHost(c->host_scratch);
+      if (c->oz_guard) cudaFree(c->oz_guard);
       delete c;
       TCI_FAIL(TCI_ERR_CUDA, "context scratch allocation failed");
     }
@@ -314,6 +324,8 @@ tci_status_t tci_destroy_context(tci_ctx_t ctx) {
     }
   if (ctx->dev_scratch) cudaFree(ctx->dev_scratch);
   if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
+  if (ctx->oz_guard) cudaFree(ctx->oz_guard);
+  ctx->oz_guard = nullptr;
   if (ctx->g_err) cudaFree(ctx->g_err);
   ctx->g_err = nullptr;
   ctx->g_nranks = 1;
@@ -347,6 +359,28 @@ tci_status_t tci_set_gemm_algorithm(tci_ctx_t ctx, int algo) {
     TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "unknown GEMM algorithm %d", algo);
   TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));   // scratch layouts may change
   ctx->zgemm_algo = algo;
+  return TCI_OK;
+}
+
+tci_status_t tci_set_ozaki_guard(tci_ctx_t ctx, double tol) {
+  CHECK(check_ctx(ctx));
+  if (!(tol == tol)) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "tolerance is NaN");
+  ctx->oz_tol = tol > 0.0 ? tol : 0.0;
+  return TCI_OK;
+}
+
+tci_status_t tci_ozaki_guard_stats(tci_ctx_t ctx, int reset, int64_t *gemms, int64_t *fallbacks, int64_t *balanced,
+                                   double *last_est, double *max_est) {
+  CHECK(check_ctx(ctx));
+  OzGuard h{};
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  TCI_CUDA_CHECK(cudaMemcpy(&h, ctx->oz_guard, sizeof h, cudaMemcpyDeviceToHost));
+  if (gemms) *gemms = (int64_t)h.gemms;
+  if (fallbacks) *fallbacks = (int64_t)h.fallbacks;
+  if (balanced) *balanced = (int64_t)h.balanced;
+  if (last_est) *last_est = h.last_est;
+  if (max_est) *max_est = h.max_est;
+  if (reset) TCI_CUDA_CHECK(cudaMemset(ctx->oz_guard, 0, sizeof(OzGuard)));
   return TCI_OK;
 }
 
@@ -1106,6 +1140,7 @@ tci_status_t tci_gather_register(tci_ctx_t ctx, int nranks, int rank, void *cons
     TCI_CUDA_CHECK(cudaMemset(ctx->g_err, 0, sizeof(int)));
   }
   TCI_CUDA_CHECK(gather_preload());
+  TCI_CUDA_CHECK(ozaki_preload());
   ctx->g_nranks = nranks;
   ctx->g_rank = rank;
   for (int i = 0; i < 8; i++) {

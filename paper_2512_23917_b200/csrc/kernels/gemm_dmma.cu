@@ -309,6 +309,8 @@ __device__ __forceinline__ void mma_step(Acc<C> &acc, const Frag<C> &f) {
 template <class C>
 __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p, int tiles_m,
                                                              int tiles_n) {
+  // Ozaki guard recomputation: nothing to do unless the guard asked for it
+  if (p.run_if && *reinterpret_cast<const volatile int *>(p.run_if) == 0) return;
   extern __shared__ __align__(128) char smem[];
   char *sA0 = smem;
   char *sB0 = smem + C::STAGES * C::A_STAGE * C::ESZ;
@@ -659,6 +661,16 @@ cudaError_t launch_tebd_fused(const TebdProblem &t, cudaStream_t s, int64_t *lau
   p.te_T = t.T;
   p.te_t[0] = t.t_a; p.te_t[1] = t.t_p; p.te_t[2] = t.t_q; p.te_t[3] = t.t_c;
   return run<TC>(p, s, launches);   // tiles: (chi_a / 64) x (chi_c / 64)
+}
+
+cudaError_t launch_gemm_dmma_if(const GemmProblem &p, const int *run_if, cudaStream_t s, int64_t *launches) {
+  GemmProblem q = p;
+  q.zalgo = kZ3M;
+  q.run_if = run_if;
+  q.npeer = 0;
+  q.rows_done = nullptr;
+  q.rows_needed = nullptr;
+  return launch_gemm_main(q, s, launches);
 }
 
 static cudaError_t launch_gemm_main(const GemmProblem &p, cudaStream_t s, int64_t *launches) {

@@ -90,8 +90,172 @@ using I8Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>,
 using I8Gemm = cutlass::gemm::device::GemmUniversalAdapter<I8Kernel>;
 
 // ---------------------------------------------------------------------------
-// step 1a: per-row (A) / per-column (B) exponent E with |x| < 2^E for every
-// entry (re and im) of that row/column; E = -100000 for an all-zero line
+// Small helpers: exact powers of two, exponent / mantissa split
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double pow2i(int h) {   // 2^h, h <= 1023; 0 below the normal range
+  return h < -1022 ? 0.0 : __hiloint2double((h + 1023) << 20, 0);
+}
+__device__ __forceinline__ double pow4i(int d) { return d < -511 ? 0.0 : pow2i(2 * d); }   // 4^d, d <= 0
+
+// the two exact power-of-two factors a * b = 2^sc used by scaled_magic
+__device__ __forceinline__ void scale_pair(int sc, double &a, double &b) {
+  const int h1 = sc >> 1, h2 = sc - h1;
+  if (h1 >= -1022 && h2 <= 1023) {
+    a = __hiloint2double((h1 + 1023) << 20, 0);
+    b = __hiloint2double((h2 + 1023) << 20, 0);
+  } else {
+    a = ldexp(1.0, h1);
+    b = ldexp(1.0, h2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// step 0 (K-balancing, R26): for every contraction index k the
+// exponent KX_k with |x| < 2^KX_k over all lines of one operand (re and im)
+// and the normalised sum of squares S_k = sum |x|^2 4^-KX_k. An online
+// (exponent, sum) pair: a larger exponent rescales the sum by a power of 4;
+// pairs merge in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void es_add(int &em, double &s, double x) {
+  if (x == 0.0) return;
+  int e;
+  const double f = frexp(x, &e);
+  if (e > em) {
+    s = em == -100000 ? 0.0 : s * pow4i(em - e);
+    em = e;
+  }
+  s = fma(f * f, pow4i(e - em), s);
+}
+__device__ __forceinline__ void es_merge(int &em, double &s, int e2, double s2) {
+  if (e2 == -100000) return;
+  if (e2 > em) {
+    s = em == -100000 ? 0.0 : s * pow4i(em - e2);
+    em = e2;
+  }
+  s = fma(s2, pow4i(e2 - em), s);
+}
+__device__ __forceinline__ void es_add(int &em, double &s, double2 x) {
+  es_add(em, s, x.x);
+  es_add(em, s, x.y);
+}
+
+// per-k statistics when the lines are contiguous (s_l == 1): one warp per k,
+// lanes walk the lines, fixed xor-tree merge
+template <class T>
+__global__ void __launch_bounds__(256) kstats_lines(const T *X, int64_t K, int64_t L, int64_t s_k, int *KE,
+                                                    double *KS) {
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= K) return;
+  int em = -100000;
+  double s = 0.0;
+  const T *p = X + k * s_k;
+  for (int64_t l = lane; l < L; l += 32) es_add(em, s, __ldg(p + l));
+  for (int o = 16; o; o >>= 1) {
+    const int e2 = __shfl_xor_sync(0xffffffffu, em, o);
+    const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    // both lanes of a pair must end with the same value: merge in lane order
+    if (lane & o) {
+      int ea = e2;
+      double sa = s2;
+      es_merge(ea, sa, em, s);
+      em = ea;
+      s = sa;
+    } else {
+      es_merge(em, s, e2, s2);
+    }
+  }
+  if (lane == 0) {
+    KE[k] = em;
+    KS[k] = s;
+  }
+}
+
+// per-k statistics when k is contiguous: thread per k (coalesced), blockIdx.y
+// takes a chunk of lines; partial pairs go to slots [chunk][k]
+template <class T>
+__global__ void __launch_bounds__(256) kstats_cols(const T *X, int64_t K, int64_t L, int64_t s_l, int64_t chunk,
+                                                   int *SE, double *SS) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int64_t l0 = blockIdx.y * chunk, l1 = min(L, l0 + chunk);
+  int em = -100000;
+  double s = 0.0;
+  const T *p = X + k;
+  int64_t l = l0;
+  for (; l + 4 <= l1; l += 4) {
+    const T v0 = __ldg(p + l * s_l), v1 = __ldg(p + (l + 1) * s_l);
+    const T v2 = __ldg(p + (l + 2) * s_l), v3 = __ldg(p + (l + 3) * s_l);
+    es_add(em, s, v0);
+    es_add(em, s, v1);
+    es_add(em, s, v2);
+    es_add(em, s, v3);
+  }
+  for (; l < l1; l++) es_add(em, s, __ldg(p + l * s_l));
+  SE[blockIdx.y * K + k] = em;
+  SS[blockIdx.y * K + k] = s;
+}
+
+__global__ void __launch_bounds__(256) kstats_merge(const int *SE, const double *SS, int nch, int64_t K, int *KE,
+                                                    double *KS) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  int em = -100000;
+  double s = 0.0;
+  for (int c = 0; c < nch; c++) es_merge(em, s, SE[c * K + k], SS[c * K + k]);
+  KE[k] = em;
+  KS[k] = s;
+}
+
+// s_k = floor((KB_k - KA_k) / 2): after A(:,k) 2^s_k and B(k,:) 2^-s_k both
+// maxima are within a factor 2 of their geometric mean (0 where either line
+// is all zero). A spread max_k s_k - min_k s_k <= 2 changes the truncation
+// error by at most ~4x: then no balancing (s = 0; bal = 0 keeps the per-line
+// fast path and the results bitwise those of the plain scheme).
+// Single block. SK has Kp entries (zero beyond K).
+__global__ void __launch_bounds__(1024) balance_prep(const int *KA, const int *KB, int64_t K, int64_t Kp, int enable,
+                                                     int *SK, int *bal) {
+  __shared__ int smin[32], smax[32];
+  __shared__ int use;
+  int lo = INT32_MAX, hi = INT32_MIN;
+  auto sval = [&](int64_t k) {
+    const int a = KA[k], b = KB[k];
+    if (a == -100000 || b == -100000) return 0;
+    return max(-500, min(500, (b - a) >> 1));   // arithmetic shift = floor
+  };
+  if (enable)
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+      if (KA[k] == -100000 || KB[k] == -100000) continue;
+      const int v = sval(k);
+      lo = min(lo, v);
+      hi = max(hi, v);
+    }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smin[threadIdx.x >> 5] = lo;
+    smax[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = INT32_MAX, b = INT32_MIN;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+      a = min(a, smin[w]);
+      b = max(b, smax[w]);
+    }
+    use = enable && a <= b && b - a > 2;
+    *bal = use;
+  }
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < Kp; k += blockDim.x) SK[k] = (use && k < K) ? sval(k) : 0;
+}
+
+// ---------------------------------------------------------------------------
+// step 1a: per-row (A) / per-column (B) exponent E with |x 2^(sgn s_k)| < 2^E
+// for every entry (re and im) of that row/column; E = -100000 for an
+// all-zero line. SK / bal: the K-balancing (applied when *bal != 0).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int exp_of(double x) {
   if (x == 0.0) return -100000;
@@ -99,23 +263,36 @@ __device__ __forceinline__ int exp_of(double x) {
   frexp(x, &e);   // |x| = f 2^e, 0.5 <= f < 1  ->  |x| < 2^e
   return e;
 }
+__device__ __forceinline__ int exp_of(double2 v) { return max(exp_of(v.x), exp_of(v.y)); }
+__device__ __forceinline__ int exp_of_shift(double2 v, int s) {
+  const int e = exp_of(v);
+  return e == -100000 ? e : e + s;
+}
+__device__ __forceinline__ int exp_of_shift(double v, int s) {
+  const int e = exp_of(v);
+  return e == -100000 ? e : e + s;
+}
 
-// line l (= m for A, n for B) of extent K; element (l, k) at base + l*s_l + k*s_k
-// (complex elements). K-contiguous lines: one warp per line. Line-contiguous
-// (s_l == 1): blockIdx.y splits K into chunks, consecutive threads take
-// consecutive lines (coalesced) and combine with atomicMax (max is order-
-// independent: deterministic). E must be pre-set to -100000 in that mode.
-__global__ void __launch_bounds__(256) line_exponent(const double2 *base, int64_t nlines, int64_t K,
-                                                     int64_t s_l, int64_t s_k, int *E) {
+// line l (= m for A, n for B) of extent K; element (l, k) at base + l*s_l + k*s_k.
+// K-contiguous lines: one warp per line. Line-contiguous (s_l == 1):
+// blockIdx.y splits K into chunks, consecutive threads take consecutive lines
+// (coalesced) and combine with atomicMax (max is order-independent:
+// deterministic). E must be pre-set to -100000 in that mode.
+template <class T>
+__global__ void __launch_bounds__(256) line_exponent(const T *base, int64_t nlines, int64_t K, int64_t s_l,
+                                                     int64_t s_k, int *E, const int *SK, int sgn,
+                                                     const int *bal) {
+  const bool b = SK && *bal;
   if (s_k == 1) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= nlines) return;
     int e = -100000;
-    const double2 *p = base + warp * s_l;
-    for (int64_t k = lane; k < K; k += 32) {
-      const double2 v = p[k];
-      e = max(e, max(exp_of(v.x), exp_of(v.y)));
+    const T *p = base + warp * s_l;
+    if (b) {
+      for (int64_t k = lane; k < K; k += 32) e = max(e, exp_of_shift(p[k], sgn * SK[k]));
+    } else {
+      for (int64_t k = lane; k < K; k += 32) e = max(e, exp_of(p[k]));
     }
     for (int o = 16; o; o >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
     if (lane == 0) E[warp] = e;
@@ -125,22 +302,38 @@ __global__ void __launch_bounds__(256) line_exponent(const double2 *base, int64_
     const int64_t kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc;
     const int64_t k1 = min(K, k0 + kc);
     int e = -100000;
-    const double2 *p = base + l * s_l;
-    for (int64_t k = k0; k < k1; k++) {
-      const double2 v = p[k * s_k];
-      e = max(e, max(exp_of(v.x), exp_of(v.y)));
+    const T *p = base + l * s_l;
+    if (b) {
+      for (int64_t k = k0; k < k1; k++) e = max(e, exp_of_shift(p[k * s_k], sgn * SK[k]));
+    } else {
+      for (int64_t k = k0; k < k1; k++) e = max(e, exp_of(p[k * s_k]));
     }
     atomicMax(E + l, e);
   }
 }
 
-__global__ void batch_moduli(int32_t *p, int planes) {
+__global__ void batch_moduli(int32_t *p, int planes, int per_mod) {
   const int i = threadIdx.x;
-  if (i < planes) p[i] = c_moduli[i / 3];
+  if (i < planes) p[i] = c_moduli[i / per_mod];
 }
 
 __global__ void fill_int(int *p, int64_t n, int v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// max of E[0..n) into *out (single block; the guard's normalisation of the
+// CRT's row sums)
+__global__ void __launch_bounds__(1024) exp_max(const int *E, int64_t n, int *out) {
+  __shared__ int sm[32];
+  int v = -100000;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v = max(v, E[i]);
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++) v = max(v, sm[w]);
+    *out = max(v, sm[0]);
+  }
 }
 
 // 1/m_l rounded to double (IEEE division, evaluated at compile time)
@@ -214,10 +407,11 @@ __device__ __forceinline__ void line_scale(int t, int E, double &s2a, double &s2
 // ---------------------------------------------------------------------------
 // step 1b + 2a: residue planes. out[(l*3 + comp)][line][kp] int8, K-major,
 // comp 0 = re, 1 = im, 2 = re + im; zero for k >= K or line >= nlines.
-// Each thread produces 8 consecutive k of one line for all planes.
+// Each thread produces 8 consecutive k of one line for all planes. With the
+// K-balancing active the scale of entry (line, k) is 2^(t - E_line + sgn s_k).
 // ---------------------------------------------------------------------------
 struct ResArgs {
-  const double2 *base;
+  const void *base;         // double2 (complex) / double (real)
   int64_t nlines, K, Kp, s_l, s_k;
   int64_t line0;            // first line of the chunk (global index)
   int64_t lines_out;        // rows in the output planes (chunk, padded)
@@ -226,7 +420,19 @@ struct ResArgs {
   int nmod;
   int8_t *out;
   int64_t plane_stride;     // lines_out * Kp
+  const int *SK;            // K-balancing exponents (Kp entries) or null
+  const int *bal;           // device flag: balancing active
+  int sgn;                  // +1 for A, -1 for B
 };
+
+// per-element scale factors of 8 consecutive k (SK has Kp >= k0 + 8 entries)
+__device__ __forceinline__ void elem_scales(const ResArgs &a, int E, int64_t k0, double (&fa)[8], double (&fb)[8]) {
+  const int4 q0 = *reinterpret_cast<const int4 *>(a.SK + k0);
+  const int4 q1 = *reinterpret_cast<const int4 *>(a.SK + k0 + 4);
+  const int s[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+  for (int j = 0; j < 8; j++) scale_pair(a.t - E + a.sgn * s[j], fa[j], fb[j]);
+}
 
 __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs a) {
   constexpr int NV = 8;
@@ -239,14 +445,21 @@ __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs 
   const int64_t line = a.line0 + row;
   ResVals<NV> x;
   if (line < a.nlines && a.E[line] > -100000) {
-    double s2a, s2b;
-    line_scale(a.t, a.E[line], s2a, s2b);
-    const double2 *p = a.base + line * a.s_l;
+    const double2 *p = static_cast<const double2 *>(a.base) + line * a.s_l;
     double2 v[NV];
 #pragma unroll
     for (int j = 0; j < NV; j++) v[j] = k0 + j < a.K ? __ldg(p + (k0 + j) * a.s_k) : make_double2(0.0, 0.0);
+    if (a.SK && *a.bal) {
+      double fa[NV], fb[NV];
+      elem_scales(a, a.E[line], k0, fa, fb);
 #pragma unroll
-    for (int j = 0; j < NV; j++) x.set(j, scaled_magic(v[j].x, s2a, s2b), scaled_magic(v[j].y, s2a, s2b));
+      for (int j = 0; j < NV; j++) x.set(j, scaled_magic(v[j].x, fa[j], fb[j]), scaled_magic(v[j].y, fa[j], fb[j]));
+    } else {
+      double s2a, s2b;
+      line_scale(a.t, a.E[line], s2a, s2b);
+#pragma unroll
+      for (int j = 0; j < NV; j++) x.set(j, scaled_magic(v[j].x, s2a, s2b), scaled_magic(v[j].y, s2a, s2b));
+    }
   } else {
 #pragma unroll
     for (int j = 0; j < NV; j++) x.set(j, kMagic, kMagic);
@@ -274,19 +487,23 @@ __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArg
     const int li = tid % 32;
     const int64_t row = r0 + li, line = a.line0 + row;
     const bool ok = row < a.lines_out && line < a.nlines && a.E[line] > -100000;
+    const bool b = a.SK && *a.bal;
     double s2a = 0.0, s2b = 0.0;   // 0 -> scaled value 0 for dead lines
-    if (ok) line_scale(a.t, a.E[line], s2a, s2b);
+    if (ok && !b) line_scale(a.t, a.E[line], s2a, s2b);
+    const double2 *base = static_cast<const double2 *>(a.base);
     double2 v[8];
 #pragma unroll
     for (int jj = 0; jj < 8; jj++) {
       const int64_t k = kb + tid / 32 + jj * 8;
-      v[jj] = ok && k < a.K ? __ldg(a.base + line + k * a.s_k) : make_double2(0.0, 0.0);
+      v[jj] = ok && k < a.K ? __ldg(base + line + k * a.s_k) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int jj = 0; jj < 8; jj++) {
       const int j = tid / 32 + jj * 8;
-      sx[0][li][j] = scaled_magic(v[jj].x, s2a, s2b);
-      sx[1][li][j] = scaled_magic(v[jj].y, s2a, s2b);
+      double fa = s2a, fb = s2b;
+      if (ok && b) scale_pair(a.t - a.E[line] + a.sgn * a.SK[kb + j], fa, fb);
+      sx[0][li][j] = scaled_magic(v[jj].x, fa, fb);
+      sx[1][li][j] = scaled_magic(v[jj].y, fa, fb);
     }
   }
   __syncthreads();
@@ -318,6 +535,9 @@ __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArg
 // R_j = S_j - q M_j is exact (q < 2^14, M_j < 2^38); carries normalise
 // the chunks to |R_0|, |R_1| <= 2^36; C' = R_2 2^74 + R_1 2^37 + R_0 is then
 // converted with ~1 ulp error.
+// Guard (R26): every tile (one row, TW columns) also leaves
+// sum_n |C'(m,n) 2^(-2t + E_n - max E_n)|^2 in rowsq[m * tpr + tile], the
+// row's squared norm up to the factor 4^(E_m + max E_n).
 // ---------------------------------------------------------------------------
 struct CrtArgs {
   const uint8_t *D;         // [3n][Mc][Np], residues in [0, m)
@@ -332,18 +552,20 @@ struct CrtArgs {
   int64_t c_sm;
   int npeer;                // peer-memory all-gather: the same element also
   double2 *peer[7];         // stored at peer[p] + (m c_sm + n) over NVLink
+  double *rowsq;            // guard row sums [M][tpr] or null
+  const int *eb_max;        // device: max_n E_n
 };
 
 template <int NCH>
-__device__ __forceinline__ double crt_value(const double (&S)[NCH], const CrtArgs &a) {
+__device__ __forceinline__ double crt_value(const double (&S)[NCH], const double (&Mch)[4], double Minv) {
   const double two37 = 137438953472.0, inv37 = 1.0 / 137438953472.0;
   double xe = S[NCH - 1];
 #pragma unroll
   for (int j = NCH - 2; j >= 0; j--) xe = fma(xe, two37, S[j]);
-  const double q = rint(xe * a.Minv);
+  const double q = rint(xe * Minv);
   double r[NCH];
 #pragma unroll
-  for (int j = 0; j < NCH; j++) r[j] = fma(-q, a.Mch[j], S[j]);
+  for (int j = 0; j < NCH; j++) r[j] = fma(-q, Mch[j], S[j]);
 #pragma unroll
   for (int j = 0; j < NCH - 1; j++) {
     const double cy = rint(r[j] * inv37);
@@ -354,6 +576,20 @@ __device__ __forceinline__ double crt_value(const double (&S)[NCH], const CrtArg
 #pragma unroll
   for (int j = NCH - 2; j >= 0; j--) x = fma(x, two37, r[j]);
   return x;
+}
+
+// fixed-order block sum of one double per thread (THREADS = 32 * warps):
+// xor tree inside each warp, warps in ascending order by thread 0
+template <int THREADS>
+__device__ __forceinline__ double block_sum_fixed(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < THREADS / 32; w++) s += red[w];
+  return s;
 }
 
 // Persistent kernel over tiles of (one row, TW = CPT * THREADS columns). The
@@ -375,12 +611,14 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
   using Shape = CrtShape<CPT, THREADS, STAGES>;
   constexpr int TW = Shape::kTW;
   extern __shared__ __align__(128) uint8_t crt_smem[];
+  __shared__ double red[2][THREADS / 32];
   constexpr int kStage = 3 * NMOD * TW;
   uint64_t *bar = reinterpret_cast<uint64_t *>(crt_smem + STAGES * kStage);
   const int64_t tpr = (a.Np + TW - 1) / TW;   // tiles per row
   const int64_t ntiles = a.Mc * tpr;
   const int64_t plane = a.Mc * a.Np;
   const int tid = threadIdx.x;
+  const int ebm = a.rowsq ? *a.eb_max : 0;
 
   auto issue = [&](int64_t tile, int s) {   // warp 0
     const int64_t r = tile / tpr, c0 = (tile % tpr) * TW;
@@ -408,6 +646,7 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
     const int s = it % STAGES;
     mbar_wait(&bar[s], (uint32_t)((it / STAGES) & 1));
     const int64_t r = tile / tpr, n0 = (tile % tpr) * TW + CPT * tid;
+    double sq = 0.0;
     if (n0 < a.N) {
       const uint8_t *st = crt_smem + s * kStage + CPT * tid;
       double Sr[CPT][NCH], Si[CPT][NCH];
@@ -460,7 +699,7 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
         const int eb = a.EB[n];
         double2 out = make_double2(0.0, 0.0);
         if (ea > -100000 && eb > -100000) {
-          const double xr = crt_value(Sr[e], a), xi = crt_value(Si[e], a);
+          const double xr = crt_value(Sr[e], a.Mch, a.Minv), xi = crt_value(Si[e], a.Mch, a.Minv);
           const int sc = sc0 + eb;
           if (sc >= -1022 && sc <= 1023) {   // 2^sc is a normal double: one exact multiply
             const double f = __hiloint2double((sc + 1023) << 20, 0);
@@ -468,13 +707,30 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
           } else {
             out = make_double2(ldexp(xr, sc), ldexp(xi, sc));
           }
+          if (a.rowsq) {
+            const double g = pow2i(-2 * a.t + eb - ebm);
+            sq = fma(xr * g, xr * g, sq);
+            sq = fma(xi * g, xi * g, sq);
+          }
         }
         __stcs(&a.C[m * a.c_sm + n], out);
 #pragma unroll 1
         for (int pp = 0; pp < a.npeer; pp++) __stcs(&a.peer[pp][m * a.c_sm + n], out);
       }
     }
+    if (a.rowsq) {
+      // deterministic tile sum; red is double-buffered across iterations
+      double v = sq;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((tid & 31) == 0) red[it & 1][tid >> 5] = v;
+    }
     __syncthreads();   // stage s fully consumed
+    if (a.rowsq && tid == 0) {
+      double v = 0.0;
+      for (int w = 0; w < THREADS / 32; w++) v += red[it & 1][w];
+      a.rowsq[(a.m0 + r) * tpr + tile % tpr] = v;
+    }
     const int64_t next = tile + (int64_t)STAGES * gridDim.x;
     if (tid < 32 && next < ntiles) issue(next, s);
   }
@@ -498,6 +754,7 @@ cudaError_t launch_crt_cfg(const CrtArgs &c, int64_t mc, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+constexpr int kCrtTW = 1024;   // CRT tile width (columns): 4 per thread x 256 threads
 // 4 columns x 256 threads x 2 stages: measured best of {2,4} x {128,256} x
 // {2,3,4} on the target shapes (the kernel is XU/FP64-issue bound there).
 template <int NMOD, int NCH>
@@ -506,12 +763,306 @@ cudaError_t launch_crt(const CrtArgs &c, int64_t mc, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// float64 (real) Ozaki-II: one residue plane per modulus (no 3M split), the
+// same scaling, moduli, INT8 GEMM + mod-m epilogue and CRT; n GEMMs instead
+// of 3n. C'(m, n) = sum_k A'(m, k) B'(k, n) with |C'| <= K 2^(2t) <= M/8.
+// ---------------------------------------------------------------------------
+// K-contiguous: 8 consecutive k of one line per thread, 8 bytes per plane
+__global__ void __launch_bounds__(256) residues_real(const __grid_constant__ ResArgs a) {
+  const int64_t kgroups = a.Kp / 8;
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= a.lines_out * kgroups) return;
+  const int64_t row = gid / kgroups, k0 = (gid % kgroups) * 8, line = a.line0 + row;
+  double x[8];
+  int lo[8];
+  if (line < a.nlines && a.E[line] > -100000) {
+    const double *p = static_cast<const double *>(a.base) + line * a.s_l;
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) v[j] = k0 + j < a.K ? __ldg(p + (k0 + j) * a.s_k) : 0.0;
+    double fa[8], fb[8];
+    if (a.SK && *a.bal) {
+      elem_scales(a, a.E[line], k0, fa, fb);
+    } else {
+      double s2a, s2b;
+      line_scale(a.t, a.E[line], s2a, s2b);
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        fa[j] = s2a;
+        fb[j] = s2b;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const double m = scaled_magic(v[j], fa[j], fb[j]);
+      x[j] = m - kMagic;
+      lo[j] = __double2loint(m);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      x[j] = 0.0;
+      lo[j] = 0;
+    }
+  }
+  int8_t *dst = a.out + row * a.Kp + k0;
+  for (int l = 0; l < a.nmod; l++) {
+    const int mi = c_moduli[l];
+    const double minv = c_minv[l];
+    int r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = bal_res(x[j], lo[j], minv, mi);
+    *reinterpret_cast<uint2 *>(dst + (int64_t)l * a.plane_stride) =
+        make_uint2(pack4(r[0], r[1], r[2], r[3]), pack4(r[4], r[5], r[6], r[7]));
+  }
+}
+
+// line-contiguous: 32-line x 64-k tile through shared memory (as residues_t)
+__global__ void __launch_bounds__(256) residues_real_t(const __grid_constant__ ResArgs a) {
+  __shared__ double sx[32][65];
+  const int64_t ntk = a.Kp / 64;
+  const int64_t tl = blockIdx.x / ntk, tk = blockIdx.x % ntk;
+  const int64_t r0 = tl * 32, kb = tk * 64;
+  const int tid = threadIdx.x;
+  {
+    const int li = tid % 32;
+    const int64_t row = r0 + li, line = a.line0 + row;
+    const bool ok = row < a.lines_out && line < a.nlines && a.E[line] > -100000;
+    const bool b = a.SK && *a.bal;
+    double s2a = 0.0, s2b = 0.0;
+    if (ok && !b) line_scale(a.t, a.E[line], s2a, s2b);
+    const double *base = static_cast<const double *>(a.base);
+    double v[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; jj++) {
+      const int64_t k = kb + tid / 32 + jj * 8;
+      v[jj] = ok && k < a.K ? __ldg(base + line + k * a.s_k) : 0.0;
+    }
+#pragma unroll
+    for (int jj = 0; jj < 8; jj++) {
+      const int j = tid / 32 + jj * 8;
+      double fa = s2a, fb = s2b;
+      if (ok && b) scale_pair(a.t - a.E[line] + a.sgn * a.SK[kb + j], fa, fb);
+      sx[li][j] = scaled_magic(v[jj], fa, fb);
+    }
+  }
+  __syncthreads();
+  const int li = tid / 8, kq = (tid % 8) * 8;
+  const int64_t row = r0 + li;
+  if (row >= a.lines_out) return;
+  double x[8];
+  int lo[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const double m = sx[li][kq + j];
+    x[j] = m - kMagic;
+    lo[j] = __double2loint(m);
+  }
+  int8_t *dst = a.out + row * a.Kp + kb + kq;
+  for (int l = 0; l < a.nmod; l++) {
+    const int mi = c_moduli[l];
+    const double minv = c_minv[l];
+    int r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = bal_res(x[j], lo[j], minv, mi);
+    *reinterpret_cast<uint2 *>(dst + (int64_t)l * a.plane_stride) =
+        make_uint2(pack4(r[0], r[1], r[2], r[3]), pack4(r[4], r[5], r[6], r[7]));
+  }
+}
+
+// CRT for real outputs: the residue of C' modulo m_l is the GEMM's byte in
+// [0, m_l) itself; 4 consecutive columns per thread (one 32-bit load per
+// plane); block b covers row b / tpr, columns (b % tpr) * 1024 + [0, 1024)
+struct CrtArgsR {
+  const uint8_t *D;          // [n][Mc][Np]
+  int64_t Mc, N, Np, m0;
+  int nmod;
+  double W[kMaxMod][4];
+  double Mch[4];
+  double Minv;
+  const int *EA, *EB;
+  int t;
+  double *C;
+  int64_t c_sm;
+  double *rowsq;             // guard row sums [M][tpr] or null
+  const int *eb_max;
+};
+
+template <int NMOD, int NCH>
+__global__ void __launch_bounds__(256) crt_real_kernel(const __grid_constant__ CrtArgsR a) {
+  __shared__ double red[8];
+  const int64_t tpr = (a.Np + kCrtTW - 1) / kCrtTW;
+  const int64_t r = blockIdx.x / tpr, tile = blockIdx.x % tpr;
+  const int64_t n0 = tile * kCrtTW + 4 * threadIdx.x;
+  const int64_t plane = a.Mc * a.Np;
+  const int64_t m = a.m0 + r;
+  double sq = 0.0;
+  if (n0 < a.N) {
+    double S[4][NCH];
+#pragma unroll
+    for (int e = 0; e < 4; e++)
+#pragma unroll
+      for (int j = 0; j < NCH; j++) S[e][j] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NMOD; i++) {
+      const uint32_t w4 = __ldg(reinterpret_cast<const uint32_t *>(a.D + i * plane + r * a.Np + n0));
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const double c = (double)((w4 >> (8 * e)) & 0xffu);
+#pragma unroll
+        for (int j = 0; j < NCH; j++) S[e][j] = fma(c, a.W[i][j], S[e][j]);
+      }
+    }
+    const int ea = a.EA[m];
+    const int ebm = a.rowsq ? *a.eb_max : 0;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int64_t n = n0 + e;
+      if (n >= a.N) break;
+      const int eb = a.EB[n];
+      double out = 0.0;
+      if (ea > -100000 && eb > -100000) {
+        const double x = crt_value(S[e], a.Mch, a.Minv);
+        const int sc = -(2 * a.t - ea) + eb;
+        out = (sc >= -1022 && sc <= 1023) ? x * __hiloint2double((sc + 1023) << 20, 0) : ldexp(x, sc);
+        if (a.rowsq) {
+          const double g = pow2i(-2 * a.t + eb - ebm);
+          sq = fma(x * g, x * g, sq);
+        }
+      }
+      a.C[m * a.c_sm + n] = out;
+    }
+  }
+  if (a.rowsq) {
+    const double v = block_sum_fixed<256>(sq, red);
+    if (threadIdx.x == 0) a.rowsq[m * tpr + tile] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Accuracy guard (R26). Operand entry (m, k) of A is rounded to an
+// integer at scale 2^(t - E_m + s_k): its error is eps 2^(E_m - t - s_k) with
+// eps uniform in [-1/2, 1/2] per real component, so (independent errors)
+//   E ||C~ - AB||_F^2 = c 4^-t (S_M ||B'||_F^2 + ||A'||_F^2 S_N),
+// S_M = sum_m 4^E_m, S_N = sum_n 4^E_n, A' = A diag(2^s), B' = diag(2^-s) B,
+// c = 1/6 (complex: two components) or 1/12 (real). The kernel compares
+// est = sqrt(that) with tol ||C~||_F and sets the recomputation flag. All
+// sums are normalised by 4^max E (no overflow) and taken in a fixed order.
+// Without per-k statistics of A (A streamed in row chunks) ||A'||^2 is
+// bounded by (2) K S_M.
+// ---------------------------------------------------------------------------
+struct GuardArgs {
+  const int *EA, *EB;
+  int64_t M, N, K, tpr;
+  const int *KA, *KB, *SK;     // KA may be null
+  const double *KSA, *KSB;     // KSA null with KA
+  const double *rowsq;
+  int t, cplx;
+  double tol;
+  int *flag;                   // out: 1 = recompute on DMMA
+  int *bal;                    // balancing was active
+  OzGuard *rec;                // optional statistics
+};
+
+__global__ void __launch_bounds__(1024) guard_finalize(const __grid_constant__ GuardArgs g) {
+  __shared__ double red[32];
+  const int tid = threadIdx.x;
+  auto bsum = [&](double v) -> double {   // fixed-order block sum, result broadcast
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w];
+    return s;
+  };
+  auto bmax = [&](const int *E, int64_t n) -> int {
+    int v = -100000;
+    for (int64_t i = tid; i < n; i += blockDim.x) v = max(v, E[i]);
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = (double)v;
+    __syncthreads();
+    double s = -100000.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s = fmax(s, red[w]);
+    return (int)s;
+  };
+  const int ea = bmax(g.EA, g.M);
+  const int eb = bmax(g.EB, g.N);
+  double sM = 0.0, sN = 0.0, nA = 0.0, nB = 0.0, nC = 0.0;
+  for (int64_t m = tid; m < g.M; m += blockDim.x) {
+    const int e = g.EA[m];
+    if (e == -100000) continue;
+    const double w = pow4i(e - ea);
+    sM += w;
+    double r = 0.0;
+    for (int64_t j = 0; j < g.tpr; j++) r += g.rowsq[m * g.tpr + j];
+    nC = fma(w, r, nC);
+  }
+  for (int64_t n = tid; n < g.N; n += blockDim.x)
+    if (g.EB[n] != -100000) sN += pow4i(g.EB[n] - eb);
+  for (int64_t k = tid; k < g.K; k += blockDim.x) {
+    const int s = g.SK ? g.SK[k] : 0;
+    if (g.KA && g.KA[k] != -100000) nA = fma(g.KSA[k], pow4i(g.KA[k] + s - ea), nA);
+    if (g.KB[k] != -100000) nB = fma(g.KSB[k], pow4i(g.KB[k] - s - eb), nB);
+  }
+  sM = bsum(sM);
+  sN = bsum(sN);
+  nC = bsum(nC);
+  nB = bsum(nB);
+  nA = g.KA ? bsum(nA) : (g.cplx ? 2.0 : 1.0) * (double)g.K * sM;
+  if (tid == 0) {
+    int fall = 0;
+    double est = 0.0;
+    if (ea != -100000 && eb != -100000) {
+      // 4^-t applied as (2^-t)^2 on the normalised sums
+      const double c = g.cplx ? 1.0 / 6.0 : 1.0 / 12.0;
+      const double e2 = c * (sM * nB + nA * sN);
+      const double st = ldexp(1.0, -g.t);
+      const double errn = sqrt(e2) * st;   // ||dC|| / 2^(ea + eb)
+      const double cn = sqrt(nC);          // ||C|| / 2^(ea + eb)
+      est = cn > 0.0 ? errn / cn : (errn > 0.0 ? INFINITY : 0.0);
+      fall = !(est <= g.tol);
+    }
+    *g.flag = fall;
+    if (g.rec) {
+      g.rec->gemms++;
+      g.rec->fallbacks += fall;
+      g.rec->balanced += (g.bal && *g.bal) ? 1 : 0;
+      g.rec->last_est = est;
+      if (!(est <= g.rec->max_est)) g.rec->max_est = est;
+    }
+  }
+}
+
+// the guard's recomputation also reaches the peers' copies of the slab
+// (fused all-gather): C rows [0, M) with row stride c_sm, copied to the same
+// offsets of every peer buffer when *run_if != 0
+struct PeerSet {
+  double2 *p[7];
+};
+__global__ void __launch_bounds__(256) copy_to_peers_if(const double2 *C, int64_t M, int64_t N, int64_t c_sm, int np,
+                                                       const __grid_constant__ PeerSet ps, const int *run_if) {
+  if (*reinterpret_cast<const volatile int *>(run_if) == 0) return;
+  double2 *const *pp = ps.p;
+  const int64_t total = M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / N, n = i % N;
+    const double2 v = C[m * c_sm + n];
+    for (int p = 0; p < np; p++) pp[p][m * c_sm + n] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host planning
 // ---------------------------------------------------------------------------
 struct OzPlan {
   int nmod, t;
-  int64_t Kp, Np, Mc, chunks;
-  size_t off_EA, off_EB, off_Bres, off_Ares, off_D, off_mod, off_cutlass, total;
+  int64_t Kp, Np, Mc, chunks, tpr, nch;
+  size_t off_EA, off_EB, off_Bres, off_Ares, off_D, off_mod, off_cutlass;
+  size_t off_KA, off_KB, off_SK, off_KSA, off_KSB, off_slotE, off_slotS, off_rowsq, off_misc;
+  size_t total;
 };
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -537,6 +1088,8 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_row
   p.Mc = std::min<int64_t>(round_up(M, 256), mc);
   if (max_rows > 0) p.Mc = std::min<int64_t>(p.Mc, std::max<int64_t>(256, round_up(max_rows, 256)));
   p.chunks = (M + p.Mc - 1) / p.Mc;
+  p.tpr = (p.Np + kCrtTW - 1) / kCrtTW;
+  p.nch = std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 22) / p.Kp));
   size_t off = 0;
   p.off_EA = off; off = align_up(off + (size_t)M * 4);
   p.off_EB = off; off = align_up(off + (size_t)N * 4);
@@ -544,6 +1097,15 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_row
   p.off_Ares = off; off = align_up(off + (size_t)planes * p.Mc * p.Kp);
   p.off_D = off; off = align_up(off + (size_t)planes * p.Mc * p.Np);
   p.off_mod = off; off = align_up(off + (size_t)planes * 4);
+  p.off_KA = off; off = align_up(off + (size_t)p.Kp * 4);
+  p.off_KB = off; off = align_up(off + (size_t)p.Kp * 4);
+  p.off_SK = off; off = align_up(off + (size_t)p.Kp * 4);
+  p.off_KSA = off; off = align_up(off + (size_t)p.Kp * 8);
+  p.off_KSB = off; off = align_up(off + (size_t)p.Kp * 8);
+  p.off_slotE = off; off = align_up(off + (size_t)p.nch * p.Kp * 4);
+  p.off_slotS = off; off = align_up(off + (size_t)p.nch * p.Kp * 8);
+  p.off_rowsq = off; off = align_up(off + (size_t)M * p.tpr * 8);
+  p.off_misc = off; off = align_up(off + 64);
   p.off_cutlass = off; off = align_up(off + ((size_t)64 << 20));   // CUTLASS workspace (small)
   p.total = off;
   return p;
@@ -570,207 +1132,205 @@ unsigned inv_mod(unsigned a, unsigned m) {
   return (unsigned)(t < 0 ? t + (int)m : t);
 }
 
-// ===========================================================================
-// float64 (real) Ozaki-II: one residue plane per modulus (no 3M split), the
-// same scaling, moduli, INT8 GEMM + mod-m epilogue and CRT; n GEMMs instead
-// of 3n. C'(m, n) = sum_k A'(m, k) B'(k, n) with |C'| <= K 2^(2t) <= M/8.
-// ===========================================================================
-__global__ void __launch_bounds__(256) line_exponent_r(const double *base, int64_t nlines, int64_t K, int64_t s_l,
-                                                       int64_t s_k, int *E) {
-  if (s_k == 1) {
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= nlines) return;
-    int e = -100000;
-    const double *p = base + warp * s_l;
-    for (int64_t k = lane; k < K; k += 32) e = max(e, exp_of(p[k]));
-    for (int o = 16; o; o >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
-    if (lane == 0) E[warp] = e;
-  } else {
-    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l >= nlines) return;
-    const int64_t kc = (K + gridDim.y - 1) / gridDim.y, k0 = blockIdx.y * kc;
-    const int64_t k1 = min(K, k0 + kc);
-    int e = -100000;
-    const double *p = base + l * s_l;
-    for (int64_t k = k0; k < k1; k++) e = max(e, exp_of(p[k * s_k]));
-    atomicMax(E + l, e);
+// CRT weight chunks (37 bits each), M chunks and ~1/M for nmod moduli
+void crt_constants(int nmod, double (&W)[kMaxMod][4], double (&Mch)[4], double &Minv) {
+  u128 Mp = 1;
+  for (int l = 0; l < nmod; l++) Mp *= (u128)kModuli[l];
+  const u128 mask = ((u128)1 << 37) - 1;
+  for (int l = 0; l < nmod; l++) {
+    const unsigned ml = (unsigned)kModuli[l];
+    const u128 Ml = Mp / ml;
+    const u128 wl = mulmod_small(Ml, inv_mod((unsigned)(Ml % ml), ml), Mp);
+    for (int j = 0; j < 4; j++) W[l][j] = (double)(uint64_t)((wl >> (37 * j)) & mask);
   }
+  for (int j = 0; j < 4; j++) Mch[j] = (double)(uint64_t)((Mp >> (37 * j)) & mask);
+  Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
 }
 
-struct ResArgsR {
-  const double *base;
-  int64_t nlines, K, Kp, s_l, s_k;
-  int64_t line0, lines_out;
-  const int *E;
-  int t, nmod;
-  int8_t *out;
-  int64_t plane_stride;
+// one batched INT8 GEMM: D[b][m][n] = (sum_k A[b][m][k] B[b][n][k]) mod m_b
+cudaError_t int8_gemm(const GemmProblem &g, const OzPlan &p, char *w, int8_t *Ares, int8_t *Bres, uint8_t *D,
+                      int32_t *bmod, int64_t mc, int planes, cudaStream_t s, int64_t *launches) {
+  using SA = typename I8Gemm::GemmKernel::StrideA;
+  using SB = typename I8Gemm::GemmKernel::StrideB;
+  using SC = typename I8Gemm::GemmKernel::StrideC;
+  using SD = typename I8Gemm::GemmKernel::StrideD;
+  const int Mi = (int)mc, Ni = (int)p.Np, Ki = (int)p.Kp, Li = planes;
+  SA sa = cutlass::make_cute_packed_stride(SA{}, {Mi, Ki, Li});
+  SB sb = cutlass::make_cute_packed_stride(SB{}, {Ni, Ki, Li});
+  SC sc = cutlass::make_cute_packed_stride(SC{}, {Mi, Ni, Li});
+  SD sd = cutlass::make_cute_packed_stride(SD{}, {Mi, Ni, Li});
+  typename ModEVT::Arguments fargs{{}, {{0}, {bmod}, {Stride<_0, _0, int64_t>{_0{}, _0{}, int64_t(1)}}}, {}};
+  typename I8Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {Mi, Ni, Ki, Li},
+                                  {Ares, sa, Bres, sb}, {fargs, nullptr, sc, D, sd}};
+  // Tile order: raster along M in swizzled groups of 8. With K = 20480 (GEMM4)
+  // each 256x256 tile streams 5.2 MB A and B panels; the default order re-read
+  // them from DRAM ~4.5x (50 GB per launch, ncu); this order halves that
+  // (24 GB) and the launch time drops 8% (profiles/r01_ncu_target_ozaki.json).
+  args.scheduler.max_swizzle_size = 8;
+  args.scheduler.raster_order = cutlass::gemm::kernel::detail::RasterOrderOptions::AlongM;
+  I8Gemm gemm;
+  if (gemm.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorNotSupported;
+  const size_t cws = I8Gemm::get_workspace_size(args);
+  if (cws > ((size_t)64 << 20)) return cudaErrorInvalidValue;
+  if (gemm.initialize(args, w + p.off_cutlass, s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
+  OzProf *pf = g.oz_prof;
+  const bool rec = pf && pf->n < 64;
+  if (rec) {
+    cudaEventCreate(&pf->a[pf->n]);
+    cudaEventCreate(&pf->b[pf->n]);
+    cudaEventRecord(pf->a[pf->n], s);
+  }
+  if (gemm.run(s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
+  if (rec) {
+    cudaEventRecord(pf->b[pf->n], s);
+    pf->ops[pf->n] = 2.0 * (double)Mi * Ni * Ki * Li;
+    pf->n++;
+  }
+  if (launches) ++*launches;
+  return cudaSuccess;
+}
+
+// Shared prologue / epilogue of the complex and real Ozaki GEMMs: per-k
+// statistics and K-balancing (step 0), exponents (step 1a), and after the
+// chunks the guard and its DMMA recomputation.
+template <class T>
+struct OzRun {
+  const GemmProblem &g;
+  const OzPlan &p;
+  char *w;
+  cudaStream_t s;
+  int64_t *launches;
+  int *EA, *EB, *KA, *KB, *SK, *misc;
+  double *KSA, *KSB, *rowsq;
+  bool guard, staged, have_ka;
+  int64_t a_sm, a_sk, b_sk, b_sn;
+
+  OzRun(const GemmProblem &g_, const OzPlan &p_, void *ws, cudaStream_t s_, int64_t *l_)
+      : g(g_), p(p_), w(static_cast<char *>(ws)), s(s_), launches(l_) {
+    EA = reinterpret_cast<int *>(w + p.off_EA);
+    EB = reinterpret_cast<int *>(w + p.off_EB);
+    KA = reinterpret_cast<int *>(w + p.off_KA);
+    KB = reinterpret_cast<int *>(w + p.off_KB);
+    SK = reinterpret_cast<int *>(w + p.off_SK);
+    KSA = reinterpret_cast<double *>(w + p.off_KSA);
+    KSB = reinterpret_cast<double *>(w + p.off_KSB);
+    rowsq = reinterpret_cast<double *>(w + p.off_rowsq);
+    misc = reinterpret_cast<int *>(w + p.off_misc);   // [0] fallback flag, [1] balancing, [2] max E_n
+    guard = g.oz_tol > 0.0;
+    staged = g.rows_needed != nullptr;
+    a_sk = g.K == 1 ? 1 : g.a_sk;
+    a_sm = g.a_sm;
+    b_sk = g.b_sk;
+    b_sn = g.N == 1 ? 1 : g.b_sn;
+    have_ka = false;
+  }
+  void count(int n = 1) {
+    if (launches) *launches += n;
+  }
+  // per-k statistics over the lines of X: element (l, k) at l*s_l + k*s_k
+  void kstats(const T *X, int64_t L, int64_t s_l, int64_t s_k, int *KE, double *KS) {
+    if (s_l == 1) {
+      kstats_lines<T><<<(unsigned)((g.K * 32 + 255) / 256), 256, 0, s>>>(X, g.K, L, s_k, KE, KS);
+      count();
+    } else {
+      int *SE = reinterpret_cast<int *>(w + p.off_slotE);
+      double *SS = reinterpret_cast<double *>(w + p.off_slotS);
+      const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(p.nch, (L + 63) / 64));
+      const int64_t chunk = (L + nch - 1) / nch;
+      dim3 grid((unsigned)((g.K + 255) / 256), (unsigned)nch);
+      kstats_cols<T><<<grid, 256, 0, s>>>(X, g.K, L, s_l, chunk, SE, SS);
+      kstats_merge<<<(unsigned)((g.K + 255) / 256), 256, 0, s>>>(SE, SS, (int)nch, g.K, KE, KS);
+      count(2);
+    }
+  }
+  void exponents(const T *X, int64_t nl, int64_t s_l, int64_t s_k, int *E, int sgn) {
+    if (s_k == 1) {
+      line_exponent<T><<<(unsigned)((nl * 32 + 255) / 256), 256, 0, s>>>(X, nl, g.K, s_l, s_k, E, SK, sgn, misc + 1);
+      count();
+    } else {
+      fill_int<<<(unsigned)std::min<int64_t>((nl + 255) / 256, 1024), 256, 0, s>>>(E, nl, -100000);
+      const int64_t ky = std::max<int64_t>(1, std::min<int64_t>((g.K + 127) / 128, 65535));
+      dim3 grid((unsigned)((nl + 255) / 256), (unsigned)ky);
+      line_exponent<T><<<grid, 256, 0, s>>>(X, nl, g.K, s_l, s_k, E, SK, sgn, misc + 1);
+      count(2);
+    }
+  }
+  // steps 0 and 1a for B (and A unless it streams in by row chunks)
+  void prologue() {
+    const T *A = static_cast<const T *>(g.A), *B = static_cast<const T *>(g.B);
+    const bool bal = g.oz_balance && !staged;
+    if (bal || guard) kstats(B, g.N, b_sn, b_sk, KB, KSB);
+    if (bal || (guard && !staged)) {
+      kstats(A, g.M, a_sm, a_sk, KA, KSA);
+      have_ka = true;
+    }
+    balance_prep<<<1, 1024, 0, s>>>(KA, KB, bal ? g.K : 0, p.Kp, bal ? 1 : 0, SK, misc + 1);
+    count();
+    if (!staged) exponents(A, g.M, a_sm, a_sk, EA, +1);
+    exponents(B, g.N, b_sn, b_sk, EB, -1);
+    if (guard) {
+      exp_max<<<1, 1024, 0, s>>>(EB, g.N, misc + 2);
+      count();
+    }
+  }
+  void res_args(ResArgs &r, bool isA, int64_t line0, int64_t lines_out, int8_t *out, int64_t plane_stride) const {
+    r.base = isA ? g.A : g.B;
+    r.nlines = isA ? g.M : g.N;
+    r.K = g.K;
+    r.Kp = p.Kp;
+    r.s_l = isA ? a_sm : b_sn;
+    r.s_k = isA ? a_sk : b_sk;
+    r.line0 = line0;
+    r.lines_out = lines_out;
+    r.E = isA ? EA : EB;
+    r.t = p.t;
+    r.nmod = p.nmod;
+    r.out = out;
+    r.plane_stride = plane_stride;
+    r.SK = SK;
+    r.bal = misc + 1;
+    r.sgn = isA ? 1 : -1;
+  }
+  // after all chunks: guard, then the gated DMMA recomputation
+  cudaError_t epilogue(bool cplx) {
+    if (!guard) return cudaGetLastError();
+    GuardArgs ga{};
+    ga.EA = EA; ga.EB = EB; ga.M = g.M; ga.N = g.N; ga.K = g.K; ga.tpr = p.tpr;
+    ga.KA = have_ka ? KA : nullptr; ga.KB = KB; ga.SK = SK;
+    ga.KSA = have_ka ? KSA : nullptr; ga.KSB = KSB;
+    ga.rowsq = rowsq; ga.t = p.t; ga.cplx = cplx ? 1 : 0; ga.tol = g.oz_tol;
+    ga.flag = misc; ga.bal = misc + 1; ga.rec = g.oz_guard;
+    guard_finalize<<<1, 1024, 0, s>>>(ga);
+    count();
+    cudaError_t e = launch_gemm_dmma_if(g, misc, s, launches);
+    if (e != cudaSuccess) return e;
+    if (cplx && g.npeer > 0) {
+      PeerSet ps{};
+      for (int i = 0; i < g.npeer && i < 7; i++) ps.p[i] = static_cast<double2 *>(g.peer_C[i]);
+      copy_to_peers_if<<<148 * 4, 256, 0, s>>>(static_cast<const double2 *>(g.C), g.M, g.N, g.c_sm,
+                                                std::min(g.npeer, 7), ps, misc);
+      count();
+    }
+    return cudaGetLastError();
+  }
 };
-
-// K-contiguous: 8 consecutive k of one line per thread, 8 bytes per plane
-__global__ void __launch_bounds__(256) residues_real(const __grid_constant__ ResArgsR a) {
-  const int64_t kgroups = a.Kp / 8;
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (gid >= a.lines_out * kgroups) return;
-  const int64_t row = gid / kgroups, k0 = (gid % kgroups) * 8, line = a.line0 + row;
-  double x[8];
-  int lo[8];
-  if (line < a.nlines && a.E[line] > -100000) {
-    double s2a, s2b;
-    line_scale(a.t, a.E[line], s2a, s2b);
-    const double *p = a.base + line * a.s_l;
-    double v[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) v[j] = k0 + j < a.K ? __ldg(p + (k0 + j) * a.s_k) : 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const double m = scaled_magic(v[j], s2a, s2b);
-      x[j] = m - kMagic;
-      lo[j] = __double2loint(m);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-      x[j] = 0.0;
-      lo[j] = 0;
-    }
-  }
-  int8_t *dst = a.out + row * a.Kp + k0;
-  for (int l = 0; l < a.nmod; l++) {
-    const int mi = c_moduli[l];
-    const double minv = c_minv[l];
-    int r[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) r[j] = bal_res(x[j], lo[j], minv, mi);
-    *reinterpret_cast<uint2 *>(dst + (int64_t)l * a.plane_stride) =
-        make_uint2(pack4(r[0], r[1], r[2], r[3]), pack4(r[4], r[5], r[6], r[7]));
-  }
-}
-
-// line-contiguous: 32-line x 64-k tile through shared memory (as residues_t)
-__global__ void __launch_bounds__(256) residues_real_t(const __grid_constant__ ResArgsR a) {
-  __shared__ double sx[32][65];
-  const int64_t ntk = a.Kp / 64;
-  const int64_t tl = blockIdx.x / ntk, tk = blockIdx.x % ntk;
-  const int64_t r0 = tl * 32, kb = tk * 64;
-  const int tid = threadIdx.x;
-  {
-    const int li = tid % 32;
-    const int64_t row = r0 + li, line = a.line0 + row;
-    const bool ok = row < a.lines_out && line < a.nlines && a.E[line] > -100000;
-    double s2a = 0.0, s2b = 0.0;
-    if (ok) line_scale(a.t, a.E[line], s2a, s2b);
-    double v[8];
-#pragma unroll
-    for (int jj = 0; jj < 8; jj++) {
-      const int64_t k = kb + tid / 32 + jj * 8;
-      v[jj] = ok && k < a.K ? __ldg(a.base + line + k * a.s_k) : 0.0;
-    }
-#pragma unroll
-    for (int jj = 0; jj < 8; jj++) sx[li][tid / 32 + jj * 8] = scaled_magic(v[jj], s2a, s2b);
-  }
-  __syncthreads();
-  const int li = tid / 8, kq = (tid % 8) * 8;
-  const int64_t row = r0 + li;
-  if (row >= a.lines_out) return;
-  double x[8];
-  int lo[8];
-#pragma unroll
-  for (int j = 0; j < 8; j++) {
-    const double m = sx[li][kq + j];
-    x[j] = m - kMagic;
-    lo[j] = __double2loint(m);
-  }
-  int8_t *dst = a.out + row * a.Kp + kb + kq;
-  for (int l = 0; l < a.nmod; l++) {
-    const int mi = c_moduli[l];
-    const double minv = c_minv[l];
-    int r[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) r[j] = bal_res(x[j], lo[j], minv, mi);
-    *reinterpret_cast<uint2 *>(dst + (int64_t)l * a.plane_stride) =
-        make_uint2(pack4(r[0], r[1], r[2], r[3]), pack4(r[4], r[5], r[6], r[7]));
-  }
-}
-
-__global__ void batch_moduli_r(int32_t *p, int planes) {
-  const int i = threadIdx.x;
-  if (i < planes) p[i] = c_moduli[i];
-}
-
-// CRT for real outputs: the residue of C' modulo m_l is the GEMM's byte in
-// [0, m_l) itself; 4 consecutive columns per thread (one 32-bit load per plane)
-struct CrtArgsR {
-  const uint8_t *D;          // [n][Mc][Np]
-  int64_t Mc, N, Np, m0;
-  int nmod;
-  double W[kMaxMod][4];
-  double Mch[4];
-  double Minv;
-  const int *EA, *EB;
-  int t;
-  double *C;
-  int64_t c_sm;
-};
-
-template <int NMOD, int NCH>
-__global__ void __launch_bounds__(256) crt_real_kernel(const __grid_constant__ CrtArgsR a) {
-  const int64_t q4 = a.Np / 4;
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (gid >= a.Mc * q4) return;
-  const int64_t r = gid / q4, n0 = (gid % q4) * 4;
-  const int64_t plane = a.Mc * a.Np;
-  double S[4][NCH];
-#pragma unroll
-  for (int e = 0; e < 4; e++)
-#pragma unroll
-    for (int j = 0; j < NCH; j++) S[e][j] = 0.0;
-#pragma unroll
-  for (int i = 0; i < NMOD; i++) {
-    const uint32_t w4 = __ldg(reinterpret_cast<const uint32_t *>(a.D + i * plane + r * a.Np + n0));
-#pragma unroll
-    for (int e = 0; e < 4; e++) {
-      const double c = (double)((w4 >> (8 * e)) & 0xffu);
-#pragma unroll
-      for (int j = 0; j < NCH; j++) S[e][j] = fma(c, a.W[i][j], S[e][j]);
-    }
-  }
-  const int64_t m = a.m0 + r;
-  const int ea = a.EA[m];
-#pragma unroll
-  for (int e = 0; e < 4; e++) {
-    const int64_t n = n0 + e;
-    if (n >= a.N) break;
-    const int eb = a.EB[n];
-    double out = 0.0;
-    if (ea > -100000 && eb > -100000) {
-      // crt_value over the real chunk sums (same reconstruction as the complex CRT)
-      const double two37 = 137438953472.0, inv37 = 1.0 / 137438953472.0;
-      double xe = S[e][NCH - 1];
-#pragma unroll
-      for (int j = NCH - 2; j >= 0; j--) xe = fma(xe, two37, S[e][j]);
-      const double q = rint(xe * a.Minv);
-      double rr[NCH];
-#pragma unroll
-      for (int j = 0; j < NCH; j++) rr[j] = fma(-q, a.Mch[j], S[e][j]);
-#pragma unroll
-      for (int j = 0; j < NCH - 1; j++) {
-        const double cy = rint(rr[j] * inv37);
-        rr[j] = fma(-cy, two37, rr[j]);
-        rr[j + 1] += cy;
-      }
-      double x = rr[NCH - 1];
-#pragma unroll
-      for (int j = NCH - 2; j >= 0; j--) x = fma(x, two37, rr[j]);
-      const int sc = -(2 * a.t - ea) + eb;
-      out = (sc >= -1022 && sc <= 1023) ? x * __hiloint2double((sc + 1023) << 20, 0) : ldexp(x, sc);
-    }
-    a.C[m * a.c_sm + n] = out;
-  }
-}
 
 }  // namespace
+
+// Load the guard's kernels now (CUDA lazy loading cannot load a kernel while
+// a cross-rank barrier kernel of the same device spins: tci_gather_register)
+cudaError_t ozaki_preload() {
+  cudaFuncAttributes fa;
+  const void *fns[] = {
+      (const void *)copy_to_peers_if, (const void *)guard_finalize, (const void *)exp_max,
+      (const void *)balance_prep, (const void *)kstats_merge, (const void *)kstats_lines<double2>,
+      (const void *)kstats_cols<double2>, (const void *)kstats_lines<double>, (const void *)kstats_cols<double>};
+  for (const void *f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
 
 void ozaki_params(int64_t K, int *nmod, int *t, const int **moduli) {
   const OzPlan p = oz_plan(1, 1, K, (size_t)8 << 30);
@@ -790,27 +1350,15 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;   // int32 residue products would overflow
   const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
-  char *w = static_cast<char *>(ws);
-  int *EA = reinterpret_cast<int *>(w + p.off_EA), *EB = reinterpret_cast<int *>(w + p.off_EB);
+  OzRun<double2> R(g, p, ws, s, launches);
+  char *w = R.w;
   int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
   uint8_t *D = reinterpret_cast<uint8_t *>(w + p.off_D);
   int32_t *bmod = reinterpret_cast<int32_t *>(w + p.off_mod);   // modulus of each batch plane
-  const double2 *A = static_cast<const double2 *>(g.A), *B = static_cast<const double2 *>(g.B);
-  // exponents: rows of A (line m: stride a_sm, along k: a_sk); columns of B
-  auto exponents = [&](const double2 *X, int64_t nl, int64_t s_l, int64_t s_k, int *E) {
-    if (s_k == 1) {
-      line_exponent<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, s>>>(X, nl, g.K, s_l, s_k, E);
-      if (launches) ++*launches;
-    } else {
-      fill_int<<<(unsigned)std::min<int64_t>((nl + 255) / 256, 1024), 256, 0, s>>>(E, nl, -100000);
-      const int64_t ky = std::max<int64_t>(1, std::min<int64_t>((g.K + 127) / 128, 65535));
-      dim3 grid((unsigned)((nl + 255) / 256), (unsigned)ky);
-      line_exponent<<<grid, 256, 0, s>>>(X, nl, g.K, s_l, s_k, E);
-      if (launches) *launches += 2;
-    }
-  };
-  if (!g.rows_needed) exponents(A, g.M, g.a_sm, g.a_sk, EA);   // else per row chunk (A streams in)
-  exponents(B, g.N, g.b_sn, g.b_sk, EB);
+  R.prologue();
+  const int planes = 3 * p.nmod;
+  batch_moduli<<<1, 64, 0, s>>>(bmod, planes, 3);
+  R.count();
   auto launch_res = [&](const ResArgs &r) {
     if (r.s_k == 1) {
       const int64_t th = r.lines_out * (r.Kp / 8);
@@ -819,90 +1367,34 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       const int64_t blocks = ((r.lines_out + 31) / 32) * (r.Kp / 64);
       residues_t<<<(unsigned)blocks, 256, 0, s>>>(r);
     }
-    if (launches) ++*launches;
+    R.count();
   };
-  const int planes = 3 * p.nmod;
-  batch_moduli<<<1, 64, 0, s>>>(bmod, planes);
-  if (launches) ++*launches;
-  // residues of B (all columns, padded to Np lines)
   {
     ResArgs r{};
-    r.base = B; r.nlines = g.N; r.K = g.K; r.Kp = p.Kp; r.s_l = g.b_sn; r.s_k = g.b_sk;
-    r.line0 = 0; r.lines_out = p.Np; r.E = EB; r.t = p.t; r.nmod = p.nmod; r.out = Bres;
-    r.plane_stride = p.Np * p.Kp;
+    R.res_args(r, false, 0, p.Np, Bres, p.Np * p.Kp);
     launch_res(r);
   }
-  // CRT weights in 37-bit chunks
   CrtArgs c{};
-  {
-    u128 Mp = 1;
-    for (int l = 0; l < p.nmod; l++) Mp *= (u128)kModuli[l];
-    const u128 mask = ((u128)1 << 37) - 1;
-    for (int l = 0; l < p.nmod; l++) {
-      const unsigned ml = (unsigned)kModuli[l];
-      const u128 Ml = Mp / ml;
-      const u128 wl = mulmod_small(Ml, inv_mod((unsigned)(Ml % ml), ml), Mp);
-      for (int j = 0; j < 4; j++) c.W[l][j] = (double)(uint64_t)((wl >> (37 * j)) & mask);
-    }
-    for (int j = 0; j < 4; j++) c.Mch[j] = (double)(uint64_t)((Mp >> (37 * j)) & mask);
-    c.Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
-  }
-  c.nmod = p.nmod; c.EA = EA; c.EB = EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
+  crt_constants(p.nmod, c.W, c.Mch, c.Minv);
+  c.nmod = p.nmod; c.EA = R.EA; c.EB = R.EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
   c.C = static_cast<double2 *>(g.C); c.c_sm = g.c_sm;
   c.npeer = std::min(g.npeer, 7);
   for (int pp = 0; pp < c.npeer; pp++) c.peer[pp] = static_cast<double2 *>(g.peer_C[pp]);
+  c.rowsq = R.guard ? R.rowsq : nullptr;
+  c.eb_max = R.misc + 2;
   for (int64_t ch = 0; ch < p.chunks; ch++) {
     const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
     if (g.rows_needed) {
       g.rows_needed(g.rows_user, m0, mc);
-      exponents(A + m0 * g.a_sm, mc, g.a_sm, g.a_sk, EA + m0);
+      R.exponents(static_cast<const double2 *>(g.A) + m0 * g.a_sm, mc, g.a_sm, g.a_sk, R.EA + m0, +1);
     }
     {
       ResArgs r{};
-      r.base = A; r.nlines = g.M; r.K = g.K; r.Kp = p.Kp; r.s_l = g.a_sm; r.s_k = g.a_sk;
-      r.line0 = m0; r.lines_out = mc; r.E = EA; r.t = p.t; r.nmod = p.nmod; r.out = Ares;
-      r.plane_stride = mc * p.Kp;
+      R.res_args(r, true, m0, mc, Ares, mc * p.Kp);
       launch_res(r);
     }
-    {
-      using SA = typename I8Gemm::GemmKernel::StrideA;
-      using SB = typename I8Gemm::GemmKernel::StrideB;
-      using SC = typename I8Gemm::GemmKernel::StrideC;
-      using SD = typename I8Gemm::GemmKernel::StrideD;
-      const int Mi = (int)mc, Ni = (int)p.Np, Ki = (int)p.Kp, Li = planes;
-      SA sa = cutlass::make_cute_packed_stride(SA{}, {Mi, Ki, Li});
-      SB sb = cutlass::make_cute_packed_stride(SB{}, {Ni, Ki, Li});
-      SC sc = cutlass::make_cute_packed_stride(SC{}, {Mi, Ni, Li});
-      SD sd = cutlass::make_cute_packed_stride(SD{}, {Mi, Ni, Li});
-      typename ModEVT::Arguments fargs{{}, {{0}, {bmod}, {Stride<_0, _0, int64_t>{_0{}, _0{}, int64_t(1)}}}, {}};
-      typename I8Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {Mi, Ni, Ki, Li},
-                                      {Ares, sa, Bres, sb}, {fargs, nullptr, sc, D, sd}};
-      // Tile order: raster along M in swizzled groups of 8. With K = 20480 (GEMM4)
-      // each 256x256 tile streams 5.2 MB A and B panels; the default order re-read
-      // them from DRAM ~4.5x (50 GB per launch, ncu); this order halves that
-      // (24 GB) and the launch time drops 8% (profiles/r01_ncu_target_ozaki.json).
-      args.scheduler.max_swizzle_size = 8;
-      args.scheduler.raster_order = cutlass::gemm::kernel::detail::RasterOrderOptions::AlongM;
-      I8Gemm gemm;
-      if (gemm.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorNotSupported;
-      const size_t cws = I8Gemm::get_workspace_size(args);
-      if (cws > ((size_t)64 << 20)) return cudaErrorInvalidValue;
-      if (gemm.initialize(args, w + p.off_cutlass, s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
-      OzProf *pf = g.oz_prof;
-      const bool rec = pf && pf->n < 64;
-      if (rec) {
-        cudaEventCreate(&pf->a[pf->n]);
-        cudaEventCreate(&pf->b[pf->n]);
-        cudaEventRecord(pf->a[pf->n], s);
-      }
-      if (gemm.run(s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
-      if (rec) {
-        cudaEventRecord(pf->b[pf->n], s);
-        pf->ops[pf->n] = 2.0 * (double)Mi * Ni * Ki * Li;
-        pf->n++;
-      }
-      if (launches) ++*launches;
-    }
+    cudaError_t ge = int8_gemm(g, p, w, Ares, Bres, D, bmod, mc, planes, s, launches);
+    if (ge != cudaSuccess) return ge;
     c.Mc = mc;
     c.m0 = m0;
     cudaError_t ce;
@@ -914,10 +1406,10 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       default: return cudaErrorInvalidValue;
     }
     if (ce != cudaSuccess) return ce;
-    if (launches) ++*launches;
+    R.count();
     if (g.rows_done) g.rows_done(g.rows_user, m0, mc);
   }
-  return cudaGetLastError();
+  return R.epilogue(true);
 }
 
 // C = A B (float64) per GemmProblem strides by real Ozaki-II on INT8 tcgen05
@@ -926,112 +1418,50 @@ cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
                                int64_t *launches) {
   if (g.M == 0 || g.N == 0) return cudaSuccess;
   if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;
+  if (g.rows_needed) return cudaErrorInvalidValue;   // the real path takes all row exponents up front
   const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
-  char *w = static_cast<char *>(ws);
-  int *EA = reinterpret_cast<int *>(w + p.off_EA), *EB = reinterpret_cast<int *>(w + p.off_EB);
+  OzRun<double> R(g, p, ws, s, launches);
+  char *w = R.w;
   int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
   uint8_t *D = reinterpret_cast<uint8_t *>(w + p.off_D);
   int32_t *bmod = reinterpret_cast<int32_t *>(w + p.off_mod);
-  const double *A = static_cast<const double *>(g.A), *B = static_cast<const double *>(g.B);
-  auto exponents = [&](const double *X, int64_t nl, int64_t s_l, int64_t s_k, int *E) {
-    if (s_k == 1) {
-      line_exponent_r<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, s>>>(X, nl, g.K, s_l, s_k, E);
-      if (launches) ++*launches;
-    } else {
-      fill_int<<<(unsigned)std::min<int64_t>((nl + 255) / 256, 1024), 256, 0, s>>>(E, nl, -100000);
-      const int64_t ky = std::max<int64_t>(1, std::min<int64_t>((g.K + 127) / 128, 65535));
-      dim3 grid((unsigned)((nl + 255) / 256), (unsigned)ky);
-      line_exponent_r<<<grid, 256, 0, s>>>(X, nl, g.K, s_l, s_k, E);
-      if (launches) *launches += 2;
-    }
-  };
-  auto launch_res = [&](const ResArgsR &r) {
+  R.prologue();
+  auto launch_res = [&](const ResArgs &r) {
     if (r.s_k == 1) {
       const int64_t th = r.lines_out * (r.Kp / 8);
       residues_real<<<(unsigned)((th + 255) / 256), 256, 0, s>>>(r);
     } else {
       residues_real_t<<<(unsigned)(((r.lines_out + 31) / 32) * (r.Kp / 64)), 256, 0, s>>>(r);
     }
-    if (launches) ++*launches;
+    R.count();
   };
-  const int64_t a_sk = g.K == 1 ? 1 : g.a_sk, a_sm = g.a_sm;
-  const int64_t b_sk = g.b_sk, b_sn = g.N == 1 ? 1 : g.b_sn;
-  exponents(A, g.M, a_sm, a_sk, EA);
-  exponents(B, g.N, b_sn, b_sk, EB);
   const int planes = p.nmod;
-  batch_moduli_r<<<1, 64, 0, s>>>(bmod, planes);
-  if (launches) ++*launches;
+  batch_moduli<<<1, 64, 0, s>>>(bmod, planes, 1);
+  R.count();
   {
-    ResArgsR r{};
-    r.base = B; r.nlines = g.N; r.K = g.K; r.Kp = p.Kp; r.s_l = b_sn; r.s_k = b_sk;
-    r.line0 = 0; r.lines_out = p.Np; r.E = EB; r.t = p.t; r.nmod = p.nmod; r.out = Bres;
-    r.plane_stride = p.Np * p.Kp;
+    ResArgs r{};
+    R.res_args(r, false, 0, p.Np, Bres, p.Np * p.Kp);
     launch_res(r);
   }
   CrtArgsR c{};
-  {
-    u128 Mp = 1;
-    for (int l = 0; l < p.nmod; l++) Mp *= (u128)kModuli[l];
-    const u128 mask = ((u128)1 << 37) - 1;
-    for (int l = 0; l < p.nmod; l++) {
-      const unsigned ml = (unsigned)kModuli[l];
-      const u128 Ml = Mp / ml;
-      const u128 wl = mulmod_small(Ml, inv_mod((unsigned)(Ml % ml), ml), Mp);
-      for (int j = 0; j < 4; j++) c.W[l][j] = (double)(uint64_t)((wl >> (37 * j)) & mask);
-    }
-    for (int j = 0; j < 4; j++) c.Mch[j] = (double)(uint64_t)((Mp >> (37 * j)) & mask);
-    c.Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
-  }
-  c.nmod = p.nmod; c.EA = EA; c.EB = EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
+  crt_constants(p.nmod, c.W, c.Mch, c.Minv);
+  c.nmod = p.nmod; c.EA = R.EA; c.EB = R.EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
   c.C = static_cast<double *>(g.C); c.c_sm = g.c_sm;
+  c.rowsq = R.guard ? R.rowsq : nullptr;
+  c.eb_max = R.misc + 2;
   for (int64_t ch = 0; ch < p.chunks; ch++) {
     const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
     {
-      ResArgsR r{};
-      r.base = A; r.nlines = g.M; r.K = g.K; r.Kp = p.Kp; r.s_l = a_sm; r.s_k = a_sk;
-      r.line0 = m0; r.lines_out = mc; r.E = EA; r.t = p.t; r.nmod = p.nmod; r.out = Ares;
-      r.plane_stride = mc * p.Kp;
+      ResArgs r{};
+      R.res_args(r, true, m0, mc, Ares, mc * p.Kp);
       launch_res(r);
     }
-    {
-      using SA = typename I8Gemm::GemmKernel::StrideA;
-      using SB = typename I8Gemm::GemmKernel::StrideB;
-      using SC = typename I8Gemm::GemmKernel::StrideC;
-      using SD = typename I8Gemm::GemmKernel::StrideD;
-      const int Mi = (int)mc, Ni = (int)p.Np, Ki = (int)p.Kp, Li = planes;
-      SA sa = cutlass::make_cute_packed_stride(SA{}, {Mi, Ki, Li});
-      SB sb = cutlass::make_cute_packed_stride(SB{}, {Ni, Ki, Li});
-      SC sc = cutlass::make_cute_packed_stride(SC{}, {Mi, Ni, Li});
-      SD sd = cutlass::make_cute_packed_stride(SD{}, {Mi, Ni, Li});
-      typename ModEVT::Arguments fargs{{}, {{0}, {bmod}, {Stride<_0, _0, int64_t>{_0{}, _0{}, int64_t(1)}}}, {}};
-      typename I8Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {Mi, Ni, Ki, Li},
-                                      {Ares, sa, Bres, sb}, {fargs, nullptr, sc, D, sd}};
-      args.scheduler.max_swizzle_size = 8;
-      args.scheduler.raster_order = cutlass::gemm::kernel::detail::RasterOrderOptions::AlongM;
-      I8Gemm gemm;
-      if (gemm.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorNotSupported;
-      if (I8Gemm::get_workspace_size(args) > ((size_t)64 << 20)) return cudaErrorInvalidValue;
-      if (gemm.initialize(args, w + p.off_cutlass, s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
-      OzProf *pf = g.oz_prof;
-      const bool rec = pf && pf->n < 64;
-      if (rec) {
-        cudaEventCreate(&pf->a[pf->n]);
-        cudaEventCreate(&pf->b[pf->n]);
-        cudaEventRecord(pf->a[pf->n], s);
-      }
-      if (gemm.run(s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
-      if (rec) {
-        cudaEventRecord(pf->b[pf->n], s);
-        pf->ops[pf->n] = 2.0 * (double)Mi * Ni * Ki * Li;
-        pf->n++;
-      }
-      if (launches) ++*launches;
-    }
+    cudaError_t ge = int8_gemm(g, p, w, Ares, Bres, D, bmod, mc, planes, s, launches);
+    if (ge != cudaSuccess) return ge;
     c.Mc = mc;
     c.m0 = m0;
-    const int64_t th = mc * (p.Np / 4);
-    const unsigned blocks = (unsigned)((th + 255) / 256);
+    const unsigned blocks = (unsigned)(mc * p.tpr);
     switch (p.nmod) {
       case 12: crt_real_kernel<12, 3><<<blocks, 256, 0, s>>>(c); break;
       case 13: crt_real_kernel<13, 3><<<blocks, 256, 0, s>>>(c); break;
@@ -1039,10 +1469,10 @@ cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       case 15: crt_real_kernel<15, 4><<<blocks, 256, 0, s>>>(c); break;
       default: return cudaErrorInvalidValue;
     }
-    if (launches) ++*launches;
+    R.count();
     if (g.rows_done) g.rows_done(g.rows_user, m0, mc);
   }
-  return cudaGetLastError();
+  return R.epilogue(false);
 }
 
 }  // namespace tci

@@ -45,6 +45,10 @@ struct tci_ctx_s {
   cudaEvent_t evs[8];         // ordering events between the context and copy streams
   cudaStream_t d2h_stream;    // library-owned lane 2 (tci_copy_async), created on first use
   cudaEvent_t lane_ev[16];    // tci_lane_record / tci_lane_wait slots
+  // Ozaki accuracy guard (R26): tolerance on the estimated relative
+  // Frobenius error (<= 0: off) and device-resident statistics
+  double oz_tol;
+  tci::OzGuard *oz_guard;
   int svd_last_sweeps;  // Jacobi sweeps of the last svd / trunc_svd (tci_svd_info)
   double svd_last_off;  // its final off-diagonal measure
 };

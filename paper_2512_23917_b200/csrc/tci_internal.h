@@ -42,6 +42,16 @@ struct GemmProblem {
   void *oz_ws = nullptr;
   size_t oz_ws_bytes = 0;
   struct OzProf *oz_prof = nullptr;   // optional: event timing of the INT8 GEMMs
+  // Ozaki accuracy guard (R26): when oz_tol > 0 the estimated
+  // relative Frobenius truncation error of the product is compared on the
+  // device with oz_tol and, if larger, the GEMM is recomputed on DMMA (a
+  // DMMA launch gated by a device flag); oz_guard (device, context-owned)
+  // accumulates statistics. oz_balance = 0 disables the K-balancing.
+  double oz_tol = 0.0;
+  struct OzGuard *oz_guard = nullptr;
+  int oz_balance = 1;
+  // DMMA kernels: when set, every CTA returns at once unless *run_if != 0
+  const int *run_if = nullptr;
   // deterministic split-K (few output tiles, long K): split z of `splitk`
   // sums k in [z*k_chunk, min(K,(z+1)*k_chunk)) into partial + z*M*N (double
   // or double2 elements, row-major [M][N]); a reduce kernel then adds the
@@ -88,6 +98,19 @@ struct OzProf {
   cudaEvent_t a[64], b[64];
   double ops[64];
 };
+// Device-resident statistics of the Ozaki accuracy guard (one per context,
+// written by one thread of the guard kernel, stream-ordered)
+struct OzGuard {
+  unsigned long long gemms;       // Ozaki GEMMs checked
+  unsigned long long fallbacks;   // of which recomputed on DMMA
+  unsigned long long balanced;    // of which ran with a non-trivial K-balancing
+  double last_est;                // estimated relative Frobenius error of the last one
+  double max_est;                 // maximum over all since the last reset
+};
+constexpr double kOzakiDefaultTol = 1e-13;
+// The DMMA path for p (complex 3M / float64), every CTA gated by *run_if
+// (gemm_dmma.cu): the Ozaki guard's recomputation
+cudaError_t launch_gemm_dmma_if(const GemmProblem &p, const int *run_if, cudaStream_t s, int64_t *launches);
 // Scratch of the Ozaki-II INT8 complex GEMM (ozaki.cu) for an M x N x K product.
 size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K);
 // float64 on the same scheme: one residue plane per modulus (ozaki.cu)
@@ -271,6 +294,7 @@ struct PeerTable {
   void *flags[kMaxRanks];   // each rank's uint32 flag array [nranks]
 };
 cudaError_t gather_preload();
+cudaError_t ozaki_preload();   // the Ozaki guard's kernels (ozaki.cu)
 cudaError_t launch_gather_barrier(const PeerTable &t, int rank, int nranks, uint32_t epoch, int *err,
                                   double timeout_s, cudaStream_t s, int64_t *launches);
 cudaError_t launch_push_rows(const void *src, const PeerTable &t, int rank, int nranks, size_t offset_bytes,

@@ -290,3 +290,44 @@ def tebd_inputs(chi: int, d: int, dtype: str, seed: int, tau: float, J=1.0, g=1.
     B = random_tensor(shB, dtype, seed, TID["B"], device)
     U = torch.from_numpy(tfim_gate(tau, J, g)).to(TORCH_DTYPE[dtype]).to(device)
     return dict(A=A, B=B, U=U)
+
+
+# ----------------------------------------------------------------------------
+# structured inputs (dynamic range the paper's states carry: Schmidt spectra,
+# Vidal-form weights, per-index scales). Each is a plain product of a uniform
+# tensor with fixed scale vectors -- no arithmetic of the method.
+# ----------------------------------------------------------------------------
+
+
+def geometric_spectrum(n: int, smallest: float) -> np.ndarray:
+    """lambda_i = smallest ** (i / (n - 1)), i = 0..n-1 (lambda_0 = 1): a
+    graded Schmidt spectrum spanning [smallest, 1]."""
+    if n == 1:
+        return np.ones(1)
+    return smallest ** (np.arange(n) / (n - 1))
+
+
+def pow2_exponents(n: int, E: int, seed: int, tensor_id: int) -> np.ndarray:
+    """n integers uniform in [-E, E] from the counter-based generator."""
+    u = uniform_draws(seed, tensor_id, n).numpy()          # [-1, 1)
+    return np.minimum(np.floor((u + 1.0) * 0.5 * (2 * E + 1)).astype(np.int64) - E, E)
+
+
+def vidal_tebd_inputs(chi: int, d: int, seed: int, tau: float, smallest: float = 1e-10, dtype="r64"):
+    """TEBD operands in Vidal form (Application A): with
+    lambda_A, lambda_B geometric spectra down to ``smallest`` and X, Y
+    uniform (the O(1) canonical tensors),
+        A[a,s,b] = lambda_B[a] X[a,s,b] lambda_A[b]      (= lambda_B Gamma_A lambda_A)
+        B[b,t,c] = Y[b,t,c] / lambda_A[b] * lambda_B[c]  (= Gamma_B lambda_B,
+                                                          Gamma_B = lambda_A^-1 B_right)
+    so A's columns and B's rows over the contracted bond b carry opposite
+    scales (1 .. 1e-10 against 1 .. 1e10)."""
+    lam_a = geometric_spectrum(chi, smallest)
+    lam_b = geometric_spectrum(chi, smallest)
+    X = random_np((chi, d, chi), dtype, seed, TID["A"])
+    Y = random_np((chi, d, chi), dtype, seed, TID["B"])
+    A = lam_b[:, None, None] * X * lam_a[None, None, :]
+    B = Y / lam_a[:, None, None] * lam_b[None, None, :]
+    U = tfim_gate(tau)
+    return dict(A=torch.from_numpy(np.ascontiguousarray(A)), B=torch.from_numpy(np.ascontiguousarray(B)),
+                U=torch.from_numpy(U).to(TORCH_DTYPE[dtype]), lam_a=lam_a, lam_b=lam_b)

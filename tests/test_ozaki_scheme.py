@@ -89,3 +89,76 @@ def test_crt_reconstruction_exact(K):
         got = _device_crt(res, mods)
         ref = float(X)
         assert got == ref or abs(got - ref) <= abs(ref) * 2.0 ** -52, (X, got, ref)
+
+
+# ---------------------------------------------------------------------------
+# K-balancing and the guard's error estimate (R26), emulated in
+# exact integer arithmetic at a small bit budget (t = 20, int64 products)
+# ---------------------------------------------------------------------------
+
+def _exps(x, axis):
+    """E with |x| < 2^E over each line (re and im), -100000 for zero lines."""
+    a = np.abs(x.real) if not np.iscomplexobj(x) else np.maximum(np.abs(x.real), np.abs(x.imag))
+    m = a.max(axis=axis)
+    return np.where(m > 0, np.frexp(m)[1], -100000)
+
+
+def _emulate(A, B, t, balance):
+    """The scheme of ozaki.cu on real data: s_k = floor((KB_k - KA_k)/2)
+    (none when its spread is <= 2), row/column exponents of the balanced
+    operands, rint to t-bit integers, exact integer product, scale back; and
+    the guard's estimate sqrt(c 4^-t (S_M ||B'||^2 + ||A'||^2 S_N)) / ||C||."""
+    KA, KB = _exps(A, 0), _exps(B, 1)
+    s = np.where((KA > -100000) & (KB > -100000), np.floor_divide(KB - KA, 2), 0)
+    if not balance or s.max() - s.min() <= 2:
+        s = np.zeros_like(s)
+    Ab, Bb = A * np.ldexp(1.0, s)[None, :], B * np.ldexp(1.0, -s)[:, None]
+    EA, EB = _exps(Ab, 1), _exps(Bb, 0)
+    Ai = np.rint(Ab * np.ldexp(1.0, t - EA)[:, None]).astype(np.int64)
+    Bi = np.rint(Bb * np.ldexp(1.0, t - EB)[None, :]).astype(np.int64)
+    C = (Ai @ Bi).astype(np.float64) * np.ldexp(1.0, -(2 * t - EA[:, None] - EB[None, :]))
+    SM, SN = np.ldexp(1.0, 2 * EA).sum(), np.ldexp(1.0, 2 * EB).sum()
+    est = math.sqrt((1 / 12) * 4.0 ** -t * (SM * (Bb * Bb).sum() + (Ab * Ab).sum() * SN)) / np.linalg.norm(C)
+    return C, est, bool(np.any(s))
+
+
+def _cases():
+    rng = np.random.default_rng(11)
+    M, K, N = 96, 384, 80
+    X, Y = rng.uniform(-1, 1, (M, K)), rng.uniform(-1, 1, (K, N))
+    e = rng.integers(-30, 31, K)
+    lam = np.geomspace(1, 1e-10, K)
+    return {
+        "uniform": (X, Y),
+        "anticorrelated_2^30": (X * np.ldexp(1.0, e)[None, :], Y * np.ldexp(1.0, -e)[:, None]),
+        "vidal": (X * lam[None, :], Y / lam[:, None] * np.geomspace(1, 1e-10, N)[None, :]),
+        "graded_rows_of_B": (X, Y * lam[:, None]),
+    }
+
+
+@pytest.mark.parametrize("name", list(_cases()))
+def test_balanced_scheme_error_matches_estimate(name):
+    """With the K-balancing the truncation error is ~2^-t for every structure
+    here, and the guard's estimate predicts it within a factor of 1.5 (it is
+    the expected value of the squared error for independent roundings)."""
+    A, B = _cases()[name]
+    t = 20
+    C, est, _ = _emulate(A, B, t, balance=True)
+    ref = A @ B
+    err = np.linalg.norm(C - ref) / np.linalg.norm(ref)
+    assert err < 2.0 ** -t * 8
+    assert est / 1.5 <= err <= est * 1.5, (err, est)
+
+
+@pytest.mark.parametrize("name", ["anticorrelated_2^30", "vidal"])
+def test_unbalanced_scheme_fails_and_estimate_flags_it(name):
+    """Without the balancing the same inputs lose ~all bits (the round-1
+    scheme); the estimate flags it (far above the guard's tolerance scaled to
+    t = 20), and the balancing is what engages."""
+    A, B = _cases()[name]
+    C, est, _ = _emulate(A, B, 20, balance=False)
+    ref = A @ B
+    err = np.linalg.norm(C - ref) / np.linalg.norm(ref)
+    assert err > 1e-3 and est > 1e-3
+    _, _, used = _emulate(A, B, 20, balance=True)
+    assert used

@@ -1,0 +1,372 @@
+// i8gemm.cu -- the Ozaki-II residue products on the INT8 tensor cores
+// (DESIGN.md §12): one persistent launch computes, for every
+// batch plane b of L,
+//     D[b][m][n] = (sum_k A[b][m][k] B[b][n][k]) mod m_b      (uint8, in [0, m_b))
+// with A [L][M][Kp], B [L][N][Kp] int8 K-major (the residue planes of the two
+// operands), exact int32 accumulation (K * 127^2 < 2^31) and the modulus
+// m_b = moduli[b / per_mod] of the plane.
+//
+// Blackwell structure (hand-written tcgen05 / TMA / TMEM, sm_100a):
+//  * CTA pairs (cluster 2x1x1) issue tcgen05.mma.cta_group::2.kind::i8 with
+//    M = 256 (128 rows per CTA) x N = 256 x K = 32 per instruction; each CTA
+//    TMA-loads its 128 rows of A and its 128 rows (half of N) of B for a
+//    128-byte K block (SWIZZLE_128B tiles, 32 KB per CTA per stage) and both
+//    CTAs' transactions complete on the leader's mbarrier;
+//  * warp roles: warp 0 TMA producer, warp 1 MMA issuer (leader CTA; TMEM
+//    allocation in both), warps 2-5 epilogue;
+//  * accumulators in TMEM (2 x 256 int32 columns: the epilogue of tile i
+//    overlaps the main loop of tile i+1), read back with tcgen05.ld 32x32b,
+//    reduced mod m_b in integer arithmetic and stored as bytes;
+//  * a static persistent schedule over (plane, M tile, N tile), M tiles
+//    rastered in groups of kGroupM per N tile so that concurrently running
+//    clusters share their A and B panels in L2.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "../tci_internal.h"
+#include "common.cuh"
+
+namespace tci {
+namespace i8g {
+
+constexpr int kBM = 128;            // rows of A per CTA (256 per CTA pair)
+constexpr int kBN = 256;            // UMMA N (each CTA loads 128 rows of B)
+constexpr int kBK = 128;            // bytes of K per stage (4 UMMA K-steps of 32)
+constexpr int kStages = 6;
+constexpr int kStageBytes = kBM * kBK + (kBN / 2) * kBK;   // 32 KB per CTA
+constexpr int kThreads = 192;       // 6 warps
+constexpr int kGroupM = 8;          // raster: M tiles per group
+constexpr int kTmemCols = 512;      // two 256-column int32 accumulators
+constexpr uint32_t kTxBytes = 2u * kStageBytes;             // both CTAs' loads land on the leader's barrier
+constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /* align */ + 256 /* barriers */;
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// arrive on the barrier at the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t rank) {
+  asm volatile(
+      "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, %1;\n"
+      " mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+// 3-D TMA load into this CTA's shared memory, completing on the pair leader's barrier
+__device__ __forceinline__ void tma_load_2sm(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;   // peer bit cleared: CTA 0 of the pair
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B (8-row x 128-byte
+// atoms, 1024 bytes apart), sm_100 descriptor version 1
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: kind::i8, signed A and B, int32 accumulator,
+// K-major A and B, M = 256 (cta_group::2), N = 256
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) | ((256u >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(acc)
+      : "memory");
+}
+// completion of this thread's prior tcgen05 ops -> one arrival on `bar` in both CTAs
+__device__ __forceinline__ void umma_commit_both(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+__constant__ int c_i8_moduli[16] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193, 1};
+
+// x mod m in [0, m) for |x| < 2^31 and odd 128 < m < 256: split
+// x = hi 2^16 + lo, y = hi (2^16 mod m) + lo + m 2^16 in [0, 2^25), then
+// q = floor(y / m) = umulhi(y, ceil(2^39 / m)) >> 7 exactly (y < 2^39 / m)
+struct ModM {
+  int m, c16;
+  uint32_t magic;
+  __device__ __forceinline__ void set(int mod) {
+    m = mod;
+    c16 = 65536 % mod;
+    magic = (uint32_t)(((1ull << 39) + (uint64_t)mod - 1) / (uint64_t)mod);
+  }
+  __device__ __forceinline__ uint32_t operator()(int x) const {
+    const uint32_t y = (uint32_t)((x >> 16) * c16 + (x & 0xffff) + (m << 16));
+    const uint32_t q = __umulhi(y, magic) >> 7;
+    return y - q * (uint32_t)m;
+  }
+};
+
+struct Params {
+  int64_t M, N, Kp;        // rows of A per plane, rows of B (= columns of D), padded K
+  int L, per_mod;          // planes, planes per modulus
+  int tiles_m, tiles_n;
+  int64_t tiles;           // L * tiles_m * tiles_n
+  uint8_t *D;              // [L][M][N]
+};
+
+// tile index -> (plane, M tile, N tile): planes outermost; inside a plane
+// groups of kGroupM M tiles walk the N tiles together
+__device__ __forceinline__ void tile_coords(const Params &p, int64_t t, int &b, int &tm, int &tn) {
+  const int64_t per_plane = (int64_t)p.tiles_m * p.tiles_n;
+  b = (int)(t / per_plane);
+  const int r = (int)(t % per_plane);
+  const int per_group = kGroupM * p.tiles_n;
+  const int g = r / per_group, first = g * kGroupM;
+  const int gsz = min(p.tiles_m - first, kGroupM);
+  const int w = r % per_group;
+  tm = first + w % gsz;
+  tn = w / gsz;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    i8gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                  const __grid_constant__ Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte aligned stage ring (SWIZZLE_128B atoms), barriers behind it
+  const uint32_t base_u = smem_u32(smem_raw);
+  uint8_t *smem = smem_raw + (((base_u + 1023u) & ~1023u) - base_u);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  uint64_t *tfull = empty + kStages;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int KB = (int)((p.Kp + kBK - 1) / kBK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) {   // TMEM: both CTAs of the pair allocate (cta_group::2)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(tmem_slot);
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs) =====
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = cluster; t < p.tiles; t += nclusters) {
+        int b, tm, tn;
+        tile_coords(p, t, b, tm, tn);
+        const int ra = tm * 256 + (int)rank * kBM, rb = tn * kBN + (int)rank * (kBN / 2);
+        for (int kb = 0; kb < KB; kb++) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *sa = smem + stage * kStageBytes;
+          uint8_t *sb = sa + kBM * kBK;
+          if (leader) mbar_expect_tx(&full[stage], kTxBytes);
+          tma_load_2sm(sa, &mapA, &full[stage], kb * kBK, ra, b);
+          tma_load_2sm(sb, &mapB, &full[stage], kb * kBK, rb, b);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader CTA, one thread) =====
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t t = cluster; t < p.tiles; t += nclusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);   // both CTAs' epilogues drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * kBN);
+        for (int kb = 0; kb < KB; kb++) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+          const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kBM * kBK);
+#pragma unroll
+          for (int k = 0; k < kBK / 32; k++)   // +32 bytes of K = +2 in the descriptor's address field
+            umma_i8(d, da + 2 * k, db + 2 * k, (kb | k) != 0);
+          umma_commit_both(&empty[stage]);     // frees the stage in both CTAs once these MMAs completed
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_both(&tfull[acc]);         // accumulator ready for both CTAs' epilogues
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===== epilogue: warps 2..5 -> TMEM lane quarter (warp % 4) =====
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    ModM mod;
+    int cur_mod = -1;
+    for (int64_t t = cluster; t < p.tiles; t += nclusters) {
+      int b, tm, tn;
+      tile_coords(p, t, b, tm, tn);
+      const int mi = b / p.per_mod;
+      if (mi != cur_mod) {
+        mod.set(c_i8_moduli[mi]);
+        cur_mod = mi;
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = (int64_t)tm * 256 + rank * kBM + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      uint8_t *drow = p.D + ((int64_t)b * p.M + (row_ok ? row : 0)) * p.N;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kBN);
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; c++) {
+        uint32_t v[32];
+        tmem_ld32(taddr + (uint32_t)(c * 32), v);
+        uint32_t w[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+          w[j] = mod((int)v[4 * j]) | (mod((int)v[4 * j + 1]) << 8) | (mod((int)v[4 * j + 2]) << 16) |
+                 (mod((int)v[4 * j + 3]) << 24);
+        const int64_t col = (int64_t)tn * kBN + c * 32;
+        if (row_ok) {
+          if (col + 32 <= p.N) {
+            uint4 *dst = reinterpret_cast<uint4 *>(drow + col);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else if (col + 16 <= p.N) {   // N is a multiple of 16
+            *reinterpret_cast<uint4 *>(drow + col) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// [L][rows][Kp] int8, boxes of 128 bytes x box_rows rows x 1 plane, SWIZZLE_128B
+bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t Kp, int L, int box_rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)L};
+  const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(rows * Kp)};
+  const cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace i8g
+
+// D[b] = (A[b] B[b]^T) mod m_(b / per_mod) over L planes; A [L][M][Kp],
+// B [L][N][Kp] int8 (Kp a multiple of 64, N a multiple of 16), D [L][M][N] uint8
+cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t M, int64_t N, int64_t Kp, int L,
+                          int per_mod, cudaStream_t s, int64_t *launches) {
+  using namespace i8g;
+  if (M <= 0 || N <= 0 || L <= 0) return cudaSuccess;
+  if (Kp % 64 || N % 16 || (uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)D % 16) return cudaErrorInvalidValue;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, Kp, L, kBM) || !make_map(&mb, B, N, Kp, L, kBN / 2)) return cudaErrorNotSupported;
+  Params p{};
+  p.M = M;
+  p.N = N;
+  p.Kp = Kp;
+  p.L = L;
+  p.per_mod = per_mod;
+  p.tiles_m = (int)((M + 255) / 256);
+  p.tiles_n = (int)((N + kBN - 1) / kBN);
+  p.tiles = (int64_t)L * p.tiles_m * p.tiles_n;
+  p.D = D;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(i8gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t clusters = std::min<int64_t>(p.tiles, sms / 2);
+  i8gemm_kernel<<<(unsigned)(2 * clusters), kThreads, kSmemBytes, s>>>(ma, mb, p);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace tci

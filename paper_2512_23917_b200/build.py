@@ -25,24 +25,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I", os.path.join(ROOT, "include")]
 
 
-def cutlass_root() -> str:
-    """CUTLASS/CuTe header tree vendored in the image (flashinfer's copy, CUTLASS 4.5)."""
-    import importlib.util
-    cands = [os.environ.get("CUTLASS_ROOT", "")]
-    spec = importlib.util.find_spec("flashinfer")
-    if spec and spec.submodule_search_locations:
-        cands.append(os.path.join(list(spec.submodule_search_locations)[0], "data", "cutlass"))
-    for c in cands:
-        if c and os.path.exists(os.path.join(c, "include", "cutlass", "cutlass.h")):
-            return c
-    raise RuntimeError("CUTLASS headers not found (set CUTLASS_ROOT)")
-
-
-# per-file extra flags: the Ozaki INT8 GEMM instantiates CUTLASS sm100 templates
-EXTRA = {
-    "ozaki.cu": lambda: ["--expt-relaxed-constexpr", "-I", os.path.join(cutlass_root(), "include"),
-                         "-I", os.path.join(cutlass_root(), "tools", "util", "include")],
-}
+# per-file extra flags (none: every kernel is hand-written; no CUTLASS / CuTe headers)
+EXTRA = {}
 
 
 def sources():
@@ -60,7 +44,7 @@ def _compile(src: str, verbose_ptxas: bool) -> str:
     newest_dep = max([os.path.getmtime(src), os.path.getmtime(__file__)] + [os.path.getmtime(h) for h in headers()])
     if not verbose_ptxas and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj   # up to date
-    cmd = [NVCC, *ARCH, *COMMON, *EXTRA.get(os.path.basename(src), lambda: [])(), "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *COMMON, *EXTRA.get(os.path.basename(src), []), "-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd[1:1] = ["-x", "cu"]
     if verbose_ptxas and src.endswith(".cu"):

@@ -17,9 +17,11 @@
 //  * accumulators in TMEM (2 x 256 int32 columns: the epilogue of tile i
 //    overlaps the main loop of tile i+1), read back with tcgen05.ld 32x32b,
 //    reduced mod m_b in integer arithmetic and stored as bytes;
-//  * a static persistent schedule over (plane, M tile, N tile), M tiles
-//    rastered in groups of kGroupM per N tile so that concurrently running
-//    clusters share their A and B panels in L2.
+//  * a dynamic persistent schedule: the leader's producer claims tile ids
+//    from a global counter in raster order (plane, then the smaller
+//    operand's panels fastest) and broadcasts them to every role of both
+//    CTAs through an mbarrier ring, so the tiles in flight always form a
+//    compact block of the raster and share their panels in L2.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -38,10 +40,9 @@ constexpr int kBK = 128;            // bytes of K per stage (4 UMMA K-steps of 3
 constexpr int kStages = 6;
 constexpr int kStageBytes = kBM * kBK + (kBN / 2) * kBK;   // 32 KB per CTA
 constexpr int kThreads = 192;       // 6 warps
-constexpr int kGroupM = 8;          // raster: M tiles per group
 constexpr int kTmemCols = 512;      // two 256-column int32 accumulators
 constexpr uint32_t kTxBytes = 2u * kStageBytes;             // both CTAs' loads land on the leader's barrier
-constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /* align */ + 256 /* barriers */;
+constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /* align */ + 512 /* barriers, ids */;
 
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
@@ -59,14 +60,26 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t rank)
       "r"(rank)
       : "memory");
 }
-// 3-D TMA load into this CTA's shared memory, completing on the pair leader's barrier
-__device__ __forceinline__ void tma_load_2sm(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2) {
+// 3-D TMA load into this CTA's shared memory, completing on the pair leader's
+// barrier, with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load_2sm(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2,
+                                             uint64_t policy) {
   const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;   // peer bit cleared: CTA 0 of the pair
   asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2)
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+  uint64_t pol;
+  if (kind == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  else if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -129,27 +142,41 @@ struct ModM {
   }
 };
 
+
 struct Params {
   int64_t M, N, Kp;        // rows of A per plane, rows of B (= columns of D), padded K
   int L, per_mod;          // planes, planes per modulus
   int tiles_m, tiles_n;
   int64_t tiles;           // L * tiles_m * tiles_n
   uint8_t *D;              // [L][M][N]
+  int *counter;            // dynamic tile counter (zero at launch)
+  int a_resident;          // raster: 1 = M tiles fastest (A panels stay in L2), 0 = N tiles fastest
+  int res_block;           // resident panels per block of the raster
+  int hintA, hintB;        // L2 eviction priority of the A / B loads (0 normal, 1 first, 2 last)
 };
 
-// tile index -> (plane, M tile, N tile): planes outermost; inside a plane
-// groups of kGroupM M tiles walk the N tiles together
+// tile index -> (plane, M tile, N tile), planes outermost. Inside a plane one
+// operand is "resident": its panels are taken in blocks of res_block (sized
+// to stay in L2), and inside a block the resident panel varies fastest while
+// the other operand's panels stream by once each. The ~74 tiles in flight
+// then share the block's resident panels and a few streamed ones: DRAM reads
+// per plane are about (streamed panels x blocks + resident panels).
 __device__ __forceinline__ void tile_coords(const Params &p, int64_t t, int &b, int &tm, int &tn) {
   const int64_t per_plane = (int64_t)p.tiles_m * p.tiles_n;
   b = (int)(t / per_plane);
   const int r = (int)(t % per_plane);
-  const int per_group = kGroupM * p.tiles_n;
-  const int g = r / per_group, first = g * kGroupM;
-  const int gsz = min(p.tiles_m - first, kGroupM);
-  const int w = r % per_group;
-  tm = first + w % gsz;
-  tn = w / gsz;
+  const int nres = p.a_resident ? p.tiles_m : p.tiles_n;   // resident panels
+  const int nstr = p.a_resident ? p.tiles_n : p.tiles_m;   // streamed panels
+  const int per_block = p.res_block * nstr;
+  const int blk = r / per_block, w = r % per_block;
+  const int bsz = min(p.res_block, nres - blk * p.res_block);
+  const int ir = blk * p.res_block + w % bsz, is = w / bsz;
+  tm = p.a_resident ? ir : is;
+  tn = p.a_resident ? is : ir;
 }
+
+constexpr int kTidSlots = 8;       // depth of the tile-id broadcast ring
+constexpr int kTidConsumers = 10;  // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue warps
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     i8gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
@@ -162,12 +189,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t *empty = full + kStages;
   uint64_t *tfull = empty + kStages;
   uint64_t *tempty = tfull + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint64_t *idfull = tempty + 2;
+  uint64_t *idempty = idfull + kTidSlots;
+  int *idslot = reinterpret_cast<int *>(idempty + kTidSlots);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(idslot + kTidSlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
-  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int KB = (int)((p.Kp + kBK - 1) / kBK);
 
   if (threadIdx.x == 0) {
@@ -178,6 +207,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; a++) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs
+    }
+    for (int i = 0; i < kTidSlots; i++) {
+      mbar_init(&idfull[i], 1);
+      mbar_init(&idempty[i], kTidConsumers);
     }
     mbar_fence_init();
   }
@@ -192,12 +225,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t *>(tmem_slot);
 
+  // consumer side of the tile-id ring: the next tile of this pair (-1: done)
+  int id_i = 0;
+  uint32_t id_phase = 0;
+  auto next_tile = [&](int &slot) -> int {
+    slot = id_i;
+    mbar_wait(&idfull[id_i], id_phase);
+    const int t = *reinterpret_cast<volatile int *>(&idslot[id_i]);
+    if (++id_i == kTidSlots) {
+      id_i = 0;
+      id_phase ^= 1;
+    }
+    return t;
+  };
+
   if (warp == 0) {
-    // ===== TMA producer (both CTAs) =====
+    // ===== TMA producer (both CTAs); the leader's also claims the tile ids =====
     if (lane == 0) {
+      const uint64_t polA = l2_policy(p.hintA), polB = l2_policy(p.hintB);
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = cluster; t < p.tiles; t += nclusters) {
+      int fi = 0;
+      uint32_t fphase = 0;
+      for (;;) {
+        int t;
+        if (leader) {
+          // dynamic schedule: tiles are claimed in raster order as pairs free
+          // up, so the tiles in flight stay a compact block of the raster
+          mbar_wait(&idempty[fi], fphase ^ 1);
+          t = atomicAdd(p.counter, 1);
+          if (t >= p.tiles) t = -1;
+          idslot[fi] = t;
+          asm volatile(
+              "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, 1;\n st.shared::cluster.b32 [ra], %1;\n}\n" ::"r"(
+                  smem_u32(&idslot[fi])),
+              "r"(t)
+              : "memory");
+          mbar_arrive_remote(&idfull[fi], 0);   // release.cluster: the slot writes are visible first
+          mbar_arrive_remote(&idfull[fi], 1);
+          if (++fi == kTidSlots) {
+            fi = 0;
+            fphase ^= 1;
+          }
+        } else {
+          int slot;
+          t = next_tile(slot);
+          mbar_arrive_remote(&idempty[slot], 0);
+        }
+        if (t < 0) break;
         int b, tm, tn;
         tile_coords(p, t, b, tm, tn);
         const int ra = tm * 256 + (int)rank * kBM, rb = tn * kBN + (int)rank * (kBN / 2);
@@ -206,8 +281,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t *sa = smem + stage * kStageBytes;
           uint8_t *sb = sa + kBM * kBK;
           if (leader) mbar_expect_tx(&full[stage], kTxBytes);
-          tma_load_2sm(sa, &mapA, &full[stage], kb * kBK, ra, b);
-          tma_load_2sm(sb, &mapB, &full[stage], kb * kBK, rb, b);
+          tma_load_2sm(sa, &mapA, &full[stage], kb * kBK, ra, b, polA);
+          tma_load_2sm(sb, &mapB, &full[stage], kb * kBK, rb, b, polB);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -222,7 +297,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t t = cluster; t < p.tiles; t += nclusters) {
+      for (;;) {
+        int slot;
+        const int t = next_tile(slot);
+        mbar_arrive_remote(&idempty[slot], 0);
+        if (t < 0) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);   // both CTAs' epilogues drained this accumulator
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * kBN);
@@ -254,7 +333,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     ModM mod;
     int cur_mod = -1;
-    for (int64_t t = cluster; t < p.tiles; t += nclusters) {
+    for (;;) {
+      int slot;
+      const int t = next_tile(slot);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&idempty[slot], 0);
+      if (t < 0) break;
       int b, tm, tn;
       tile_coords(p, t, b, tm, tn);
       const int mi = b / p.per_mod;
@@ -278,13 +362,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           w[j] = mod((int)v[4 * j]) | (mod((int)v[4 * j + 1]) << 8) | (mod((int)v[4 * j + 2]) << 16) |
                  (mod((int)v[4 * j + 3]) << 24);
         const int64_t col = (int64_t)tn * kBN + c * 32;
-        if (row_ok) {
+        if (row_ok) {   // streaming stores: the bytes are read once, by the CRT
           if (col + 32 <= p.N) {
             uint4 *dst = reinterpret_cast<uint4 *>(drow + col);
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            __stcs(dst, make_uint4(w[0], w[1], w[2], w[3]));
+            __stcs(dst + 1, make_uint4(w[4], w[5], w[6], w[7]));
           } else if (col + 16 <= p.N) {   // N is a multiple of 16
-            *reinterpret_cast<uint4 *>(drow + col) = make_uint4(w[0], w[1], w[2], w[3]);
+            __stcs(reinterpret_cast<uint4 *>(drow + col), make_uint4(w[0], w[1], w[2], w[3]));
           }
         }
       }
@@ -320,6 +404,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// lab overrides (tools/i8gemm_lab.cu): TMA L2 promotion (0 none, 1 128B,
+// 2 256B), raster (-1 auto), L2 eviction hints of the A / B loads
+int g_i8_promo = 2;
+int g_i8_raster = -1;
+int g_i8_hintA = 0, g_i8_hintB = 0;
+int g_i8_res_mb = 48;   // L2 budget of the resident panels (MB)
+
 // [L][rows][Kp] int8, boxes of 128 bytes x box_rows rows x 1 plane, SWIZZLE_128B
 bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t Kp, int L, int box_rows) {
   auto enc = encode_fn();
@@ -328,20 +419,25 @@ bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t Kp, int L,
   const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(rows * Kp)};
   const cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapL2promotion promo = g_i8_promo == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                       : g_i8_promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                         : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace i8g
 
 // D[b] = (A[b] B[b]^T) mod m_(b / per_mod) over L planes; A [L][M][Kp],
-// B [L][N][Kp] int8 (Kp a multiple of 64, N a multiple of 16), D [L][M][N] uint8
+// B [L][N][Kp] int8 (Kp a multiple of 64, N a multiple of 16), D [L][M][N]
+// uint8; counter: one device int of scratch (the dynamic tile counter)
 cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t M, int64_t N, int64_t Kp, int L,
-                          int per_mod, cudaStream_t s, int64_t *launches) {
+                          int per_mod, int *counter, cudaStream_t s, int64_t *launches) {
   using namespace i8g;
   if (M <= 0 || N <= 0 || L <= 0) return cudaSuccess;
-  if (Kp % 64 || N % 16 || (uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)D % 16) return cudaErrorInvalidValue;
+  if (Kp % 64 || N % 16 || (uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)D % 16 || !counter)
+    return cudaErrorInvalidValue;
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, M, Kp, L, kBM) || !make_map(&mb, B, N, Kp, L, kBN / 2)) return cudaErrorNotSupported;
   Params p{};
@@ -354,6 +450,15 @@ cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t 
   p.tiles_n = (int)((N + kBN - 1) / kBN);
   p.tiles = (int64_t)L * p.tiles_m * p.tiles_n;
   p.D = D;
+  p.counter = counter;
+  p.a_resident = g_i8_raster >= 0 ? g_i8_raster : (M <= N ? 1 : 0);   // the smaller panel set stays in L2
+  {
+    const int nres = p.a_resident ? p.tiles_m : p.tiles_n;
+    const int64_t fit = ((int64_t)g_i8_res_mb << 20) / (256 * Kp);   // a panel: 256 rows x Kp bytes
+    p.res_block = (int)std::max<int64_t>(1, std::min<int64_t>(nres, fit));
+  }
+  p.hintA = g_i8_hintA;
+  p.hintB = g_i8_hintB;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(i8gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
@@ -364,6 +469,8 @@ cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t clusters = std::min<int64_t>(p.tiles, sms / 2);
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
   i8gemm_kernel<<<(unsigned)(2 * clusters), kThreads, kSmemBytes, s>>>(ma, mb, p);
   if (launches) ++*launches;
   return cudaGetLastError();

@@ -1,26 +1,34 @@
-// ozaki.cu -- complex128 GEMM on the INT8 tensor cores (tcgen05 kind::i8) by
-// the Ozaki-II integer-modular scheme:
+// ozaki.cu -- complex128 / float64 GEMM on the INT8 tensor cores (tcgen05
+// kind::i8) by the Ozaki-II integer-modular scheme (DESIGN.md
+// §12, reading R26):
 //
-//   1. scale: for every row m of A (both re and im) pick s_m so that
-//      |A(m,k)| 2^{s_m} < 2^t, and A'(m,k) = rint(A(m,k) 2^{s_m}) (t-bit
-//      integers, exact in fp64); likewise B'(k,n) = rint(B(k,n) 2^{r_n});
+//   0. balance: per contraction index k an exact power of two 2^{s_k} moves
+//      between A's column k and B's row k (A diag(2^s) diag(2^-s) B = AB),
+//      s_k = floor((KB_k - KA_k)/2) from the per-k maxima, so entries that
+//      multiply each other sit on a common scale;
+//   1. scale: for every row m of A (re and im) pick E_m with |A'(m,k)| < 2^E_m
+//      and round A'(m,k) 2^(t - E_m) to a t-bit integer (exact in fp64);
+//      likewise the columns of B';
 //   2. the integer complex product C' = A'B' is computed EXACTLY from its
-//      residues modulo n coprime moduli m_l <= 255 (prod m_l > 2 max|C'|):
+//      residues modulo n coprime moduli m_l <= 255 (prod m_l > 4 max|C'|):
 //      with the 3M split (exact in integer arithmetic)
 //        P = A'r B'r,  Q = A'i B'i,  S = (A'r + A'i)(B'r + B'i),
 //        C'r = P - Q,  C'i = S - P - Q,
-//      every residue operand is an int8 in [-127, 127] and every batch of the
-//      3n INT8 GEMMs (int32 accumulation, exact for K <= 133 000) runs in ONE
-//      batched CUTLASS sm100 INT8 GEMM (2-SM 256x256x128 tiles, TMA, TMEM);
+//      every residue operand is an int8 in [-127, 127] and all 3n INT8 GEMMs
+//      (int32 accumulation, exact for K <= 131072) run in ONE launch of the
+//      hand-written tcgen05 kernel of i8gemm.cu, which leaves each product
+//      reduced mod m_l as a byte;
 //   3. CRT: C' = sum_l c_l w_l mod M (w_l the CRT weights, M = prod m_l) in
-//      exact 128-bit integer arithmetic, reduced to (-M/2, M/2], converted to
-//      fp64 and scaled back by 2^-(s_m + r_n).
+//      exact chunked fp64 integer arithmetic, converted to fp64 and scaled
+//      back by 2^-(2t - E_m - E_n);
+//   4. guard: the expected squared truncation error (independent roundings,
+//      R26) against ||C||_F on the device; above the tolerance the product is
+//      recomputed on DMMA by a launch gated on a device flag.
 //
-// The only rounding is step 1's truncation to t >= 46 bits (relative error
-// ~2^-46 per operand entry, well inside the 1e-12 relative-Frobenius bar;
-// DESIGN.md R26) and the final conversion to fp64. t and n are chosen from K:
-// 2t + 3 + log2 K <= log2 M. Rows are processed in chunks so the int32 GEMM
-// outputs (3n x Mc x N) fit a bounded workspace.
+// The only roundings are step 1's truncation (|delta| <= 2^(E_m - t - 1) per
+// component) and the final conversion. t and n are chosen from K:
+// 2t + 3 + log2 K <= log2 M. Rows are processed in chunks so the residue
+// planes and byte outputs fit a bounded workspace.
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -30,64 +38,12 @@
 #include "../tci_internal.h"
 #include "common.cuh"
 
-#include "cutlass/cutlass.h"
-#include "cute/tensor.hpp"
-#include "cutlass/gemm/dispatch_policy.hpp"
-#include "cutlass/gemm/collective/collective_builder.hpp"
-#include "cutlass/epilogue/collective/collective_builder.hpp"
-#include "cutlass/epilogue/fusion/sm90_callbacks_tma_warpspecialized.hpp"
-#include "cutlass/gemm/device/gemm_universal_adapter.h"
-#include "cutlass/gemm/kernel/gemm_universal.hpp"
-#include "cutlass/util/packed_stride.hpp"
-
 namespace tci {
 namespace {
-
-using namespace cute;
 
 constexpr int kMaxMod = 15;
 constexpr int kModuli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
 __constant__ int c_moduli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
-
-// ---------------------------------------------------------------------------
-// CUTLASS sm100 INT8 GEMM with a fused epilogue (EVT):
-//   D[b][m][n] = (sum_k A[b][m][k] B[b][n][k]) mod m_b   in [0, m_b), uint8
-// The int32 accumulator (exact) is reduced by its batch's modulus in the
-// epilogue (per-batch scalar broadcast), so the residue planes leave the
-// tensor cores as bytes: 4x less traffic than int32 outputs.
-// ---------------------------------------------------------------------------
-template <class T>
-struct ModNonneg;
-template <int N>
-struct ModNonneg<cutlass::Array<int32_t, N>> {
-  CUTLASS_HOST_DEVICE cutlass::Array<int32_t, N> operator()(cutlass::Array<int32_t, N> const &a,
-                                                           cutlass::Array<int32_t, N> const &m) const {
-    cutlass::Array<int32_t, N> r;
-    CUTLASS_PRAGMA_UNROLL
-    for (int i = 0; i < N; ++i) {
-      const int32_t x = a[i] % m[i];
-      r[i] = x < 0 ? x + m[i] : x;
-    }
-    return r;
-  }
-};
-namespace fu = cutlass::epilogue::fusion;
-using ModEVT = fu::Sm90EVT<fu::Sm90Compute<ModNonneg, uint8_t, int32_t, cutlass::FloatRoundStyle::round_to_nearest>,
-                           fu::Sm90AccFetch, fu::Sm90ScalarBroadcast<int32_t, Stride<_0, _0, int64_t>>>;
-using TileShape = Shape<_256, _256, _128>;
-using ClusterShape = Shape<_2, _1, _1>;
-using Epi = typename cutlass::epilogue::collective::CollectiveBuilder<
-    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, TileShape, ClusterShape,
-    cutlass::epilogue::collective::EpilogueTileAuto, int32_t, int32_t, void, cutlass::layout::RowMajor, 16,
-    uint8_t, cutlass::layout::RowMajor, 16, cutlass::epilogue::collective::EpilogueScheduleAuto,
-    ModEVT>::CollectiveOp;
-using Main = typename cutlass::gemm::collective::CollectiveBuilder<
-    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, int8_t, cutlass::layout::RowMajor, 16, int8_t,
-    cutlass::layout::ColumnMajor, 16, int32_t, TileShape, ClusterShape,
-    cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename Epi::SharedStorage))>,
-    cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
-using I8Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Main, Epi, void>;
-using I8Gemm = cutlass::gemm::device::GemmUniversalAdapter<I8Kernel>;
 
 // ---------------------------------------------------------------------------
 // Small helpers: exact powers of two, exponent / mantissa split
@@ -310,11 +266,6 @@ __global__ void __launch_bounds__(256) line_exponent(const T *base, int64_t nlin
     }
     atomicMax(E + l, e);
   }
-}
-
-__global__ void batch_moduli(int32_t *p, int planes, int per_mod) {
-  const int i = threadIdx.x;
-  if (i < planes) p[i] = c_moduli[i / per_mod];
 }
 
 __global__ void fill_int(int *p, int64_t n, int v) {
@@ -1060,7 +1011,7 @@ __global__ void __launch_bounds__(256) copy_to_peers_if(const double2 *C, int64_
 struct OzPlan {
   int nmod, t;
   int64_t Kp, Np, Mc, chunks, tpr, nch;
-  size_t off_EA, off_EB, off_Bres, off_Ares, off_D, off_mod, off_cutlass;
+  size_t off_EA, off_EB, off_Bres, off_Ares, off_D;
   size_t off_KA, off_KB, off_SK, off_KSA, off_KSB, off_slotE, off_slotS, off_rowsq, off_misc;
   size_t total;
 };
@@ -1096,7 +1047,6 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_row
   p.off_Bres = off; off = align_up(off + (size_t)planes * p.Np * p.Kp);
   p.off_Ares = off; off = align_up(off + (size_t)planes * p.Mc * p.Kp);
   p.off_D = off; off = align_up(off + (size_t)planes * p.Mc * p.Np);
-  p.off_mod = off; off = align_up(off + (size_t)planes * 4);
   p.off_KA = off; off = align_up(off + (size_t)p.Kp * 4);
   p.off_KB = off; off = align_up(off + (size_t)p.Kp * 4);
   p.off_SK = off; off = align_up(off + (size_t)p.Kp * 4);
@@ -1106,7 +1056,6 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_row
   p.off_slotS = off; off = align_up(off + (size_t)p.nch * p.Kp * 8);
   p.off_rowsq = off; off = align_up(off + (size_t)M * p.tpr * 8);
   p.off_misc = off; off = align_up(off + 64);
-  p.off_cutlass = off; off = align_up(off + ((size_t)64 << 20));   // CUTLASS workspace (small)
   p.total = off;
   return p;
 }
@@ -1148,31 +1097,9 @@ void crt_constants(int nmod, double (&W)[kMaxMod][4], double (&Mch)[4], double &
 }
 
 // one batched INT8 GEMM: D[b][m][n] = (sum_k A[b][m][k] B[b][n][k]) mod m_b
-cudaError_t int8_gemm(const GemmProblem &g, const OzPlan &p, char *w, int8_t *Ares, int8_t *Bres, uint8_t *D,
-                      int32_t *bmod, int64_t mc, int planes, cudaStream_t s, int64_t *launches) {
-  using SA = typename I8Gemm::GemmKernel::StrideA;
-  using SB = typename I8Gemm::GemmKernel::StrideB;
-  using SC = typename I8Gemm::GemmKernel::StrideC;
-  using SD = typename I8Gemm::GemmKernel::StrideD;
-  const int Mi = (int)mc, Ni = (int)p.Np, Ki = (int)p.Kp, Li = planes;
-  SA sa = cutlass::make_cute_packed_stride(SA{}, {Mi, Ki, Li});
-  SB sb = cutlass::make_cute_packed_stride(SB{}, {Ni, Ki, Li});
-  SC sc = cutlass::make_cute_packed_stride(SC{}, {Mi, Ni, Li});
-  SD sd = cutlass::make_cute_packed_stride(SD{}, {Mi, Ni, Li});
-  typename ModEVT::Arguments fargs{{}, {{0}, {bmod}, {Stride<_0, _0, int64_t>{_0{}, _0{}, int64_t(1)}}}, {}};
-  typename I8Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {Mi, Ni, Ki, Li},
-                                  {Ares, sa, Bres, sb}, {fargs, nullptr, sc, D, sd}};
-  // Tile order: raster along M in swizzled groups of 8. With K = 20480 (GEMM4)
-  // each 256x256 tile streams 5.2 MB A and B panels; the default order re-read
-  // them from DRAM ~4.5x (50 GB per launch, ncu); this order halves that
-  // (24 GB) and the launch time drops 8% (profiles/r01_ncu_target_ozaki.json).
-  args.scheduler.max_swizzle_size = 8;
-  args.scheduler.raster_order = cutlass::gemm::kernel::detail::RasterOrderOptions::AlongM;
-  I8Gemm gemm;
-  if (gemm.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorNotSupported;
-  const size_t cws = I8Gemm::get_workspace_size(args);
-  if (cws > ((size_t)64 << 20)) return cudaErrorInvalidValue;
-  if (gemm.initialize(args, w + p.off_cutlass, s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
+// (i8gemm.cu: hand-written tcgen05 kind::i8, TMA, TMEM)
+cudaError_t int8_gemm(const GemmProblem &g, const OzPlan &p, const int8_t *Ares, const int8_t *Bres, uint8_t *D,
+                      int64_t mc, int planes, int per_mod, int *counter, cudaStream_t s, int64_t *launches) {
   OzProf *pf = g.oz_prof;
   const bool rec = pf && pf->n < 64;
   if (rec) {
@@ -1180,13 +1107,13 @@ cudaError_t int8_gemm(const GemmProblem &g, const OzPlan &p, char *w, int8_t *Ar
     cudaEventCreate(&pf->b[pf->n]);
     cudaEventRecord(pf->a[pf->n], s);
   }
-  if (gemm.run(s) != cutlass::Status::kSuccess) return cudaErrorUnknown;
+  cudaError_t e = launch_i8gemm(Ares, Bres, D, mc, p.Np, p.Kp, planes, per_mod, counter, s, launches);
+  if (e != cudaSuccess) return e;
   if (rec) {
     cudaEventRecord(pf->b[pf->n], s);
-    pf->ops[pf->n] = 2.0 * (double)Mi * Ni * Ki * Li;
+    pf->ops[pf->n] = 2.0 * (double)mc * p.Np * p.Kp * planes;
     pf->n++;
   }
-  if (launches) ++*launches;
   return cudaSuccess;
 }
 
@@ -1215,7 +1142,7 @@ struct OzRun {
     KSA = reinterpret_cast<double *>(w + p.off_KSA);
     KSB = reinterpret_cast<double *>(w + p.off_KSB);
     rowsq = reinterpret_cast<double *>(w + p.off_rowsq);
-    misc = reinterpret_cast<int *>(w + p.off_misc);   // [0] fallback flag, [1] balancing, [2] max E_n
+    misc = reinterpret_cast<int *>(w + p.off_misc);   // [0] fallback flag, [1] balancing, [2] max E_n, [3] tile counter
     guard = g.oz_tol > 0.0;
     staged = g.rows_needed != nullptr;
     a_sk = g.K == 1 ? 1 : g.a_sk;
@@ -1354,11 +1281,8 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   char *w = R.w;
   int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
   uint8_t *D = reinterpret_cast<uint8_t *>(w + p.off_D);
-  int32_t *bmod = reinterpret_cast<int32_t *>(w + p.off_mod);   // modulus of each batch plane
   R.prologue();
   const int planes = 3 * p.nmod;
-  batch_moduli<<<1, 64, 0, s>>>(bmod, planes, 3);
-  R.count();
   auto launch_res = [&](const ResArgs &r) {
     if (r.s_k == 1) {
       const int64_t th = r.lines_out * (r.Kp / 8);
@@ -1393,7 +1317,7 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       R.res_args(r, true, m0, mc, Ares, mc * p.Kp);
       launch_res(r);
     }
-    cudaError_t ge = int8_gemm(g, p, w, Ares, Bres, D, bmod, mc, planes, s, launches);
+    cudaError_t ge = int8_gemm(g, p, Ares, Bres, D, mc, planes, 3, R.misc + 3, s, launches);
     if (ge != cudaSuccess) return ge;
     c.Mc = mc;
     c.m0 = m0;
@@ -1425,7 +1349,6 @@ cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   char *w = R.w;
   int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
   uint8_t *D = reinterpret_cast<uint8_t *>(w + p.off_D);
-  int32_t *bmod = reinterpret_cast<int32_t *>(w + p.off_mod);
   R.prologue();
   auto launch_res = [&](const ResArgs &r) {
     if (r.s_k == 1) {
@@ -1437,8 +1360,6 @@ cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
     R.count();
   };
   const int planes = p.nmod;
-  batch_moduli<<<1, 64, 0, s>>>(bmod, planes, 1);
-  R.count();
   {
     ResArgs r{};
     R.res_args(r, false, 0, p.Np, Bres, p.Np * p.Kp);
@@ -1457,7 +1378,7 @@ cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       R.res_args(r, true, m0, mc, Ares, mc * p.Kp);
       launch_res(r);
     }
-    cudaError_t ge = int8_gemm(g, p, w, Ares, Bres, D, bmod, mc, planes, s, launches);
+    cudaError_t ge = int8_gemm(g, p, Ares, Bres, D, mc, planes, 1, R.misc + 3, s, launches);
     if (ge != cudaSuccess) return ge;
     c.Mc = mc;
     c.m0 = m0;

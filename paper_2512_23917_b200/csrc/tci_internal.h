@@ -124,6 +124,12 @@ constexpr int64_t kOzakiMaxK = 131072;
 inline bool ozaki_worthwhile(int64_t M, int64_t N, int64_t K) {
   return (double)M * (double)N * (double)K >= 4.0e9 && M >= 256 && N >= 256 && K >= 64 && K <= kOzakiMaxK;
 }
+// The residue products of one Ozaki GEMM in one launch (i8gemm.cu, tcgen05
+// kind::i8): D[b] = (A[b] B[b]^T) mod m_(b / per_mod) over L planes,
+// A [L][M][Kp], B [L][N][Kp] int8 K-major, D [L][M][N] uint8; counter: one
+// device int of scratch (dynamic tile schedule)
+cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t M, int64_t N, int64_t Kp, int L,
+                          int per_mod, int *counter, cudaStream_t s, int64_t *launches);
 // moduli count and integer bit budget chosen for a contraction length K
 void ozaki_params(int64_t K, int *nmod, int *t, const int **moduli);
 

@@ -6,11 +6,71 @@
 // bench-sized ones are compared with a plain int64 dot product mod m.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "../paper_2512_23917_b200/csrc/kernels/i8gemm.cu"
 
+#ifdef WITH_CUTLASS
+// the library INT8 GEMM the round-1 build used, for an A/B in the same process
+#include "cutlass/cutlass.h"
+#include "cute/tensor.hpp"
+#include "cutlass/gemm/dispatch_policy.hpp"
+#include "cutlass/gemm/collective/collective_builder.hpp"
+#include "cutlass/epilogue/collective/collective_builder.hpp"
+#include "cutlass/epilogue/fusion/sm90_callbacks_tma_warpspecialized.hpp"
+#include "cutlass/gemm/device/gemm_universal_adapter.h"
+#include "cutlass/gemm/kernel/gemm_universal.hpp"
+#include "cutlass/util/packed_stride.hpp"
+namespace cl {
+using namespace cute;
+template <class T> struct ModNonneg;
+template <int N> struct ModNonneg<cutlass::Array<int32_t, N>> {
+  CUTLASS_HOST_DEVICE cutlass::Array<int32_t, N> operator()(cutlass::Array<int32_t, N> const &a,
+                                                           cutlass::Array<int32_t, N> const &m) const {
+    cutlass::Array<int32_t, N> r;
+    for (int i = 0; i < N; ++i) { const int32_t x = a[i] % m[i]; r[i] = x < 0 ? x + m[i] : x; }
+    return r;
+  }
+};
+namespace fu = cutlass::epilogue::fusion;
+using ModEVT = fu::Sm90EVT<fu::Sm90Compute<ModNonneg, uint8_t, int32_t, cutlass::FloatRoundStyle::round_to_nearest>,
+                           fu::Sm90AccFetch, fu::Sm90ScalarBroadcast<int32_t, Stride<_0, _0, int64_t>>>;
+using TileShape = Shape<_256, _256, _128>;
+using ClusterShape = Shape<_2, _1, _1>;
+using Epi = typename cutlass::epilogue::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, TileShape, ClusterShape,
+    cutlass::epilogue::collective::EpilogueTileAuto, int32_t, int32_t, void, cutlass::layout::RowMajor, 16,
+    uint8_t, cutlass::layout::RowMajor, 16, cutlass::epilogue::collective::EpilogueScheduleAuto, ModEVT>::CollectiveOp;
+using Main = typename cutlass::gemm::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, int8_t, cutlass::layout::RowMajor, 16, int8_t,
+    cutlass::layout::ColumnMajor, 16, int32_t, TileShape, ClusterShape,
+    cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename Epi::SharedStorage))>,
+    cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
+using I8Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Main, Epi, void>;
+using I8Gemm = cutlass::gemm::device::GemmUniversalAdapter<I8Kernel>;
+static void *cws = nullptr;
+cudaError_t run(const int8_t *A, const int8_t *B, uint8_t *D, int32_t *bmod, int M, int N, int K, int L) {
+  using SA = typename I8Gemm::GemmKernel::StrideA; using SB = typename I8Gemm::GemmKernel::StrideB;
+  using SC = typename I8Gemm::GemmKernel::StrideC; using SD = typename I8Gemm::GemmKernel::StrideD;
+  SA sa = cutlass::make_cute_packed_stride(SA{}, {M, K, L}); SB sb = cutlass::make_cute_packed_stride(SB{}, {N, K, L});
+  SC sc = cutlass::make_cute_packed_stride(SC{}, {M, N, L}); SD sd = cutlass::make_cute_packed_stride(SD{}, {M, N, L});
+  typename ModEVT::Arguments fargs{{}, {{0}, {bmod}, {Stride<_0, _0, int64_t>{_0{}, _0{}, int64_t(1)}}}, {}};
+  typename I8Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, L},
+                                  {A, sa, B, sb}, {fargs, nullptr, sc, D, sd}};
+  args.scheduler.max_swizzle_size = 8;
+  args.scheduler.raster_order = cutlass::gemm::kernel::detail::RasterOrderOptions::AlongM;
+  I8Gemm g;
+  if (g.can_implement(args) != cutlass::Status::kSuccess) return cudaErrorNotSupported;
+  if (!cws) cudaMalloc(&cws, 64 << 20);
+  if (g.initialize(args, cws, 0) != cutlass::Status::kSuccess) return cudaErrorUnknown;
+  return g.run(0) == cutlass::Status::kSuccess ? cudaSuccess : cudaErrorUnknown;
+}
+}  // namespace cl
+#endif
+
 using namespace tci;
+using namespace tci::i8g;
 
 __global__ void fill_rand(int8_t *p, size_t n, uint64_t seed) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -47,6 +107,8 @@ static int check(int64_t M, int64_t N, int64_t Kp, int L, int per_mod, bool full
   cudaMalloc(&B, (size_t)L * N * Kp);
   cudaMalloc(&D, (size_t)L * M * N);
   cudaMalloc(&mods, sizeof hm);
+  int *ctr;
+  cudaMalloc(&ctr, 4);
   cudaMemcpy(mods, hm, sizeof hm, cudaMemcpyHostToDevice);
   fill_rand<<<1024, 256>>>(A, (size_t)L * M * Kp, 1);
   fill_rand<<<1024, 256>>>(B, (size_t)L * N * Kp, 2);
@@ -63,7 +125,7 @@ static int check(int64_t M, int64_t N, int64_t Kp, int L, int per_mod, bool full
     cudaMemcpy(idx, hidx.data(), nidx * 8, cudaMemcpyHostToDevice);
   }
   cudaMalloc(&R, nidx);
-  cudaError_t e = launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, 0, nullptr);
+  cudaError_t e = launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, ctr, 0, nullptr);
   if (e != cudaSuccess) { printf("launch: %s\n", cudaGetErrorString(e)); return 1; }
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("run: %s\n", cudaGetErrorString(e)); return 1; }
@@ -85,27 +147,61 @@ static int check(int64_t M, int64_t N, int64_t Kp, int L, int per_mod, bool full
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, 0, nullptr);
+    launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, ctr, 0, nullptr);
     cudaEventRecord(a);
-    for (int r = 0; r < reps; r++) launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, 0, nullptr);
+    for (int r = 0; r < reps; r++) launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, ctr, 0, nullptr);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float t;
     cudaEventElapsedTime(&t, a, b);
     ms = t / reps;
   }
+  double ms_cl = 0;
+#ifdef WITH_CUTLASS
+  if (reps) {
+    int32_t *bm;
+    std::vector<int32_t> hb(L);
+    for (int b = 0; b < L; b++) hb[b] = hm[b / per_mod];
+    cudaMalloc(&bm, L * 4);
+    cudaMemcpy(bm, hb.data(), L * 4, cudaMemcpyHostToDevice);
+    cl::run(A, B, D, bm, (int)M, (int)N, (int)Kp, L);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; r++) cl::run(A, B, D, bm, (int)M, (int)N, (int)Kp, L);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float t;
+    cudaEventElapsedTime(&t, a, b);
+    ms_cl = t / reps;
+    cudaFree(bm);
+  }
+#endif
   const double ops = 2.0 * M * N * Kp * L;
   printf("M=%lld N=%lld K=%lld L=%d: %lld/%lld mismatches%s", (long long)M, (long long)N, (long long)Kp, L,
          (long long)bad, (long long)nidx, full ? " (all)" : " (sampled)");
   if (reps) printf("  %.3f ms  %.1f TOPS", ms, ops / ms * 1e-9);
+  if (ms_cl > 0) printf("  | CUTLASS %.3f ms  %.1f TOPS", ms_cl, ops / ms_cl * 1e-9);
   printf("\n");
-  cudaFree(A); cudaFree(B); cudaFree(D); cudaFree(R); cudaFree(mods);
+  cudaFree(A); cudaFree(B); cudaFree(D); cudaFree(R); cudaFree(mods); cudaFree(ctr);
   if (idx) cudaFree(idx);
   return bad != 0;
 }
 
 int main(int argc, char **argv) {
   int fails = 0;
+  if (argc > 1 && !strcmp(argv[1], "sweep")) {   // L2-policy sweep on the bench chunk shapes
+    const int mbs[] = {24, 32, 48, 64, 96, 1000};
+    for (int mb : mbs) {
+      g_i8_res_mb = mb;
+      printf("resident budget %d MB\n", mb);
+      fails += check(9216, 16384, 4096, 42, 3, false, 3);
+      fails += check(7680, 4096, 20480, 42, 3, false, 3);
+    }
+    printf(fails ? "FAIL\n" : "ALL OK\n");
+    return fails;
+  }
   fails += check(256, 256, 128, 1, 1, true, 0);
   fails += check(300, 272, 192, 3, 3, true, 0);
   fails += check(513, 528, 1088, 4, 1, true, 0);

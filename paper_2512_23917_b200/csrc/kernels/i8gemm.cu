@@ -13,10 +13,12 @@
 //    128-byte K block (SWIZZLE_128B tiles, 32 KB per CTA per stage) and both
 //    CTAs' transactions complete on the leader's mbarrier;
 //  * warp roles: warp 0 TMA producer, warp 1 MMA issuer (leader CTA; TMEM
-//    allocation in both), warps 2-5 epilogue;
+//    allocation in both), warps 2-9 epilogue (two per TMEM lane quarter);
 //  * accumulators in TMEM (2 x 256 int32 columns: the epilogue of tile i
 //    overlaps the main loop of tile i+1), read back with tcgen05.ld 32x32b,
-//    reduced mod m_b in integer arithmetic and stored as bytes;
+//    reduced mod m_b in integer arithmetic, packed to bytes in shared memory
+//    and written by TMA tensor stores (no generic global stores: the
+//    release-arrives that hand TMEM back never wait on store traffic);
 //  * a dynamic persistent schedule: the leader's producer claims tile ids
 //    from a global counter in raster order (plane, then the smaller
 //    operand's panels fastest) and broadcasts them to every role of both
@@ -39,10 +41,13 @@ constexpr int kBN = 256;            // UMMA N (each CTA loads 128 rows of B)
 constexpr int kBK = 128;            // bytes of K per stage (4 UMMA K-steps of 32)
 constexpr int kStages = 6;
 constexpr int kStageBytes = kBM * kBK + (kBN / 2) * kBK;   // 32 KB per CTA
-constexpr int kThreads = 192;       // 6 warps
+constexpr int kEpiWarps = 8;        // two warps per TMEM lane quarter, 4 column chunks each
+constexpr int kThreads = 64 + 32 * kEpiWarps;   // producer, MMA, epilogue warps
 constexpr int kTmemCols = 512;      // two 256-column int32 accumulators
 constexpr uint32_t kTxBytes = 2u * kStageBytes;             // both CTAs' loads land on the leader's barrier
-constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + 1024 /* align */ + 512 /* barriers, ids */;
+constexpr int kStgBytes = 2 * 32 * 32;   // per epilogue warp: two 32 x 32-byte output boxes
+constexpr size_t kSmemBytes =
+    (size_t)kStages * kStageBytes + (size_t)kEpiWarps * kStgBytes + 1024 /* align */ + 512 /* barriers, ids */;
 
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
@@ -176,16 +181,17 @@ __device__ __forceinline__ void tile_coords(const Params &p, int64_t t, int &b, 
 }
 
 constexpr int kTidSlots = 8;       // depth of the tile-id broadcast ring
-constexpr int kTidConsumers = 10;  // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue warps
+constexpr int kTidConsumers = 2 + 2 * kEpiWarps;   // leader: MMA + epilogue warps; peer: producer + epilogue warps
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     i8gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                  const __grid_constant__ Params p) {
+                  const __grid_constant__ CUtensorMap mapD, const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned stage ring (SWIZZLE_128B atoms), barriers behind it
   const uint32_t base_u = smem_u32(smem_raw);
   uint8_t *smem = smem_raw + (((base_u + 1023u) & ~1023u) - base_u);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
+  uint8_t *stg = smem + kStages * kStageBytes;   // epilogue output boxes
+  uint64_t *full = reinterpret_cast<uint64_t *>(stg + kEpiWarps * kStgBytes);
   uint64_t *empty = full + kStages;
   uint64_t *tfull = empty + kStages;
   uint64_t *tempty = tfull + 2;
@@ -206,7 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; a++) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[a], 2 * kEpiWarps);   // epilogue warps of both CTAs
     }
     for (int i = 0; i < kTidSlots; i++) {
       mbar_init(&idfull[i], 1);
@@ -247,32 +253,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int fi = 0;
       uint32_t fphase = 0;
-      for (;;) {
-        int t;
-        if (leader) {
-          // dynamic schedule: tiles are claimed in raster order as pairs free
-          // up, so the tiles in flight stay a compact block of the raster
-          mbar_wait(&idempty[fi], fphase ^ 1);
-          t = atomicAdd(p.counter, 1);
-          if (t >= p.tiles) t = -1;
-          idslot[fi] = t;
-          asm volatile(
-              "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, 1;\n st.shared::cluster.b32 [ra], %1;\n}\n" ::"r"(
-                  smem_u32(&idslot[fi])),
-              "r"(t)
-              : "memory");
-          mbar_arrive_remote(&idfull[fi], 0);   // release.cluster: the slot writes are visible first
-          mbar_arrive_remote(&idfull[fi], 1);
-          if (++fi == kTidSlots) {
-            fi = 0;
-            fphase ^= 1;
-          }
-        } else {
-          int slot;
-          t = next_tile(slot);
-          mbar_arrive_remote(&idempty[slot], 0);
+      // leader: publish tile id t in the ring (both CTAs); dynamic schedule:
+      // tiles are claimed in raster order as pairs free up, so the tiles in
+      // flight stay a compact block of the raster
+      auto publish = [&](int t) {
+        mbar_wait(&idempty[fi], fphase ^ 1);
+        idslot[fi] = t;
+        asm volatile(
+            "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, 1;\n st.shared::cluster.b32 [ra], %1;\n}\n" ::"r"(
+                smem_u32(&idslot[fi])),
+            "r"(t)
+            : "memory");
+        mbar_arrive_remote(&idfull[fi], 0);   // release.cluster: the slot writes are visible first
+        mbar_arrive_remote(&idfull[fi], 1);
+        if (++fi == kTidSlots) {
+          fi = 0;
+          fphase ^= 1;
         }
-        if (t < 0) break;
+      };
+      auto claim = [&]() {
+        const int c = atomicAdd(p.counter, 1);
+        return c < p.tiles ? c : -1;
+      };
+      int t;
+      if (leader) {
+        t = claim();
+        publish(t);
+      } else {
+        int slot;
+        t = next_tile(slot);
+        mbar_arrive_remote(&idempty[slot], 0);
+      }
+      while (t >= 0) {
+        // the next claim is in flight while this tile's loads issue (its
+        // latency stays off the tile boundary)
+        const int t_next_raw = leader ? atomicAdd(p.counter, 1) : 0;
         int b, tm, tn;
         tile_coords(p, t, b, tm, tn);
         const int ra = tm * 256 + (int)rank * kBM, rb = tn * kBN + (int)rank * (kBN / 2);
@@ -287,6 +302,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             stage = 0;
             phase ^= 1;
           }
+        }
+        if (leader) {
+          t = t_next_raw < p.tiles ? t_next_raw : -1;
+          publish(t);
+        } else {
+          int slot;
+          t = next_tile(slot);
+          mbar_arrive_remote(&idempty[slot], 0);
         }
       }
     }
@@ -327,12 +350,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ===== epilogue: warps 2..5 -> TMEM lane quarter (warp % 4) =====
-    const int q = warp & 3;
+    // ===== epilogue: warps 2..9; warp w reads TMEM lane quarter w % 4 and
+    // column chunks [4h, 4h + 4) (h = which of the two warps of that quarter) =====
+    const int e = warp - 2, q = warp & 3, h = e >> 2;
+    uint8_t *box = stg + e * kStgBytes;
     int acc = 0;
     uint32_t acc_phase = 0;
     ModM mod;
     int cur_mod = -1;
+    int nbox = 0;
     for (;;) {
       int slot;
       const int t = next_tile(slot);
@@ -348,12 +374,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t row = (int64_t)tm * 256 + rank * kBM + q * 32 + lane;
-      const bool row_ok = row < p.M;
-      uint8_t *drow = p.D + ((int64_t)b * p.M + (row_ok ? row : 0)) * p.N;
+      const int row0 = tm * 256 + (int)rank * kBM + q * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kBN);
 #pragma unroll 1
-      for (int c = 0; c < kBN / 32; c++) {
+      for (int c = 4 * h; c < 4 * h + 4; c++) {
         uint32_t v[32];
         tmem_ld32(taddr + (uint32_t)(c * 32), v);
         uint32_t w[8];
@@ -361,16 +385,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 8; j++)
           w[j] = mod((int)v[4 * j]) | (mod((int)v[4 * j + 1]) << 8) | (mod((int)v[4 * j + 2]) << 16) |
                  (mod((int)v[4 * j + 3]) << 24);
-        const int64_t col = (int64_t)tn * kBN + c * 32;
-        if (row_ok) {   // streaming stores: the bytes are read once, by the CRT
-          if (col + 32 <= p.N) {
-            uint4 *dst = reinterpret_cast<uint4 *>(drow + col);
-            __stcs(dst, make_uint4(w[0], w[1], w[2], w[3]));
-            __stcs(dst + 1, make_uint4(w[4], w[5], w[6], w[7]));
-          } else if (col + 16 <= p.N) {   // N is a multiple of 16
-            __stcs(reinterpret_cast<uint4 *>(drow + col), make_uint4(w[0], w[1], w[2], w[3]));
-          }
+        // 32 rows x 32 bytes through shared memory, out by one TMA store (rows
+        // and columns beyond M / N are clipped by the tensor map)
+        uint8_t *bx = box + (nbox & 1) * 1024;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        __syncwarp();
+        uint4 *dst = reinterpret_cast<uint4 *>(bx + lane * 32);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                           reinterpret_cast<uint64_t>(&mapD)),
+                       "r"(tn * kBN + c * 32), "r"(row0), "r"(b), "r"(smem_u32(bx))
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         }
+        nbox++;
       }
       tc_fence_before();
       __syncwarp();
@@ -380,6 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   }
 
   __syncwarp();
@@ -427,6 +460,19 @@ bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t Kp, int L,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// the output D [L][M][N] uint8 in 32 x 32-byte boxes (TMA stores)
+bool make_map_d(CUtensorMap *m, void *base, int64_t M, int64_t N, int L) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)L};
+  const cuuint64_t strides[2] = {(cuuint64_t)N, (cuuint64_t)(M * N)};
+  const cuuint32_t box[3] = {32, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 }  // namespace i8g
 
 // D[b] = (A[b] B[b]^T) mod m_(b / per_mod) over L planes; A [L][M][Kp],
@@ -438,8 +484,9 @@ cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t 
   if (M <= 0 || N <= 0 || L <= 0) return cudaSuccess;
   if (Kp % 64 || N % 16 || (uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)D % 16 || !counter)
     return cudaErrorInvalidValue;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, Kp, L, kBM) || !make_map(&mb, B, N, Kp, L, kBN / 2)) return cudaErrorNotSupported;
+  CUtensorMap ma, mb, md;
+  if (!make_map(&ma, A, M, Kp, L, kBM) || !make_map(&mb, B, N, Kp, L, kBN / 2) || !make_map_d(&md, D, M, N, L))
+    return cudaErrorNotSupported;
   Params p{};
   p.M = M;
   p.N = N;
@@ -471,7 +518,7 @@ cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t 
   const int64_t clusters = std::min<int64_t>(p.tiles, sms / 2);
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
-  i8gemm_kernel<<<(unsigned)(2 * clusters), kThreads, kSmemBytes, s>>>(ma, mb, p);
+  i8gemm_kernel<<<(unsigned)(2 * clusters), kThreads, kSmemBytes, s>>>(ma, mb, md, p);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

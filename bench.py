@@ -318,7 +318,7 @@ def run_tci(args):
     # ---- timed region (device time, CUDA events on the launching stream) ----
     sampler = ClockSampler(gpu_index(local)) if rank == 0 else None
     time.sleep(0.3 if sampler else 0)
-    tci.tci_profile_enable(ctx.handle, True)
+    ctx.ozaki_guard_stats(reset=True)
     n0 = ctx.launch_count()
     barrier()
     torch.cuda.synchronize()
@@ -332,11 +332,32 @@ def run_tci(args):
     barrier()
     t_step = e0.elapsed_time(e1) / 1e3 / args.steps
     launches = ctx.launch_count() - n0
+    clocks = sampler.stop() if sampler else None
+    # Ozaki accuracy guard over the timed steps (R26): GEMMs checked,
+    # recomputed on DMMA, largest estimated relative Frobenius error
+    gs = ctx.ozaki_guard_stats()
+    guard = {"ozaki_gemms": gs["gemms"], "dmma_recomputations": gs["fallbacks"],
+             "balanced": gs["balanced"], "max_est_rel_frob": gs["max_est"]} if algo == "ozaki" else None
+    if gather == "p2p" and ctx.gather_status():
+        raise SystemExit(f"[rank {rank}] peer-memory gather barrier timed out in the timed region")
+    # per-kernel profile (roofline inputs) from separate steps: CUDA events on
+    # the context stream around every GEMM / INT8 GEMM / MPO-pass launch
+    # (kept out of the timed region above)
+    prof_steps = max(1, min(args.steps, 3))
+    tci.tci_profile_enable(ctx.handle, True)
+    torch.cuda.synchronize()
+    ep0 = torch.cuda.Event(enable_timing=True)
+    ep1 = torch.cuda.Event(enable_timing=True)
+    ep0.record(stream)
+    for _ in range(prof_steps):
+        step()
+    ep1.record(stream)
+    torch.cuda.synchronize()
+    t_prof = ep0.elapsed_time(ep1) / 1e3
     prof = {k: tci.tci_profile_query(ctx.handle, v) for k, v in
             (("gemm", tci.PROF_GEMM), ("skinny", tci.PROF_SKINNY), ("permute", tci.PROF_PERMUTE),
              ("int8_gemm", tci.PROF_I8))}
     tci.tci_profile_enable(ctx.handle, False)
-    clocks = sampler.stop() if sampler else None
     if ws > 1:
         import torch.distributed as dist
         tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
@@ -522,6 +543,9 @@ def run_tci(args):
                    "h2d_bound_ms_per_step": h2d / (h2d_gbs * 1e9) * 1e3,
                    "single_call": e2e_single}
             del bufs, outs
+    torch.cuda.synchronize()
+    if gather == "p2p" and ctx.gather_status():
+        raise SystemExit(f"[rank {rank}] peer-memory gather barrier timed out in the end-to-end loops")
 
     if rank != 0:
         ctx.close()
@@ -539,18 +563,26 @@ def run_tci(args):
     sk = prof["skinny"]
     i8 = prof["int8_gemm"]
     if algo == "ozaki" and i8["launches"]:
-        # dominant kernel: the CUTLASS sm100 INT8 tcgen05 GEMM (batched residue products)
-        i8_peak = peaks.get("bf16_tflops", 1646.4) * 2.0   # measured bf16 x nominal int8/bf16 (4.5/2.25)
+        # dominant kernel: the hand-written tcgen05 kind::i8 GEMM (i8gemm.cu; all
+        # residue products of one Ozaki GEMM in one launch). It runs inside a
+        # ~100 ms step under the power cap, so the roofline denominator is the
+        # SUSTAINED measured bf16 rate x the nominal int8/bf16 ratio (2); the
+        # burst-based fraction is kept beside it.
+        i8_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1646.4)) * 2.0
+        i8_burst = peaks.get("bf16_tflops", 1646.4) * 2.0
         i8_ach = i8["flops"] / (i8["ms"] / 1e3) / 1e12
         roofline = {
-            "bound": "tensor", "kernel": "CUTLASS sm100 INT8 tcgen05 GEMM (Ozaki-II residue products; UTCIMMA)",
+            "bound": "tensor",
+            "kernel": "i8gemm_kernel (hand-written tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM; UTCIMMA)",
             "achieved": i8_ach, "peak": i8_peak, "unit": "TOPS", "frac": i8_ach / i8_peak,
+            "frac_vs_burst_peak": i8_ach / i8_burst,
             "traffic": traffic_from_profiles(name + "_ozaki"),
-            "peak_source": f"MEASURED_PEAKS.json bf16_tflops x 2 (nominal int8/bf16 = 4.5/2.25 PFLOP/s)",
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8/bf16 = 4.5/2.25 PFLOP/s); "
+                            "burst: bf16_tflops x 2"),
             "ops_per_launch": i8["flops"] / i8["launches"], "launches": i8["launches"],
-            "share_of_step": i8["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
+            "share_of_step": i8["ms"] / 1e3 / t_prof if t_prof > 0 else None,
             "ozaki_gemm_fp64_equivalent_tflops": achieved,
-            "ozaki_gemm_share_of_step": g["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
+            "ozaki_gemm_share_of_step": g["ms"] / 1e3 / t_prof if t_prof > 0 else None,
         }
     else:
         roofline = {
@@ -559,13 +591,13 @@ def run_tci(args):
             "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": traffic,
             "peak_source": FP64_PEAK_SOURCE,
             "flops_per_launch": gemm_flops_per_launch, "launches": g["launches"],
-            "gemm_share_of_step": g["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
+            "gemm_share_of_step": g["ms"] / 1e3 / t_prof if t_prof > 0 else None,
         }
     roofline["secondary"] = {
         "kernel": "skinny_dmma_kernel (MPO pass, FP64 tensor cores, 3M)", "bound": "hbm",
         "achieved": (sk["bytes"] / (sk["ms"] / 1e3) / 1e9) if sk["launches"] else None,
         "peak": peaks.get("hbm_gbs"), "unit": "GB/s", "peak_source": peak_src,
-        "share_of_step": sk["ms"] / 1e3 / (t_step * args.steps) if t_step > 0 else None,
+        "share_of_step": sk["ms"] / 1e3 / t_prof if t_prof > 0 else None,
     }
 
     cpu = None
@@ -603,8 +635,16 @@ def run_tci(args):
                                       if gather == "p2p" else "by NCCL")) if ws > 1 else "single GPU",
                    "l2": "inputs larger than L2 (L, psi, R >= 1 GB each): no flush"},
         "pct_fp64_tc_peak": value / FP64_PEAK_TFLOPS * 100, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+        "pct_fp64_tc_peak_note": ("algorithmic fp64 flops per second over the native FP64 tensor-core (DMMA) "
+                                  "peak; with the Ozaki algorithm this is the emulation's gain over native "
+                                  "FP64, not a fraction of an executing unit (that is roofline.frac)"),
+        "native_fp64_dmma": ({"value": alt["value"], "unit": UNIT, "pct_fp64_tc_peak": alt["pct_fp64_tc_peak"],
+                              "algorithm": alt["algorithm"]} if alt else None),
+        "ozaki_guard": guard,
         "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
-        "cpu_baseline": cpu, "parity": parity, "profile": prof,
+        "cpu_baseline": cpu, "parity": parity,
+        "profile": dict(prof, steps=prof_steps, ms_total=t_prof * 1e3,
+                        note="separate profiled steps (CUDA events around each launch), not the timed region"),
     }
     print(json.dumps(line), flush=True)
     ctx.close()

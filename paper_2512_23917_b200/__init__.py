@@ -595,20 +595,38 @@ class Context:
         self._ws_need.clear()
 
     # -- workspace -----------------------------------------------------------
+    def _on_stream(self):
+        """Allocations for work on the context stream are made on that stream
+        (the caching allocator then orders their reuse after it)."""
+        return self.torch.cuda.stream(self.stream)
+
     def ensure_workspace(self, nbytes: int):
         if nbytes <= self._ws_bytes:
             return
         torch = self.torch
         nbytes = int(nbytes)
-        self._ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        if self._ws is not None:
+            # kernels already queued on the context stream may still use the
+            # old workspace: its memory is reused only after they complete
+            self._ws.record_stream(self.stream)
+        with self._on_stream():
+            self._ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
         ptr = (self._ws.data_ptr() + 255) // 256 * 256
         tci_workspace_attach(self.handle, ptr, nbytes)
         self._ws_bytes = nbytes
 
+    def _empty(self, shape, dtype, device=None):
+        with self._on_stream():
+            return self.torch.empty(shape, dtype=dtype, device=device if device is not None else f"cuda:{self.device}")
+
+    def _empty_like(self, x):
+        with self._on_stream():
+            return self.torch.empty_like(x)
+
     # -- operations ----------------------------------------------------------
     def permute(self, x, new_order, out=None):
         if out is None:
-            out = self.torch.empty([x.shape[p] for p in new_order], dtype=x.dtype, device=x.device)
+            out = self._empty([x.shape[p] for p in new_order], dtype=x.dtype, device=x.device)
         tci_permute(self.handle, self.tensor(x), list(new_order), self.tensor(out))
         return out
 
@@ -618,7 +636,7 @@ class Context:
     def contract(self, a, la, b, lb, lc, out=None):
         if out is None:
             shape = self.contract_out_shape(a, la, b, lb, lc)
-            out = self.torch.empty(shape, dtype=a.dtype, device=a.device)
+            out = self._empty(shape, dtype=a.dtype, device=a.device)
         ha, hb, hc = self.tensor(a), self.tensor(b), self.tensor(out)
         key = (ha, hb, hc, la if isinstance(la, str) else tuple(la), lb if isinstance(lb, str) else tuple(lb),
                lc if isinstance(lc, str) else tuple(lc))
@@ -640,7 +658,7 @@ class Context:
 
     def heff_apply(self, L, W1, W2, R, psi, out=None):
         if out is None:
-            out = self.torch.empty((L.shape[2], psi.shape[1], psi.shape[2], R.shape[2]), dtype=psi.dtype,
+            out = self._empty((L.shape[2], psi.shape[1], psi.shape[2], R.shape[2]), dtype=psi.dtype,
                                    device=psi.device)
         self.ensure_workspace(self.heff_workspace_size(L, W1, W2, R, psi))
         tci_heff_apply(self.handle, *[self.tensor(x) for x in (L, W1, W2, R, psi, out)])
@@ -660,7 +678,7 @@ class Context:
         if out is None:
             shape = ((ket.shape[2], W.shape[1], bra.shape[2]) if side == 0 else
                      (ket.shape[0], W.shape[0], bra.shape[0]))
-            out = self.torch.empty(shape, dtype=ket.dtype, device=ket.device)
+            out = self._empty(shape, dtype=ket.dtype, device=ket.device)
         h = [self.tensor(x) for x in (E, ket, W, bra, out)]
         self.ensure_workspace(tci_env_workspace_size(self.handle, side, *h))
         tci_env_update(self.handle, side, *h)
@@ -669,7 +687,7 @@ class Context:
     def cplx_conj(self, x, out=None):
         """Complex conjugate (tci_cplx_conj); out=x conjugates in place."""
         if out is None:
-            out = self.torch.empty_like(x)
+            out = self._empty_like(x)
         tci_cplx_conj(self.handle, self.tensor(x), self.tensor(out))
         return out
 
@@ -679,7 +697,7 @@ class Context:
             for t, l in ((A, la), (B, lb), (U, lu)):
                 for ch, n in zip(l, t.shape):
                     dims[ch] = n
-            out = self.torch.empty([dims[ch] for ch in lt], dtype=A.dtype, device=A.device)
+            out = self._empty([dims[ch] for ch in lt], dtype=A.dtype, device=A.device)
         self.ensure_workspace(tci_tebd_workspace_size(self.handle, self.tensor(A), la, self.tensor(B), lb,
                                                       self.tensor(U), lu, self.tensor(out), lt))
         tci_tebd_theta(self.handle, self.tensor(A), la, self.tensor(B), lb, self.tensor(U), lu,
@@ -688,9 +706,9 @@ class Context:
 
     def _svd_outputs(self, a, k, cap):
         torch = self.torch
-        u = torch.empty(tuple(a.shape[:k]) + (cap,), dtype=a.dtype, device=a.device)
-        s = torch.empty((cap,), dtype=torch.float64, device=a.device)
-        vd = torch.empty((cap,) + tuple(a.shape[k:]), dtype=a.dtype, device=a.device)
+        u = self._empty(tuple(a.shape[:k]) + (cap,), dtype=a.dtype, device=a.device)
+        s = self._empty((cap,), dtype=torch.float64, device=a.device)
+        vd = self._empty((cap,) + tuple(a.shape[k:]), dtype=a.dtype, device=a.device)
         return u, s, vd
 
     def _fresh(self, t) -> int:
@@ -743,7 +761,7 @@ class Context:
             c = 1 if i == n - 1 else min(int(chi_max), left * dout, A[i].shape[2] * W[i].shape[1])
             caps.append((left, dout, c))
             left = c
-        B = [torch.empty(c, dtype=A[0].dtype, device=A[0].device) for c in caps]
+        B = [self._empty(c, dtype=A[0].dtype, device=A[0].device) for c in caps]
         ha, hw = [self.tensor(x) for x in A], [self.tensor(x) for x in W]
         self.ensure_workspace(tci_mps_mpo_zipup_workspace_size(self.handle, ha, hw, chi_max))
         hb = [self._fresh(x) for x in B]
@@ -780,13 +798,13 @@ class Context:
 
     def linear_combine(self, ins, coefs=None, out=None):
         if out is None:
-            out = self.torch.empty_like(ins[0])
+            out = self._empty_like(ins[0])
         tci_linear_combine(self.handle, [self.tensor(x) for x in ins], coefs, self.tensor(out))
         return out
 
     def scale(self, x, s, out=None):
         if out is None:
-            out = self.torch.empty_like(x)
+            out = self._empty_like(x)
         tci_scale(self.handle, self.tensor(x), s, self.tensor(out))
         return out
 
@@ -798,7 +816,7 @@ class Context:
 
     def mps_overlap(self, bra, ket, out=None):
         if out is None:
-            out = self.torch.empty((bra[-1].shape[2], ket[-1].shape[2]), dtype=bra[0].dtype, device=bra[0].device)
+            out = self._empty((bra[-1].shape[2], ket[-1].shape[2]), dtype=bra[0].dtype, device=bra[0].device)
         tci_mps_overlap(self.handle, [self.tensor(x) for x in bra], [self.tensor(x) for x in ket], self.tensor(out))
         return out
 

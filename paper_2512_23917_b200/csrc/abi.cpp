@@ -1076,7 +1076,10 @@ tci_status_t tci_allgather(tci_ctx_t ctx, tci_tensor_t shard, tci_tensor_t full)
 // Peer-memory all-gather
 // ---------------------------------------------------------------------------
 static std::mutex g_ipc_mu;
-static std::map<void *, void *> g_ipc_base;   // pointer handed out -> mapped base
+// pointer handed out -> (mapped base, opens): cudaIpcOpenMemHandle returns the
+// same base (reference-counted) when one handle is opened twice in a context,
+// so every tci_ipc_open is matched by exactly one cudaIpcCloseMemHandle
+static std::map<void *, std::pair<void *, int>> g_ipc_base;
 
 tci_status_t tci_ipc_handle(const void *dev_ptr, void *handle, size_t *offset) {
   if (!dev_ptr || !handle || !offset) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL argument");
@@ -1109,7 +1112,9 @@ tci_status_t tci_ipc_open(const void *handle, size_t offset, void **dev_ptr) {
   TCI_CUDA_CHECK(cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess));
   *dev_ptr = static_cast<char *>(base) + offset;
   std::lock_guard<std::mutex> lk(g_ipc_mu);
-  g_ipc_base[*dev_ptr] = base;
+  auto it = g_ipc_base.find(*dev_ptr);
+  if (it == g_ipc_base.end()) g_ipc_base[*dev_ptr] = {base, 1};
+  else it->second.second++;
   return TCI_OK;
 }
 
@@ -1119,8 +1124,8 @@ tci_status_t tci_ipc_close(void *dev_ptr) {
     std::lock_guard<std::mutex> lk(g_ipc_mu);
     auto it = g_ipc_base.find(dev_ptr);
     if (it == g_ipc_base.end()) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "ipc_close: pointer was not opened by tci_ipc_open");
-    base = it->second;
-    g_ipc_base.erase(it);
+    base = it->second.first;
+    if (--it->second.second == 0) g_ipc_base.erase(it);
   }
   TCI_CUDA_CHECK(cudaIpcCloseMemHandle(base));
   return TCI_OK;
@@ -1137,8 +1142,10 @@ tci_status_t tci_gather_register(tci_ctx_t ctx, int nranks, int rank, void *cons
   if (!ctx->g_err) {
     TCI_CUDA_CHECK(cudaSetDevice(ctx->device));
     TCI_CUDA_CHECK(cudaMalloc(&ctx->g_err, sizeof(int)));   // registration time, not a compute call
-    TCI_CUDA_CHECK(cudaMemset(ctx->g_err, 0, sizeof(int)));
   }
+  // a new registration starts without the previous one's (sticky) timeout
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  TCI_CUDA_CHECK(cudaMemset(ctx->g_err, 0, sizeof(int)));
   TCI_CUDA_CHECK(gather_preload());
   TCI_CUDA_CHECK(ozaki_preload());
   ctx->g_nranks = nranks;

@@ -10,7 +10,8 @@
 //    stores, then spins until every slot of its own array reached `epoch`.
 //    Flags only grow (epoch counter per context), so they never need a reset.
 //    A %globaltimer bound turns a missing peer into an error flag instead of
-//    a hang.
+//    a hang; the flag is sticky until the next tci_gather_register (later
+//    barriers return at once) and tci_gather_status reports it.
 //  * push_rows: the unfused path (DMMA GEMM4 or the generic tree): the local
 //    slab is copied to every peer with 16-byte stores over NVLink.
 #include <algorithm>
@@ -45,6 +46,9 @@ __global__ void gather_barrier(const PeerTable t, int rank, int nranks, uint32_t
     st_release_sys(static_cast<uint32_t *>(t.flags[j]) + rank, epoch);
   }
   __syncthreads();
+  // sticky error: once a barrier of this registration timed out, later
+  // barriers do not wait again (the run is already reported as failed)
+  if (*reinterpret_cast<volatile int *>(err)) return;
   if (j < nranks) {
     const uint32_t *mine = static_cast<const uint32_t *>(t.flags[rank]) + j;
     const uint64_t t0 = globaltimer();

@@ -306,12 +306,9 @@ __device__ __forceinline__ void mma_step(Acc<C> &acc, const Frag<C> &f) {
     }
 }
 
+// one output tile (grid position bid) of the GEMM
 template <class C>
-__global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p, int tiles_m,
-                                                             int tiles_n) {
-  // Ozaki guard recomputation: nothing to do unless the guard asked for it
-  if (p.run_if && *reinterpret_cast<const volatile int *>(p.run_if) == 0) return;
-  extern __shared__ __align__(128) char smem[];
+__device__ __forceinline__ void gemm_dmma_tile(const GemmProblem &p, int tiles_m, int tiles_n, int bid, char *smem) {
   char *sA0 = smem;
   char *sB0 = smem + C::STAGES * C::A_STAGE * C::ESZ;
   double *sumA0 = reinterpret_cast<double *>(smem + C::STAGES * (C::A_STAGE + C::B_STAGE) * C::ESZ);
@@ -320,7 +317,6 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
   // grouped rasterization: GROUP M-tiles walk the N-tiles together so the
   // B panels they share stay in L2
   constexpr int GROUP = 8;
-  const int bid = blockIdx.x;
   const int per_group = GROUP * tiles_n;
   const int first_m = (bid / per_group) * GROUP;
   const int gsize = min(tiles_m - first_m, GROUP);
@@ -525,6 +521,22 @@ __global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p
 }
 
 template <class C>
+__global__ void __launch_bounds__(C::NT, 1) gemm_dmma_kernel(const GemmProblem p, int tiles_m, int tiles_n) {
+  extern __shared__ __align__(128) char smem[];
+  if (!p.run_if) {   // one CTA per tile
+    gemm_dmma_tile<C>(p, tiles_m, tiles_n, blockIdx.x, smem);
+    return;
+  }
+  // the Ozaki guard's recomputation: a small persistent grid that does
+  // nothing unless the guard set the flag (cheap when it did not)
+  if (*reinterpret_cast<const volatile int *>(p.run_if) == 0) return;
+  for (int bid = blockIdx.x; bid < tiles_m * tiles_n; bid += gridDim.x) {
+    __syncthreads();   // the previous tile's shared-memory reads are done
+    gemm_dmma_tile<C>(p, tiles_m, tiles_n, bid, smem);
+  }
+}
+
+template <class C>
 cudaError_t run(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   auto kern = gemm_dmma_kernel<C>;
   static uint64_t attr_set = 0;   // per instantiation, one bit per device
@@ -537,7 +549,8 @@ cudaError_t run(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   }
   const int64_t tm = (p.M + C::BM - 1) / C::BM, tn = (p.N + C::BN - 1) / C::BN;
   if (tm * tn > 0x7fffffffLL || p.splitk > 65535) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)(tm * tn), 1, (unsigned)(p.splitk > 1 ? p.splitk : 1));
+  dim3 grid((unsigned)(p.run_if ? std::min<int64_t>(tm * tn, 2 * 148) : tm * tn), 1,
+            (unsigned)(p.splitk > 1 ? p.splitk : 1));
   kern<<<grid, C::NT, C::SMEM, s>>>(p, (int)tm, (int)tn);
   if (launches) ++*launches;
   return cudaGetLastError();

@@ -150,6 +150,18 @@ def oracle_rows_run(inp_np, rows):
     return res, time.perf_counter() - t0
 
 
+def cpu_model():
+    """Host CPU model name (lscpu's "Model name"), for the cpu_baseline record."""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(inp_np, chi, flops_full, budget_s=15.0, gpu_out=None):
     import oracle
     oracle.build()
@@ -163,6 +175,7 @@ def cpu_baseline(inp_np, chi, flops_full, budget_s=15.0, gpu_out=None):
     t = t1 + t2
     val = len(rows_all) * (flops_full / chi) / t / 1e12
     out = {"value": val, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+           "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
            "sample": f"{len(rows_all)} output rows b (of {chi}) of the same apply, exact chain "
                      f"(oracle.heff_rows: L sliced at b); {t:.1f} s; TFLOP/s = rows x flops/row / time"}
     parity = None
@@ -207,6 +220,7 @@ def run_reference(args):
         "data": "synthetic (seeded counter-based generator; exact model MPO)",
         "config": {"workload": name, "chi": chi, "d": d, "D": D, "dtype": cfg["dtype"], "model": cfg["model"]},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+                         "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
                          "sample": f"{rows_per_step} output rows per step (of {chi}); TFLOP/s = rows x "
                                    f"full-apply flops/chi / time"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -3,7 +3,7 @@
 // Pure data movement: bitwise exact. HBM-bound (roofline = measured copy
 // bandwidth, 2 x bytes per element).
 //
-// The caller (plan.cpp) has fused adjacent legs that stay adjacent and
+// The caller (contract.cpp permute_exec / permute_into) has fused adjacent legs that stay adjacent and
 // dropped extent-1 legs, so the problem is `n` fused out legs with the input
 // stride of each. Two kernels:
 //  * copy_rows: the out-fastest leg is also in-contiguous -> each thread

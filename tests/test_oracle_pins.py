@@ -364,6 +364,31 @@ def test_heff_rows_bitwise(oracle_mod):
     assert np.array_equal(oracle_mod.heff_rows(*args, rows), full[rows])
 
 
+@pytest.mark.parametrize("side", [0, 1])
+def test_env_rows_bitwise(oracle_mod, side):
+    """env_rows (the sampled checker of the full-size environment tests) equals
+    the matching rows of the full env_left / env_right bitwise: slicing the
+    ket's outgoing bond is a free leg of every pairwise contract in the chain,
+    so no element's summation order changes. env_left/env_right themselves
+    are pinned against dense operators and closed forms below."""
+    rng = np.random.default_rng(31 + side)
+    chi, d, D, chi2 = 5, 2, 3, 7
+
+    def c(*s):
+        return rng.standard_normal(s) + 1j * rng.standard_normal(s)
+    W = c(D, D, d, d)
+    if side == 0:
+        E, ket, bra = c(chi, D, chi), c(chi, d, chi2), c(chi, d, chi2)
+        full = oracle_mod.env_left(E, ket, W, bra)
+    else:
+        E, ket, bra = c(chi, D, chi), c(chi2, d, chi), c(chi2, d, chi)
+        full = oracle_mod.env_right(E, ket, W, bra)
+    rows = [0, 2, chi2 - 1]
+    got = oracle_mod.env_rows(side, E, ket, W, bra, rows)
+    assert got.shape == (len(rows),) + full.shape[1:]
+    assert np.array_equal(got, full[rows])
+
+
 def test_heisenberg_singlet(oracle_mod):
     g = golden("closed_forms.json")["heisenberg_two_site"]
     W, lb, rb = synth.heisenberg_mpo(1.0)

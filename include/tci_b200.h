@@ -139,6 +139,30 @@ TCI_API tci_status_t tci_set_gemm_algorithm(tci_ctx_t ctx, int algo);
  * |A'| < 2^t), and the moduli (moduli[nmod], may be NULL). Returns 0, or
  * OUT_OF_RANGE when K is outside 1..131072 (the int32 exactness limit). */
 TCI_API int tci_ozaki_params(int64_t K, int *nmod, int *t, int *moduli);
+
+/* Complex128 Ozaki-II variant of a context (reading R33):
+ *  TCI_OZAKI_CPLX_GAUSS (default): Gaussian moduli -- odd, pairwise coprime,
+ *    every prime factor = 1 mod 4 -- each with a root j_l, j_l^2 = -1 (mod
+ *    m_l); a + ib is mapped to (a + j_l b, a - j_l b) mod m_l, a ring
+ *    homomorphism Z[i] -> Z_m x Z_m, so a complex product modulo m_l is two
+ *    INT8 residue GEMMs (15 moduli -> 30 GEMMs for K <= ~69k);
+ *  TCI_OZAKI_CPLX_3M: the float64 moduli with the 3M split (P = ArBr,
+ *    Q = AiBi, S = (Ar+Ai)(Br+Bi)): three GEMMs per modulus (14 -> 42).
+ * Both are exact up to the same operand truncation (R26). The initial value
+ * comes from TCI_OZAKI_CPLX = gauss | 3m (read at context creation).
+ * Synchronizes the context stream. Errors: DEAD_CONTEXT, INVALID_ARGUMENT. */
+#define TCI_OZAKI_CPLX_GAUSS 0
+#define TCI_OZAKI_CPLX_3M 1
+TCI_API tci_status_t tci_set_ozaki_complex(tci_ctx_t ctx, int variant);
+
+/* Diagnostic (pure host): the parameters of the complex128 Ozaki GEMMs of
+ * `variant` for contraction length K: moduli count, bit budget t, moduli,
+ * the roots j_l (Gaussian; 0 for 3M) and the residue planes per modulus
+ * (2 Gaussian, 3 3M). Arrays hold up to 16 entries; any out-pointer may be
+ * NULL. Returns 0, INVALID_ARGUMENT for an unknown variant, or OUT_OF_RANGE
+ * when K is outside 1..131072. */
+TCI_API int tci_ozaki_params_complex(int64_t K, int variant, int *nmod, int *t, int *moduli, int *roots,
+                                     int *planes_per_mod);
 TCI_API tci_status_t tci_get_gemm_algorithm(tci_ctx_t ctx, int *algo);
 
 /* Accuracy guard of the Ozaki-II GEMMs (reading R26; the north

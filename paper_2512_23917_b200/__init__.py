@@ -52,7 +52,8 @@ EXPORTED = [
     "tci_mps_mpo_zipup_workspace_size", "tci_mps_mpo_zipup", "tci_heff_apply_staged",
     "tci_ipc_handle", "tci_ipc_open", "tci_ipc_close", "tci_gather_register", "tci_heff_apply_gather",
     "tci_gather_status", "tci_tebd_workspace_size", "tci_copy_async", "tci_lane_record", "tci_lane_wait",
-    "tci_set_ozaki_guard", "tci_ozaki_guard_stats",
+    "tci_set_ozaki_guard", "tci_ozaki_guard_stats", "tci_ozaki_params_complex",
+    "tci_set_ozaki_complex",
 ]
 
 
@@ -122,6 +123,8 @@ _sig = {
     "tci_set_gemm_algorithm": ([_vp, ctypes.c_int], ctypes.c_int),
     "tci_ozaki_params": ([ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                           ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "tci_ozaki_params_complex": ([ctypes.c_int64, ctypes.c_int] + [ctypes.POINTER(ctypes.c_int)] * 5, ctypes.c_int),
+    "tci_set_ozaki_complex": ([_vp, ctypes.c_int], ctypes.c_int),
     "tci_get_gemm_algorithm": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_set_ozaki_guard": ([_vp, ctypes.c_double], ctypes.c_int),
     "tci_ozaki_guard_stats": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
@@ -450,6 +453,22 @@ def tci_ozaki_params(K: int):
     mods = (ctypes.c_int * 16)()
     st = _lib.tci_ozaki_params(int(K), ctypes.byref(n), ctypes.byref(t), mods)
     return st, n.value, t.value, [mods[i] for i in range(n.value)]
+
+
+TCI_OZAKI_CPLX_GAUSS = 0
+TCI_OZAKI_CPLX_3M = 1
+
+
+def tci_set_ozaki_complex(ctx: int, variant: int) -> None:
+    _ok(_lib.tci_set_ozaki_complex(_vp(ctx), int(variant)), "tci_set_ozaki_complex")
+
+
+def tci_ozaki_params_complex(K: int, variant: int = TCI_OZAKI_CPLX_GAUSS):
+    n, t, ppm = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    mods, roots = (ctypes.c_int * 16)(), (ctypes.c_int * 16)()
+    st = _lib.tci_ozaki_params_complex(int(K), int(variant), ctypes.byref(n), ctypes.byref(t), mods, roots,
+                                       ctypes.byref(ppm))
+    return st, n.value, t.value, [mods[i] for i in range(n.value)], [roots[i] for i in range(n.value)], ppm.value
 
 
 def tci_set_ozaki_guard(ctx: int, tol: float) -> None:
@@ -782,6 +801,9 @@ class Context:
 
     def set_ozaki_guard(self, tol: float):
         tci_set_ozaki_guard(self.handle, tol)
+
+    def set_ozaki_complex(self, variant: int):
+        tci_set_ozaki_complex(self.handle, variant)
 
     def ozaki_guard_stats(self, reset: bool = False) -> dict:
         return tci_ozaki_guard_stats(self.handle, reset)

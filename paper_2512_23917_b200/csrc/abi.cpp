@@ -59,6 +59,7 @@ tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g) {
   if (ctx->prof_on && g.zalgo == kZOzaki) gg.oz_prof = &pf;
   gg.oz_tol = ctx->oz_tol;
   gg.oz_guard = ctx->oz_guard;
+  gg.oz_gauss = ctx->oz_gauss;
   TCI_CUDA_CHECK(launch_gemm(gg, ctx->stream, &ctx->launches));
   ps.done();
   for (int i = 0; i < pf.n; i++) ctx->prof.push_back({kProfI8, pf.a[i], pf.b[i], pf.ops[i], 0.0});
@@ -242,6 +243,10 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
     if (!strcmp(e, "0") || !strcmp(e, "off")) c->oz_tol = 0.0;
   }
   c->oz_guard = nullptr;
+  c->oz_gauss = 1;
+  if (const char *e = getenv("TCI_OZAKI_CPLX")) {
+    if (!strcmp(e, "3m") || !strcmp(e, "3M")) c->oz_gauss = 0;
+  }
   {
     cudaError_t e1 = cudaMalloc(&c->dev_scratch, reduce_scratch_bytes());
     cudaError_t e2 = cudaMallocHost(&c->host_scratch, 2 * kMaxMIOut * sizeof(double) + 64);
@@ -366,6 +371,15 @@ tci_status_t tci_set_ozaki_guard(tci_ctx_t ctx, double tol) {
   CHECK(check_ctx(ctx));
   if (!(tol == tol)) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "tolerance is NaN");
   ctx->oz_tol = tol > 0.0 ? tol : 0.0;
+  return TCI_OK;
+}
+
+tci_status_t tci_set_ozaki_complex(tci_ctx_t ctx, int variant) {
+  CHECK(check_ctx(ctx));
+  if (variant != TCI_OZAKI_CPLX_GAUSS && variant != TCI_OZAKI_CPLX_3M)
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "unknown Ozaki complex variant %d", variant);
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  ctx->oz_gauss = variant == TCI_OZAKI_CPLX_GAUSS ? 1 : 0;
   return TCI_OK;
 }
 
@@ -1226,9 +1240,25 @@ ag_fn nccl_allgather_ptr() { return g_nccl.allgather; }
 extern "C" int tci_ozaki_params(int64_t K, int *nmod, int *t, int *moduli) {
   const int *m = nullptr;
   int n = 0;
-  tci::ozaki_params(K, &n, t, &m);
+  tci::ozaki_params(K, 0, &n, t, &m, nullptr);
   if (nmod) *nmod = n;
   if (moduli)
     for (int i = 0; i < n; i++) moduli[i] = m[i];
+  return (K >= 1 && K <= tci::kOzakiMaxK) ? 0 : (int)TCI_ERR_OUT_OF_RANGE;
+}
+
+extern "C" int tci_ozaki_params_complex(int64_t K, int variant, int *nmod, int *t, int *moduli, int *roots,
+                                        int *planes_per_mod) {
+  if (variant != TCI_OZAKI_CPLX_GAUSS && variant != TCI_OZAKI_CPLX_3M) return (int)TCI_ERR_INVALID_ARGUMENT;
+  const bool g = variant == TCI_OZAKI_CPLX_GAUSS;
+  const int *m = nullptr, *r = nullptr;
+  int n = 0;
+  tci::ozaki_params(K, g ? 2 : 1, &n, t, &m, &r);
+  if (nmod) *nmod = n;
+  if (planes_per_mod) *planes_per_mod = g ? 2 : 3;
+  for (int i = 0; i < n; i++) {
+    if (moduli) moduli[i] = m[i];
+    if (roots) roots[i] = r ? r[i] : 0;
+  }
   return (K >= 1 && K <= tci::kOzakiMaxK) ? 0 : (int)TCI_ERR_OUT_OF_RANGE;
 }

@@ -127,22 +127,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-__constant__ int c_i8_moduli[16] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193, 1};
-
-// x mod m in [0, m) for |x| < 2^31 and odd 128 < m < 256: split
+// x mod m in [0, m) for |x| < 2^31 and odd 64 < m < 256: split
 // x = hi 2^16 + lo, y = hi (2^16 mod m) + lo + m 2^16 in [0, 2^25), then
-// q = floor(y / m) = umulhi(y, ceil(2^39 / m)) >> 7 exactly (y < 2^39 / m)
+// q = floor(y / m) = umulhi(y, ceil(2^(32+sh) / m)) >> sh with
+// sh = floor(log2 m) (the magic fits 32 bits; its excess e < m over
+// 2^(32+sh) / m shifts y/m by y e / (m 2^(32+sh)) < 1/m: exact for y < 2^(32+sh) / m)
 struct ModM {
-  int m, c16;
+  int m, c16, sh;
   uint32_t magic;
   __device__ __forceinline__ void set(int mod) {
     m = mod;
     c16 = 65536 % mod;
-    magic = (uint32_t)(((1ull << 39) + (uint64_t)mod - 1) / (uint64_t)mod);
+    sh = 31 - __clz(mod);
+    magic = (uint32_t)(((1ull << (32 + sh)) + (uint64_t)mod - 1) / (uint64_t)mod);
   }
   __device__ __forceinline__ uint32_t operator()(int x) const {
     const uint32_t y = (uint32_t)((x >> 16) * c16 + (x & 0xffff) + (m << 16));
-    const uint32_t q = __umulhi(y, magic) >> 7;
+    const uint32_t q = __umulhi(y, magic) >> sh;
     return y - q * (uint32_t)m;
   }
 };
@@ -158,6 +159,7 @@ struct Params {
   int a_resident;          // raster: 1 = M tiles fastest (A panels stay in L2), 0 = N tiles fastest
   int res_block;           // resident panels per block of the raster
   int hintA, hintB;        // L2 eviction priority of the A / B loads (0 normal, 1 first, 2 last)
+  int mods[16];            // modulus of planes [l * per_mod, (l + 1) * per_mod)
 };
 
 // tile index -> (plane, M tile, N tile), planes outermost. Inside a plane one
@@ -369,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(p, t, b, tm, tn);
       const int mi = b / p.per_mod;
       if (mi != cur_mod) {
-        mod.set(c_i8_moduli[mi]);
+        mod.set(p.mods[mi]);
         cur_mod = mi;
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -479,11 +481,15 @@ bool make_map_d(CUtensorMap *m, void *base, int64_t M, int64_t N, int L) {
 // B [L][N][Kp] int8 (Kp a multiple of 64, N a multiple of 16), D [L][M][N]
 // uint8; counter: one device int of scratch (the dynamic tile counter)
 cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t M, int64_t N, int64_t Kp, int L,
-                          int per_mod, int *counter, cudaStream_t s, int64_t *launches) {
+                          int per_mod, const int *moduli, int nmod, int *counter, cudaStream_t s,
+                          int64_t *launches) {
   using namespace i8g;
   if (M <= 0 || N <= 0 || L <= 0) return cudaSuccess;
   if (Kp % 64 || N % 16 || (uintptr_t)A % 16 || (uintptr_t)B % 16 || (uintptr_t)D % 16 || !counter)
     return cudaErrorInvalidValue;
+  if (!moduli || per_mod < 1 || nmod < 1 || nmod > 16 || (int64_t)per_mod * nmod < L) return cudaErrorInvalidValue;
+  for (int l = 0; l < nmod; l++)
+    if (moduli[l] <= 64 || moduli[l] >= 256 || !(moduli[l] & 1)) return cudaErrorInvalidValue;
   CUtensorMap ma, mb, md;
   if (!make_map(&ma, A, M, Kp, L, kBM) || !make_map(&mb, B, N, Kp, L, kBN / 2) || !make_map_d(&md, D, M, N, L))
     return cudaErrorNotSupported;
@@ -493,6 +499,7 @@ cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t 
   p.Kp = Kp;
   p.L = L;
   p.per_mod = per_mod;
+  for (int l = 0; l < 16; l++) p.mods[l] = l < nmod ? moduli[l] : 1;
   p.tiles_m = (int)((M + 255) / 256);
   p.tiles_n = (int)((N + kBN - 1) / kBN);
   p.tiles = (int64_t)L * p.tiles_m * p.tiles_n;

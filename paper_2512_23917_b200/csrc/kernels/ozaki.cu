@@ -34,6 +34,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "../tci_internal.h"
 #include "common.cuh"
@@ -44,6 +45,23 @@ namespace {
 constexpr int kMaxMod = 15;
 constexpr int kModuli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
 __constant__ int c_moduli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+
+// Gaussian moduli of the complex path (R33): odd, pairwise
+// coprime, every prime factor = 1 mod 4 (221 = 13 17, 205 = 5 41), so -1 has
+// a square root j_l mod m_l (kGRoots: the balanced one, j^2 = -1 mod m) and
+// a + ib -> (a + j b, a - j b) mod m is a ring homomorphism Z[i] -> Z_m x Z_m:
+// a complex product mod m costs two real products instead of three (3M).
+constexpr int kMaxGMod = 16;
+constexpr int kGModuli[kMaxGMod] = {241, 233, 229, 221, 205, 197, 193, 181, 173, 157, 149, 137, 113, 109, 101, 97};
+constexpr int kGRoots[kMaxGMod] = {64, 89, 107, 21, 32, 14, 81, 19, 80, 28, 44, 37, 15, 33, 10, 22};
+__constant__ int c_gmod[kMaxGMod] = {241, 233, 229, 221, 205, 197, 193, 181, 173, 157, 149, 137, 113, 109, 101, 97};
+__constant__ int c_groot[kMaxGMod] = {64, 89, 107, 21, 32, 14, 81, 19, 80, 28, 44, 37, 15, 33, 10, 22};
+__constant__ double c_gminv[kMaxGMod] = {1.0 / 241, 1.0 / 233, 1.0 / 229, 1.0 / 221, 1.0 / 205, 1.0 / 197,
+                                         1.0 / 193, 1.0 / 181, 1.0 / 173, 1.0 / 157, 1.0 / 149, 1.0 / 137,
+                                         1.0 / 113, 1.0 / 109, 1.0 / 101, 1.0 / 97};
+__constant__ float c_gminvf[kMaxGMod] = {1.0f / 241, 1.0f / 233, 1.0f / 229, 1.0f / 221, 1.0f / 205, 1.0f / 197,
+                                         1.0f / 193, 1.0f / 181, 1.0f / 173, 1.0f / 157, 1.0f / 149, 1.0f / 137,
+                                         1.0f / 113, 1.0f / 109, 1.0f / 101, 1.0f / 97};
 
 // ---------------------------------------------------------------------------
 // Small helpers: exact powers of two, exponent / mantissa split
@@ -348,6 +366,57 @@ __device__ __forceinline__ void residue_words(const ResVals<NV> &v, int l, uint3
                       bal_res(v.x[c][q * 4 + 3], v.lo[c][q * 4 + 3], minv, mi));
 }
 
+// balanced residue of a small integer |u| < 2^22 modulo odd m < 256: the
+// quotient rint(u/m) sits in the low mantissa bits of fma(u, 1/m, 1.5 2^23)
+// (|u/m - rint(u/m)| >= 1/(2m) > the fp32 error |u| 2^-24 / m)
+__device__ __forceinline__ int small_bal(int u, float minvf, int m) {
+  const float q = fmaf((float)u, minvf, 12582912.0f);
+  return u - (__float_as_int(q) - 0x4B400000) * m;
+}
+
+// the two Gaussian residue planes (a + j b, a - j b) mod m_l of NV
+// consecutive values (x[0] = re, x[1] = im), balanced, packed 4 bytes per word
+template <int NV>
+__device__ __forceinline__ void residue_words_g(const ResVals<NV> &v, int l, uint32_t (&w)[2][NV / 4]) {
+  const int mi = c_gmod[l], jr = c_groot[l];
+  const double minv = c_gminv[l];
+  const float minvf = c_gminvf[l];
+  int u[NV], d[NV];
+#pragma unroll
+  for (int j = 0; j < NV; j++) {
+    const int rr = bal_res(v.x[0][j], v.lo[0][j], minv, mi);
+    const int ri = bal_res(v.x[1][j], v.lo[1][j], minv, mi);
+    const int tj = jr * ri;   // |.| <= 120 * 120
+    u[j] = small_bal(rr + tj, minvf, mi);
+    d[j] = small_bal(rr - tj, minvf, mi);
+  }
+#pragma unroll
+  for (int q = 0; q < NV / 4; q++) {
+    w[0][q] = pack4(u[q * 4 + 0], u[q * 4 + 1], u[q * 4 + 2], u[q * 4 + 3]);
+    w[1][q] = pack4(d[q * 4 + 0], d[q * 4 + 1], d[q * 4 + 2], d[q * 4 + 3]);
+  }
+}
+
+// the residue planes of one modulus (3M: re, im, re + im; Gaussian: a + jb,
+// a - jb) stored at dst + (l * PPM + c) * plane_stride, 8 bytes per plane
+template <bool G, int NV>
+__device__ __forceinline__ void store_planes(const ResVals<NV> &x, int l, int8_t *dst, int64_t plane_stride) {
+  static_assert(NV == 8, "8 values per thread");
+  if constexpr (G) {
+    uint32_t w[2][NV / 4];
+    residue_words_g<NV>(x, l, w);
+#pragma unroll
+    for (int comp = 0; comp < 2; comp++)
+      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 2 + comp) * plane_stride) = make_uint2(w[comp][0], w[comp][1]);
+  } else {
+    uint32_t w[3][NV / 4];
+    residue_words<NV>(x, l, w);
+#pragma unroll
+    for (int comp = 0; comp < 3; comp++)
+      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 3 + comp) * plane_stride) = make_uint2(w[comp][0], w[comp][1]);
+  }
+}
+
 // scale factors 2^sc = s2a * s2b of one line (E > -100000)
 __device__ __forceinline__ void line_scale(int t, int E, double &s2a, double &s2b) {
   const int sc = t - E, h1 = sc / 2;
@@ -385,6 +454,7 @@ __device__ __forceinline__ void elem_scales(const ResArgs &a, int E, int64_t k0,
   for (int j = 0; j < 8; j++) scale_pair(a.t - E + a.sgn * s[j], fa[j], fb[j]);
 }
 
+template <bool G>
 __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs a) {
   constexpr int NV = 8;
   const int64_t kgroups = a.Kp / NV;
@@ -416,18 +486,13 @@ __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs 
     for (int j = 0; j < NV; j++) x.set(j, kMagic, kMagic);
   }
   int8_t *dst = a.out + row * a.Kp + k0;
-  for (int l = 0; l < a.nmod; l++) {
-    uint32_t w[3][NV / 4];
-    residue_words<NV>(x, l, w);
-#pragma unroll
-    for (int comp = 0; comp < 3; comp++)
-      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 3 + comp) * a.plane_stride) = make_uint2(w[comp][0], w[comp][1]);
-  }
+  for (int l = 0; l < a.nmod; l++) store_planes<G, NV>(x, l, dst, a.plane_stride);
 }
 
 // line-contiguous source (s_l == 1): a 32-line x 64-k tile is read along the
 // lines (coalesced), turned into integers in shared memory and written along
 // k: eight threads write one line's 64 contiguous residue bytes per plane.
+template <bool G>
 __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArgs a) {
   __shared__ double sx[2][32][65];
   const int64_t ntk = a.Kp / 64;
@@ -466,13 +531,7 @@ __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArg
 #pragma unroll
   for (int j = 0; j < 8; j++) x.set(j, sx[0][li][kq + j], sx[1][li][kq + j]);
   int8_t *dst = a.out + row * a.Kp + kb + kq;
-  for (int l = 0; l < a.nmod; l++) {
-    uint32_t w[3][2];
-    residue_words<8>(x, l, w);
-#pragma unroll
-    for (int comp = 0; comp < 3; comp++)
-      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 3 + comp) * a.plane_stride) = make_uint2(w[comp][0], w[comp][1]);
-  }
+  for (int l = 0; l < a.nmod; l++) store_planes<G, 8>(x, l, dst, a.plane_stride);
 }
 
 // ---------------------------------------------------------------------------
@@ -494,7 +553,8 @@ struct CrtArgs {
   const uint8_t *D;         // [3n][Mc][Np], residues in [0, m)
   int64_t Mc, N, Np, m0;    // chunk rows, columns, padded columns, first row
   int nmod;
-  double W[kMaxMod][4];     // CRT weight chunks (exact integers, 37 bits each)
+  double W[kMaxGMod][4];    // CRT weight chunks (exact integers, 37 bits each; Gaussian: 40 bits, Re weights)
+  double WI[kMaxGMod][3];   // Gaussian: Im weights (40-bit chunks)
   double Mch[4];            // M chunks
   double Minv;              // ~1 / M
   const int *EA, *EB;       // exponents
@@ -507,9 +567,9 @@ struct CrtArgs {
   const int *eb_max;        // device: max_n E_n
 };
 
-template <int NCH>
+template <int NCH, int CB = 37>
 __device__ __forceinline__ double crt_value(const double (&S)[NCH], const double (&Mch)[4], double Minv) {
-  const double two37 = 137438953472.0, inv37 = 1.0 / 137438953472.0;
+  const double two37 = (double)(1ull << CB), inv37 = 1.0 / (double)(1ull << CB);   // chunk base 2^CB
   double xe = S[NCH - 1];
 #pragma unroll
   for (int j = NCH - 2; j >= 0; j--) xe = fma(xe, two37, S[j]);
@@ -548,22 +608,31 @@ __device__ __forceinline__ double block_sum_fixed(double v, double *red) {
 // memory by cp.async.bulk (TMA) into a STAGES-deep ring completed on
 // mbarriers, so later tiles' bytes are in flight while this one is reduced;
 // each thread reconstructs CPT consecutive columns.
-template <int CPT, int THREADS, int STAGES>
+template <int CPT, int THREADS, int STAGES, int PPM = 3>
 struct CrtShape {
   static constexpr int kTW = CPT * THREADS;
-  static constexpr size_t smem(int nmod) { return (size_t)STAGES * 3 * nmod * kTW + 8 * STAGES; }
+  static constexpr size_t smem(int nmod) { return (size_t)STAGES * PPM * nmod * kTW + 8 * STAGES; }
 };
 
 // NCH = 3 chunks while sum_l 3 m_l w_lj stays below 2^53 (nmod <= 14: top
 // chunk < 2^36, sums < 2^50); 4 chunks for nmod = 15 (M > 2^117).
-template <int NMOD, int NCH, int CPT, int THREADS, int STAGES>
+//
+// Gaussian variant (G, R33): two planes per modulus hold c+ = phi+(C') and
+// c- = phi-(C') in [0, m); Re C' = (c+ + c-) / 2 and Im C' = (c+ - c-) / (2j)
+// mod m. The inverses are folded into the CRT weights (WR_l = 2^-1 w_l,
+// WI_l = (2j)^-1 w_l mod M), applied to the representatives c+ + c- in
+// [0, 2m) and c+ - c- + m in (0, 2m); 40-bit chunks keep every chunk sum
+// exact (16 * 482 * 2^40 < 2^53) with 3 chunks for up to 16 moduli.
+template <int NMOD, int NCH, int CPT, int THREADS, int STAGES, bool G = false>
 __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ CrtArgs a) {
   static_assert(CPT == 2 || CPT == 4, "columns per thread");
-  using Shape = CrtShape<CPT, THREADS, STAGES>;
+  constexpr int PPM = G ? 2 : 3;       // planes per modulus
+  constexpr int CB = G ? 40 : 37;      // CRT chunk bits
+  using Shape = CrtShape<CPT, THREADS, STAGES, PPM>;
   constexpr int TW = Shape::kTW;
   extern __shared__ __align__(128) uint8_t crt_smem[];
   __shared__ double red[2][THREADS / 32];
-  constexpr int kStage = 3 * NMOD * TW;
+  constexpr int kStage = PPM * NMOD * TW;
   uint64_t *bar = reinterpret_cast<uint64_t *>(crt_smem + STAGES * kStage);
   const int64_t tpr = (a.Np + TW - 1) / TW;   // tiles per row
   const int64_t ntiles = a.Mc * tpr;
@@ -576,10 +645,10 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
     const uint32_t w = (uint32_t)(a.Np - c0 < TW ? a.Np - c0 : TW);   // multiple of 16
     if (tid == 0) {
       fence_proxy_async_smem();
-      mbar_expect_tx(&bar[s], 3 * NMOD * w);
+      mbar_expect_tx(&bar[s], PPM * NMOD * w);
     }
     __syncwarp();
-    for (int q = tid; q < 3 * NMOD; q += 32)
+    for (int q = tid; q < PPM * NMOD; q += 32)
       bulk_g2s(crt_smem + s * kStage + q * TW, a.D + q * plane + r * a.Np + c0, w, &bar[s]);
   };
 
@@ -607,6 +676,36 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
         for (int j = 0; j < NCH; j++) Sr[e][j] = Si[e][j] = 0.0;
 #pragma unroll
       for (int i = 0; i < NMOD; i++) {
+        if constexpr (G) {
+          uint32_t P, Q;
+          if constexpr (CPT == 4) {
+            P = *reinterpret_cast<const uint32_t *>(st + (2 * i + 0) * TW);
+            Q = *reinterpret_cast<const uint32_t *>(st + (2 * i + 1) * TW);
+          } else {
+            P = *reinterpret_cast<const uint16_t *>(st + (2 * i + 0) * TW);
+            Q = *reinterpret_cast<const uint16_t *>(st + (2 * i + 1) * TW);
+          }
+          const uint32_t m2 = (uint32_t)c_gmod[i] * 0x10001u;
+#pragma unroll
+          for (int half = 0; half < CPT / 2; half++) {
+            const uint32_t sel = half ? 0x4342u : 0x4140u;
+            const uint32_t p2 = __byte_perm(P, 0, sel), q2 = __byte_perm(Q, 0, sel);
+            const uint32_t xr2 = p2 + q2;          // [0, 2m) per 16-bit lane
+            const uint32_t xi2 = p2 + m2 - q2;     // (0, 2m)
+#pragma unroll
+            for (int lane = 0; lane < 2; lane++) {
+              const int e = half * 2 + lane;
+              const double dr = (double)(lane ? xr2 >> 16 : xr2 & 0xffffu);
+              const double di = (double)(lane ? xi2 >> 16 : xi2 & 0xffffu);
+#pragma unroll
+              for (int j = 0; j < NCH; j++) {
+                Sr[e][j] = fma(dr, a.W[i][j], Sr[e][j]);
+                Si[e][j] = fma(di, a.WI[i][j], Si[e][j]);
+              }
+            }
+          }
+          continue;
+        }
         uint32_t P, Q, S;
         if constexpr (CPT == 4) {
           P = *reinterpret_cast<const uint32_t *>(st + (3 * i + 0) * TW);
@@ -650,7 +749,8 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
         const int eb = a.EB[n];
         double2 out = make_double2(0.0, 0.0);
         if (ea > -100000 && eb > -100000) {
-          const double xr = crt_value(Sr[e], a.Mch, a.Minv), xi = crt_value(Si[e], a.Mch, a.Minv);
+          const double xr = crt_value<NCH, CB>(Sr[e], a.Mch, a.Minv);
+          const double xi = crt_value<NCH, CB>(Si[e], a.Mch, a.Minv);
           const int sc = sc0 + eb;
           if (sc >= -1022 && sc <= 1023) {   // 2^sc is a normal double: one exact multiply
             const double f = __hiloint2double((sc + 1023) << 20, 0);
@@ -687,10 +787,10 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
   }
 }
 
-template <int NMOD, int NCH, int CPT, int THREADS, int STAGES>
+template <int NMOD, int NCH, int CPT, int THREADS, int STAGES, bool G = false>
 cudaError_t launch_crt_cfg(const CrtArgs &c, int64_t mc, cudaStream_t s) {
-  using Shape = CrtShape<CPT, THREADS, STAGES>;
-  auto kern = crt_kernel<NMOD, NCH, CPT, THREADS, STAGES>;
+  using Shape = CrtShape<CPT, THREADS, STAGES, G ? 2 : 3>;
+  auto kern = crt_kernel<NMOD, NCH, CPT, THREADS, STAGES, G>;
   const size_t smem = Shape::smem(NMOD);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -708,9 +808,9 @@ cudaError_t launch_crt_cfg(const CrtArgs &c, int64_t mc, cudaStream_t s) {
 constexpr int kCrtTW = 1024;   // CRT tile width (columns): 4 per thread x 256 threads
 // 4 columns x 256 threads x 2 stages: measured best of {2,4} x {128,256} x
 // {2,3,4} on the target shapes (the kernel is XU/FP64-issue bound there).
-template <int NMOD, int NCH>
+template <int NMOD, int NCH, bool G = false>
 cudaError_t launch_crt(const CrtArgs &c, int64_t mc, cudaStream_t s) {
-  return launch_crt_cfg<NMOD, NCH, 4, 256, 2>(c, mc, s);
+  return launch_crt_cfg<NMOD, NCH, 4, 256, 2, G>(c, mc, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1008,8 +1108,11 @@ __global__ void __launch_bounds__(256) copy_to_peers_if(const double2 *C, int64_
 // ---------------------------------------------------------------------------
 // host planning
 // ---------------------------------------------------------------------------
+// moduli sets: 3M complex and real (kModuli), Gaussian complex (kGModuli)
+enum OzKind { kOzReal = 0, kOz3M = 1, kOzGauss = 2 };
+
 struct OzPlan {
-  int nmod, t;
+  int kind, nmod, t, ppm;   // ppm: residue planes per modulus (1 real, 3 3M, 2 Gaussian)
   int64_t Kp, Np, Mc, chunks, tpr, nch;
   size_t off_EA, off_EB, off_Bres, off_Ares, off_D;
   size_t off_KA, off_KB, off_SK, off_KSA, off_KSB, off_slotE, off_slotS, off_rowsq, off_misc;
@@ -1019,20 +1122,26 @@ struct OzPlan {
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 size_t align_up(size_t x) { return (x + 255) / 256 * 256; }
 
-OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_rows = 0) {
+// exactness (R26/R33): |C'| <= 2 K 2^(2t) <= M/4, i.e. 2t + 3 + log2 K <= log2 M;
+// the fewest moduli that allow t >= 46, then the largest such t
+OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_rows = 0, int kind = kOz3M) {
   OzPlan p{};
+  p.kind = kind;
+  p.ppm = kind == kOzReal ? 1 : kind == kOz3M ? 3 : 2;
+  const int *mods = kind == kOzGauss ? kGModuli : kModuli;
+  const int nmax = kind == kOzGauss ? kMaxGMod : kMaxMod;
   const double lk = std::log2((double)std::max<int64_t>(K, 1));
   double lm = 0;
   p.nmod = 0;
-  for (int l = 0; l < kMaxMod; l++) {
-    lm += std::log2((double)kModuli[l]);
+  for (int l = 0; l < nmax; l++) {
+    lm += std::log2((double)mods[l]);
     p.nmod = l + 1;
     if (std::floor((lm - 3.0 - lk) / 2.0) >= 46) break;
   }
   p.t = (int)std::floor((lm - 3.0 - lk) / 2.0);
   p.Kp = round_up(K, 64);
   p.Np = round_up(N, 16);
-  const int64_t planes = 3 * p.nmod;
+  const int64_t planes = p.ppm * p.nmod;
   // rows per chunk: uint8 residue outputs + A residues within budget_D, multiple of 256
   int64_t mc = (int64_t)(budget_D / ((size_t)planes * (p.Np + p.Kp)));
   mc = std::max<int64_t>(256, mc / 256 * 256);
@@ -1096,6 +1205,35 @@ void crt_constants(int nmod, double (&W)[kMaxMod][4], double (&Mch)[4], double &
   Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
 }
 
+// Gaussian set (R33): WR_l = (2^-1 mod m_l) w_l mod M and WI_l = ((2 j_l)^-1
+// mod m_l) w_l mod M in 40-bit chunks (3 chunks: M < 2^118), M chunks, ~1/M
+void crt_constants_gauss(int nmod, double (&WR)[kMaxGMod][4], double (&WI)[kMaxGMod][3], double (&Mch)[4],
+                         double &Minv) {
+  u128 Mp = 1;
+  for (int l = 0; l < nmod; l++) Mp *= (u128)kGModuli[l];
+  const u128 mask = ((u128)1 << 40) - 1;
+  for (int l = 0; l < kMaxGMod; l++)
+    for (int j = 0; j < 4; j++) {
+      WR[l][j] = 0.0;
+      if (j < 3) WI[l][j] = 0.0;
+    }
+  for (int l = 0; l < nmod; l++) {
+    const unsigned ml = (unsigned)kGModuli[l];
+    const u128 Ml = Mp / ml;
+    const u128 wl = mulmod_small(Ml, inv_mod((unsigned)(Ml % ml), ml), Mp);
+    const unsigned h = inv_mod(2u, ml);
+    const unsigned jl = (unsigned)((kGRoots[l] % (int)ml + (int)ml) % (int)ml);
+    const unsigned g = inv_mod((2u * jl) % ml, ml);
+    const u128 wr = mulmod_small(wl, h, Mp), wi = mulmod_small(wl, g, Mp);
+    for (int j = 0; j < 3; j++) {
+      WR[l][j] = (double)(uint64_t)((wr >> (40 * j)) & mask);
+      WI[l][j] = (double)(uint64_t)((wi >> (40 * j)) & mask);
+    }
+  }
+  for (int j = 0; j < 4; j++) Mch[j] = j < 3 ? (double)(uint64_t)((Mp >> (40 * j)) & mask) : 0.0;
+  Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
+}
+
 // one batched INT8 GEMM: D[b][m][n] = (sum_k A[b][m][k] B[b][n][k]) mod m_b
 // (i8gemm.cu: hand-written tcgen05 kind::i8, TMA, TMEM)
 cudaError_t int8_gemm(const GemmProblem &g, const OzPlan &p, const int8_t *Ares, const int8_t *Bres, uint8_t *D,
@@ -1107,7 +1245,8 @@ cudaError_t int8_gemm(const GemmProblem &g, const OzPlan &p, const int8_t *Ares,
     cudaEventCreate(&pf->b[pf->n]);
     cudaEventRecord(pf->a[pf->n], s);
   }
-  cudaError_t e = launch_i8gemm(Ares, Bres, D, mc, p.Np, p.Kp, planes, per_mod, counter, s, launches);
+  cudaError_t e = launch_i8gemm(Ares, Bres, D, mc, p.Np, p.Kp, planes, per_mod,
+                                p.kind == kOzGauss ? kGModuli : kModuli, p.nmod, counter, s, launches);
   if (e != cudaSuccess) return e;
   if (rec) {
     cudaEventRecord(pf->b[pf->n], s);
@@ -1259,15 +1398,19 @@ cudaError_t ozaki_preload() {
   return cudaSuccess;
 }
 
-void ozaki_params(int64_t K, int *nmod, int *t, const int **moduli) {
-  const OzPlan p = oz_plan(1, 1, K, (size_t)8 << 30);
+void ozaki_params(int64_t K, int kind, int *nmod, int *t, const int **moduli, const int **roots) {
+  const OzPlan p = oz_plan(1, 1, K, (size_t)8 << 30, 0, kind);
   if (nmod) *nmod = p.nmod;
   if (t) *t = p.t;
-  if (moduli) *moduli = kModuli;
+  if (moduli) *moduli = kind == kOzGauss ? kGModuli : kModuli;
+  if (roots) *roots = kind == kOzGauss ? kGRoots : nullptr;
 }
 
 size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K) {
-  return oz_plan(M, N, K, (size_t)8 << 30).total;
+  // sized for the largest plane count of any kind (3M) so the kind can change
+  // without re-sizing
+  return std::max(oz_plan(M, N, K, (size_t)8 << 30, 0, kOz3M).total,
+                  oz_plan(M, N, K, (size_t)8 << 30, 0, kOzGauss).total);
 }
 
 // C = A B (complex128) per GemmProblem strides, by Ozaki-II on INT8 tcgen05.
@@ -1275,21 +1418,28 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
                                int64_t *launches) {
   if (g.M == 0 || g.N == 0) return cudaSuccess;
   if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;   // int32 residue products would overflow
-  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows);
+  const bool gauss = g.oz_gauss != 0;
+  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows, gauss ? kOzGauss : kOz3M);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
   OzRun<double2> R(g, p, ws, s, launches);
   char *w = R.w;
   int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
   uint8_t *D = reinterpret_cast<uint8_t *>(w + p.off_D);
   R.prologue();
-  const int planes = 3 * p.nmod;
+  const int planes = p.ppm * p.nmod;
   auto launch_res = [&](const ResArgs &r) {
     if (r.s_k == 1) {
-      const int64_t th = r.lines_out * (r.Kp / 8);
-      residues<<<(unsigned)((th + 255) / 256), 256, 0, s>>>(r);
+      const unsigned blocks = (unsigned)((r.lines_out * (r.Kp / 8) + 255) / 256);
+      if (gauss)
+        residues<true><<<blocks, 256, 0, s>>>(r);
+      else
+        residues<false><<<blocks, 256, 0, s>>>(r);
     } else {
-      const int64_t blocks = ((r.lines_out + 31) / 32) * (r.Kp / 64);
-      residues_t<<<(unsigned)blocks, 256, 0, s>>>(r);
+      const unsigned blocks = (unsigned)(((r.lines_out + 31) / 32) * (r.Kp / 64));
+      if (gauss)
+        residues_t<true><<<blocks, 256, 0, s>>>(r);
+      else
+        residues_t<false><<<blocks, 256, 0, s>>>(r);
     }
     R.count();
   };
@@ -1299,7 +1449,14 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
     launch_res(r);
   }
   CrtArgs c{};
-  crt_constants(p.nmod, c.W, c.Mch, c.Minv);
+  if (gauss) {
+    crt_constants_gauss(p.nmod, c.W, c.WI, c.Mch, c.Minv);
+  } else {
+    double W[kMaxMod][4];
+    crt_constants(p.nmod, W, c.Mch, c.Minv);
+    for (int l = 0; l < kMaxMod; l++)
+      for (int j = 0; j < 4; j++) c.W[l][j] = W[l][j];
+  }
   c.nmod = p.nmod; c.EA = R.EA; c.EB = R.EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
   c.C = static_cast<double2 *>(g.C); c.c_sm = g.c_sm;
   c.npeer = std::min(g.npeer, 7);
@@ -1317,17 +1474,25 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
       R.res_args(r, true, m0, mc, Ares, mc * p.Kp);
       launch_res(r);
     }
-    cudaError_t ge = int8_gemm(g, p, Ares, Bres, D, mc, planes, 3, R.misc + 3, s, launches);
+    cudaError_t ge = int8_gemm(g, p, Ares, Bres, D, mc, planes, p.ppm, R.misc + 3, s, launches);
     if (ge != cudaSuccess) return ge;
     c.Mc = mc;
     c.m0 = m0;
     cudaError_t ce;
-    switch (p.nmod) {
-      case 12: ce = launch_crt<12, 3>(c, mc, s); break;
-      case 13: ce = launch_crt<13, 3>(c, mc, s); break;
-      case 14: ce = launch_crt<14, 3>(c, mc, s); break;
-      case 15: ce = launch_crt<15, 4>(c, mc, s); break;
-      default: return cudaErrorInvalidValue;
+    if (gauss) {
+      switch (p.nmod) {
+        case 15: ce = launch_crt<15, 3, true>(c, mc, s); break;
+        case 16: ce = launch_crt<16, 3, true>(c, mc, s); break;
+        default: return cudaErrorInvalidValue;
+      }
+    } else {
+      switch (p.nmod) {
+        case 12: ce = launch_crt<12, 3>(c, mc, s); break;
+        case 13: ce = launch_crt<13, 3>(c, mc, s); break;
+        case 14: ce = launch_crt<14, 3>(c, mc, s); break;
+        case 15: ce = launch_crt<15, 4>(c, mc, s); break;
+        default: return cudaErrorInvalidValue;
+      }
     }
     if (ce != cudaSuccess) return ce;
     R.count();
@@ -1343,7 +1508,7 @@ cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   if (g.M == 0 || g.N == 0) return cudaSuccess;
   if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;
   if (g.rows_needed) return cudaErrorInvalidValue;   // the real path takes all row exponents up front
-  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows);
+  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows, kOzReal);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
   OzRun<double> R(g, p, ws, s, launches);
   char *w = R.w;

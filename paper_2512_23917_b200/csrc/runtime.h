@@ -49,6 +49,7 @@ struct tci_ctx_s {
   // Frobenius error (<= 0: off) and device-resident statistics
   double oz_tol;
   tci::OzGuard *oz_guard;
+  int oz_gauss;         // complex Ozaki variant: 1 Gaussian moduli (R33), 0 3M
   int svd_last_sweeps;  // Jacobi sweeps of the last svd / trunc_svd (tci_svd_info)
   double svd_last_off;  // its final off-diagonal measure
 };

@@ -50,6 +50,9 @@ struct GemmProblem {
   double oz_tol = 0.0;
   struct OzGuard *oz_guard = nullptr;
   int oz_balance = 1;
+  // complex Ozaki GEMMs: Gaussian moduli, two planes per modulus (1, R33) or
+  // the 3M split, three planes per modulus (0)
+  int oz_gauss = 1;
   // DMMA kernels: when set, every CTA returns at once unless *run_if != 0
   const int *run_if = nullptr;
   // deterministic split-K (few output tiles, long K): split z of `splitk`
@@ -126,12 +129,17 @@ inline bool ozaki_worthwhile(int64_t M, int64_t N, int64_t K) {
 }
 // The residue products of one Ozaki GEMM in one launch (i8gemm.cu, tcgen05
 // kind::i8): D[b] = (A[b] B[b]^T) mod m_(b / per_mod) over L planes,
-// A [L][M][Kp], B [L][N][Kp] int8 K-major, D [L][M][N] uint8; counter: one
-// device int of scratch (dynamic tile schedule)
+// A [L][M][Kp], B [L][N][Kp] int8 K-major, D [L][M][N] uint8; moduli[nmod]
+// (odd, 64 < m < 256, L <= per_mod * nmod); counter: one device int of
+// scratch (dynamic tile schedule)
 cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t M, int64_t N, int64_t Kp, int L,
-                          int per_mod, int *counter, cudaStream_t s, int64_t *launches);
-// moduli count and integer bit budget chosen for a contraction length K
-void ozaki_params(int64_t K, int *nmod, int *t, const int **moduli);
+                          int per_mod, const int *moduli, int nmod, int *counter, cudaStream_t s,
+                          int64_t *launches);
+// moduli count and integer bit budget chosen for a contraction length K;
+// kind 0 = float64, 1 = complex 3M, 2 = complex Gaussian (roots j_l with
+// j_l^2 = -1 mod m_l; null for the other kinds)
+void ozaki_params(int64_t K, int kind, int *nmod, int *t, const int **moduli, const int **roots);
+
 
 // Output tile of the GEMM kernel used for `dtype` (for the planner's split-K choice).
 void gemm_tile(tci_dtype_t dtype, int *bm, int *bn);

@@ -688,20 +688,60 @@ def test_ozaki_contract_vs_dmma_and_oracle(ctx, ozctx, oracle_mod, layout):
     assert torch.equal(c_oz, c2)                         # deterministic
 
 
+@pytest.mark.parametrize("variant", [tci.TCI_OZAKI_CPLX_GAUSS, tci.TCI_OZAKI_CPLX_3M])
 @pytest.mark.parametrize("mnk", [(320, 320, 40960), (256, 256, 131072)])
-def test_ozaki_large_k_fifteen_moduli(ozctx, oracle_mod, mnk):
-    """K > 28k needs 15 moduli (M > 2^117): the CRT runs with four 37-bit
-    weight chunks so every chunk sum stays an exact fp64 integer (R27)."""
+def test_ozaki_large_k_moduli_counts(ozctx, oracle_mod, mnk, variant):
+    """Long K needs the largest moduli sets: 3M takes 15 moduli (M > 2^117,
+    four 37-bit CRT weight chunks, R27); the Gaussian set 15 at K = 40960 and
+    16 at K = 131072 (three 40-bit chunks, R33). Both within 1e-12 of the
+    oracle."""
     M, N, K = mnk
-    st, nmod, t, _ = tci.tci_ozaki_params(K)
-    assert st == 0 and nmod == 15 and t >= 46
+    st, nmod, t, _, _, ppm = tci.tci_ozaki_params_complex(K, variant)
+    if variant == tci.TCI_OZAKI_CPLX_3M:
+        assert st == 0 and nmod == 15 and t >= 46 and ppm == 3
+    else:
+        assert st == 0 and nmod == (15 if K < 69000 else 16) and t >= 46 and ppm == 2
     A = synth.random_tensor((M, K), "c128", 493, 1)
     B = synth.random_tensor((K, N), "c128", 493, 2)
-    c = host(ozctx.contract(dev(A), "mk", dev(B), "kn", "mn"))
+    ozctx.set_ozaki_complex(variant)
+    try:
+        c = host(ozctx.contract(dev(A), "mk", dev(B), "kn", "mn"))
+    finally:
+        ozctx.set_ozaki_complex(tci.TCI_OZAKI_CPLX_GAUSS)
     rows = [0, 1, M // 2, M - 1]
     ref = oracle_mod.contract(A.numpy()[rows], "mk", B.numpy(), "kn", "mn")
     assert rel_frob(c[rows], ref) <= 1e-12
     assert ozctx.launch_count() > 0
+
+
+@pytest.mark.parametrize("la", ["mk", "km"])
+def test_ozaki_gaussian_vs_3m_vs_oracle(ozctx, oracle_mod, la):
+    """The two complex variants on the same product (M = 1300, N = 1100,
+    K = 4100: ragged against every tile; both residue kernels): each within
+    1e-12 of the oracle on sampled rows, and of each other everywhere; the
+    Gaussian variant ran 2 INT8 planes per modulus (its INT8 op count is
+    2/3 x 15/14 of the 3M one's)."""
+    M, N, K = 1300, 1100, 4100
+    A = synth.random_tensor((M, K), "c128", 497, 1)
+    B = synth.random_tensor((K, N), "c128", 497, 2)
+    At = A if la == "mk" else A.T.contiguous()
+    outs, ops = {}, {}
+    for v in (tci.TCI_OZAKI_CPLX_GAUSS, tci.TCI_OZAKI_CPLX_3M):
+        ozctx.set_ozaki_complex(v)
+        tci.tci_profile_enable(ozctx.handle, True)
+        outs[v] = ozctx.contract(dev(At), la, dev(B), "kn", "mn")
+        ops[v] = tci.tci_profile_query(ozctx.handle, tci.PROF_I8)["flops"]
+        tci.tci_profile_enable(ozctx.handle, False)
+    ozctx.set_ozaki_complex(tci.TCI_OZAKI_CPLX_GAUSS)
+    _, ng, _, _, _, _ = tci.tci_ozaki_params_complex(K, tci.TCI_OZAKI_CPLX_GAUSS)
+    _, n3, _, _, _, _ = tci.tci_ozaki_params_complex(K, tci.TCI_OZAKI_CPLX_3M)
+    assert abs(ops[0] / ops[1] - (2 * ng) / (3 * n3)) < 1e-9
+    g, m3 = outs[tci.TCI_OZAKI_CPLX_GAUSS], outs[tci.TCI_OZAKI_CPLX_3M]
+    assert ((g - m3).abs().pow(2).sum().sqrt() / m3.abs().pow(2).sum().sqrt()).item() <= 1e-12
+    rows = [0, 1, 647, M - 1]
+    ref = oracle_mod.contract(A.numpy()[rows], "mk", B.numpy(), "kn", "mn")
+    for o in (g, m3):
+        assert rel_frob(host(o)[rows], ref) <= 1e-12
 
 
 def test_ozaki_heff_cfg2(ozctx, oracle_mod):

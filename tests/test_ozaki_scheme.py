@@ -162,3 +162,153 @@ def test_unbalanced_scheme_fails_and_estimate_flags_it(name):
     assert err > 1e-3 and est > 1e-3
     _, _, used = _emulate(A, B, 20, balance=True)
     assert used
+
+
+# ---------------------------------------------------------------------------
+# Gaussian moduli of the complex path (R33): a + ib -> (a + j b,
+# a - j b) mod m is a ring homomorphism when j^2 = -1 (mod m), so a complex
+# product mod m is two real products; the CRT folds 2^-1 and (2j)^-1 into
+# its weights. Emulated here with Python big integers and numpy float64.
+# ---------------------------------------------------------------------------
+
+def _prime_factors(n):
+    f, p = set(), 2
+    while p * p <= n:
+        while n % p == 0:
+            f.add(p)
+            n //= p
+        p += 1
+    if n > 1:
+        f.add(n)
+    return f
+
+
+@pytest.mark.parametrize("K", [1, 64, 1000, 4096, 20480, 24576, 69000, 131072])
+def test_params_complex_gaussian(K):
+    st, n, t, mods, roots, ppm = lib().tci_ozaki_params_complex(K, 0)
+    assert st == 0 and ppm == 2
+    assert all(m % 2 == 1 and 64 < m < 256 for m in mods)
+    assert all(math.gcd(a, b) == 1 for i, a in enumerate(mods) for b in mods[i + 1:])
+    assert all(p % 4 == 1 for m in mods for p in _prime_factors(m))      # sqrt(-1) exists mod m
+    assert all((j * j + 1) % m == 0 and abs(j) <= (m - 1) // 2 for m, j in zip(mods, roots))
+    M = math.prod(mods)
+    assert 2 * K * 2 ** (2 * t) <= M // 4           # |Re C'|, |Im C'| <= 2 K 2^(2t) <= M/4
+    assert K * (max(mods) // 2) ** 2 < 2 ** 31      # balanced int8 residues, exact int32 sums
+    assert t >= 46
+    # 40-bit CRT chunks: 3 cover M, chunk sums of 16 terms < 482 * 2^40 stay exact
+    assert M < 2 ** 120 and 16 * 482 * 2 ** 40 < 2 ** 53
+
+
+def _gauss_crt(xs, mods, weights):
+    """crt_value<3, 40> of the kernel on the representatives xs (numpy float64)."""
+    M = math.prod(mods)
+    mask, cb, nch = (1 << 40) - 1, 40, 3
+    Wc = np.array([[float((w >> (cb * j)) & mask) for j in range(nch)] for w in weights])
+    Mch = np.array([float((M >> (cb * j)) & mask) for j in range(nch)])
+    assert M >> (cb * nch) == 0
+    S = np.zeros(nch)
+    S_int = [0] * nch
+    for c, w in zip(xs, Wc):
+        S = S + float(c) * w
+        S_int = [s + c * int(x) for s, x in zip(S_int, w)]
+    assert [int(s) for s in S] == S_int and max(abs(s) for s in S_int) < 2 ** 53
+    two = float(2 ** cb)
+    xe = S[2] * two * two + S[1] * two + S[0]
+    q = np.rint(xe * (1.0 / float(M)))
+    r = S - q * Mch
+    for j in range(nch - 1):
+        cy = np.rint(r[j] / two)
+        r[j] = r[j] - cy * two
+        r[j + 1] = r[j + 1] + cy
+    return (r[2] * two + r[1]) * two + r[0]
+
+
+def _gauss_weights(mods, roots):
+    M = math.prod(mods)
+    WR, WI = [], []
+    for m, j in zip(mods, roots):
+        Ml = M // m
+        w = (Ml * pow(Ml % m, -1, m)) % M
+        WR.append((w * pow(2, -1, m)) % M)
+        WI.append((w * pow((2 * j) % m, -1, m)) % M)
+    return WR, WI
+
+
+def _bal(x, m):
+    r = x % m
+    return r - m if r > m // 2 else r
+
+
+@pytest.mark.parametrize("K", [64, 4096, 20480])
+def test_gaussian_scheme_exact_complex_product(K):
+    """Integer complex matrices with t-bit entries: balanced Gaussian residues
+    (int8), the two modular products per modulus (the INT8 GEMMs + mod-m
+    epilogue), the kernel's CRT with folded weights: the exact integer
+    complex product, to one ulp of its float64 value."""
+    st, n, t, mods, roots, _ = lib().tci_ozaki_params_complex(K)
+    rng = np.random.default_rng(K + 5)
+    Mr, Nr, Ks = 3, 2, min(K, 48)      # a few output entries; K terms of which Ks random, rest at the bound
+    lim = 2 ** t - 1
+
+    def ent():
+        return int(rng.integers(-lim, lim, endpoint=True)), int(rng.integers(-lim, lim, endpoint=True))
+    A = [[ent() for _ in range(Ks)] for _ in range(Mr)]
+    B = [[ent() for _ in range(Nr)] for _ in range(Ks)]
+    A[0] = [(lim, lim)] * Ks                              # extreme entries
+    B = [[(lim, -lim)] + row[1:] for row in B]
+    WR, WI = _gauss_weights(mods, roots)
+    for i in range(Mr):
+        for jn in range(Nr):
+            cr = sum(A[i][k][0] * B[k][jn][0] - A[i][k][1] * B[k][jn][1] for k in range(Ks))
+            ci = sum(A[i][k][0] * B[k][jn][1] + A[i][k][1] * B[k][jn][0] for k in range(Ks))
+            xr, xi = [], []
+            for m, j in zip(mods, roots):
+                cp = cm = 0
+                for k in range(Ks):
+                    ar, ai = _bal(A[i][k][0], m), _bal(A[i][k][1], m)
+                    br, bi = _bal(B[k][jn][0], m), _bal(B[k][jn][1], m)
+                    up, um = _bal(ar + j * ai, m), _bal(ar - j * ai, m)     # int8 planes of A
+                    vp, vm = _bal(br + j * bi, m), _bal(br - j * bi, m)     # int8 planes of B
+                    assert max(abs(up), abs(um), abs(vp), abs(vm)) <= 127
+                    cp += up * vp
+                    cm += um * vm
+                cp, cm = cp % m, cm % m                                     # GEMM epilogue bytes
+                xr.append(cp + cm)                                          # [0, 2m)
+                xi.append(cp - cm + m)                                      # (0, 2m)
+            gr, gi = _gauss_crt(xr, mods, WR), _gauss_crt(xi, mods, WI)
+            for got, ref in ((gr, cr), (gi, ci)):
+                assert got == float(ref) or abs(got - ref) <= abs(ref) * 2.0 ** -52, (got, ref)
+
+
+@pytest.mark.parametrize("K", [4096, 20480, 131072])
+def test_gaussian_crt_full_range(K):
+    """The reconstruction over the whole guaranteed range |C'| <= 2 K 2^(2t):
+    representatives c+ + c- and c+ - c- + m of random and extreme values."""
+    st, n, t, mods, roots, _ = lib().tci_ozaki_params_complex(K)
+    WR, WI = _gauss_weights(mods, roots)
+    bound = 2 * K * 2 ** (2 * t)
+    rng = np.random.default_rng(K)
+    vals = [(0, 0), (bound, -bound), (-bound, bound), (1, -1), (bound - 777, 3)]
+    vals += [(int(rng.integers(-2 ** 62, 2 ** 62)) << (2 * t + 14 - 62), int(rng.integers(-2 ** 62, 2 ** 62)))
+             for _ in range(100)]
+    for cr, ci in vals:
+        cr, ci = max(-bound, min(bound, cr)), max(-bound, min(bound, ci))
+        xr, xi = [], []
+        for m, j in zip(mods, roots):
+            cp, cm = (cr + j * ci) % m, (cr - j * ci) % m
+            xr.append(cp + cm)
+            xi.append(cp - cm + m)
+        gr, gi = _gauss_crt(xr, mods, WR), _gauss_crt(xi, mods, WI)
+        for got, ref in ((gr, cr), (gi, ci)):
+            assert got == float(ref) or abs(got - ref) <= abs(ref) * 2.0 ** -52, (got, ref)
+
+
+def test_params_complex_3m_and_errors():
+    st, n, t, mods, roots, ppm = lib().tci_ozaki_params_complex(20480, 1)
+    st0, n0, t0, mods0 = lib().tci_ozaki_params(20480)
+    assert st == 0 and ppm == 3 and roots == [0] * n and (n, t, mods) == (n0, t0, mods0)
+    assert lib().tci_ozaki_params_complex(20480, 7)[0] != 0
+    assert lib().tci_ozaki_params_complex(131073, 0)[0] != 0
+    # the Gaussian variant needs 2n' INT8 GEMMs against 3n: 30 vs 42 at the bench's K
+    _, ng, _, _, _, _ = lib().tci_ozaki_params_complex(20480, 0)
+    assert (2 * ng, 3 * n) == (30, 42)

@@ -97,12 +97,13 @@ __global__ void ref_kernel(const int8_t *A, const int8_t *B, int64_t M, int64_t 
   out[i] = (uint8_t)r;
 }
 
+static const int hm[16] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193, 1};
+
 static int check(int64_t M, int64_t N, int64_t Kp, int L, int per_mod, bool full, int reps) {
   int8_t *A, *B;
   uint8_t *D, *R;
   int64_t *idx = nullptr;
   int *mods;
-  const int hm[16] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193, 1};
   cudaMalloc(&A, (size_t)L * M * Kp);
   cudaMalloc(&B, (size_t)L * N * Kp);
   cudaMalloc(&D, (size_t)L * M * N);
@@ -125,7 +126,7 @@ static int check(int64_t M, int64_t N, int64_t Kp, int L, int per_mod, bool full
     cudaMemcpy(idx, hidx.data(), nidx * 8, cudaMemcpyHostToDevice);
   }
   cudaMalloc(&R, nidx);
-  cudaError_t e = launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, ctr, 0, nullptr);
+  cudaError_t e = launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, hm, (L + per_mod - 1) / per_mod, ctr, 0, nullptr);
   if (e != cudaSuccess) { printf("launch: %s\n", cudaGetErrorString(e)); return 1; }
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("run: %s\n", cudaGetErrorString(e)); return 1; }
@@ -147,9 +148,9 @@ static int check(int64_t M, int64_t N, int64_t Kp, int L, int per_mod, bool full
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, ctr, 0, nullptr);
+    launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, hm, (L + per_mod - 1) / per_mod, ctr, 0, nullptr);
     cudaEventRecord(a);
-    for (int r = 0; r < reps; r++) launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, ctr, 0, nullptr);
+    for (int r = 0; r < reps; r++) launch_i8gemm(A, B, D, M, N, Kp, L, per_mod, hm, (L + per_mod - 1) / per_mod, ctr, 0, nullptr);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float t;

@@ -151,6 +151,27 @@ TCI_API int tci_ozaki_params(int64_t K, int *nmod, int *t, int *moduli);
  * Both are exact up to the same operand truncation (R26). The initial value
  * comes from TCI_OZAKI_CPLX = gauss | 3m (read at context creation).
  * Synchronizes the context stream. Errors: DEAD_CONTEXT, INVALID_ARGUMENT. */
+/* Float32 / complex64 GEMM algorithm of a context (reading R34):
+ *  TCI_F32_OZAKI_INT8 (default): GEMMs of >= 4e9 MACs run the Ozaki-II scheme
+ *    on the INT8 tcgen05 tensor cores with a bit budget t >= 24 (8-9 moduli
+ *    real, 9-10 Gaussian complex): operand entries within a factor 2 of their
+ *    line maximum are exact, the integer products and sums are exact, the
+ *    result is rounded once to float32. Guarded like the float64 path, with
+ *    tolerance max(guard tol, 1e-7); a flagged GEMM is recomputed on the FP64
+ *    cores;
+ *  TCI_F32_FP64_CORES: products and sums in float64 on the CUDA cores (R20).
+ * The initial value comes from TCI_F32_ALGO = ozaki | fp64 (context
+ * creation). Synchronizes the context stream. Errors: DEAD_CONTEXT,
+ * INVALID_ARGUMENT. */
+/* Diagnostic (pure host): the Ozaki parameters of float32 (cplx = 0) or
+ * complex64 (cplx != 0, Gaussian moduli) GEMMs for contraction length K:
+ * moduli count, bit budget t (>= 24), moduli[<= 16], residue planes per
+ * modulus (1 or 2). Out-pointers may be NULL. Returns 0 or OUT_OF_RANGE. */
+TCI_API int tci_ozaki_params_f32(int64_t K, int cplx, int *nmod, int *t, int *moduli, int *planes_per_mod);
+#define TCI_F32_OZAKI_INT8 0
+#define TCI_F32_FP64_CORES 1
+TCI_API tci_status_t tci_set_f32_algorithm(tci_ctx_t ctx, int algo);
+
 #define TCI_OZAKI_CPLX_GAUSS 0
 #define TCI_OZAKI_CPLX_3M 1
 TCI_API tci_status_t tci_set_ozaki_complex(tci_ctx_t ctx, int variant);

@@ -53,7 +53,7 @@ EXPORTED = [
     "tci_ipc_handle", "tci_ipc_open", "tci_ipc_close", "tci_gather_register", "tci_heff_apply_gather",
     "tci_gather_status", "tci_tebd_workspace_size", "tci_copy_async", "tci_lane_record", "tci_lane_wait",
     "tci_set_ozaki_guard", "tci_ozaki_guard_stats", "tci_ozaki_params_complex",
-    "tci_set_ozaki_complex",
+    "tci_set_ozaki_complex", "tci_set_f32_algorithm", "tci_ozaki_params_f32",
 ]
 
 
@@ -125,6 +125,8 @@ _sig = {
                           ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_ozaki_params_complex": ([ctypes.c_int64, ctypes.c_int] + [ctypes.POINTER(ctypes.c_int)] * 5, ctypes.c_int),
     "tci_set_ozaki_complex": ([_vp, ctypes.c_int], ctypes.c_int),
+    "tci_set_f32_algorithm": ([_vp, ctypes.c_int], ctypes.c_int),
+    "tci_ozaki_params_f32": ([ctypes.c_int64, ctypes.c_int] + [ctypes.POINTER(ctypes.c_int)] * 4, ctypes.c_int),
     "tci_get_gemm_algorithm": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_set_ozaki_guard": ([_vp, ctypes.c_double], ctypes.c_int),
     "tci_ozaki_guard_stats": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
@@ -453,6 +455,22 @@ def tci_ozaki_params(K: int):
     mods = (ctypes.c_int * 16)()
     st = _lib.tci_ozaki_params(int(K), ctypes.byref(n), ctypes.byref(t), mods)
     return st, n.value, t.value, [mods[i] for i in range(n.value)]
+
+
+TCI_F32_OZAKI_INT8 = 0
+TCI_F32_FP64_CORES = 1
+
+
+def tci_ozaki_params_f32(K: int, cplx: bool):
+    n, t, ppm = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    mods = (ctypes.c_int * 16)()
+    st = _lib.tci_ozaki_params_f32(int(K), 1 if cplx else 0, ctypes.byref(n), ctypes.byref(t), mods,
+                                   ctypes.byref(ppm))
+    return st, n.value, t.value, [mods[i] for i in range(n.value)], ppm.value
+
+
+def tci_set_f32_algorithm(ctx: int, algo: int) -> None:
+    _ok(_lib.tci_set_f32_algorithm(_vp(ctx), int(algo)), "tci_set_f32_algorithm")
 
 
 TCI_OZAKI_CPLX_GAUSS = 0
@@ -804,6 +822,9 @@ class Context:
 
     def set_ozaki_complex(self, variant: int):
         tci_set_ozaki_complex(self.handle, variant)
+
+    def set_f32_algorithm(self, algo: int):
+        tci_set_f32_algorithm(self.handle, algo)
 
     def ozaki_guard_stats(self, reset: bool = False) -> dict:
         return tci_ozaki_guard_stats(self.handle, reset)

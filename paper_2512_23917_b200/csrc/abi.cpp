@@ -57,7 +57,8 @@ tci_status_t run_gemm(tci_ctx_s *ctx, const GemmProblem &g) {
   OzProf pf{};
   GemmProblem gg = g;
   if (ctx->prof_on && g.zalgo == kZOzaki) gg.oz_prof = &pf;
-  gg.oz_tol = ctx->oz_tol;
+  const bool f32 = g.dtype == TCI_R32 || g.dtype == TCI_C64;
+  gg.oz_tol = (f32 && ctx->oz_tol > 0.0) ? std::max(ctx->oz_tol, kOzakiF32Tol) : ctx->oz_tol;
   gg.oz_guard = ctx->oz_guard;
   gg.oz_gauss = ctx->oz_gauss;
   TCI_CUDA_CHECK(launch_gemm(gg, ctx->stream, &ctx->launches));
@@ -244,6 +245,10 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   }
   c->oz_guard = nullptr;
   c->oz_gauss = 1;
+  c->f32_algo = TCI_F32_OZAKI_INT8;
+  if (const char *e = getenv("TCI_F32_ALGO")) {
+    if (!strcmp(e, "fp64") || !strcmp(e, "simt")) c->f32_algo = TCI_F32_FP64_CORES;
+  }
   if (const char *e = getenv("TCI_OZAKI_CPLX")) {
     if (!strcmp(e, "3m") || !strcmp(e, "3M")) c->oz_gauss = 0;
   }
@@ -371,6 +376,15 @@ tci_status_t tci_set_ozaki_guard(tci_ctx_t ctx, double tol) {
   CHECK(check_ctx(ctx));
   if (!(tol == tol)) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "tolerance is NaN");
   ctx->oz_tol = tol > 0.0 ? tol : 0.0;
+  return TCI_OK;
+}
+
+tci_status_t tci_set_f32_algorithm(tci_ctx_t ctx, int algo) {
+  CHECK(check_ctx(ctx));
+  if (algo != TCI_F32_OZAKI_INT8 && algo != TCI_F32_FP64_CORES)
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "unknown float32 GEMM algorithm %d", algo);
+  TCI_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  ctx->f32_algo = algo;
   return TCI_OK;
 }
 
@@ -1242,6 +1256,18 @@ extern "C" int tci_ozaki_params(int64_t K, int *nmod, int *t, int *moduli) {
   int n = 0;
   tci::ozaki_params(K, 0, &n, t, &m, nullptr);
   if (nmod) *nmod = n;
+  if (moduli)
+    for (int i = 0; i < n; i++) moduli[i] = m[i];
+  return (K >= 1 && K <= tci::kOzakiMaxK) ? 0 : (int)TCI_ERR_OUT_OF_RANGE;
+}
+
+extern "C" int tci_ozaki_params_f32(int64_t K, int cplx, int *nmod, int *t, int *moduli, int *planes_per_mod) {
+  const int *m = nullptr;
+  int n = 0;
+  // complex64 takes the Gaussian moduli (2 planes per modulus), float32 the real ones
+  tci::ozaki_params(K, cplx ? 2 : 0, &n, t, &m, nullptr, tci::kOzakiTminF32);
+  if (nmod) *nmod = n;
+  if (planes_per_mod) *planes_per_mod = cplx ? 2 : 1;
   if (moduli)
     for (int i = 0; i < n; i++) moduli[i] = m[i];
   return (K >= 1 && K <= tci::kOzakiMaxK) ? 0 : (int)TCI_ERR_OUT_OF_RANGE;

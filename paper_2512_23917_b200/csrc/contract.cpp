@@ -341,6 +341,11 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   const int64_t M = extent(I, dim_of), N = extent(J, dim_of), K = extent(S, dim_of);
   const size_t es = dtype_size(a.dtype);
 
+  // the INT8 tensor-core path (Ozaki-II) for this dtype under the context's
+  // choice: float64 / complex128 when the GEMM algorithm is Ozaki, float32 /
+  // complex64 unless the context keeps them on the FP64 cores (R34)
+  const bool oz_dtype = ((a.dtype == TCI_C128 || a.dtype == TCI_R64) && ctx->zgemm_algo == kZOzaki) ||
+                        ((a.dtype == TCI_R32 || a.dtype == TCI_C64) && ctx->f32_algo == TCI_F32_OZAKI_INT8);
   // deterministic split-K when the output has too few tiles to fill the 148
   // SMs and K is long: S partial GEMMs over K chunks + an ascending-order sum
   int splitk = 1;
@@ -352,8 +357,7 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
     const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
     // (not when the GEMM goes to the INT8 tensor cores: its 3n / n residue
     // GEMMs of one launch fill the machine by themselves)
-    const bool oz_candidate = (a.dtype == TCI_C128 || a.dtype == TCI_R64) && ctx->zgemm_algo == kZOzaki &&
-                              ozaki_worthwhile(M, N, K);
+    const bool oz_candidate = oz_dtype && ozaki_worthwhile(M, N, K);
     if (tiles < 2 * 148 && K >= 256 && !oz_candidate) {
       int64_t S = std::min<int64_t>({(4 * 148 + tiles - 1) / tiles, K / 128, 1024});
       if (S >= 2) {
@@ -366,8 +370,7 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   // complex128 GEMM algorithm
   int zalgo = ctx->zgemm_algo == kZOzaki ? kZ3M : ctx->zgemm_algo;
   // (float64 too: real Ozaki-II, one residue plane per modulus)
-  const bool use_ozaki = (a.dtype == TCI_C128 || a.dtype == TCI_R64) && ctx->zgemm_algo == kZOzaki &&
-                         splitk <= 1 && ozaki_worthwhile(M, N, K);
+  const bool use_ozaki = oz_dtype && splitk <= 1 && ozaki_worthwhile(M, N, K);
   // gamma-order scatter epilogue (8(a6)): an output that is not a [I,J] /
   // [J,I] block is written in place through row / column offset tables
   // instead of GEMM -> scratch -> permute; the GEMM is oriented so that the

@@ -690,7 +690,13 @@ static cudaError_t launch_gemm_main(const GemmProblem &p, cudaStream_t s, int64_
   if (p.M == 0 || p.N == 0) return cudaSuccess;
   // one of M, N, K tiny: HBM-bound, no tensor-core tile (gemm_thin.cu)
   if (gemm_thin_applies(p)) return launch_gemm_thin(p, s, launches);
-  if (p.dtype == TCI_R32 || p.dtype == TCI_C64) return launch_gemm_f32(p, s, launches);
+  if (p.dtype == TCI_R32 || p.dtype == TCI_C64) {
+    // float32 / complex64 on the INT8 tensor cores (Ozaki-II, t >= 24: R34)
+    if (p.zalgo == kZOzaki && p.splitk <= 1 && p.mode == 0 && !p.c_row)
+      return p.dtype == TCI_C64 ? launch_ozaki_zgemm(p, p.oz_ws, p.oz_ws_bytes, s, launches)
+                                : launch_ozaki_dgemm(p, p.oz_ws, p.oz_ws_bytes, s, launches);
+    return launch_gemm_f32(p, s, launches);
+  }
   // The planner canonicalises strides (contract.cpp): a_sk == 1 selects the
   // K-contiguous loader, otherwise a_sm == 1; same for B.
   const bool ak = (p.a_sk == 1), bk = (p.b_sk == 1);

@@ -51,6 +51,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
   // operands are widened to fp64 once, when staged (products exact, R20)
   __shared__ Acc As[2][BK][BM];
   __shared__ Acc Bs[2][BK][BN];
+  // the Ozaki guard's gated recomputation (R34): nothing to do unless *run_if
+  if (p.run_if && *reinterpret_cast<const volatile int *>(p.run_if) == 0) return;
   const int tid = threadIdx.x;
   const int tile_m = blockIdx.x / tiles_n, tile_n = blockIdx.x % tiles_n;
   const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN;

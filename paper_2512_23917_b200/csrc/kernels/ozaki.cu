@@ -35,6 +35,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "../tci_internal.h"
 #include "common.cuh"
@@ -43,6 +44,10 @@ namespace tci {
 namespace {
 
 constexpr int kMaxMod = 15;
+// bit budget of float32 / complex64 sources (R34): operand entries keep 24
+// bits relative to their line maximum -- every entry within 2^0 of it is
+// exact (a float32 mantissa), smaller ones round as fp32 arithmetic would
+constexpr int kOzTminF32 = kOzakiTminF32;
 constexpr int kModuli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
 __constant__ int c_moduli[kMaxMod] = {255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
 
@@ -111,6 +116,12 @@ __device__ __forceinline__ void es_merge(int &em, double &s, int e2, double s2) 
 __device__ __forceinline__ void es_add(int &em, double &s, double2 x) {
   es_add(em, s, x.x);
   es_add(em, s, x.y);
+}
+// float32 sources (exact widening)
+__device__ __forceinline__ void es_add(int &em, double &s, float x) { es_add(em, s, (double)x); }
+__device__ __forceinline__ void es_add(int &em, double &s, float2 x) {
+  es_add(em, s, (double)x.x);
+  es_add(em, s, (double)x.y);
 }
 
 // per-k statistics when the lines are contiguous (s_l == 1): one warp per k,
@@ -238,6 +249,29 @@ __device__ __forceinline__ int exp_of(double x) {
   return e;
 }
 __device__ __forceinline__ int exp_of(double2 v) { return max(exp_of(v.x), exp_of(v.y)); }
+__device__ __forceinline__ int exp_of(float v) { return exp_of((double)v); }
+__device__ __forceinline__ int exp_of(float2 v) { return max(exp_of((double)v.x), exp_of((double)v.y)); }
+__device__ __forceinline__ int exp_of_shift(float2 v, int s) {
+  const int e = exp_of(v);
+  return e == -100000 ? e : e + s;
+}
+__device__ __forceinline__ int exp_of_shift(float v, int s) {
+  const int e = exp_of(v);
+  return e == -100000 ? e : e + s;
+}
+// operand loads widened to double (float32 sources: exact)
+__device__ __forceinline__ double2 ld_c(const double2 *p) { return __ldg(p); }
+__device__ __forceinline__ double2 ld_c(const float2 *p) {
+  const float2 v = __ldg(p);
+  return make_double2(v.x, v.y);
+}
+__device__ __forceinline__ double ld_r(const double *p) { return __ldg(p); }
+__device__ __forceinline__ double ld_r(const float *p) { return (double)__ldg(p); }
+// result stores (streaming); float32 results are rounded once
+__device__ __forceinline__ void st_c(double2 *p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_c(float2 *p, double2 v) { __stcs(p, make_float2((float)v.x, (float)v.y)); }
+__device__ __forceinline__ void st_r(double *p, double v) { *p = v; }
+__device__ __forceinline__ void st_r(float *p, double v) { *p = (float)v; }
 __device__ __forceinline__ int exp_of_shift(double2 v, int s) {
   const int e = exp_of(v);
   return e == -100000 ? e : e + s;
@@ -370,7 +404,9 @@ __device__ __forceinline__ void residue_words(const ResVals<NV> &v, int l, uint3
 // quotient rint(u/m) sits in the low mantissa bits of fma(u, 1/m, 1.5 2^23)
 // (|u/m - rint(u/m)| >= 1/(2m) > the fp32 error |u| 2^-24 / m)
 __device__ __forceinline__ int small_bal(int u, float minvf, int m) {
-  const float q = fmaf((float)u, minvf, 12582912.0f);
+  // (float)u without an I2F (XU pipe): u sits in the low mantissa bits of 1.5 2^23 + u
+  const float uf = __int_as_float(0x4B400000 + u) - 12582912.0f;
+  const float q = fmaf(uf, minvf, 12582912.0f);
   return u - (__float_as_int(q) - 0x4B400000) * m;
 }
 
@@ -443,7 +479,56 @@ struct ResArgs {
   const int *SK;            // K-balancing exponents (Kp entries) or null
   const int *bal;           // device flag: balancing active
   int sgn;                  // +1 for A, -1 for B
+  // Gaussian planes (R33): the moduli in groups [gfirst[g], gfirst[g+1]) whose
+  // products P_g < 2^44 (odd) reduce each integer once per group
+  double gP[3], gPinv[3];
+  int gPlo[3], gfirst[4];
 };
+
+// The two Gaussian planes of every modulus for 8 values of one line (R33).
+// Per group: x = q P + r_P exactly (q = rint(x / P) from one DFMA, r_P by a
+// second, its low word by an IMAD on the low words), so every modulus of the
+// group works on |r_P| < 2^43 instead of |x| < 2^49: x_u = r_P(re) + j r_P(im)
+// is an exact double (|x_u| < 2^50) whose balanced residue needs one DFMA
+// (the quotient) and one IMAD on the low words (lo(x_u) = lo(r_re) + j lo(r_im)).
+// 2 DFMA + 5 integer ops per modulus and value instead of 2 full reductions of
+// re and im plus two small ones (the kernel was instruction-issue bound).
+__device__ __forceinline__ void gauss_planes(const ResVals<8> &v, const ResArgs &a, int8_t *dst) {
+#pragma unroll 1
+  for (int g = 0; g < 3; g++) {
+    const int l0 = a.gfirst[g], l1 = min(a.gfirst[g + 1], a.nmod);
+    if (l0 >= l1) break;
+    const double P = a.gP[g], Pinv = a.gPinv[g];
+    const int Plo = a.gPlo[g];
+    double rp[8], ip[8];
+    int lr[8], li[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const double mr = fma(v.x[0][j], Pinv, kMagic), mi = fma(v.x[1][j], Pinv, kMagic);
+      rp[j] = fma(kMagic - mr, P, v.x[0][j]);   // x - q P, q = mr - kMagic (exact)
+      ip[j] = fma(kMagic - mi, P, v.x[1][j]);
+      lr[j] = v.lo[0][j] - __double2loint(mr) * Plo;
+      li[j] = v.lo[1][j] - __double2loint(mi) * Plo;
+    }
+#pragma unroll 1
+    for (int l = l0; l < l1; l++) {
+      const int mi = c_gmod[l], jr = c_groot[l];
+      const double minv = c_gminv[l], jd = (double)c_groot[l];
+      int u[8], d[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const double xu = fma(jd, ip[j], rp[j]), xd = fma(-jd, ip[j], rp[j]);
+        const int tj = jr * li[j];
+        u[j] = (lr[j] + tj) - __double2loint(fma(xu, minv, kMagic)) * mi;
+        d[j] = (lr[j] - tj) - __double2loint(fma(xd, minv, kMagic)) * mi;
+      }
+      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 2) * a.plane_stride) =
+          make_uint2(pack4(u[0], u[1], u[2], u[3]), pack4(u[4], u[5], u[6], u[7]));
+      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 2 + 1) * a.plane_stride) =
+          make_uint2(pack4(d[0], d[1], d[2], d[3]), pack4(d[4], d[5], d[6], d[7]));
+    }
+  }
+}
 
 // per-element scale factors of 8 consecutive k (SK has Kp >= k0 + 8 entries)
 __device__ __forceinline__ void elem_scales(const ResArgs &a, int E, int64_t k0, double (&fa)[8], double (&fb)[8]) {
@@ -454,7 +539,7 @@ __device__ __forceinline__ void elem_scales(const ResArgs &a, int E, int64_t k0,
   for (int j = 0; j < 8; j++) scale_pair(a.t - E + a.sgn * s[j], fa[j], fb[j]);
 }
 
-template <bool G>
+template <bool G, class TS>
 __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs a) {
   constexpr int NV = 8;
   const int64_t kgroups = a.Kp / NV;
@@ -466,10 +551,10 @@ __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs 
   const int64_t line = a.line0 + row;
   ResVals<NV> x;
   if (line < a.nlines && a.E[line] > -100000) {
-    const double2 *p = static_cast<const double2 *>(a.base) + line * a.s_l;
+    const TS *p = static_cast<const TS *>(a.base) + line * a.s_l;
     double2 v[NV];
 #pragma unroll
-    for (int j = 0; j < NV; j++) v[j] = k0 + j < a.K ? __ldg(p + (k0 + j) * a.s_k) : make_double2(0.0, 0.0);
+    for (int j = 0; j < NV; j++) v[j] = k0 + j < a.K ? ld_c(p + (k0 + j) * a.s_k) : make_double2(0.0, 0.0);
     if (a.SK && *a.bal) {
       double fa[NV], fb[NV];
       elem_scales(a, a.E[line], k0, fa, fb);
@@ -486,13 +571,16 @@ __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs 
     for (int j = 0; j < NV; j++) x.set(j, kMagic, kMagic);
   }
   int8_t *dst = a.out + row * a.Kp + k0;
-  for (int l = 0; l < a.nmod; l++) store_planes<G, NV>(x, l, dst, a.plane_stride);
+  if constexpr (G)
+    gauss_planes(x, a, dst);
+  else
+    for (int l = 0; l < a.nmod; l++) store_planes<G, NV>(x, l, dst, a.plane_stride);
 }
 
 // line-contiguous source (s_l == 1): a 32-line x 64-k tile is read along the
 // lines (coalesced), turned into integers in shared memory and written along
 // k: eight threads write one line's 64 contiguous residue bytes per plane.
-template <bool G>
+template <bool G, class TS>
 __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArgs a) {
   __shared__ double sx[2][32][65];
   const int64_t ntk = a.Kp / 64;
@@ -506,12 +594,12 @@ __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArg
     const bool b = a.SK && *a.bal;
     double s2a = 0.0, s2b = 0.0;   // 0 -> scaled value 0 for dead lines
     if (ok && !b) line_scale(a.t, a.E[line], s2a, s2b);
-    const double2 *base = static_cast<const double2 *>(a.base);
+    const TS *base = static_cast<const TS *>(a.base);
     double2 v[8];
 #pragma unroll
     for (int jj = 0; jj < 8; jj++) {
       const int64_t k = kb + tid / 32 + jj * 8;
-      v[jj] = ok && k < a.K ? __ldg(base + line + k * a.s_k) : make_double2(0.0, 0.0);
+      v[jj] = ok && k < a.K ? ld_c(base + line + k * a.s_k) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int jj = 0; jj < 8; jj++) {
@@ -531,7 +619,10 @@ __global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArg
 #pragma unroll
   for (int j = 0; j < 8; j++) x.set(j, sx[0][li][kq + j], sx[1][li][kq + j]);
   int8_t *dst = a.out + row * a.Kp + kb + kq;
-  for (int l = 0; l < a.nmod; l++) store_planes<G, 8>(x, l, dst, a.plane_stride);
+  if constexpr (G)
+    gauss_planes(x, a, dst);
+  else
+    for (int l = 0; l < a.nmod; l++) store_planes<G, 8>(x, l, dst, a.plane_stride);
 }
 
 // ---------------------------------------------------------------------------
@@ -553,16 +644,17 @@ struct CrtArgs {
   const uint8_t *D;         // [3n][Mc][Np], residues in [0, m)
   int64_t Mc, N, Np, m0;    // chunk rows, columns, padded columns, first row
   int nmod;
-  double W[kMaxGMod][4];    // CRT weight chunks (exact integers, 37 bits each; Gaussian: 40 bits, Re weights)
-  double WI[kMaxGMod][3];   // Gaussian: Im weights (40-bit chunks)
+  double W[kMaxGMod][4];    // CRT weight chunks (exact integers, 37 bits each; Gaussian: 39 bits, Re weights)
+  double WI[kMaxGMod][4];   // Gaussian: Im weights (39-bit chunks)
+  double Cr[4], Ci[4];      // 2^XS sum_l W[l][j] (Re) and over WI (Im): offsets of the 1 + x 2^-XS encoding
   double Mch[4];            // M chunks
   double Minv;              // ~1 / M
   const int *EA, *EB;       // exponents
   int t;
-  double2 *C;
+  void *C;                  // double2 (complex128) or float2 (complex64, TO)
   int64_t c_sm;
   int npeer;                // peer-memory all-gather: the same element also
-  double2 *peer[7];         // stored at peer[p] + (m c_sm + n) over NVLink
+  void *peer[7];            // stored at peer[p] + (m c_sm + n) over NVLink
   double *rowsq;            // guard row sums [M][tpr] or null
   const int *eb_max;        // device: max_n E_n
 };
@@ -589,6 +681,18 @@ __device__ __forceinline__ double crt_value(const double (&S)[NCH], const double
   return x;
 }
 
+// The small representative x < 2^XS as the double 1 + x 2^-XS, built with
+// integer ops only (x in the top mantissa bits of the high word): the CRT
+// needs no int -> double conversion (an XU-pipe instruction that would bound
+// the kernel: 30 of them per complex output against 16 XU ops / clk / SM).
+// sum_l (1 + x_l 2^-XS) W_l = sum_l W_l + 2^-XS sum_l x_l W_l: every partial
+// sum is a multiple of 2^-XS below 2^(53-XS), hence exact, and
+// 2^XS T - 2^XS sum_l W_l recovers sum_l x_l W_l exactly.
+template <int XS>
+__device__ __forceinline__ double one_plus(uint32_t x) {
+  return __hiloint2double((int)(0x3FF00000u | (x << (20 - XS))), 0);
+}
+
 // fixed-order block sum of one double per thread (THREADS = 32 * warps):
 // xor tree inside each warp, warps in ascending order by thread 0
 template <int THREADS>
@@ -611,7 +715,7 @@ __device__ __forceinline__ double block_sum_fixed(double v, double *red) {
 template <int CPT, int THREADS, int STAGES, int PPM = 3>
 struct CrtShape {
   static constexpr int kTW = CPT * THREADS;
-  static constexpr size_t smem(int nmod) { return (size_t)STAGES * PPM * nmod * kTW + 8 * STAGES; }
+  static constexpr size_t smem(int nmod) { return (size_t)STAGES * PPM * nmod * kTW + 16 * STAGES; }
 };
 
 // NCH = 3 chunks while sum_l 3 m_l w_lj stays below 2^53 (nmod <= 14: top
@@ -623,48 +727,61 @@ struct CrtShape {
 // WI_l = (2j)^-1 w_l mod M), applied to the representatives c+ + c- in
 // [0, 2m) and c+ - c- + m in (0, 2m); 40-bit chunks keep every chunk sum
 // exact (16 * 482 * 2^40 < 2^53) with 3 chunks for up to 16 moduli.
-template <int NMOD, int NCH, int CPT, int THREADS, int STAGES, bool G = false>
-__global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ CrtArgs a) {
+template <int NMOD, int NCH, int CPT, int THREADS, int STAGES, bool G, class TO>
+__global__ void __launch_bounds__(THREADS + 32, 2) crt_kernel(const __grid_constant__ CrtArgs a) {
   static_assert(CPT == 2 || CPT == 4, "columns per thread");
   constexpr int PPM = G ? 2 : 3;       // planes per modulus
-  constexpr int CB = G ? 40 : 37;      // CRT chunk bits
+  constexpr int CB = G ? 39 : 37;      // CRT chunk bits
+  constexpr int XS = G ? 9 : 10;       // representatives < 2^XS (Gaussian < 2m <= 482, 3M < 3m <= 765)
   using Shape = CrtShape<CPT, THREADS, STAGES, PPM>;
   constexpr int TW = Shape::kTW;
   extern __shared__ __align__(128) uint8_t crt_smem[];
   __shared__ double red[2][THREADS / 32];
   constexpr int kStage = PPM * NMOD * TW;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(crt_smem + STAGES * kStage);
+  // full[s]: the stage's bytes landed (TMA transaction count); empty[s]: every
+  // compute warp finished reading it
+  uint64_t *full = reinterpret_cast<uint64_t *>(crt_smem + STAGES * kStage);
+  uint64_t *empty = full + STAGES;
   const int64_t tpr = (a.Np + TW - 1) / TW;   // tiles per row
   const int64_t ntiles = a.Mc * tpr;
   const int64_t plane = a.Mc * a.Np;
   const int tid = threadIdx.x;
-  const int ebm = a.rowsq ? *a.eb_max : 0;
-
-  auto issue = [&](int64_t tile, int s) {   // warp 0
-    const int64_t r = tile / tpr, c0 = (tile % tpr) * TW;
-    const uint32_t w = (uint32_t)(a.Np - c0 < TW ? a.Np - c0 : TW);   // multiple of 16
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      mbar_expect_tx(&bar[s], PPM * NMOD * w);
-    }
-    __syncwarp();
-    for (int q = tid; q < PPM * NMOD; q += 32)
-      bulk_g2s(crt_smem + s * kStage + q * TW, a.D + q * plane + r * a.Np + c0, w, &bar[s]);
-  };
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; s++) mbar_init(&bar[s], 1);
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], THREADS / 32);
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  if (tid < 32)
-    for (int s = 0; s < STAGES; s++)
-      if (blockIdx.x + (int64_t)s * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)s * gridDim.x, s);
 
+  if (tid >= THREADS) {
+    // producer warp: the PPM * NMOD plane rows of each tile by cp.async.bulk
+    // (TMA), STAGES tiles ahead of the compute warps; it never joins their
+    // barriers, so its serialized copy issue is off their critical path
+    const int lane = tid - THREADS;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+      const int s = it % STAGES;
+      if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
+      const int64_t r = tile / tpr, c0 = (tile % tpr) * TW;
+      const uint32_t w = (uint32_t)(a.Np - c0 < TW ? a.Np - c0 : TW);   // multiple of 16
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(&full[s], PPM * NMOD * w);
+      }
+      __syncwarp();
+      for (int q = lane; q < PPM * NMOD; q += 32)
+        bulk_g2s(crt_smem + s * kStage + q * TW, a.D + q * plane + r * a.Np + c0, w, &full[s]);
+    }
+    return;
+  }
+  const int ebm = a.rowsq ? *a.eb_max : 0;
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
     const int s = it % STAGES;
-    mbar_wait(&bar[s], (uint32_t)((it / STAGES) & 1));
+    mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
     const int64_t r = tile / tpr, n0 = (tile % tpr) * TW + CPT * tid;
     double sq = 0.0;
     if (n0 < a.N) {
@@ -695,8 +812,8 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
 #pragma unroll
             for (int lane = 0; lane < 2; lane++) {
               const int e = half * 2 + lane;
-              const double dr = (double)(lane ? xr2 >> 16 : xr2 & 0xffffu);
-              const double di = (double)(lane ? xi2 >> 16 : xi2 & 0xffffu);
+              const double dr = one_plus<XS>(lane ? xr2 >> 16 : xr2 & 0xffffu);
+              const double di = one_plus<XS>(lane ? xi2 >> 16 : xi2 & 0xffffu);
 #pragma unroll
               for (int j = 0; j < NCH; j++) {
                 Sr[e][j] = fma(dr, a.W[i][j], Sr[e][j]);
@@ -729,16 +846,24 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
 #pragma unroll
           for (int lane = 0; lane < 2; lane++) {
             const int e = half * 2 + lane;
-            const double dr = (double)(lane ? cr2 >> 16 : cr2 & 0xffffu);   // I2F on the XU pipe,
-            const double di = (double)(lane ? ci2 >> 16 : ci2 & 0xffffu);   // beside the saturated FP64 pipe
+            const double dr = one_plus<XS>(lane ? cr2 >> 16 : cr2 & 0xffffu);
+            const double di = one_plus<XS>(lane ? ci2 >> 16 : ci2 & 0xffffu);
 #pragma unroll
             for (int j = 0; j < NCH; j++) {
               Sr[e][j] = fma(dr, a.W[i][j], Sr[e][j]);
-              Si[e][j] = fma(di, a.W[i][j], Si[e][j]);
+              Si[e][j] = fma(di, a.WI[i][j], Si[e][j]);
             }
           }
         }
       }
+      // undo the 1 + x 2^-XS encoding: S_j = 2^XS T_j - 2^XS sum_l W_lj (exact)
+#pragma unroll
+      for (int e = 0; e < CPT; e++)
+#pragma unroll
+        for (int j = 0; j < NCH; j++) {
+          Sr[e][j] = fma(Sr[e][j], (double)(1 << XS), -a.Cr[j]);
+          Si[e][j] = fma(Si[e][j], (double)(1 << XS), -a.Ci[j]);
+        }
       const int64_t m = a.m0 + r;
       const int ea = a.EA[m];
       const int sc0 = -(2 * a.t - ea);
@@ -764,9 +889,9 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
             sq = fma(xi * g, xi * g, sq);
           }
         }
-        __stcs(&a.C[m * a.c_sm + n], out);
+        st_c(static_cast<TO *>(a.C) + m * a.c_sm + n, out);
 #pragma unroll 1
-        for (int pp = 0; pp < a.npeer; pp++) __stcs(&a.peer[pp][m * a.c_sm + n], out);
+        for (int pp = 0; pp < a.npeer; pp++) st_c(static_cast<TO *>(a.peer[pp]) + m * a.c_sm + n, out);
       }
     }
     if (a.rowsq) {
@@ -776,41 +901,44 @@ __global__ void __launch_bounds__(THREADS) crt_kernel(const __grid_constant__ Cr
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if ((tid & 31) == 0) red[it & 1][tid >> 5] = v;
     }
-    __syncthreads();   // stage s fully consumed
-    if (a.rowsq && tid == 0) {
-      double v = 0.0;
-      for (int w = 0; w < THREADS / 32; w++) v += red[it & 1][w];
-      a.rowsq[(a.m0 + r) * tpr + tile % tpr] = v;
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
+    if (a.rowsq) {
+      named_bar_sync(1, THREADS);                   // compute warps only
+      if (tid == 0) {
+        double v = 0.0;
+        for (int w = 0; w < THREADS / 32; w++) v += red[it & 1][w];
+        a.rowsq[(a.m0 + tile / tpr) * tpr + tile % tpr] = v;
+      }
     }
-    const int64_t next = tile + (int64_t)STAGES * gridDim.x;
-    if (tid < 32 && next < ntiles) issue(next, s);
   }
 }
 
-template <int NMOD, int NCH, int CPT, int THREADS, int STAGES, bool G = false>
+template <int NMOD, int NCH, int CPT, int THREADS, int STAGES, bool G, class TO>
 cudaError_t launch_crt_cfg(const CrtArgs &c, int64_t mc, cudaStream_t s) {
   using Shape = CrtShape<CPT, THREADS, STAGES, G ? 2 : 3>;
-  auto kern = crt_kernel<NMOD, NCH, CPT, THREADS, STAGES, G>;
+  auto kern = crt_kernel<NMOD, NCH, CPT, THREADS, STAGES, G, TO>;
   const size_t smem = Shape::smem(NMOD);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS + 32, smem);
   if (e != cudaSuccess) return e;
   const int64_t ntiles = mc * ((c.Np + Shape::kTW - 1) / Shape::kTW);
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)std::max(per_sm, 1) * sms);
-  kern<<<grid, THREADS, smem, s>>>(c);
+  kern<<<grid, THREADS + 32, smem, s>>>(c);   // + the producer warp
   return cudaGetLastError();
 }
 
 constexpr int kCrtTW = 1024;   // CRT tile width (columns): 4 per thread x 256 threads
 // 4 columns x 256 threads x 2 stages: measured best of {2,4} x {128,256} x
 // {2,3,4} on the target shapes (the kernel is XU/FP64-issue bound there).
-template <int NMOD, int NCH, bool G = false>
+template <int NMOD, int NCH, bool G, class TO>
 cudaError_t launch_crt(const CrtArgs &c, int64_t mc, cudaStream_t s) {
-  return launch_crt_cfg<NMOD, NCH, 4, 256, 2, G>(c, mc, s);
+  // Gaussian stages are 2/3 the size of 3M ones: three fit beside a second CTA
+  return launch_crt_cfg<NMOD, NCH, 4, 256, G ? 3 : 2, G, TO>(c, mc, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -819,6 +947,7 @@ cudaError_t launch_crt(const CrtArgs &c, int64_t mc, cudaStream_t s) {
 // of 3n. C'(m, n) = sum_k A'(m, k) B'(k, n) with |C'| <= K 2^(2t) <= M/8.
 // ---------------------------------------------------------------------------
 // K-contiguous: 8 consecutive k of one line per thread, 8 bytes per plane
+template <class TS>
 __global__ void __launch_bounds__(256) residues_real(const __grid_constant__ ResArgs a) {
   const int64_t kgroups = a.Kp / 8;
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -827,10 +956,10 @@ __global__ void __launch_bounds__(256) residues_real(const __grid_constant__ Res
   double x[8];
   int lo[8];
   if (line < a.nlines && a.E[line] > -100000) {
-    const double *p = static_cast<const double *>(a.base) + line * a.s_l;
+    const TS *p = static_cast<const TS *>(a.base) + line * a.s_l;
     double v[8];
 #pragma unroll
-    for (int j = 0; j < 8; j++) v[j] = k0 + j < a.K ? __ldg(p + (k0 + j) * a.s_k) : 0.0;
+    for (int j = 0; j < 8; j++) v[j] = k0 + j < a.K ? ld_r(p + (k0 + j) * a.s_k) : 0.0;
     double fa[8], fb[8];
     if (a.SK && *a.bal) {
       elem_scales(a, a.E[line], k0, fa, fb);
@@ -869,6 +998,7 @@ __global__ void __launch_bounds__(256) residues_real(const __grid_constant__ Res
 }
 
 // line-contiguous: 32-line x 64-k tile through shared memory (as residues_t)
+template <class TS>
 __global__ void __launch_bounds__(256) residues_real_t(const __grid_constant__ ResArgs a) {
   __shared__ double sx[32][65];
   const int64_t ntk = a.Kp / 64;
@@ -882,12 +1012,12 @@ __global__ void __launch_bounds__(256) residues_real_t(const __grid_constant__ R
     const bool b = a.SK && *a.bal;
     double s2a = 0.0, s2b = 0.0;
     if (ok && !b) line_scale(a.t, a.E[line], s2a, s2b);
-    const double *base = static_cast<const double *>(a.base);
+    const TS *base = static_cast<const TS *>(a.base);
     double v[8];
 #pragma unroll
     for (int jj = 0; jj < 8; jj++) {
       const int64_t k = kb + tid / 32 + jj * 8;
-      v[jj] = ok && k < a.K ? __ldg(base + line + k * a.s_k) : 0.0;
+      v[jj] = ok && k < a.K ? ld_r(base + line + k * a.s_k) : 0.0;
     }
 #pragma unroll
     for (int jj = 0; jj < 8; jj++) {
@@ -929,17 +1059,18 @@ struct CrtArgsR {
   int64_t Mc, N, Np, m0;
   int nmod;
   double W[kMaxMod][4];
+  double C0[4];              // 2^8 sum_l W[l][j] (one_plus<8> encoding offset)
   double Mch[4];
   double Minv;
   const int *EA, *EB;
   int t;
-  double *C;
+  void *C;                   // double or float (TO)
   int64_t c_sm;
   double *rowsq;             // guard row sums [M][tpr] or null
   const int *eb_max;
 };
 
-template <int NMOD, int NCH>
+template <int NMOD, int NCH, class TO>
 __global__ void __launch_bounds__(256) crt_real_kernel(const __grid_constant__ CrtArgsR a) {
   __shared__ double red[8];
   const int64_t tpr = (a.Np + kCrtTW - 1) / kCrtTW;
@@ -959,11 +1090,15 @@ __global__ void __launch_bounds__(256) crt_real_kernel(const __grid_constant__ C
       const uint32_t w4 = __ldg(reinterpret_cast<const uint32_t *>(a.D + i * plane + r * a.Np + n0));
 #pragma unroll
       for (int e = 0; e < 4; e++) {
-        const double c = (double)((w4 >> (8 * e)) & 0xffu);
+        const double c = one_plus<8>((w4 >> (8 * e)) & 0xffu);   // 1 + byte 2^-8, no I2F
 #pragma unroll
         for (int j = 0; j < NCH; j++) S[e][j] = fma(c, a.W[i][j], S[e][j]);
       }
     }
+#pragma unroll
+    for (int e = 0; e < 4; e++)
+#pragma unroll
+      for (int j = 0; j < NCH; j++) S[e][j] = fma(S[e][j], 256.0, -a.C0[j]);
     const int ea = a.EA[m];
     const int ebm = a.rowsq ? *a.eb_max : 0;
 #pragma unroll
@@ -981,7 +1116,7 @@ __global__ void __launch_bounds__(256) crt_real_kernel(const __grid_constant__ C
           sq = fma(x * g, x * g, sq);
         }
       }
-      a.C[m * a.c_sm + n] = out;
+      st_r(static_cast<TO *>(a.C) + m * a.c_sm + n, out);
     }
   }
   if (a.rowsq) {
@@ -1123,8 +1258,10 @@ int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 size_t align_up(size_t x) { return (x + 255) / 256 * 256; }
 
 // exactness (R26/R33): |C'| <= 2 K 2^(2t) <= M/4, i.e. 2t + 3 + log2 K <= log2 M;
-// the fewest moduli that allow t >= 46, then the largest such t
-OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_rows = 0, int kind = kOz3M) {
+// the fewest moduli that allow t >= tmin (46 for float64 sources, 24 for
+// float32: R34), then the largest such t
+OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_rows = 0, int kind = kOz3M,
+               int tmin = 46) {
   OzPlan p{};
   p.kind = kind;
   p.ppm = kind == kOzReal ? 1 : kind == kOz3M ? 3 : 2;
@@ -1136,7 +1273,7 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_row
   for (int l = 0; l < nmax; l++) {
     lm += std::log2((double)mods[l]);
     p.nmod = l + 1;
-    if (std::floor((lm - 3.0 - lk) / 2.0) >= 46) break;
+    if (std::floor((lm - 3.0 - lk) / 2.0) >= tmin) break;
   }
   p.t = (int)std::floor((lm - 3.0 - lk) / 2.0);
   p.Kp = round_up(K, 64);
@@ -1206,17 +1343,16 @@ void crt_constants(int nmod, double (&W)[kMaxMod][4], double (&Mch)[4], double &
 }
 
 // Gaussian set (R33): WR_l = (2^-1 mod m_l) w_l mod M and WI_l = ((2 j_l)^-1
-// mod m_l) w_l mod M in 40-bit chunks (3 chunks: M < 2^118), M chunks, ~1/M
-void crt_constants_gauss(int nmod, double (&WR)[kMaxGMod][4], double (&WI)[kMaxGMod][3], double (&Mch)[4],
+// mod m_l) w_l mod M in 39-bit chunks (3 chunks for 15 moduli, M < 2^112;
+// 4 for 16), M chunks, ~1/M
+constexpr int kGaussCB = 39;
+void crt_constants_gauss(int nmod, double (&WR)[kMaxGMod][4], double (&WI)[kMaxGMod][4], double (&Mch)[4],
                          double &Minv) {
   u128 Mp = 1;
   for (int l = 0; l < nmod; l++) Mp *= (u128)kGModuli[l];
-  const u128 mask = ((u128)1 << 40) - 1;
+  const u128 mask = ((u128)1 << kGaussCB) - 1;
   for (int l = 0; l < kMaxGMod; l++)
-    for (int j = 0; j < 4; j++) {
-      WR[l][j] = 0.0;
-      if (j < 3) WI[l][j] = 0.0;
-    }
+    for (int j = 0; j < 4; j++) WR[l][j] = WI[l][j] = 0.0;
   for (int l = 0; l < nmod; l++) {
     const unsigned ml = (unsigned)kGModuli[l];
     const u128 Ml = Mp / ml;
@@ -1225,12 +1361,12 @@ void crt_constants_gauss(int nmod, double (&WR)[kMaxGMod][4], double (&WI)[kMaxG
     const unsigned jl = (unsigned)((kGRoots[l] % (int)ml + (int)ml) % (int)ml);
     const unsigned g = inv_mod((2u * jl) % ml, ml);
     const u128 wr = mulmod_small(wl, h, Mp), wi = mulmod_small(wl, g, Mp);
-    for (int j = 0; j < 3; j++) {
-      WR[l][j] = (double)(uint64_t)((wr >> (40 * j)) & mask);
-      WI[l][j] = (double)(uint64_t)((wi >> (40 * j)) & mask);
+    for (int j = 0; j < 4; j++) {
+      WR[l][j] = (double)(uint64_t)((wr >> (kGaussCB * j)) & mask);
+      WI[l][j] = (double)(uint64_t)((wi >> (kGaussCB * j)) & mask);
     }
   }
-  for (int j = 0; j < 4; j++) Mch[j] = j < 3 ? (double)(uint64_t)((Mp >> (40 * j)) & mask) : 0.0;
+  for (int j = 0; j < 4; j++) Mch[j] = (double)(uint64_t)((Mp >> (kGaussCB * j)) & mask);
   Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
 }
 
@@ -1356,6 +1492,19 @@ struct OzRun {
     r.SK = SK;
     r.bal = misc + 1;
     r.sgn = isA ? 1 : -1;
+    if (p.kind == kOzGauss) {
+      // groups of the Gaussian moduli: 0-4, 5-9, 10-15 (products < 2^44)
+      const int first[4] = {0, 5, 10, kMaxGMod};
+      for (int gi = 0; gi < 3; gi++) {
+        double P = 1.0;
+        for (int l = first[gi]; l < std::min(first[gi + 1], p.nmod); l++) P *= (double)kGModuli[l];
+        r.gP[gi] = P;                      // exact: < 2^44
+        r.gPinv[gi] = 1.0 / P;
+        r.gPlo[gi] = (int)(uint32_t)(uint64_t)P;
+        r.gfirst[gi] = first[gi];
+      }
+      r.gfirst[3] = kMaxGMod;
+    }
   }
   // after all chunks: guard, then the gated DMMA recomputation
   cudaError_t epilogue(bool cplx) {
@@ -1398,8 +1547,8 @@ cudaError_t ozaki_preload() {
   return cudaSuccess;
 }
 
-void ozaki_params(int64_t K, int kind, int *nmod, int *t, const int **moduli, const int **roots) {
-  const OzPlan p = oz_plan(1, 1, K, (size_t)8 << 30, 0, kind);
+void ozaki_params(int64_t K, int kind, int *nmod, int *t, const int **moduli, const int **roots, int tmin) {
+  const OzPlan p = oz_plan(1, 1, K, (size_t)8 << 30, 0, kind, tmin);
   if (nmod) *nmod = p.nmod;
   if (t) *t = p.t;
   if (moduli) *moduli = kind == kOzGauss ? kGModuli : kModuli;
@@ -1407,21 +1556,25 @@ void ozaki_params(int64_t K, int kind, int *nmod, int *t, const int **moduli, co
 }
 
 size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K) {
-  // sized for the largest plane count of any kind (3M) so the kind can change
-  // without re-sizing
+  // sized for the largest plane count of any kind (3M, float64 sources) so
+  // the variant can change without re-sizing
   return std::max(oz_plan(M, N, K, (size_t)8 << 30, 0, kOz3M).total,
                   oz_plan(M, N, K, (size_t)8 << 30, 0, kOzGauss).total);
 }
 
-// C = A B (complex128) per GemmProblem strides, by Ozaki-II on INT8 tcgen05.
-cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
-                               int64_t *launches) {
+namespace {
+
+// C = A B (complex128, or complex64 with TS = TO = float2) per GemmProblem
+// strides, by Ozaki-II on INT8 tcgen05.
+template <class TS>
+cudaError_t ozaki_zgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s, int64_t *launches) {
   if (g.M == 0 || g.N == 0) return cudaSuccess;
   if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;   // int32 residue products would overflow
   const bool gauss = g.oz_gauss != 0;
-  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows, gauss ? kOzGauss : kOz3M);
+  const int tmin = std::is_same<TS, float2>::value ? kOzTminF32 : 46;
+  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows, gauss ? kOzGauss : kOz3M, tmin);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
-  OzRun<double2> R(g, p, ws, s, launches);
+  OzRun<TS> R(g, p, ws, s, launches);
   char *w = R.w;
   int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
   uint8_t *D = reinterpret_cast<uint8_t *>(w + p.off_D);
@@ -1431,15 +1584,15 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
     if (r.s_k == 1) {
       const unsigned blocks = (unsigned)((r.lines_out * (r.Kp / 8) + 255) / 256);
       if (gauss)
-        residues<true><<<blocks, 256, 0, s>>>(r);
+        residues<true, TS><<<blocks, 256, 0, s>>>(r);
       else
-        residues<false><<<blocks, 256, 0, s>>>(r);
+        residues<false, TS><<<blocks, 256, 0, s>>>(r);
     } else {
       const unsigned blocks = (unsigned)(((r.lines_out + 31) / 32) * (r.Kp / 64));
       if (gauss)
-        residues_t<true><<<blocks, 256, 0, s>>>(r);
+        residues_t<true, TS><<<blocks, 256, 0, s>>>(r);
       else
-        residues_t<false><<<blocks, 256, 0, s>>>(r);
+        residues_t<false, TS><<<blocks, 256, 0, s>>>(r);
     }
     R.count();
   };
@@ -1455,19 +1608,32 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
     double W[kMaxMod][4];
     crt_constants(p.nmod, W, c.Mch, c.Minv);
     for (int l = 0; l < kMaxMod; l++)
-      for (int j = 0; j < 4; j++) c.W[l][j] = W[l][j];
+      for (int j = 0; j < 4; j++) c.W[l][j] = c.WI[l][j] = W[l][j];
+  }
+  {
+    const double xs = gauss ? 512.0 : 1024.0;   // 2^XS of crt_kernel
+    for (int j = 0; j < 4; j++) {
+      double sr = 0.0, si = 0.0;
+      for (int l = 0; l < p.nmod; l++) {
+        sr += c.W[l][j];
+        si += c.WI[l][j];
+      }
+      c.Cr[j] = xs * sr;
+      c.Ci[j] = xs * si;
+    }
   }
   c.nmod = p.nmod; c.EA = R.EA; c.EB = R.EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
-  c.C = static_cast<double2 *>(g.C); c.c_sm = g.c_sm;
+  c.C = g.C; c.c_sm = g.c_sm;
   c.npeer = std::min(g.npeer, 7);
-  for (int pp = 0; pp < c.npeer; pp++) c.peer[pp] = static_cast<double2 *>(g.peer_C[pp]);
+  for (int pp = 0; pp < c.npeer; pp++) c.peer[pp] = g.peer_C[pp];
   c.rowsq = R.guard ? R.rowsq : nullptr;
   c.eb_max = R.misc + 2;
+  using TO = TS;
   for (int64_t ch = 0; ch < p.chunks; ch++) {
     const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
     if (g.rows_needed) {
       g.rows_needed(g.rows_user, m0, mc);
-      R.exponents(static_cast<const double2 *>(g.A) + m0 * g.a_sm, mc, g.a_sm, g.a_sk, R.EA + m0, +1);
+      R.exponents(static_cast<const TS *>(g.A) + m0 * g.a_sm, mc, g.a_sm, g.a_sk, R.EA + m0, +1);
     }
     {
       ResArgs r{};
@@ -1481,16 +1647,22 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
     cudaError_t ce;
     if (gauss) {
       switch (p.nmod) {
-        case 15: ce = launch_crt<15, 3, true>(c, mc, s); break;
-        case 16: ce = launch_crt<16, 3, true>(c, mc, s); break;
+        case 9: ce = launch_crt<9, 2, true, TO>(c, mc, s); break;
+        case 10: ce = launch_crt<10, 2, true, TO>(c, mc, s); break;
+        case 11: ce = launch_crt<11, 3, true, TO>(c, mc, s); break;
+        case 15: ce = launch_crt<15, 3, true, TO>(c, mc, s); break;
+        case 16: ce = launch_crt<16, 4, true, TO>(c, mc, s); break;
         default: return cudaErrorInvalidValue;
       }
     } else {
       switch (p.nmod) {
-        case 12: ce = launch_crt<12, 3>(c, mc, s); break;
-        case 13: ce = launch_crt<13, 3>(c, mc, s); break;
-        case 14: ce = launch_crt<14, 3>(c, mc, s); break;
-        case 15: ce = launch_crt<15, 4>(c, mc, s); break;
+        case 8: ce = launch_crt<8, 2, false, TO>(c, mc, s); break;
+        case 9: ce = launch_crt<9, 2, false, TO>(c, mc, s); break;
+        case 10: ce = launch_crt<10, 3, false, TO>(c, mc, s); break;
+        case 12: ce = launch_crt<12, 3, false, TO>(c, mc, s); break;
+        case 13: ce = launch_crt<13, 3, false, TO>(c, mc, s); break;
+        case 14: ce = launch_crt<14, 3, false, TO>(c, mc, s); break;
+        case 15: ce = launch_crt<15, 4, false, TO>(c, mc, s); break;
         default: return cudaErrorInvalidValue;
       }
     }
@@ -1501,16 +1673,17 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   return R.epilogue(true);
 }
 
-// C = A B (float64) per GemmProblem strides by real Ozaki-II on INT8 tcgen05
-// (layout of ozaki_workspace_bytes: sized for 3n planes, n used here).
-cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
-                               int64_t *launches) {
+// C = A B (float64, or float32 with TS = float) by real Ozaki-II on INT8
+// tcgen05 (layout of ozaki_workspace_bytes: sized for 3n planes, n used here).
+template <class TS>
+cudaError_t ozaki_dgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s, int64_t *launches) {
   if (g.M == 0 || g.N == 0) return cudaSuccess;
   if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;
   if (g.rows_needed) return cudaErrorInvalidValue;   // the real path takes all row exponents up front
-  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows, kOzReal);
+  const int tmin = std::is_same<TS, float>::value ? kOzTminF32 : 46;
+  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows, kOzReal, tmin);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
-  OzRun<double> R(g, p, ws, s, launches);
+  OzRun<TS> R(g, p, ws, s, launches);
   char *w = R.w;
   int8_t *Bres = reinterpret_cast<int8_t *>(w + p.off_Bres), *Ares = reinterpret_cast<int8_t *>(w + p.off_Ares);
   uint8_t *D = reinterpret_cast<uint8_t *>(w + p.off_D);
@@ -1518,9 +1691,9 @@ cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   auto launch_res = [&](const ResArgs &r) {
     if (r.s_k == 1) {
       const int64_t th = r.lines_out * (r.Kp / 8);
-      residues_real<<<(unsigned)((th + 255) / 256), 256, 0, s>>>(r);
+      residues_real<TS><<<(unsigned)((th + 255) / 256), 256, 0, s>>>(r);
     } else {
-      residues_real_t<<<(unsigned)(((r.lines_out + 31) / 32) * (r.Kp / 64)), 256, 0, s>>>(r);
+      residues_real_t<TS><<<(unsigned)(((r.lines_out + 31) / 32) * (r.Kp / 64)), 256, 0, s>>>(r);
     }
     R.count();
   };
@@ -1532,10 +1705,16 @@ cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
   }
   CrtArgsR c{};
   crt_constants(p.nmod, c.W, c.Mch, c.Minv);
+  for (int j = 0; j < 4; j++) {
+    double sw = 0.0;
+    for (int l = 0; l < p.nmod; l++) sw += c.W[l][j];
+    c.C0[j] = 256.0 * sw;
+  }
   c.nmod = p.nmod; c.EA = R.EA; c.EB = R.EB; c.t = p.t; c.N = g.N; c.Np = p.Np; c.D = D;
-  c.C = static_cast<double *>(g.C); c.c_sm = g.c_sm;
+  c.C = g.C; c.c_sm = g.c_sm;
   c.rowsq = R.guard ? R.rowsq : nullptr;
   c.eb_max = R.misc + 2;
+  using TO = TS;
   for (int64_t ch = 0; ch < p.chunks; ch++) {
     const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
     {
@@ -1549,16 +1728,33 @@ cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
     c.m0 = m0;
     const unsigned blocks = (unsigned)(mc * p.tpr);
     switch (p.nmod) {
-      case 12: crt_real_kernel<12, 3><<<blocks, 256, 0, s>>>(c); break;
-      case 13: crt_real_kernel<13, 3><<<blocks, 256, 0, s>>>(c); break;
-      case 14: crt_real_kernel<14, 3><<<blocks, 256, 0, s>>>(c); break;
-      case 15: crt_real_kernel<15, 4><<<blocks, 256, 0, s>>>(c); break;
+      case 8: crt_real_kernel<8, 2, TO><<<blocks, 256, 0, s>>>(c); break;
+      case 9: crt_real_kernel<9, 2, TO><<<blocks, 256, 0, s>>>(c); break;
+      case 10: crt_real_kernel<10, 3, TO><<<blocks, 256, 0, s>>>(c); break;
+      case 12: crt_real_kernel<12, 3, TO><<<blocks, 256, 0, s>>>(c); break;
+      case 13: crt_real_kernel<13, 3, TO><<<blocks, 256, 0, s>>>(c); break;
+      case 14: crt_real_kernel<14, 3, TO><<<blocks, 256, 0, s>>>(c); break;
+      case 15: crt_real_kernel<15, 4, TO><<<blocks, 256, 0, s>>>(c); break;
       default: return cudaErrorInvalidValue;
     }
     R.count();
     if (g.rows_done) g.rows_done(g.rows_user, m0, mc);
   }
   return R.epilogue(false);
+}
+
+}  // namespace
+
+cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
+                               int64_t *launches) {
+  return g.dtype == TCI_C64 ? ozaki_zgemm_impl<float2>(g, ws, ws_bytes, s, launches)
+                            : ozaki_zgemm_impl<double2>(g, ws, ws_bytes, s, launches);
+}
+
+cudaError_t launch_ozaki_dgemm(const GemmProblem &g, void *ws, size_t ws_bytes, cudaStream_t s,
+                               int64_t *launches) {
+  return g.dtype == TCI_R32 ? ozaki_dgemm_impl<float>(g, ws, ws_bytes, s, launches)
+                            : ozaki_dgemm_impl<double>(g, ws, ws_bytes, s, launches);
 }
 
 }  // namespace tci

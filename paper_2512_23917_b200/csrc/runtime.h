@@ -34,6 +34,7 @@ struct tci_ctx_s {
   std::unordered_map<std::string, std::vector<int64_t>> plan_cache;
   int64_t plan_hits, plan_misses;
   int zgemm_algo;       // complex128 GEMM algorithm (kZ3M default; tci_set_gemm_algorithm)
+  int f32_algo;         // float32 / complex64 GEMMs: TCI_F32_OZAKI_INT8 (default) or TCI_F32_FP64_CORES
   void *dev_scratch;    // reductions (vec.cu): allocated once at creation
   void *host_scratch;   // pinned, reduction results
   cudaStream_t copy_stream;   // library-owned (created on first use): staged H2D / D2H copies

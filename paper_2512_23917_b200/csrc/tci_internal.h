@@ -111,6 +111,9 @@ struct OzGuard {
   double max_est;                 // maximum over all since the last reset
 };
 constexpr double kOzakiDefaultTol = 1e-13;
+// the guard's tolerance for float32 / complex64 Ozaki GEMMs (R34: 100x under
+// the 1e-5 fp32 bar)
+constexpr double kOzakiF32Tol = 1e-7;
 // The DMMA path for p (complex 3M / float64), every CTA gated by *run_if
 // (gemm_dmma.cu): the Ozaki guard's recomputation
 cudaError_t launch_gemm_dmma_if(const GemmProblem &p, const int *run_if, cudaStream_t s, int64_t *launches);
@@ -138,7 +141,8 @@ cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t 
 // moduli count and integer bit budget chosen for a contraction length K;
 // kind 0 = float64, 1 = complex 3M, 2 = complex Gaussian (roots j_l with
 // j_l^2 = -1 mod m_l; null for the other kinds)
-void ozaki_params(int64_t K, int kind, int *nmod, int *t, const int **moduli, const int **roots);
+void ozaki_params(int64_t K, int kind, int *nmod, int *t, const int **moduli, const int **roots, int tmin = 46);
+constexpr int kOzakiTminF32 = 24;   // float32 / complex64 sources (R34; ozaki.cu kOzTminF32)
 
 
 // Output tile of the GEMM kernel used for `dtype` (for the planner's split-K choice).

@@ -378,6 +378,55 @@ def test_zipup_long_chain_heisenberg(ctx, oracle_mod):
     assert abs(got - ref) <= 1e-10 * abs(ref)
 
 
+@pytest.mark.parametrize("dt", ["r64", "c128"])
+def test_zipup_long_chain_truncating_gap(ctx, oracle_mod, dt):
+    """A TRUNCATING 40-site zip-up whose cuts are well separated (R32): psi is
+    right-canonical (chi = 8), the MPO is W = I + eps H (Heisenberg, eps =
+    1e-4; the last site closes both the identity and the Hamiltonian path),
+    so every carry T = C A_i W_i has chi values O(1) and 4 chi values O(eps):
+    chi_max = 8 cuts inside that gap. The truncated state is then unique up
+    to gauge: the GPU and oracle results have fidelity 1 to 1e-12, equal
+    norms and <psi|B> to 1e-11, and trunc_err (sum of discarded weights,
+    ~1e-8 here) agrees to 1e-6 relative."""
+    n, chi, eps = 40, 8, 1e-4
+    rng = np.random.default_rng(41)
+    cp = dt == "c128"
+    bonds = [1] + [min(chi, 2 ** min(i + 1, n - i - 1)) for i in range(n - 1)] + [1]
+
+    def r(*sh):
+        x = rng.uniform(-1, 1, sh)
+        return x + 1j * rng.uniform(-1, 1, sh) if cp else x
+    A = [r(bonds[i], 2, bonds[i + 1]) for i in range(n)]
+    for i in range(n - 1, 0, -1):          # right-canonical (QR from the right, input preparation)
+        a, _, c = A[i].shape
+        q, rr = np.linalg.qr(A[i].reshape(a, 2 * c).conj().T)
+        k = q.shape[1]
+        A[i] = q.conj().T.reshape(k, 2, c)
+        A[i - 1] = np.einsum("xsa,ak->xsk", A[i - 1], rr.conj().T)
+    A[0] /= np.linalg.norm(A[0])
+    Wh, lb, rb = synth.heisenberg_mpo(1.0)
+    Wh = np.asarray(Wh).real.copy()
+    Wh[lb, 1:4] *= eps                      # eps S.S couplings
+    Wh = Wh.astype(np.complex128) if cp else Wh
+    W = [Wh[lb:lb + 1]] + [Wh] * (n - 2) + [Wh[:, rb:rb + 1] + Wh[:, lb:lb + 1]]
+    B, err = ctx.mps_mpo_zipup([dev(x) for x in A], [dev(x) for x in W], chi)
+    RB, rerr = oracle_mod.mps_mpo_zipup(A, W, chi)
+    assert [tuple(b.shape) for b in B] == [b.shape for b in RB]
+    assert 1e-12 < rerr < 1e-4
+    assert abs(err - rerr) <= 1e-6 * rerr
+
+    def overlap(bra, ket):
+        E = np.ones((1, 1), dtype=np.complex128)
+        for x, y in zip(bra, ket):
+            E = np.einsum("xz,xsy,zsw->yw", E, np.conj(x), y)
+        return complex(E[0, 0])
+    Bh = [host(b) for b in B]
+    gg, oo, go = overlap(Bh, Bh), overlap(RB, RB), overlap(Bh, RB)
+    assert abs(abs(go) ** 2 / (gg.real * oo.real) - 1.0) <= 1e-12
+    assert abs(gg - oo) <= 1e-11 * abs(oo)
+    assert abs(overlap(A, Bh) - overlap(A, RB)) <= 1e-11 * abs(overlap(A, RB))
+
+
 def test_trunc_svd_tebd_theta_full_size(ctx, oracle_mod):
     """Config 3 at full size (chi = 2048, d = 2, f64): theta = A.B.U on the GPU
     (4096 x 4096), trunc_svd to chi_max = 2048 on the GPU. Checked against

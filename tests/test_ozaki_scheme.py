@@ -48,11 +48,15 @@ def _device_crt(residues, mods):
     Wc = np.array([[float((w >> (37 * j)) & mask) for j in range(nch)] for w in W])
     Mch = np.array([float((M >> (37 * j)) & mask) for j in range(nch)])
     assert all((M >> (37 * nch)) == 0 for _ in [0]) and all(w >> (37 * nch) == 0 for w in W)
-    S = np.zeros(nch)
+    # the kernel's encoding: each representative c < 2^10 enters as the double
+    # 1 + c 2^-10; T_j = sum_l (1 + c_l 2^-10) W_lj, S_j = 2^10 T_j - 2^10 sum_l W_lj
+    T = np.zeros(nch)
     S_int = [0] * nch
     for c, w in zip(residues, Wc):
-        S = S + float(c) * w
+        assert 0 <= c < 1024
+        T = T + (1.0 + float(c) / 1024.0) * w
         S_int = [s + c * int(x) for s, x in zip(S_int, w)]
+    S = T * 1024.0 - 1024.0 * Wc.sum(axis=0)
     assert [int(s) for s in S] == S_int and max(abs(s) for s in S_int) < 2 ** 53   # exact chunk sums
     two37 = float(2 ** 37)
     xe = S[nch - 1]
@@ -195,32 +199,45 @@ def test_params_complex_gaussian(K):
     assert 2 * K * 2 ** (2 * t) <= M // 4           # |Re C'|, |Im C'| <= 2 K 2^(2t) <= M/4
     assert K * (max(mods) // 2) ** 2 < 2 ** 31      # balanced int8 residues, exact int32 sums
     assert t >= 46
-    # 40-bit CRT chunks: 3 cover M, chunk sums of 16 terms < 482 * 2^40 stay exact
-    assert M < 2 ** 120 and 16 * 482 * 2 ** 40 < 2 ** 53
+    # 39-bit CRT chunks: 3 cover M for 15 moduli, 4 for 16; the encoded chunk
+    # sums sum_l W_l (512 + x_l) < 16 2^39 (512 + 482) stay exact in float64
+    assert M < 2 ** (39 * (3 if n <= 15 else 4)) and 16 * 2 ** 39 * (512 + 482) < 2 ** 53
 
 
 def _gauss_crt(xs, mods, weights):
-    """crt_value<3, 40> of the kernel on the representatives xs (numpy float64)."""
+    """crt_value<NCH, 39> of the kernel on the representatives xs (numpy
+    float64): 39-bit chunks, 3 for 15 moduli and 4 for 16; each x < 2^9
+    enters as the double 1 + x 2^-9 (crt_kernel's one_plus<9>)."""
     M = math.prod(mods)
-    mask, cb, nch = (1 << 40) - 1, 40, 3
+    cb = 39
+    nch = 3 if len(mods) <= 15 else 4
+    mask = (1 << cb) - 1
     Wc = np.array([[float((w >> (cb * j)) & mask) for j in range(nch)] for w in weights])
     Mch = np.array([float((M >> (cb * j)) & mask) for j in range(nch)])
     assert M >> (cb * nch) == 0
-    S = np.zeros(nch)
+    T = np.zeros(nch)
     S_int = [0] * nch
     for c, w in zip(xs, Wc):
-        S = S + float(c) * w
+        assert 0 <= c < 512
+        T = T + (1.0 + float(c) / 512.0) * w
         S_int = [s + c * int(x) for s, x in zip(S_int, w)]
+    assert all(float(t) * 512 == int(t * 512) for t in T)       # partial sums stay exact
+    S = T * 512.0 - 512.0 * Wc.sum(axis=0)
     assert [int(s) for s in S] == S_int and max(abs(s) for s in S_int) < 2 ** 53
     two = float(2 ** cb)
-    xe = S[2] * two * two + S[1] * two + S[0]
+    xe = S[nch - 1]
+    for j in range(nch - 2, -1, -1):
+        xe = xe * two + S[j]
     q = np.rint(xe * (1.0 / float(M)))
     r = S - q * Mch
     for j in range(nch - 1):
         cy = np.rint(r[j] / two)
         r[j] = r[j] - cy * two
         r[j + 1] = r[j + 1] + cy
-    return (r[2] * two + r[1]) * two + r[0]
+    x = r[nch - 1]
+    for j in range(nch - 2, -1, -1):
+        x = x * two + r[j]
+    return x
 
 
 def _gauss_weights(mods, roots):

@@ -540,7 +540,7 @@ __device__ __forceinline__ void elem_scales(const ResArgs &a, int E, int64_t k0,
 }
 
 template <bool G, class TS>
-__global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs a) {
+__global__ void __launch_bounds__(256, 2) residues(const __grid_constant__ ResArgs a) {
   constexpr int NV = 8;
   const int64_t kgroups = a.Kp / NV;
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(256) residues(const __grid_constant__ ResArgs 
 // lines (coalesced), turned into integers in shared memory and written along
 // k: eight threads write one line's 64 contiguous residue bytes per plane.
 template <bool G, class TS>
-__global__ void __launch_bounds__(256) residues_t(const __grid_constant__ ResArgs a) {
+__global__ void __launch_bounds__(256, 2) residues_t(const __grid_constant__ ResArgs a) {
   __shared__ double sx[2][32][65];
   const int64_t ntk = a.Kp / 64;
   const int64_t tl = blockIdx.x / ntk, tk = blockIdx.x % ntk;

@@ -643,7 +643,7 @@ def run_tci(args):
         "alt": alt,
         "data": "synthetic (seeded counter-based generator; exact model MPO as W1=W2)",
         "config": {"workload": name, "chi": chi, "d": d, "D": D, "dtype": dt, "model": cfg["model"],
-                   "gemm_algorithm": algo,
+                   "gemm_algorithm": algo, "gather": gather,
                    "parallelism": (f"output bond b sharded over {ws} rank(s); all-gather of out per step "
                                    + ("over peer memory fused into the GEMM4 epilogue (CUDA IPC, NVLink)"
                                       if gather == "p2p" else "by NCCL")) if ws > 1 else "single GPU",

@@ -112,6 +112,25 @@ TCI_API tci_status_t tci_destroy_context(tci_ctx_t ctx);
  * Errors: DEAD_CONTEXT, CUDA (including sticky asynchronous faults). */
 TCI_API tci_status_t tci_synchronize(tci_ctx_t ctx);
 
+/* CUDA-graph capture of a call sequence (host-path latency of short chains,
+ * e.g. config 1's 20 small contracts; PAPER.md:473 notes the per-call
+ * overhead at small bond dimensions). Between tci_graph_begin and
+ * tci_graph_end the calls on this context record their kernels into a CUDA
+ * graph (stream capture of the context stream, thread-local mode) instead
+ * of running them; tci_graph_launch replays the recorded kernels on the
+ * context stream with the same pointers and shapes (the caller keeps the
+ * tensors and the attached workspace alive and unchanged in size). Calls
+ * that synchronize or read results on the host (Lanczos, SVD, guard
+ * statistics, profiling, staged copies) fail inside a capture; so does a
+ * workspace that would need to grow. tci_graph_end always ends the capture.
+ * Errors: DEAD_CONTEXT, INVALID_ARGUMENT (NULL out / not capturing / already
+ * capturing), CUDA (an illegal call during capture invalidates it). */
+typedef struct tci_graph_s *tci_graph_t;
+TCI_API tci_status_t tci_graph_begin(tci_ctx_t ctx);
+TCI_API tci_status_t tci_graph_end(tci_ctx_t ctx, tci_graph_t *graph);
+TCI_API tci_status_t tci_graph_launch(tci_ctx_t ctx, tci_graph_t graph);
+TCI_API tci_status_t tci_graph_destroy(tci_graph_t graph);
+
 /* Thread-local message describing the last failed call on this thread
  * ("" if none). Static thread-local storage; valid until the next call. */
 TCI_API const char *tci_last_error(void);

@@ -54,6 +54,7 @@ EXPORTED = [
     "tci_gather_status", "tci_tebd_workspace_size", "tci_copy_async", "tci_lane_record", "tci_lane_wait",
     "tci_set_ozaki_guard", "tci_ozaki_guard_stats", "tci_ozaki_params_complex",
     "tci_set_ozaki_complex", "tci_set_f32_algorithm", "tci_ozaki_params_f32",
+    "tci_graph_begin", "tci_graph_end", "tci_graph_launch", "tci_graph_destroy",
 ]
 
 
@@ -126,6 +127,10 @@ _sig = {
     "tci_ozaki_params_complex": ([ctypes.c_int64, ctypes.c_int] + [ctypes.POINTER(ctypes.c_int)] * 5, ctypes.c_int),
     "tci_set_ozaki_complex": ([_vp, ctypes.c_int], ctypes.c_int),
     "tci_set_f32_algorithm": ([_vp, ctypes.c_int], ctypes.c_int),
+    "tci_graph_begin": ([_vp], ctypes.c_int),
+    "tci_graph_end": ([_vp, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "tci_graph_launch": ([_vp, _vp], ctypes.c_int),
+    "tci_graph_destroy": ([_vp], ctypes.c_int),
     "tci_ozaki_params_f32": ([ctypes.c_int64, ctypes.c_int] + [ctypes.POINTER(ctypes.c_int)] * 4, ctypes.c_int),
     "tci_get_gemm_algorithm": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "tci_set_ozaki_guard": ([_vp, ctypes.c_double], ctypes.c_int),
@@ -455,6 +460,24 @@ def tci_ozaki_params(K: int):
     mods = (ctypes.c_int * 16)()
     st = _lib.tci_ozaki_params(int(K), ctypes.byref(n), ctypes.byref(t), mods)
     return st, n.value, t.value, [mods[i] for i in range(n.value)]
+
+
+def tci_graph_begin(ctx: int) -> None:
+    _ok(_lib.tci_graph_begin(_vp(ctx)), "tci_graph_begin")
+
+
+def tci_graph_end(ctx: int) -> int:
+    g = ctypes.c_void_p()
+    _ok(_lib.tci_graph_end(_vp(ctx), ctypes.byref(g)), "tci_graph_end")
+    return g.value
+
+
+def tci_graph_launch(ctx: int, graph: int) -> None:
+    _ok(_lib.tci_graph_launch(_vp(ctx), _vp(graph)), "tci_graph_launch")
+
+
+def tci_graph_destroy(graph: int) -> None:
+    _ok(_lib.tci_graph_destroy(_vp(graph)), "tci_graph_destroy")
 
 
 TCI_F32_OZAKI_INT8 = 0
@@ -825,6 +848,26 @@ class Context:
 
     def set_f32_algorithm(self, algo: int):
         tci_set_f32_algorithm(self.handle, algo)
+
+    def capture(self, fn):
+        """Record the library calls fn() makes on this context into a CUDA
+        graph (tci_graph_begin / tci_graph_end) without running them; returns
+        (graph handle, fn's return value). Outputs must be preallocated
+        (out=...) and the workspace already large enough: run fn once eagerly
+        first. Replay with replay(graph); free with tci_graph_destroy."""
+        tci_graph_begin(self.handle)
+        try:
+            r = fn()
+        except BaseException:
+            try:
+                tci_graph_destroy(tci_graph_end(self.handle))
+            except TciError:
+                pass
+            raise
+        return tci_graph_end(self.handle), r
+
+    def replay(self, graph: int):
+        tci_graph_launch(self.handle, graph)
 
     def ozaki_guard_stats(self, reset: bool = False) -> dict:
         return tci_ozaki_guard_stats(self.handle, reset)

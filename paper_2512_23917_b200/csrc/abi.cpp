@@ -237,6 +237,7 @@ tci_status_t tci_create_context(tci_ctx_t *ctx, int device, void *stream) {
   for (int i = 0; i < 8; i++) c->g_full[i] = c->g_flags[i] = nullptr;
   c->g_epoch = 0;
   c->g_err = nullptr;
+  c->capturing = false;
   c->svd_last_sweeps = 0;
   c->svd_last_off = 0.0;
   c->oz_tol = kOzakiDefaultTol;
@@ -345,6 +346,67 @@ tci_status_t tci_destroy_context(tci_ctx_t ctx) {
   ctx->ws = nullptr;
   ctx->ws_bytes = 0;
   ctx->alive = false;   // handle kept (not freed) so later calls see DEAD_CONTEXT
+  return TCI_OK;
+}
+
+// ---- CUDA-graph capture (host-path latency of short chains) ----
+namespace {
+constexpr uint32_t kGraphMagic = 0x54434947u;   // "TCIG"
+int64_t g_capture_launch0[64];
+}  // namespace
+
+tci_status_t tci_graph_begin(tci_ctx_t ctx) {
+  CHECK(check_ctx(ctx));
+  if (ctx->capturing) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "graph capture already active on this context");
+  TCI_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  ctx->capturing = true;
+  g_capture_launch0[ctx->device & 63] = ctx->launches;
+  return TCI_OK;
+}
+
+tci_status_t tci_graph_end(tci_ctx_t ctx, tci_graph_t *graph) {
+  CHECK(check_ctx(ctx));
+  if (!ctx->capturing) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "no graph capture active on this context");
+  ctx->capturing = false;
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);   // always ends the capture
+  if (e != cudaSuccess || !g) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    TCI_FAIL(TCI_ERR_CUDA, "graph capture failed: %s (a call in the capture synchronized or read results)",
+             cudaGetErrorString(e));
+  }
+  if (!graph) {
+    cudaGraphDestroy(g);
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL graph out-pointer");
+  }
+  cudaGraphExec_t x = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&x, g, 0);
+  if (ei != cudaSuccess) {
+    cudaGraphDestroy(g);
+    TCI_FAIL(TCI_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ei));
+  }
+  auto *h = new tci_graph_s{kGraphMagic, g, x, ctx->launches - g_capture_launch0[ctx->device & 63]};
+  ctx->launches = g_capture_launch0[ctx->device & 63];   // nothing ran yet
+  *graph = h;
+  return TCI_OK;
+}
+
+tci_status_t tci_graph_launch(tci_ctx_t ctx, tci_graph_t graph) {
+  CHECK(check_ctx(ctx));
+  if (!graph || graph->magic != kGraphMagic) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "not a graph handle");
+  if (ctx->capturing) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "graph launch inside a capture");
+  TCI_CUDA_CHECK(cudaGraphLaunch(graph->exec, ctx->stream));
+  ctx->launches += graph->kernels;
+  return TCI_OK;
+}
+
+tci_status_t tci_graph_destroy(tci_graph_t graph) {
+  if (!graph || graph->magic != kGraphMagic) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "not a graph handle");
+  graph->magic = 0;
+  cudaGraphExecDestroy(graph->exec);
+  cudaGraphDestroy(graph->graph);
+  delete graph;
   return TCI_OK;
 }
 

@@ -513,15 +513,11 @@ cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t 
   }
   p.hintA = g_i8_hintA;
   p.hintB = g_i8_hintB;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(i8gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  {
+    cudaError_t e = ensure_smem_attr((const void *)i8gemm_kernel, kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms();
   const int64_t clusters = std::min<int64_t>(p.tiles, sms / 2);
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;

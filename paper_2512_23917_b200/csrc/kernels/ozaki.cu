@@ -919,13 +919,9 @@ cudaError_t launch_crt_cfg(const CrtArgs &c, int64_t mc, cudaStream_t s) {
   using Shape = CrtShape<CPT, THREADS, STAGES, G ? 2 : 3>;
   auto kern = crt_kernel<NMOD, NCH, CPT, THREADS, STAGES, G, TO>;
   const size_t smem = Shape::smem(NMOD);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr((const void *)kern, smem);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS + 32, smem);
-  if (e != cudaSuccess) return e;
+  const int sms = device_sms(), per_sm = occupancy_per_sm((const void *)kern, THREADS + 32, smem);
   const int64_t ntiles = mc * ((c.Np + Shape::kTW - 1) / Shape::kTW);
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)std::max(per_sm, 1) * sms);
   kern<<<grid, THREADS + 32, smem, s>>>(c);   // + the producer warp

@@ -608,7 +608,7 @@ cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launc
       auto k = permute_groups<ESZ, 1>;
       if (V == 4) k = permute_groups<ESZ, (VMAX >= 4 ? 4 : 1)>;
       else if (V == 2) k = permute_groups<ESZ, (VMAX >= 2 ? 2 : 1)>;
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e = ensure_smem_attr((const void *)k, smem);
       if (e != cudaSuccess) return e;
       const int64_t blocks = std::min<int64_t>(ga.ntiles, 148 * 8);
       k<<<(unsigned)blocks, 256, smem, s>>>(ga);

@@ -409,10 +409,9 @@ cudaError_t launch_dmma_knm(const SkinnyProblem &p, cudaStream_t s) {
   const size_t smem = (size_t)KS * NTL * 3 * 32 * 8 + 2 * (size_t)std::max(p.K, p.N) * TD * 16;
   const int64_t ntiles = p.nb[0] * p.nb[1] * ((p.nb[2] + TD - 1) / TD);
   auto k = skinny_dmma_kernel<KS, NTL, MT>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr((const void *)k, smem);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTH, smem);
+  const int per_sm = occupancy_per_sm((const void *)k, NTH, smem);
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)148 * std::max(1, per_sm));
   k<<<(unsigned)grid, NTH, smem, s>>>(p, ntiles);
   return cudaGetLastError();
@@ -454,10 +453,9 @@ cudaError_t launch_stream_npt(const SkinnyProblem &p, cudaStream_t s) {
   const size_t smem = (size_t)(NW * p.K * p.N + (NW * p.K * p.N) % 2) * 8 + 2 * (size_t)p.K * TBS * es;
   const int64_t ntiles = p.nb[0] * p.nb[1] * ((p.nb[2] + TBS - 1) / TBS);
   auto k = (p.N == NPT * NG) ? skinny_stream_kernel<CPLX, NPT, true> : skinny_stream_kernel<CPLX, NPT, false>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr((const void *)k, smem);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTH, smem);
+  const int per_sm = occupancy_per_sm((const void *)k, NTH, smem);
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)148 * std::max(1, per_sm));
   k<<<(unsigned)grid, NTH, smem, s>>>(p, ntiles);
   return cudaGetLastError();
@@ -483,7 +481,7 @@ cudaError_t launch_stream(const SkinnyProblem &p, cudaStream_t s) {
 template <bool CPLX, int NPT>
 cudaError_t launch_npt(const SkinnyProblem &p, size_t smem, int64_t blocks, cudaStream_t s) {
   auto k = skinny_kernel<CPLX, NPT>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr((const void *)k, smem);
   if (e != cudaSuccess) return e;
   k<<<(unsigned)blocks, NTH, smem, s>>>(p);
   return cudaGetLastError();

@@ -51,8 +51,16 @@ struct tci_ctx_s {
   double oz_tol;
   tci::OzGuard *oz_guard;
   int oz_gauss;         // complex Ozaki variant: 1 Gaussian moduli (R33), 0 3M
+  bool capturing;       // between tci_graph_begin and tci_graph_end
   int svd_last_sweeps;  // Jacobi sweeps of the last svd / trunc_svd (tci_svd_info)
   double svd_last_off;  // its final off-diagonal measure
+};
+
+struct tci_graph_s {
+  uint32_t magic;
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  int64_t kernels;      // kernels recorded (added to the context's launch count per replay)
 };
 
 struct tci_tensor_s {

@@ -10,6 +10,14 @@
 
 namespace tci {
 
+// Host-side launch-attribute caches (launch_cache.cpp): the dynamic shared
+// memory opt-in of a kernel (set only when `bytes` exceeds what was set for
+// that kernel on this device), blocks per SM from the occupancy calculator,
+// and the SM count -- answered from tables after the first call.
+cudaError_t ensure_smem_attr(const void *fn, size_t bytes);
+int occupancy_per_sm(const void *fn, int threads, size_t smem);
+int device_sms();
+
 constexpr int kMaxOrder = TCI_MAX_ORDER;
 
 inline size_t dtype_size(tci_dtype_t t) {

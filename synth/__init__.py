@@ -183,8 +183,9 @@ def hubbard_mpo(t: float = 1.0, U: float = 4.0):
     return mpo_from_operator_matrix(ops), 5, 0
 
 
-def tfim_gate(tau: float, J: float = 1.0, g: float = 1.0) -> np.ndarray:
-    """U[p,q,s,t] = expm(-tau h)[(p q),(s t)], h = -J Z(x)Z + (g/2)(X(x)I + I(x)X).
+def tfim_gate(tau: float, J: float = 1.0, g: float = 1.0, real_time: bool = False) -> np.ndarray:
+    """U[p,q,s,t] = expm(-tau h)[(p q),(s t)], h = -J Z(x)Z + (g/2)(X(x)I + I(x)X);
+    real_time: the unitary expm(-i tau h) (complex128) of real-time TEBD.
 
     PAPER.md:394-397 (Eq. of the 1D TFIM, Application A); the field split in
     halves over the two bond sublattices as in SPEC.md:587-595. Built by
@@ -195,9 +196,9 @@ def tfim_gate(tau: float, J: float = 1.0, g: float = 1.0) -> np.ndarray:
     I = np.eye(2)
     h = -J * np.kron(Zm, Zm) + 0.5 * g * (np.kron(X, I) + np.kron(I, X))
     w, v = np.linalg.eigh(h)
-    Um = (v * np.exp(-tau * w)) @ v.T
+    Um = (v * np.exp((-1j if real_time else -1.0) * tau * w)) @ v.T
     if tau == 0.0:
-        Um = np.eye(4)
+        Um = np.eye(4, dtype=Um.dtype)
     return Um.reshape(2, 2, 2, 2)
 
 
@@ -282,13 +283,14 @@ TEBD_CONFIG = dict(chi=2048, d=2, dtype="r64", seed=4, tau=0.01, J=1.0, g=1.0)
 
 def tebd_inputs(chi: int, d: int, dtype: str, seed: int, tau: float, J=1.0, g=1.0,
                 device="cpu", physical_first: bool = False):
-    """A[a,s,b], B[b,t,c] uniform; U = TFIM gate. Variant (ii) stores A as
-    [s,a,b] and B as [t,b,c] (physical-first)."""
+    """A[a,s,b], B[b,t,c] uniform; U = TFIM gate (complex dtypes: the
+    real-time unitary expm(-i tau h)). Variant (ii) stores A as [s,a,b] and B
+    as [t,b,c] (physical-first)."""
     shA = (d, chi, chi) if physical_first else (chi, d, chi)
     shB = (d, chi, chi) if physical_first else (chi, d, chi)
     A = random_tensor(shA, dtype, seed, TID["A"], device)
     B = random_tensor(shB, dtype, seed, TID["B"], device)
-    U = torch.from_numpy(tfim_gate(tau, J, g)).to(TORCH_DTYPE[dtype]).to(device)
+    U = torch.from_numpy(tfim_gate(tau, J, g, real_time=dtype in ("c64", "c128"))).to(TORCH_DTYPE[dtype]).to(device)
     return dict(A=A, B=B, U=U)
 
 
@@ -331,3 +333,36 @@ def vidal_tebd_inputs(chi: int, d: int, seed: int, tau: float, smallest: float =
     U = tfim_gate(tau)
     return dict(A=torch.from_numpy(np.ascontiguousarray(A)), B=torch.from_numpy(np.ascontiguousarray(B)),
                 U=torch.from_numpy(U).to(TORCH_DTYPE[dtype]), lam_a=lam_a, lam_b=lam_b)
+
+
+# ----------------------------------------------------------------------------
+# config 5: random contraction instances
+# ----------------------------------------------------------------------------
+
+SWEEP_DIMS = [1, 2, 3, 5, 7, 8, 16, 37, 64, 128, 256]
+
+
+def sweep_instance(rng, max_elems: int = 2 ** 28, rank_min: int = 3, rank_max: int = 6):
+    """One random pairwise contraction (labels and dims only, no data):
+    orders r_A, r_B in [rank_min, rank_max], 1 <= #contracted < min(r_A, r_B),
+    dims from SWEEP_DIMS, random label permutations of A, B and the output;
+    the largest dim is halved until every tensor has <= max_elems elements.
+    Returns (la, lb, lc, dims, shared_labels)."""
+    import string
+    ra, rb = int(rng.integers(rank_min, rank_max + 1)), int(rng.integers(rank_min, rank_max + 1))
+    nc = int(rng.integers(1, min(ra, rb)))
+    letters = list(string.ascii_letters)
+    rng.shuffle(letters)
+    sh, fa, fb = letters[:nc], letters[nc:ra], letters[ra:ra + rb - nc]
+    la, lb, lc = sh + fa, sh + fb, fa + fb
+    rng.shuffle(la)
+    rng.shuffle(lb)
+    rng.shuffle(lc)
+    dims = {l: int(rng.choice(SWEEP_DIMS)) for l in la + lb}
+
+    def size(ls):
+        return int(np.prod([dims[l] for l in ls], dtype=np.int64))
+    while max(size(la), size(lb), size(lc)) > max_elems:
+        big = max(dims, key=dims.get)
+        dims[big] = max(1, dims[big] // 2)
+    return "".join(la), "".join(lb), "".join(lc), dims, "".join(sh)

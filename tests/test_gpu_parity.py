@@ -428,6 +428,28 @@ def test_tebd_theta(ctx, oracle_mod, chi, layout):
     assert rel_frob(host(th), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("chi", [1, 33, 130, 1030])
+@pytest.mark.parametrize("layout", ["natural", "physical_first"])
+def test_tebd_theta_complex_real_time(ctx, ozctx, oracle_mod, chi, layout):
+    """complex128 theta with the real-time gate expm(-i tau h) (Application
+    A's real-time evolution; K = C): A.B on
+    the complex GEMM path (DMMA 3M; and Ozaki at chi = 1030, 4.4e9 MACs) and
+    the gate as the skinny pass, both layouts, vs the oracle <= 1e-12."""
+    pf = layout == "physical_first"
+    inp = synth.tebd_inputs(chi, 2, "c128", 420 + chi, 0.05, physical_first=pf)
+    la, lb, lt = ("sab", "tbc", "paqc") if pf else ("asb", "btc", "apqc")
+    assert inp["U"].dtype == torch.complex128
+    A = inp["A"].numpy()
+    rows = list(range(chi)) if chi < 1024 else [0, 1, chi // 2, chi - 1]     # a-leg rows the oracle forms
+    As = A[:, rows] if pf else A[rows]
+    ref = oracle_mod.tebd_theta(np.ascontiguousarray(As), inp["B"].numpy(), inp["U"].numpy(), la=la, lb=lb,
+                                lu="pqst", lt=lt)
+    for c in ((ctx, ozctx) if chi >= 1024 else (ctx,)):
+        th = host(c.tebd_theta(dev(inp["A"]), la, dev(inp["B"]), lb, dev(inp["U"]), "pqst", lt))
+        got = th[:, rows] if pf else th[rows]          # theta[p,a,q,c] / theta[a,p,q,c]
+        assert rel_frob(got, ref) <= 1e-12
+
+
 def test_tebd_identity_gate_equals_AB_bitwise(ctx):
     inp = synth.tebd_inputs(64, 2, "r64", 410, 0.0)
     A, B = dev(inp["A"]), dev(inp["B"])
@@ -465,6 +487,52 @@ def test_mps_norm_cfg1(ctx, oracle_mod):
     assert rel_frob(host(_gpu_overlap(ctx, phi, psi)), oracle_mod.mps_overlap(phi, psi)) <= 1e-12
     prod = synth.product_state_sites(10)
     assert host(_gpu_overlap(ctx, prod, prod))[0, 0] == 1.0
+
+
+def test_graph_capture_cfg1_chain(oracle_mod):
+    """Config 1's 20-contract transfer chain recorded into a CUDA graph
+    (tci_graph_begin / end) and replayed: bitwise equal to the eager chain,
+    the oracle's norm within 1e-12, the graph's kernel count charged per
+    replay, and an illegal call inside a capture (a host read) reported as an
+    error without leaving the context capturing."""
+    s = torch.cuda.Stream()
+    c = tci.Context(0, s)
+    try:
+        psi = [dev(a) for a in synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1)]
+        E0 = torch.ones(1, 1, dtype=torch.float64, device="cuda")
+        bufs = {}
+
+        def chain():
+            E = E0
+            for i, A in enumerate(psi):
+                X = c.contract(E, "xz", A, "xsy", "zsy", out=bufs.get(("X", i)))
+                bufs[("X", i)] = X
+                E = c.contract(X, "zsy", A, "zsw", "yw", out=bufs.get(("E", i)))
+                bufs[("E", i)] = E
+            return E
+        eager = chain().clone()            # allocates the outputs, sizes the workspace
+        torch.cuda.synchronize()
+        out = bufs[("E", len(psi) - 1)]
+        out.zero_()
+        torch.cuda.synchronize()
+        n0 = c.launch_count()
+        g, _ = c.capture(chain)
+        assert c.launch_count() == n0 and out.abs().max().item() == 0.0     # recorded, not run
+        for _ in range(3):
+            c.replay(g)
+        c.synchronize()
+        assert torch.equal(out, eager)
+        dn = c.launch_count() - n0
+        assert dn >= 3 * 20 and dn % 3 == 0
+        ref = oracle_mod.mps_norm2(synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1))
+        assert rel_frob(host(out), ref) <= 1e-12
+        tci.tci_graph_destroy(g)
+        # a synchronizing call inside a capture fails, and the capture is over afterwards
+        with pytest.raises(tci.TciError):
+            c.capture(lambda: c.ozaki_guard_stats())
+        assert torch.equal(chain(), eager)
+    finally:
+        c.close()
 
 
 def test_mps_overlap_single_kernel(ctx, oracle_mod):
@@ -1015,3 +1083,80 @@ def test_ozaki_real_heff(ctx, ozctx, oracle_mod):
     want = oracle_mod.heff_rows(n["L"], n["W1"], n["W2"], n["R"], n["psi"], rows)
     assert rel_frob(host(got)[rows], want) <= 1e-12
     assert torch.equal(got, ozctx.heff_apply(d["L"], d["W1"], d["W2"], d["R"], d["psi"]))
+
+
+# ---------------------------------------------------------------------------
+# Config 5 at full size
+# ---------------------------------------------------------------------------
+
+def _sampled_check(A, la, B, lb, C, lc, sh, dims, oracle_mod, tol, rng, nsamp=64):
+    """Sampled parity of C = contract(A, B) (host arrays): 64 coordinates of
+    A's free legs x 64 of B's (4096 output elements, each set containing the
+    first and last index of every free leg: the leg boundaries) recomputed by
+    the oracle from the sliced operands; plus a host-side Freivalds check
+    C . x = A . (B . x) for a random x over B's free legs."""
+    fa = [l for l in la if l not in sh]
+    fb = [l for l in lb if l not in sh]
+
+    def coords(legs):
+        n = nsamp
+        cs = [{l: int(rng.integers(0, dims[l])) for l in legs} for _ in range(n)]
+        cs[0] = {l: 0 for l in legs}
+        cs[1] = {l: dims[l] - 1 for l in legs}
+        for k, l in enumerate(legs):                       # each leg's boundaries alone
+            if 2 + 2 * k + 1 < n:
+                cs[2 + 2 * k][l] = 0
+                cs[3 + 2 * k][l] = dims[l] - 1
+        return cs
+    ca, cb = coords(fa), coords(fb)
+    # A sliced at the sampled free coordinates -> [64, S...] in sh order
+    At = np.transpose(A, [la.index(l) for l in fa + list(sh)])
+    Bt = np.transpose(B, [lb.index(l) for l in list(sh) + fb])
+    Afree = At.reshape(int(np.prod([dims[l] for l in fa], dtype=np.int64)) if fa else 1, -1)
+    Bfree = Bt.reshape(-1, int(np.prod([dims[l] for l in fb], dtype=np.int64)) if fb else 1)
+
+    def flat(c, legs):
+        i = 0
+        for l in legs:
+            i = i * dims[l] + c[l]
+        return i
+    ia = [flat(c, fa) for c in ca]
+    ib = [flat(c, fb) for c in cb]
+    ref = oracle_mod.contract(np.ascontiguousarray(Afree[ia]), "ms", np.ascontiguousarray(Bfree[:, ib]), "sn", "mn")
+    Ct = np.transpose(C, [lc.index(l) for l in fa + fb]).reshape(Afree.shape[0], Bfree.shape[1])
+    got = Ct[np.ix_(ia, ib)]
+    assert rel_frob(got, ref) <= tol
+    # Freivalds, projected on the host: (C x) vs A (B x); the oracle forms B x and A (B x)
+    x = rng.uniform(-1, 1, Bfree.shape[1]).astype(C.dtype)
+    Cx = Ct.astype(np.float64) @ x.astype(np.float64)      # float64 projection of the GPU result
+    Bx = oracle_mod.contract(np.ascontiguousarray(Bfree), "sn", x, "n", "s")
+    ABx = oracle_mod.contract(np.ascontiguousarray(Afree), "ms", Bx, "s", "m")
+    assert rel_frob(Cx, ABx) <= tol
+
+
+@pytest.mark.parametrize("dt", ["r64", "r32"])
+def test_contract_sweep_cfg5_full_size(ctx, oracle_mod, dt):
+    """Random rank 3..6 contractions with tensors up to 2^26 elements (>= 1e7
+    for most instances) in the layout mix of config 5: full oracle comparison
+    when |C| |S| <= 2e8 MACs, otherwise 4096 sampled output elements
+    (including every leg boundary) + a host-side Freivalds projection.
+    Tolerance: 1e-12 (f64), 1e-5 (f32) relative Frobenius."""
+    rng = np.random.default_rng(55 if dt == "r64" else 56)
+    tol = TOL[dt]
+    big = 0
+    for i in range(14):
+        la, lb, lc, dims, sh = synth.sweep_instance(rng, max_elems=2 ** 26, rank_min=4 if i % 2 else 3)
+        A = synth.random_tensor([dims[l] for l in la], dt, 7000 + i, 1)
+        B = synth.random_tensor([dims[l] for l in lb], dt, 7000 + i, 2)
+        C = host(ctx.contract(dev(A), la, dev(B), lb, lc))
+
+        def size(ls):
+            return int(np.prod([dims[l] for l in ls], dtype=np.int64))
+        big += max(size(la), size(lb), size(lc)) >= 10 ** 7
+        if size(lc) * size(sh) <= 2 * 10 ** 8:
+            ref = oracle_mod.contract(A.numpy(), la, B.numpy(), lb, lc)
+            assert rel_frob(C, ref) <= tol, (la, lb, lc, dims)
+        else:
+            _sampled_check(A.numpy(), la, B.numpy(), lb, C, lc, sh, dims, oracle_mod, tol, rng)
+        del A, B, C
+    assert big >= 5

@@ -215,8 +215,6 @@ def test_tebd_step_theta_then_trunc_svd(ctx, oracle_mod, dt):
     """One TEBD bond update (Application A): theta = A.B.U on the
     GPU, then trunc_svd back to chi; compared with the oracle's
     theta and trunc_svd. Gate = TFIM expm(-tau h) (R25)."""
-    if dt == "c128":
-        pytest.skip("tebd_theta is real (float64) in this build")
     chi = 40
     inp = synth.tebd_inputs(chi, 2, dt, 4, 0.01)
     A, B, U = (inp[k] for k in ("A", "B", "U"))

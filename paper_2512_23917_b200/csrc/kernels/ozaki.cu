@@ -61,6 +61,10 @@ constexpr int kGModuli[kMaxGMod] = {241, 233, 229, 221, 205, 197, 193, 181, 173,
 constexpr int kGRoots[kMaxGMod] = {64, 89, 107, 21, 32, 14, 81, 19, 80, 28, 44, 37, 15, 33, 10, 22};
 __constant__ int c_gmod[kMaxGMod] = {241, 233, 229, 221, 205, 197, 193, 181, 173, 157, 149, 137, 113, 109, 101, 97};
 __constant__ int c_groot[kMaxGMod] = {64, 89, 107, 21, 32, 14, 81, 19, 80, 28, 44, 37, 15, 33, 10, 22};
+// negated moduli and roots (so every integer step of gauss_planes is one IMAD)
+__constant__ int c_gnmod[kMaxGMod] = {-241, -233, -229, -221, -205, -197, -193, -181, -173, -157, -149, -137, -113, -109, -101, -97};
+__constant__ int c_gnroot[kMaxGMod] = {-64, -89, -107, -21, -32, -14, -81, -19, -80, -28, -44, -37, -15, -33, -10, -22};
+__constant__ double c_grootd[kMaxGMod] = {64, 89, 107, 21, 32, 14, 81, 19, 80, 28, 44, 37, 15, 33, 10, 22};
 __constant__ double c_gminv[kMaxGMod] = {1.0 / 241, 1.0 / 233, 1.0 / 229, 1.0 / 221, 1.0 / 205, 1.0 / 197,
                                          1.0 / 193, 1.0 / 181, 1.0 / 173, 1.0 / 157, 1.0 / 149, 1.0 / 137,
                                          1.0 / 113, 1.0 / 109, 1.0 / 101, 1.0 / 97};
@@ -494,12 +498,13 @@ struct ResArgs {
 // 2 DFMA + 5 integer ops per modulus and value instead of 2 full reductions of
 // re and im plus two small ones (the kernel was instruction-issue bound).
 __device__ __forceinline__ void gauss_planes(const ResVals<8> &v, const ResArgs &a, int8_t *dst) {
+  const int64_t ps2 = 2 * a.plane_stride;
 #pragma unroll 1
   for (int g = 0; g < 3; g++) {
     const int l0 = a.gfirst[g], l1 = min(a.gfirst[g + 1], a.nmod);
     if (l0 >= l1) break;
     const double P = a.gP[g], Pinv = a.gPinv[g];
-    const int Plo = a.gPlo[g];
+    const int nPlo = -a.gPlo[g];
     double rp[8], ip[8];
     int lr[8], li[8];
 #pragma unroll
@@ -507,24 +512,24 @@ __device__ __forceinline__ void gauss_planes(const ResVals<8> &v, const ResArgs 
       const double mr = fma(v.x[0][j], Pinv, kMagic), mi = fma(v.x[1][j], Pinv, kMagic);
       rp[j] = fma(kMagic - mr, P, v.x[0][j]);   // x - q P, q = mr - kMagic (exact)
       ip[j] = fma(kMagic - mi, P, v.x[1][j]);
-      lr[j] = v.lo[0][j] - __double2loint(mr) * Plo;
-      li[j] = v.lo[1][j] - __double2loint(mi) * Plo;
+      lr[j] = __double2loint(mr) * nPlo + v.lo[0][j];
+      li[j] = __double2loint(mi) * nPlo + v.lo[1][j];
     }
+    int8_t *du = dst + l0 * ps2;
 #pragma unroll 1
-    for (int l = l0; l < l1; l++) {
-      const int mi = c_gmod[l], jr = c_groot[l];
-      const double minv = c_gminv[l], jd = (double)c_groot[l];
+    for (int l = l0; l < l1; l++, du += ps2) {
+      // every integer step one IMAD: lo(x_u) = li j + lr, r = q (-m) + lo(x_u)
+      const int nm = c_gnmod[l], jr = c_groot[l], njr = c_gnroot[l];
+      const double minv = c_gminv[l], jd = c_grootd[l];
       int u[8], d[8];
 #pragma unroll
       for (int j = 0; j < 8; j++) {
         const double xu = fma(jd, ip[j], rp[j]), xd = fma(-jd, ip[j], rp[j]);
-        const int tj = jr * li[j];
-        u[j] = (lr[j] + tj) - __double2loint(fma(xu, minv, kMagic)) * mi;
-        d[j] = (lr[j] - tj) - __double2loint(fma(xd, minv, kMagic)) * mi;
+        u[j] = __double2loint(fma(xu, minv, kMagic)) * nm + (li[j] * jr + lr[j]);
+        d[j] = __double2loint(fma(xd, minv, kMagic)) * nm + (li[j] * njr + lr[j]);
       }
-      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 2) * a.plane_stride) =
-          make_uint2(pack4(u[0], u[1], u[2], u[3]), pack4(u[4], u[5], u[6], u[7]));
-      *reinterpret_cast<uint2 *>(dst + (int64_t)(l * 2 + 1) * a.plane_stride) =
+      *reinterpret_cast<uint2 *>(du) = make_uint2(pack4(u[0], u[1], u[2], u[3]), pack4(u[4], u[5], u[6], u[7]));
+      *reinterpret_cast<uint2 *>(du + a.plane_stride) =
           make_uint2(pack4(d[0], d[1], d[2], d[3]), pack4(d[4], d[5], d[6], d[7]));
     }
   }

@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "../tci_internal.h"
@@ -505,6 +506,12 @@ cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t 
   p.tiles = (int64_t)L * p.tiles_m * p.tiles_n;
   p.D = D;
   p.counter = counter;
+  static const bool env_read = [] {   // tuning overrides: TCI_I8_RES_MB, TCI_I8_RASTER
+    if (const char *e = getenv("TCI_I8_RES_MB")) g_i8_res_mb = atoi(e) > 0 ? atoi(e) : g_i8_res_mb;
+    if (const char *e = getenv("TCI_I8_RASTER")) g_i8_raster = atoi(e);
+    return true;
+  }();
+  (void)env_read;
   p.a_resident = g_i8_raster >= 0 ? g_i8_raster : (M <= N ? 1 : 0);   // the smaller panel set stays in L2
   {
     const int nres = p.a_resident ? p.tiles_m : p.tiles_n;

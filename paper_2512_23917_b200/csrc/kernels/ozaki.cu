@@ -497,7 +497,9 @@ struct ResArgs {
 // (the quotient) and one IMAD on the low words (lo(x_u) = lo(r_re) + j lo(r_im)).
 // 2 DFMA + 5 integer ops per modulus and value instead of 2 full reductions of
 // re and im plus two small ones (the kernel was instruction-issue bound).
-__device__ __forceinline__ void gauss_planes(const ResVals<8> &v, const ResArgs &a, int8_t *dst) {
+template <int NV>
+__device__ __forceinline__ void gauss_planes(const ResVals<NV> &v, const ResArgs &a, int8_t *dst) {
+  static_assert(NV == 4 || NV == 8, "4 or 8 values per thread");
   const int64_t ps2 = 2 * a.plane_stride;
 #pragma unroll 1
   for (int g = 0; g < 3; g++) {
@@ -505,10 +507,10 @@ __device__ __forceinline__ void gauss_planes(const ResVals<8> &v, const ResArgs 
     if (l0 >= l1) break;
     const double P = a.gP[g], Pinv = a.gPinv[g];
     const int nPlo = -a.gPlo[g];
-    double rp[8], ip[8];
-    int lr[8], li[8];
+    double rp[NV], ip[NV];
+    int lr[NV], li[NV];
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
+    for (int j = 0; j < NV; j++) {
       const double mr = fma(v.x[0][j], Pinv, kMagic), mi = fma(v.x[1][j], Pinv, kMagic);
       rp[j] = fma(kMagic - mr, P, v.x[0][j]);   // x - q P, q = mr - kMagic (exact)
       ip[j] = fma(kMagic - mi, P, v.x[1][j]);
@@ -521,32 +523,42 @@ __device__ __forceinline__ void gauss_planes(const ResVals<8> &v, const ResArgs 
       // every integer step one IMAD: lo(x_u) = li j + lr, r = q (-m) + lo(x_u)
       const int nm = c_gnmod[l], jr = c_groot[l], njr = c_gnroot[l];
       const double minv = c_gminv[l], jd = c_grootd[l];
-      int u[8], d[8];
+      int u[NV], d[NV];
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
+      for (int j = 0; j < NV; j++) {
         const double xu = fma(jd, ip[j], rp[j]), xd = fma(-jd, ip[j], rp[j]);
         u[j] = __double2loint(fma(xu, minv, kMagic)) * nm + (li[j] * jr + lr[j]);
         d[j] = __double2loint(fma(xd, minv, kMagic)) * nm + (li[j] * njr + lr[j]);
       }
-      *reinterpret_cast<uint2 *>(du) = make_uint2(pack4(u[0], u[1], u[2], u[3]), pack4(u[4], u[5], u[6], u[7]));
-      *reinterpret_cast<uint2 *>(du + a.plane_stride) =
-          make_uint2(pack4(d[0], d[1], d[2], d[3]), pack4(d[4], d[5], d[6], d[7]));
+      if constexpr (NV == 8) {
+        *reinterpret_cast<uint2 *>(du) = make_uint2(pack4(u[0], u[1], u[2], u[3]), pack4(u[4], u[5], u[6], u[7]));
+        *reinterpret_cast<uint2 *>(du + a.plane_stride) =
+            make_uint2(pack4(d[0], d[1], d[2], d[3]), pack4(d[4], d[5], d[6], d[7]));
+      } else {
+        *reinterpret_cast<uint32_t *>(du) = pack4(u[0], u[1], u[2], u[3]);
+        *reinterpret_cast<uint32_t *>(du + a.plane_stride) = pack4(d[0], d[1], d[2], d[3]);
+      }
     }
   }
 }
 
 // per-element scale factors of 8 consecutive k (SK has Kp >= k0 + 8 entries)
-__device__ __forceinline__ void elem_scales(const ResArgs &a, int E, int64_t k0, double (&fa)[8], double (&fb)[8]) {
-  const int4 q0 = *reinterpret_cast<const int4 *>(a.SK + k0);
-  const int4 q1 = *reinterpret_cast<const int4 *>(a.SK + k0 + 4);
-  const int s[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+template <int NV = 8>
+__device__ __forceinline__ void elem_scales(const ResArgs &a, int E, int64_t k0, double (&fa)[NV], double (&fb)[NV]) {
 #pragma unroll
-  for (int j = 0; j < 8; j++) scale_pair(a.t - E + a.sgn * s[j], fa[j], fb[j]);
+  for (int h = 0; h < NV / 4; h++) {
+    const int4 q = *reinterpret_cast<const int4 *>(a.SK + k0 + 4 * h);
+    const int s[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) scale_pair(a.t - E + a.sgn * s[j], fa[4 * h + j], fb[4 * h + j]);
+  }
 }
 
 template <bool G, class TS>
-__global__ void __launch_bounds__(256, 2) residues(const __grid_constant__ ResArgs a) {
-  constexpr int NV = 8;
+__global__ void __launch_bounds__(256, G ? 3 : 2) residues(const __grid_constant__ ResArgs a) {
+  // Gaussian: 4 values per thread (more warps in flight: the kernel waits on
+  // its loads), 4-byte stores per plane (a warp still writes 128 contiguous B)
+  constexpr int NV = G ? 4 : 8;
   const int64_t kgroups = a.Kp / NV;
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (gid >= a.lines_out * kgroups) return;
@@ -562,14 +574,21 @@ __global__ void __launch_bounds__(256, 2) residues(const __grid_constant__ ResAr
     for (int j = 0; j < NV; j++) v[j] = k0 + j < a.K ? ld_c(p + (k0 + j) * a.s_k) : make_double2(0.0, 0.0);
     if (a.SK && *a.bal) {
       double fa[NV], fb[NV];
-      elem_scales(a, a.E[line], k0, fa, fb);
+      elem_scales<NV>(a, a.E[line], k0, fa, fb);
 #pragma unroll
       for (int j = 0; j < NV; j++) x.set(j, scaled_magic(v[j].x, fa[j], fb[j]), scaled_magic(v[j].y, fa[j], fb[j]));
     } else {
-      double s2a, s2b;
-      line_scale(a.t, a.E[line], s2a, s2b);
+      const int sc = a.t - a.E[line];
+      if (sc >= -1022 && sc <= 1023) {   // 2^sc normal: one DFMA per component (v 2^sc exact)
+        const double f = pow2i(sc);
 #pragma unroll
-      for (int j = 0; j < NV; j++) x.set(j, scaled_magic(v[j].x, s2a, s2b), scaled_magic(v[j].y, s2a, s2b));
+        for (int j = 0; j < NV; j++) x.set(j, fma(v[j].x, f, kMagic), fma(v[j].y, f, kMagic));
+      } else {
+        double s2a, s2b;
+        line_scale(a.t, a.E[line], s2a, s2b);
+#pragma unroll
+        for (int j = 0; j < NV; j++) x.set(j, scaled_magic(v[j].x, s2a, s2b), scaled_magic(v[j].y, s2a, s2b));
+      }
     }
   } else {
 #pragma unroll
@@ -577,7 +596,7 @@ __global__ void __launch_bounds__(256, 2) residues(const __grid_constant__ ResAr
   }
   int8_t *dst = a.out + row * a.Kp + k0;
   if constexpr (G)
-    gauss_planes(x, a, dst);
+    gauss_planes<NV>(x, a, dst);
   else
     for (int l = 0; l < a.nmod; l++) store_planes<G, NV>(x, l, dst, a.plane_stride);
 }
@@ -625,7 +644,7 @@ __global__ void __launch_bounds__(256, 2) residues_t(const __grid_constant__ Res
   for (int j = 0; j < 8; j++) x.set(j, sx[0][li][kq + j], sx[1][li][kq + j]);
   int8_t *dst = a.out + row * a.Kp + kb + kq;
   if constexpr (G)
-    gauss_planes(x, a, dst);
+    gauss_planes<8>(x, a, dst);
   else
     for (int l = 0; l < a.nmod; l++) store_planes<G, 8>(x, l, dst, a.plane_stride);
 }
@@ -938,7 +957,13 @@ constexpr int kCrtTW = 1024;   // CRT tile width (columns): 4 per thread x 256 t
 // {2,3,4} on the target shapes (the kernel is XU/FP64-issue bound there).
 template <int NMOD, int NCH, bool G, class TO>
 cudaError_t launch_crt(const CrtArgs &c, int64_t mc, cudaStream_t s) {
-  // Gaussian stages are 2/3 the size of 3M ones: three fit beside a second CTA
+  // Gaussian stages are 2/3 the size of 3M ones: three fit beside a second CTA.
+  // TCI_CRT_CFG=1 (tuning): 2 columns x 512 threads (same 1024-column tile)
+  static const int cfg = [] {
+    const char *e = std::getenv("TCI_CRT_CFG");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (G && cfg == 1) return launch_crt_cfg<NMOD, NCH, 2, 512, 3, G, TO>(c, mc, s);
   return launch_crt_cfg<NMOD, NCH, 4, 256, G ? 3 : 2, G, TO>(c, mc, s);
 }
 
@@ -1244,6 +1269,17 @@ __global__ void __launch_bounds__(256) copy_to_peers_if(const double2 *C, int64_
 // ---------------------------------------------------------------------------
 // host planning
 // ---------------------------------------------------------------------------
+// scratch budget of the residue planes + byte outputs of one row chunk
+// (8 GB; TCI_OZ_CHUNK_GB overrides, read once)
+size_t oz_budget() {
+  static const size_t b = [] {
+    const char *e = std::getenv("TCI_OZ_CHUNK_GB");
+    const long v = e ? std::atol(e) : 0;
+    return (size_t)(v > 0 && v <= 64 ? v : 8) << 30;
+  }();
+  return b;
+}
+
 // moduli sets: 3M complex and real (kModuli), Gaussian complex (kGModuli)
 enum OzKind { kOzReal = 0, kOz3M = 1, kOzGauss = 2 };
 
@@ -1549,7 +1585,7 @@ cudaError_t ozaki_preload() {
 }
 
 void ozaki_params(int64_t K, int kind, int *nmod, int *t, const int **moduli, const int **roots, int tmin) {
-  const OzPlan p = oz_plan(1, 1, K, (size_t)8 << 30, 0, kind, tmin);
+  const OzPlan p = oz_plan(1, 1, K, oz_budget(), 0, kind, tmin);
   if (nmod) *nmod = p.nmod;
   if (t) *t = p.t;
   if (moduli) *moduli = kind == kOzGauss ? kGModuli : kModuli;
@@ -1559,8 +1595,8 @@ void ozaki_params(int64_t K, int kind, int *nmod, int *t, const int **moduli, co
 size_t ozaki_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   // sized for the largest plane count of any kind (3M, float64 sources) so
   // the variant can change without re-sizing
-  return std::max(oz_plan(M, N, K, (size_t)8 << 30, 0, kOz3M).total,
-                  oz_plan(M, N, K, (size_t)8 << 30, 0, kOzGauss).total);
+  return std::max(oz_plan(M, N, K, oz_budget(), 0, kOz3M).total,
+                  oz_plan(M, N, K, oz_budget(), 0, kOzGauss).total);
 }
 
 namespace {
@@ -1573,7 +1609,7 @@ cudaError_t ozaki_zgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cu
   if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;   // int32 residue products would overflow
   const bool gauss = g.oz_gauss != 0;
   const int tmin = std::is_same<TS, float2>::value ? kOzTminF32 : 46;
-  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows, gauss ? kOzGauss : kOz3M, tmin);
+  const OzPlan p = oz_plan(g.M, g.N, g.K, oz_budget(), g.max_chunk_rows, gauss ? kOzGauss : kOz3M, tmin);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
   OzRun<TS> R(g, p, ws, s, launches);
   char *w = R.w;
@@ -1583,7 +1619,7 @@ cudaError_t ozaki_zgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cu
   const int planes = p.ppm * p.nmod;
   auto launch_res = [&](const ResArgs &r) {
     if (r.s_k == 1) {
-      const unsigned blocks = (unsigned)((r.lines_out * (r.Kp / 8) + 255) / 256);
+      const unsigned blocks = (unsigned)((r.lines_out * (r.Kp / (gauss ? 4 : 8)) + 255) / 256);
       if (gauss)
         residues<true, TS><<<blocks, 256, 0, s>>>(r);
       else
@@ -1682,7 +1718,7 @@ cudaError_t ozaki_dgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cu
   if (g.K > kOzakiMaxK) return cudaErrorInvalidValue;
   if (g.rows_needed) return cudaErrorInvalidValue;   // the real path takes all row exponents up front
   const int tmin = std::is_same<TS, float>::value ? kOzTminF32 : 46;
-  const OzPlan p = oz_plan(g.M, g.N, g.K, (size_t)8 << 30, g.max_chunk_rows, kOzReal, tmin);
+  const OzPlan p = oz_plan(g.M, g.N, g.K, oz_budget(), g.max_chunk_rows, kOzReal, tmin);
   if (ws_bytes < p.total || !ws) return cudaErrorInvalidValue;
   OzRun<TS> R(g, p, ws, s, launches);
   char *w = R.w;

@@ -23,6 +23,7 @@ import paper_2512_23917_b200 as tci  # noqa: E402
 import synth  # noqa: E402
 
 FP64_PEAK = 37.06e12
+FP32_PEAK = 148 * 128 * 2 * 1.965e9   # FFMA (SURVEY 8(d) roofline of fp32 sweep GEMMs); the INT8 path can exceed it
 HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9 \
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6.65e12
 
@@ -97,7 +98,37 @@ def cfg1(ctx):
     torch.cuda.current_stream().wait_stream(s)
     med_g, _ = timed(lambda: g.replay(), reps=200, warm=10)
     err_g = float(abs(Eg.cpu().numpy() - ref).max() / abs(ref).max())
+    # (d) the same chain recorded through the C ABI (tci_graph_begin / end, ctx.capture) and replayed:
+    # wall time per chain from the host's point of view (one tci_graph_launch)
+    s2 = torch.cuda.Stream()
+    ctx_c = tci.Context(0, s2)
+    bufs = {}
+
+    def chain_c():
+        E = E0
+        for i, A in enumerate(psi):
+            X = ctx_c.contract(E, "xz", A, "xsy", "zsy", out=bufs.get(("X", i)))
+            bufs[("X", i)] = X
+            E = ctx_c.contract(X, "zsy", A, "zsw", "yw", out=bufs.get(("E", i)))
+            bufs[("E", i)] = E
+        return E
+    chain_c()
+    torch.cuda.synchronize()
+    gc, Ec = ctx_c.capture(chain_c)
+    for _ in range(10):
+        ctx_c.replay(gc)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(200):
+        ctx_c.replay(gc)
+    torch.cuda.synchronize()
+    wall_c = (time.perf_counter() - t0) / 200
+    err_c = float(abs(Ec.cpu().numpy() - ref).max() / abs(ref).max())
+    tci.tci_graph_destroy(gc)
+    ctx_c.close()
     return {"workload": "10-site MPS norm, chi=16, d=2, f64 (20 contracts, 46808 MACs)",
+            "tci_graph_us_per_chain_wall": wall_c * 1e6, "tci_graph_us_per_contract_wall": wall_c * 1e6 / 20,
+            "tci_graph_rel_err": err_c,
             "gpu_us_per_chain_device": med * 1e6, "gpu_us_per_contract_device": med * 1e6 / 20,
             "gpu_us_per_chain_wall": wall * 1e6, "gpu_us_per_contract_wall": wall * 1e6 / 20,
             "single_kernel_us_per_chain_device": med_k * 1e6, "single_kernel_us_per_chain_wall": wall_k * 1e6,
@@ -331,7 +362,7 @@ def sweep(ctx, seeds=24):
             es = 8 if dt == "r64" else 4
             S = size(sh)
             flops = 2.0 * size(lc) * S
-            t_roof = max(flops / FP64_PEAK, (size(la) + size(lb) + size(lc)) * es / HBM)
+            t_roof = max(flops / (FP64_PEAK if dt == "r64" else FP32_PEAK), (size(la) + size(lb) + size(lc)) * es / HBM)
             rows.append({"dtype": dt, "la": la_, "lb": lb_, "lc": lc_, "dims": dims, "elems_max": max(size(la), size(lb), size(lc)),
                          "us": med * 1e6, "roofline_us": t_roof * 1e6, "frac_of_roofline": t_roof / med})
             del A, B, holder

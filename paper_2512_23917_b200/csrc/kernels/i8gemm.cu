@@ -66,6 +66,16 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t rank)
       "r"(rank)
       : "memory");
 }
+// arrival on a barrier of the pair leader (CTA 0): the leader's own threads
+// arrive locally (release at CTA scope: a plain SYNCS arrive), the peer's at
+// cluster scope (mapa + release.cluster, which ptxas implements with a
+// MEMBAR.GPU) -- halves the heavy fences per tile
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar, bool leader) {
+  if (leader)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+  else
+    mbar_arrive_remote(bar, 0);
+}
 // 3-D TMA load into this CTA's shared memory, completing on the pair leader's
 // barrier, with an L2 eviction-priority policy (createpolicy)
 __device__ __forceinline__ void tma_load_2sm(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2,
@@ -326,7 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (;;) {
         int slot;
         const int t = next_tile(slot);
-        mbar_arrive_remote(&idempty[slot], 0);
+        mbar_arrive_leader(&idempty[slot], true);
         if (t < 0) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);   // both CTAs' epilogues drained this accumulator
         tc_fence_after();
@@ -366,7 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int slot;
       const int t = next_tile(slot);
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&idempty[slot], 0);
+      if (lane == 0) mbar_arrive_leader(&idempty[slot], leader);
       if (t < 0) break;
       int b, tm, tn;
       tile_coords(p, t, b, tm, tn);
@@ -409,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
+      if (lane == 0) mbar_arrive_leader(&tempty[acc], leader);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;

@@ -957,13 +957,8 @@ constexpr int kCrtTW = 1024;   // CRT tile width (columns): 4 per thread x 256 t
 // {2,3,4} on the target shapes (the kernel is XU/FP64-issue bound there).
 template <int NMOD, int NCH, bool G, class TO>
 cudaError_t launch_crt(const CrtArgs &c, int64_t mc, cudaStream_t s) {
-  // Gaussian stages are 2/3 the size of 3M ones: three fit beside a second CTA.
-  // TCI_CRT_CFG=1 (tuning): 2 columns x 512 threads (same 1024-column tile)
-  static const int cfg = [] {
-    const char *e = std::getenv("TCI_CRT_CFG");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (G && cfg == 1) return launch_crt_cfg<NMOD, NCH, 2, 512, 3, G, TO>(c, mc, s);
+  // Gaussian stages are 2/3 the size of 3M ones: three fit beside a second CTA
+  // (2 columns x 512 threads measured slower: 6.82 vs 6.46 ms per apply)
   return launch_crt_cfg<NMOD, NCH, 4, 256, G ? 3 : 2, G, TO>(c, mc, s);
 }
 

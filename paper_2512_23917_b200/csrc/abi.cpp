@@ -724,11 +724,12 @@ static tci_status_t contract_common(tci_ctx_t ctx, tci_tensor_t a, const int32_t
   if ((a->order && !la) || (b->order && !lb) || (c->order && !lc))
     TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "NULL label array");
   size_t n = 0;
-  CHECK(contract_exec(ctx, view_of(a), la, view_of(b), lb, view_of(c), lc, true, &n, nullptr, 0));
-  if (need) *need = n;
-  if (dry) return TCI_OK;
-  if (n > ctx->ws_bytes || (n && !ctx->ws))
-    TCI_FAIL(TCI_ERR_WORKSPACE, "contract needs %zu bytes of workspace, %zu attached", n, ctx->ws_bytes);
+  if (dry) {
+    CHECK(contract_exec(ctx, view_of(a), la, view_of(b), lb, view_of(c), lc, true, &n, nullptr, 0));
+    if (need) *need = n;
+    return TCI_OK;
+  }
+  // one planning pass: contract_exec checks the workspace before it launches anything
   Verbose vb(ctx, "contract", {a, b, c});
   return contract_exec(ctx, view_of(a), la, view_of(b), lb, view_of(c), lc, false, &n, ctx->ws,
                        ctx->ws_bytes);

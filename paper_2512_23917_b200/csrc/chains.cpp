@@ -152,9 +152,9 @@ static size_t heff_ozaki_bytes(tci_dtype_t dt, int zalgo, int64_t chi_l, int64_t
   if ((dt != TCI_C128 && dt != TCI_R64) || zalgo != kZOzaki) return 0;   // r64: real Ozaki-II
   size_t b = 0;
   const int64_t M1 = D * chi_lo, N1 = d * d * chi_r, K1 = chi_l;
-  if (ozaki_worthwhile(M1, N1, K1)) b = std::max(b, ozaki_workspace_bytes(M1, N1, K1));
+  if (ozaki_worthwhile(M1, N1, K1, dt)) b = std::max(b, ozaki_workspace_bytes(M1, N1, K1));
   const int64_t M4 = chi_lo * d * d, N4 = chi_ro, K4 = chi_r * D2;
-  if (ozaki_worthwhile(M4, N4, K4)) b = std::max(b, ozaki_workspace_bytes(M4, N4, K4));
+  if (ozaki_worthwhile(M4, N4, K4, dt)) b = std::max(b, ozaki_workspace_bytes(M4, N4, K4));
   return b ? align_up(b) : 0;
 }
 
@@ -324,7 +324,7 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
   auto set_zalgo = [&](GemmProblem &g) {
     g.zalgo = ctx->zgemm_algo == kZOzaki ? kZ3M : ctx->zgemm_algo;
     // (the real Ozaki GEMM takes its row exponents up front: not with staged input)
-    if (oz_b && ozaki_worthwhile(g.M, g.N, g.K) && !(dt == TCI_R64 && stage)) {
+    if (oz_b && ozaki_worthwhile(g.M, g.N, g.K, g.dtype) && !(dt == TCI_R64 && stage)) {
       g.zalgo = kZOzaki;
       g.oz_ws = ws + lay.total;
       g.oz_ws_bytes = oz_b;
@@ -358,7 +358,7 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
         gc.M = std::min(ch, M - m0);
         gc.A = static_cast<const char *>(g.A) + m0 * dtype_size(dt);
         gc.C = static_cast<char *>(g.C) + m0 * g.c_sm * dtype_size(dt);
-        if (gc.zalgo == kZOzaki && !ozaki_worthwhile(gc.M, gc.N, gc.K)) gc.zalgo = kZ3M;
+        if (gc.zalgo == kZOzaki && !ozaki_worthwhile(gc.M, gc.N, gc.K, gc.dtype)) gc.zalgo = kZ3M;
         stage_L_in(stage, m0, gc.M);
         TCI_CUDA_CHECK(stage->err);
         { tci_status_t _r = run_gemm(ctx, gc); if (_r) return _r; }
@@ -495,7 +495,7 @@ tci_status_t heff_exec(tci_ctx_s *ctx, const View &L, const View &W1, const View
         gc.M = std::min(ch, M - m0);
         gc.A = static_cast<const char *>(g.A) + m0 * g.a_sm * dtype_size(dt);
         gc.C = static_cast<char *>(g.C) + m0 * g.c_sm * dtype_size(dt);
-        if (gc.zalgo == kZOzaki && !ozaki_worthwhile(gc.M, gc.N, gc.K)) gc.zalgo = kZ3M;
+        if (gc.zalgo == kZOzaki && !ozaki_worthwhile(gc.M, gc.N, gc.K, gc.dtype)) gc.zalgo = kZ3M;
         { tci_status_t _r = run_gemm(ctx, gc); if (_r) return _r; }
         stage_rows_out(stage, m0, gc.M);
         TCI_CUDA_CHECK(stage->err);

@@ -357,7 +357,7 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
     const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
     // (not when the GEMM goes to the INT8 tensor cores: its 3n / n residue
     // GEMMs of one launch fill the machine by themselves)
-    const bool oz_candidate = oz_dtype && ozaki_worthwhile(M, N, K);
+    const bool oz_candidate = oz_dtype && ozaki_worthwhile(M, N, K, a.dtype);
     if (tiles < 2 * 148 && K >= 256 && !oz_candidate) {
       int64_t S = std::min<int64_t>({(4 * 148 + tiles - 1) / tiles, K / 128, 1024});
       if (S >= 2) {
@@ -370,7 +370,7 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   // complex128 GEMM algorithm
   int zalgo = ctx->zgemm_algo == kZOzaki ? kZ3M : ctx->zgemm_algo;
   // (float64 too: real Ozaki-II, one residue plane per modulus)
-  const bool use_ozaki = oz_dtype && splitk <= 1 && ozaki_worthwhile(M, N, K);
+  const bool use_ozaki = oz_dtype && splitk <= 1 && ozaki_worthwhile(M, N, K, a.dtype);
   // gamma-order scatter epilogue (8(a6)): an output that is not a [I,J] /
   // [J,I] block is written in place through row / column offset tables
   // instead of GEMM -> scratch -> permute; the GEMM is oriented so that the

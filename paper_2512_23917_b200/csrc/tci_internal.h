@@ -135,8 +135,23 @@ cudaError_t launch_ozaki_zgemm(const GemmProblem &g, void *ws, size_t ws_bytes, 
 // Ozaki pays ~10 passes over the operands: use it only for big products.
 // K <= 131072 keeps every int32 residue dot product exact (K * 127^2 < 2^31).
 constexpr int64_t kOzakiMaxK = 131072;
-inline bool ozaki_worthwhile(int64_t M, int64_t N, int64_t K) {
-  return (double)M * (double)N * (double)K >= 4.0e9 && M >= 256 && N >= 256 && K >= 64 && K <= kOzakiMaxK;
+// Beyond the size gate, a cost model (seconds at measured B200 rates): the
+// INT8 GEMMs, the residue planes of both operands, and the byte planes the
+// GEMM writes + the CRT reads + the output, against the DMMA (float64 /
+// complex128) or FP64-core (float32 / complex64) GEMM. Short K loses: the
+// CRT's M N (2 planes + out) bytes then outweigh 2 M N K flops (sweep
+// instances with K = 64..80 ran 3-9x slower on the INT8 path).
+inline bool ozaki_worthwhile(int64_t M, int64_t N, int64_t K, tci_dtype_t dt = TCI_C128) {
+  if (!((double)M * (double)N * (double)K >= 4.0e9 && M >= 256 && N >= 256 && K >= 64 && K <= kOzakiMaxK))
+    return false;
+  const bool cplx = dt == TCI_C128 || dt == TCI_C64, f32 = dt == TCI_R32 || dt == TCI_C64;
+  const double planes = cplx ? (f32 ? 20.0 : 30.0) : (f32 ? 9.0 : 14.0);
+  const double es = (cplx ? 16.0 : 8.0) / (f32 ? 2.0 : 1.0);
+  const double mnk = (double)M * (double)N * (double)K, mn = (double)M * (double)N;
+  const double t_oz = planes * 2.0 * mnk / 2.8e15 + (double)(M + N) * (double)K * (es + planes) / 5e12 +
+                      mn * (2.0 * planes + es) / 5e12;
+  const double t_alt = (cplx ? 8.0 : 2.0) * mnk / (f32 ? (cplx ? 25e12 : 30e12) : (cplx ? 45e12 : 35e12));
+  return t_oz < 0.8 * t_alt;
 }
 // The residue products of one Ozaki GEMM in one launch (i8gemm.cu, tcgen05
 // kind::i8): D[b] = (A[b] B[b]^T) mod m_(b / per_mod) over L planes,

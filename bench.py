@@ -667,6 +667,45 @@ def run_tci(args):
         dist.destroy_process_group()
 
 
+def run_oracle_configs():
+    """SURVEY 8(d) "CPU oracle timed beside it": the oracle on the host cores
+    for configs 1-3, single-threaded and with every host thread (config 1:
+    the full 10-site norm chain; configs 2 and 3: sampled output rows, time
+    per row x rows = the extrapolated full time, labelled as such). One JSON
+    line; not part of the timed GPU contract."""
+    import oracle
+    oracle.build()
+    nthreads = oracle.max_threads()
+    res = {"kind": "oracle", "cpu_model": cpu_model(), "host_cpus": os.cpu_count(), "threads_all": nthreads}
+    sites = synth.mps_sites(synth.MPS_BONDS_CFG1, 2, 1)
+    for th, key in ((1, "1_thread"), (nthreads, "all_threads")):
+        t0 = time.perf_counter()
+        for _ in range(20):
+            oracle.mps_norm2(sites, threads=th)
+        res.setdefault("cfg1_mps_norm_chain_us", {})[key] = (time.perf_counter() - t0) / 20 * 1e6
+    cfg = synth.HEFF_CONFIGS["cfg2_heisenberg_chi1024"]
+    inp = {k: v.numpy() for k, v in synth.heff_inputs(cfg["chi"], cfg["d"], cfg["D"], cfg["dtype"], cfg["seed"],
+                                                       cfg["model"]).items()}
+    rows = [0, 511, 1023]
+    for th, key in ((1, "1_thread"), (nthreads, "all_threads")):
+        t0 = time.perf_counter()
+        oracle.heff_rows(inp["L"], inp["W1"], inp["W2"], inp["R"], inp["psi"], rows, threads=th)
+        t = (time.perf_counter() - t0) / len(rows) * cfg["chi"]
+        res.setdefault("cfg2_heff_chi1024_s_extrapolated", {})[key] = t
+    tc = synth.TEBD_CONFIG
+    ti = synth.tebd_inputs(tc["chi"], tc["d"], tc["dtype"], tc["seed"], tc["tau"])
+    A, B, U = ti["A"].numpy(), ti["B"].numpy(), ti["U"].numpy()
+    arows = [0, 1]
+    for th, key in ((1, "1_thread"), (nthreads, "all_threads")):
+        t0 = time.perf_counter()
+        oracle.tebd_theta(np.ascontiguousarray(A[arows]), B, U, threads=th)
+        t = (time.perf_counter() - t0) / len(arows) * tc["chi"]
+        res.setdefault("cfg3_tebd_chi2048_s_extrapolated", {})[key] = t
+    res["note"] = ("configs 2-3: rows of the output timed and scaled by chi (extrapolated full time); "
+                   "config 1: the whole chain")
+    print(json.dumps(res), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -687,7 +726,12 @@ def main():
                     help="complex128 GEMM algorithm of the timed apply (DESIGN.md §12)")
     ap.add_argument("--alt", default="dmma3m",
                     help="also time this algorithm (reported under 'alt'; 'none' to skip)")
+    ap.add_argument("--oracle-configs", action="store_true",
+                    help="time the CPU oracle on configs 1-3 (1 thread and all threads) and exit")
     args = ap.parse_args()
+    if args.oracle_configs:
+        run_oracle_configs()
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

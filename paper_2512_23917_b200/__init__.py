@@ -641,6 +641,10 @@ class Context:
         key = (t.data_ptr(), tuple(t.shape), t.dtype)
         h = self._desc.get(key)
         if h is None:
+            if len(self._desc) >= 8192:   # bounded: descriptors are host-side only (no kernel holds one)
+                for old in self._desc.values():
+                    tci_tensor_free(self.handle, old)
+                self._desc.clear()
             h = tci_tensor_create(self.handle, _torch_dtype_code(t), tuple(t.shape), t.data_ptr())
             self._desc[key] = h
         return h
@@ -675,9 +679,15 @@ class Context:
         tci_workspace_attach(self.handle, ptr, nbytes)
         self._ws_bytes = nbytes
 
+    def _on_current_stream(self) -> bool:
+        return self.torch.cuda.current_stream(self.device).cuda_stream == self.stream.cuda_stream
+
     def _empty(self, shape, dtype, device=None):
+        dev = device if device is not None else f"cuda:{self.device}"
+        if self._on_current_stream():   # (the stream context manager costs several us per call)
+            return self.torch.empty(shape, dtype=dtype, device=dev)
         with self._on_stream():
-            return self.torch.empty(shape, dtype=dtype, device=device if device is not None else f"cuda:{self.device}")
+            return self.torch.empty(shape, dtype=dtype, device=dev)
 
     def _empty_like(self, x):
         with self._on_stream():
@@ -698,10 +708,15 @@ class Context:
             shape = self.contract_out_shape(a, la, b, lb, lc)
             out = self._empty(shape, dtype=a.dtype, device=a.device)
         ha, hb, hc = self.tensor(a), self.tensor(b), self.tensor(out)
-        key = (ha, hb, hc, la if isinstance(la, str) else tuple(la), lb if isinstance(lb, str) else tuple(lb),
+        # the planner's workspace answer depends on dtype, shapes, labels and
+        # whether the output aliases an input (R8) -- not on the addresses
+        pc, nc = out.data_ptr(), out.numel() * out.element_size()
+        alias = any(x.data_ptr() < pc + nc and pc < x.data_ptr() + x.numel() * x.element_size() for x in (a, b))
+        key = (a.dtype, tuple(a.shape), tuple(b.shape), tuple(out.shape), alias,
+               la if isinstance(la, str) else tuple(la), lb if isinstance(lb, str) else tuple(lb),
                lc if isinstance(lc, str) else tuple(lc))
         ws = self._ws_need.get(key)
-        if ws is None:   # the planner's answer depends only on the descriptors and labels
+        if ws is None:
             ws = tci_contract_workspace_size(self.handle, ha, _labels_list(la), hb, _labels_list(lb), hc,
                                              _labels_list(lc))
             self._ws_need[key] = ws

@@ -81,7 +81,15 @@ tci_status_t run_tebd(tci_ctx_s *ctx, const TebdProblem &t) {
   const double M = 2.0 * t.chi_a, N = 2.0 * t.chi_c, K = (double)t.chi_b;
   ProfScope ps(ctx, kProfGemm, 2.0 * M * N * K + 2.0 * 16.0 * t.chi_a * t.chi_c,
                8.0 * (M * K + K * N + M * N));
-  TCI_CUDA_CHECK(launch_tebd_fused(t, ctx->stream, &ctx->launches));
+  // TMA-loaded tiles (tebd_tma.cu) unless TCI_TEBD_TMA=0; the cp.async kernel otherwise
+  static const bool use_tma = [] {
+    const char *e = getenv("TCI_TEBD_TMA");
+    return !(e && !strcmp(e, "0"));
+  }();
+  if (use_tma && tebd_tma_supported(t))
+    TCI_CUDA_CHECK(launch_tebd_tma(t, ctx->stream, &ctx->launches));
+  else
+    TCI_CUDA_CHECK(launch_tebd_fused(t, ctx->stream, &ctx->launches));
   ps.done();
   return TCI_OK;
 }

@@ -192,6 +192,10 @@ struct TebdProblem {
 };
 cudaError_t launch_tebd_fused(const TebdProblem &p, cudaStream_t s, int64_t *launches);
 bool tebd_fused_supported(const TebdProblem &p);
+// the same with TMA-loaded operand tiles (tebd_tma.cu; config 3's
+// "TMA-fused permutes"): natural and physical-first layouts
+cudaError_t launch_tebd_tma(const TebdProblem &p, cudaStream_t s, int64_t *launches);
+bool tebd_tma_supported(const TebdProblem &p);
 
 // ---------------------------------------------------------------------------
 // Permute: out[c_out] = in[c_in], c_in[perm[k]] = c_out[k].

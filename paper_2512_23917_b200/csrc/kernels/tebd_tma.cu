@@ -8,9 +8,9 @@
 //  * CTA tile: 64 a x 2 s rows by 2 t x 64 c columns (the four (s,t) gate
 //    inputs of 64 x 64 (a,c) pairs), K = b in steps of 16, 4-stage mbarrier
 //    ring filled by one thread: A as ONE 3-D box (16 b, 2 s, 64 a) -- or
-//    (16 b, 64 a, 2 s) physical-first -- and B as eight 3-D boxes
-//    (16 c, 1 t, 16 b) / (16 c, 16 b, 1 t), all SWIZZLE_128B (1 KB atoms of
-//    8 rows x 128 B). Out-of-range a / b / c (ragged chi) arrive as zeros.
+//    (16 b, 64 a, 2 s) physical-first -- SWIZZLE_128B, and B as sixteen
+//    unswizzled 3-D boxes (8 c, 1 t, 16 b) / (8 c, 16 b, 1 t) of 64-byte
+//    rows. Out-of-range a / b / c (ragged chi) arrive as zeros.
 //  * FP64 DMMA m8n8k4, 8 warps of 64 x 32, k consumed in the same order as
 //    the plain GEMM kernel (groups of 4 ascending), so an identity gate
 //    gives A.B bitwise. (Permuting each DMMA's k values to {0,1,4,5}, ...
@@ -37,7 +37,7 @@ constexpr int kABytes = kBM * kBK * 8;   // 16 KB: 128 rows x 128 B
 constexpr int kBBytes = kBK * kBN * 8;   // 16 KB: 8 sub-tiles of 16 k x 16 c
 constexpr int kStage = kABytes + kBBytes;
 constexpr int kPC = kBN + 1;             // staged C pitch (doubles)
-constexpr int kSmem = 1024 + std::max(kST * kStage + 8 * kST, kBM * kPC * 8);
+constexpr int kSmem = 1024 + std::max(kST * kStage + 16 * kST, kBM * kPC * 8);
 
 struct TebdTmaArgs {
   int64_t chi_a, chi_b, chi_c;
@@ -62,15 +62,18 @@ __device__ __forceinline__ void tma3d(void *dst, const CUtensorMap *map, uint64_
 __device__ __forceinline__ uint32_t a_off(int r, int k) {
   return (uint32_t)(r * 128 + ((((k >> 1) ^ r) & 7) << 4) + ((k & 1) << 3));
 }
-// byte offset of B(k, n = t * 64 + c): sub-tile (t, c / 16) of 16 rows k x 16 doubles
+// byte offset of B(k, n = t * 64 + c): sub-tile (t, c / 8) of 16 rows k x 8
+// doubles, unswizzled: a DMMA B fragment (4 rows k x 8 n) reads 4 x 64 B
+// that fall alternately into the two halves of the bank space -- two
+// wavefronts, the minimum for 256 B
 __device__ __forceinline__ uint32_t b_off(int k, int n) {
-  const int st = ((n >> 6) << 2) + ((n & 63) >> 4), cw = n & 15;
-  return (uint32_t)(kABytes + st * 2048 + k * 128 + ((((cw >> 1) ^ k) & 7) << 4) + ((cw & 1) << 3));
+  const int st = ((n >> 6) << 3) + ((n & 63) >> 3), cw = n & 7;
+  return (uint32_t)(kABytes + st * 1024 + k * 64 + cw * 8);
 }
 // the k index lane-column lc uses in DMMA k-step kk of a 16-wide stage
 __device__ __forceinline__ int kperm(int kk, int lc) { return 4 * kk + lc; }
 
-__global__ void __launch_bounds__(kNT, 1) tebd_tma_kernel(const __grid_constant__ CUtensorMap mA,
+__global__ void __launch_bounds__(kNT + 32, 1) tebd_tma_kernel(const __grid_constant__ CUtensorMap mA,
                                                         const __grid_constant__ CUtensorMap mB,
                                                         const __grid_constant__ TebdTmaArgs p) {
   extern __shared__ uint8_t raw[];
@@ -78,38 +81,57 @@ __global__ void __launch_bounds__(kNT, 1) tebd_tma_kernel(const __grid_constant_
   uint8_t *sm = raw + (((base_u + 1023u) & ~1023u) - base_u);
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + kST * kStage);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile_m = blockIdx.x / p.tiles_n, tile_n = blockIdx.x % p.tiles_n;
+  // grouped raster (as the DMMA GEMM): 8 M-tiles walk the N-tiles together,
+  // so the B panels they share stay in L2
+  constexpr int GROUP = 8;
+  const int bid = blockIdx.x, per_group = GROUP * p.tiles_n;
+  const int first_m = (bid / per_group) * GROUP;
+  const int gsize = min(p.tiles_m - first_m, GROUP);
+  const int tile_m = first_m + (bid % per_group) % gsize;
+  const int tile_n = (bid % per_group) / gsize;
   const int a0 = tile_m * 64, c0 = tile_n * 64;
   const int KT = (int)((p.chi_b + kBK - 1) / kBK);
 
+  uint64_t *empty = full + kST;
   if (tid == 0) {
-    for (int s = 0; s < kST; s++) mbar_init(&full[s], 1);
+    for (int s = 0; s < kST; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNT / 32);   // one arrival per compute warp
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  auto issue = [&](int kt, int s) {   // thread 0
-    uint8_t *st = sm + s * kStage;
-    const int b0 = kt * kBK;
-    mbar_expect_tx(&full[s], kStage);
-    if (p.pfA)
-      tma3d(st, &mA, &full[s], b0, a0, 0);
-    else
-      tma3d(st, &mA, &full[s], b0, 0, a0);
-    // B boxes of 16 c x 16 b for one t: coordinates (c, t, b) natural,
-    // (c, b, t) physical-first (the map lists the dims slowest-last)
-#pragma unroll
-    for (int t = 0; t < 2; t++)
-#pragma unroll
-      for (int cc = 0; cc < 4; cc++) {
-        uint8_t *dst = st + kABytes + (t * 4 + cc) * 2048;
-        if (p.pfB)
-          tma3d(dst, &mB, &full[s], c0 + 16 * cc, b0, t);
+
+  if (tid >= kNT) {
+    // ===== producer warp: the 17 boxes of each stage, kST stages ahead of
+    // the compute warps (full / empty mbarriers; no block-wide barrier in
+    // the main loop) =====
+    if (lane == 0) {
+      for (int kt = 0; kt < KT; kt++) {
+        const int s = kt % kST;
+        if (kt >= kST) mbar_wait(&empty[s], (uint32_t)(((kt / kST) - 1) & 1));
+        uint8_t *st = sm + s * kStage;
+        const int b0 = kt * kBK;
+        fence_proxy_async_smem();
+        mbar_expect_tx(&full[s], kStage);
+        if (p.pfA)
+          tma3d(st, &mA, &full[s], b0, a0, 0);
         else
-          tma3d(dst, &mB, &full[s], c0 + 16 * cc, t, b0);
+          tma3d(st, &mA, &full[s], b0, 0, a0);
+        // B boxes of 8 c x 16 b for one t: coordinates (c, t, b) natural,
+        // (c, b, t) physical-first (the map lists the dims slowest-last)
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const int t = j >> 3, cc = j & 7;
+          uint8_t *dst = st + kABytes + j * 1024;
+          if (p.pfB)
+            tma3d(dst, &mB, &full[s], c0 + 8 * cc, b0, t);
+          else
+            tma3d(dst, &mB, &full[s], c0 + 8 * cc, t, b0);
+        }
       }
-  };
-  if (tid == 0)
-    for (int s = 0; s < kST && s < KT; s++) issue(s, s);
+    }
+  }
 
   const int wm0 = (warp >> 2) * 64, wn0 = (warp & 3) * 32;
   const int lr = lane >> 2, lc = lane & 3;
@@ -119,33 +141,39 @@ __global__ void __launch_bounds__(kNT, 1) tebd_tma_kernel(const __grid_constant_
 #pragma unroll
     for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int kt = 0; kt < KT; kt++) {
-    const int s = kt % kST;
-    mbar_wait(&full[s], (uint32_t)((kt / kST) & 1));
-    const uint8_t *st = sm + s * kStage;
+  // fragments double-buffered in registers: k-step kk + 1's shared-memory
+  // loads are in flight while kk's 32 DMMAs issue
+  auto load_frags = [&](const uint8_t *st, int kk, double (&fa)[8], double (&fb)[4]) {
+    const int k = kperm(kk, lc);
 #pragma unroll
-    for (int kk = 0; kk < kBK / 4; kk++) {
-      const int k = kperm(kk, lc);
-      double fa[8], fb[4];
+    for (int i = 0; i < 8; i++) fa[i] = *reinterpret_cast<const double *>(st + a_off(wm0 + i * 8 + lr, k));
 #pragma unroll
-      for (int i = 0; i < 8; i++) fa[i] = *reinterpret_cast<const double *>(st + a_off(wm0 + i * 8 + lr, k));
+    for (int j = 0; j < 4; j++) fb[j] = *reinterpret_cast<const double *>(st + b_off(k, wn0 + j * 8 + lr));
+  };
+  if (tid < kNT) {
+    for (int kt = 0; kt < KT; kt++) {
+      const int s = kt % kST;
+      mbar_wait(&full[s], (uint32_t)((kt / kST) & 1));
+      const uint8_t *st = sm + s * kStage;
+      double fa[2][8], fb[2][4];
+      load_frags(st, 0, fa[0], fb[0]);
 #pragma unroll
-      for (int j = 0; j < 4; j++) fb[j] = *reinterpret_cast<const double *>(st + b_off(k, wn0 + j * 8 + lr));
+      for (int kk = 0; kk < kBK / 4; kk++) {
+        if (kk + 1 < kBK / 4) load_frags(st, kk + 1, fa[(kk + 1) & 1], fb[(kk + 1) & 1]);
 #pragma unroll
-      for (int i = 0; i < 8; i++)
+        for (int i = 0; i < 8; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) dmma884(acc[i][j], fa[i], fb[j]);
-    }
-    __syncthreads();   // every warp is done with stage s
-    if (tid == 0 && kt + kST < KT) {
-      fence_proxy_async_smem();   // generic reads of the stage before the async-proxy refill
-      issue(kt + kST, s);
+          for (int j = 0; j < 4; j++) dmma884(acc[i][j], fa[kk & 1][i], fb[kk & 1][j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
     }
   }
 
   // ---- epilogue: C tile through shared memory, then the gate per (a, c) ----
-  __syncthreads();
+  __syncthreads();   // every stage consumed (and no TMA write in flight: all were waited on)
   double *Cs = reinterpret_cast<double *>(sm);
+  if (tid < kNT)
 #pragma unroll
   for (int i = 0; i < 8; i++)
 #pragma unroll
@@ -164,7 +192,7 @@ __global__ void __launch_bounds__(kNT, 1) tebd_tma_kernel(const __grid_constant_
 #pragma unroll
         for (int t_ = 0; t_ < 2; t_++) u[pp][q][s_][t_] = p.U[pp * p.u[0] + q * p.u[1] + s_ * p.u[2] + t_ * p.u[3]];
   __syncthreads();
-  for (int idx = tid; idx < 64 * 64; idx += kNT) {
+  for (int idx = tid; tid < kNT && idx < 64 * 64; idx += kNT) {
     const int al = idx >> 6, cl = idx & 63;
     const int64_t a = a0 + al, c = c0 + cl;
     if (a >= p.chi_a || c >= p.chi_c) continue;
@@ -205,7 +233,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tebd_encode_fn() {
 // 3-D float64 map over base with dims d (innermost first, d[0] unit stride),
 // byte strides of dims 1 and 2, box b, SWIZZLE_128B (b[0] = 16 doubles)
 bool map3(CUtensorMap *m, const double *base, const uint64_t (&d)[3], const uint64_t (&st)[2],
-          const uint32_t (&b)[3]) {
+          const uint32_t (&b)[3], bool swz) {
   auto enc = tebd_encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[3] = {d[0], d[1], d[2]};
@@ -213,7 +241,8 @@ bool map3(CUtensorMap *m, const double *base, const uint64_t (&d)[3], const uint
   const cuuint32_t box[3] = {b[0], b[1], b[2]};
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -234,17 +263,17 @@ cudaError_t launch_tebd_tma(const TebdProblem &t, cudaStream_t s, int64_t *launc
   bool ok;
   if (pfA)   // A[s][a][b]: dims (b, a, s)
     ok = map3(&mA, t.A, {(uint64_t)t.chi_b, (uint64_t)t.chi_a, 2}, {(uint64_t)t.a_a * 8, (uint64_t)t.a_s * 8},
-              {16, 64, 2});
+              {16, 64, 2}, true);
   else       // A[a][s][b]: dims (b, s, a)
     ok = map3(&mA, t.A, {(uint64_t)t.chi_b, 2, (uint64_t)t.chi_a}, {(uint64_t)t.a_s * 8, (uint64_t)t.a_a * 8},
-              {16, 2, 64});
+              {16, 2, 64}, true);
   if (ok) {
     if (pfB)   // B[t][b][c]: dims (c, b, t)
       ok = map3(&mB, t.B, {(uint64_t)t.chi_c, (uint64_t)t.chi_b, 2}, {(uint64_t)t.b_b * 8, (uint64_t)t.b_t * 8},
-                {16, 16, 1});
+                {8, 16, 1}, false);
     else       // B[b][t][c]: dims (c, t, b)
       ok = map3(&mB, t.B, {(uint64_t)t.chi_c, 2, (uint64_t)t.chi_b}, {(uint64_t)t.b_t * 8, (uint64_t)t.b_b * 8},
-                {16, 1, 16});
+                {8, 1, 16}, false);
   }
   if (!ok) return cudaErrorNotSupported;
   TebdTmaArgs a{};
@@ -261,7 +290,7 @@ cudaError_t launch_tebd_tma(const TebdProblem &t, cudaStream_t s, int64_t *launc
   a.t[0] = t.t_a; a.t[1] = t.t_p; a.t[2] = t.t_q; a.t[3] = t.t_c;
   cudaError_t e = ensure_smem_attr((const void *)tebd_tma_kernel, kSmem);
   if (e != cudaSuccess) return e;
-  tebd_tma_kernel<<<(unsigned)((int64_t)a.tiles_m * a.tiles_n), kNT, kSmem, s>>>(mA, mB, a);
+  tebd_tma_kernel<<<(unsigned)((int64_t)a.tiles_m * a.tiles_n), kNT + 32, kSmem, s>>>(mA, mB, a);   // + producer warp
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../paper_2512_23917_b200/csrc/kernels/i8gemm.cu"
+#include "../paper_2512_23917_b200/csrc/launch_cache.cpp"
 
 #ifdef WITH_CUTLASS
 // the library INT8 GEMM the round-1 build used, for an A/B in the same process
@@ -192,6 +193,13 @@ static int check(int64_t M, int64_t N, int64_t Kp, int L, int per_mod, bool full
 
 int main(int argc, char **argv) {
   int fails = 0;
+  if (argc > 1 && !strcmp(argv[1], "kscan")) {   // per-tile overhead: fixed M x N (GEMM1 chunk), K varied
+    const int ks[] = {1024, 2048, 4096, 8192, 16384};
+    for (int k : ks) fails += check(9216, 16384, k, 30, 2, false, 3);
+    fails += check(10752, 4096, 20480, 30, 2, false, 3);   // GEMM4 chunk
+    printf(fails ? "FAIL\n" : "ALL OK\n");
+    return fails;
+  }
   if (argc > 1 && !strcmp(argv[1], "sweep")) {   // L2-policy sweep on the bench chunk shapes
     const int mbs[] = {24, 32, 48, 64, 96, 1000};
     for (int mb : mbs) {

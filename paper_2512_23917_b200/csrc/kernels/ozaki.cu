@@ -185,6 +185,110 @@ __global__ void __launch_bounds__(256) kstats_cols(const T *X, int64_t K, int64_
   SS[blockIdx.y * K + k] = s;
 }
 
+// ---- fused pass (round 2): the per-k statistics AND the unbalanced per-line
+// exponents E (max over k of the frexp exponents, re and im) from ONE read of
+// the operand; when the K-balancing then turns out inactive (the common case)
+// E is final and the separate line_exponent pass is skipped (it runs gated on
+// the device flag otherwise). Same (exponent, sum) arithmetic and merge orders
+// as kstats_lines / kstats_cols: the statistics are bitwise the same.
+__device__ __forceinline__ int es_add_e(int &em, double &s, double x) {   // returns x's exponent
+  if (x == 0.0) return -100000;
+  int e;
+  const double f = frexp(x, &e);
+  if (e > em) {
+    s = em == -100000 ? 0.0 : s * pow4i(em - e);
+    em = e;
+  }
+  s = fma(f * f, pow4i(e - em), s);
+  return e;
+}
+__device__ __forceinline__ int es_add_e(int &em, double &s, double2 x) {
+  const int a = es_add_e(em, s, x.x), b = es_add_e(em, s, x.y);
+  return max(a, b);
+}
+__device__ __forceinline__ int es_add_e(int &em, double &s, float x) { return es_add_e(em, s, (double)x); }
+__device__ __forceinline__ int es_add_e(int &em, double &s, float2 x) {
+  const int a = es_add_e(em, s, (double)x.x), b = es_add_e(em, s, (double)x.y);
+  return max(a, b);
+}
+
+// K-contiguous lines (s_k == 1): thread per k (coalesced), the block's chunk
+// of lines in order; line maxima by a warp max + shared atomicMax, then one
+// global atomicMax per line and block (max is order-independent)
+template <class T>
+__global__ void __launch_bounds__(256) kstats_cols_lx(const T *X, int64_t K, int64_t L, int64_t s_l, int64_t chunk,
+                                                      int *SE, double *SS, int *E) {
+  extern __shared__ int sE[];
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t l0 = blockIdx.y * chunk, l1 = min(L, l0 + chunk);
+  for (int64_t i = threadIdx.x; i < l1 - l0; i += blockDim.x) sE[i] = -100000;
+  __syncthreads();
+  const bool kin = k < K;
+  int em = -100000;
+  double s = 0.0;
+  const T *p = X + (kin ? k : 0);
+#pragma unroll 4
+  for (int64_t l = l0; l < l1; l++) {
+    int ex = -100000;
+    if (kin) ex = es_add_e(em, s, __ldg(p + l * s_l));
+    const int wm = __reduce_max_sync(0xffffffffu, ex);
+    if ((threadIdx.x & 31) == 0 && wm > -100000) atomicMax(&sE[l - l0], wm);
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < l1 - l0; i += blockDim.x)
+    if (sE[i] > -100000) atomicMax(E + l0 + i, sE[i]);
+  if (kin) {
+    SE[blockIdx.y * K + k] = em;
+    SS[blockIdx.y * K + k] = s;
+  }
+}
+
+// line-contiguous lines (s_l == 1): warp per k as kstats_lines (lanes walk
+// the chunk's lines, coalesced; the same xor-tree merge), 4 k per warp and
+// 32 per block; line maxima by shared atomicMax over the block's 32 k, then
+// one global atomicMax per line and block
+template <class T>
+__global__ void __launch_bounds__(256) kstats_lines_lx(const T *X, int64_t K, int64_t L, int64_t s_k, int64_t chunk,
+                                                       int *SE, double *SS, int *E) {
+  extern __shared__ int sE[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t l0 = blockIdx.y * chunk, l1 = min(L, l0 + chunk);
+  for (int64_t i = threadIdx.x; i < l1 - l0; i += blockDim.x) sE[i] = -100000;
+  __syncthreads();
+  for (int kk = 0; kk < 4; kk++) {
+    const int64_t k = blockIdx.x * 32 + warp * 4 + kk;
+    int em = -100000;
+    double s = 0.0;
+    if (k < K) {
+      const T *p = X + k * s_k;
+      for (int64_t l = l0 + lane; l < l1; l += 32) {
+        const int e = es_add_e(em, s, __ldg(p + l));
+        if (e > -100000) atomicMax(&sE[l - l0], e);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const int e2 = __shfl_xor_sync(0xffffffffu, em, o);
+      const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane & o) {
+        int ea = e2;
+        double sa = s2;
+        es_merge(ea, sa, em, s);
+        em = ea;
+        s = sa;
+      } else {
+        es_merge(em, s, e2, s2);
+      }
+    }
+    if (lane == 0 && k < K) {
+      SE[blockIdx.y * K + k] = em;
+      SS[blockIdx.y * K + k] = s;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < l1 - l0; i += blockDim.x)
+    if (sE[i] > -100000) atomicMax(E + l0 + i, sE[i]);
+}
+
 __global__ void __launch_bounds__(256) kstats_merge(const int *SE, const double *SS, int nch, int64_t K, int *KE,
                                                     double *KS) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -293,8 +397,9 @@ __device__ __forceinline__ int exp_of_shift(double v, int s) {
 template <class T>
 __global__ void __launch_bounds__(256) line_exponent(const T *base, int64_t nlines, int64_t K, int64_t s_l,
                                                      int64_t s_k, int *E, const int *SK, int sgn,
-                                                     const int *bal) {
+                                                     const int *bal, int only_if_bal = 0) {
   const bool b = SK && *bal;
+  if (only_if_bal && !b) return;   // the fused stats pass already left the unbalanced E
   if (s_k == 1) {
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -324,7 +429,8 @@ __global__ void __launch_bounds__(256) line_exponent(const T *base, int64_t nlin
   }
 }
 
-__global__ void fill_int(int *p, int64_t n, int v) {
+__global__ void fill_int(int *p, int64_t n, int v, const int *only_if = nullptr) {
+  if (only_if && !*only_if) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
@@ -1462,6 +1568,30 @@ struct OzRun {
     if (launches) *launches += n;
   }
   // per-k statistics over the lines of X: element (l, k) at l*s_l + k*s_k
+  // fused variant: also the unbalanced line exponents E (pre-filled with
+  // -100000 here); returns false when it does not apply (E untouched)
+  bool kstats_lx(const T *X, int64_t L, int64_t s_l, int64_t s_k, int *KE, double *KS, int *E) {
+    int *SE = reinterpret_cast<int *>(w + p.off_slotE);
+    double *SS = reinterpret_cast<double *>(w + p.off_slotS);
+    // line chunks: >= 64 lines per (k-block, chunk) for the thread-per-k
+    // variant (as kstats_cols), up to 4096 for the warp-per-k one; their line
+    // maxima live in shared memory
+    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(p.nch, s_l == 1 ? (L + 4095) / 4096 : (L + 63) / 64));
+    const int64_t chunk = (L + nch - 1) / nch;
+    if (s_l != 1 && s_k != 1) return false;
+    if (chunk * 4 > 48 * 1024) return false;   // shared line maxima of one chunk
+    fill_int<<<(unsigned)std::min<int64_t>((L + 255) / 256, 1024), 256, 0, s>>>(E, L, -100000);
+    if (s_l == 1) {
+      dim3 grid((unsigned)((g.K + 31) / 32), (unsigned)nch);
+      kstats_lines_lx<T><<<grid, 256, (size_t)chunk * 4, s>>>(X, g.K, L, s_k, chunk, SE, SS, E);
+    } else {
+      dim3 grid((unsigned)((g.K + 255) / 256), (unsigned)nch);
+      kstats_cols_lx<T><<<grid, 256, (size_t)chunk * 4, s>>>(X, g.K, L, s_l, chunk, SE, SS, E);
+    }
+    kstats_merge<<<(unsigned)((g.K + 255) / 256), 256, 0, s>>>(SE, SS, (int)nch, g.K, KE, KS);
+    count(3);
+    return true;
+  }
   void kstats(const T *X, int64_t L, int64_t s_l, int64_t s_k, int *KE, double *KS) {
     if (s_l == 1) {
       kstats_lines<T><<<(unsigned)((g.K * 32 + 255) / 256), 256, 0, s>>>(X, g.K, L, s_k, KE, KS);
@@ -1477,15 +1607,20 @@ struct OzRun {
       count(2);
     }
   }
-  void exponents(const T *X, int64_t nl, int64_t s_l, int64_t s_k, int *E, int sgn) {
+  // only_if_bal: E already holds the unbalanced exponents (fused stats
+  // pass); recompute only when the device flag says the balancing is on
+  void exponents(const T *X, int64_t nl, int64_t s_l, int64_t s_k, int *E, int sgn, bool only_if_bal = false) {
+    const int oib = only_if_bal ? 1 : 0;
     if (s_k == 1) {
-      line_exponent<T><<<(unsigned)((nl * 32 + 255) / 256), 256, 0, s>>>(X, nl, g.K, s_l, s_k, E, SK, sgn, misc + 1);
+      line_exponent<T><<<(unsigned)((nl * 32 + 255) / 256), 256, 0, s>>>(X, nl, g.K, s_l, s_k, E, SK, sgn, misc + 1,
+                                                                         oib);
       count();
     } else {
-      fill_int<<<(unsigned)std::min<int64_t>((nl + 255) / 256, 1024), 256, 0, s>>>(E, nl, -100000);
+      fill_int<<<(unsigned)std::min<int64_t>((nl + 255) / 256, 1024), 256, 0, s>>>(E, nl, -100000,
+                                                                                   only_if_bal ? misc + 1 : nullptr);
       const int64_t ky = std::max<int64_t>(1, std::min<int64_t>((g.K + 127) / 128, 65535));
       dim3 grid((unsigned)((nl + 255) / 256), (unsigned)ky);
-      line_exponent<T><<<grid, 256, 0, s>>>(X, nl, g.K, s_l, s_k, E, SK, sgn, misc + 1);
+      line_exponent<T><<<grid, 256, 0, s>>>(X, nl, g.K, s_l, s_k, E, SK, sgn, misc + 1, oib);
       count(2);
     }
   }
@@ -1493,15 +1628,17 @@ struct OzRun {
   void prologue() {
     const T *A = static_cast<const T *>(g.A), *B = static_cast<const T *>(g.B);
     const bool bal = g.oz_balance && !staged;
-    if (bal || guard) kstats(B, g.N, b_sn, b_sk, KB, KSB);
+    bool fusedB = false, fusedA = false;   // E from the statistics pass
+    if (bal || guard) fusedB = kstats_lx(B, g.N, b_sn, b_sk, KB, KSB, EB) || (kstats(B, g.N, b_sn, b_sk, KB, KSB), false);
     if (bal || (guard && !staged)) {
-      kstats(A, g.M, a_sm, a_sk, KA, KSA);
+      fusedA = !staged && kstats_lx(A, g.M, a_sm, a_sk, KA, KSA, EA);
+      if (!fusedA) kstats(A, g.M, a_sm, a_sk, KA, KSA);
       have_ka = true;
     }
     balance_prep<<<1, 1024, 0, s>>>(KA, KB, bal ? g.K : 0, p.Kp, bal ? 1 : 0, SK, misc + 1);
     count();
-    if (!staged) exponents(A, g.M, a_sm, a_sk, EA, +1);
-    exponents(B, g.N, b_sn, b_sk, EB, -1);
+    if (!staged) exponents(A, g.M, a_sm, a_sk, EA, +1, fusedA);
+    exponents(B, g.N, b_sn, b_sk, EB, -1, fusedB);
     if (guard) {
       exp_max<<<1, 1024, 0, s>>>(EB, g.N, misc + 2);
       count();

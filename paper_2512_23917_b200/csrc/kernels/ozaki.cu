@@ -648,7 +648,63 @@ __device__ __forceinline__ void gauss_planes(const ResVals<NV> &v, const ResArgs
   }
 }
 
-// per-element scale factors of 8 consecutive k (SK has Kp >= k0 + 8 entries)
+// the same with the moduli count known at compile time (15 or 16: the
+// float64-source complex GEMMs): every loop unrolled, so the per-modulus
+// constants are immediate constant-bank operands instead of indexed LDCs and
+// the store addresses are constant offsets (groups 0-4, 5-9, 10-15 as in
+// res_args)
+template <int NV, int NMOD>
+__device__ __forceinline__ void gauss_planes_ct(const ResVals<NV> &v, const ResArgs &a, int8_t *dst) {
+  const int64_t ps = a.plane_stride;
+#pragma unroll
+  for (int g = 0; g < 3; g++) {
+    const int l0 = 5 * g, l1 = g == 2 ? NMOD : 5 * (g + 1);
+    const double P = a.gP[g], Pinv = a.gPinv[g];
+    const int nPlo = -a.gPlo[g];
+    double rp[NV], ip[NV];
+    int lr[NV], li[NV];
+#pragma unroll
+    for (int j = 0; j < NV; j++) {
+      const double mr = fma(v.x[0][j], Pinv, kMagic), mi = fma(v.x[1][j], Pinv, kMagic);
+      rp[j] = fma(kMagic - mr, P, v.x[0][j]);
+      ip[j] = fma(kMagic - mi, P, v.x[1][j]);
+      lr[j] = __double2loint(mr) * nPlo + v.lo[0][j];
+      li[j] = __double2loint(mi) * nPlo + v.lo[1][j];
+    }
+#pragma unroll
+    for (int l = l0; l < l1; l++) {
+      const int nm = c_gnmod[l], jr = c_groot[l], njr = c_gnroot[l];
+      const double minv = c_gminv[l], jd = c_grootd[l];
+      int u[NV], d[NV];
+#pragma unroll
+      for (int j = 0; j < NV; j++) {
+        const double xu = fma(jd, ip[j], rp[j]), xd = fma(-jd, ip[j], rp[j]);
+        u[j] = __double2loint(fma(xu, minv, kMagic)) * nm + (li[j] * jr + lr[j]);
+        d[j] = __double2loint(fma(xd, minv, kMagic)) * nm + (li[j] * njr + lr[j]);
+      }
+      int8_t *du = dst + (int64_t)(2 * l) * ps;
+      if constexpr (NV == 8) {
+        *reinterpret_cast<uint2 *>(du) = make_uint2(pack4(u[0], u[1], u[2], u[3]), pack4(u[4], u[5], u[6], u[7]));
+        *reinterpret_cast<uint2 *>(du + ps) = make_uint2(pack4(d[0], d[1], d[2], d[3]), pack4(d[4], d[5], d[6], d[7]));
+      } else {
+        *reinterpret_cast<uint32_t *>(du) = pack4(u[0], u[1], u[2], u[3]);
+        *reinterpret_cast<uint32_t *>(du + ps) = pack4(d[0], d[1], d[2], d[3]);
+      }
+    }
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ void gauss_planes_any(const ResVals<NV> &v, const ResArgs &a, int8_t *dst) {
+  if (a.nmod == 15)
+    gauss_planes_ct<NV, 15>(v, a, dst);
+  else if (a.nmod == 16)
+    gauss_planes_ct<NV, 16>(v, a, dst);
+  else
+    gauss_planes<NV>(v, a, dst);
+}
+
+// per-element scale factors of 8 consecutive k (SK has Kp >= k0 + 8 entries)// per-element scale factors of 8 consecutive k (SK has Kp >= k0 + 8 entries)
 template <int NV = 8>
 __device__ __forceinline__ void elem_scales(const ResArgs &a, int E, int64_t k0, double (&fa)[NV], double (&fb)[NV]) {
 #pragma unroll
@@ -702,7 +758,7 @@ __global__ void __launch_bounds__(256, G ? 3 : 2) residues(const __grid_constant
   }
   int8_t *dst = a.out + row * a.Kp + k0;
   if constexpr (G)
-    gauss_planes<NV>(x, a, dst);
+    gauss_planes_any<NV>(x, a, dst);
   else
     for (int l = 0; l < a.nmod; l++) store_planes<G, NV>(x, l, dst, a.plane_stride);
 }
@@ -711,7 +767,7 @@ __global__ void __launch_bounds__(256, G ? 3 : 2) residues(const __grid_constant
 // lines (coalesced), turned into integers in shared memory and written along
 // k: eight threads write one line's 64 contiguous residue bytes per plane.
 template <bool G, class TS>
-__global__ void __launch_bounds__(256, 2) residues_t(const __grid_constant__ ResArgs a) {
+__global__ void __launch_bounds__(256, G ? 3 : 2) residues_t(const __grid_constant__ ResArgs a) {
   __shared__ double sx[2][32][65];
   const int64_t ntk = a.Kp / 64;
   const int64_t tl = blockIdx.x / ntk, tk = blockIdx.x % ntk;
@@ -741,18 +797,30 @@ __global__ void __launch_bounds__(256, 2) residues_t(const __grid_constant__ Res
     }
   }
   __syncthreads();
-  const int li = tid / 8, kq = (tid % 8) * 8;
-  const int64_t row = r0 + li;
-  if (row >= a.lines_out) return;
-  // the thread's 8 values, read from shared memory once for all moduli
-  ResVals<8> x;
+  if constexpr (G) {
+    // Gaussian: 16 threads per line x 4 values (64 contiguous bytes per line
+    // and plane per store instruction), the 32-line tile in two halves
+#pragma unroll 1
+    for (int h = 0; h < 2; h++) {
+      const int li = h * 16 + tid / 16, kq = (tid % 16) * 4;
+      const int64_t row = r0 + li;
+      if (row >= a.lines_out) break;
+      ResVals<4> x;
 #pragma unroll
-  for (int j = 0; j < 8; j++) x.set(j, sx[0][li][kq + j], sx[1][li][kq + j]);
-  int8_t *dst = a.out + row * a.Kp + kb + kq;
-  if constexpr (G)
-    gauss_planes<8>(x, a, dst);
-  else
+      for (int j = 0; j < 4; j++) x.set(j, sx[0][li][kq + j], sx[1][li][kq + j]);
+      gauss_planes_any<4>(x, a, a.out + row * a.Kp + kb + kq);
+    }
+  } else {
+    const int li = tid / 8, kq = (tid % 8) * 8;
+    const int64_t row = r0 + li;
+    if (row >= a.lines_out) return;
+    // the thread's 8 values, read from shared memory once for all moduli
+    ResVals<8> x;
+#pragma unroll
+    for (int j = 0; j < 8; j++) x.set(j, sx[0][li][kq + j], sx[1][li][kq + j]);
+    int8_t *dst = a.out + row * a.Kp + kb + kq;
     for (int l = 0; l < a.nmod; l++) store_planes<G, 8>(x, l, dst, a.plane_stride);
+  }
 }
 
 // ---------------------------------------------------------------------------

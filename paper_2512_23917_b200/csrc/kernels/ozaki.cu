@@ -255,33 +255,42 @@ __global__ void __launch_bounds__(256) kstats_lines_lx(const T *X, int64_t K, in
   const int64_t l0 = blockIdx.y * chunk, l1 = min(L, l0 + chunk);
   for (int64_t i = threadIdx.x; i < l1 - l0; i += blockDim.x) sE[i] = -100000;
   __syncthreads();
+  // the warp's 4 k per line in registers: one shared atomicMax per line and warp
+  const int64_t kb = blockIdx.x * 32 + warp * 4;
+  int em[4];
+  double sv[4];
+#pragma unroll
   for (int kk = 0; kk < 4; kk++) {
-    const int64_t k = blockIdx.x * 32 + warp * 4 + kk;
-    int em = -100000;
-    double s = 0.0;
-    if (k < K) {
-      const T *p = X + k * s_k;
-      for (int64_t l = l0 + lane; l < l1; l += 32) {
-        const int e = es_add_e(em, s, __ldg(p + l));
-        if (e > -100000) atomicMax(&sE[l - l0], e);
-      }
-    }
+    em[kk] = -100000;
+    sv[kk] = 0.0;
+  }
+  for (int64_t l = l0 + lane; l < l1; l += 32) {
+    int lmax = -100000;
+#pragma unroll
+    for (int kk = 0; kk < 4; kk++)
+      if (kb + kk < K) lmax = max(lmax, es_add_e(em[kk], sv[kk], __ldg(X + (kb + kk) * s_k + l)));
+    if (lmax > -100000) atomicMax(&sE[l - l0], lmax);
+  }
+#pragma unroll
+  for (int kk = 0; kk < 4; kk++) {
+    int e = em[kk];
+    double sk = sv[kk];
     for (int o = 16; o; o >>= 1) {
-      const int e2 = __shfl_xor_sync(0xffffffffu, em, o);
-      const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const int e2 = __shfl_xor_sync(0xffffffffu, e, o);
+      const double s2 = __shfl_xor_sync(0xffffffffu, sk, o);
       if (lane & o) {
         int ea = e2;
         double sa = s2;
-        es_merge(ea, sa, em, s);
-        em = ea;
-        s = sa;
+        es_merge(ea, sa, e, sk);
+        e = ea;
+        sk = sa;
       } else {
-        es_merge(em, s, e2, s2);
+        es_merge(e, sk, e2, s2);
       }
     }
-    if (lane == 0 && k < K) {
-      SE[blockIdx.y * K + k] = em;
-      SS[blockIdx.y * K + k] = s;
+    if (lane == 0 && kb + kk < K) {
+      SE[blockIdx.y * K + kb + kk] = e;
+      SS[blockIdx.y * K + kb + kk] = sk;
     }
   }
   __syncthreads();

@@ -288,7 +288,14 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
       lowf.swap(lowf_new);
       TCI_CUDA_CHECK(cudaMemcpyAsync(dlow, lowf.data(), d.npad * sizeof(int), cudaMemcpyHostToDevice, s));
       TCI_CUDA_CHECK(cudaStreamSynchronize(s));
-      if (!(off > tol) && kept_ok) break;   // every kept row was checked against every row
+      if (!(off > tol) && kept_ok) {
+        // converged with skipping: one final sweep over EVERY pair
+        // -- two flagged rows, each below half the cut, may still be mutually
+        // non-orthogonal, and then the discarded block's top singular value
+        // could exceed the cut; the plain sweep must also meet the tolerance
+        skip_active = false;
+        if (trace) fprintf(stderr, "tci:svd verification sweep over all pairs after sweep %d\n", sweeps);
+      }
       continue;
     }
     if (!(off > tol)) break;

@@ -123,8 +123,11 @@ TCI_API tci_status_t tci_synchronize(tci_ctx_t ctx);
  * that synchronize or read results on the host (Lanczos, SVD, guard
  * statistics, profiling, staged copies) fail inside a capture; so does a
  * workspace that would need to grow. tci_graph_end always ends the capture.
+ * The context stream must be a created stream: the legacy NULL stream
+ * cannot be captured (INVALID_ARGUMENT).
  * Errors: DEAD_CONTEXT, INVALID_ARGUMENT (NULL out / not capturing / already
- * capturing), CUDA (an illegal call during capture invalidates it). */
+ * capturing / legacy NULL stream), CUDA (an illegal call during capture
+ * invalidates it). */
 typedef struct tci_graph_s *tci_graph_t;
 TCI_API tci_status_t tci_graph_begin(tci_ctx_t ctx);
 TCI_API tci_status_t tci_graph_end(tci_ctx_t ctx, tci_graph_t *graph);

@@ -366,6 +366,8 @@ int64_t g_capture_launch0[64];
 tci_status_t tci_graph_begin(tci_ctx_t ctx) {
   CHECK(check_ctx(ctx));
   if (ctx->capturing) TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "graph capture already active on this context");
+  if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy)
+    TCI_FAIL(TCI_ERR_INVALID_ARGUMENT, "the legacy NULL stream cannot be captured; create the context on a stream");
   TCI_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   ctx->capturing = true;
   g_capture_launch0[ctx->device & 63] = ctx->launches;

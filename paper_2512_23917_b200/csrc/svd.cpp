@@ -225,6 +225,8 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
   // current top chi_max ran flagged in the sweep just done
   bool kept_ok = false;
   int64_t near_cut = 0;   // rows within [cut/2, cut): many = no spectral gap at the cut
+  double last_cut = 0.0, flag_max = 0.0;   // the cut and the largest flagged row norm of the last flags
+  int64_t nflag = 0;
   auto flags_from_norms = [&](std::vector<int> &f, const std::vector<int> &prev) -> tci_status_t {
     TCI_CUDA_CHECK(launch_svd_norms(p, s, &ctx->launches));
     std::vector<double> nr(d.npad);
@@ -244,6 +246,14 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
       f[i] = prev[i] ? (nr[i] < 0.75 * cut) : (nr[i] < 0.5 * cut);
       if (nr[i] >= cut && prev[i]) kept_ok = false;
     }
+    last_cut = cut;
+    flag_max = 0.0;
+    nflag = 0;
+    for (int64_t i = 0; i < d.n; i++)
+      if (f[i]) {
+        nflag++;
+        flag_max = std::max(flag_max, nr[i]);
+      }
     return TCI_OK;
   };
   // Skipping is only safe to converge when the discarded rows are separated
@@ -252,6 +262,7 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
   // reduced (discarded, discarded) mass back and convergence turns linear,
   // so it is switched off on that signature (below) or after 25 sweeps.
   bool skip_active = lowskip;
+  bool verifying = false;
   std::vector<double> off_hist;
   for (; sweeps < max_sweeps;) {
     p.low = (skip_active && sweeps > 0) ? dlow : nullptr;
@@ -289,16 +300,32 @@ tci_status_t svd_exec(tci_ctx_s *ctx, const View &a, int k, bool trunc, int64_t 
       TCI_CUDA_CHECK(cudaMemcpyAsync(dlow, lowf.data(), d.npad * sizeof(int), cudaMemcpyHostToDevice, s));
       TCI_CUDA_CHECK(cudaStreamSynchronize(s));
       if (!(off > tol) && kept_ok) {
-        // converged with skipping: one final sweep over EVERY pair
-        // -- two flagged rows, each below half the cut, may still be mutually
-        // non-orthogonal, and then the discarded block's top singular value
-        // could exceed the cut; the plain sweep must also meet the tolerance
+        // converged with skipping: one sweep over EVERY pair verifies it
+        // -- flagged rows, each below half the cut, were never
+        // rotated against each other, so the discarded block's top singular
+        // value could in principle exceed the cut
         skip_active = false;
+        verifying = true;
         if (trace) fprintf(stderr, "tci:svd verification sweep over all pairs after sweep %d\n", sweeps);
       }
       continue;
     }
     if (!(off > tol)) break;
+    if (verifying) {
+      // the verification sweep measured every pair's normalized off-diagonal
+      // <= off. Gershgorin on the flagged block's Gram matrix F F^T (diagonal
+      // = squared row norms <= flag_max^2): lambda_max <= flag_max^2 (1 +
+      // (nflag - 1) off). Rotations among flagged rows leave F's singular
+      // values unchanged and the (kept, flagged) ones are converged, so when
+      // that bound is below cut^2 no discarded direction can reach the kept
+      // spectrum: the truncation is the dominant subspace and we stop.
+      verifying = false;
+      const double bound = flag_max * flag_max * (1.0 + (double)std::max<int64_t>(nflag - 1, 0) * off);
+      if (bound < last_cut * last_cut) {
+        if (trace) fprintf(stderr, "tci:svd flagged block bounded below the cut (%.3e < %.3e)\n", std::sqrt(bound), last_cut);
+        break;
+      }
+    }
   }
   p.low = nullptr;
   ctx->svd_last_sweeps = sweeps;

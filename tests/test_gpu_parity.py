@@ -284,6 +284,44 @@ def test_errors(ctx):
     tci.tci_tensor_free(ctx.handle, hh)
 
 
+def test_errors_round2_entry_points():
+    """The round-2 ABI calls validate their arguments: unknown float32 / Ozaki
+    complex variants are INVALID_ARGUMENT; graph capture rejects a second
+    begin, an end without begin and the legacy NULL stream; a dead context
+    answers DEAD_CONTEXT."""
+    c0 = tci.Context(0, torch.cuda.default_stream(0))    # the legacy NULL stream
+    try:
+        with pytest.raises(tci.TciError) as e:
+            tci.tci_graph_begin(c0.handle)
+        assert e.value.code == 8
+    finally:
+        c0.close()
+    c = tci.Context(0, torch.cuda.Stream())
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_set_f32_algorithm(c.handle, 7)
+    assert e.value.code == 8                              # INVALID_ARGUMENT
+    with pytest.raises(tci.TciError) as e:
+        tci.tci_set_ozaki_complex(c.handle, 9)
+    assert e.value.code == 8
+    st, *_ = tci.tci_ozaki_params_complex(4096, 5)
+    assert st == 8
+    with pytest.raises(tci.TciError):
+        tci.tci_graph_end(c.handle)                       # not capturing
+    tci.tci_graph_begin(c.handle)
+    with pytest.raises(tci.TciError):
+        tci.tci_graph_begin(c.handle)                     # already capturing
+    g = tci.tci_graph_end(c.handle)                       # an empty graph is a valid graph
+    tci.tci_graph_launch(c.handle, g)
+    tci.tci_graph_destroy(g)
+    h = c.handle
+    c.close()                                             # the handle stays valid but dead (P:356)
+    for fn, args in ((tci.tci_set_f32_algorithm, (0,)), (tci.tci_set_ozaki_complex, (0,)),
+                     (tci.tci_graph_begin, ())):
+        with pytest.raises(tci.TciError) as e:
+            fn(h, *args)
+        assert e.value.code == 6                          # DEAD_CONTEXT
+
+
 def test_workspace_and_dead_context(oracle_mod):
     c = tci.Context(0)
     a = dev(synth.random_tensor((4, 5, 6), "r64", 85, 1))

@@ -1354,6 +1354,21 @@ struct GuardArgs {
   OzGuard *rec;                // optional statistics
 };
 
+// rowsq[m][0] = sum_j rowsq[m][j]: warp per row, the slots read coalesced
+// and summed in a fixed order (lane-strided partials, then an xor tree)
+__global__ void __launch_bounds__(256) rowsq_fold(double *rowsq, int64_t M, int64_t tpr) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; m < M;
+       m += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double r = 0.0;
+    for (int64_t j = lane; j < tpr; j += 32) r += rowsq[m * tpr + j];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    __syncwarp();
+    if (lane == 0) rowsq[m * tpr] = r;
+  }
+}
+
 __global__ void __launch_bounds__(1024) guard_finalize(const __grid_constant__ GuardArgs g) {
   __shared__ double red[32];
   const int tid = threadIdx.x;
@@ -1381,14 +1396,13 @@ __global__ void __launch_bounds__(1024) guard_finalize(const __grid_constant__ G
   const int ea = bmax(g.EA, g.M);
   const int eb = bmax(g.EB, g.N);
   double sM = 0.0, sN = 0.0, nA = 0.0, nB = 0.0, nC = 0.0;
+  // row sums: slot 0 of each row (rowsq_fold ran first when tpr > 1)
   for (int64_t m = tid; m < g.M; m += blockDim.x) {
     const int e = g.EA[m];
     if (e == -100000) continue;
     const double w = pow4i(e - ea);
     sM += w;
-    double r = 0.0;
-    for (int64_t j = 0; j < g.tpr; j++) r += g.rowsq[m * g.tpr + j];
-    nC = fma(w, r, nC);
+    nC = fma(w, g.rowsq[m * g.tpr], nC);
   }
   for (int64_t n = tid; n < g.N; n += blockDim.x)
     if (g.EB[n] != -100000) sN += pow4i(g.EB[n] - eb);
@@ -1475,6 +1489,7 @@ size_t align_up(size_t x) { return (x + 255) / 256 * 256; }
 // exactness (R26/R33): |C'| <= 2 K 2^(2t) <= M/4, i.e. 2t + 3 + log2 K <= log2 M;
 // the fewest moduli that allow t >= tmin (46 for float64 sources, 24 for
 // float32: R34), then the largest such t
+bool crt_mma_enabled();
 OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_rows = 0, int kind = kOz3M,
                int tmin = 46) {
   OzPlan p{};
@@ -1500,7 +1515,7 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_row
   p.Mc = std::min<int64_t>(round_up(M, 256), mc);
   if (max_rows > 0) p.Mc = std::min<int64_t>(p.Mc, std::max<int64_t>(256, round_up(max_rows, 256)));
   p.chunks = (M + p.Mc - 1) / p.Mc;
-  p.tpr = (p.Np + kCrtTW - 1) / kCrtTW;
+  p.tpr = kind == kOzGauss && crt_mma_enabled() ? crt_mma_slots_per_row(p.Np) : (p.Np + kCrtTW - 1) / kCrtTW;
   p.nch = std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 22) / p.Kp));
   size_t off = 0;
   p.off_EA = off; off = align_up(off + (size_t)M * 4);
@@ -1583,6 +1598,47 @@ void crt_constants_gauss(int nmod, double (&WR)[kMaxGMod][4], double (&WI)[kMaxG
   }
   for (int j = 0; j < 4; j++) Mch[j] = (double)(uint64_t)((Mp >> (kGaussCB * j)) & mask);
   Minv = 1.0 / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
+}
+
+// The tensor-core CRT (crt_mma.cu, default; TCI_CRT_MMA=0 keeps crt_kernel):
+// digit matrix Bd[k][j] (plane k = 2l: c+_l, 2l + 1: c-_l; columns 0..15 the
+// base-256 digits of WR_l, 16..31 those of WI_l for c+ and of M - WI_l for
+// c-), 32-bit chunks of M, ~1/M
+bool crt_mma_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("TCI_CRT_MMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+void crt_digits_gauss(int nmod, CrtMmaArgs &c) {
+  u128 Mp = 1;
+  for (int l = 0; l < nmod; l++) Mp *= (u128)kGModuli[l];
+  for (int k = 0; k < 32; k++)
+    for (int j = 0; j < 32; j++) c.Bd[k][j] = 0;
+  for (int l = 0; l < nmod; l++) {
+    const unsigned ml = (unsigned)kGModuli[l];
+    const u128 Ml = Mp / ml;
+    const u128 wl = mulmod_small(Ml, inv_mod((unsigned)(Ml % ml), ml), Mp);
+    const unsigned h = inv_mod(2u, ml);
+    const unsigned jl = (unsigned)((kGRoots[l] % (int)ml + (int)ml) % (int)ml);
+    const unsigned g = inv_mod((2u * jl) % ml, ml);
+    const u128 wr = mulmod_small(wl, h, Mp), wi = mulmod_small(wl, g, Mp);
+    const u128 wim = wi ? Mp - wi : 0;
+    for (int j = 0; j < 16; j++) {
+      c.Bd[2 * l][j] = c.Bd[2 * l + 1][j] = (uint8_t)(wr >> (8 * j));
+      c.Bd[2 * l][16 + j] = (uint8_t)(wi >> (8 * j));
+      c.Bd[2 * l + 1][16 + j] = (uint8_t)(wim >> (8 * j));
+    }
+  }
+  int bits = 0;
+  for (u128 x = Mp; x; x >>= 1) bits++;
+  c.nd = (bits + 7) / 8;
+  c.planes = 2 * nmod;
+  for (int j = 0; j < 4; j++) c.Mch[j] = (double)(uint64_t)((Mp >> (32 * j)) & 0xFFFFFFFFu);
+  // 2^(32 (NC - 2)) / M, NC = the 32-bit chunks the epilogue uses (crt_mma.cu)
+  const int nc = ((c.nd + 1) / 2 + 1) / 2;
+  c.Minv = std::ldexp(1.0, 32 * (nc - 2)) / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
 }
 
 // one batched INT8 GEMM: D[b][m][n] = (sum_k A[b][m][k] B[b][n][k]) mod m_b
@@ -1761,6 +1817,11 @@ struct OzRun {
     ga.KSA = have_ka ? KSA : nullptr; ga.KSB = KSB;
     ga.rowsq = rowsq; ga.t = p.t; ga.cplx = cplx ? 1 : 0; ga.tol = g.oz_tol;
     ga.flag = misc; ga.bal = misc + 1; ga.rec = g.oz_guard;
+    if (p.tpr > 1) {   // fold each row's slots into its slot 0 first (many CTAs; fixed order)
+      const unsigned blocks = (unsigned)std::min<int64_t>((g.M + 7) / 8, 4 * (int64_t)device_sms());
+      rowsq_fold<<<blocks, 256, 0, s>>>(rowsq, g.M, p.tpr);
+      count();
+    }
     guard_finalize<<<1, 1024, 0, s>>>(ga);
     count();
     cudaError_t e = launch_gemm_dmma_if(g, misc, s, launches);
@@ -1783,9 +1844,10 @@ struct OzRun {
 cudaError_t ozaki_preload() {
   cudaFuncAttributes fa;
   const void *fns[] = {
-      (const void *)copy_to_peers_if, (const void *)guard_finalize, (const void *)exp_max,
+      (const void *)copy_to_peers_if, (const void *)guard_finalize, (const void *)rowsq_fold, (const void *)exp_max,
       (const void *)balance_prep, (const void *)kstats_merge, (const void *)kstats_lines<double2>,
       (const void *)kstats_cols<double2>, (const void *)kstats_lines<double>, (const void *)kstats_cols<double>};
+  if (cudaError_t e = crt_mma_preload(); e != cudaSuccess) return e;
   for (const void *f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&fa, f);
     if (e != cudaSuccess) return e;
@@ -1875,6 +1937,15 @@ cudaError_t ozaki_zgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cu
   c.rowsq = R.guard ? R.rowsq : nullptr;
   c.eb_max = R.misc + 2;
   using TO = TS;
+  const bool crt_tc = gauss && crt_mma_enabled();
+  CrtMmaArgs cm{};
+  if (crt_tc) {
+    crt_digits_gauss(p.nmod, cm);
+    cm.D = D; cm.N = g.N; cm.Np = p.Np; cm.EA = R.EA; cm.EB = R.EB; cm.t = p.t;
+    cm.C = g.C; cm.c_sm = g.c_sm; cm.npeer = c.npeer;
+    for (int pp = 0; pp < c.npeer; pp++) cm.peer[pp] = c.peer[pp];
+    cm.rowsq = c.rowsq; cm.slots_per_row = p.tpr; cm.eb_max = c.eb_max;
+  }
   for (int64_t ch = 0; ch < p.chunks; ch++) {
     const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
     if (g.rows_needed) {
@@ -1891,7 +1962,11 @@ cudaError_t ozaki_zgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cu
     c.Mc = mc;
     c.m0 = m0;
     cudaError_t ce;
-    if (gauss) {
+    if (crt_tc) {
+      cm.Mc = mc;
+      cm.m0 = m0;
+      ce = launch_crt_mma(cm, std::is_same<TO, float2>::value, s);
+    } else if (gauss) {
       switch (p.nmod) {
         case 9: ce = launch_crt<9, 2, true, TO>(c, mc, s); break;
         case 10: ce = launch_crt<10, 2, true, TO>(c, mc, s); break;

@@ -6,6 +6,7 @@ normalisation, all in float64) is re-implemented here with Python big
 integers / numpy float64 and must recover the integer exactly (to one ulp of
 its float64 value) for integers spanning the whole guaranteed range."""
 import math
+import random
 
 import numpy as np
 import pytest
@@ -240,6 +241,53 @@ def _gauss_crt(xs, mods, weights):
     return x
 
 
+def _gauss_crt_tc(cps, cms, mods, roots):
+    """crt_mma.cu's reconstruction of (Re C', Im C') from the byte planes
+    c+_l, c-_l: the INT8 tensor-core digit sums s_j = sum_k c_k Bd[k][j]
+    (exact integers), 16-bit digit pairs, 32-bit chunks, the quotient from the
+    top two chunks, r_c = S_c - q M_c and Horner from the top -- every float64
+    operation emulated with correct rounding (Python int -> float)."""
+    M = math.prod(mods)
+    WR, WI = _gauss_weights(mods, roots)
+    n = len(mods)
+    nd = (M.bit_length() + 7) // 8
+    npair = (nd + 1) // 2
+    nc = (npair + 1) // 2
+    Bd = [[0] * 32 for _ in range(32)]
+    for l in range(n):
+        for j in range(16):
+            Bd[2 * l][j] = Bd[2 * l + 1][j] = (WR[l] >> (8 * j)) & 255
+            Bd[2 * l][16 + j] = (WI[l] >> (8 * j)) & 255
+            Bd[2 * l + 1][16 + j] = ((M - WI[l]) >> (8 * j)) & 255
+    c = [0] * 32
+    for l in range(n):
+        assert 0 <= cps[l] < mods[l] and 0 <= cms[l] < mods[l]
+        c[2 * l], c[2 * l + 1] = cps[l], cms[l]
+    sd = [sum(c[k] * Bd[k][j] for k in range(32)) for j in range(32)]
+    assert max(sd) < 2 ** 21                                   # exact int32 accumulators
+    Mch = [(M >> (32 * j)) & 0xFFFFFFFF for j in range(nc)]
+    assert M >> (32 * nc) == 0
+    mtop = float(2 ** (32 * (nc - 2))) / float(M)
+    out = []
+    for v in (0, 1):
+        d = sd[16 * v:16 * v + 16]
+        p = [d[2 * k] + 256 * d[2 * k + 1] for k in range(8)]
+        assert max(p) < 2 ** 30
+        S = [p[2 * k] + (p[2 * k + 1] << 16 if 2 * k + 1 < npair else 0) for k in range(nc)]
+        assert max(S) < 2 ** 47
+        xe = float(S[nc - 1] * 2 ** 32 + S[nc - 2])            # fma: one rounding
+        q = int(np.rint(xe * mtop))
+        r = [S[j] - q * Mch[j] for j in range(nc)]             # exact (|q M_c| < 2^45)
+        assert q < 2 ** 13 and max(abs(x) for x in r) < 2 ** 53
+        if nc == 4:   # M > 2^96: the first Horner step is exact (|C'| / 2^64 < 2^47)
+            assert abs(r[nc - 1] * 2 ** 32 + r[nc - 2]) < 2 ** 53
+        x = float(r[nc - 1])
+        for j in range(nc - 2, -1, -1):
+            x = float(int(x) * 2 ** 32 + r[j])                 # fma(x, 2^32, r_j): one rounding
+        out.append(x)
+    return out
+
+
 def _gauss_weights(mods, roots):
     M = math.prod(mods)
     WR, WI = [], []
@@ -295,6 +343,11 @@ def test_gaussian_scheme_exact_complex_product(K):
             gr, gi = _gauss_crt(xr, mods, WR), _gauss_crt(xi, mods, WI)
             for got, ref in ((gr, cr), (gi, ci)):
                 assert got == float(ref) or abs(got - ref) <= abs(ref) * 2.0 ** -52, (got, ref)
+            cps = [(xr[l] + xi[l] - m) // 2 % m for l, m in enumerate(mods)]   # c+ = ((c+ + c-) + (c+ - c- + m) - m) / 2
+            cms = [(xr[l] - cps[l]) % m for l, m in enumerate(mods)]
+            tr, ti = _gauss_crt_tc(cps, cms, mods, roots)
+            for got, ref in ((tr, cr), (ti, ci)):
+                assert got == float(ref) or abs(got - ref) <= abs(ref) * 2.0 ** -51, (got, ref)
 
 
 @pytest.mark.parametrize("K", [4096, 20480, 131072])
@@ -318,6 +371,37 @@ def test_gaussian_crt_full_range(K):
         gr, gi = _gauss_crt(xr, mods, WR), _gauss_crt(xi, mods, WI)
         for got, ref in ((gr, cr), (gi, ci)):
             assert got == float(ref) or abs(got - ref) <= abs(ref) * 2.0 ** -52, (got, ref)
+
+
+@pytest.mark.parametrize("K", [64, 4096, 20480, 131072])
+@pytest.mark.parametrize("tmin", [46, 24])
+def test_gaussian_crt_tensor_core_full_range(K, tmin):
+    """crt_mma.cu's digit-sum CRT (the default complex CRT) over the whole
+    guaranteed range |Re C'|, |Im C'| <= 2 K 2^(2t), for the float64 (t >= 46)
+    and float32 (t >= 24) moduli sets: within 2 ulp of the integer (exact
+    below 2^53)."""
+    if tmin == 46:
+        st, n, t, mods, roots, _ = lib().tci_ozaki_params_complex(K, 0)
+    else:
+        st, n, t, mods, ppm = lib().tci_ozaki_params_f32(K, True)
+        assert ppm == 2
+        root_of = dict(zip(*lib().tci_ozaki_params_complex(131072, 0)[3:5]))
+        roots = [root_of[m] for m in mods]
+    assert st == 0 and t >= tmin
+    bound = 2 * K * 2 ** (2 * t)
+    rnd = random.Random(K + tmin)
+    vals = [(0, 0), (bound, -bound), (-bound, bound), (1, -1), (bound - 777, 3), (2 ** 53 + 1, -(2 ** 52) - 3)]
+    for _ in range(60):
+        e = rnd.randrange(bound.bit_length())
+        vals.append((rnd.randint(-2 ** e, 2 ** e), rnd.randint(-bound, bound)))
+    for cr, ci in vals:
+        cr, ci = max(-bound, min(bound, cr)), max(-bound, min(bound, ci))
+        cps = [(cr + j * ci) % m for m, j in zip(mods, roots)]
+        cms = [(cr - j * ci) % m for m, j in zip(mods, roots)]
+        for got, ref in zip(_gauss_crt_tc(cps, cms, mods, roots), (cr, ci)):
+            assert got == float(ref) or abs(got - ref) <= abs(ref) * 2.0 ** -51, (got, ref)
+            if abs(ref) < 2 ** 53:
+                assert got == ref
 
 
 def test_params_complex_3m_and_errors():

@@ -264,6 +264,102 @@ __global__ void __launch_bounds__(NTH) skinny_stream_kernel(const __grid_constan
 }
 
 // ---------------------------------------------------------------------------
+// Expansion variant (K <= 8, N >= 4 K: output-write bound, e.g. the site-local
+// MPS-MPO application B[a,w,t,b,v] = sum_s A[a,s,b] W[w,v,s,t], 8(a10)): when
+// the trailing n-run of length n_lo sits right after b2 in the output
+// (out_sb[2] == n_lo, each run contiguous), the outputs of a tile of TBX b2
+// values form, for every leading n-group, ONE contiguous block of TBX n_lo
+// elements. Each thread computes the elements it stores -- consecutive
+// lanes, consecutive addresses -- straight from the staged input tile and W
+// (shared memory), so every warp store is a contiguous 512-byte run (complex)
+// and nothing is staged on the way out. Persistent CTAs, several per SM, hide
+// the per-tile input latency. Complex products are direct (4 real FMAs per
+// MAC, k ascending): exact for unit / zero weights.
+// ---------------------------------------------------------------------------
+constexpr int TBX = 128;          // b2 values per tile
+constexpr int kExpandMaxK = 8, kExpandMaxNL = 8;
+constexpr int kExpandJ = TBX * kExpandMaxNL / NTH;   // block elements per thread (<= 4)
+
+template <bool CPLX>
+__global__ void __launch_bounds__(NTH) skinny_expand_kernel(const __grid_constant__ SkinnyProblem a,
+                                                            int64_t ntiles) {
+  using Ops = SkE<CPLX>;
+  using T = typename Ops::T;
+  extern __shared__ __align__(16) char sm[];
+  const int K = a.K, N = a.N, NL = a.n_lo, NH = N / NL;
+  T *sW = reinterpret_cast<T *>(sm);   // [K][N]
+  T *sIn = sW + K * N;                 // [K][TBX]
+  const T *W = reinterpret_cast<const T *>(a.W);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < K * N; i += NTH) {
+    const int k = i / N, n = i % N;
+    sW[i] = W[a.w_koff[k] + a.w_noff[n]];
+  }
+  // this thread's block elements i = tid + NTH j -> (b2 offset c, run position l): fixed for every tile
+  int cc[kExpandJ], ll[kExpandJ];
+#pragma unroll
+  for (int j = 0; j < kExpandJ; j++) {
+    const int i = tid + NTH * j;
+    cc[j] = i / NL;
+    ll[j] = i % NL;
+  }
+  const int64_t tiles2 = (a.nb[2] + TBX - 1) / TBX;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t t2 = t % tiles2, r = t / tiles2;
+    const int64_t i1 = r % a.nb[1], i0 = r / a.nb[1];
+    const int64_t c0 = t2 * TBX;
+    const int nc = (int)min((int64_t)TBX, a.nb[2] - c0);
+    const T *in = reinterpret_cast<const T *>(a.in) + i0 * a.in_sb[0] + i1 * a.in_sb[1] + c0 * a.in_sb[2];
+    T *out = reinterpret_cast<T *>(a.out) + i0 * a.out_sb[0] + i1 * a.out_sb[1] + c0 * a.out_sb[2];
+    __syncthreads();   // the previous tile is done with sIn
+    for (int i = tid; i < K * TBX; i += NTH) {
+      const int k = i / TBX, c = i % TBX;
+      sIn[i] = c < nc ? in[c * a.in_sb[2] + a.in_koff[k]] : Ops::zero();
+    }
+    __syncthreads();
+    const int nb = nc * NL;   // valid elements of each block
+    for (int nh = 0; nh < NH; nh++) {
+      T *ob = out + a.out_noff[nh * NL];
+      const T *w = sW + nh * NL;
+#pragma unroll
+      for (int j = 0; j < kExpandJ; j++) {
+        const int i = tid + NTH * j;
+        if (i < nb) {
+          T acc = Ops::zero();
+          for (int k = 0; k < K; k++) Ops::mac(acc, sIn[k * TBX + cc[j]], w[k * N + ll[j]]);
+          __stcs(ob + i, acc);
+        }
+      }
+    }
+  }
+}
+
+template <bool CPLX>
+cudaError_t launch_expand(const SkinnyProblem &p, cudaStream_t s) {
+  const size_t es = CPLX ? 16 : 8;
+  const size_t smem = (size_t)(p.K * p.N + p.K * TBX) * es;
+  const int64_t ntiles = p.nb[0] * p.nb[1] * ((p.nb[2] + TBX - 1) / TBX);
+  auto k = skinny_expand_kernel<CPLX>;
+  cudaError_t e = ensure_smem_attr((const void *)k, smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm = occupancy_per_sm((const void *)k, NTH, smem);
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)device_sms() * std::max(1, per_sm));
+  k<<<(unsigned)grid, NTH, smem, s>>>(p, ntiles);
+  return cudaGetLastError();
+}
+
+// the expansion layout: few k, many n, the n-runs of length n_lo contiguous
+// and interleaved right after b2 in the output
+bool expand_ok(const SkinnyProblem &p) {
+  if (p.K > kExpandMaxK || p.N < 4 * p.K || p.n_lo < 1 || p.n_lo > kExpandMaxNL || p.N % p.n_lo) return false;
+  if (p.out_sb[2] != p.n_lo || p.nb[2] < TBX / 2) return false;
+  for (int n = 0; n < p.N; n++)
+    if (p.out_noff[n] != p.out_noff[n - n % p.n_lo] + n % p.n_lo) return false;
+  const size_t es = p.dtype == TCI_C128 ? 16 : 8;
+  return (uintptr_t)p.out % es == 0;
+}
+
+// ---------------------------------------------------------------------------
 // Tensor-core variant of the streaming complex pass (K, N <= 32; the H_eff
 // MPO pass is K = N = 20 at d = 2, D = 5): the contraction of a tile of TD
 // b2 values is the [TD x K] x [K x N] product, run as FP64 DMMA m8n8k4 with
@@ -515,6 +611,15 @@ bool dmma_pass_disabled() {
   return off;
 }
 
+// TCI_SKINNY_EXPAND=0 keeps the streaming kernel for expansion layouts (A/B)
+bool expand_disabled() {
+  static const int off = [] {
+    const char *e = getenv("TCI_SKINNY_EXPAND");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 }  // namespace
 
 size_t skinny_smem_bytes(int K, int N, size_t esz) {
@@ -529,6 +634,11 @@ cudaError_t launch_skinny(const SkinnyProblem &p0, cudaStream_t s, int64_t *laun
   const size_t smem = skinny_smem_bytes(p.K, p.N, cplx ? 16 : 8);
   const int64_t blocks = p.nb[0] * p.nb[1] * ((p.nb[2] + TB - 1) / TB);
   if (blocks == 0) return cudaSuccess;
+  if (expand_ok(p) && !expand_disabled()) {
+    cudaError_t e = cplx ? launch_expand<true>(p, s) : launch_expand<false>(p, s);
+    if (launches) ++*launches;
+    return e;
+  }
   // streaming variant: b2 unit-stride in the input, 16-byte aligned rows
   {
     const size_t es = cplx ? 16 : 8;

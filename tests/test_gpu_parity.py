@@ -638,6 +638,40 @@ def test_mps_mpo_apply(ctx, oracle_mod):
     assert rel_frob(host(B).reshape(ref.shape), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("dt", ["c128", "r64"])
+@pytest.mark.parametrize("a,d,b,D", [(40, 2, 301, 5), (7, 3, 1000, 4), (3, 4, 64, 8), (5, 2, 129, 2)])
+def test_mps_mpo_apply_expansion_layout(ctx, oracle_mod, dt, a, d, b, D):
+    """8(a10) at b-extents that take the skinny expansion kernel (few k, the
+    output's trailing v-run right after b): ragged b tiles (128 per tile),
+    K = d = 2..4, runs of D = 2..8; identity MPO bitwise, random MPO vs the
+    oracle."""
+    A = synth.random_tensor((a, d, b), dt, 421, 1)
+    I = torch.eye(d, dtype=A.dtype).reshape(1, 1, d, d)
+    B = ctx.contract(dev(A), "asb", dev(I), "wvst", "awtbv")
+    assert torch.equal(B.cpu().reshape(a, d, b), A)
+    W = synth.random_tensor((D, D, d, d), dt, 421, 2)
+    B = ctx.contract(dev(A), "asb", dev(W), "wvst", "awtbv")
+    ref = oracle_mod.mps_mpo_apply(A.numpy(), W.numpy())
+    assert rel_frob(host(B).reshape(ref.shape), ref) <= 1e-12
+
+
+def test_mps_mpo_apply_full_size_sampled(ctx, oracle_mod):
+    """The bench_extra 8(a10) workload (chi = 4096, d = 2, D = 5, c128: 13.4 GB
+    out) in the launch configuration it is timed in; oracle on sampled rows a
+    (first, last, ragged middle)."""
+    chi, d, D = 4096, 2, 5
+    A = synth.random_tensor((chi, d, chi), "c128", 31, 1, device="cuda")
+    Wh, _, _ = synth.heisenberg_mpo(1.0)
+    W = torch.from_numpy(np.asarray(Wh)).to(torch.complex128)
+    B = ctx.contract(A, "asb", dev(W), "wvst", "awtbv")
+    rows = [0, 1, 2047, 4095]
+    got = B[rows].cpu().numpy()
+    ref = oracle_mod.mps_mpo_apply(A[rows].cpu().numpy(), W.numpy())
+    assert rel_frob(got.reshape(ref.shape), ref) <= 1e-12
+    del A, B
+    torch.cuda.empty_cache()
+
+
 # ---------------------------------------------------------------------------
 # multi-GPU plumbing (8(e)) on one GPU: NCCL communicator of one rank
 # ---------------------------------------------------------------------------

@@ -94,6 +94,22 @@ struct Operand {
   Leg leg[kMaxOrder];
 };
 
+// Target leg order of an operand that must be permuted for the GEMM: [F, S]
+// or [S, F] (F its free legs, S the contracted ones), whichever keeps the
+// operand's fastest leg fastest -- the GEMM loaders take either major-ness.
+static std::vector<int> permute_target(const Operand &o, const std::vector<int> &F, const std::vector<int> &S,
+                                       const std::vector<char> &inF) {
+  std::vector<int> t;
+  const bool fast_free = o.n > 0 && inF[o.leg[o.n - 1].id];
+  const std::vector<int> &first = fast_free ? S : F, &second = fast_free ? F : S;
+  t.insert(t.end(), first.begin(), first.end());
+  t.insert(t.end(), second.begin(), second.end());
+  return t;
+}
+static bool keeps_fastest(const Operand &o, const std::vector<int> &target) {
+  return o.n == 0 || target.empty() || target.back() == o.leg[o.n - 1].id;
+}
+
 Operand reduce(int order, const int64_t *shape, const int *ids) {
   Operand o;
   int64_t st = 1;
@@ -323,7 +339,15 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
       const std::vector<int> &J = (ch & 2) ? Jb : Jg;
       const std::vector<int> &S = (ch & 4) ? Sb : Sa;
       const int fa = blocks(legsA, I, S), fb = blocks(legsB, S, J), fc = blocks(legsC, I, J);
-      const int64_t cost = (fa ? 0 : 2 * nA) + (fb ? 0 : 2 * nB) + (fc ? 0 : 2 * nC);
+      // a permute that keeps the operand's fastest leg fastest runs as row
+      // copies (~5.5 TB/s); one that moves it is a transpose (~2-3 TB/s):
+      // those bytes count twice
+      const int64_t pa = fa ? 0 : 2 * nA * (keeps_fastest(A, permute_target(A, I, S, inI)) ? 1 : 2);
+      const int64_t pb = fb ? 0 : 2 * nB * (keeps_fastest(B, permute_target(B, J, S, inJ)) ? 1 : 2);
+      const bool c_keeps = C.n == 0 || (!I.empty() && C.leg[C.n - 1].id == I.back()) ||
+                           (!J.empty() && C.leg[C.n - 1].id == J.back());
+      const int64_t pc = fc ? 0 : 2 * nC * (c_keeps ? 1 : 2);
+      const int64_t cost = pa + pb + pc;
       if (best < 0 || cost < best) {
         best = cost;
         choice = ch;
@@ -461,20 +485,22 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   const void *Ap = a.data;
   int fa = formA;
   if (!formA) {
-    st = permute_into(A, a.data, cat(I, S), wsb + offA);
+    const std::vector<int> tA = permute_target(A, I, S, inI);
+    st = permute_into(A, a.data, tA, wsb + offA);
     if (st != TCI_OK) return st;
     Ap = wsb + offA;
-    fa = 1;
+    fa = (!S.empty() && tA.back() == S.back()) || I.empty() ? 1 : 2;   // [I, S] or [S, I]
   }
   if (fa == 1) { g.a_sm = K; g.a_sk = 1; }   // [I, S]
   else { g.a_sm = 1; g.a_sk = M; }           // [S, I]
   const void *Bp = b.data;
   int fb = formB;
   if (!formB) {
-    st = permute_into(B, b.data, cat(S, J), wsb + offB);
+    const std::vector<int> tB = permute_target(B, J, S, inJ);   // [J, S] or [S, J]
+    st = permute_into(B, b.data, tB, wsb + offB);
     if (st != TCI_OK) return st;
     Bp = wsb + offB;
-    fb = 1;
+    fb = (!J.empty() && tB.back() == J.back()) || S.empty() ? 1 : 2;   // [S, J] or [J, S]
   }
   if (fb == 1) { g.b_sk = N; g.b_sn = 1; }   // [S, J]
   else { g.b_sk = 1; g.b_sn = K; }           // [J, S]
@@ -488,7 +514,10 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   };
   // C layout: formC == 2 means gamma = [J, I] -> swap roles (also for a
   // scatter whose fastest gamma leg is an I leg)
-  const bool swap = ((formC == 2) || (scatter && scat_swap)) && !alias;
+  // (and a GEMM -> scratch -> refold whose fastest gamma leg is an I leg: the
+  // scratch then holds [J, I], so the refold keeps that leg fastest)
+  const bool c_swap_refold = c_scratch && !alias && !formC && !scatter && C.n > 0 && inI[C.leg[C.n - 1].id];
+  const bool swap = (((formC == 2) || (scatter && scat_swap)) && !alias) || c_swap_refold;
   void *Cp = c_scratch ? (void *)(wsb + offC) : c.data;
   int64_t *rowt = nullptr, *colt = nullptr;
   if (scatter) {
@@ -545,10 +574,10 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
     if (formC == 1 || (formC == 2 && swap)) {
       TCI_CUDA_CHECK(launch_copy(c.data, Cp, c.bytes(), ctx->stream, &ctx->launches));
     } else {
-      // scratch holds [I, J] (or [J, I] never: swap only without scratch)
+      // scratch holds [I, J], or [J, I] after the operand swap
       Operand Ct;
       Ct.n = 0;
-      const std::vector<int> IJ = cat(I, J);
+      const std::vector<int> IJ = swap ? cat(J, I) : cat(I, J);
       int64_t s = 1;
       int64_t strides[2 * kMaxOrder];
       for (int k = (int)IJ.size() - 1; k >= 0; k--) { strides[k] = s; s *= dim_of[IJ[k]]; }

@@ -11,6 +11,8 @@
 // buffer. Operand strides are generic: the loader maps consecutive threads to
 // whichever of the two legs has unit stride, so global reads coalesce for any
 // of the four operand layouts.
+#include <cstdlib>
+
 #include "../tci_internal.h"
 #include "common.cuh"
 
@@ -153,6 +155,160 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmProblem p, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// float32 on the FP64 tensor cores (DMMA m8n8k4): the operands are widened to
+// fp64 exactly while they are staged (as the SIMT kernel above), then each warp
+// runs DMMAs on fragments read from shared memory instead of one DFMA per
+// product -- 256 products per warp instruction, ~1/20 of the SIMT kernel's
+// shared-memory traffic per product, so the FP64 datapath (shared by DFMA and
+// DMMA) is kept busy. Same R20 arithmetic: exact products, fp64 sums in a
+// fixed k order (ascending, 4 per DMMA), one rounding to fp32.
+// CTA BM x BN (128 x 128: 16 warps; 128 x 64 / 64 x 128 for narrow outputs:
+// 8 warps), warp tiles 32 x 32 (4 x 4 accumulator fragments), BK 16 with a
+// register-prefetched double buffer; rows of the staged tiles padded by 8
+// doubles (fragment reads hit each bank pair at most twice: the 2-wavefront
+// minimum of a 256-byte read).
+// ---------------------------------------------------------------------------
+constexpr int kFdBK = 16, kFdPad = 8;
+template <int BM, int BN>
+constexpr size_t fd_smem() { return (size_t)2 * kFdBK * ((BM + kFdPad) + (BN + kFdPad)) * sizeof(double); }
+
+template <int BM, int BN>
+__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
+    gemm_f32_dmma_kernel(const GemmProblem p, int tiles_m, int tiles_n) {
+  constexpr int BK = kFdBK, LDA = BM + kFdPad, LDB = BN + kFdPad;
+  constexpr int WX = BN / 32, NT = (BM / 32) * WX * 32;
+  extern __shared__ __align__(16) double fd_sm[];
+  double (*As)[BK][LDA] = reinterpret_cast<double (*)[BK][LDA]>(fd_sm);
+  double (*Bs)[BK][LDB] = reinterpret_cast<double (*)[BK][LDB]>(fd_sm + 2 * BK * LDA);
+  if (p.run_if && *reinterpret_cast<const volatile int *>(p.run_if) == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile_m = blockIdx.x / tiles_n, tile_n = blockIdx.x % tiles_n;
+  const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN;
+  const float *A = static_cast<const float *>(p.A);
+  const float *B = static_cast<const float *>(p.B);
+  float *C = static_cast<float *>(p.C);
+  int64_t Kl = p.K;
+  double *Pz = nullptr;
+  if (p.splitk > 1) {
+    const int64_t kb = (int64_t)blockIdx.z * p.k_chunk;
+    Kl = p.K - kb < p.k_chunk ? p.K - kb : p.k_chunk;
+    A += kb * p.a_sk;
+    B += kb * p.b_sk;
+    Pz = static_cast<double *>(p.partial) + (int64_t)blockIdx.z * p.M * p.N;
+  }
+  const bool a_mfast = (p.a_sk != 1), b_nfast = (p.b_sk != 1);
+  constexpr int LA = BM * BK / NT, LB = BN * BK / NT;
+  float ra[LA], rb[LB];
+  auto gload = [&](int64_t k0) {
+#pragma unroll
+    for (int i = 0; i < LA; i++) {
+      const int idx = tid + i * NT;
+      int m, k;
+      if (a_mfast) { k = idx / BM; m = idx % BM; } else { m = idx / BK; k = idx % BK; }
+      const int64_t gm = m0 + m, gk = k0 + k;
+      ra[i] = (gm < p.M && gk < Kl) ? A[gm * p.a_sm + gk * p.a_sk] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < LB; i++) {
+      const int idx = tid + i * NT;
+      int n, k;
+      if (b_nfast) { k = idx / BN; n = idx % BN; } else { n = idx / BK; k = idx % BK; }
+      const int64_t gn = n0 + n, gk = k0 + k;
+      rb[i] = (gn < p.N && gk < Kl) ? B[gk * p.b_sk + gn * p.b_sn] : 0.f;
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < LA; i++) {
+      const int idx = tid + i * NT;
+      int m, k;
+      if (a_mfast) { k = idx / BM; m = idx % BM; } else { m = idx / BK; k = idx % BK; }
+      As[buf][k][m] = (double)ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < LB; i++) {
+      const int idx = tid + i * NT;
+      int n, k;
+      if (b_nfast) { k = idx / BN; n = idx % BN; } else { n = idx / BK; k = idx % BK; }
+      Bs[buf][k][n] = (double)rb[i];
+    }
+  };
+  const int wm = (warp / WX) * 32, wn = (warp % WX) * 32;
+  const int fr = lane >> 2, fk = lane & 3;   // fragment row / k of this lane
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KT = (int)((Kl + BK - 1) / BK);
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  for (int kt = 0; kt < KT; kt++) {
+    const int buf = kt & 1;
+    if (kt + 1 < KT) gload((int64_t)(kt + 1) * BK);
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) a[i] = As[buf][k4 + fk][wm + 8 * i + fr];
+#pragma unroll
+      for (int j = 0; j < 4; j++) b[j] = Bs[buf][k4 + fk][wn + 8 * j + fr];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) dmma884(acc[i][j], a[i], b[j]);
+    }
+    if (kt + 1 < KT) {
+      sstore(buf ^ 1);
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const int64_t m = m0 + wm + 8 * i + fr;
+    if (m >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int64_t n = n0 + wn + 8 * j + 2 * fk + h;
+        if (n >= p.N) continue;
+        if (Pz) Pz[m * p.N + n] = acc[i][j][h];
+        else C[p.c_row ? p.c_row[m] + p.c_col[n] : m * p.c_sm + n] = (float)acc[i][j][h];
+      }
+  }
+}
+
+// TCI_F32_DMMA=0 keeps the SIMT kernel for float32 (A/B)
+bool f32_dmma_disabled() {
+  static const bool off = [] {
+    const char *e = getenv("TCI_F32_DMMA");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
+template <int BM, int BN>
+cudaError_t run_f32_dmma_t(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
+  const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
+  if (tm * tn > 0x7fffffffLL || p.splitk > 65535) return cudaErrorInvalidConfiguration;
+  auto k = gemm_f32_dmma_kernel<BM, BN>;
+  cudaError_t e = ensure_smem_attr((const void *)k, fd_smem<BM, BN>());
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)(tm * tn), 1, (unsigned)(p.splitk > 1 ? p.splitk : 1));
+  k<<<grid, (BM / 32) * (BN / 32) * 32, fd_smem<BM, BN>(), s>>>(p, (int)tm, (int)tn);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+cudaError_t run_f32_dmma(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
+  if (p.N <= 64 && p.M > 64) return run_f32_dmma_t<128, 64>(p, s, launches);
+  if (p.M <= 64 && p.N > 64) return run_f32_dmma_t<64, 128>(p, s, launches);
+  return run_f32_dmma_t<128, 128>(p, s, launches);
+}
+
 template <typename E, int BM, int BN, int BK, int TM, int TN>
 cudaError_t run_simt(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
@@ -167,6 +323,7 @@ cudaError_t run_simt(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
 
 cudaError_t launch_gemm_f32(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   if (p.dtype == TCI_R32) {
+    if (!f32_dmma_disabled()) return run_f32_dmma(p, s, launches);
     // narrow N or M: a 128 x 64 (64 x 128) tile wastes less of the register tile
     if (p.N <= 64 && p.M > 64) return run_simt<float, 128, 64, 8, 8, 4>(p, s, launches);
     if (p.M <= 64 && p.N > 64) return run_simt<float, 64, 128, 8, 4, 8>(p, s, launches);

@@ -499,15 +499,28 @@ def run_tci(args):
                     for k in KEYS:
                         ctx.copy_async(hosts[k], bufs[b][k], 1)
                     ctx.lane_record(1, IN + b)
-                load(0)
+                # at N = 1 the first step streams its own inputs behind its compute
+                # (tci_heff_apply_staged without a host output: psi + W first, L in
+                # column blocks as GEMM1 reaches them, R behind L, all on copy lane
+                # 1), so the pipeline fill is not a whole unoverlapped input copy
+                staged0 = ws == 1 and not args.no_staged_fill
+                if not staged0:
+                    load(0)
                 for i in range(n):
                     b = i % 2
                     ob = b if ws == 1 else 0
-                    if i + 1 < n:
-                        load(1 - b)
-                    ctx.lane_wait(0, IN + b)
-                    ctx.lane_wait(0, OUT + ob)          # the d2h that last read this output is done
-                    compute(b)
+                    if i == 0 and staged0:
+                        ctx.lane_wait(0, OUT + ob)
+                        ctx.heff_apply_staged([hosts[k] for k in KEYS] + [None],
+                                              [bufs[0][k] for k in KEYS] + [outs[0]])
+                        if n > 1:
+                            load(1)                      # queued on lane 1 behind step 0's inputs
+                    else:
+                        if i + 1 < n:
+                            load(1 - b)
+                        ctx.lane_wait(0, IN + b)
+                        ctx.lane_wait(0, OUT + ob)      # the d2h that last read this output is done
+                        compute(b)
                     ctx.lane_record(0, DONE + b)
                     ctx.lane_wait(2, DONE + b)
                     ctx.copy_async(outs[b], hout, 2)
@@ -551,7 +564,9 @@ def run_tci(args):
                             ("tci_heff_apply" if ws == 1 else
                              "tci_heff_apply_gather" if gather == "p2p" else "tci_heff_apply + tci_allgather") +
                             " of step i (double-buffered device inputs, ordered by tci_lane_record / "
-                            "tci_lane_wait)"),
+                            "tci_lane_wait)" + ("; the first step streams its own inputs behind its compute "
+                                                "(tci_heff_apply_staged, host output NULL)"
+                                                if ws == 1 and not args.no_staged_fill else "")),
                    "results_identical_across_buffers": ok,
                    "h2d_gbs_measured": h2d_gbs,
                    "h2d_bound_ms_per_step": h2d / (h2d_gbs * 1e9) * 1e3,
@@ -719,6 +734,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="report the single-call e2e instead of a stream of applies")
+    ap.add_argument("--no-staged-fill", action="store_true",
+                    help="streaming e2e: copy the first step's inputs in whole before its compute")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-rows", type=int, default=4)

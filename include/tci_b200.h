@@ -625,8 +625,11 @@ TCI_API tci_status_t tci_trunc_svd(tci_ctx_t ctx, tci_tensor_t a, int num_of_bds
  * tci_heff_apply, tci_copy, and stream-ordered on the context stream like
  * them (the context stream waits for the last D2H copy). Each *_h tensor
  * must match its device twin in dtype and shape (host or device memory;
- * pinned host memory for overlap). Errors: as tci_heff_apply, plus
- * SHAPE_MISMATCH for a twin mismatch. Scratch: tci_heff_workspace_size. */
+ * pinned host memory for overlap). out_h may be NULL: the inputs are staged
+ * in the same way and the result stays in `out` (the first step of a stream
+ * of applies whose results are copied out separately). Errors: as
+ * tci_heff_apply, plus SHAPE_MISMATCH for a twin mismatch. Scratch:
+ * tci_heff_workspace_size. */
 TCI_API tci_status_t tci_heff_apply_staged(tci_ctx_t ctx, tci_tensor_t L_h, tci_tensor_t W1_h, tci_tensor_t W2_h,
                                            tci_tensor_t R_h, tci_tensor_t psi_h, tci_tensor_t out_h,
                                            tci_tensor_t L, tci_tensor_t W1, tci_tensor_t W2, tci_tensor_t R,

@@ -741,11 +741,12 @@ class Context:
 
     def heff_apply_staged(self, hosts, devs):
         """tci_heff_apply_staged: hosts / devs = (L, W1, W2, R, psi, out) host and
-        device twins; the result lands in hosts[5] (copies overlap compute)."""
-        L = devs[0]
+        device twins; the result lands in hosts[5] (copies overlap compute), or
+        stays in devs[5] when hosts[5] is None (inputs staged only)."""
         self.ensure_workspace(self.heff_workspace_size(devs[0], devs[1], devs[2], devs[3], devs[4]))
-        tci_heff_apply_staged(self.handle, *[self.tensor(x) for x in hosts], *[self.tensor(x) for x in devs])
-        return hosts[5]
+        tci_heff_apply_staged(self.handle, *[None if x is None else self.tensor(x) for x in hosts],
+                              *[self.tensor(x) for x in devs])
+        return devs[5] if hosts[5] is None else hosts[5]
 
     def env_update(self, side, E, ket, W, bra=None, out=None):
         """Environment update (tci_env_update): side 0 = left, 1 = right; bra defaults to ket."""

@@ -800,6 +800,10 @@ tci_status_t tci_heff_apply_staged(tci_ctx_t ctx, tci_tensor_t L_h, tci_tensor_t
   CHECK(check_ctx(ctx));
   const tci_tensor_t hs[6] = {L_h, W1_h, W2_h, R_h, psi_h, out_h}, ds[6] = {L, W1, W2, R, psi, out};
   for (int i = 0; i < 6; i++) {
+    if (i == 5 && !out_h) {   // inputs staged only: the result stays on the device
+      CHECK(check_ten(ctx, ds[i], true));
+      continue;
+    }
     CHECK(check_ten(ctx, hs[i], false));
     CHECK(check_ten(ctx, ds[i], true));
     if (hs[i]->dtype != ds[i]->dtype || hs[i]->order != ds[i]->order)
@@ -846,7 +850,7 @@ tci_status_t tci_heff_apply_staged(tci_ctx_t ctx, tci_tensor_t L_h, tci_tensor_t
   st.R_host = static_cast<const char *>(R_h->data);
   st.R_dev = static_cast<char *>(R->data);
   st.R_bytes = view_of(R).bytes();
-  st.out_host = static_cast<char *>(out_h->data);
+  st.out_host = out_h ? static_cast<char *>(out_h->data) : nullptr;
   st.out_dev = static_cast<const char *>(out->data);
   st.row_bytes = out->shape[3] * (int64_t)dtype_size(out->dtype);
   const int64_t rows = out->shape[0] * out->shape[1] * out->shape[2];

@@ -240,7 +240,7 @@ namespace {
 // GEMM4 row chunk finished (enqueued) on the context stream: copy it out
 void stage_rows_out(void *user, int64_t m0, int64_t mc) {
   HeffStaging *st = static_cast<HeffStaging *>(user);
-  if (st->err != cudaSuccess) return;
+  if (st->err != cudaSuccess || !st->out_host) return;   // no host twin: the result stays on the device
   tci_ctx_s *ctx = st->ctx;
   cudaError_t e = cudaEventRecord(st->ev_rows, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->copy_stream, st->ev_rows, 0);

@@ -828,6 +828,31 @@ def test_ozaki_contract_vs_dmma_and_oracle(ctx, ozctx, oracle_mod, layout):
     assert torch.equal(c_oz, c2)                         # deterministic
 
 
+@pytest.mark.parametrize("dt,tol", [("c128", 1e-12), ("c64", 1e-5)])
+@pytest.mark.parametrize("mnk", [(1029, 1040, 4100), (300, 1552, 9000)])
+def test_ozaki_tensor_core_crt_ragged(ozctx, oracle_mod, dt, tol, mnk):
+    """The tensor-core CRT (crt_mma.cu) at ragged extents: N = 1040 / 1552 leave
+    a partial 512-column tile and a partial 128-output MMA; M = 1029 / 300
+    leave ragged rows; zero rows and columns give exact zeros; complex64 runs
+    the 9-10-moduli digit epilogue (float2 stores). Oracle on sampled rows,
+    every column; deterministic."""
+    M, N, K = mnk
+    A = synth.random_tensor((M, K), dt, 491, 1)
+    B = synth.random_tensor((K, N), dt, 491, 2)
+    A[5] = 0
+    B[:, N - 3] = 0
+    c1 = ozctx.contract(dev(A), "mk", dev(B), "kn", "mn")
+    st = ozctx.ozaki_guard_stats()
+    assert st["gemms"] >= 1 and st["fallbacks"] == 0, st
+    assert torch.count_nonzero(c1[5]).item() == 0 and torch.count_nonzero(c1[:, N - 3]).item() == 0
+    rows = [0, 1, M // 2, M - 2, M - 1]
+    ref = oracle_mod.contract(A.numpy()[rows].astype(np.complex128), "mk", B.numpy().astype(np.complex128), "kn",
+                              "mn")
+    got = host(c1)[rows].astype(np.complex128)
+    assert rel_frob(got, ref) <= tol
+    assert torch.equal(c1, ozctx.contract(dev(A), "mk", dev(B), "kn", "mn"))
+
+
 @pytest.mark.parametrize("variant", [tci.TCI_OZAKI_CPLX_GAUSS, tci.TCI_OZAKI_CPLX_3M])
 @pytest.mark.parametrize("mnk", [(320, 320, 40960), (256, 256, 131072)])
 def test_ozaki_large_k_moduli_counts(ozctx, oracle_mod, mnk, variant):

@@ -233,33 +233,33 @@ tci_status_t lanczos_exec(tci_ctx_s *ctx, const View &L, const View &W1, const V
   for (; j < max_iter; j++) {
     st = apply_h(V[j], w);
     if (st) return st;
-    double ip[2];
-    st = vec_inner(ctx, V[j], w, 1, ip);
-    if (st) return st;
-    alpha.push_back(ip[0]);
-    {   // w -= alpha_j v_j + beta_{j-1} v_{j-1}
-      View ins[3] = {w, V[j], j > 0 ? V[j - 1] : V[j]};
-      const double c[6] = {1.0, 0.0, -ip[0], 0.0, j > 0 ? -beta[j - 1] : 0.0, 0.0};
-      st = vec_lincomb(ctx, j > 0 ? 3 : 2, ins, c, w);
-      if (st) return st;
-    }
-    for (int pass = 0; pass < 2; pass++) {   // full re-orthogonalisation (CGS2)
+    // Full re-orthogonalisation by classical Gram-Schmidt against v_0..v_j
+    // (its i = j, j-1 terms are the three-term recurrence; alpha_j = <v_j|H v_j>
+    // is the first pass's coefficient i = j, bitwise vec_inner's), repeated
+    // only when the pass cancelled more than 1 - 1/sqrt(2) of w (Kahan-Parlett
+    // "twice is enough", the DGKS criterion; ||w before|| from Pythagoras,
+    // no extra read): one pass costs 2j + 5 vector reads / writes.
+    double b = 0;
+    for (int pass = 0; pass < 2; pass++) {
       std::vector<View> ins(1, w);
       std::vector<double> c = {1.0, 0.0};
       std::vector<double> q(2 * (j + 1));
       st = vec_multi_inner(ctx, j + 1, V.data(), w, 1, q.data());   // all <v_i|w> in one pass over w
       if (st) return st;
+      if (pass == 0) alpha.push_back(q[2 * j]);
+      double removed = 0;
       for (int i = 0; i <= j; i++) {
         ins.push_back(V[i]);
         c.push_back(-q[2 * i]);
         c.push_back(cplx ? -q[2 * i + 1] : 0.0);
+        removed += q[2 * i] * q[2 * i] + q[2 * i + 1] * q[2 * i + 1];
       }
       st = vec_lincomb(ctx, (int)ins.size(), ins.data(), c.data(), w);
       if (st) return st;
+      st = vec_norm(ctx, w, &b);
+      if (st) return st;
+      if (b >= std::sqrt(0.5 * (b * b + removed))) break;   // ||w_after|| >= ||w_before|| / sqrt 2
     }
-    double b = 0;
-    st = vec_norm(ctx, w, &b);
-    if (st) return st;
     beta.push_back(b);
     // lowest Ritz pair of T_{j+1}
     std::vector<double> d(alpha), e(j + 1, 0.0), z;

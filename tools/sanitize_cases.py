@@ -6,7 +6,7 @@
     cases: ozaki (INT8 tcgen05 GEMM + Gaussian residues + CRT TMA ring + guard),
            ozaki_real, f32, gather (2 emulated ranks: flag barrier + remote CRT stores),
            svd (DSMEM cluster Jacobi round), heff (DMMA chain + MPO pass + permutes),
-           lanczos, tebd
+           lanczos, tebd, mpo (skinny expansion kernel + float32 DMMA GEMM)
 Each case checks its own result loosely (the point is the sanitizer report)."""
 import os
 import sys
@@ -116,6 +116,20 @@ def case_tebd():
     inp = synth.tebd_inputs(130, 2, "r64", 9, 0.01, device="cuda")
     th = c.tebd_theta(inp["A"], "asb", inp["B"], "btc", inp["U"], "pqst", "apqc")
     return float(th.abs().max())
+
+
+def case_mpo():
+    """the skinny expansion kernel (8(a10)) on a ragged b extent, and the
+    float32 GEMM on the FP64 tensor cores"""
+    ctx = tci.Context(0)
+    A = synth.random_tensor((7, 3, 301), "c128", 4, 1, device="cuda")
+    W = synth.random_tensor((4, 4, 3, 3), "c128", 4, 2, device="cuda")
+    B = ctx.contract(A, "asb", W, "wvst", "awtbv")
+    ref = torch.einsum("asb,wvst->awtbv", A, W)
+    X = synth.random_tensor((300, 200), "r32", 4, 3, device="cuda")
+    Y = synth.random_tensor((200, 130), "r32", 4, 4, device="cuda")
+    Z = ctx.contract(X, "mk", Y, "kn", "mn")
+    return max(rel(B, ref), rel(Z.double(), X.double() @ Y.double()))
 
 
 if __name__ == "__main__":

@@ -29,9 +29,11 @@ def ncu_csv(rep, *args):
 
 def main(rep, dst):
     rows = ncu_csv(rep, "--page", "raw")
-    hdr, vals = rows[0], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2]
     raw = dict(zip(hdr, vals))
-    res = {"report": rep, "kernel": raw.get("Kernel Name", "")[:160], "metrics": {}}
+    unit = dict(zip(hdr, units))
+    res = {"report": rep, "kernel": raw.get("Kernel Name", "")[:160], "metrics": {},
+           "units": {m: unit.get(m, "") for m in METRICS if m in raw}}
     for m in METRICS:
         if m in raw:
             try:

@@ -378,12 +378,15 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   {
     int bm, bn;
     gemm_tile(a.dtype, &bm, &bn);
-    const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+    // thin GEMMs (gemm_thin.cu: one thread / warp per row of the long side)
+    // parallelise over 256-row blocks, not GEMM tiles
+    const bool thin = std::min(M, N) <= (dtype_is_complex(a.dtype) ? 16 : 32);
+    const int64_t tiles = thin ? (std::max(M, N) + 255) / 256 : ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
     // (not when the GEMM goes to the INT8 tensor cores: its 3n / n residue
     // GEMMs of one launch fill the machine by themselves)
     const bool oz_candidate = oz_dtype && ozaki_worthwhile(M, N, K, a.dtype);
     if (tiles < 2 * 148 && K >= 256 && !oz_candidate) {
-      int64_t S = std::min<int64_t>({(4 * 148 + tiles - 1) / tiles, K / 128, 1024});
+      int64_t S = std::min<int64_t>({(4 * 148 + tiles - 1) / tiles, K / 64, 1024});
       if (S >= 2) {
         k_chunk = ((K + S - 1) / S + 15) / 16 * 16;
         S = (K + k_chunk - 1) / k_chunk;

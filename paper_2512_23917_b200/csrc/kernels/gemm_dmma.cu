@@ -614,10 +614,78 @@ __global__ void __launch_bounds__(256) splitk_reduce(const P *__restrict__ part,
     }
   }
 }
+// Few outputs, many splits (thin / small GEMMs): a warp per output, lane l
+// summing splits l, l + 32, ... in ascending order, then a fixed xor tree --
+// deterministic, and the 148 SMs share the S reads of each output instead of
+// one thread walking them
+template <class P, class O>
+__global__ void __launch_bounds__(256) splitk_reduce_w(const P *__restrict__ part, O *__restrict__ C,
+                                                       int64_t M, int64_t N, int64_t c_sm, int S,
+                                                       const int64_t *c_row, const int64_t *c_col) {
+  const int64_t MN = M * N;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < MN;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double ax = 0.0, ay = 0.0;
+    for (int z = lane; z < S; z += 32) {
+      const P v = part[(int64_t)z * MN + i];
+      if constexpr (sizeof(P) == 16) {
+        ax += reinterpret_cast<const double2 &>(v).x;
+        ay += reinterpret_cast<const double2 &>(v).y;
+      } else {
+        ax += reinterpret_cast<const double &>(v);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      ax += __shfl_xor_sync(0xffffffffu, ax, o);
+      if constexpr (sizeof(P) == 16) ay += __shfl_xor_sync(0xffffffffu, ay, o);
+    }
+    if (lane == 0) {
+      const int64_t m = i / N, n = i % N;
+      const int64_t ci = c_row ? c_row[m] + c_col[n] : m * c_sm + n;
+      if constexpr (sizeof(P) == 16) {
+        if constexpr (sizeof(O) == 16) {
+          const double2 r = make_double2(ax, ay);
+          C[ci] = reinterpret_cast<const O &>(r);
+        } else {
+          const float2 r = make_float2((float)ax, (float)ay);
+          C[ci] = reinterpret_cast<const O &>(r);
+        }
+      } else {
+        if constexpr (sizeof(O) == 8) {
+          C[ci] = reinterpret_cast<const O &>(ax);
+        } else {
+          const float r = (float)ax;
+          C[ci] = reinterpret_cast<const O &>(r);
+        }
+      }
+    }
+  }
+}
 }  // namespace
 
 static cudaError_t launch_splitk_reduce(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
   const int64_t MN = p.M * p.N;
+  if (p.splitk >= 8 && MN < 148 * 256) {
+    const unsigned blocks = (unsigned)std::min<int64_t>((MN + 7) / 8, 148 * 8);
+    switch (p.dtype) {
+      case TCI_C128:
+        splitk_reduce_w<double2, double2><<<blocks, 256, 0, s>>>((const double2 *)p.partial, (double2 *)p.C, p.M, p.N, p.c_sm, p.splitk, p.c_row, p.c_col);
+        break;
+      case TCI_R64:
+        splitk_reduce_w<double, double><<<blocks, 256, 0, s>>>((const double *)p.partial, (double *)p.C, p.M, p.N, p.c_sm, p.splitk, p.c_row, p.c_col);
+        break;
+      case TCI_C64:
+        splitk_reduce_w<double2, float2><<<blocks, 256, 0, s>>>((const double2 *)p.partial, (float2 *)p.C, p.M, p.N, p.c_sm, p.splitk, p.c_row, p.c_col);
+        break;
+      case TCI_R32:
+        splitk_reduce_w<double, float><<<blocks, 256, 0, s>>>((const double *)p.partial, (float *)p.C, p.M, p.N, p.c_sm, p.splitk, p.c_row, p.c_col);
+        break;
+    }
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   const unsigned blocks = (unsigned)std::min<int64_t>((MN + 255) / 256, 148 * 8);
   switch (p.dtype) {
     case TCI_C128:

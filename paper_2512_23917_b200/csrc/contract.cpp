@@ -524,23 +524,14 @@ tci_status_t contract_exec(tci_ctx_s *ctx, const View &a, const int32_t *la, con
   void *Cp = c_scratch ? (void *)(wsb + offC) : c.data;
   int64_t *rowt = nullptr, *colt = nullptr;
   if (scatter) {
-    // gamma offsets of the I legs (rows) and J legs (columns), slowest first
-    auto table = [&](const std::vector<int> &legs, int64_t *dst, int64_t n) -> tci_status_t {
-      int64_t ext[kMaxOrder], str[kMaxOrder];
-      int nl = 0;
-      for (int id : legs) {
-        ext[nl] = dim_of[id];
-        str[nl] = stride_in(C, id);
-        nl++;
-      }
-      TCI_CUDA_CHECK(launch_offsets(dst, n, nl, ext, str, ctx->stream, &ctx->launches));
-      return TCI_OK;
-    };
+    // gamma offsets of the I legs (rows) and J legs (columns), slowest first:
+    // both tables in one launch
+    int64_t exi[kMaxOrder], sti[kMaxOrder], exj[kMaxOrder], stj[kMaxOrder];
+    int ni = 0, nj = 0;
+    for (int id : I) { exi[ni] = dim_of[id]; sti[ni] = stride_in(C, id); ni++; }
+    for (int id : J) { exj[nj] = dim_of[id]; stj[nj] = stride_in(C, id); nj++; }
     int64_t *ti = reinterpret_cast<int64_t *>(wsb + offR), *tj = reinterpret_cast<int64_t *>(wsb + offCol);
-    st = table(I, ti, M);
-    if (st != TCI_OK) return st;
-    st = table(J, tj, N);
-    if (st != TCI_OK) return st;
+    TCI_CUDA_CHECK(launch_offsets2(ti, M, ni, exi, sti, tj, N, nj, exj, stj, ctx->stream, &ctx->launches));
     rowt = swap ? tj : ti;
     colt = swap ? ti : tj;
   }

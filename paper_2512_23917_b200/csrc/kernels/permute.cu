@@ -681,7 +681,39 @@ __global__ void offsets_kernel(int64_t *offs, int64_t n, const OffLegs L) {
     offs[i] = o;
   }
 }
+// both tables of a scatter epilogue in one launch: index i < n1 fills offs1
+// from L1, the rest offs2 from L2
+__global__ void offsets2_kernel(int64_t *offs1, int64_t n1, const OffLegs L1, int64_t *offs2, int64_t n2,
+                                const OffLegs L2) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n1 + n2; j += (int64_t)gridDim.x * blockDim.x) {
+    const bool first = j < n1;
+    const OffLegs &L = first ? L1 : L2;
+    const int64_t i = first ? j : j - n1;
+    int64_t r = i, o = 0;
+    for (int l = L.nl - 1; l >= 0; l--) {
+      o += (r % L.ext[l]) * L.stride[l];
+      r /= L.ext[l];
+    }
+    (first ? offs1 : offs2)[i] = o;
+  }
+}
 }  // namespace
+
+cudaError_t launch_offsets2(int64_t *offs1, int64_t n1, int nl1, const int64_t *ext1, const int64_t *stride1,
+                            int64_t *offs2, int64_t n2, int nl2, const int64_t *ext2, const int64_t *stride2,
+                            cudaStream_t s, int64_t *launches) {
+  if (n1 + n2 == 0) return cudaSuccess;
+  if (nl1 > kMaxOrder || nl2 > kMaxOrder) return cudaErrorInvalidValue;
+  OffLegs L1{}, L2{};
+  L1.nl = nl1;
+  L2.nl = nl2;
+  for (int l = 0; l < nl1; l++) { L1.ext[l] = ext1[l]; L1.stride[l] = stride1[l]; }
+  for (int l = 0; l < nl2; l++) { L2.ext[l] = ext2[l]; L2.stride[l] = stride2[l]; }
+  offsets2_kernel<<<(unsigned)std::min<int64_t>((n1 + n2 + 255) / 256, 148 * 4), 256, 0, s>>>(offs1, n1, L1, offs2,
+                                                                                           n2, L2);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_offsets(int64_t *offs, int64_t n, int nl, const int64_t *ext, const int64_t *stride,
                            cudaStream_t s, int64_t *launches) {

@@ -306,6 +306,10 @@ cudaError_t launch_lincomb(bool cplx, const double *const *in, const double *cr,
 // the GEMM rows / columns for the scatter epilogue
 cudaError_t launch_offsets(int64_t *offs, int64_t n, int nl, const int64_t *ext, const int64_t *stride,
                            cudaStream_t s, int64_t *launches);
+// the row and column tables of one scatter epilogue in a single launch
+cudaError_t launch_offsets2(int64_t *offs1, int64_t n1, int nl1, const int64_t *ext1, const int64_t *stride1,
+                            int64_t *offs2, int64_t n2, int nl2, const int64_t *ext2, const int64_t *stride2,
+                            cudaStream_t s, int64_t *launches);
 
 // out[r, :] = s[r] * in[r, :] over rows x cols elements (r64 / c128)
 cudaError_t launch_row_scale(bool cplx, const double *in, const double *s, double *out, int64_t rows, int64_t cols,

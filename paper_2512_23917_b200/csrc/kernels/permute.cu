@@ -13,6 +13,7 @@
 //    16-byte loads into padded shared memory and written along j with
 //    16-byte stores; every other leg indexes the tile grid.
 #include <algorithm>
+#include <cstdlib>
 
 #include "../tci_internal.h"
 #include "common.cuh"
@@ -523,9 +524,65 @@ bool plan_groups(const PermuteProblem &p, const int64_t *out_stride, GroupArgs &
   return true;
 }
 
+// Small tensors (<= 8 MB, L2-resident): one output element per thread in
+// output order (coalesced stores), its input offset from the output index by
+// multiply-high divisions, reads served by L2. The tiled kernels' per-CTA
+// setup (offset tables, tile geometry) is the cost at this size: a 2 MB
+// six-leg permute took ~28 us through the leg-group tiles.
+constexpr int64_t kSmallPermuteBytes = 8 << 20;
+// TCI_PERMUTE_SMALL=0 sends small tensors through the tiled kernels (A/B)
+bool small_permute_disabled() {
+  static const bool off = [] {
+    const char *e = getenv("TCI_PERMUTE_SMALL");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+struct SmallArgs {
+  int n;
+  FDiv div[kMaxOrder];      // output extents, fastest first
+  int64_t in_st[kMaxOrder]; // input strides, fastest first
+  int64_t total;
+  const void *in;
+  void *out;
+};
+template <int ESZ>
+__global__ void __launch_bounds__(256) permute_small(const __grid_constant__ SmallArgs a) {
+  using E = typename std::conditional<ESZ == 16, int4,
+                                      typename std::conditional<ESZ == 8, int2, int>::type>::type;
+  const E *in = reinterpret_cast<const E *>(a.in);
+  E *out = reinterpret_cast<E *>(a.out);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.total; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t r = (uint32_t)i;
+    int64_t off = 0;
+#pragma unroll 4
+    for (int k = 0; k < a.n; k++) {
+      const uint32_t q = fdiv(r, a.div[k]);
+      off += (int64_t)(r - q * a.div[k].d) * a.in_st[k];
+      r = q;
+    }
+    out[i] = __ldg(in + off);
+  }
+}
+
 template <int ESZ>
 cudaError_t launch_typed(const PermuteProblem &p, cudaStream_t s, int64_t *launches) {
   const int n = p.n;
+  if (n > 1 && p.total * ESZ <= kSmallPermuteBytes && p.total < (1LL << 31) && !small_permute_disabled()) {
+    SmallArgs a{};
+    a.n = n;
+    a.total = p.total;
+    a.in = p.in;
+    a.out = p.out;
+    for (int k = 0; k < n; k++) {
+      a.div[k] = make_fdiv((uint32_t)p.shape_out[n - 1 - k]);
+      a.in_st[k] = p.in_stride_for_out[n - 1 - k];
+    }
+    const int64_t blocks = std::min<int64_t>((p.total + 255) / 256, 148 * 8);
+    permute_small<ESZ><<<(unsigned)blocks, 256, 0, s>>>(a);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   int64_t out_stride[kMaxOrder];
   {
     int64_t st = 1;

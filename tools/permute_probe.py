@@ -13,6 +13,10 @@ import paper_2512_23917_b200 as tci  # noqa: E402
 import synth  # noqa: E402
 
 CASES = [  # (dtype, shape, perm)
+    ("r64", (3, 8, 8, 37, 5, 37), (0, 2, 4, 1, 3, 5)),      # small: OMxuHR -> O x H M u R
+    ("r64", (3, 8, 8, 37, 5, 37), (0, 2, 4, 5, 3, 1)),      # small: OMxuHR -> O x H R u M
+    ("r64", (37, 64, 37, 8), (1, 0, 2, 3)),                 # small: RduM -> d R u M
+    ("r64", (37, 64, 37, 8), (1, 3, 2, 0)),                 # small: RduM -> d M u R
     ("r32", (37, 8, 128, 7, 7, 128), (1, 2, 3, 5, 0, 4)),   # rXcByH -> X c B H r y
     ("r32", (37, 8, 128, 7, 7, 128), (0, 4, 1, 2, 3, 5)),   # rXcByH -> r y X c B H
     ("r32", (7, 64, 7, 64, 256, 5), (0, 1, 2, 4, 5, 3)),    # xdKTQF -> x d K Q F T

@@ -1064,6 +1064,12 @@ def test_heff_apply_staged_bitwise(algo, oracle_mod):
         rows = [0, 511, 1023]
         ref = oracle_mod.heff_rows(n["L"], n["W1"], n["W2"], n["R"], n["psi"], rows)
         assert rel_frob(hout.numpy()[rows], ref) <= 1e-12
+        # inputs staged only (host output NULL: bench.py's first streaming step)
+        devs2 = [torch.empty_like(d_in[k]) for k in keys] + [torch.empty_like(ref_dev)]
+        r2 = c.heff_apply_staged(hosts + [None], devs2)
+        c.synchronize()
+        assert r2 is devs2[5] and torch.equal(devs2[5], ref_dev)
+        assert all(torch.equal(devs2[i], d_in[k]) for i, k in enumerate(keys))
     finally:
         c.close()
 

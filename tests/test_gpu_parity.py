@@ -75,6 +75,48 @@ def test_permute_leg_groups_bitwise(ctx, oracle_mod, dt):
             assert np.array_equal(host(y).astype(ref.dtype), ref), (shape, perm)
 
 
+def test_permute_tiled_kernels_bitwise():
+    """Tensors up to 8 MB take permute_small; the tiled kernels (row copies,
+    2-D transpose tiles, leg-group tiles with cut legs and ragged chunks) are
+    run here on the same shapes with TCI_PERMUTE_SMALL=0 (read once per
+    process: a child process), bitwise vs the oracle for r32 / r64 / c128."""
+    code = (
+        "import numpy as np, torch, synth, oracle, paper_2512_23917_b200 as t\n"
+        "c = t.Context(0)\n"
+        "rng = np.random.default_rng(11)\n"
+        "shapes = [(5, 7, 3, 11), (2, 3, 2, 5, 2, 7, 3), (1000, 3, 5), (3, 5, 1031), (37, 130, 65, 2),\n"
+        "          (17, 2, 513, 3), (64, 1, 64, 5), (6, 4000), (4000, 6), (2, 2, 2, 2, 2, 2, 2), (37, 130, 65)]\n"
+        "n = 0\n"
+        "for dt in ('r32', 'r64', 'c128'):\n"
+        "    for i, shape in enumerate(shapes):\n"
+        "        x = synth.random_tensor(shape, dt, 700 + i, 1)\n"
+        "        for _ in range(4):\n"
+        "            perm = list(rng.permutation(len(shape)))\n"
+        "            y = c.permute(x.cuda(), perm)\n"
+        "            ref = oracle.permute(x.numpy(), perm)\n"
+        "            assert np.array_equal(y.cpu().numpy().astype(ref.dtype), ref), (dt, shape, perm)\n"
+        "            n += 1\n"
+        "print('checked', n)\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
+                       env=dict(os.environ, TCI_PERMUTE_SMALL="0"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "checked 132" in r.stdout
+
+
+@pytest.mark.parametrize("dt", ["r32", "c128"])
+def test_permute_large_tiled_bitwise(ctx, oracle_mod, dt):
+    """Tensors above the 8 MB small-permute bound in the default process:
+    the tiled kernels, bitwise vs the oracle."""
+    rng = np.random.default_rng(12)
+    for i, shape in enumerate([(7, 300, 5, 300), (64, 37, 130, 9), (3, 5, 1031, 300)]):
+        x = synth.random_tensor(shape, dt, 800 + i, 1)
+        for _ in range(2):
+            perm = list(rng.permutation(len(shape)))
+            y = ctx.permute(dev(x), perm)
+            ref = oracle_mod.permute(x.numpy(), perm)
+            assert np.array_equal(host(y).astype(ref.dtype), ref), (shape, perm)
+
+
 def test_permute_paper_example(ctx):
     a = synth.random_tensor((3, 2, 4), "r64", 12, 1)
     a2 = ctx.permute(dev(a), [1, 0, 2])

@@ -103,6 +103,34 @@ def test_permute_tiled_kernels_bitwise():
     assert "checked 132" in r.stdout
 
 
+def test_ab_switch_fallback_paths():
+    """The A/B switches keep their kernels correct: TCI_CRT_MMA=0 (the CUDA-core
+    Gaussian CRT), TCI_F32_DMMA=0 (the SIMT float32 GEMM) and
+    TCI_SKINNY_EXPAND=0 (the streaming kernel for expansion layouts), in a
+    child process, against the oracle."""
+    code = (
+        "import numpy as np, torch, synth, oracle, paper_2512_23917_b200 as t\n"
+        "def rel(a, b): return float(np.linalg.norm(a - b) / np.linalg.norm(b))\n"
+        "c = t.Context(0); c.set_gemm_algorithm(t.TCI_GEMM_OZAKI_INT8)\n"
+        "A = synth.random_tensor((1029, 4100), 'c128', 5, 1); B = synth.random_tensor((4100, 1040), 'c128', 5, 2)\n"
+        "C = c.contract(A.cuda(), 'mk', B.cuda(), 'kn', 'mn').cpu().numpy()\n"
+        "st = c.ozaki_guard_stats(); assert st['gemms'] == 1 and st['fallbacks'] == 0, st\n"
+        "rows = [0, 514, 1028]\n"
+        "e1 = rel(C[rows], oracle.contract(A.numpy()[rows], 'mk', B.numpy(), 'kn', 'mn'))\n"
+        "X = synth.random_tensor((300, 700), 'r32', 5, 3); Y = synth.random_tensor((700, 200), 'r32', 5, 4)\n"
+        "Z = c.contract(X.cuda(), 'mk', Y.cuda(), 'kn', 'mn').cpu().numpy()\n"
+        "e2 = rel(Z.astype(np.float64), oracle.contract(X.numpy().astype(np.float64), 'mk', Y.numpy().astype(np.float64), 'kn', 'mn'))\n"
+        "P = synth.random_tensor((7, 3, 301), 'c128', 5, 5); W = synth.random_tensor((4, 4, 3, 3), 'c128', 5, 6)\n"
+        "Q = c.contract(P.cuda(), 'asb', W.cuda(), 'wvst', 'awtbv').cpu().numpy()\n"
+        "e3 = rel(Q.reshape(-1), oracle.mps_mpo_apply(P.numpy(), W.numpy()).reshape(-1))\n"
+        "print('errs', e1, e2, e3)\n"
+        "assert e1 <= 1e-12 and e2 <= 1e-5 and e3 <= 1e-12\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
+                       env=dict(os.environ, TCI_CRT_MMA="0", TCI_F32_DMMA="0", TCI_SKINNY_EXPAND="0"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "errs" in r.stdout
+
+
 @pytest.mark.parametrize("dt", ["r32", "c128"])
 def test_permute_large_tiled_bitwise(ctx, oracle_mod, dt):
     """Tensors above the 8 MB small-permute bound in the default process:

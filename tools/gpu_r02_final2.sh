@@ -14,7 +14,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --csv --log-file gpurun_out/launches.csv $B > /dev/null 2>&1
 python tools/launch_table.py gpurun_out/launches.csv --steps 3 > gpurun_out/launches.txt 2>&1
 head -12 gpurun_out/launches.txt
-for spec in gemm1:i8gemm_kernel:0 gemm4:i8gemm_kernel:2 crt_mma:crt_mma_kernel:0 res_k:^residues\$:0 res_l:^residues_t\$:0 skinny:skinny_dmma_kernel:0 kst_cols:kstats_cols_lx:0 kst_lines:kstats_lines_lx:0; do
+for spec in gemm1:i8gemm_kernel:0 gemm4:i8gemm_kernel:2 crt_mma:crt_mma_kernel:0 res_k:^residues\$:0 res_l:^residues_t\$:0 skinny:skinny_dmma_kernel:0; do
   IFS=: read name rx skip <<< "$spec"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s "$skip" -c 1 -o /tmp/prof_$name -f $B > /dev/null 2>&1
   python tools/ncu_kernel_summary.py /tmp/prof_$name.ncu-rep gpurun_out/ncu_$name.json > /dev/null 2>&1

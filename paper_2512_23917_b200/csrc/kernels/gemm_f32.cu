@@ -282,6 +282,144 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   }
 }
 
+// complex64 on the FP64 tensor cores: the same staging (re / im planes widened
+// to fp64), 4M with exact products: Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br
+// (four DMMAs per fragment pair, fixed order). CTA 64 x 64, 8 warps of 32 x 16.
+constexpr int kCdBM = 64, kCdBN = 64;
+constexpr size_t cd_smem() { return (size_t)2 * 2 * kFdBK * ((kCdBM + kFdPad) + (kCdBN + kFdPad)) * sizeof(double); }
+
+__global__ void __launch_bounds__(256, 2) gemm_c64_dmma_kernel(const GemmProblem p, int tiles_m, int tiles_n) {
+  constexpr int BM = kCdBM, BN = kCdBN, BK = kFdBK, LDA = BM + kFdPad, LDB = BN + kFdPad, NT = 256;
+  extern __shared__ __align__(16) double cd_sm[];
+  double (*Ar)[BK][LDA] = reinterpret_cast<double (*)[BK][LDA]>(cd_sm);
+  double (*Ai)[BK][LDA] = reinterpret_cast<double (*)[BK][LDA]>(cd_sm + 2 * BK * LDA);
+  double (*Br)[BK][LDB] = reinterpret_cast<double (*)[BK][LDB]>(cd_sm + 4 * BK * LDA);
+  double (*Bi)[BK][LDB] = reinterpret_cast<double (*)[BK][LDB]>(cd_sm + 4 * BK * LDA + 2 * BK * LDB);
+  if (p.run_if && *reinterpret_cast<const volatile int *>(p.run_if) == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile_m = blockIdx.x / tiles_n, tile_n = blockIdx.x % tiles_n;
+  const int64_t m0 = (int64_t)tile_m * BM, n0 = (int64_t)tile_n * BN;
+  const float2 *A = static_cast<const float2 *>(p.A);
+  const float2 *B = static_cast<const float2 *>(p.B);
+  float2 *C = static_cast<float2 *>(p.C);
+  int64_t Kl = p.K;
+  double2 *Pz = nullptr;
+  if (p.splitk > 1) {
+    const int64_t kb = (int64_t)blockIdx.z * p.k_chunk;
+    Kl = p.K - kb < p.k_chunk ? p.K - kb : p.k_chunk;
+    A += kb * p.a_sk;
+    B += kb * p.b_sk;
+    Pz = static_cast<double2 *>(p.partial) + (int64_t)blockIdx.z * p.M * p.N;
+  }
+  const bool a_mfast = (p.a_sk != 1), b_nfast = (p.b_sk != 1);
+  constexpr int LA = BM * BK / NT, LB = BN * BK / NT;
+  float2 ra[LA], rb[LB];
+  auto gload = [&](int64_t k0) {
+#pragma unroll
+    for (int i = 0; i < LA; i++) {
+      const int idx = tid + i * NT;
+      int m, k;
+      if (a_mfast) { k = idx / BM; m = idx % BM; } else { m = idx / BK; k = idx % BK; }
+      const int64_t gm = m0 + m, gk = k0 + k;
+      ra[i] = (gm < p.M && gk < Kl) ? A[gm * p.a_sm + gk * p.a_sk] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < LB; i++) {
+      const int idx = tid + i * NT;
+      int n, k;
+      if (b_nfast) { k = idx / BN; n = idx % BN; } else { n = idx / BK; k = idx % BK; }
+      const int64_t gn = n0 + n, gk = k0 + k;
+      rb[i] = (gn < p.N && gk < Kl) ? B[gk * p.b_sk + gn * p.b_sn] : make_float2(0.f, 0.f);
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < LA; i++) {
+      const int idx = tid + i * NT;
+      int m, k;
+      if (a_mfast) { k = idx / BM; m = idx % BM; } else { m = idx / BK; k = idx % BK; }
+      Ar[buf][k][m] = (double)ra[i].x;
+      Ai[buf][k][m] = (double)ra[i].y;
+    }
+#pragma unroll
+    for (int i = 0; i < LB; i++) {
+      const int idx = tid + i * NT;
+      int n, k;
+      if (b_nfast) { k = idx / BN; n = idx % BN; } else { n = idx / BK; k = idx % BK; }
+      Br[buf][k][n] = (double)rb[i].x;
+      Bi[buf][k][n] = (double)rb[i].y;
+    }
+  };
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;   // 2 x 4 warps of 32 x 16
+  const int fr = lane >> 2, fk = lane & 3;
+  double cr[4][2][2], ci[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+  const int KT = (int)((Kl + BK - 1) / BK);
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  for (int kt = 0; kt < KT; kt++) {
+    const int buf = kt & 1;
+    if (kt + 1 < KT) gload((int64_t)(kt + 1) * BK);
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double ar[4], ai[4], nai[4], br[2], bi[2];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        ar[i] = Ar[buf][k4 + fk][wm + 8 * i + fr];
+        ai[i] = Ai[buf][k4 + fk][wm + 8 * i + fr];
+        nai[i] = -ai[i];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        br[j] = Br[buf][k4 + fk][wn + 8 * j + fr];
+        bi[j] = Bi[buf][k4 + fk][wn + 8 * j + fr];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+          dmma884(cr[i][j], ar[i], br[j]);
+          dmma884(cr[i][j], nai[i], bi[j]);
+          dmma884(ci[i][j], ar[i], bi[j]);
+          dmma884(ci[i][j], ai[i], br[j]);
+        }
+    }
+    if (kt + 1 < KT) {
+      sstore(buf ^ 1);
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const int64_t m = m0 + wm + 8 * i + fr;
+    if (m >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int64_t n = n0 + wn + 8 * j + 2 * fk + h;
+        if (n >= p.N) continue;
+        if (Pz) Pz[m * p.N + n] = make_double2(cr[i][j][h], ci[i][j][h]);
+        else C[p.c_row ? p.c_row[m] + p.c_col[n] : m * p.c_sm + n] = make_float2((float)cr[i][j][h], (float)ci[i][j][h]);
+      }
+  }
+}
+
+cudaError_t run_c64_dmma(const GemmProblem &p, cudaStream_t s, int64_t *launches) {
+  const int64_t tm = (p.M + kCdBM - 1) / kCdBM, tn = (p.N + kCdBN - 1) / kCdBN;
+  if (tm * tn > 0x7fffffffLL || p.splitk > 65535) return cudaErrorInvalidConfiguration;
+  cudaError_t e = ensure_smem_attr((const void *)gemm_c64_dmma_kernel, cd_smem());
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)(tm * tn), 1, (unsigned)(p.splitk > 1 ? p.splitk : 1));
+  gemm_c64_dmma_kernel<<<grid, 256, cd_smem(), s>>>(p, (int)tm, (int)tn);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
 // TCI_F32_DMMA=0 keeps the SIMT kernel for float32 (A/B)
 bool f32_dmma_disabled() {
   static const bool off = [] {
@@ -329,6 +467,7 @@ cudaError_t launch_gemm_f32(const GemmProblem &p, cudaStream_t s, int64_t *launc
     if (p.M <= 64 && p.N > 64) return run_simt<float, 64, 128, 8, 4, 8>(p, s, launches);
     return run_simt<float, 128, 128, 8, 8, 8>(p, s, launches);
   }
+  if (!f32_dmma_disabled()) return run_c64_dmma(p, s, launches);
   return run_simt<float2, 64, 64, 8, 4, 4>(p, s, launches);
 }
 

@@ -123,8 +123,12 @@ def test_ab_switch_fallback_paths():
         "P = synth.random_tensor((7, 3, 301), 'c128', 5, 5); W = synth.random_tensor((4, 4, 3, 3), 'c128', 5, 6)\n"
         "Q = c.contract(P.cuda(), 'asb', W.cuda(), 'wvst', 'awtbv').cpu().numpy()\n"
         "e3 = rel(Q.reshape(-1), oracle.mps_mpo_apply(P.numpy(), W.numpy()).reshape(-1))\n"
-        "print('errs', e1, e2, e3)\n"
-        "assert e1 <= 1e-12 and e2 <= 1e-5 and e3 <= 1e-12\n")
+        "U = synth.random_tensor((130, 300), 'c64', 5, 7); V = synth.random_tensor((300, 90), 'c64', 5, 8)\n"
+        "c.set_f32_algorithm(t.TCI_F32_FP64_CORES)\n"
+        "Wc = c.contract(U.cuda(), 'mk', V.cuda(), 'kn', 'mn').cpu().numpy()\n"
+        "e4 = rel(Wc.astype(np.complex128), oracle.contract(U.numpy().astype(np.complex128), 'mk', V.numpy().astype(np.complex128), 'kn', 'mn'))\n"
+        "print('errs', e1, e2, e3, e4)\n"
+        "assert e1 <= 1e-12 and e2 <= 1e-5 and e3 <= 1e-12 and e4 <= 1e-5\n")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
                        env=dict(os.environ, TCI_CRT_MMA="0", TCI_F32_DMMA="0", TCI_SKINNY_EXPAND="0"))
     assert r.returncode == 0, r.stderr[-3000:]

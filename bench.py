@@ -653,7 +653,9 @@ def run_tci(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": ("c128 (fp64-accurate: Ozaki-II exact INT8 tensor-core residue GEMMs + CRT)"
+        # the arithmetic the path computes in: INT8 x INT8 -> INT32 residue GEMMs (and the
+        # CRT digit GEMM) on the tensor cores, f64 scaling / reconstruction; c128 in and out
+        "dtype": ("i8 (tensor-core residue GEMMs, i32 sums) + f64; complex128 data"
                   if algo == "ozaki" else ("c128" if dt == "c128" else "f64")),
         "alt": alt,
         "data": "synthetic (seeded counter-based generator; exact model MPO as W1=W2)",

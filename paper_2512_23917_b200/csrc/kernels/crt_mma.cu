@@ -38,6 +38,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "../tci_internal.h"
 #include "common.cuh"
@@ -142,6 +143,9 @@ __device__ __forceinline__ double crt_digits(const uint32_t *s, const double (&M
 __device__ __forceinline__ double pow2i(int h) { return h < -1022 ? 0.0 : __hiloint2double((h + 1023) << 20, 0); }
 __device__ __forceinline__ void st_c(double2 *p, double2 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_c(float2 *p, double2 v) { __stcs(p, make_float2((float)v.x, (float)v.y)); }
+// real outputs (float64 / float32 Ozaki GEMMs): the value is v.x
+__device__ __forceinline__ void st_c(double *p, double2 v) { __stcs(p, v.x); }
+__device__ __forceinline__ void st_c(float *p, double2 v) { __stcs(p, (float)v.x); }
 
 template <int NP, class TO>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -275,11 +279,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);   // TMEM read: hand the accumulator back
+      // complex: (Re, Im) of two outputs; real (TO = double / float): columns
+      // 0..15 hold the one value's digits, 16..31 are zero
+      constexpr bool CPLX = sizeof(TO) == 16 || std::is_same<TO, float2>::value;
       double x[4];
       x[0] = crt_digits<NP>(v0, a.Mch, a.Minv);
-      x[1] = crt_digits<NP>(v0 + 16, a.Mch, a.Minv);
       x[2] = crt_digits<NP>(v1, a.Mch, a.Minv);
-      x[3] = crt_digits<NP>(v1 + 16, a.Mch, a.Minv);
+      if constexpr (CPLX) {
+        x[1] = crt_digits<NP>(v0 + 16, a.Mch, a.Minv);
+        x[3] = crt_digits<NP>(v1 + 16, a.Mch, a.Minv);
+      } else {
+        x[1] = x[3] = 0.0;
+      }
       // branch-free scaling by 2^sc = 2^h1 2^h2 (h2 = 0, a multiply by 1, whenever
       // 2^sc is a normal double); zero lines (exponent -100000) give exact zeros
       TO *crow = static_cast<TO *>(a.C) + m * a.c_sm;
@@ -380,7 +391,12 @@ cudaError_t crt_mma_preload() {
                        (const void *)crt_mma_kernel<6, double2>, (const void *)crt_mma_kernel<7, double2>,
                        (const void *)crt_mma_kernel<8, double2>, (const void *)crt_mma_kernel<4, float2>,
                        (const void *)crt_mma_kernel<5, float2>,  (const void *)crt_mma_kernel<6, float2>,
-                       (const void *)crt_mma_kernel<7, float2>,  (const void *)crt_mma_kernel<8, float2>};
+                       (const void *)crt_mma_kernel<7, float2>,  (const void *)crt_mma_kernel<8, float2>,
+                       (const void *)crt_mma_kernel<4, double>,  (const void *)crt_mma_kernel<5, double>,
+                       (const void *)crt_mma_kernel<6, double>,  (const void *)crt_mma_kernel<7, double>,
+                       (const void *)crt_mma_kernel<8, double>,  (const void *)crt_mma_kernel<4, float>,
+                       (const void *)crt_mma_kernel<5, float>,   (const void *)crt_mma_kernel<6, float>,
+                       (const void *)crt_mma_kernel<7, float>,   (const void *)crt_mma_kernel<8, float>};
   for (const void *f : fns)
     if (cudaError_t e = cudaFuncGetAttributes(&fa, f); e != cudaSuccess) return e;
   return cudaSuccess;
@@ -388,7 +404,7 @@ cudaError_t crt_mma_preload() {
 
 int64_t crt_mma_slots_per_row(int64_t Np) { return (Np + crtm::kTW - 1) / crtm::kTW; }
 
-cudaError_t launch_crt_mma(const CrtMmaArgs &a, bool f32_out, cudaStream_t s) {
+cudaError_t launch_crt_mma(const CrtMmaArgs &a, bool f32_out, bool real, cudaStream_t s) {
   using namespace crtm;
   if (a.Mc <= 0 || a.N <= 0) return cudaSuccess;
   if (a.planes < 1 || a.planes > 32 || a.Np % 16 || (uintptr_t)a.D % 16 || a.nd < 1 || a.nd > 16)
@@ -406,24 +422,22 @@ cudaError_t launch_crt_mma(const CrtMmaArgs &a, bool f32_out, cudaStream_t s) {
     return cudaErrorNotSupported;
   const int64_t ntiles = a.Mc * ((a.Np + kTW - 1) / kTW);
   const int np = (a.nd + 1) / 2;   // 16-bit digit pairs
-  if (f32_out) {
-    switch (np) {
-      case 4: return launch_np<4, float2>(map, a, ntiles, s);
-      case 5: return launch_np<5, float2>(map, a, ntiles, s);
-      case 6: return launch_np<6, float2>(map, a, ntiles, s);
-      case 7: return launch_np<7, float2>(map, a, ntiles, s);
-      case 8: return launch_np<8, float2>(map, a, ntiles, s);
-      default: return cudaErrorInvalidValue;
-    }
+#define TCI_CRT_NP(TO)                                          \
+  switch (np) {                                                 \
+    case 4: return launch_np<4, TO>(map, a, ntiles, s);         \
+    case 5: return launch_np<5, TO>(map, a, ntiles, s);         \
+    case 6: return launch_np<6, TO>(map, a, ntiles, s);         \
+    case 7: return launch_np<7, TO>(map, a, ntiles, s);         \
+    case 8: return launch_np<8, TO>(map, a, ntiles, s);         \
+    default: return cudaErrorInvalidValue;                      \
   }
-  switch (np) {
-    case 4: return launch_np<4, double2>(map, a, ntiles, s);
-    case 5: return launch_np<5, double2>(map, a, ntiles, s);
-    case 6: return launch_np<6, double2>(map, a, ntiles, s);
-    case 7: return launch_np<7, double2>(map, a, ntiles, s);
-    case 8: return launch_np<8, double2>(map, a, ntiles, s);
-    default: return cudaErrorInvalidValue;
+  if (real) {
+    if (f32_out) { TCI_CRT_NP(float) }
+    TCI_CRT_NP(double)
   }
+  if (f32_out) { TCI_CRT_NP(float2) }
+  TCI_CRT_NP(double2)
+#undef TCI_CRT_NP
 }
 
 }  // namespace tci

@@ -1515,7 +1515,8 @@ OzPlan oz_plan(int64_t M, int64_t N, int64_t K, size_t budget_D, int64_t max_row
   p.Mc = std::min<int64_t>(round_up(M, 256), mc);
   if (max_rows > 0) p.Mc = std::min<int64_t>(p.Mc, std::max<int64_t>(256, round_up(max_rows, 256)));
   p.chunks = (M + p.Mc - 1) / p.Mc;
-  p.tpr = kind == kOzGauss && crt_mma_enabled() ? crt_mma_slots_per_row(p.Np) : (p.Np + kCrtTW - 1) / kCrtTW;
+  p.tpr = (kind == kOzGauss || kind == kOzReal) && crt_mma_enabled() ? crt_mma_slots_per_row(p.Np)
+                                                                    : (p.Np + kCrtTW - 1) / kCrtTW;
   p.nch = std::max<int64_t>(1, std::min<int64_t>(64, ((int64_t)1 << 22) / p.Kp));
   size_t off = 0;
   p.off_EA = off; off = align_up(off + (size_t)M * 4);
@@ -1637,6 +1638,28 @@ void crt_digits_gauss(int nmod, CrtMmaArgs &c) {
   c.planes = 2 * nmod;
   for (int j = 0; j < 4; j++) c.Mch[j] = (double)(uint64_t)((Mp >> (32 * j)) & 0xFFFFFFFFu);
   // 2^(32 (NC - 2)) / M, NC = the 32-bit chunks the epilogue uses (crt_mma.cu)
+  const int nc = ((c.nd + 1) / 2 + 1) / 2;
+  c.Minv = std::ldexp(1.0, 32 * (nc - 2)) / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
+}
+
+// real outputs: plane l holds c_l = C' mod m_l (moduli kModuli); columns
+// 0..15 the base-256 digits of the CRT weight w_l, 16..31 zero
+void crt_digits_real(int nmod, CrtMmaArgs &c) {
+  u128 Mp = 1;
+  for (int l = 0; l < nmod; l++) Mp *= (u128)kModuli[l];
+  for (int k = 0; k < 32; k++)
+    for (int j = 0; j < 32; j++) c.Bd[k][j] = 0;
+  for (int l = 0; l < nmod; l++) {
+    const unsigned ml = (unsigned)kModuli[l];
+    const u128 Ml = Mp / ml;
+    const u128 wl = mulmod_small(Ml, inv_mod((unsigned)(Ml % ml), ml), Mp);
+    for (int j = 0; j < 16; j++) c.Bd[l][j] = (uint8_t)(wl >> (8 * j));
+  }
+  int bits = 0;
+  for (u128 x = Mp; x; x >>= 1) bits++;
+  c.nd = (bits + 7) / 8;
+  c.planes = nmod;
+  for (int j = 0; j < 4; j++) c.Mch[j] = (double)(uint64_t)((Mp >> (32 * j)) & 0xFFFFFFFFu);
   const int nc = ((c.nd + 1) / 2 + 1) / 2;
   c.Minv = std::ldexp(1.0, 32 * (nc - 2)) / ((double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp);
 }
@@ -1965,7 +1988,7 @@ cudaError_t ozaki_zgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cu
     if (crt_tc) {
       cm.Mc = mc;
       cm.m0 = m0;
-      ce = launch_crt_mma(cm, std::is_same<TO, float2>::value, s);
+      ce = launch_crt_mma(cm, std::is_same<TO, float2>::value, false, s);
     } else if (gauss) {
       switch (p.nmod) {
         case 9: ce = launch_crt<9, 2, true, TO>(c, mc, s); break;
@@ -2036,6 +2059,14 @@ cudaError_t ozaki_dgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cu
   c.rowsq = R.guard ? R.rowsq : nullptr;
   c.eb_max = R.misc + 2;
   using TO = TS;
+  const bool crt_tc = crt_mma_enabled();
+  CrtMmaArgs cm{};
+  if (crt_tc) {
+    crt_digits_real(p.nmod, cm);
+    cm.D = D; cm.N = g.N; cm.Np = p.Np; cm.EA = R.EA; cm.EB = R.EB; cm.t = p.t;
+    cm.C = g.C; cm.c_sm = g.c_sm; cm.npeer = 0;
+    cm.rowsq = c.rowsq; cm.slots_per_row = p.tpr; cm.eb_max = c.eb_max;
+  }
   for (int64_t ch = 0; ch < p.chunks; ch++) {
     const int64_t m0 = ch * p.Mc, mc = std::min<int64_t>(p.Mc, g.M - m0);
     {
@@ -2047,6 +2078,15 @@ cudaError_t ozaki_dgemm_impl(const GemmProblem &g, void *ws, size_t ws_bytes, cu
     if (ge != cudaSuccess) return ge;
     c.Mc = mc;
     c.m0 = m0;
+    if (crt_tc) {   // the tensor-core CRT (crt_mma.cu), real outputs
+      cm.Mc = mc;
+      cm.m0 = m0;
+      cudaError_t ce = launch_crt_mma(cm, std::is_same<TO, float>::value, true, s);
+      if (ce != cudaSuccess) return ce;
+      R.count();
+      if (g.rows_done) g.rows_done(g.rows_user, m0, mc);
+      continue;
+    }
     const unsigned blocks = (unsigned)(mc * p.tpr);
     switch (p.nmod) {
       case 8: crt_real_kernel<8, 2, TO><<<blocks, 256, 0, s>>>(c); break;

@@ -161,9 +161,10 @@ inline bool ozaki_worthwhile(int64_t M, int64_t N, int64_t K, tci_dtype_t dt = T
 cudaError_t launch_i8gemm(const int8_t *A, const int8_t *B, uint8_t *D, int64_t M, int64_t N, int64_t Kp, int L,
                           int per_mod, const int *moduli, int nmod, int *counter, cudaStream_t s,
                           int64_t *launches);
-// The complex (Gaussian) Ozaki CRT on the INT8 tensor cores (crt_mma.cu): the
-// residue planes D [planes][Mc][Np] (planes = 2n <= 32) times the base-256
-// digits Bd[k][j] of the CRT weights (columns 0..15 Re, 16..31 Im), then the
+// The Ozaki CRT on the INT8 tensor cores (crt_mma.cu): the residue planes
+// D [planes][Mc][Np] (complex: planes = 2n <= 32; real: n) times the base-256
+// digits Bd[k][j] of the CRT weights (columns 0..15 Re / the real value,
+// 16..31 Im, zero for real outputs), then the
 // exact digit -> double reconstruction and the 2^(-2t + E_m + E_n) scaling
 // into C (complex128, or complex64 when f32_out); guard row sums in
 // rowsq[m * slots_per_row + ...] (crt_mma_slots_per_row(Np) slots per row)
@@ -184,7 +185,7 @@ struct CrtMmaArgs {
   int64_t slots_per_row;
   const int *eb_max;
 };
-cudaError_t launch_crt_mma(const CrtMmaArgs &a, bool f32_out, cudaStream_t s);
+cudaError_t launch_crt_mma(const CrtMmaArgs &a, bool f32_out, bool real, cudaStream_t s);
 int64_t crt_mma_slots_per_row(int64_t Np);
 cudaError_t crt_mma_preload();   // load every instance now (see ozaki_preload)
 

@@ -404,6 +404,46 @@ def test_gaussian_crt_tensor_core_full_range(K, tmin):
                 assert got == ref
 
 
+def _real_crt_tc(cs, mods):
+    """crt_mma.cu for real outputs: plane l = C' mod m_l, digit columns 0..15 the
+    base-256 digits of w_l = (M/m_l) ((M/m_l)^-1 mod m_l), the same epilogue
+    as _gauss_crt_tc on the one value (float64 operations emulated exactly)."""
+    M = math.prod(mods)
+    nd = (M.bit_length() + 7) // 8
+    npair = (nd + 1) // 2
+    nc = (npair + 1) // 2
+    W = [(M // m) * pow((M // m) % m, -1, m) % M for m in mods]
+    sd = [sum(c * ((w >> (8 * j)) & 255) for c, w in zip(cs, W)) for j in range(16)]
+    assert max(sd) < 2 ** 21
+    p = [sd[2 * k] + 256 * sd[2 * k + 1] for k in range(8)]
+    S = [p[2 * k] + (p[2 * k + 1] << 16 if 2 * k + 1 < npair else 0) for k in range(nc)]
+    Mch = [(M >> (32 * j)) & 0xFFFFFFFF for j in range(nc)]
+    xe = float(S[nc - 1] * 2 ** 32 + S[nc - 2])
+    q = int(np.rint(xe * (float(2 ** (32 * (nc - 2))) / float(M))))
+    r = [S[j] - q * Mch[j] for j in range(nc)]
+    x = float(r[nc - 1])
+    for j in range(nc - 2, -1, -1):
+        x = float(int(x) * 2 ** 32 + r[j])
+    return x
+
+
+@pytest.mark.parametrize("K", [64, 4096, 20480, 131072])
+def test_real_crt_tensor_core_full_range(K):
+    """The real tensor-core CRT (float64 / float32 Ozaki GEMMs) over the whole
+    guaranteed range |C'| <= K 2^(2t) (real products), exact below 2^53."""
+    for st, n, t, mods in (lib().tci_ozaki_params(K), lib().tci_ozaki_params_f32(K, False)[:4]):
+        assert st == 0
+        bound = 2 * K * 2 ** (2 * t)
+        rnd = random.Random(K + t)
+        vals = [0, 1, -1, bound, -bound, 2 ** 53 + 1] + [rnd.randint(-bound, bound) for _ in range(40)]
+        vals += [rnd.randint(-2 ** e, 2 ** e) for e in range(0, bound.bit_length(), 7)]
+        for v in vals:
+            got = _real_crt_tc([v % m for m in mods], mods)
+            assert got == float(v) or abs(got - v) <= abs(v) * 2.0 ** -51, (got, v)
+            if abs(v) < 2 ** 53:
+                assert got == v
+
+
 def test_params_complex_3m_and_errors():
     st, n, t, mods, roots, ppm = lib().tci_ozaki_params_complex(20480, 1)
     st0, n0, t0, mods0 = lib().tci_ozaki_params(20480)

@@ -499,22 +499,24 @@ def run_tci(args):
                     for k in KEYS:
                         ctx.copy_async(hosts[k], bufs[b][k], 1)
                     ctx.lane_record(1, IN + b)
-                # at N = 1 the first step streams its own inputs behind its compute
+                # at N = 1 every step streams its own inputs behind its compute
                 # (tci_heff_apply_staged without a host output: psi + W first, L in
                 # column blocks as GEMM1 reaches them, R behind L, all on copy lane
-                # 1), so the pipeline fill is not a whole unoverlapped input copy
+                # 1, ordered by the lane events), so the copies of step i + 1 run
+                # while step i computes and no step waits for a whole input copy
                 staged0 = ws == 1 and not args.no_staged_fill
                 if not staged0:
                     load(0)
                 for i in range(n):
                     b = i % 2
                     ob = b if ws == 1 else 0
-                    if i == 0 and staged0:
+                    if staged0:
+                        # every step streams its inputs behind its own compute; copy
+                        # lane 1 first waits for the compute that last read buffer b
+                        ctx.lane_wait(1, DONE + b)
                         ctx.lane_wait(0, OUT + ob)
                         ctx.heff_apply_staged([hosts[k] for k in KEYS] + [None],
-                                              [bufs[0][k] for k in KEYS] + [outs[0]])
-                        if n > 1:
-                            load(1)                      # queued on lane 1 behind step 0's inputs
+                                              [bufs[b][k] for k in KEYS] + [outs[b]])
                     else:
                         if i + 1 < n:
                             load(1 - b)
@@ -564,8 +566,8 @@ def run_tci(args):
                             ("tci_heff_apply" if ws == 1 else
                              "tci_heff_apply_gather" if gather == "p2p" else "tci_heff_apply + tci_allgather") +
                             " of step i (double-buffered device inputs, ordered by tci_lane_record / "
-                            "tci_lane_wait)" + ("; the first step streams its own inputs behind its compute "
-                                                "(tci_heff_apply_staged, host output NULL)"
+                            "tci_lane_wait)" + ("; every step streams its own inputs behind its compute "
+                                                "(tci_heff_apply_staged, host output NULL, copy lane ordered by lane events)"
                                                 if ws == 1 and not args.no_staged_fill else "")),
                    "results_identical_across_buffers": ok,
                    "h2d_gbs_measured": h2d_gbs,

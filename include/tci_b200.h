@@ -626,8 +626,10 @@ TCI_API tci_status_t tci_trunc_svd(tci_ctx_t ctx, tci_tensor_t a, int num_of_bds
  * them (the context stream waits for the last D2H copy). Each *_h tensor
  * must match its device twin in dtype and shape (host or device memory;
  * pinned host memory for overlap). out_h may be NULL: the inputs are staged
- * in the same way and the result stays in `out` (the first step of a stream
- * of applies whose results are copied out separately). Errors: as
+ * in the same way and the result stays in `out`; the copies then do NOT wait
+ * for work already queued on the context stream -- the caller orders copy
+ * lane 1 (tci_lane_record / tci_lane_wait) so that `L`..`psi` are free, which
+ * lets a stream of applies stage step i+1's inputs while step i computes. Errors: as
  * tci_heff_apply, plus SHAPE_MISMATCH for a twin mismatch. Scratch:
  * tci_heff_workspace_size. */
 TCI_API tci_status_t tci_heff_apply_staged(tci_ctx_t ctx, tci_tensor_t L_h, tci_tensor_t W1_h, tci_tensor_t W2_h,

@@ -824,9 +824,14 @@ tci_status_t tci_heff_apply_staged(tci_ctx_t ctx, tci_tensor_t L_h, tci_tensor_t
   for (auto &e : ctx->evs)
     if (!e) TCI_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   cudaStream_t s0 = ctx->stream, s1 = ctx->copy_stream;
-  // the copy stream starts after everything already queued on the context stream
-  TCI_CUDA_CHECK(cudaEventRecord(ctx->evs[0], s0));
-  TCI_CUDA_CHECK(cudaStreamWaitEvent(s1, ctx->evs[0], 0));
+  // the copy stream starts after everything already queued on the context
+  // stream -- unless the host output is NULL: then the caller orders the copy
+  // lane (tci_lane_wait on lane 1) so a stream of applies can stage step i+1's
+  // inputs while step i computes
+  if (out_h) {
+    TCI_CUDA_CHECK(cudaEventRecord(ctx->evs[0], s0));
+    TCI_CUDA_CHECK(cudaStreamWaitEvent(s1, ctx->evs[0], 0));
+  }
   auto h2d = [&](int i) -> tci_status_t {
     const View v = view_of(ds[i]);
     TCI_CUDA_CHECK(cudaMemcpyAsync(v.data, hs[i]->data, v.bytes(), cudaMemcpyDefault, s1));
